@@ -1,0 +1,253 @@
+"""Pins for the oracle's Algorithm 1 and financial terms
+(P:176-179): SPEC worked examples, a brute-force straight-line reference in
+pure Python (its own Philox, scipy special functions, linear search over the
+XELT records instead of the direct-access table), exact integer sums with
+sigma = 0, additivity over XELTs, order invariance (G6), thread-count
+determinism."""
+import numpy as np
+import pytest
+import scipy.special as sp
+
+import oracle as O
+
+M32 = 0xFFFFFFFF
+
+
+def philox_py(ctr, key):
+    c0, c1, c2, c3 = ctr
+    k0, k1 = key
+    for r in range(10):
+        if r:
+            k0 = (k0 + 0x9E3779B9) & M32
+            k1 = (k1 + 0xBB67AE85) & M32
+        p0 = 0xD2511F53 * c0
+        p1 = 0xCD9E8D57 * c2
+        c0, c1, c2, c3 = ((p1 >> 32) ^ c1 ^ k0) & M32, p1 & M32, ((p0 >> 32) ^ c3 ^ k1) & M32, p0 & M32
+    return c0, c1, c2, c3
+
+
+def u_py(x):
+    return (2 * (x >> 9) + 1) * 2.0 ** -24
+
+
+def loss_py(mu, si, sc, mx, zp, ze):
+    sig = si + sc
+    if sig == 0:
+        return mu
+    if mu == 0:
+        return 0.0
+    if mu == mx:
+        return mx
+    sb, mb = sig / mx, mu / mx
+    smax = np.sqrt(mb * (1 - mb))
+    if sb >= smax:
+        sb = smax * (1 - 1e-6)
+    k = (smax / sb) ** 2 - 1
+    a, b = mb * k, (1 - mb) * k
+    wi, wc = si / sig, sc / sig
+    v = (sp.ndtri(zp) * wi + sp.ndtri(ze) * wc) / np.sqrt(wi * wi + wc * wc)
+    z, q = sp.ndtr(v), sp.ndtr(-v)
+    return mx * sp.betaincinv(a, b, z) if z <= 0.5 else mx * (1 - sp.betaincinv(b, a, q))
+
+
+def brute_force(pf, yet, seed, su, trial_index):
+    """Straight-line Algorithm 1: linear search over each XELT's record list."""
+    key = (seed & M32, (seed >> 32) & M32)
+    nl = len(pf["layer_prog"])
+    n = len(yet["trial_off"]) - 1
+    ylt = np.zeros((nl, n)); gross = np.zeros((nl, n))
+    for li in range(nl):
+        p = int(pf["layer_prog"][li])
+        occr, occl, aggr, aggl = pf["layer_terms"][li]
+        elts = pf["layer_elts"][int(pf["layer_elt_off"][li]):int(pf["layer_elt_off"][li + 1])]
+        for t in range(n):
+            i = int(trial_index[t])
+            S = 0.0
+            evs = yet["events"][int(yet["trial_off"][t]):int(yet["trial_off"][t + 1])]
+            for k, e in enumerate(evs):
+                l = 0.0
+                for j in elts:
+                    j = int(j)
+                    lo, hi = int(pf["elt_off"][j]), int(pf["elt_off"][j + 1])
+                    hit = [r for r in range(lo, hi) if int(pf["rec_event"][r]) == int(e)]
+                    if not hit:
+                        continue
+                    r = hit[0]
+                    mu, si, sc, mx = (float(pf[f][r]) for f in
+                                      ("rec_mean", "rec_sigma_i", "rec_sigma_c", "rec_max"))
+                    if su:
+                        zp = u_py(philox_py((i & M32, k, p, 1), key)[0])
+                        ze = u_py(philox_py((i & M32, k, j, 2), key)[0])
+                        x = loss_py(mu, si, sc, mx, zp, ze)
+                    else:
+                        x = mu
+                    if pf.get("elt_terms") is not None:
+                        R, Lm, sh = pf["elt_terms"][j]
+                        x = sh * min(max(x - R, 0.0), Lm)
+                    l += x
+                S += min(max(l - occr, 0.0), occl)
+            gross[li, t] = S
+            ylt[li, t] = min(max(S - aggr, 0.0), aggl)
+    return ylt, gross
+
+
+def tiny_case(rng, n_layers=None, n_elts=None, n_trials=None, sigma=True, integer=False,
+              xelt_terms=False):
+    C = int(rng.integers(5, 40))
+    n_elts = n_elts or int(rng.integers(1, 5))
+    recs = {k: [] for k in ("rec_event", "rec_mean", "rec_sigma_i", "rec_sigma_c", "rec_max")}
+    off = [0]
+    for j in range(n_elts):
+        R = int(rng.integers(0, C + 1))
+        evs = rng.choice(C, size=R, replace=False)
+        for e in evs:
+            mu = float(rng.integers(1, 1000)) if integer else float(10 ** rng.uniform(2, 6))
+            recs["rec_event"].append(int(e))
+            recs["rec_mean"].append(mu)
+            recs["rec_max"].append(mu * float(rng.uniform(1.5, 8)) if not integer else mu * 3)
+            recs["rec_sigma_i"].append(mu * float(rng.uniform(0, 0.4)) if sigma else 0.0)
+            recs["rec_sigma_c"].append(mu * float(rng.uniform(0, 0.3)) if sigma else 0.0)
+        off.append(off[-1] + R)
+    nl = n_layers or int(rng.integers(1, 4))
+    lel, loff = [], [0]
+    for _ in range(nl):
+        m = int(rng.integers(1, n_elts + 1))
+        lel += sorted(rng.choice(n_elts, size=m, replace=False).tolist())
+        loff.append(len(lel))
+    if integer:
+        terms = [[float(rng.integers(0, 500)), float(rng.integers(1, 3000)),
+                  float(rng.integers(0, 2000)), float(rng.integers(1, 20000))] for _ in range(nl)]
+    else:
+        terms = [[float(rng.uniform(0, 1e4)), float(rng.uniform(1e4, 1e6)),
+                  float(rng.uniform(0, 1e5)), float(rng.uniform(1e5, 1e7))] for _ in range(nl)]
+    pf = {"catalog_size": C, "elt_off": np.array(off, np.uint64),
+          **{k: np.array(v, np.uint32 if k == "rec_event" else np.float64) for k, v in recs.items()},
+          "elt_terms": (np.array([[float(rng.uniform(0, 100)), float(rng.uniform(1e3, 1e5)),
+                                   float(rng.uniform(0.1, 1))] for _ in range(n_elts)])
+                        if xelt_terms else None),
+          "layer_prog": rng.integers(0, 3, nl).astype(np.uint32),
+          "layer_elt_off": np.array(loff, np.uint64), "layer_elts": np.array(lel, np.uint32),
+          "layer_terms": np.array(terms)}
+    n = n_trials or int(rng.integers(1, 20))
+    lens = rng.integers(0, 11, n)
+    toff = np.zeros(n + 1, np.uint64); toff[1:] = np.cumsum(lens)
+    yet = {"trial_off": toff, "events": rng.integers(0, C, int(toff[-1])).astype(np.uint32)}
+    return pf, yet
+
+
+def test_occ_agg_terms_examples(golden):
+    for c in golden["occ_terms"]:
+        assert O.occ_terms(c["l"], c["R"], c["L"]) == c["y"], c["src"]
+    for c in golden["agg_terms"]:
+        assert O.agg_terms(c["s"], c["R"], c["L"]) == c["y"], c["src"]
+    assert O.xelt_terms(150.0, 100.0, 30.0, 0.5) == 15.0
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_engine_vs_brute_force(seed):
+    # <= 3 layers x 4 XELTs x 20 trials x 10 events, 100 seeds
+    rng = np.random.default_rng(1000 + seed)
+    pf, yet = tiny_case(rng, xelt_terms=(seed % 4 == 0))
+    su = seed % 5 != 0
+    tidx = rng.integers(0, 2 ** 32, len(yet["trial_off"]) - 1, dtype=np.uint64)
+    rseed = int(rng.integers(0, 2 ** 63))
+    got = O.run(pf, yet, seed=rseed, su=su, n_threads=2, trial_index=tidx)
+    ylt, gross = brute_force(pf, yet, rseed, su, tidx)
+    np.testing.assert_allclose(got["gross"], gross, rtol=1e-9, atol=1e-6)
+    np.testing.assert_allclose(got["ylt"], ylt, rtol=1e-9, atol=1e-6 * max(1.0, gross.max()))
+
+
+def test_engine_integer_sigma0_exact():
+    rng = np.random.default_rng(77)
+    for _ in range(20):
+        pf, yet = tiny_case(rng, sigma=False, integer=True)
+        got = O.run(pf, yet, seed=1, su=True)
+        ylt, gross = brute_force(pf, yet, 1, False, np.arange(len(yet["trial_off"]) - 1))
+        assert np.array_equal(got["gross"], gross)
+        assert np.array_equal(got["ylt"], ylt)
+        assert np.array_equal(got["ylt"], np.round(got["ylt"]))
+
+
+def test_engine_sigma0_su_on_equals_su_off():
+    rng = np.random.default_rng(78)
+    pf, yet = tiny_case(rng, sigma=False, n_trials=15)
+    a = O.run(pf, yet, seed=9, su=True)
+    b = O.run(pf, yet, seed=9, su=False)
+    assert np.array_equal(a["ylt"], b["ylt"])
+
+
+def test_engine_lookup_count_and_hash():
+    rng = np.random.default_rng(79)
+    pf, yet = tiny_case(rng, n_layers=2, n_elts=3, n_trials=12)
+    got = O.run(pf, yet, seed=3, su=False)
+    for li in range(2):
+        elts = pf["layer_elts"][int(pf["layer_elt_off"][li]):int(pf["layer_elt_off"][li + 1])]
+        for t in range(12):
+            evs = yet["events"][int(yet["trial_off"][t]):int(yet["trial_off"][t + 1])]
+            cnt, h = 0, 0
+            for k, e in enumerate(evs):
+                for j in elts:
+                    lo, hi = int(pf["elt_off"][j]), int(pf["elt_off"][j + 1])
+                    for r in range(lo, hi):
+                        if pf["rec_event"][r] == e:
+                            cnt += 1
+                            h = (h + O.lookup_hash(k, int(j), r - lo)) % 2 ** 64
+            assert got["count"][li, t] == cnt
+            assert int(got["hash"][li, t]) == h
+
+
+def test_engine_additivity_over_xelts():
+    # identity terms (OccR=0, OccL=inf, AggR=0, AggL=inf): YLT(A u B) = YLT(A) + YLT(B)
+    rng = np.random.default_rng(80)
+    pf, yet = tiny_case(rng, n_layers=1, n_elts=4, n_trials=15)
+    pf["layer_terms"] = np.array([[0.0, np.inf, 0.0, np.inf]])
+    pf["layer_prog"] = np.zeros(1, np.uint32)
+
+    def with_elts(elts):
+        q = dict(pf)
+        q["layer_elts"] = np.array(elts, np.uint32)
+        q["layer_elt_off"] = np.array([0, len(elts)], np.uint64)
+        return O.run(q, yet, seed=5, su=True)["ylt"][0]
+
+    np.testing.assert_allclose(with_elts([0, 1, 2, 3]), with_elts([0, 1]) + with_elts([2, 3]),
+                               rtol=1e-12)
+
+
+def test_engine_yearloss_order_invariant_sigma0():
+    # reading G6: with sigma = 0 the year loss g_agg(sum_k g_occ(l_k)) does not
+    # depend on the order of occurrences, even when the aggregate limit binds.
+    rng = np.random.default_rng(81)
+    pf, yet = tiny_case(rng, sigma=False, integer=True, n_trials=10)
+    base = O.run(pf, yet, seed=1, su=False)["ylt"]
+    ev = yet["events"].copy()
+    for t in range(10):
+        s, e = int(yet["trial_off"][t]), int(yet["trial_off"][t + 1])
+        ev[s:e] = rng.permutation(ev[s:e])
+    perm = O.run(pf, {"trial_off": yet["trial_off"], "events": ev}, seed=1, su=False)["ylt"]
+    assert np.array_equal(base, perm)
+
+
+def test_engine_thread_count_determinism():
+    rng = np.random.default_rng(82)
+    pf, yet = tiny_case(rng, n_trials=19)
+    outs = [O.run(pf, yet, seed=11, su=True, n_threads=t) for t in (1, 2, 8)]
+    for o in outs[1:]:
+        for k in ("ylt", "gross", "count", "hash"):
+            assert np.array_equal(o[k], outs[0][k])
+
+
+def test_engine_empty_and_bounds():
+    rng = np.random.default_rng(83)
+    pf, _ = tiny_case(rng, n_trials=3)
+    yet = {"trial_off": np.zeros(4, np.uint64), "events": np.zeros(0, np.uint32)}
+    out = O.run(pf, yet, seed=1, su=True)
+    assert (out["ylt"] == 0).all() and (out["count"] == 0).all()
+    pf2, yet2 = tiny_case(rng, n_trials=15)
+    out2 = O.run(pf2, yet2, seed=2, su=True)
+    for li in range(len(pf2["layer_prog"])):
+        assert (out2["ylt"][li] >= 0).all() and (out2["ylt"][li] <= pf2["layer_terms"][li][3]).all()
+    bad = dict(yet2); bad["events"] = yet2["events"].copy()
+    if bad["events"].size:
+        bad["events"][0] = pf2["catalog_size"]
+        with pytest.raises(O.OracleError):
+            O.run(pf2, bad, seed=2)

@@ -1,0 +1,211 @@
+/*
+ * ara.h -- C ABI of libara, the B200-native (sm_100a) hot path of Aggregate
+ * Risk Analysis with secondary uncertainty (Varghese & Rau-Chaplin,
+ * arXiv 1310.2274).  Citations: P:n = PAPER.md line n; Gn = a reading of the
+ * paper listed in DESIGN.md (numbered as in SURVEY.md section 8(c)).
+ *
+ * Problem statement (Algorithm 1): Input YET, XELT, PF; Output
+ * YLT; risk measures PML and TVaR from the YLT.
+ *
+ * Conventions for every entry point:
+ *  - Return value: ARA_OK (0) or one of the ARA_E* codes below.  Nothing is
+ *    thrown across the ABI.  ara_last_error() returns a thread-local message
+ *    with context (layer / XELT / record index, or trial) for the last
+ *    failure on the calling thread.
+ *  - Pointers marked "host or device" are classified with
+ *    cudaPointerGetAttributes; host memory may be pageable or pinned.
+ *  - Inputs are copied: the caller may free its arrays after the call
+ *    returns (device inputs are copied device-to-device on the context's
+ *    stream, so they must stay valid until that stream reaches the copy).
+ *  - Handles are owned by the library until the matching *_destroy call.
+ *  - All device work is enqueued on the context's CUDA stream; calls that
+ *    return host results synchronise that stream.
+ *  - No CPU fallback exists: every step of the path runs in CUDA kernels.
+ *    Creating a context fails with ARA_ECUDA when no device is usable.
+ */
+#ifndef ARA_H
+#define ARA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define ARA_OK 0
+#define ARA_EINVAL 1    /* invalid argument / failed validation            */
+#define ARA_ERANGE 2    /* event id or index out of range                  */
+#define ARA_EDUP 3      /* duplicate event in an XELT / XELT in a layer    */
+#define ARA_ENOMEM 4    /* host or device allocation failed                */
+#define ARA_ECUDA 5     /* CUDA runtime / launch error                     */
+#define ARA_ECONVERGE 6 /* beta quantile failed to converge for >=1 sample;
+                           outputs are still written, count in last_error  */
+#define ARA_ENCCL 7     /* reserved (collectives live above the ABI)       */
+
+/* ---- ara_run flags ----------------------------------------------------- */
+#define ARA_SU 1u            /* apply secondary uncertainty (section 3)     */
+#define ARA_DEBUG_LOOKUP 2u  /* also write per-(layer,trial) lookup count
+                                and hash (bit-exact check of Alg.1 line 6) */
+
+/* ---- limits (validated) ------------------------------------------------ */
+#define ARA_MAX_SLOTS 224    /* sum over layers of XELTs per layer          */
+#define ARA_MAX_LAYERS 64
+#define ARA_MAX_EVENTS_PER_TRIAL (1u << 24)
+
+typedef struct ara_ctx ara_ctx;
+typedef struct ara_portfolio ara_portfolio;
+typedef struct ara_yet ara_yet;
+
+/* One eXtended event loss XEL_i = {E_i, mu_l, sigma_I, sigma_C, max_l}
+ * (P:76).  Constraints: 0 <= mean_loss <= max_loss,
+ * sigma_i >= 0, sigma_c >= 0, max_loss > 0, all finite.  z_(E) is not
+ * stored: it is drawn per (trial, occurrence, XELT) (reading G2). */
+typedef struct {
+    uint32_t event_id;
+    float mean_loss;
+    float sigma_i;
+    float sigma_c;
+    float max_loss;
+} ara_record;
+
+/* Layer terms T = (OccR, OccL, AggR, AggL).  Retentions
+ * >= 0 and finite; limits > 0, +INFINITY allowed. */
+typedef struct {
+    double occ_retention;
+    double occ_limit;
+    double agg_retention;
+    double agg_limit;
+} ara_layer_terms;
+
+/* Optional XELT financial terms I (Alg.1 line 8; reading G7):
+ * x -> share * min(max(x - retention, 0), limit).  retention >= 0,
+ * limit > 0 (+INF ok), 0 < share <= 1. */
+typedef struct {
+    double retention;
+    double limit;
+    double share;
+} ara_elt_terms;
+
+/* Thread-local description of the last failure ("" if none). */
+const char *ara_last_error(void);
+
+/* Library version as 10000*major + 100*minor + patch. */
+int ara_version(void);
+
+/* Create a context on CUDA device `device`, enqueuing all work on
+ * `cuda_stream` (a cudaStream_t; NULL = the legacy default stream).
+ * ARA_ECUDA if the device is unavailable. */
+int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out);
+void ara_ctx_destroy(ara_ctx *ctx);
+/* Block until all work enqueued by this context has finished. */
+int ara_ctx_synchronize(ara_ctx *ctx);
+
+/* Host-only validation of a portfolio (no device needed); same arguments
+ * and checks as ara_create_portfolio.  Host pointers only.
+ *   catalog_size        number of events in the catalogue (event ids < it)
+ *   n_elts              number of XELTs
+ *   elt_rec_offsets     [n_elts+1] record ranges; records of XELT j are
+ *                       records[elt_rec_offsets[j] .. elt_rec_offsets[j+1])
+ *   records             [elt_rec_offsets[n_elts]] XELT records
+ *   elt_terms           [n_elts] or NULL (identity, G7)
+ *   n_layers            layers in the portfolio, <= ARA_MAX_LAYERS
+ *   layer_program       [n_layers] program id of each layer (keys z_(Prog,E))
+ *   layer_elt_offsets   [n_layers+1] ranges into layer_elts
+ *   layer_elts          XELT ids covered by each layer, no duplicates within
+ *                       a layer; sum of layer sizes <= ARA_MAX_SLOTS
+ *   layer_terms         [n_layers]
+ * Errors: ARA_EINVAL (bad value / shape), ARA_ERANGE (event id >=
+ * catalog_size, XELT id >= n_elts), ARA_EDUP (duplicate event in an XELT or
+ * duplicate XELT in a layer). */
+int ara_validate_portfolio(uint32_t catalog_size, uint32_t n_elts,
+                           const uint64_t *elt_rec_offsets, const ara_record *records,
+                           const ara_elt_terms *elt_terms, uint32_t n_layers,
+                           const uint32_t *layer_program, const uint64_t *layer_elt_offsets,
+                           const uint32_t *layer_elts, const ara_layer_terms *layer_terms);
+
+/* Preprocessing stage (direct-access lookup P:157): validate,
+ * build the event-major direct-access index and the presence bitmap on the
+ * host, upload, and derive the per-record beta parameters in a
+ * device kernel.  Arguments as ara_validate_portfolio (host pointers). */
+int ara_create_portfolio(ara_ctx *ctx, uint32_t catalog_size, uint32_t n_elts,
+                         const uint64_t *elt_rec_offsets, const ara_record *records,
+                         const ara_elt_terms *elt_terms, uint32_t n_layers,
+                         const uint32_t *layer_program, const uint64_t *layer_elt_offsets,
+                         const uint32_t *layer_elts, const ara_layer_terms *layer_terms,
+                         ara_portfolio **out);
+void ara_portfolio_destroy(ara_portfolio *pf);
+
+/* Load a YET: trial i of this table has global index
+ * first_trial + i (the Philox counters use the global index, so a
+ * trial-sharded run is bit-identical to a single run, reading G2/G4).
+ *   n_trials        trials in this table (>= 0)
+ *   first_trial     global index of trial 0; first_trial + n_trials <= 2^32
+ *   trial_offsets   [n_trials+1] host CSR offsets, or NULL for fixed length
+ *   fixed_len       events per trial when trial_offsets == NULL
+ *   event_ids       [total events] uint32, host or device, trial-major,
+ *                   occurrence order within a trial
+ *   timestamps      NULL, or [total events] host floats that must be sorted
+ *                   ascending within each trial; validated, then not
+ *                   used (reading G19: the year loss is order-invariant)
+ * Event ids are range-checked against the portfolio in ara_run (ARA_ERANGE). */
+int ara_load_yet(ara_ctx *ctx, uint64_t n_trials, uint64_t first_trial,
+                 const uint64_t *trial_offsets, uint32_t fixed_len, const uint32_t *event_ids,
+                 const float *timestamps, ara_yet **out);
+/* Replace the event ids of an existing YET (same shape) from host or device
+ * memory; asynchronous on the context stream (the host buffer must stay valid
+ * until the stream passes the copy; pinned memory makes it a true DMA). */
+int ara_yet_refill(ara_ctx *ctx, ara_yet *yet, const uint32_t *event_ids);
+uint64_t ara_yet_num_trials(const ara_yet *yet);
+void ara_yet_destroy(ara_yet *yet);
+
+/* Algorithm 1 for every layer over every trial of `yet`:
+ * lookup (line 6), secondary uncertainty (line 7, section 3) if
+ * flags & ARA_SU else the mean loss, XELT terms (line 8), per-occurrence
+ * sum (line 9), occurrence terms (line 11), aggregate terms on the trial sum
+ * (line 12, reading G6), YLT (line 17).
+ *   seed      64-bit key of the z_(Prog,E) / z_(E) Philox streams
+ *   ylt       DEVICE [n_layers][n_trials] fp32, caller-allocated
+ *   dbg_count NULL or DEVICE [n_layers][n_trials] present-pair counts
+ *   dbg_hash  NULL or DEVICE [n_layers][n_trials] sum of lookup fingerprints
+ * (dbg_* require flags & ARA_DEBUG_LOOKUP.)  Asynchronous except for the
+ * convergence / range flags, read back at the end (one small D2H).
+ * Errors: ARA_ERANGE (an event id >= catalog_size), ARA_ECONVERGE. */
+int ara_run(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint64_t seed,
+            uint32_t flags, float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash);
+
+/* PML and TVaR (reading G17) at each return period of one layer's
+ * YLT, or of the portfolio roll-up sum over layers (layer = -1, G16), by a
+ * device radix select over the fp32 bit patterns plus a sort of the tail.
+ *   ylt        DEVICE fp32, laid out [n_shards][n_layers][n_total/n_shards]
+ *              (n_shards = 1 for a single run; > 1 for an all-gathered set
+ *              of per-rank shards -- the measures are permutation-invariant)
+ *   n_total    trials over all shards (divisible by n_shards), >= 1
+ *   rps        [n_rp] return periods, each > 1 (host)
+ *   pml_out, tvar_out  [n_rp] host
+ * PML(RP): r = (N+1)/RP on the descending order statistics L(1)>=...>=L(N),
+ * linear interpolation, clamped to [L(N), L(1)]; TVaR(RP): mean of all
+ * entries >= VaR, VaR = the descending order statistic of rank ceil(N/RP)
+ * (integer RP) -- the conventions of SPEC S:345-387.  Synchronous. */
+int ara_risk_measures(ara_ctx *ctx, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                      uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
+                      double *pml_out, double *tvar_out);
+
+/* ---- component entry points (row-level parity tests) ------------------ */
+
+/* Secondary-uncertainty loss draws for n independent
+ * (record, z_(Prog,E), z_(E)) triples, on the device.  All pointers host;
+ * z values must lie in (0,1).  loss_out[n] host.  ARA_ECONVERGE as ara_run. */
+int ara_sample_losses(ara_ctx *ctx, uint64_t n, const ara_record *records,
+                      const float *z_prog, const float *z_event, float *loss_out);
+
+/* The uniforms the path draws (reading G2/G4): for each of n (trial i,
+ * occurrence k, id, tag) counters, U(lane 0 of Philox4x32-10(seed, ctr)).
+ * ctr: host [n][4] uint32 (i, k, program-or-XELT id, tag 1|2); out host [n]. */
+int ara_draw_uniforms(ara_ctx *ctx, uint64_t seed, uint64_t n, const uint32_t *ctr,
+                      float *u_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARA_H */

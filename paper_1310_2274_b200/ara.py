@@ -1,0 +1,267 @@
+"""Thin Python binding of libara's C ABI (include/ara.h).
+
+Argument marshalling only: every step of the method runs in libara's CUDA
+kernels.  PyTorch supplies device memory and the current CUDA stream.  There
+is no CPU fallback: importing this module without the built library, or
+creating a context without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libara.so")
+
+OK, EINVAL, ERANGE, EDUP, ENOMEM, ECUDA, ECONVERGE, ENCCL = range(8)
+SU = 1
+DEBUG_LOOKUP = 2
+MAX_SLOTS = 224
+MAX_LAYERS = 64
+
+RECORD_DTYPE = np.dtype([("event_id", "<u4"), ("mean_loss", "<f4"), ("sigma_i", "<f4"),
+                         ("sigma_c", "<f4"), ("max_loss", "<f4")])
+assert RECORD_DTYPE.itemsize == 20
+
+_NAMES = {OK: "ARA_OK", EINVAL: "ARA_EINVAL", ERANGE: "ARA_ERANGE", EDUP: "ARA_EDUP",
+          ENOMEM: "ARA_ENOMEM", ECUDA: "ARA_ECUDA", ECONVERGE: "ARA_ECONVERGE", ENCCL: "ARA_ENCCL"}
+
+# every entry point declared in include/ara.h
+EXPORTS = (
+    "ara_last_error", "ara_version", "ara_ctx_create", "ara_ctx_destroy", "ara_ctx_synchronize",
+    "ara_validate_portfolio", "ara_create_portfolio", "ara_portfolio_destroy", "ara_load_yet",
+    "ara_yet_refill", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_risk_measures",
+    "ara_sample_losses", "ara_draw_uniforms",
+)
+
+
+class AraError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libara.so not built ({LIB_PATH}); run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32
+    L.ara_last_error.restype = C.c_char_p
+    L.ara_version.restype = C.c_int
+    L.ara_ctx_create.argtypes = [C.c_int, vp, C.POINTER(vp)]
+    L.ara_ctx_destroy.argtypes = [vp]; L.ara_ctx_destroy.restype = None
+    L.ara_ctx_synchronize.argtypes = [vp]
+    pf_args = [u32, u32, vp, vp, vp, u32, vp, vp, vp, vp]
+    L.ara_validate_portfolio.argtypes = pf_args
+    L.ara_create_portfolio.argtypes = [vp] + pf_args + [C.POINTER(vp)]
+    L.ara_portfolio_destroy.argtypes = [vp]; L.ara_portfolio_destroy.restype = None
+    L.ara_load_yet.argtypes = [vp, u64, u64, vp, u32, vp, vp, C.POINTER(vp)]
+    L.ara_yet_refill.argtypes = [vp, vp, vp]
+    L.ara_yet_num_trials.argtypes = [vp]; L.ara_yet_num_trials.restype = u64
+    L.ara_yet_destroy.argtypes = [vp]; L.ara_yet_destroy.restype = None
+    L.ara_run.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp]
+    L.ara_risk_measures.argtypes = [vp, vp, u32, u64, u32, i32, vp, u32, vp, vp]
+    L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, vp]
+    L.ara_draw_uniforms.argtypes = [vp, u64, u64, vp, vp]
+    for n in EXPORTS:            # fail loudly if an entry point is missing
+        getattr(L, n)
+    return L
+
+
+lib = _load()
+
+
+def last_error() -> str:
+    return lib.ara_last_error().decode()
+
+
+def _check(st):
+    if st != OK:
+        raise AraError(st, last_error())
+
+
+def _p(a):
+    """ctypes pointer for a numpy array, a torch tensor, an int address, or None."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return C.c_void_p(a)
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _current_stream_handle(device):
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+# ---------------------------------------------------------------------------
+class Context:
+    """ara_ctx: a device plus the CUDA stream all work is enqueued on."""
+
+    def __init__(self, device: int = 0, stream=None):
+        if stream is None:
+            stream = _current_stream_handle(device)
+        elif hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        self.device = device
+        self.stream = stream
+        h = C.c_void_p()
+        _check(lib.ara_ctx_create(device, C.c_void_p(stream), C.byref(h)))
+        self.h = h
+
+    def synchronize(self):
+        _check(lib.ara_ctx_synchronize(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ara_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _records(pf):
+    recs = np.empty(len(pf["rec_event"]), RECORD_DTYPE)
+    recs["event_id"] = pf["rec_event"]
+    recs["mean_loss"] = pf["rec_mean"]
+    recs["sigma_i"] = pf["rec_sigma_i"]
+    recs["sigma_c"] = pf["rec_sigma_c"]
+    recs["max_loss"] = pf["rec_max"]
+    return recs
+
+
+def _pf_arrays(pf):
+    recs = _records(pf)
+    eoff = np.ascontiguousarray(pf["elt_off"], np.uint64)
+    et = pf.get("elt_terms")
+    et = None if et is None else np.ascontiguousarray(np.asarray(et, np.float64).reshape(-1, 3))
+    lprog = np.ascontiguousarray(pf["layer_prog"], np.uint32)
+    loff = np.ascontiguousarray(pf["layer_elt_off"], np.uint64)
+    lelts = np.ascontiguousarray(pf["layer_elts"], np.uint32)
+    lt = np.ascontiguousarray(np.asarray(pf["layer_terms"], np.float64).reshape(-1, 4))
+    keep = (recs, eoff, et, lprog, loff, lelts, lt)
+    args = [int(pf["catalog_size"]), len(eoff) - 1, _p(eoff), _p(recs), _p(et), len(lprog),
+            _p(lprog), _p(loff), _p(lelts), _p(lt)]
+    return args, keep
+
+
+def validate_portfolio(pf):
+    """ara_validate_portfolio (host only); raises AraError."""
+    args, _keep = _pf_arrays(pf)
+    _check(lib.ara_validate_portfolio(*args))
+
+
+class Portfolio:
+    """ara_portfolio built from the flat-array portfolio dict (see aragen)."""
+
+    def __init__(self, ctx: Context, pf):
+        args, _keep = _pf_arrays(pf)
+        h = C.c_void_p()
+        _check(lib.ara_create_portfolio(ctx.h, *args, C.byref(h)))
+        self.h, self.ctx = h, ctx
+        self.n_layers = len(pf["layer_prog"])
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ara_portfolio_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Yet:
+    """ara_yet: event ids (host numpy / pinned torch, or device torch)."""
+
+    def __init__(self, ctx: Context, events, trial_off=None, fixed_len=0, first_trial=0,
+                 n_trials=None, timestamps=None):
+        off = None if trial_off is None else np.ascontiguousarray(trial_off, np.uint64)
+        if n_trials is None:
+            n_trials = len(off) - 1 if off is not None else (len(events) // fixed_len if fixed_len else 0)
+        ts = None if timestamps is None else np.ascontiguousarray(timestamps, np.float32)
+        h = C.c_void_p()
+        _check(lib.ara_load_yet(ctx.h, int(n_trials), int(first_trial), _p(off),
+                                int(fixed_len) if off is None else 0, _p(events), _p(ts), C.byref(h)))
+        self.h, self.ctx = h, ctx
+        self.n_trials = int(n_trials)
+        self.first_trial = int(first_trial)
+
+    @classmethod
+    def from_dict(cls, ctx, yet, events=None):
+        """From aragen.build_yet's dict (fixed length uses the compact form)."""
+        ev = yet["events"] if events is None else events
+        if yet.get("fixed_len"):
+            return cls(ctx, ev, fixed_len=yet["fixed_len"], first_trial=yet.get("first_trial", 0),
+                       n_trials=len(yet["trial_off"]) - 1)
+        return cls(ctx, ev, trial_off=yet["trial_off"], first_trial=yet.get("first_trial", 0))
+
+    def refill(self, events):
+        _check(lib.ara_yet_refill(self.ctx.h, self.h, _p(events)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ara_yet_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug: bool = False,
+        ylt=None):
+    """ara_run; returns the device YLT [n_layers, n_trials] (and count/hash if debug)."""
+    import torch
+    dev = torch.device("cuda", ctx.device)
+    if ylt is None:
+        ylt = torch.empty((pf.n_layers, yet.n_trials), dtype=torch.float32, device=dev)
+    cnt = hsh = None
+    if debug:
+        cnt = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int32, device=dev)
+        hsh = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int64, device=dev)
+    flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0)
+    _check(lib.ara_run(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(cnt),
+                       _p(hsh)))
+    return (ylt, cnt, hsh) if debug else ylt
+
+
+def risk_measures(ctx: Context, ylt, n_layers: int, n_total: int, layer: int = 0,
+                  rps=(100, 250, 500), n_shards: int = 1):
+    """ara_risk_measures; returns (pml[n_rp], tvar[n_rp]) as numpy fp64."""
+    r = np.ascontiguousarray(rps, np.float64)
+    pml = np.empty(len(r)); tvar = np.empty(len(r))
+    _check(lib.ara_risk_measures(ctx.h, _p(ylt), int(n_layers), int(n_total), int(n_shards),
+                                 int(layer), _p(r), len(r), _p(pml), _p(tvar)))
+    return pml, tvar
+
+
+def sample_losses(ctx: Context, records, z_prog, z_event):
+    """ara_sample_losses: device loss draws for (record, z_P, z_E) triples."""
+    recs = np.ascontiguousarray(records, RECORD_DTYPE)
+    zp = np.ascontiguousarray(z_prog, np.float32)
+    ze = np.ascontiguousarray(z_event, np.float32)
+    out = np.empty(len(recs), np.float32)
+    _check(lib.ara_sample_losses(ctx.h, len(recs), _p(recs), _p(zp), _p(ze), _p(out)))
+    return out
+
+
+def draw_uniforms(ctx: Context, seed: int, ctr):
+    """ara_draw_uniforms: U(lane0(Philox(seed, ctr))) for ctr rows (i, k, id, tag)."""
+    c = np.ascontiguousarray(ctr, np.uint32).reshape(-1, 4)
+    out = np.empty(len(c), np.float32)
+    _check(lib.ara_draw_uniforms(ctx.h, int(seed) & 0xFFFFFFFFFFFFFFFF, len(c), _p(c), _p(out)))
+    return out

@@ -1,0 +1,550 @@
+// ara_api.cu -- the C ABI of libara (include/ara.h): validation, the host
+// planner that lays the portfolio out in HBM (event-major direct-access
+// index, presence bitmap, slot tables), YET handling, and launch plumbing.
+// All arithmetic of the method runs in the kernels (ara_kernels.cu,
+// ara_measures.cu); this file only validates, lays out and copies.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "ara_internal.cuh"
+#include "ara_measures.cuh"
+
+using namespace ara;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                        \
+    do {                                                                                \
+        cudaError_t _e = (call);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return fail(ARA_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e),     \
+                        __FILE__, __LINE__);                                            \
+    } while (0)
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+cudaError_t dalloc(T **p, size_t n) {
+    return cudaMalloc(reinterpret_cast<void **>(p), (n ? n : 1) * sizeof(T));
+}
+
+}  // namespace
+
+struct ara_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 0;
+    RunStatus *d_status = nullptr;
+    RunStatus *h_status = nullptr;     // pinned
+    MeasuresScratch ms;
+};
+
+struct ara_portfolio {
+    ara_ctx *ctx = nullptr;
+    PortfolioDev dev{};
+    uint32_t *d_index = nullptr, *d_bitmap = nullptr, *d_rec_orig = nullptr;
+    BetaRec *d_recs = nullptr;
+    float *d_mu = nullptr;
+    SlotInfo *d_slots = nullptr;
+    LayerInfo *d_layers = nullptr;
+};
+
+struct ara_yet {
+    ara_ctx *ctx = nullptr;
+    YetDev dev{};
+    uint32_t *d_events = nullptr;
+    uint64_t *d_offsets = nullptr;
+};
+
+extern "C" {
+
+const char *ara_last_error(void) { return g_err.c_str(); }
+
+int ara_version(void) { return 100; }
+
+int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
+    if (!out) return fail(ARA_EINVAL, "out is NULL");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(ARA_ECUDA, "no CUDA device available (%s); libara has no CPU path",
+                    cudaGetErrorString(e));
+    if (device < 0 || device >= n) return fail(ARA_EINVAL, "device %d out of range [0,%d)", device, n);
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return fail(ARA_ECUDA, "device %d is sm_%d%d; libara is built for sm_100a", device,
+                    prop.major, prop.minor);
+    ara_ctx *c = new ara_ctx();
+    c->device = device;
+    c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    c->num_sms = prop.multiProcessorCount;
+    if (cudaMalloc(&c->d_status, sizeof(RunStatus)) != cudaSuccess ||
+        cudaMallocHost(&c->h_status, sizeof(RunStatus)) != cudaSuccess ||
+        dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 256) != cudaSuccess ||
+        dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
+        dalloc(&c->ms.d_out, 128) != cudaSuccess) {
+        ara_ctx_destroy(c);
+        return fail(ARA_ENOMEM, "device allocation failed in ara_ctx_create");
+    }
+    *out = c;
+    return ARA_OK;
+}
+
+void ara_ctx_destroy(ara_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaFree(c->d_status);
+    cudaFreeHost(c->h_status);
+    cudaFree(c->ms.vals);
+    cudaFree(c->ms.buf);
+    cudaFree(c->ms.hist);
+    cudaFree(c->ms.state);
+    cudaFree(c->ms.d_rps);
+    cudaFree(c->ms.d_out);
+    delete c;
+}
+
+int ara_ctx_synchronize(ara_ctx *c) {
+    if (!c) return fail(ARA_EINVAL, "ctx is NULL");
+    CU(cudaSetDevice(c->device));
+    CU(cudaStreamSynchronize(c->stream));
+    return ARA_OK;
+}
+
+int ara_validate_portfolio(uint32_t C, uint32_t n_elts, const uint64_t *eoff, const ara_record *rec,
+                           const ara_elt_terms *et, uint32_t n_layers, const uint32_t *lprog,
+                           const uint64_t *loff, const uint32_t *lelts, const ara_layer_terms *lt) {
+    if (C == 0) return fail(ARA_EINVAL, "catalog_size must be >= 1");
+    if (!eoff) return fail(ARA_EINVAL, "elt_rec_offsets is NULL");
+    if (eoff[0] != 0) return fail(ARA_EINVAL, "elt_rec_offsets[0] must be 0");
+    for (uint32_t j = 0; j < n_elts; ++j)
+        if (eoff[j + 1] < eoff[j]) return fail(ARA_EINVAL, "elt_rec_offsets not monotone at XELT %u", j);
+    const uint64_t R = eoff[n_elts];
+    if (R && !rec) return fail(ARA_EINVAL, "records is NULL");
+    if (R >= (1ull << 32)) return fail(ARA_EINVAL, "too many records (%llu)", (unsigned long long)R);
+    std::vector<uint32_t> seen(C, 0xffffffffu);
+    for (uint32_t j = 0; j < n_elts; ++j) {
+        for (uint64_t r = eoff[j]; r < eoff[j + 1]; ++r) {
+            const ara_record &q = rec[r];
+            if (q.event_id >= C)
+                return fail(ARA_ERANGE, "XELT %u record %llu: event %u >= catalog_size %u", j,
+                            (unsigned long long)(r - eoff[j]), q.event_id, C);
+            if (seen[q.event_id] == j)
+                return fail(ARA_EDUP, "XELT %u: duplicate event %u (record %llu)", j, q.event_id,
+                            (unsigned long long)(r - eoff[j]));
+            seen[q.event_id] = j;
+            const bool fin = std::isfinite(q.mean_loss) && std::isfinite(q.sigma_i) &&
+                             std::isfinite(q.sigma_c) && std::isfinite(q.max_loss);
+            if (!fin || q.max_loss <= 0.0f || q.mean_loss < 0.0f || q.mean_loss > q.max_loss ||
+                q.sigma_i < 0.0f || q.sigma_c < 0.0f)
+                return fail(ARA_EINVAL,
+                            "XELT %u record %llu (event %u): need finite 0 <= mean <= max, max > 0, "
+                            "sigmas >= 0 (mean=%g sI=%g sC=%g max=%g)",
+                            j, (unsigned long long)(r - eoff[j]), q.event_id, q.mean_loss, q.sigma_i,
+                            q.sigma_c, q.max_loss);
+        }
+        if (et) {
+            const ara_elt_terms &t = et[j];
+            if (!(t.retention >= 0.0 && std::isfinite(t.retention)) || !(t.limit > 0.0) ||
+                std::isnan(t.limit) || !(t.share > 0.0 && t.share <= 1.0))
+                return fail(ARA_EINVAL, "XELT %u terms: need retention >= 0, limit > 0, 0 < share <= 1", j);
+        }
+    }
+    if (n_layers == 0) return fail(ARA_EINVAL, "portfolio has no layers");
+    if (n_layers > ARA_MAX_LAYERS) return fail(ARA_EINVAL, "n_layers %u > %d", n_layers, ARA_MAX_LAYERS);
+    if (!lprog || !loff || !lt) return fail(ARA_EINVAL, "layer arrays are NULL");
+    if (loff[0] != 0) return fail(ARA_EINVAL, "layer_elt_offsets[0] must be 0");
+    const uint64_t nslots = loff[n_layers];
+    if (nslots > ARA_MAX_SLOTS)
+        return fail(ARA_EINVAL, "sum of XELTs over layers %llu > %d", (unsigned long long)nslots, ARA_MAX_SLOTS);
+    if (nslots && !lelts) return fail(ARA_EINVAL, "layer_elts is NULL");
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        if (loff[l + 1] <= loff[l]) return fail(ARA_EINVAL, "layer %u covers no XELT", l);
+        for (uint64_t x = loff[l]; x < loff[l + 1]; ++x) {
+            if (lelts[x] >= n_elts)
+                return fail(ARA_ERANGE, "layer %u: XELT id %u >= n_elts %u", l, lelts[x], n_elts);
+            for (uint64_t y = loff[l]; y < x; ++y)
+                if (lelts[y] == lelts[x]) return fail(ARA_EDUP, "layer %u: duplicate XELT %u", l, lelts[x]);
+        }
+        const ara_layer_terms &t = lt[l];
+        if (!(t.occ_retention >= 0.0 && std::isfinite(t.occ_retention)) ||
+            !(t.agg_retention >= 0.0 && std::isfinite(t.agg_retention)) || !(t.occ_limit > 0.0) ||
+            !(t.agg_limit > 0.0) || std::isnan(t.occ_limit) || std::isnan(t.agg_limit))
+            return fail(ARA_EINVAL, "layer %u terms: need retentions >= 0 finite, limits > 0", l);
+    }
+    return ARA_OK;
+}
+
+int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t *eoff,
+                         const ara_record *rec, const ara_elt_terms *et, uint32_t n_layers,
+                         const uint32_t *lprog, const uint64_t *loff, const uint32_t *lelts,
+                         const ara_layer_terms *lt, ara_portfolio **out) {
+    if (!c || !out) return fail(ARA_EINVAL, "ctx/out is NULL");
+    *out = nullptr;
+    int st = ara_validate_portfolio(C, n_elts, eoff, rec, et, n_layers, lprog, loff, lelts, lt);
+    if (st != ARA_OK) return st;
+    CU(cudaSetDevice(c->device));
+
+    // slots: (layer, XELT) pairs, layer-major
+    const uint32_t S = (uint32_t)loff[n_layers];
+    std::vector<SlotInfo> slots(S);
+    for (uint32_t l = 0; l < n_layers; ++l)
+        for (uint64_t x = loff[l]; x < loff[l + 1]; ++x) {
+            SlotInfo &s = slots[x];
+            const uint32_t j = lelts[x];
+            s.elt = j; s.prog = lprog[l]; s.layer = l;
+            s.has_terms = et ? 1u : 0u;
+            s.ret = et ? (float)et[j].retention : 0.0f;
+            s.lim = et ? (float)et[j].limit : INFINITY;
+            s.share = et ? (float)et[j].share : 1.0f;
+            s.pad = 0.0f;
+        }
+    std::vector<LayerInfo> layers(n_layers);
+    for (uint32_t l = 0; l < n_layers; ++l)
+        layers[l] = {lt[l].occ_retention, lt[l].occ_limit, lt[l].agg_retention, lt[l].agg_limit};
+
+    // event-major direct-access index: per event the slots with a record
+    const uint32_t MW = (S + 31) / 32;
+    const uint32_t mwt = MW <= 1 ? 1 : (MW <= 3 ? 3 : 7);
+    const uint32_t stride = mwt == 1 ? 2 : (mwt == 3 ? 4 : 8);
+    std::vector<uint32_t> index((size_t)C * stride, 0u);
+    for (uint32_t s = 0; s < S; ++s) {
+        const uint32_t j = slots[s].elt;
+        for (uint64_t r = eoff[j]; r < eoff[j + 1]; ++r)
+            index[(size_t)rec[r].event_id * stride + 1 + (s >> 5)] |= 1u << (s & 31);
+    }
+    uint64_t total = 0;
+    for (uint32_t e = 0; e < C; ++e) {
+        uint32_t *ix = &index[(size_t)e * stride];
+        ix[0] = (uint32_t)total;
+        for (uint32_t w = 0; w < MW; ++w) total += (uint32_t)__builtin_popcount(ix[1 + w]);
+    }
+    if (total >= (1ull << 32)) return fail(ARA_EINVAL, "too many (layer, record) pairs");
+    std::vector<uint32_t> rec_src(total), rec_orig(total);
+    for (uint32_t s = 0; s < S; ++s) {
+        const uint32_t j = slots[s].elt;
+        for (uint64_t r = eoff[j]; r < eoff[j + 1]; ++r) {
+            const uint32_t *ix = &index[(size_t)rec[r].event_id * stride];
+            uint32_t rank = 0;
+            for (uint32_t w = 0; w < (s >> 5); ++w) rank += (uint32_t)__builtin_popcount(ix[1 + w]);
+            rank += (uint32_t)__builtin_popcount(ix[1 + (s >> 5)] & ((1u << (s & 31)) - 1u));
+            rec_src[ix[0] + rank] = (uint32_t)r;
+            rec_orig[ix[0] + rank] = (uint32_t)(r - eoff[j]);
+        }
+    }
+    // presence bitmap (any slot present), at most 2^20 bits (128 KiB of smem)
+    uint32_t shift = 0;
+    while (((uint64_t)C + (1ull << shift) - 1) >> shift > (1ull << 20)) ++shift;
+    const uint64_t bits = ((uint64_t)C + (1ull << shift) - 1) >> shift;
+    const uint32_t words = (uint32_t)((bits + 31) / 32);
+    std::vector<uint32_t> bitmap(words, 0u);
+    for (uint32_t e = 0; e < C; ++e) {
+        bool any = false;
+        for (uint32_t w = 0; w < MW; ++w) any |= index[(size_t)e * stride + 1 + w] != 0;
+        if (any) bitmap[(e >> shift) >> 5] |= 1u << ((e >> shift) & 31);
+    }
+
+    ara_portfolio *p = new ara_portfolio();
+    p->ctx = c;
+    ara_record *d_raw = nullptr;
+    uint32_t *d_src = nullptr;
+    const uint64_t R = eoff[n_elts];
+    cudaStream_t s = c->stream;
+    auto cleanup = [&](int code) {
+        cudaFree(d_raw); cudaFree(d_src);
+        ara_portfolio_destroy(p);
+        return code;
+    };
+    if (dalloc(&p->d_index, index.size()) || dalloc(&p->d_bitmap, words) ||
+        dalloc(&p->d_rec_orig, total) || dalloc(&p->d_recs, total) || dalloc(&p->d_mu, total) ||
+        dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) || dalloc(&d_raw, R) ||
+        dalloc(&d_src, total)) {
+        cudaGetLastError();
+        return cleanup(fail(ARA_ENOMEM, "device allocation failed in ara_create_portfolio"));
+    }
+    cudaError_t e = cudaSuccess;
+#define UP(dst, src, n) if (e == cudaSuccess && (n)) e = cudaMemcpyAsync(dst, src, (n) * sizeof(*(src)), cudaMemcpyHostToDevice, s)
+    UP(p->d_index, index.data(), index.size());
+    UP(p->d_bitmap, bitmap.data(), (size_t)words);
+    UP(p->d_rec_orig, rec_orig.data(), (size_t)total);
+    UP(p->d_slots, slots.data(), (size_t)S);
+    UP(p->d_layers, layers.data(), (size_t)n_layers);
+    UP(d_raw, rec, (size_t)R);
+    UP(d_src, rec_src.data(), (size_t)total);
+#undef UP
+    if (e != cudaSuccess) return cleanup(fail(ARA_ECUDA, "upload: %s", cudaGetErrorString(e)));
+    launch_prep_records(d_raw, d_src, total, p->d_recs, p->d_mu, s);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);     // host vectors die at return
+    cudaFree(d_raw); cudaFree(d_src);
+    d_raw = nullptr; d_src = nullptr;
+    if (e != cudaSuccess) return cleanup(fail(ARA_ECUDA, "record preparation: %s", cudaGetErrorString(e)));
+
+    PortfolioDev &d = p->dev;
+    d.catalog = C; d.n_slots = S; d.n_layers = n_layers; d.mask_words = mwt; d.idx_stride = stride;
+    d.bitmap_shift = shift; d.bitmap_words = words; d.n_dev_records = total;
+    d.index = p->d_index; d.bitmap = p->d_bitmap; d.recs = p->d_recs; d.rec_mu = p->d_mu;
+    d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
+    *out = p;
+    return ARA_OK;
+}
+
+void ara_portfolio_destroy(ara_portfolio *p) {
+    if (!p) return;
+    if (p->ctx) cudaSetDevice(p->ctx->device);
+    cudaFree(p->d_index); cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig); cudaFree(p->d_recs);
+    cudaFree(p->d_mu); cudaFree(p->d_slots); cudaFree(p->d_layers);
+    delete p;
+}
+
+int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint64_t *toff,
+                 uint32_t fixed_len, const uint32_t *events, const float *ts, ara_yet **out) {
+    if (!c || !out) return fail(ARA_EINVAL, "ctx/out is NULL");
+    *out = nullptr;
+    if (first_trial + n_trials > (1ull << 32))
+        return fail(ARA_EINVAL, "first_trial + n_trials must be <= 2^32 (Philox counter word)");
+    uint64_t total;
+    if (toff) {
+        if (toff[0] != 0) return fail(ARA_EINVAL, "trial_offsets[0] must be 0");
+        for (uint64_t t = 0; t < n_trials; ++t) {
+            if (toff[t + 1] < toff[t])
+                return fail(ARA_EINVAL, "trial_offsets not monotone at trial %llu", (unsigned long long)t);
+            if (toff[t + 1] - toff[t] > ARA_MAX_EVENTS_PER_TRIAL)
+                return fail(ARA_EINVAL, "trial %llu has more than 2^24 events", (unsigned long long)t);
+        }
+        total = toff[n_trials];
+    } else {
+        if (fixed_len > ARA_MAX_EVENTS_PER_TRIAL) return fail(ARA_EINVAL, "fixed_len > 2^24");
+        total = n_trials * (uint64_t)fixed_len;
+    }
+    if (total && !events) return fail(ARA_EINVAL, "event_ids is NULL");
+    if (ts) {
+        for (uint64_t t = 0; t < n_trials; ++t) {
+            const uint64_t b = toff ? toff[t] : t * fixed_len, e = toff ? toff[t + 1] : b + fixed_len;
+            for (uint64_t x = b; x < e; ++x) {
+                if (!std::isfinite(ts[x])) return fail(ARA_EINVAL, "trial %llu: non-finite timestamp", (unsigned long long)t);
+                if (x > b && ts[x] < ts[x - 1])
+                    return fail(ARA_EINVAL, "trial %llu: timestamps not sorted (P:58)", (unsigned long long)t);
+            }
+        }
+    }
+    CU(cudaSetDevice(c->device));
+    ara_yet *y = new ara_yet();
+    y->ctx = c;
+    if (dalloc(&y->d_events, total) != cudaSuccess ||
+        (toff && dalloc(&y->d_offsets, n_trials + 1) != cudaSuccess)) {
+        cudaGetLastError();
+        ara_yet_destroy(y);
+        return fail(ARA_ENOMEM, "device allocation of %llu event ids failed", (unsigned long long)total);
+    }
+    cudaError_t e = cudaSuccess;
+    if (total)
+        e = cudaMemcpyAsync(y->d_events, events, total * sizeof(uint32_t),
+                            is_device_ptr(events) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            c->stream);
+    if (e == cudaSuccess && toff)
+        e = cudaMemcpyAsync(y->d_offsets, toff, (n_trials + 1) * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        ara_yet_destroy(y);
+        return fail(ARA_ECUDA, "YET upload: %s", cudaGetErrorString(e));
+    }
+    y->dev.n_trials = n_trials; y->dev.first_trial = first_trial;
+    y->dev.fixed_len = toff ? 0u : fixed_len;
+    y->dev.offsets = y->d_offsets; y->dev.events = y->d_events; y->dev.n_events = total;
+    *out = y;
+    return ARA_OK;
+}
+
+int ara_yet_refill(ara_ctx *c, ara_yet *y, const uint32_t *events) {
+    if (!c || !y) return fail(ARA_EINVAL, "ctx/yet is NULL");
+    if (y->dev.n_events == 0) return ARA_OK;
+    if (!events) return fail(ARA_EINVAL, "event_ids is NULL");
+    CU(cudaSetDevice(c->device));
+    CU(cudaMemcpyAsync(y->d_events, events, y->dev.n_events * sizeof(uint32_t),
+                       is_device_ptr(events) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       c->stream));
+    return ARA_OK;
+}
+
+uint64_t ara_yet_num_trials(const ara_yet *y) { return y ? y->dev.n_trials : 0; }
+
+void ara_yet_destroy(ara_yet *y) {
+    if (!y) return;
+    if (y->ctx) cudaSetDevice(y->ctx->device);
+    cudaFree(y->d_events);
+    cudaFree(y->d_offsets);
+    delete y;
+}
+
+int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
+            float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash) {
+    if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
+    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP)) return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
+    if (y->dev.n_trials == 0) return ARA_OK;
+    if (!ylt) return fail(ARA_EINVAL, "ylt is NULL");
+    if ((dbg_count || dbg_hash) && !(flags & ARA_DEBUG_LOOKUP))
+        return fail(ARA_EINVAL, "dbg_count/dbg_hash need ARA_DEBUG_LOOKUP");
+    if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
+    CU(cudaSetDevice(c->device));
+    CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
+    CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, c->stream,
+                   c->num_sms));
+    CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (c->h_status->bad_event)
+        return fail(ARA_ERANGE, "%u event occurrences have event id >= catalog_size %u",
+                    c->h_status->bad_event, p->dev.catalog);
+    if (c->h_status->nonconverged)
+        return fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples",
+                    c->h_status->nonconverged);
+    return ARA_OK;
+}
+
+static uint64_t needed_rank(uint64_t N, double rp) {
+    uint64_t fl, m;
+    if (rp == std::floor(rp) && rp < 1.8e19) {
+        const uint64_t R = (uint64_t)rp;
+        fl = (N + 1) / R;
+        m = (N + R - 1) / R;
+    } else {
+        fl = (uint64_t)std::floor((double)(N + 1) / rp);
+        const uint64_t a = (uint64_t)std::floor((1.0 - 1.0 / rp) * (double)N) + 1;
+        m = N - (a < N ? a : N) + 1;
+    }
+    uint64_t k = fl + 1 > m ? fl + 1 : m;
+    if (k < 1) k = 1;
+    if (k > N) k = N;
+    return k;
+}
+
+int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                      uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
+                      double *pml_out, double *tvar_out) {
+    if (!c || !ylt || !rps || !pml_out || !tvar_out) return fail(ARA_EINVAL, "NULL argument");
+    if (n_total == 0) return fail(ARA_EINVAL, "empty YLT");
+    if (n_layers == 0 || n_shards == 0 || n_total % n_shards)
+        return fail(ARA_EINVAL, "need n_layers >= 1, n_shards >= 1 dividing n_total");
+    if (layer < -1 || layer >= (int32_t)n_layers) return fail(ARA_EINVAL, "layer %d out of range", layer);
+    if (n_rp == 0 || n_rp > 64) return fail(ARA_EINVAL, "n_rp must be in [1, 64]");
+    uint64_t k_need = 1;
+    for (uint32_t q = 0; q < n_rp; ++q) {
+        if (!(rps[q] > 1.0) || !std::isfinite(rps[q]))
+            return fail(ARA_EINVAL, "return period %g must be finite and > 1", rps[q]);
+        const uint64_t k = needed_rank(n_total, rps[q]);
+        if (k > k_need) k_need = k;
+    }
+    if (k_need > kSortCap)
+        return fail(ARA_EINVAL, "return period too short for the tail select: needs rank %llu > %u",
+                    (unsigned long long)k_need, kSortCap);
+    if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
+    CU(cudaSetDevice(c->device));
+    if (c->ms.capacity < n_total) {
+        cudaFree(c->ms.vals);
+        c->ms.vals = nullptr;
+        c->ms.capacity = 0;
+        CU(dalloc(&c->ms.vals, n_total));
+        c->ms.capacity = n_total;
+    }
+    CU(cudaMemcpyAsync(c->ms.d_rps, rps, n_rp * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CU(launch_measures(ylt, n_layers, n_total, n_shards, layer, c->ms.d_rps, n_rp, k_need, c->ms,
+                       c->ms.d_out, c->stream));
+    double out[128];
+    CU(cudaMemcpyAsync(out, c->ms.d_out, 2 * n_rp * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    for (uint32_t q = 0; q < n_rp; ++q) {
+        pml_out[q] = out[2 * q];
+        tvar_out[q] = out[2 * q + 1];
+    }
+    return ARA_OK;
+}
+
+int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const float *zp,
+                      const float *ze, float *loss_out) {
+    if (!c) return fail(ARA_EINVAL, "ctx is NULL");
+    if (n == 0) return ARA_OK;
+    if (!recs || !zp || !ze || !loss_out) return fail(ARA_EINVAL, "NULL argument");
+    for (uint64_t t = 0; t < n; ++t)
+        if (!(zp[t] > 0.0f && zp[t] < 1.0f && ze[t] > 0.0f && ze[t] < 1.0f))
+            return fail(ARA_EINVAL, "z values must lie in (0,1) (index %llu)", (unsigned long long)t);
+    CU(cudaSetDevice(c->device));
+    ara_record *d_raw = nullptr;
+    BetaRec *d_recs = nullptr;
+    float *d_mu = nullptr, *d_zp = nullptr, *d_ze = nullptr, *d_out = nullptr;
+    int code = ARA_OK;
+    cudaError_t e = cudaSuccess;
+    if (dalloc(&d_raw, n) || dalloc(&d_recs, n) || dalloc(&d_mu, n) || dalloc(&d_zp, n) ||
+        dalloc(&d_ze, n) || dalloc(&d_out, n)) {
+        cudaGetLastError();
+        code = fail(ARA_ENOMEM, "device allocation failed");
+    } else {
+        cudaStream_t s = c->stream;
+        e = cudaMemcpyAsync(d_raw, recs, n * sizeof(ara_record), cudaMemcpyHostToDevice, s);
+        if (!e) e = cudaMemcpyAsync(d_zp, zp, n * sizeof(float), cudaMemcpyHostToDevice, s);
+        if (!e) e = cudaMemcpyAsync(d_ze, ze, n * sizeof(float), cudaMemcpyHostToDevice, s);
+        if (!e) e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
+        if (!e) { launch_prep_records(d_raw, nullptr, n, d_recs, d_mu, s); e = cudaGetLastError(); }
+        if (!e) e = launch_sample_losses(d_recs, d_zp, d_ze, n, d_out, c->d_status, s);
+        if (!e) e = cudaMemcpyAsync(loss_out, d_out, n * sizeof(float), cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaStreamSynchronize(s);
+        if (e) code = fail(ARA_ECUDA, "ara_sample_losses: %s", cudaGetErrorString(e));
+        else if (c->h_status->nonconverged)
+            code = fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples", c->h_status->nonconverged);
+    }
+    cudaFree(d_raw); cudaFree(d_recs); cudaFree(d_mu); cudaFree(d_zp); cudaFree(d_ze); cudaFree(d_out);
+    return code;
+}
+
+int ara_draw_uniforms(ara_ctx *c, uint64_t seed, uint64_t n, const uint32_t *ctr, float *u_out) {
+    if (!c) return fail(ARA_EINVAL, "ctx is NULL");
+    if (n == 0) return ARA_OK;
+    if (!ctr || !u_out) return fail(ARA_EINVAL, "NULL argument");
+    CU(cudaSetDevice(c->device));
+    uint4 *d_ctr = nullptr;
+    float *d_out = nullptr;
+    int code = ARA_OK;
+    if (dalloc(&d_ctr, n) || dalloc(&d_out, n)) {
+        cudaGetLastError();
+        code = fail(ARA_ENOMEM, "device allocation failed");
+    } else {
+        cudaError_t e = cudaMemcpyAsync(d_ctr, ctr, n * sizeof(uint4), cudaMemcpyHostToDevice, c->stream);
+        if (!e) e = launch_draw_uniforms(seed, d_ctr, n, d_out, c->stream);
+        if (!e) e = cudaMemcpyAsync(u_out, d_out, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream);
+        if (!e) e = cudaStreamSynchronize(c->stream);
+        if (e) code = fail(ARA_ECUDA, "ara_draw_uniforms: %s", cudaGetErrorString(e));
+    }
+    cudaFree(d_ctr); cudaFree(d_out);
+    return code;
+}
+
+}  // extern "C"

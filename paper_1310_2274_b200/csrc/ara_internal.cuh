@@ -1,0 +1,86 @@
+// ara_internal.cuh -- device data layout shared by the host planner
+// (ara_api.cu) and the kernels.  See DESIGN.md "Data layout in HBM".
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ara.h"
+
+namespace ara {
+
+// Per (layer, XELT) "slot": slots are numbered layer-major, in each layer's
+// XELT order, so the present pairs of one occurrence, enumerated in slot
+// order, are grouped by layer.
+struct SlotInfo {
+    uint32_t elt;       // XELT id j (keys z_(E), reading G2)
+    uint32_t prog;      // program of the slot's layer (keys z_(Prog,E))
+    uint32_t layer;     // layer index
+    uint32_t has_terms; // 1 if XELT terms apply (G7)
+    float ret, lim, share, pad;
+};
+
+struct LayerInfo {
+    double occ_r, occ_l, agg_r, agg_l;
+};
+
+// Per-record sampler constants, derived on the device in fp64 from the
+// record and stored fp32: 32 B, one L2 sector.
+//   a, b      : alpha, beta, capped per G9
+//   c0        : a ln m + b ln(1-m) - ln B(a,b) with m = fl(a/(a+b))
+//   wi, wc    : sigma_I/sigma, sigma_C/sigma divided by sqrt(sum of squares)
+//               (steps 3-4 of section 3.2 folded into two weights)
+//   scale     : max_l; for degenerate records (G10) the loss itself
+//   mu_l, sd_l: mean and sd of logit(X), X ~ Beta(a,b): psi(a)-psi(b) and
+//               sqrt(psi1(a)+psi1(b)) -- only the solver's initial guess
+// a <= 0 marks a degenerate record: loss = scale.
+struct __align__(16) BetaRec {
+    float a, b, c0, wi;
+    float wc, scale, mu_l, sd_l;
+};
+
+struct PortfolioDev {
+    uint32_t catalog;
+    uint32_t n_slots, n_layers;
+    uint32_t mask_words;      // 32-bit words of the per-event slot mask
+    uint32_t idx_stride;      // uint32 words per event index entry (2, 4 or 8)
+    uint32_t bitmap_shift;    // event e -> presence bit e >> shift
+    uint32_t bitmap_words;
+    uint64_t n_dev_records;
+    const uint32_t *index;    // [catalog][idx_stride]: first record, mask words
+    const uint32_t *bitmap;   // [bitmap_words]
+    const BetaRec *recs;      // [n_dev_records] event-major, slot order
+    const float *rec_mu;      // [n_dev_records] mean loss (primary uncertainty)
+    const uint32_t *rec_orig; // [n_dev_records] record index within its XELT
+    const SlotInfo *slots;    // [n_slots]
+    const LayerInfo *layers;  // [n_layers]
+};
+
+struct YetDev {
+    uint64_t n_trials, first_trial;
+    uint32_t fixed_len;       // 0 => CSR
+    const uint64_t *offsets;  // device [n_trials+1] or null
+    const uint32_t *events;
+    uint64_t n_events;
+};
+
+// device-side status words
+struct RunStatus {
+    unsigned long long next_trial;   // dynamic trial scheduler
+    unsigned int nonconverged;
+    unsigned int bad_event;
+    unsigned int first_bad_trial_lo;
+};
+
+// kernels
+void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_t n,
+                         BetaRec *out, float *out_mu, cudaStream_t s);
+cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed, uint32_t flags,
+                        float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
+                        cudaStream_t s, int num_sms);
+cudaError_t launch_sample_losses(const BetaRec *recs, const float *zp, const float *ze,
+                                 uint64_t n, float *out, RunStatus *status, cudaStream_t s);
+cudaError_t launch_draw_uniforms(uint64_t seed, const uint4 *ctr, uint64_t n, float *out,
+                                 cudaStream_t s);
+cudaError_t launch_max_event(const uint32_t *ev, uint64_t n, uint32_t *out, cudaStream_t s);
+
+}  // namespace ara

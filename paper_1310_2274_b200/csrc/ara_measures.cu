@@ -1,0 +1,179 @@
+// ara_measures.cu -- PML / TVaR from the YLT on the device (reading
+// G17 with SPEC's conventions S:345-387).  A 4-pass, 8-bit MSB-first radix
+// select over order-preserving uint32 keys of the fp32 losses finds the
+// threshold T = the K-th largest loss (K = the deepest rank any return
+// period needs); the losses above T are compacted and bitonic-sorted in one
+// CTA; ties at T are counted, never materialised.  PML interpolates the
+// descending order statistics at r = (N+1)/RP; TVaR is the mean of all
+// losses >= VaR = L(ceil(N/RP)).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ara_measures.cuh"
+
+namespace ara {
+
+__device__ __forceinline__ uint32_t okey(float v) {
+    const uint32_t b = __float_as_uint(v == 0.0f ? 0.0f : v);   // -0 -> +0
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float okey_inv(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// vals[t] for the requested layer, or the roll-up (sum over layers, G16),
+// from a [n_shards][n_layers][per] layout.
+__global__ void gather_kernel(const float *ylt, uint32_t n_layers, uint64_t per, uint32_t n_shards,
+                              int32_t layer, float *vals) {
+    const uint64_t n = per * n_shards;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = t / per, i = t - s * per;
+        const float *base = ylt + s * (uint64_t)n_layers * per + i;
+        float v;
+        if (layer >= 0) {
+            v = base[(uint64_t)layer * per];
+        } else {
+            v = 0.0f;
+            for (uint32_t l = 0; l < n_layers; ++l) v += base[(uint64_t)l * per];
+        }
+        vals[t] = v;
+    }
+}
+
+__global__ void hist_kernel(const float *vals, uint64_t n, const SelectState *st, int shift,
+                            unsigned int *hist) {
+    __shared__ unsigned int h[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const uint32_t prefix = st->prefix, pmask = st->pmask;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = okey(vals[t]);
+        if ((k & pmask) == prefix) atomicAdd(&h[(k >> shift) & 0xffu], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// pick the digit holding the K_rem-th largest key among those matching
+__global__ void select_digit_kernel(SelectState *st, const unsigned int *hist, int shift) {
+    if (threadIdx.x != 0) return;
+    uint64_t need = st->k_rem;
+    int d = 255;
+    for (; d > 0; --d) {
+        if (hist[d] >= need) break;
+        need -= hist[d];
+    }
+    st->k_rem = need;
+    st->prefix |= (uint32_t)d << shift;
+    st->pmask |= 0xffu << shift;
+}
+
+__global__ void compact_kernel(const float *vals, uint64_t n, SelectState *st, float *buf,
+                               uint32_t cap) {
+    const uint32_t T = st->prefix;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const float v = vals[t];
+        const uint32_t k = okey(v);
+        if (k > T) {
+            const unsigned long long p = atomicAdd(&st->n_gt, 1ull);
+            if (p < cap) buf[p] = v;
+        } else if (k == T) {
+            atomicAdd(&st->n_eq, 1ull);
+        }
+    }
+}
+
+// one CTA: bitonic sort (descending) of up to kSortCap values, then the measures
+__global__ void __launch_bounds__(1024) sort_measures_kernel(const float *buf, SelectState *st,
+                                                             const double *rps, uint32_t n_rp,
+                                                             uint64_t n_total, double *out) {
+    extern __shared__ float sv[];
+    const uint32_t ng = (uint32_t)st->n_gt;
+    uint32_t P = 1;
+    while (P < ng) P <<= 1;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sv[i] = (i < ng) ? buf[i] : -INFINITY;
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                const uint32_t l = i ^ j;
+                if (l > i) {
+                    const float a = sv[i], b = sv[l];
+                    const bool desc = (i & k) == 0;
+                    if (desc ? (a < b) : (a > b)) { sv[i] = b; sv[l] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x != 0) return;
+    const float T = okey_inv(st->prefix);
+    const uint64_t neq = st->n_eq, N = n_total;
+    auto L = [&](uint64_t r) -> double {         // descending order statistic, 1-based
+        return r <= ng ? (double)sv[r - 1] : (double)T;
+    };
+    for (uint32_t q = 0; q < n_rp; ++q) {
+        const double rp = rps[q];
+        uint64_t fl, m;
+        double frac;
+        if (rp == floor(rp) && rp < 1.8e19) {
+            const uint64_t R = (uint64_t)rp;
+            fl = (N + 1) / R;
+            frac = (double)((N + 1) % R) / rp;
+            m = (N + R - 1) / R;
+        } else {
+            const double r = (double)(N + 1) / rp;
+            fl = (uint64_t)floor(r);
+            frac = r - (double)fl;
+            const uint64_t a = (uint64_t)floor((1.0 - 1.0 / rp) * (double)N) + 1;
+            m = N - (a < N ? a : N) + 1;
+        }
+        if (m < 1) m = 1;
+        if (m > N) m = N;
+        double pml;
+        if (fl < 1 || (fl == 1 && frac == 0.0)) pml = L(1);
+        else if (fl >= N) pml = L(N);
+        else pml = L(fl) + frac * (L(fl + 1) - L(fl));
+        const double var = L(m);
+        double sum = 0.0;
+        uint64_t cnt = 0;
+        for (uint32_t i = 0; i < ng && (double)sv[i] >= var; ++i) { sum += (double)sv[i]; ++cnt; }
+        if (var == (double)T) { sum += (double)neq * (double)T; cnt += neq; }
+        out[2 * q] = pml;
+        out[2 * q + 1] = sum / (double)cnt;
+    }
+}
+
+cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
+                            int32_t layer, const double *d_rps, uint32_t n_rp, uint64_t k_need,
+                            MeasuresScratch &S, double *d_out, cudaStream_t s) {
+    const uint64_t per = n_total / n_shards;
+    const int blocks = 148 * 4;
+    gather_kernel<<<blocks, 256, 0, s>>>(ylt, n_layers, per, n_shards, layer, S.vals);
+    SelectState init{};
+    init.k_rem = k_need;
+    cudaError_t e = cudaMemcpyAsync(S.state, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        e = cudaMemsetAsync(S.hist, 0, 256 * sizeof(unsigned int), s);
+        if (e != cudaSuccess) return e;
+        hist_kernel<<<blocks, 256, 0, s>>>(S.vals, n_total, S.state, shift, S.hist);
+        select_digit_kernel<<<1, 32, 0, s>>>(S.state, S.hist, shift);
+    }
+    compact_kernel<<<blocks, 256, 0, s>>>(S.vals, n_total, S.state, S.buf, kSortCap);
+    uint32_t P = 1;
+    while (P < k_need) P <<= 1;
+    const size_t smem = sizeof(float) * (P < 1 ? 1 : P);
+    e = cudaFuncSetAttribute(sort_measures_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(float) * kSortCap));
+    if (e != cudaSuccess) return e;
+    sort_measures_kernel<<<1, 1024, smem, s>>>(S.buf, S.state, d_rps, n_rp, n_total, d_out);
+    return cudaGetLastError();
+}
+
+}  // namespace ara

@@ -1,0 +1,327 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
+the same seeded inputs.
+
+Bars: lookup counts and hashes bit-exact; uniforms
+bit-exact; YLT entry-wise |g - o| <= 1e-4 |o| + 1e-6 S_o (S_o = the
+oracle's gross trial sum, the floor near the aggregate-retention clip);
+PML / TVaR within 1e-4 relative (+ the same floor); sigma = 0 with
+integer means bit-exact."""
+import numpy as np
+import pytest
+
+import aragen
+import oracle
+from oracle import measures as OM
+
+pytestmark = pytest.mark.gpu
+
+REL, FLOOR = 1e-4, 1e-6
+
+
+@pytest.fixture(scope="module")
+def A():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1310_2274_b200 import ara
+    return ara
+
+
+@pytest.fixture(scope="module")
+def ctx(A):
+    return A.Context(0)
+
+
+def ylt_check(g, ref, li=None):
+    o, S = ref["ylt"], ref["gross"]
+    if li is not None:
+        o, S = o[li], S[li]
+    g = np.asarray(g, np.float64)
+    err = np.abs(g - o)
+    tol = REL * np.abs(o) + FLOOR * S
+    bad = err > tol
+    assert not bad.any(), (f"{bad.sum()} of {bad.size} YLT entries out of tolerance; worst "
+                           f"{(err / np.maximum(tol, 1e-300)).max():.3g}x tol")
+    nz = o > 0
+    return float((err[nz] / o[nz]).max()) if nz.any() else 0.0
+
+
+def run_both(A, ctx, pf, yet, seed, su=True, trial_index=None):
+    P = A.Portfolio(ctx, pf)
+    Y = A.Yet.from_dict(ctx, yet)
+    ylt, cnt, hsh = A.run(ctx, P, Y, seed=seed, su=su, debug=True)
+    ref = oracle.run(pf, yet, seed=seed, su=su, trial_index=trial_index)
+    return (ylt.cpu().numpy(), cnt.cpu().numpy().astype(np.uint32),
+            hsh.cpu().numpy().view(np.uint64)), ref
+
+
+# ---- row a3: draws ----------------------------------------------------------
+def test_uniforms_bit_exact(A, ctx):
+    rng = np.random.default_rng(0)
+    n = 20000
+    ctr = np.stack([rng.integers(0, 2 ** 32, n), rng.integers(0, 2 ** 32, n),
+                    rng.integers(0, 256, n), rng.integers(1, 3, n)], 1).astype(np.uint32)
+    seed = 0x123456789ABCDEF
+    u = A.draw_uniforms(ctx, seed, ctr)
+    for t in range(0, n, 37):
+        i, k, j, tag = (int(x) for x in ctr[t])
+        ref = oracle.z_prog(seed, j, i, k) if tag == 1 else oracle.z_event(seed, i, k, j)
+        assert float(u[t]) == ref
+
+
+# ---- rows a4-a6: the sampler ---------------------------------------------------
+def gen_records(n, seed=0):
+    cfg = aragen.load_config("cfg3")
+    cfg.update(records_per_elt=n, catalog=max(n, 1000))
+    pf = aragen.build_portfolio(cfg)
+    from paper_1310_2274_b200 import ara
+    recs = np.empty(n, ara.RECORD_DTYPE)
+    recs["event_id"] = 0
+    recs["mean_loss"] = pf["rec_mean"][:n]
+    recs["sigma_i"] = pf["rec_sigma_i"][:n]
+    recs["sigma_c"] = pf["rec_sigma_c"][:n]
+    recs["max_loss"] = pf["rec_max"][:n]
+    return recs
+
+
+def grid_uniforms(rng, n):
+    return ((rng.integers(0, 2 ** 23, n) * 2 + 1) * 2.0 ** -24).astype(np.float32)
+
+
+def test_sampler_vs_oracle(A, ctx):
+    n = 200000
+    recs = gen_records(n)
+    rng = np.random.default_rng(1)
+    zp, ze = grid_uniforms(rng, n), grid_uniforms(rng, n)
+    g = A.sample_losses(ctx, recs, zp, ze).astype(np.float64)
+    o = oracle.sample_batch(recs["mean_loss"], recs["sigma_i"], recs["sigma_c"], recs["max_loss"],
+                            zp.astype(np.float64), ze.astype(np.float64))
+    mx = recs["max_loss"].astype(np.float64)
+    rel = np.abs(g - o) / np.maximum(o, 1e-300)
+    assert (np.abs(g - o) <= 1e-4 * o + 1e-7 * mx).all()
+    big = o > 1e-3 * mx
+    assert np.quantile(rel[big], 0.99) < 5e-6
+    assert np.median(rel[big]) < 5e-7
+    assert abs(np.mean((g[big] - o[big]) / o[big])) < 2e-7      # no systematic bias
+    assert ((g >= 0) & (g <= mx)).all()
+
+
+def test_sampler_extreme_v_and_edges(A, ctx):
+    recs = gen_records(4000)
+    rng = np.random.default_rng(2)
+    n = len(recs)
+    # deepest tails of the uniform grid: v up to |7.5|
+    zp = np.where(rng.uniform(size=n) < 0.5, 2.0 ** -24, 1 - 2.0 ** -24).astype(np.float32)
+    ze = zp.copy()
+    g = A.sample_losses(ctx, recs, zp, ze).astype(np.float64)
+    o = oracle.sample_batch(recs["mean_loss"], recs["sigma_i"], recs["sigma_c"], recs["max_loss"],
+                            zp.astype(np.float64), ze.astype(np.float64))
+    mx = recs["max_loss"].astype(np.float64)
+    assert np.isfinite(g).all()
+    assert (np.abs(g - o) <= 1e-4 * o + 1e-7 * mx).all()
+    # degenerate records (G10) and sigma_I = 0 / sigma_C = 0 extremes
+    from paper_1310_2274_b200 import ara
+    r = np.zeros(6, ara.RECORD_DTYPE)
+    r["max_loss"] = 100.0
+    r["mean_loss"] = [30, 0, 100, 25, 25, 50]
+    r["sigma_i"] = [0, 5, 5, 10, 0, 60]
+    r["sigma_c"] = [0, 5, 5, 0, 10, 0]
+    zp = np.array([0.3, 0.3, 0.3, 0.9, 0.9, 0.7], np.float32)
+    ze = np.array([0.6, 0.6, 0.6, 0.2, 0.2, 0.1], np.float32)
+    g = A.sample_losses(ctx, r, zp, ze).astype(np.float64)
+    assert g[0] == 30 and g[1] == 0 and g[2] == 100
+    for t in (3, 4, 5):     # sigma_C = 0 uses z_P only, sigma_I = 0 z_E only, capped
+        o = oracle.sample_loss(r["mean_loss"][t], r["sigma_i"][t], r["sigma_c"][t], 100.0,
+                               float(zp[t]), float(ze[t]))
+        assert abs(g[t] - o) <= 1e-4 * o + 1e-5, (t, g[t], o)
+
+
+# ---- the whole path on cfg1 (rows a1-a11) ------------------------------------
+def test_cfg1_full(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, cfg["seed"])
+    assert np.array_equal(cnt, ref["count"])
+    assert np.array_equal(hsh, ref["hash"])
+    ylt_check(g, ref)
+    lim = pf["layer_terms"][0][3]
+    assert (g >= 0).all() and (g <= lim).all()
+    assert (g == np.float32(lim)).sum() == (ref["ylt"] == lim).sum()     # limit binds identically
+
+
+def test_primary_integer_bit_exact(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    cfg.update(sigma_scale=0.0, integer_mu=True, n_trials=600, catalog=3000, records_per_elt=900,
+               layer_terms=[[2e5, 5e6, 2.0e7, 3.0e7]])
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    for su in (False, True):
+        (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, 5, su=su)
+        assert np.array_equal(cnt, ref["count"])
+        assert np.array_equal(g, ref["ylt"].astype(np.float32))
+
+
+def test_ragged_empty_trials_and_repeats(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    cfg.update(k_min=0, k_max=150, n_trials=700, catalog=300, records_per_elt=120)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg, first_trial=1000)
+    lens = np.diff(yet["trial_off"].astype(np.int64))
+    assert (lens == 0).any() and lens.max() > 64
+    (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, 9)
+    assert np.array_equal(cnt, ref["count"]) and np.array_equal(hsh, ref["hash"])
+    ylt_check(g, ref)
+
+
+@pytest.mark.parametrize("n_layers,J", [(8, 16), (3, 14), (1, 1), (2, 33)])
+def test_multi_layer_and_wide_masks(A, ctx, n_layers, J):
+    cfg = aragen.load_config("cfg1")
+    terms = [[2e5 * (l + 1), 5e6, 1.0e6, 5.0e7] for l in range(n_layers)]
+    cfg.update(n_layers=n_layers, elts_per_layer=J, catalog=4000, records_per_elt=600,
+               n_trials=300, layer_terms=terms)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    pf["layer_prog"] = (np.arange(n_layers) % 3).astype(np.uint32)    # several programs (G26)
+    (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, 77)
+    assert np.array_equal(cnt, ref["count"]) and np.array_equal(hsh, ref["hash"])
+    for li in range(n_layers):
+        ylt_check(g[li], ref, li)
+
+
+def test_shared_elts_and_xelt_terms(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    cfg.update(n_layers=1, elts_per_layer=4, catalog=2000, records_per_elt=500, n_trials=400,
+               layer_terms=[[1e5, 5e6, 0.0, np.inf]])
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    # two layers over overlapping XELTs, same program -> identical draws
+    pf["layer_prog"] = np.zeros(2, np.uint32)
+    pf["layer_elt_off"] = np.array([0, 3, 6], np.uint64)
+    pf["layer_elts"] = np.array([0, 1, 2, 1, 2, 3], np.uint32)
+    pf["layer_terms"] = np.array([[1e5, 5e6, 0.0, np.inf], [0.0, np.inf, 1e6, 4e7]])
+    pf["elt_terms"] = np.array([[1e4, 2e6, 0.5], [0.0, np.inf, 1.0], [5e3, 1e7, 0.8], [0, 3e6, 0.25]])
+    (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, 3)
+    assert np.array_equal(cnt, ref["count"]) and np.array_equal(hsh, ref["hash"])
+    for li in range(2):
+        ylt_check(g[li], ref, li)
+
+
+def test_determinism_and_sharding(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    pf = aragen.build_portfolio(cfg)
+    full = aragen.build_yet(cfg)
+    P = A.Portfolio(ctx, pf)
+    Y = A.Yet.from_dict(ctx, full)
+    a = A.run(ctx, P, Y, seed=11).cpu().numpy()
+    b = A.run(ctx, P, Y, seed=11).cpu().numpy()
+    assert np.array_equal(a, b)
+    parts = []
+    for r in range(4):        # trial-sharded "ranks": global keying -> identical YLT
+        n = cfg["n_trials"] // 4
+        y = aragen.build_yet(cfg, first_trial=r * n, n_trials=n)
+        parts.append(A.run(ctx, P, A.Yet.from_dict(ctx, y), seed=11).cpu().numpy())
+    assert np.array_equal(np.concatenate(parts, axis=1), a)
+
+
+def test_event_out_of_range(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg, n_trials=10)
+    yet["events"][17] = cfg["catalog"]
+    P = A.Portfolio(ctx, pf)
+    Y = A.Yet.from_dict(ctx, yet)
+    with pytest.raises(A.AraError) as ei:
+        A.run(ctx, P, Y, seed=1)
+    assert ei.value.code == A.ERANGE
+
+
+# ---- row a12: PML / TVaR -------------------------------------------------------
+@pytest.mark.parametrize("n", [1, 7, 1000, 100003, 800000])
+def test_measures_vs_oracle_sort(A, ctx, n):
+    import torch
+    rng = np.random.default_rng(n)
+    x = rng.lognormal(15, 1.2, n).astype(np.float32)
+    x[rng.uniform(size=n) < 0.1] = 0.0                       # retention clip mass
+    x[rng.uniform(size=n) < 0.002] = np.float32(3.0e8)       # limit clip ties
+    rps = [2, 10, 100, 250, 500] if n >= 1000 else [1.5, 2, 4]
+    d = torch.from_numpy(x).cuda()
+    pml, tvar = A.risk_measures(ctx, d, 1, n, 0, rps=rps)
+    for q, rp in enumerate(rps):
+        if OM.tvar_rp(x, rp) is None:
+            continue
+        assert pml[q] == pytest.approx(OM.pml(x.astype(np.float64), rp), rel=1e-12, abs=1e-9)
+        assert tvar[q] == pytest.approx(OM.tvar_rp(x.astype(np.float64), rp)[1], rel=1e-10)
+
+
+def test_measures_rollup_and_shards(A, ctx):
+    import torch
+    rng = np.random.default_rng(5)
+    L, n, P = 3, 40000, 4
+    y = rng.lognormal(12, 1, (P, L, n // P)).astype(np.float32)
+    d = torch.from_numpy(y).cuda()
+    flat = y.transpose(1, 0, 2).reshape(L, n)            # [L][n] in shard order
+    for layer in (-1, 0, 2):
+        v = flat.sum(axis=0, dtype=np.float32) if layer < 0 else flat[layer]
+        if layer < 0:
+            v = (flat[0] + flat[1]) + flat[2]            # fp32, ascending layer order
+        pml, tvar = A.risk_measures(ctx, d, L, n, layer, rps=(100, 250), n_shards=P)
+        for q, rp in enumerate((100, 250)):
+            assert pml[q] == pytest.approx(OM.pml(v.astype(np.float64), rp), rel=1e-12)
+            assert tvar[q] == pytest.approx(OM.tvar_rp(v.astype(np.float64), rp)[1], rel=1e-10)
+
+
+def test_measures_errors(A, ctx):
+    import torch
+    d = torch.zeros(10, device="cuda")
+    with pytest.raises(A.AraError):
+        A.risk_measures(ctx, d, 1, 10, 0, rps=(1.0,))
+    with pytest.raises(A.AraError):
+        A.risk_measures(ctx, d, 1, 0, 0, rps=(10,))
+    pml, tvar = A.risk_measures(ctx, d, 1, 10, 0, rps=(10,))
+    assert pml[0] == 0 and tvar[0] == 0
+
+
+# ---- full-size configurations, sampled ---------------------------------------
+@pytest.mark.parametrize("name,n_sample", [("cfg2", 300), ("cfg3", 300)])
+def test_full_size_sampled(A, ctx, name, n_sample):
+    import torch
+    cfg = aragen.load_config(name)
+    pf = aragen.build_portfolio(cfg)
+    N, K = cfg["n_trials"], cfg["events_per_trial"]
+    ev = torch.empty(N * K, dtype=torch.int32).pin_memory()
+    yet = aragen.build_yet(cfg, out=ev.numpy().view(np.uint32))
+    P = A.Portfolio(ctx, pf)
+    Y = A.Yet(ctx, ev, fixed_len=K, n_trials=N)
+    ylt = A.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"]).cpu().numpy()
+    lim = pf["layer_terms"][0][3]
+    assert (ylt >= 0).all() and (ylt <= lim).all()
+    rng = np.random.default_rng(123)
+    idx = np.sort(rng.choice(N, n_sample, replace=False))
+    idx[0], idx[-1] = 0, N - 1
+    sub = aragen.yet_for_trials(cfg, idx)
+    ref = oracle.run(pf, sub, seed=cfg["seed"], su=cfg["su"], trial_index=sub["trial_index"])
+    ylt_check(ylt[:, idx], ref)
+    # measures at full size: properties only (end-to-end parity of PML/TVaR is
+    # test_measures_end_to_end, where the oracle computes every trial)
+    pml, tvar = A.risk_measures(ctx, torch.from_numpy(ylt).cuda(), 1, N, 0, rps=cfg["return_periods"])
+    assert (np.diff(pml) >= 0).all() and (np.diff(tvar) >= 0).all()
+    assert (tvar >= pml * (1 - 1e-6)).all() and (tvar <= lim).all()
+
+
+@pytest.mark.parametrize("name,n", [("cfg1", None), ("cfg3", 20000), ("cfg5", 4000)])
+def test_measures_end_to_end(A, ctx, name, n):
+    cfg = aragen.load_config(name)
+    if n is not None:
+        cfg["n_trials"] = n
+    if name == "cfg5":
+        cfg.update(catalog=200000, records_per_elt=2000)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    ylt = A.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"])
+    ref = oracle.run(pf, yet, seed=cfg["seed"], su=cfg["su"])
+    ylt_check(ylt.cpu().numpy(), ref)
+    rps = [10, 50, 100] if cfg["n_trials"] < 20000 else cfg["return_periods"]
+    L = cfg["n_layers"]
+    for layer in ([0] if L == 1 else [0, L - 1, -1]):
+        pml, tvar = A.risk_measures(ctx, ylt, L, cfg["n_trials"], layer, rps=rps)
+        o = OM.rollup(ref["ylt"]) if layer < 0 else ref["ylt"][layer]
+        S = ref["gross"].sum(axis=0) if layer < 0 else ref["gross"][layer]
+        floor = FLOOR * S.max()
+        for q, rp in enumerate(rps):
+            po, to = OM.pml(o, rp), OM.tvar_rp(o, rp)[1]
+            assert abs(pml[q] - po) <= REL * abs(po) + floor, (layer, rp, pml[q], po)
+            assert abs(tvar[q] - to) <= REL * abs(to) + floor, (layer, rp, tvar[q], to)

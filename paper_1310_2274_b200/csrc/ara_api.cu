@@ -110,7 +110,9 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
         cudaMallocHost(&c->h_status, sizeof(RunStatus)) != cudaSuccess ||
         dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 256) != cudaSuccess ||
         dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
-        dalloc(&c->ms.d_out, 128) != cudaSuccess) {
+        dalloc(&c->ms.d_out, 128) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
+        dalloc(&c->ms.part_sum, kRedBlocks) != cudaSuccess ||
+        dalloc(&c->ms.part_cnt, kRedBlocks) != cudaSuccess) {
         ara_ctx_destroy(c);
         return fail(ARA_ENOMEM, "device allocation failed in ara_ctx_create");
     }
@@ -129,6 +131,9 @@ void ara_ctx_destroy(ara_ctx *c) {
     cudaFree(c->ms.state);
     cudaFree(c->ms.d_rps);
     cudaFree(c->ms.d_out);
+    cudaFree(c->ms.states);
+    cudaFree(c->ms.part_sum);
+    cudaFree(c->ms.part_cnt);
     delete c;
 }
 
@@ -463,9 +468,6 @@ int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t 
         const uint64_t k = needed_rank(n_total, rps[q]);
         if (k > k_need) k_need = k;
     }
-    if (k_need > kSortCap)
-        return fail(ARA_EINVAL, "return period too short for the tail select: needs rank %llu > %u",
-                    (unsigned long long)k_need, kSortCap);
     if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
     CU(cudaSetDevice(c->device));
     if (c->ms.capacity < n_total) {
@@ -476,8 +478,13 @@ int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t 
         c->ms.capacity = n_total;
     }
     CU(cudaMemcpyAsync(c->ms.d_rps, rps, n_rp * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CU(launch_measures(ylt, n_layers, n_total, n_shards, layer, c->ms.d_rps, n_rp, k_need, c->ms,
-                       c->ms.d_out, c->stream));
+    if (k_need <= kSortCap) {
+        CU(launch_measures(ylt, n_layers, n_total, n_shards, layer, c->ms.d_rps, n_rp, k_need, c->ms,
+                           c->ms.d_out, c->stream));
+    } else {   // deep ranks: a radix select per needed order statistic
+        CU(launch_measures_deep(ylt, n_layers, n_total, n_shards, layer, rps, n_rp, c->ms,
+                                c->ms.d_out, c->stream));
+    }
     double out[128];
     CU(cudaMemcpyAsync(out, c->ms.d_out, 2 * n_rp * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));

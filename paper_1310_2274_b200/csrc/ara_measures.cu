@@ -148,6 +148,108 @@ __global__ void __launch_bounds__(1024) sort_measures_kernel(const float *buf, S
     }
 }
 
+// ---- deep ranks (K > kSortCap): one radix select per needed rank ----------
+__global__ void tail_sum_kernel(const float *vals, uint64_t n, const SelectState *st, double *part_sum,
+                                unsigned long long *part_cnt) {
+    __shared__ double ss[256];
+    __shared__ unsigned long long sc[256];
+    const uint32_t T = st->prefix;                // key of VaR
+    double acc = 0.0;
+    unsigned long long c = 0;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const float v = vals[t];
+        if (okey(v) >= T) { acc += (double)v; ++c; }
+    }
+    ss[threadIdx.x] = acc; sc[threadIdx.x] = c;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) { ss[threadIdx.x] += ss[threadIdx.x + o]; sc[threadIdx.x] += sc[threadIdx.x + o]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { part_sum[blockIdx.x] = ss[0]; part_cnt[blockIdx.x] = sc[0]; }
+}
+
+struct DeepRp { uint64_t fl, m; double frac; };
+
+__global__ void deep_final_kernel(const SelectState *states, const DeepRp *q, uint32_t rp_index,
+                                  uint64_t N, const double *part_sum, const unsigned long long *part_cnt,
+                                  int nblocks, double *out) {
+    if (threadIdx.x != 0) return;
+    const SelectState *st = states + 3 * rp_index;
+    const double L1 = okey_inv(st[0].prefix), L2 = okey_inv(st[1].prefix);   // L(fl), L(fl+1)
+    const DeepRp r = q[rp_index];
+    double pml;
+    if (r.fl < 1 || (r.fl == 1 && r.frac == 0.0)) pml = L1;                   // rank clamped to 1
+    else if (r.fl >= N) pml = L1;                                             // rank clamped to N
+    else pml = L1 + r.frac * (L2 - L1);
+    double sum = 0.0;
+    unsigned long long cnt = 0;
+    for (int b = 0; b < nblocks; ++b) { sum += part_sum[b]; cnt += part_cnt[b]; }
+    out[2 * rp_index] = pml;
+    out[2 * rp_index + 1] = sum / (double)cnt;
+}
+
+static cudaError_t select_rank(const float *vals, uint64_t n, SelectState *st, unsigned int *hist,
+                               cudaStream_t s) {
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        cudaError_t e = cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned int), s);
+        if (e != cudaSuccess) return e;
+        hist_kernel<<<148 * 4, 256, 0, s>>>(vals, n, st, shift, hist);
+        select_digit_kernel<<<1, 32, 0, s>>>(st, hist, shift);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_measures_deep(const float *ylt, uint32_t n_layers, uint64_t n_total,
+                                 uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
+                                 MeasuresScratch &S, double *d_out, cudaStream_t s) {
+    const uint64_t per = n_total / n_shards, N = n_total;
+    gather_kernel<<<148 * 4, 256, 0, s>>>(ylt, n_layers, per, n_shards, layer, S.vals);
+    static thread_local SelectState init[kMaxRanks];
+    static thread_local DeepRp q[64];
+    for (uint32_t i = 0; i < n_rp; ++i) {
+        const double rp = rps[i];
+        uint64_t fl, m;
+        double frac;
+        if (rp == floor(rp) && rp < 1.8e19) {
+            const uint64_t R = (uint64_t)rp;
+            fl = (N + 1) / R; frac = (double)((N + 1) % R) / rp; m = (N + R - 1) / R;
+        } else {
+            const double r = (double)(N + 1) / rp;
+            fl = (uint64_t)floor(r); frac = r - (double)fl;
+            const uint64_t a = (uint64_t)floor((1.0 - 1.0 / rp) * (double)N) + 1;
+            m = N - (a < N ? a : N) + 1;
+        }
+        if (m < 1) m = 1;
+        if (m > N) m = N;
+        q[i] = {fl, m, frac};
+        const uint64_t r0 = fl < 1 ? 1 : (fl > N ? N : fl);
+        const uint64_t r1 = fl + 1 > N ? N : fl + 1;
+        init[3 * i] = SelectState{r0, 0u, 0u, 0ull, 0ull};
+        init[3 * i + 1] = SelectState{r1, 0u, 0u, 0ull, 0ull};
+        init[3 * i + 2] = SelectState{m, 0u, 0u, 0ull, 0ull};
+    }
+    cudaError_t e = cudaMemcpyAsync(S.states, init, 3 * n_rp * sizeof(SelectState),
+                                    cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    DeepRp *d_q = reinterpret_cast<DeepRp *>(S.buf);          // reuse the tail buffer
+    e = cudaMemcpyAsync(d_q, q, n_rp * sizeof(DeepRp), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    for (uint32_t i = 0; i < 3 * n_rp; ++i) {
+        e = select_rank(S.vals, N, S.states + i, S.hist, s);
+        if (e != cudaSuccess) return e;
+    }
+    for (uint32_t i = 0; i < n_rp; ++i) {
+        tail_sum_kernel<<<kRedBlocks, 256, 0, s>>>(S.vals, N, S.states + 3 * i + 2, S.part_sum, S.part_cnt);
+        deep_final_kernel<<<1, 32, 0, s>>>(S.states, d_q, i, N, S.part_sum, S.part_cnt, kRedBlocks, d_out);
+    }
+    e = cudaStreamSynchronize(s);          // host staging arrays are reused next call
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
                             int32_t layer, const double *d_rps, uint32_t n_rp, uint64_t k_need,
                             MeasuresScratch &S, double *d_out, cudaStream_t s) {

@@ -22,10 +22,21 @@ struct MeasuresScratch {
     SelectState *state = nullptr;
     double *d_rps = nullptr;   // [64]
     double *d_out = nullptr;   // [128]
+    // deep-rank path (K > kSortCap): one select per needed rank + a tail sum
+    SelectState *states = nullptr;       // [kMaxRanks]
+    double *part_sum = nullptr;          // [kRedBlocks]
+    unsigned long long *part_cnt = nullptr;
 };
+
+constexpr int kMaxRanks = 3 * 64;
+constexpr int kRedBlocks = 592;
 
 cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
                             int32_t layer, const double *d_rps, uint32_t n_rp, uint64_t k_need,
                             MeasuresScratch &S, double *d_out, cudaStream_t s);
+
+cudaError_t launch_measures_deep(const float *ylt, uint32_t n_layers, uint64_t n_total,
+                                 uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
+                                 MeasuresScratch &S, double *d_out, cudaStream_t s);
 
 }  // namespace ara

@@ -162,7 +162,7 @@ def test_primary_integer_bit_exact(A, ctx):
 def test_ragged_empty_trials_and_repeats(A, ctx):
     cfg = aragen.load_config("cfg1")
     cfg.update(k_min=0, k_max=150, n_trials=700, catalog=300, records_per_elt=120)
-    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg, first_trial=1000)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg, first_trial=1000, n_trials=700)
     lens = np.diff(yet["trial_off"].astype(np.int64))
     assert (lens == 0).any() and lens.max() > 64
     (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, 9)

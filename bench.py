@@ -202,6 +202,7 @@ def run_ours(args, cfg, rank, world, local):
     ctx = ara.Context(local, stream)
     pf = aragen.build_portfolio(cfg)
     P = ara.Portfolio(ctx, pf)
+    pf_info = P.info()
     # YET for this rank's global trials, generated into pinned host memory
     ev_host = torch.empty(n_loc * K, dtype=torch.int32).pin_memory()
     aragen.build_yet(cfg, first_trial=lo, n_trials=n_loc, out=ev_host.numpy().view(np.uint32))
@@ -330,6 +331,7 @@ def run_ours(args, cfg, rank, world, local):
         "gpu_launches": gpu_launches,
         "roofline": roof,
         "cpu_baseline": cpu,
+        "portfolio": pf_info,
         "clocks": clk.summary(),
         "measures": {str(layers[i]): {"pml": list(map(float, r[0])), "tvar": list(map(float, r[1]))}
                      for i, r in enumerate(res)},

@@ -47,6 +47,9 @@ extern "C" {
 #define ARA_SU 1u            /* apply secondary uncertainty (section 3)     */
 #define ARA_DEBUG_LOOKUP 2u  /* also write per-(layer,trial) lookup count
                                 and hash (bit-exact check of Alg.1 line 6) */
+#define ARA_EXACT 4u         /* solve every beta quantile per sample in fp64
+                                instead of the per-record quantile tables
+                                (validation mode; slow)                    */
 
 /* ---- limits (validated) ------------------------------------------------ */
 #define ARA_MAX_SLOTS 224    /* sum over layers of XELTs per layer          */
@@ -135,6 +138,13 @@ int ara_create_portfolio(ara_ctx *ctx, uint32_t catalog_size, uint32_t n_elts,
                          const uint32_t *layer_elts, const ara_layer_terms *layer_terms,
                          ara_portfolio **out);
 void ara_portfolio_destroy(ara_portfolio *pf);
+/* Layout facts of a built portfolio (any pointer may be NULL):
+ *   n_device_records  (layer, record) pairs held on the device
+ *   n_table_less      records whose quantile table failed its midpoint check
+ *                     (sampled by the fp64 per-sample solve instead)
+ *   device_bytes      HBM held by the portfolio */
+int ara_portfolio_info(const ara_portfolio *pf, uint64_t *n_device_records,
+                       uint64_t *n_table_less, uint64_t *device_bytes);
 
 /* Load a YET: trial i of this table has global index
  * first_trial + i (the Philox counters use the global index, so a
@@ -194,10 +204,14 @@ int ara_risk_measures(ara_ctx *ctx, const float *ylt, uint32_t n_layers, uint64_
 /* ---- component entry points (row-level parity tests) ------------------ */
 
 /* Secondary-uncertainty loss draws for n independent
- * (record, z_(Prog,E), z_(E)) triples, on the device.  All pointers host;
- * z values must lie in (0,1).  loss_out[n] host.  ARA_ECONVERGE as ara_run. */
+ * (record, z_(Prog,E), z_(E)) triples, on the device: record preparation
+ * (incl. the quantile table) then one draw each.  All pointers
+ * host; z values must lie in (0,1).  flags: 0, or ARA_EXACT to solve each
+ * quantile in fp64 instead of using the table.  loss_out[n] host.
+ * ARA_ECONVERGE as ara_run. */
 int ara_sample_losses(ara_ctx *ctx, uint64_t n, const ara_record *records,
-                      const float *z_prog, const float *z_event, float *loss_out);
+                      const float *z_prog, const float *z_event, uint32_t flags,
+                      float *loss_out);
 
 /* The uniforms the path draws (reading G2/G4): for each of n (trial i,
  * occurrence k, id, tag) counters, U(lane 0 of Philox4x32-10(seed, ctr)).

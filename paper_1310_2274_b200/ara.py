@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libara.so")
 OK, EINVAL, ERANGE, EDUP, ENOMEM, ECUDA, ECONVERGE, ENCCL = range(8)
 SU = 1
 DEBUG_LOOKUP = 2
+EXACT = 4
 MAX_SLOTS = 224
 MAX_LAYERS = 64
 
@@ -31,7 +32,8 @@ _NAMES = {OK: "ARA_OK", EINVAL: "ARA_EINVAL", ERANGE: "ARA_ERANGE", EDUP: "ARA_E
 # every entry point declared in include/ara.h
 EXPORTS = (
     "ara_last_error", "ara_version", "ara_ctx_create", "ara_ctx_destroy", "ara_ctx_synchronize",
-    "ara_validate_portfolio", "ara_create_portfolio", "ara_portfolio_destroy", "ara_load_yet",
+    "ara_validate_portfolio", "ara_create_portfolio", "ara_portfolio_destroy", "ara_portfolio_info",
+    "ara_load_yet",
     "ara_yet_refill", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_risk_measures",
     "ara_sample_losses", "ara_draw_uniforms",
 )
@@ -58,13 +60,14 @@ def _load():
     L.ara_validate_portfolio.argtypes = pf_args
     L.ara_create_portfolio.argtypes = [vp] + pf_args + [C.POINTER(vp)]
     L.ara_portfolio_destroy.argtypes = [vp]; L.ara_portfolio_destroy.restype = None
+    L.ara_portfolio_info.argtypes = [vp, vp, vp, vp]
     L.ara_load_yet.argtypes = [vp, u64, u64, vp, u32, vp, vp, C.POINTER(vp)]
     L.ara_yet_refill.argtypes = [vp, vp, vp]
     L.ara_yet_num_trials.argtypes = [vp]; L.ara_yet_num_trials.restype = u64
     L.ara_yet_destroy.argtypes = [vp]; L.ara_yet_destroy.restype = None
     L.ara_run.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp]
     L.ara_risk_measures.argtypes = [vp, vp, u32, u64, u32, i32, vp, u32, vp, vp]
-    L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, vp]
+    L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, u32, vp]
     L.ara_draw_uniforms.argtypes = [vp, u64, u64, vp, vp]
     for n in EXPORTS:            # fail loudly if an entry point is missing
         getattr(L, n)
@@ -170,6 +173,12 @@ class Portfolio:
         self.h, self.ctx = h, ctx
         self.n_layers = len(pf["layer_prog"])
 
+    def info(self):
+        """dict(n_device_records, n_table_less, device_bytes) (ara_portfolio_info)."""
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib.ara_portfolio_info(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"n_device_records": a.value, "n_table_less": b.value, "device_bytes": c.value}
+
     def close(self):
         if getattr(self, "h", None):
             lib.ara_portfolio_destroy(self.h)
@@ -223,7 +232,7 @@ class Yet:
 
 
 def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug: bool = False,
-        ylt=None):
+        ylt=None, exact: bool = False):
     """ara_run; returns the device YLT [n_layers, n_trials] (and count/hash if debug)."""
     import torch
     dev = torch.device("cuda", ctx.device)
@@ -233,7 +242,7 @@ def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug
     if debug:
         cnt = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int32, device=dev)
         hsh = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int64, device=dev)
-    flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0)
+    flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (EXACT if exact else 0)
     _check(lib.ara_run(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(cnt),
                        _p(hsh)))
     return (ylt, cnt, hsh) if debug else ylt
@@ -249,13 +258,14 @@ def risk_measures(ctx: Context, ylt, n_layers: int, n_total: int, layer: int = 0
     return pml, tvar
 
 
-def sample_losses(ctx: Context, records, z_prog, z_event):
+def sample_losses(ctx: Context, records, z_prog, z_event, exact: bool = False):
     """ara_sample_losses: device loss draws for (record, z_P, z_E) triples."""
     recs = np.ascontiguousarray(records, RECORD_DTYPE)
     zp = np.ascontiguousarray(z_prog, np.float32)
     ze = np.ascontiguousarray(z_event, np.float32)
     out = np.empty(len(recs), np.float32)
-    _check(lib.ara_sample_losses(ctx.h, len(recs), _p(recs), _p(zp), _p(ze), _p(out)))
+    _check(lib.ara_sample_losses(ctx.h, len(recs), _p(recs), _p(zp), _p(ze), EXACT if exact else 0,
+                                 _p(out)))
     return out
 
 

@@ -69,6 +69,7 @@ struct ara_portfolio {
     PortfolioDev dev{};
     uint32_t *d_index = nullptr, *d_bitmap = nullptr, *d_rec_orig = nullptr;
     BetaRec *d_recs = nullptr;
+    float2 *d_tables = nullptr;
     float *d_mu = nullptr;
     SlotInfo *d_slots = nullptr;
     LayerInfo *d_layers = nullptr;
@@ -79,6 +80,7 @@ struct ara_yet {
     YetDev dev{};
     uint32_t *d_events = nullptr;
     uint64_t *d_offsets = nullptr;
+    uint32_t *d_redo = nullptr;        // trials to re-run with the fp64 kernel
 };
 
 extern "C" {
@@ -290,6 +292,7 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     };
     if (dalloc(&p->d_index, index.size()) || dalloc(&p->d_bitmap, words) ||
         dalloc(&p->d_rec_orig, total) || dalloc(&p->d_recs, total) || dalloc(&p->d_mu, total) ||
+        dalloc(&p->d_tables, total * kTabStride) ||
         dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) || dalloc(&d_raw, R) ||
         dalloc(&d_src, total)) {
         cudaGetLastError();
@@ -306,8 +309,12 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     UP(d_src, rec_src.data(), (size_t)total);
 #undef UP
     if (e != cudaSuccess) return cleanup(fail(ARA_ECUDA, "upload: %s", cudaGetErrorString(e)));
-    launch_prep_records(d_raw, d_src, total, p->d_recs, p->d_mu, s);
-    e = cudaGetLastError();
+    e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
+    if (e == cudaSuccess) {
+        launch_prep_records(d_raw, d_src, total, p->d_recs, p->d_mu, p->d_tables, &c->d_status->nonconverged, s);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);     // host vectors die at return
     cudaFree(d_raw); cudaFree(d_src);
     d_raw = nullptr; d_src = nullptr;
@@ -316,9 +323,24 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     PortfolioDev &d = p->dev;
     d.catalog = C; d.n_slots = S; d.n_layers = n_layers; d.mask_words = mwt; d.idx_stride = stride;
     d.bitmap_shift = shift; d.bitmap_words = words; d.n_dev_records = total;
+    d.n_exact_records = c->h_status->nonconverged;
     d.index = p->d_index; d.bitmap = p->d_bitmap; d.recs = p->d_recs; d.rec_mu = p->d_mu;
+    d.tables = p->d_tables;
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
     *out = p;
+    return ARA_OK;
+}
+
+int ara_portfolio_info(const ara_portfolio *p, uint64_t *n_dev, uint64_t *n_tl, uint64_t *bytes) {
+    if (!p) return fail(ARA_EINVAL, "portfolio is NULL");
+    const PortfolioDev &d = p->dev;
+    if (n_dev) *n_dev = d.n_dev_records;
+    if (n_tl) *n_tl = d.n_exact_records;
+    if (bytes)
+        *bytes = (uint64_t)d.catalog * d.idx_stride * 4 + (uint64_t)d.bitmap_words * 4 +
+                 d.n_dev_records * (sizeof(BetaRec) + sizeof(float) + sizeof(uint32_t) +
+                                    kTabStride * sizeof(float2)) +
+                 d.n_slots * sizeof(SlotInfo) + d.n_layers * sizeof(LayerInfo);
     return ARA_OK;
 }
 
@@ -326,7 +348,7 @@ void ara_portfolio_destroy(ara_portfolio *p) {
     if (!p) return;
     if (p->ctx) cudaSetDevice(p->ctx->device);
     cudaFree(p->d_index); cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig); cudaFree(p->d_recs);
-    cudaFree(p->d_mu); cudaFree(p->d_slots); cudaFree(p->d_layers);
+    cudaFree(p->d_mu); cudaFree(p->d_slots); cudaFree(p->d_layers); cudaFree(p->d_tables);
     delete p;
 }
 
@@ -364,7 +386,7 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
     CU(cudaSetDevice(c->device));
     ara_yet *y = new ara_yet();
     y->ctx = c;
-    if (dalloc(&y->d_events, total) != cudaSuccess ||
+    if (dalloc(&y->d_events, total) != cudaSuccess || dalloc(&y->d_redo, n_trials) != cudaSuccess ||
         (toff && dalloc(&y->d_offsets, n_trials + 1) != cudaSuccess)) {
         cudaGetLastError();
         ara_yet_destroy(y);
@@ -408,24 +430,35 @@ void ara_yet_destroy(ara_yet *y) {
     if (y->ctx) cudaSetDevice(y->ctx->device);
     cudaFree(y->d_events);
     cudaFree(y->d_offsets);
+    cudaFree(y->d_redo);
     delete y;
 }
 
 int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
             float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash) {
     if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
-    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP)) return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
+    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT)) return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
     if (y->dev.n_trials == 0) return ARA_OK;
     if (!ylt) return fail(ARA_EINVAL, "ylt is NULL");
     if ((dbg_count || dbg_hash) && !(flags & ARA_DEBUG_LOOKUP))
         return fail(ARA_EINVAL, "dbg_count/dbg_hash need ARA_DEBUG_LOOKUP");
     if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
     CU(cudaSetDevice(c->device));
+    const bool exact = (flags & ARA_EXACT) != 0 && (flags & ARA_SU) != 0;
     CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
-    CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, c->stream,
-                   c->num_sms));
+    CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, nullptr, 0,
+                   y->d_redo, exact, c->stream, c->num_sms));
     CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
+    if (c->h_status->n_redo && !c->h_status->bad_event) {
+        // trials that met a table-less record: redo them with the fp64 kernel
+        const unsigned int n_redo = c->h_status->n_redo;
+        CU(cudaMemsetAsync(&c->d_status->next_trial, 0, sizeof(unsigned long long), c->stream));
+        CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, y->d_redo,
+                       n_redo, nullptr, true, c->stream, c->num_sms));
+        CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
     if (c->h_status->bad_event)
         return fail(ARA_ERANGE, "%u event occurrences have event id >= catalog_size %u",
                     c->h_status->bad_event, p->dev.catalog);
@@ -496,7 +529,8 @@ int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t 
 }
 
 int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const float *zp,
-                      const float *ze, float *loss_out) {
+                      const float *ze, uint32_t flags, float *loss_out) {
+    if (flags & ~ARA_EXACT) return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
     if (!c) return fail(ARA_EINVAL, "ctx is NULL");
     if (n == 0) return ARA_OK;
     if (!recs || !zp || !ze || !loss_out) return fail(ARA_EINVAL, "NULL argument");
@@ -506,11 +540,12 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
     CU(cudaSetDevice(c->device));
     ara_record *d_raw = nullptr;
     BetaRec *d_recs = nullptr;
+    float2 *d_tab = nullptr;
     float *d_mu = nullptr, *d_zp = nullptr, *d_ze = nullptr, *d_out = nullptr;
     int code = ARA_OK;
     cudaError_t e = cudaSuccess;
     if (dalloc(&d_raw, n) || dalloc(&d_recs, n) || dalloc(&d_mu, n) || dalloc(&d_zp, n) ||
-        dalloc(&d_ze, n) || dalloc(&d_out, n)) {
+        dalloc(&d_ze, n) || dalloc(&d_out, n) || dalloc(&d_tab, n * kTabStride)) {
         cudaGetLastError();
         code = fail(ARA_ENOMEM, "device allocation failed");
     } else {
@@ -519,8 +554,9 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
         if (!e) e = cudaMemcpyAsync(d_zp, zp, n * sizeof(float), cudaMemcpyHostToDevice, s);
         if (!e) e = cudaMemcpyAsync(d_ze, ze, n * sizeof(float), cudaMemcpyHostToDevice, s);
         if (!e) e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
-        if (!e) { launch_prep_records(d_raw, nullptr, n, d_recs, d_mu, s); e = cudaGetLastError(); }
-        if (!e) e = launch_sample_losses(d_recs, d_zp, d_ze, n, d_out, c->d_status, s);
+        if (!e) { launch_prep_records(d_raw, nullptr, n, d_recs, d_mu, d_tab, nullptr, s); e = cudaGetLastError(); }
+        if (!e) e = launch_sample_losses(d_recs, d_tab, d_zp, d_ze, n, (flags & ARA_EXACT) != 0, d_out,
+                                         c->d_status, s);
         if (!e) e = cudaMemcpyAsync(loss_out, d_out, n * sizeof(float), cudaMemcpyDeviceToHost, s);
         if (!e) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
         if (!e) e = cudaStreamSynchronize(s);
@@ -529,6 +565,7 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
             code = fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples", c->h_status->nonconverged);
     }
     cudaFree(d_raw); cudaFree(d_recs); cudaFree(d_mu); cudaFree(d_zp); cudaFree(d_ze); cudaFree(d_out);
+    cudaFree(d_tab);
     return code;
 }
 

@@ -26,16 +26,23 @@ struct LayerInfo {
 // Per-record sampler constants, derived on the device in fp64 from the
 // record and stored fp32: 32 B, one L2 sector.
 //   a, b      : alpha, beta, capped per G9
-//   c0        : a ln m + b ln(1-m) - ln B(a,b) with m = fl(a/(a+b))
 //   wi, wc    : sigma_I/sigma, sigma_C/sigma divided by sqrt(sum of squares)
 //               (steps 3-4 of section 3.2 folded into two weights)
 //   scale     : max_l; for degenerate records (G10) the loss itself
-//   mu_l, sd_l: mean and sd of logit(X), X ~ Beta(a,b): psi(a)-psi(b) and
-//               sqrt(psi1(a)+psi1(b)) -- only the solver's initial guess
-// a <= 0 marks a degenerate record: loss = scale.
+//   mu_l, sd_l: mean and sd of logit(X), X ~ Beta(a,b) (psi(a)-psi(b),
+//               sqrt(psi1(a)+psi1(b))): initial guess of the fp64 solve
+//   mode      : kModeTable (quantile table), kModeExact (per-sample fp64
+//               solve), kModeDegenerate (loss = scale)
+// quantile tables: lambda(v) = logit I^-1(Phi(v); a, b) at v = -8 + 0.5 j
+constexpr int kTabNodes = 33;           // j = 0..32
+constexpr int kTabStride = 34;          // float2 per record (padded)
+constexpr float kTabV0 = -8.0f, kTabH = 0.5f;
+
+constexpr uint32_t kModeTable = 0, kModeExact = 1, kModeDegenerate = 2;
 struct __align__(16) BetaRec {
-    float a, b, c0, wi;
-    float wc, scale, mu_l, sd_l;
+    float a, b, wi, wc;
+    float scale, mu_l, sd_l;
+    uint32_t mode;
 };
 
 struct PortfolioDev {
@@ -46,9 +53,11 @@ struct PortfolioDev {
     uint32_t bitmap_shift;    // event e -> presence bit e >> shift
     uint32_t bitmap_words;
     uint64_t n_dev_records;
+    uint32_t n_exact_records; // records without a quantile table (fp64 per-sample solve)
     const uint32_t *index;    // [catalog][idx_stride]: first record, mask words
     const uint32_t *bitmap;   // [bitmap_words]
     const BetaRec *recs;      // [n_dev_records] event-major, slot order
+    const float2 *tables;     // [n_dev_records][kTabStride] (lambda, lambda') nodes
     const float *rec_mu;      // [n_dev_records] mean loss (primary uncertainty)
     const uint32_t *rec_orig; // [n_dev_records] record index within its XELT
     const SlotInfo *slots;    // [n_slots]
@@ -66,21 +75,28 @@ struct YetDev {
 // device-side status words
 struct RunStatus {
     unsigned long long next_trial;   // dynamic trial scheduler
-    unsigned int nonconverged;
-    unsigned int bad_event;
-    unsigned int first_bad_trial_lo;
+    unsigned int nonconverged;       // fp64 solves that did not converge
+    unsigned int bad_event;          // occurrences with event id >= catalog
+    unsigned int n_redo;             // trials touching a table-less record
+    unsigned int pad;
 };
 
 // kernels
 void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_t n,
-                         BetaRec *out, float *out_mu, cudaStream_t s);
+                         BetaRec *out, float *out_mu, float2 *tables, unsigned int *n_exact,
+                         cudaStream_t s);
+// Scan every trial of `yet`, or (trial_list != null) only the n_list listed
+// trials.  Without ARA_EXACT the table-only kernel runs and appends to
+// `redo` every trial that met a table-less record; the caller re-runs those
+// with exact = true (the fp64 per-sample kernel).
 cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed, uint32_t flags,
                         float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
+                        const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
                         cudaStream_t s, int num_sms);
-cudaError_t launch_sample_losses(const BetaRec *recs, const float *zp, const float *ze,
-                                 uint64_t n, float *out, RunStatus *status, cudaStream_t s);
+cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float *zp,
+                                 const float *ze, uint64_t n, bool exact, float *out,
+                                 RunStatus *status, cudaStream_t s);
 cudaError_t launch_draw_uniforms(uint64_t seed, const uint4 *ctr, uint64_t n, float *out,
                                  cudaStream_t s);
-cudaError_t launch_max_event(const uint32_t *ev, uint64_t n, uint32_t *out, cudaStream_t s);
 
 }  // namespace ara

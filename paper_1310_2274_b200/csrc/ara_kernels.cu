@@ -1,6 +1,7 @@
 // ara_kernels.cu -- sm_100a kernels of the ARA hot path (arXiv 1310.2274):
-// record preparation, the fused YET scan (Algorithm 1,
-// P:134-170), and component kernels used by the row-level parity tests.
+// record preparation + quantile tables, the fused YET scan
+// (Algorithm 1), and component kernels used by the row-level
+// parity tests.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -10,28 +11,37 @@
 namespace ara {
 
 // ---------------------------------------------------------------------------
-// Record preparation (preprocessing stage): beta parameters with the
-// sigma_beta cap (G9), degenerate records (G10), sampler constants.
-// fp64 on the device, stored fp32.
+// Record preparation (preprocessing stage), one thread per record, fp64:
+// beta parameters with the sigma_beta cap (G9), degenerate records
+// (G10), the steps-3/4 weights, and the record's quantile table
+// lambda(v) = logit I^-1(Phi(v); a, b) at v = -8, -7.5, ..., 8 with its
+// derivative.  The table is accepted only if the quintic Hermite interpolant
+// (evaluated from the stored fp32 values, as the sampler will) matches an
+// exact solve at every interval midpoint to (1-x)|dlambda| <= 1e-5 (10x
+// inside the parity tolerance; typical table error is < 1e-8);
+// otherwise the record is marked for the per-sample fp64 solve.
 // ---------------------------------------------------------------------------
-__device__ double digamma_d(double x) {
-    double r = 0.0;
-    while (x < 6.0) { r -= 1.0 / x; x += 1.0; }
-    const double f = 1.0 / (x * x);
-    return r + log(x) - 0.5 / x -
-           f * (1.0 / 12 - f * (1.0 / 120 - f * (1.0 / 252 - f * (1.0 / 240 - f / 132))));
-}
-__device__ double trigamma_d(double x) {
-    double r = 0.0;
-    while (x < 6.0) { r += 1.0 / (x * x); x += 1.0; }
-    const double f = 1.0 / (x * x);
-    return r + 1.0 / x + f / 2.0 +
-           f / x * (1.0 / 6 - f * (1.0 / 30 - f * (1.0 / 42 - f * (1.0 / 30))));
+__device__ double quintic_mid64(float l0, float d0, float l1, float d1, double v0, double a, double b) {
+    // the sampler's interpolant at t = 1/2, evaluated in fp64 on the fp32 table values
+    auto s2 = [&](double lam, double d, double v) {
+        const double x = 1.0 / (1.0 + exp(-lam)), y = 1.0 / (1.0 + exp(lam));
+        return d * (-v - (a * y - b * x) * d);
+    };
+    const double H = kTabH;
+    const double s0 = s2(l0, d0, v0), s1 = s2(l1, d1, v0 + H);
+    // basis at t = 1/2: h01 = 1/2, h10 = 1/8 * 5/4... computed generically
+    const double t = 0.5, omt = 0.5, t2 = t * t, t3 = t2 * t;
+    const double h01 = t3 * (10.0 + t * (-15.0 + 6.0 * t));
+    const double h10 = t * omt * omt * omt * (1.0 + 3.0 * t);
+    const double h11 = -t3 * omt * (4.0 - 3.0 * t);
+    const double h20 = 0.5 * t2 * omt * omt * omt, h21 = 0.5 * t3 * omt * omt;
+    return l0 + h01 * ((double)l1 - l0) + h10 * H * d0 + h11 * H * d1 + h20 * H * H * s0 + h21 * H * H * s1;
 }
 
-__global__ void prep_records_kernel(const ara_record *__restrict__ raw,
-                                    const uint32_t *__restrict__ src, uint64_t n,
-                                    BetaRec *__restrict__ out, float *__restrict__ out_mu) {
+__global__ void prep_records_kernel(const ara_record *__restrict__ raw, const uint32_t *__restrict__ src,
+                                    uint64_t n, BetaRec *__restrict__ out, float *__restrict__ out_mu,
+                                    float2 *__restrict__ tables, unsigned int *n_exact) {
+    const double LN_SQRT_2PI = 0.91893853320467274178;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const ara_record q = raw[src ? src[t] : t];
@@ -40,9 +50,9 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw,
         BetaRec r;
         const double sigma = si + sc;                          // step 1
         if (sigma == 0.0 || mu == 0.0 || mu == mx) {           // G10
-            r.a = -1.0f; r.b = 0.0f; r.c0 = 0.0f; r.wi = 0.0f; r.wc = 0.0f;
+            r.a = 0.0f; r.b = 0.0f; r.wi = 0.0f; r.wc = 0.0f;
             r.scale = (sigma == 0.0) ? q.mean_loss : (mu == 0.0 ? 0.0f : q.max_loss);
-            r.mu_l = 0.0f; r.sd_l = 0.0f;
+            r.mu_l = 0.0f; r.sd_l = 0.0f; r.mode = kModeDegenerate;
             out[t] = r;
             continue;
         }
@@ -50,55 +60,100 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw,
         const double smax = sqrt(mub * (1.0 - mub));
         const double sb = (sb0 >= smax) ? smax * (1.0 - 1e-6) : sb0;
         const double kappa = (smax / sb) * (smax / sb) - 1.0;
-        const float af = (float)(mub * kappa), bf = (float)((1.0 - mub) * kappa);
-        const double a = af, b = bf;
-        const float mf = __fdiv_rn(af, __fadd_rn(af, bf));     // same op as the sampler
-        const double m = mf;
-        const double lnB = lgamma(a) + lgamma(b) - lgamma(a + b);
+        const double a = mub * kappa, b = (1.0 - mub) * kappa;
         const double wi = si / sigma, wc = sc / sigma;
         const double nr = sqrt(wi * wi + wc * wc);
-        r.a = af; r.b = bf;
-        r.c0 = (float)(a * log(m) + b * log1p(-m) - lnB);
+        const double lnB = lgamma(a) + lgamma(b) - lgamma(a + b);
+        const double mu_l = digamma_d(a) - digamma_d(b);
+        r.a = (float)a; r.b = (float)b;
         r.wi = (float)(wi / nr); r.wc = (float)(wc / nr);
         r.scale = q.max_loss;
-        r.mu_l = (float)(digamma_d(a) - digamma_d(b));
+        r.mu_l = (float)mu_l;
         r.sd_l = (float)sqrt(trigamma_d(a) + trigamma_d(b));
+        r.mode = kModeTable;
+        if (tables) {
+            float2 *tab = tables + t * kTabStride;
+            double lam[kTabNodes], d1[kTabNodes], d2[kTabNodes];
+            bool good = true;
+            auto node = [&](int j, double guess) {
+                const double v = kTabV0 + kTabH * j;
+                bool ok;
+                const double l = lambda_exact64(v, a, b, lnB, guess, ok);
+                const Tail64 e = tail64(l, v <= 0.0, a, b, lnB);
+                const double lnd = -0.5 * v * v - LN_SQRT_2PI + lnB - a * e.lnx - b * e.lny;
+                const double d = exp(lnd);
+                lam[j] = l; d1[j] = d;
+                d2[j] = d * (-v - (a * e.y - b * e.x) * d);
+                if (!ok || !isfinite(l) || !isfinite(d) || !isfinite(d2[j]) || fabs(l) > 1e30 || d > 1e30)
+                    good = false;
+            };
+            const int mid = kTabNodes / 2;
+            node(mid, mu_l);
+            for (int j = mid + 1; j < kTabNodes && good; ++j)
+                node(j, lam[j - 1] + kTabH * d1[j - 1] + 0.5 * kTabH * kTabH * d2[j - 1]);
+            for (int j = mid - 1; j >= 0 && good; --j)
+                node(j, lam[j + 1] - kTabH * d1[j + 1] + 0.5 * kTabH * kTabH * d2[j + 1]);
+            if (good) {
+                for (int j = 0; j < kTabNodes; ++j) tab[j] = make_float2((float)lam[j], (float)d1[j]);
+                tab[kTabNodes] = make_float2(0.0f, 0.0f);
+                for (int j = 0; j + 1 < kTabNodes && good; ++j) {
+                    const double v0 = kTabV0 + kTabH * j;
+                    const double li = quintic_mid64(tab[j].x, tab[j].y, tab[j + 1].x, tab[j + 1].y, v0,
+                                                    (double)r.a, (double)r.b);
+                    bool ok;
+                    const double le = lambda_exact64(v0 + 0.5 * kTabH, a, b, lnB, li, ok);
+                    const double x = 1.0 / (1.0 + exp(-le));
+                    // loss = max_l x: only the relative error of x matters, and
+                    // not at all once x < 1e-7 (fp32 cannot hold lambda ~ -100 to 1e-5)
+                    if (!ok || !isfinite(li) || (x > 1e-7 && (1.0 - x) * fabs(li - le) > 1e-5)) good = false;
+                }
+            }
+            if (!good) {
+                r.mode = kModeExact;
+                if (n_exact) atomicAdd(n_exact, 1u);
+            }
+        }
         out[t] = r;
     }
 }
 
 void launch_prep_records(const ara_record *raw, const uint32_t *src, uint64_t n, BetaRec *out,
-                         float *out_mu, cudaStream_t s) {
+                         float *out_mu, float2 *tables, unsigned int *n_exact, cudaStream_t s) {
     if (n == 0) return;
-    const int threads = 256;
+    const int threads = 128;
     const uint64_t blocks = (n + threads - 1) / threads;
     prep_records_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), threads, 0, s>>>(
-        raw, src, n, out, out_mu);
+        raw, src, n, out, out_mu, tables, n_exact);
 }
 
 // ---------------------------------------------------------------------------
 // The fused YET scan.  One warp owns one trial at a time (dynamic trial
-// scheduler); per 32-occurrence chunk it streams the event ids (coalesced,
-// evict-first), tests the shared-memory presence bitmap, fetches the
-// event-major index entry from L2 for hits, and enqueues every present
-// (occurrence, slot) pair into a warp-private shared-memory queue.  A flush
-// samples all queued pairs with all 32 lanes busy, then reduces per
-// (occurrence, layer) segment, applies the occurrence terms, and adds to
-// the trial's per-layer fp64 sum.  At the end of the trial the aggregate
-// terms give the YLT entry.  All reductions are fixed trees: the YLT is a
-// pure function of the inputs.
+// scheduler).  Per trial:
+//   1. stream the event ids, 128 per warp-load (uint4 per lane, evict-first,
+//      next chunk prefetched), test each against the shared-memory presence
+//      bitmap and compact the hits (k, e) into a warp list;
+//   2. per 64 hits, fetch the event-major index entries (L2-resident) with
+//      all loads in flight, and enqueue every present (occurrence, slot) pair
+//      into the warp's shared-memory queue, whole occurrences at a time;
+//   3. when the queue is full (and at the end of the trial): sample all
+//      queued pairs with all 32 lanes busy (Philox draws, steps 2-4, quantile
+//      table), then reduce each (occurrence, layer) segment, apply the
+//      occurrence terms and add to the trial's per-layer fp64 sum;
+//   4. apply the aggregate terms -> YLT.
+// All reductions are fixed trees / fixed orders: the YLT is a pure function
+// of the inputs (bit-identical across runs and trial shardings).
 // ---------------------------------------------------------------------------
-constexpr int kWarps = 16;          // warps per CTA
-constexpr int kQCap = 256;          // queue capacity (pairs) per warp (>= ARA_MAX_SLOTS)
+constexpr int kWarps = 24;          // warps per CTA (1 CTA per SM)
+constexpr int kQCap = 256;          // pair queue capacity per warp (>= ARA_MAX_SLOTS)
+constexpr int kHCap = 64;           // hit list capacity per warp (flushed at >= 32)
 static_assert(kQCap >= ARA_MAX_SLOTS, "queue must hold one occurrence's pairs");
 
-struct WarpSmem {
+struct WarpBuf {
     uint2 q[kQCap];                 // {device record, (k << 8) | slot}
     float xs[kQCap];                // sampled loss per queued pair
-    double S[ARA_MAX_LAYERS];       // per-layer trial sums
-    unsigned int cnt[ARA_MAX_LAYERS];
-    unsigned long long hsh[ARA_MAX_LAYERS];
+    uint2 hits[kHCap];              // {k, event}
 };
+// followed per warp by: double S[L]; unsigned long long hsh[L]; unsigned cnt[L]
 
 struct ScanArgs {
     PortfolioDev pf;
@@ -109,6 +164,9 @@ struct ScanArgs {
     uint32_t *dbg_count;
     uint64_t *dbg_hash;
     RunStatus *status;
+    const uint32_t *trial_list;     // null: all trials
+    uint64_t n_list;
+    uint32_t *redo;                 // trials to re-run with the fp64 kernel
 };
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
@@ -124,198 +182,308 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
     return v;
 }
 
-template <bool SU>
-__device__ __forceinline__ void flush_queue(const ScanArgs &A, WarpSmem &W, const SlotInfo *slots,
-                                            const LayerInfo *layers, int qn, uint32_t trial_g,
-                                            int lane) {
-    // phase 1: one loss per queued pair, all lanes busy
+// this warp's shared-memory pieces and the block's tables
+struct WarpMem {
+    WarpBuf *B;
+    double *S;
+    unsigned long long *hsh;
+    unsigned int *cnt;
+    const SlotInfo *slots;
+    const LayerInfo *layers;
+};
+
+// what the sampler needs from the launch arguments (passed by value into the
+// out-of-line helpers so they read registers, not the param space)
+struct SampleArgs {
+    const BetaRec *recs;
+    const float2 *tables;
+    const float *rec_mu;
+    const uint32_t *rec_orig;
+    RunStatus *status;
+    uint64_t seed;
+    bool exact;
+    bool dbg;
+};
+
+// Sample every queued pair, reduce the (occurrence, layer) segments, apply the
+// occurrence terms, add to the layer sums.  Out of line: one copy of the
+// sampler in the kernel keeps the instruction working set in the I-cache.
+// Returns 1 if a table-less record was met (the trial must be redone).
+template <bool SU, bool EX>
+__device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uint32_t trial_g, int lane,
+                                        int qn) {
+    WarpBuf &B = *M.B;
+    int redo = 0;
+    // sample: one loss per queued pair, all lanes busy (Alg.1 lines 7-8)
     for (int p = lane; p < qn; p += 32) {
-        const uint2 e = W.q[p];
+        const uint2 e = B.q[p];
         const uint32_t slot = e.y & 0xffu, k = e.y >> 8;
-        const SlotInfo &si = slots[slot];
+        const SlotInfo &si = M.slots[slot];
         float x;
         if (SU) {
-            const BetaRec r = A.pf.recs[e.x];
-            if (r.a <= 0.0f) {
+            const BetaRec r = G.recs[e.x];
+            if (r.mode == kModeDegenerate) {
                 x = r.scale;
+            } else if (!EX && r.mode == kModeExact) {
+                x = 0.0f;                 // table-less record: this trial is redone by the fp64 kernel
+                redo = 1;
             } else {
-                const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, A.seed);   // z_(Prog,E)
-                const uint32_t be = philox_lane0(trial_g, k, si.elt, 2u, A.seed);    // z_(E)
+                const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, G.seed);   // z_(Prog,E)
+                const uint32_t be = philox_lane0(trial_g, k, si.elt, 2u, G.seed);    // z_(E)
                 const float v = combine_v(r, norm_quantile_from_bits(bp), norm_quantile_from_bits(be));
                 bool ok;
-                int steps = 0, iters = 0;
-                x = sample_loss_from_v(r, v, ok, steps, iters);
-                if (!ok) atomicAdd(&A.status->nonconverged, 1u);
+                x = sample_loss_from_v<EX>(r, G.tables, e.x, v, G.exact, ok);
+                if (!ok) atomicAdd(&G.status->nonconverged, 1u);
             }
         } else {
-            x = __ldg(A.pf.rec_mu + e.x);
+            x = __ldg(G.rec_mu + e.x);
         }
-        if (si.has_terms) x = si.share * fminf(fmaxf(x - si.ret, 0.0f), si.lim);     // line 8
-        W.xs[p] = x;
+        if (si.has_terms) x = si.share * fminf(fmaxf(x - si.ret, 0.0f), si.lim);
+        B.xs[p] = x;
     }
     __syncwarp();
-    // phase 2: segments = runs of equal (occurrence, layer); sum (line 9),
-    // occurrence terms (line 11), add to the layer's trial sum
+    // segments = runs of equal (occurrence, layer): sum (line 9), occurrence
+    // terms (line 11), add to the layer's trial sum
     for (int base = 0; base < qn; base += 32) {
         const int p = base + lane;
         bool head = false;
         uint32_t layer = 0;
         double g = 0.0;
         if (p < qn) {
-            const uint2 e = W.q[p];
-            layer = slots[e.y & 0xffu].layer;
-            const uint32_t key = ((e.y >> 8) << 8) | layer;
+            const uint2 e = B.q[p];
+            layer = M.slots[e.y & 0xffu].layer;
+            const uint32_t key = (e.y & 0xffffff00u) | layer;
             if (p == 0) {
                 head = true;
             } else {
-                const uint2 ep = W.q[p - 1];
-                head = (((ep.y >> 8) << 8) | slots[ep.y & 0xffu].layer) != key;
+                const uint2 ep = B.q[p - 1];
+                head = ((ep.y & 0xffffff00u) | M.slots[ep.y & 0xffu].layer) != key;
             }
             if (head) {
                 double l = 0.0;
                 for (int r = p; r < qn; ++r) {
-                    const uint2 er = W.q[r];
-                    if ((((er.y >> 8) << 8) | slots[er.y & 0xffu].layer) != key) break;
-                    l += (double)W.xs[r];
+                    const uint2 er = B.q[r];
+                    if (((er.y & 0xffffff00u) | M.slots[er.y & 0xffu].layer) != key) break;
+                    l += (double)B.xs[r];
                 }
-                const LayerInfo &L = layers[layer];
+                const LayerInfo &L = M.layers[layer];
                 g = fmin(fmax(l - L.occ_r, 0.0), L.occ_l);
             }
         }
         // deterministic per-layer reduction: one fixed-tree warp sum per
-        // distinct layer present among this round's segment heads
+        // distinct layer among this round's segment heads
         unsigned pending = __ballot_sync(0xffffffffu, head);
         while (pending) {
             const int leader = __ffs(pending) - 1;
             const uint32_t lay = __shfl_sync(0xffffffffu, layer, leader);
             const bool mine = head && layer == lay;
-            const double s = warp_sum_f64(mine ? g : 0.0);
-            if (lane == 0) W.S[lay] += s;
+            const double sum = warp_sum_f64(mine ? g : 0.0);
+            if (lane == 0) M.S[lay] += sum;
             pending &= ~__ballot_sync(0xffffffffu, mine);
         }
     }
     __syncwarp();
+    return __any_sync(0xffffffffu, redo) ? 1 : 0;
 }
 
-template <bool SU, int MW>
+// enqueue the pairs of one occurrence per lane (whole occurrences only);
+// returns the new queue length
+template <bool SU, bool EX, int MW>
+__device__ __forceinline__ int enqueue(const SampleArgs &G, const WarpMem &M, uint32_t trial_g, int lane,
+                                       int qn, bool todo, uint32_t k, uint32_t first,
+                                       const uint32_t (&mask)[MW], int &redo) {
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < MW; ++i) cnt += __popc(mask[i]);
+    todo = todo && cnt > 0;
+    while (__any_sync(0xffffffffu, todo)) {
+        uint32_t incl = todo ? cnt : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const bool fits = todo && incl <= (uint32_t)(kQCap - qn);
+        if (fits) {
+            uint32_t pos = (uint32_t)qn + incl - cnt;
+            uint32_t rec = first;
+#pragma unroll
+            for (int i = 0; i < MW; ++i) {
+                uint32_t mw = mask[i];
+                while (mw) {
+                    const uint32_t slot = (uint32_t)(i * 32 + __ffs(mw) - 1);
+                    mw &= mw - 1;
+                    M.B->q[pos++] = make_uint2(rec, (k << 8) | slot);
+                    if (G.dbg) {
+                        const uint32_t lay = M.slots[slot].layer;
+                        atomicAdd(&M.cnt[lay], 1u);
+                        const uint64_t h = splitmix64(splitmix64(splitmix64((uint64_t)k) ^ M.slots[slot].elt) ^
+                                                      G.rec_orig[rec]);
+                        atomicAdd(&M.hsh[lay], (unsigned long long)h);
+                    }
+                    ++rec;
+                }
+            }
+            todo = false;
+        }
+        const unsigned fitmask = __ballot_sync(0xffffffffu, fits);
+        if (fitmask) qn += (int)__shfl_sync(0xffffffffu, incl, 31 - __clz(fitmask));
+        __syncwarp();
+        if (__any_sync(0xffffffffu, todo)) {
+            redo |= flush_queue<SU, EX>(G, M, trial_g, lane, qn);
+            qn = 0;
+        }
+    }
+    return qn;
+}
+
+template <int MW>
+__device__ __forceinline__ void load_index(const uint32_t *index, uint32_t stride, uint32_t e,
+                                           uint32_t &first, uint32_t (&mask)[MW]) {
+    const uint32_t *ix = index + (uint64_t)e * stride;
+    if (MW == 1) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(ix));
+        first = v.x; mask[0] = v.y;
+    } else {
+        const uint4 v0 = __ldg(reinterpret_cast<const uint4 *>(ix));
+        first = v0.x; mask[0] = v0.y;
+        if (MW > 1) mask[1] = v0.z;
+        if (MW > 2) mask[2] = v0.w;
+        if (MW > 3) {
+            const uint4 v1 = __ldg(reinterpret_cast<const uint4 *>(ix) + 1);
+            mask[3] = v1.x;
+            if (MW > 4) mask[4] = v1.y;
+            if (MW > 5) mask[5] = v1.z;
+            if (MW > 6) mask[6] = v1.w;
+        }
+    }
+}
+
+// index lookups for the warp's hit list (two per lane in flight), then
+// enqueue.  Out of line (called from several places).  Returns the new queue
+// length, | 0x10000 if a table-less record was met.
+template <bool SU, bool EX, int MW>
+__device__ __noinline__ int process_hits(const SampleArgs G, const WarpMem M, const uint32_t *index,
+                                         uint32_t stride, uint32_t trial_g, int lane, int nh, int qn) {
+    const bool h0 = lane < nh, h1 = lane + 32 < nh;
+    const uint2 a0 = h0 ? M.B->hits[lane] : make_uint2(0, 0);
+    const uint2 a1 = h1 ? M.B->hits[lane + 32] : make_uint2(0, 0);
+    uint32_t f0 = 0, f1 = 0, m0[MW], m1[MW];
+#pragma unroll
+    for (int i = 0; i < MW; ++i) { m0[i] = 0u; m1[i] = 0u; }
+    if (h0) load_index<MW>(index, stride, a0.y, f0, m0);                  // Alg.1 line 6
+    if (h1) load_index<MW>(index, stride, a1.y, f1, m1);
+    __syncwarp();
+    int redo = 0;
+    qn = enqueue<SU, EX, MW>(G, M, trial_g, lane, qn, h0, a0.x, f0, m0, redo);
+    qn = enqueue<SU, EX, MW>(G, M, trial_g, lane, qn, h1, a1.x, f1, m1, redo);
+    return qn | (redo << 16);
+}
+
+template <bool SU, bool EX, int MW>
 __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_constant__ ScanArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpSmem *wsm = reinterpret_cast<WarpSmem *>(smem_raw);
-    SlotInfo *slots = reinterpret_cast<SlotInfo *>(wsm + kWarps);
+    const uint32_t nl = A.pf.n_layers;
+    const size_t per_warp = sizeof(WarpBuf) + nl * (sizeof(double) + sizeof(unsigned long long) +
+                                                    sizeof(unsigned int));
+    const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
+    SlotInfo *slots = reinterpret_cast<SlotInfo *>(smem_raw);
     LayerInfo *layers = reinterpret_cast<LayerInfo *>(slots + ARA_MAX_SLOTS);
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(layers + ARA_MAX_LAYERS);
+    unsigned char *warp_base = reinterpret_cast<unsigned char *>(bitmap) +
+                               ((size_t)A.pf.bitmap_words * 4 + 15) / 16 * 16;
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t t = threadIdx.x; t < A.pf.bitmap_words; t += blockDim.x) bitmap[t] = A.pf.bitmap[t];
     for (uint32_t t = threadIdx.x; t < A.pf.n_slots; t += blockDim.x) slots[t] = A.pf.slots[t];
-    for (uint32_t t = threadIdx.x; t < A.pf.n_layers; t += blockDim.x) layers[t] = A.pf.layers[t];
+    for (uint32_t t = threadIdx.x; t < nl; t += blockDim.x) layers[t] = A.pf.layers[t];
     __syncthreads();
 
-    WarpSmem &W = wsm[warp];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpMem M;
+    unsigned char *mine = warp_base + per_warp_al * warp;
+    M.B = reinterpret_cast<WarpBuf *>(mine);
+    M.S = reinterpret_cast<double *>(mine + sizeof(WarpBuf));
+    M.hsh = reinterpret_cast<unsigned long long *>(M.S + nl);
+    M.cnt = reinterpret_cast<unsigned int *>(M.hsh + nl);
+    M.slots = slots;
+    M.layers = layers;
     const bool dbg = (A.flags & ARA_DEBUG_LOOKUP) != 0;
-    const uint32_t nl = A.pf.n_layers;
+    const SampleArgs G{A.pf.recs, A.pf.tables, A.pf.rec_mu, A.pf.rec_orig, A.status, A.seed,
+                       (A.flags & ARA_EXACT) != 0, dbg};
     const uint64_t n_trials = A.yet.n_trials;
+    const uint64_t n_work = A.trial_list ? A.n_list : n_trials;
+    const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift;
+    const uint32_t *index = A.pf.index;
+    const uint32_t stride = A.pf.idx_stride;
 
     while (true) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(&A.status->next_trial, 1ull);
         t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= n_trials) break;
+        if (t >= n_work) break;
+        if (A.trial_list) t = A.trial_list[t];
         const uint64_t base = A.yet.fixed_len ? t * (uint64_t)A.yet.fixed_len : A.yet.offsets[t];
-        const uint32_t len = A.yet.fixed_len ? A.yet.fixed_len
-                                             : (uint32_t)(A.yet.offsets[t + 1] - base);
-        const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);   // global index i
-        for (uint32_t l = lane; l < nl; l += 32) { W.S[l] = 0.0; W.cnt[l] = 0u; W.hsh[l] = 0ull; }
+        const uint32_t len = A.yet.fixed_len ? A.yet.fixed_len : (uint32_t)(A.yet.offsets[t + 1] - base);
+        const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);        // global trial index i
+        for (uint32_t l = lane; l < nl; l += 32) { M.S[l] = 0.0; M.cnt[l] = 0u; M.hsh[l] = 0ull; }
         __syncwarp();
-        int qn = 0;
-        for (uint32_t c = 0; c < len; c += 32) {
-            const uint32_t k = c + lane;
-            uint32_t mask[MW];
+        int qn = 0, nh = 0, redo = 0;
+        const uint32_t *ev = A.yet.events + base;
+        const bool vec = (base & 3u) == 0;
+        auto load4 = [&](uint32_t c) -> uint4 {                     // events c+4*lane .. +3
+            const uint32_t k = c + 4u * lane;
+            if (vec && k + 3 < len) return __ldcs(reinterpret_cast<const uint4 *>(ev + k));
+            uint4 r = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+            if (k < len) r.x = __ldcs(ev + k);
+            if (k + 1 < len) r.y = __ldcs(ev + k + 1);
+            if (k + 2 < len) r.z = __ldcs(ev + k + 2);
+            if (k + 3 < len) r.w = __ldcs(ev + k + 3);
+            return r;
+        };
+        uint4 cur = len ? load4(0) : make_uint4(0, 0, 0, 0);
+        for (uint32_t c = 0; c < len; c += 128) {                   // Alg.1 line 4
+            const uint4 nxt = (c + 128 < len) ? load4(c + 128) : make_uint4(0, 0, 0, 0);
+            const uint32_t e4[4] = {cur.x, cur.y, cur.z, cur.w};
 #pragma unroll
-            for (int w = 0; w < MW; ++w) mask[w] = 0u;
-            uint32_t first = 0, cnt = 0;
-            if (k < len) {
-                const uint32_t e = __ldcs(A.yet.events + base + k);                  // line 4
-                if (e >= A.pf.catalog) {
-                    atomicAdd(&A.status->bad_event, 1u);
-                } else {
-                    const uint32_t bit = e >> A.pf.bitmap_shift;
-                    if ((bitmap[bit >> 5] >> (bit & 31)) & 1u) {                      // line 6
-                        const uint32_t *ix = A.pf.index + (uint64_t)e * A.pf.idx_stride;
-                        if (MW == 1) {
-                            const uint2 v = __ldg(reinterpret_cast<const uint2 *>(ix));
-                            first = v.x; mask[0] = v.y;
-                        } else {
-                            const uint4 v0 = __ldg(reinterpret_cast<const uint4 *>(ix));
-                            first = v0.x; mask[0] = v0.y;
-                            if (MW > 1) mask[1] = v0.z;
-                            if (MW > 2) mask[2] = v0.w;
-                            if (MW > 3) {
-                                const uint4 v1 = __ldg(reinterpret_cast<const uint4 *>(ix) + 1);
-                                mask[3] = v1.x;
-                                if (MW > 4) mask[4] = v1.y;
-                                if (MW > 5) mask[5] = v1.z;
-                                if (MW > 6) mask[6] = v1.w;
-                            }
-                        }
-#pragma unroll
-                        for (int w = 0; w < MW; ++w) cnt += __popc(mask[w]);
+            for (int qd = 0; qd < 4; ++qd) {
+                const uint32_t k = c + 4u * lane + qd;
+                const uint32_t e = e4[qd];
+                bool hit = false;
+                if (k < len) {
+                    if (e >= C) {
+                        atomicAdd(&A.status->bad_event, 1u);
+                    } else {
+                        const uint32_t bit = e >> shift;
+                        hit = (bitmap[bit >> 5] >> (bit & 31)) & 1u;
                     }
                 }
-            }
-            // enqueue whole occurrences, flushing when the queue would overflow
-            bool todo = cnt > 0;
-            while (__any_sync(0xffffffffu, todo)) {
-                uint32_t incl = todo ? cnt : 0u;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                const uint32_t room = (uint32_t)(kQCap - qn);
-                const bool fits = todo && incl <= room;
-                if (fits) {
-                    uint32_t pos = (uint32_t)qn + incl - cnt;
-                    uint32_t rec = first;
-#pragma unroll
-                    for (int w = 0; w < MW; ++w) {
-                        uint32_t mw = mask[w];
-                        while (mw) {
-                            const int bpos = __ffs(mw) - 1;
-                            mw &= mw - 1;
-                            const uint32_t slot = (uint32_t)(w * 32 + bpos);
-                            W.q[pos++] = make_uint2(rec++, (k << 8) | slot);
-                            if (dbg) {
-                                const uint32_t lay = slots[slot].layer;
-                                atomicAdd(&W.cnt[lay], 1u);
-                                const uint64_t h = splitmix64(
-                                    splitmix64(splitmix64((uint64_t)k) ^ slots[slot].elt) ^
-                                    A.pf.rec_orig[rec - 1]);
-                                atomicAdd(&W.hsh[lay], (unsigned long long)h);
-                            }
-                        }
-                    }
-                    todo = false;
-                }
-                const uint32_t added = __shfl_sync(0xffffffffu, fits ? incl : 0u, 31 - __clz(__ballot_sync(0xffffffffu, fits) | 1u));
-                const unsigned fitmask = __ballot_sync(0xffffffffu, fits);
-                qn += fitmask ? (int)added : 0;
-                __syncwarp();
-                if (__any_sync(0xffffffffu, todo)) {
-                    flush_queue<SU>(A, W, slots, layers, qn, trial_g, lane);
-                    qn = 0;
+                const unsigned hm = __ballot_sync(0xffffffffu, hit);
+                if (hit) M.B->hits[nh + __popc(hm & ((1u << lane) - 1u))] = make_uint2(k, e);
+                nh += __popc(hm);
+                if (nh >= 32) {                      // <= 63 queued: two index loads per lane
+                    __syncwarp();
+                    const int r = process_hits<SU, EX, MW>(G, M, index, stride, trial_g, lane, nh, qn);
+                    qn = r & 0xffff; redo |= r >> 16; nh = 0;
                 }
             }
+            cur = nxt;
         }
-        if (qn > 0) flush_queue<SU>(A, W, slots, layers, qn, trial_g, lane);
+        __syncwarp();
+        if (nh) {
+            const int r = process_hits<SU, EX, MW>(G, M, index, stride, trial_g, lane, nh, qn);
+            qn = r & 0xffff; redo |= r >> 16;
+        }
+        if (qn) redo |= flush_queue<SU, EX>(G, M, trial_g, lane, qn);
+        if (!EX && redo) {
+            if (lane == 0) A.redo[atomicAdd(&A.status->n_redo, 1u)] = (uint32_t)t;
+        }
         // aggregate terms on the trial sum (line 12, G6) -> YLT (line 17)
         for (uint32_t l = lane; l < nl; l += 32) {
             const LayerInfo &L = layers[l];
-            const double S = W.S[l];
-            A.ylt[(uint64_t)l * n_trials + t] = (float)fmin(fmax(S - L.agg_r, 0.0), L.agg_l);
+            A.ylt[(uint64_t)l * n_trials + t] = (float)fmin(fmax(M.S[l] - L.agg_r, 0.0), L.agg_l);
             if (dbg) {
-                if (A.dbg_count) A.dbg_count[(uint64_t)l * n_trials + t] = W.cnt[l];
-                if (A.dbg_hash) A.dbg_hash[(uint64_t)l * n_trials + t] = W.hsh[l];
+                if (A.dbg_count) A.dbg_count[(uint64_t)l * n_trials + t] = M.cnt[l];
+                if (A.dbg_hash) A.dbg_hash[(uint64_t)l * n_trials + t] = M.hsh[l];
             }
         }
         __syncwarp();
@@ -323,62 +491,69 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
 }
 
 static size_t scan_smem_bytes(const PortfolioDev &pf) {
-    return sizeof(WarpSmem) * kWarps + sizeof(SlotInfo) * ARA_MAX_SLOTS +
-           sizeof(LayerInfo) * ARA_MAX_LAYERS + sizeof(uint32_t) * (size_t)pf.bitmap_words;
+    const size_t per_warp = sizeof(WarpBuf) + pf.n_layers * (sizeof(double) + sizeof(unsigned long long) +
+                                                             sizeof(unsigned int));
+    return sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
+           ((size_t)pf.bitmap_words * 4 + 15) / 16 * 16 + kWarps * ((per_warp + 15) & ~size_t(15));
 }
 
-template <bool SU, int MW>
+template <bool SU, bool EX, int MW>
 static cudaError_t launch_scan_t(const ScanArgs &A, cudaStream_t s, int num_sms) {
     const size_t smem = scan_smem_bytes(A.pf);
-    cudaError_t err = cudaFuncSetAttribute(scan_kernel<SU, MW>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = scan_kernel<SU, EX, MW>;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     int per_sm = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_kernel<SU, MW>, kWarps * 32, smem);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    scan_kernel<SU, MW><<<num_sms * per_sm, kWarps * 32, smem, s>>>(A);
+    kern<<<num_sms * per_sm, kWarps * 32, smem, s>>>(A);
     return cudaGetLastError();
+}
+
+template <int MW>
+static cudaError_t launch_scan_mw(const ScanArgs &A, bool exact_kernel, cudaStream_t s, int num_sms) {
+    if (!(A.flags & ARA_SU)) return launch_scan_t<false, false, MW>(A, s, num_sms);
+    // the fp64 per-sample solve lives in a separate kernel (its register demand
+    // would otherwise throttle the table path)
+    if (exact_kernel) return launch_scan_t<true, true, MW>(A, s, num_sms);
+    return launch_scan_t<true, false, MW>(A, s, num_sms);
 }
 
 cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed, uint32_t flags,
                         float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
+                        const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
                         cudaStream_t s, int num_sms) {
-    ScanArgs A{pf, yet, seed, flags, ylt, dbg_count, dbg_hash, status};
-    const bool su = (flags & ARA_SU) != 0;
-    if (pf.mask_words == 1) return su ? launch_scan_t<true, 1>(A, s, num_sms) : launch_scan_t<false, 1>(A, s, num_sms);
-    if (pf.mask_words <= 3) return su ? launch_scan_t<true, 3>(A, s, num_sms) : launch_scan_t<false, 3>(A, s, num_sms);
-    return su ? launch_scan_t<true, 7>(A, s, num_sms) : launch_scan_t<false, 7>(A, s, num_sms);
+    ScanArgs A{pf, yet, seed, flags, ylt, dbg_count, dbg_hash, status, trial_list, n_list, redo};
+    if (trial_list && n_list == 0) return cudaSuccess;
+    if (pf.mask_words == 1) return launch_scan_mw<1>(A, exact_kernel, s, num_sms);
+    if (pf.mask_words <= 3) return launch_scan_mw<3>(A, exact_kernel, s, num_sms);
+    return launch_scan_mw<7>(A, exact_kernel, s, num_sms);
 }
 
 // ---------------------------------------------------------------------------
 // Component kernels (row-level parity tests)
 // ---------------------------------------------------------------------------
-__global__ void sample_losses_kernel(const BetaRec *recs, const float *zp, const float *ze,
-                                     uint64_t n, float *out, RunStatus *status) {
+__global__ void sample_losses_kernel(const BetaRec *recs, const float2 *tables, const float *zp,
+                                     const float *ze, uint64_t n, bool exact, float *out,
+                                     RunStatus *status) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const BetaRec r = recs[t];
-        if (r.a <= 0.0f) { out[t] = r.scale; continue; }
-        // z given as fp32 in (0,1): Phi^-1 on the smaller tail
-        const float a = zp[t], b = ze[t];
-        const float vp = (a < 0.5f) ? -1.41421356237f * erfcinvf(2.0f * a)
-                                    : 1.41421356237f * erfcinvf(2.0f * (1.0f - a));
-        const float ve = (b < 0.5f) ? -1.41421356237f * erfcinvf(2.0f * b)
-                                    : 1.41421356237f * erfcinvf(2.0f * (1.0f - b));
+        const float v = combine_v(r, norm_quantile_f(zp[t]), norm_quantile_f(ze[t]));
         bool ok;
-        int steps = 0, iters = 0;
-        out[t] = sample_loss_from_v(r, combine_v(r, vp, ve), ok, steps, iters);
+        out[t] = sample_loss_from_v<true>(r, tables, t, v, exact, ok);
         if (!ok) atomicAdd(&status->nonconverged, 1u);
     }
 }
 
-cudaError_t launch_sample_losses(const BetaRec *recs, const float *zp, const float *ze, uint64_t n,
-                                 float *out, RunStatus *status, cudaStream_t s) {
+cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float *zp,
+                                 const float *ze, uint64_t n, bool exact, float *out,
+                                 RunStatus *status, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const uint64_t blocks = (n + 255) / 256;
     sample_losses_kernel<<<(unsigned)(blocks < 1u << 20 ? blocks : 1u << 20), 256, 0, s>>>(
-        recs, zp, ze, n, out, status);
+        recs, tables, zp, ze, n, exact, out, status);
     return cudaGetLastError();
 }
 
@@ -395,30 +570,6 @@ cudaError_t launch_draw_uniforms(uint64_t seed, const uint4 *ctr, uint64_t n, fl
     if (n == 0) return cudaSuccess;
     const uint64_t blocks = (n + 255) / 256;
     draw_uniforms_kernel<<<(unsigned)(blocks < 1u << 20 ? blocks : 1u << 20), 256, 0, s>>>(seed, ctr, n, out);
-    return cudaGetLastError();
-}
-
-__global__ void max_event_kernel(const uint32_t *ev, uint64_t n, uint32_t *out) {
-    uint32_t m = 0;
-    const uint64_t n4 = n / 4;
-    const uint4 *ev4 = reinterpret_cast<const uint4 *>(ev);
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n4;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint4 v = __ldcs(ev4 + t);
-        m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
-    }
-    for (uint64_t t = n4 * 4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
-         t += (uint64_t)gridDim.x * blockDim.x)
-        m = max(m, ev[t]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
-}
-
-cudaError_t launch_max_event(const uint32_t *ev, uint64_t n, uint32_t *out, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(uint32_t), s);
-    if (e != cudaSuccess || n == 0) return e;
-    max_event_kernel<<<148 * 4, 256, 0, s>>>(ev, n, out);
     return cudaGetLastError();
 }
 

@@ -1,19 +1,28 @@
 // ara_sampler.cuh -- device functions of the secondary-uncertainty sampler
-// (section 3 of arXiv 1310.2274), fp32 on sm_100a.
+// (section 3 of arXiv 1310.2274) on sm_100a.
 //
 //   draws    : Philox4x32-10 keyed by the run seed; z_(Prog,E) from counter
 //              (i, k, program, 1), z_(E) from (i, k, XELT, 2) (readings G2,
 //              G4); U(x) = (2(x>>9)+1) 2^-24, exact in fp32.
-//   steps 2-4: v = wi * Phi^-1(z_P) + wc * Phi^-1(z_E) (G1)
-//   step 5   : the smaller tail t = Phi(-|v|) and its side (G13)
-//   quantile : x with I_x(a,b) = t (v <= 0) or 1 - I_x(a,b) = t (v > 0)
-//              (G11), solved by Halley iteration on
-//              ln(tail) as a function of lambda = logit(x), so that both x
-//              and 1-x keep full relative precision and both tails are
-//              near-linear.  The tail is evaluated from the continued
-//              fraction of DLMF 8.17.22 with the division-free forward
-//              (Wallis) recurrence and exact power-of-two rescaling.
+//   steps 2-4: v = wi * Phi^-1(z_P) + wc * Phi^-1(z_E) (G1);
+//              fp32, Phi^-1 taken on the smaller tail (exact for U's grid)
+//   steps 5+ : x = I^-1(Phi(v); a, b) (G11).  The map
+//              v -> lambda(v) = logit x(v) is smooth, so each record carries
+//              a table of (lambda, dlambda/dv) at v = -8, -7.5, ..., 8, built
+//              ONCE at ara_create_portfolio by an fp64 solve (below) and
+//              evaluated per sample by quintic Hermite interpolation, the
+//              second derivative coming from the ODE
+//                  dlambda/dv = phi(v) B(a,b) / (x^a (1-x)^b),
+//                  d2lambda/dv2 = lambda' (-v - (a(1-x) - b x) lambda').
+//              Records whose table misses a midpoint check fall back to the
+//              fp64 per-sample solve (mode kModeExact), as does ARA_EXACT.
 //   loss     : max_l * x
+//
+// The fp64 solver: Halley iteration on ln(tail) as a function of lambda, so
+// x and 1-x keep full relative precision and both tails are near-linear;
+// the tail from the continued fraction of DLMF 8.17.22 (modified Lentz),
+// on whichever of I_x(a,b) / I_{1-x}(b,a) converges fast; the smaller tail
+// t = Phi(-|v|) is matched directly (reading G13).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -22,6 +31,7 @@
 
 namespace ara {
 
+// ---------------------------------------------------------------- draws ---
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
@@ -34,7 +44,6 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
     return c;
 }
 
-// lane 0 of Philox for one counter
 __device__ __forceinline__ uint32_t philox_lane0(uint32_t i, uint32_t k, uint32_t id, uint32_t tag,
                                                  uint64_t seed) {
     return philox4x32_10(make_uint4(i, k, id, tag), (uint32_t)seed, (uint32_t)(seed >> 32)).x;
@@ -44,8 +53,7 @@ __device__ __forceinline__ float u01_from_bits(uint32_t x) {
     return (float)(2u * (x >> 9) + 1u) * 5.9604644775390625e-08f;
 }
 
-// Phi^-1(U(x)) computed on the smaller tail, which is exact for U's grid:
-// z = (2m+1) 2^-24; min(z, 1-z) = (2m+1) or (2^24-2m-1) times 2^-24.
+// Phi^-1(U(x)) on the smaller tail: z = (2m+1) 2^-24 and min(z, 1-z) are exact.
 __device__ __forceinline__ float norm_quantile_from_bits(uint32_t x) {
     const uint32_t m = x >> 9;
     const bool low = m < (1u << 22);
@@ -55,136 +63,174 @@ __device__ __forceinline__ float norm_quantile_from_bits(uint32_t x) {
     return low ? -r : r;
 }
 
-__device__ __forceinline__ float softplusf(float z) {
-    // log(1 + e^z); absolute accuracy suffices where it is used
-    return fmaxf(z, 0.0f) + __logf(1.0f + __expf(-fabsf(z)));
-}
-
-// 1 / (1 + d1/(1 + d2/(1 + ...))) of DLMF 8.17.22 for I_x(a,b), forward
-// recurrence on the equivalent fraction b_n = q_n, a_n = q_{n-1} p_n where
-// d_n = p_n / q_n; converged when consecutive convergents agree to 2e-7.
-__device__ __forceinline__ float betacf_recip(float x, float a, float b, int &steps) {
-    float Am = 1.0f, Bm = 0.0f;   // A_{n-2}, B_{n-2}
-    float A = 1.0f, B = 1.0f;     // A_{n-1}, B_{n-1}
-    float qprev = 1.0f;
-    const float apb = a + b;
-    int n = 1;
-    for (; n < 600; n += 2) {
-        const float m = (float)(n >> 1);
-        // odd step n = 2m+1
-        float u = fmaf(2.0f, m, a);
-        float q = u * (u + 1.0f);
-        float p = -(a + m) * (apb + m) * x;
-        float c = qprev * p;
-        float An = fmaf(q, A, c * Am), Bn = fmaf(q, B, c * Bm);
-        Am = A; Bm = B; A = An; B = Bn; qprev = q;
-        // even step n+1 = 2(m+1)
-        const float m1 = m + 1.0f;
-        u = fmaf(2.0f, m1, a);
-        q = (u - 1.0f) * u;
-        p = m1 * (b - m1) * x;
-        c = qprev * p;
-        An = fmaf(q, A, c * Am); Bn = fmaf(q, B, c * Bm);
-        Am = A; Bm = B; A = An; B = Bn; qprev = q;
-        // exact power-of-two rescale by A's exponent
-        const int e = min(max((__float_as_int(A) >> 23) & 0xff, 1), 253);
-        const float s = __int_as_float((254 - e) << 23);
-        A *= s; B *= s; Am *= s; Bm *= s;
-        // |h_n - h_{n-1}| <= eps |h_n|  <=>  |A B_{n-1} - A_{n-1} B| <= eps |A B_{n-1}|
-        const float t1 = A * Bm;
-        const float diff = fmaf(Am, B, -t1);
-        if (fabsf(diff) <= 2e-7f * fabsf(t1)) break;
-    }
-    steps += n + 1;
-    return B / A;
-}
-
-struct TailEval {
-    float lnT;    // log of the matched tail probability at lambda
-    float hp;     // d lnT / d lambda
-    float dphi;   // d phi / d lambda = a(1-x) - b x
-};
-
-// Evaluate ln(tail) at lambda = logit(x) (see file header).
-__device__ __forceinline__ TailEval tail_at(float lam, bool lower, float a, float b, float m,
-                                            float lnm, float ln1m, float c0, int &steps) {
-    const float ex = __expf(-lam);
-    const float x = __frcp_rn(1.0f + ex);                 // x = sigmoid(lam)
-    const float y = __frcp_rn(1.0f + __frcp_rn(ex));      // 1 - x, full relative precision
-    const float lnx = -softplusf(-lam), lny = -softplusf(lam);
-    const float d = x - m;
-    // ln(x/m) and ln((1-x)/(1-m)); log1p near the centre keeps the large
-    // a ln x + b ln(1-x) - ln B cancellation out of fp32
-    const float t1 = (fabsf(d) < 0.5f * m) ? log1pf(__fdividef(d, m)) : lnx - lnm;
-    const float t2 = (fabsf(d) < 0.5f * (1.0f - m)) ? log1pf(__fdividef(-d, 1.0f - m)) : lny - ln1m;
-    const float phi = fmaf(a, t1, fmaf(b, t2, c0));      // ln(x^a (1-x)^b / B(a,b))
-    const bool direct = x < __fdividef(a + 1.0f, a + b + 2.0f);
-    const float xa = direct ? x : y, aa = direct ? a : b, bb = direct ? b : a;
-    const float cf = betacf_recip(xa, aa, bb, steps);
-    const float lnG = phi + __logf(__fdividef(cf, aa));  // ln of the directly computed tail
-    const float G = __expf(lnG);
-    const float lnOther = log1pf(-fminf(G, 1.0f));
-    const float lnP = direct ? lnG : lnOther;
-    const float lnQ = direct ? lnOther : lnG;
-    TailEval r;
-    r.lnT = lower ? lnP : lnQ;
-    const float h = __expf(phi - r.lnT);
-    r.hp = lower ? h : -h;
-    r.dphi = fmaf(a, y, -b * x);
-    return r;
-}
-
-// Solve for x = I^-1 on the given tail; returns x, sets *ok.
-__device__ __forceinline__ float beta_quantile_tail(float t, bool lower, float v, const BetaRec &r,
-                                                    bool &ok, int &steps, int &iters) {
-    const float a = r.a, b = r.b;
-    const float m = __fdiv_rn(a, a + b);
-    const float lnm = logf(m), ln1m = log1pf(-m);
-    const float lnt = logf(t);
-    // initial guess: logit(X) ~ N(psi(a)-psi(b), psi1(a)+psi1(b)), bounded
-    // by the tail asymptotes x^a/(a B) = t (lower) / (1-x)^b/(b B) = t (upper)
-    float lam = fmaf(v, r.sd_l, r.mu_l);
-    const float lnB = fmaf(a, lnm, fmaf(b, ln1m, -r.c0));
-    if (lower && b >= 1.0f) lam = fmaxf(lam, __fdividef(lnt + __logf(a) + lnB, a));
-    if (!lower && a >= 1.0f) lam = fminf(lam, -__fdividef(lnt + __logf(b) + lnB, b));
-    float lo = -INFINITY, hi = INFINITY;
-    ok = false;
-    int it = 0;
-    for (; it < 64; ++it) {
-        const TailEval e = tail_at(lam, lower, a, b, m, lnm, ln1m, r.c0, steps);
-        const float g = e.lnT - lnt;
-        const bool toolow = lower ? (g < 0.0f) : (g > 0.0f);
-        if (toolow) lo = lam; else hi = lam;
-        const float hpp = e.hp * (e.dphi - e.hp);
-        const float step = __fdividef(2.0f * g * e.hp, fmaf(2.0f * e.hp, e.hp, -g * hpp));
-        float nl = lam - step;
-        const float scale = fmaxf(1.0f, fabsf(lam));
-        const bool small = fabsf(step) <= 2e-6f * scale;
-        if (!(nl > lo && nl < hi) && !small) {
-            if (isfinite(lo) && isfinite(hi)) nl = 0.5f * (lo + hi);
-            else if (isfinite(lo)) nl = lo + 2.0f;
-            else nl = hi - 2.0f;
-        }
-        const bool conv = fabsf(nl - lam) <= 1e-3f * scale;
-        lam = nl;
-        if (conv) { ok = true; ++it; break; }
-    }
-    iters += it;
-    return __frcp_rn(1.0f + __expf(-lam));
-}
-
-// One loss draw (Alg.1 line 7) for record r and the two uniforms' bits.
-__device__ __forceinline__ float sample_loss_from_v(const BetaRec &r, float v, bool &ok,
-                                                    int &steps, int &iters) {
-    if (r.a <= 0.0f) { ok = true; return r.scale; }       // degenerate (G10)
-    const float t = 0.5f * erfcf(fabsf(v) * 0.70710678118654752f);
-    const bool lower = v <= 0.0f;
-    const float x = beta_quantile_tail(t, lower, v, r, ok, steps, iters);
-    return r.scale * x;
+// Phi^-1 of an arbitrary fp32 probability in (0,1) (component entry point)
+__device__ __forceinline__ float norm_quantile_f(float z) {
+    return (z < 0.5f) ? -1.41421356237f * erfcinvf(2.0f * z) : 1.41421356237f * erfcinvf(2.0f * (1.0f - z));
 }
 
 __device__ __forceinline__ float combine_v(const BetaRec &r, float vp, float ve) {
     return fmaf(r.wi, vp, r.wc * ve);                     // steps 3-4
+}
+
+// -------------------------------------------------------- fp64 solver ----
+__device__ __forceinline__ double betacf64(double x, double a, double b) {
+    // returns 1/(1 + d1/(1 + d2/(1 + ...))) (DLMF 8.17.22), modified Lentz
+    const double tiny = 1e-300;
+    double f = 1.0, C = 1.0, D = 0.0;
+    for (int n = 1; n < 20000; ++n) {
+        const double m = (double)(n >> 1);
+        const double d = (n & 1) ? -((a + m) * (a + b + m) * x) / ((a + 2.0 * m) * (a + 2.0 * m + 1.0))
+                                 : (m * (b - m) * x) / ((a + 2.0 * m - 1.0) * (a + 2.0 * m));
+        D = 1.0 + d * D;
+        if (fabs(D) < tiny) D = tiny;
+        C = 1.0 + d / C;
+        if (fabs(C) < tiny) C = tiny;
+        D = 1.0 / D;
+        const double delta = C * D;
+        f *= delta;
+        if (fabs(delta - 1.0) < 1e-15) break;
+    }
+    return 1.0 / f;
+}
+
+struct Tail64 {
+    double lnT, hp, dphi, x, y, lnx, lny;
+};
+
+// ln of the matched tail (P = I_x(a,b) if lower, else Q = 1 - P) at lambda = logit x
+__device__ __forceinline__ Tail64 tail64(double lam, bool lower, double a, double b, double lnB) {
+    Tail64 r;
+    const double e = exp(-fabs(lam));
+    const double sp = log1p(e);                            // softplus(-|lam|)
+    const double lnx = lam >= 0.0 ? -sp : lam - sp;
+    const double lny = lam >= 0.0 ? -lam - sp : -sp;
+    const double x = exp(lnx), y = exp(lny);
+    const double phi = a * lnx + b * lny - lnB;            // ln(x^a y^b / B)
+    const bool direct = x < (a + 1.0) / (a + b + 2.0);
+    const double cf = direct ? betacf64(x, a, b) : betacf64(y, b, a);
+    const double lnG = phi + log(cf / (direct ? a : b));
+    const double G = exp(lnG);
+    const double lnOther = log1p(-fmin(G, 1.0));
+    r.lnT = lower ? (direct ? lnG : lnOther) : (direct ? lnOther : lnG);
+    const double h = exp(phi - r.lnT);
+    r.hp = lower ? h : -h;
+    r.dphi = a * y - b * x;
+    r.x = x; r.y = y; r.lnx = lnx; r.lny = lny;
+    return r;
+}
+
+// lambda = logit(x) with tail(x) = exp(lnt) (lower: I_x(a,b); upper: 1 - I_x(a,b)).
+__device__ __forceinline__ double solve_logit64(double lnt, bool lower, double a, double b,
+                                                double lnB, double lam, bool &ok) {
+    double lo = -INFINITY, hi = INFINITY;
+    ok = false;
+    for (int it = 0; it < 300; ++it) {
+        const Tail64 e = tail64(lam, lower, a, b, lnB);
+        const double g = e.lnT - lnt;
+        if (g == 0.0) { ok = true; break; }
+        const bool toolow = lower ? (g < 0.0) : (g > 0.0);
+        if (toolow) lo = lam; else hi = lam;
+        const double hpp = e.hp * (e.dphi - e.hp);
+        double nl = lam - 2.0 * g * e.hp / (2.0 * e.hp * e.hp - g * hpp);
+        const double scale = fmax(1.0, fabs(lam));
+        if (!(nl > lo && nl < hi)) {
+            if (isfinite(lo) && isfinite(hi)) nl = 0.5 * (lo + hi);
+            else if (isfinite(lo)) nl = lo + fmax(2.0, fabs(lo));      // expand geometrically
+            else nl = hi - fmax(2.0, fabs(hi));
+        }
+        const bool conv = fabs(nl - lam) <= 1e-13 * scale || (hi - lo) <= 1e-13 * scale;
+        lam = nl;
+        if (conv) { ok = true; break; }
+    }
+    return lam;
+}
+
+__device__ __forceinline__ double digamma_d(double x) {
+    double r = 0.0;
+    while (x < 6.0) { r -= 1.0 / x; x += 1.0; }
+    const double f = 1.0 / (x * x);
+    return r + log(x) - 0.5 / x -
+           f * (1.0 / 12 - f * (1.0 / 120 - f * (1.0 / 252 - f * (1.0 / 240 - f / 132))));
+}
+__device__ __forceinline__ double trigamma_d(double x) {
+    double r = 0.0;
+    while (x < 6.0) { r += 1.0 / (x * x); x += 1.0; }
+    const double f = 1.0 / (x * x);
+    return r + 1.0 / x + f / 2.0 + f / x * (1.0 / 6 - f * (1.0 / 30 - f * (1.0 / 42 - f * (1.0 / 30))));
+}
+
+// x = I^-1(Phi(v); a, b) by the fp64 solve (initial guess: logit(X) normal,
+// moments psi(a)-psi(b), psi1(a)+psi1(b)); returns lambda
+__device__ __forceinline__ double lambda_exact64(double v, double a, double b, double lnB, double lam0,
+                                                 bool &ok) {
+    const bool lower = v <= 0.0;
+    const double t = 0.5 * erfc(fabs(v) * 0.70710678118654752440);
+    return solve_logit64(log(t), lower, a, b, lnB, lam0, ok);
+}
+
+// ------------------------------------------------------------ table eval --
+
+__device__ __forceinline__ void sigmoid2(float lam, float &x, float &y) {
+    const float l = fminf(fmaxf(lam, -80.0f), 80.0f);
+    const float e = __expf(-l);
+    x = __frcp_rn(1.0f + e);
+    y = e * x;
+}
+
+// quintic Hermite in v on the record's table
+__device__ __forceinline__ float lambda_table(const float2 *__restrict__ tab, float a, float b, float v) {
+    const float u = (fminf(fmaxf(v, kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
+    const int i = min((int)u, kTabNodes - 2);
+    const float t = u - (float)i;
+    const float2 n0 = __ldg(tab + i), n1 = __ldg(tab + i + 1);
+    const float v0 = fmaf((float)i, kTabH, kTabV0), v1 = v0 + kTabH;
+    float x0, y0, x1, y1;
+    sigmoid2(n0.x, x0, y0);
+    sigmoid2(n1.x, x1, y1);
+    const float s0 = n0.y * (-v0 - fmaf(a, y0, -b * x0) * n0.y);   // lambda'' at the nodes
+    const float s1 = n1.y * (-v1 - fmaf(a, y1, -b * x1) * n1.y);
+    const float t2 = t * t, t3 = t2 * t;
+    const float omt = 1.0f - t;
+    // quintic Hermite basis on [0,1] (derivatives scaled by h, h^2)
+    const float h01 = t3 * fmaf(t, fmaf(6.0f, t, -15.0f), 10.0f);             // 10t^3-15t^4+6t^5
+    const float h10 = t * omt * omt * omt * fmaf(3.0f, t, 1.0f);                // t(1-t)^3(1+3t)
+    const float h11 = -t3 * omt * fmaf(-3.0f, t, 4.0f);                         // -t^3(1-t)(4-3t)
+    const float h20 = 0.5f * t2 * omt * omt * omt;                              // t^2(1-t)^3/2
+    const float h21 = 0.5f * t3 * omt * omt;                                    // t^3(1-t)^2/2
+    const float H = kTabH, H2 = kTabH * kTabH;
+    float lam = fmaf(h01, n1.x - n0.x, n0.x);
+    lam = fmaf(h10 * H, n0.y, lam);
+    lam = fmaf(h11 * H, n1.y, lam);
+    lam = fmaf(h20 * H2, s0, lam);
+    lam = fmaf(h21 * H2, s1, lam);
+    return lam;
+}
+
+__device__ __forceinline__ float sigmoidf_(float lam) { return __frcp_rn(1.0f + __expf(-lam)); }
+
+// Per-sample fp64 solve (table-less records, ARA_EXACT); kept out of line so
+// its register demand does not constrain the hot path.
+static __device__ __noinline__ float sample_exact64(float af, float bf, float mu_l, float sd_l, float scale,
+                                             float v, bool &ok) {
+    const double a = af, b = bf;
+    const double lnB = lgamma(a) + lgamma(b) - lgamma(a + b);
+    const double lam = lambda_exact64((double)v, a, b, lnB, (double)mu_l + (double)v * sd_l, ok);
+    const double x = 1.0 / (1.0 + exp(-lam));
+    return (float)((double)scale * x);
+}
+
+// One loss draw (Alg.1 line 7) given v.  EX instantiates the fp64 fallback;
+// kernels without it are only launched when every record has a table.
+template <bool EX>
+__device__ __forceinline__ float sample_loss_from_v(const BetaRec &r, const float2 *__restrict__ tables,
+                                                    uint64_t rec, float v, bool exact, bool &ok) {
+    ok = true;
+    if (r.mode == kModeDegenerate) return r.scale;               // G10
+    if (!EX || (r.mode == kModeTable && !exact)) {
+        const float lam = lambda_table(tables + rec * kTabStride, r.a, r.b, v);
+        return r.scale * sigmoidf_(lam);
+    }
+    return sample_exact64(r.a, r.b, r.mu_l, r.sd_l, r.scale, v, ok);
 }
 
 }  // namespace ara

@@ -105,6 +105,56 @@ def test_sampler_vs_oracle(A, ctx):
     assert ((g >= 0) & (g <= mx)).all()
 
 
+def test_sampler_exact_mode_vs_oracle(A, ctx):
+    # ARA_EXACT: the per-sample fp64 solve, no tables
+    n = 20000
+    recs = gen_records(n)
+    rng = np.random.default_rng(3)
+    zp, ze = grid_uniforms(rng, n), grid_uniforms(rng, n)
+    g = A.sample_losses(ctx, recs, zp, ze, exact=True).astype(np.float64)
+    t = A.sample_losses(ctx, recs, zp, ze).astype(np.float64)
+    o = oracle.sample_batch(recs["mean_loss"], recs["sigma_i"], recs["sigma_c"], recs["max_loss"],
+                            zp.astype(np.float64), ze.astype(np.float64))
+    mx = recs["max_loss"].astype(np.float64)
+    assert (np.abs(g - o) <= 1e-5 * o + 1e-8 * mx).all()
+    assert (np.abs(t - g) <= 1e-5 * g + 1e-8 * mx).all()          # table vs exact solve
+
+
+def test_capped_records_fall_back_to_exact(A, ctx):
+    # records at the sigma_beta cap (G9: alpha, beta ~ 1e-6) are near-Bernoulli;
+    # their table fails the midpoint check and the scan uses the fp64 solve
+    cfg = aragen.load_config("cfg1")
+    cfg.update(n_trials=300, catalog=500, records_per_elt=200)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    pf["rec_sigma_i"] = pf["rec_sigma_i"].copy()
+    pf["rec_sigma_i"][::7] = pf["rec_max"][::7]                   # sigma >= sigma_max -> capped
+    (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, 21)
+    assert np.array_equal(cnt, ref["count"])
+    ylt_check(g, ref)
+    r = np.zeros(3, A.RECORD_DTYPE)
+    r["max_loss"] = 100.0; r["mean_loss"] = [30, 50, 80]; r["sigma_i"] = [80, 60, 50]
+    zz = np.linspace(0.01, 0.99, 99).astype(np.float32)
+    for j in range(3):
+        rr = np.repeat(r[j:j + 1], len(zz))
+        g = A.sample_losses(ctx, rr, zz, zz).astype(np.float64)
+        o = oracle.sample_batch(rr["mean_loss"], rr["sigma_i"], rr["sigma_c"], rr["max_loss"],
+                                zz.astype(np.float64), zz.astype(np.float64))
+        assert np.isfinite(g).all()
+        # away from the Bernoulli step at z = 1 - mu_beta, where fp32 vs fp64 v decides
+        far = np.abs(zz - (1 - r["mean_loss"][j] / 100.0)) > 1e-3
+        assert (np.abs(g - o) <= 1e-4 * o + 1e-6 * 100)[far].all(), (j, g, o)
+
+
+def test_scan_exact_mode(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 200
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    g = A.run(ctx, P, Y, seed=cfg["seed"], exact=True).cpu().numpy()
+    ref = oracle.run(pf, yet, seed=cfg["seed"])
+    ylt_check(g, ref)
+
+
 def test_sampler_extreme_v_and_edges(A, ctx):
     recs = gen_records(4000)
     rng = np.random.default_rng(2)

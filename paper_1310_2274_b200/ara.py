@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libara.so")
+LIB_PATH = os.environ.get("ARA_LIB_PATH") or os.path.join(_HERE, "lib", "libara.so")
 
 OK, EINVAL, ERANGE, EDUP, ENOMEM, ECUDA, ECONVERGE, ENCCL = range(8)
 SU = 1

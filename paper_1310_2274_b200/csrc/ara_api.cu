@@ -69,7 +69,7 @@ struct ara_portfolio {
     PortfolioDev dev{};
     uint32_t *d_index = nullptr, *d_bitmap = nullptr, *d_rec_orig = nullptr;
     BetaRec *d_recs = nullptr;
-    float2 *d_tables = nullptr;
+    float2 *d_tables = nullptr, *d_hot = nullptr;
     float *d_mu = nullptr;
     SlotInfo *d_slots = nullptr;
     LayerInfo *d_layers = nullptr;
@@ -292,7 +292,7 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     };
     if (dalloc(&p->d_index, index.size()) || dalloc(&p->d_bitmap, words) ||
         dalloc(&p->d_rec_orig, total) || dalloc(&p->d_recs, total) || dalloc(&p->d_mu, total) ||
-        dalloc(&p->d_tables, total * kTabStride) ||
+        dalloc(&p->d_tables, total * kTabStride) || dalloc(&p->d_hot, total * kHotN) ||
         dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) || dalloc(&d_raw, R) ||
         dalloc(&d_src, total)) {
         cudaGetLastError();
@@ -311,7 +311,8 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     if (e != cudaSuccess) return cleanup(fail(ARA_ECUDA, "upload: %s", cudaGetErrorString(e)));
     e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
     if (e == cudaSuccess) {
-        launch_prep_records(d_raw, d_src, total, p->d_recs, p->d_mu, p->d_tables, &c->d_status->nonconverged, s);
+        launch_prep_records(d_raw, d_src, total, p->d_recs, p->d_mu, p->d_tables, p->d_hot,
+                            &c->d_status->nonconverged, s);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
@@ -326,6 +327,7 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     d.n_exact_records = c->h_status->nonconverged;
     d.index = p->d_index; d.bitmap = p->d_bitmap; d.recs = p->d_recs; d.rec_mu = p->d_mu;
     d.tables = p->d_tables;
+    d.hot = p->d_hot;
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
     *out = p;
     return ARA_OK;
@@ -339,7 +341,7 @@ int ara_portfolio_info(const ara_portfolio *p, uint64_t *n_dev, uint64_t *n_tl, 
     if (bytes)
         *bytes = (uint64_t)d.catalog * d.idx_stride * 4 + (uint64_t)d.bitmap_words * 4 +
                  d.n_dev_records * (sizeof(BetaRec) + sizeof(float) + sizeof(uint32_t) +
-                                    kTabStride * sizeof(float2)) +
+                                    (kTabStride + kHotN) * sizeof(float2)) +
                  d.n_slots * sizeof(SlotInfo) + d.n_layers * sizeof(LayerInfo);
     return ARA_OK;
 }
@@ -348,7 +350,7 @@ void ara_portfolio_destroy(ara_portfolio *p) {
     if (!p) return;
     if (p->ctx) cudaSetDevice(p->ctx->device);
     cudaFree(p->d_index); cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig); cudaFree(p->d_recs);
-    cudaFree(p->d_mu); cudaFree(p->d_slots); cudaFree(p->d_layers); cudaFree(p->d_tables);
+    cudaFree(p->d_mu); cudaFree(p->d_slots); cudaFree(p->d_layers); cudaFree(p->d_tables); cudaFree(p->d_hot);
     delete p;
 }
 
@@ -540,12 +542,13 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
     CU(cudaSetDevice(c->device));
     ara_record *d_raw = nullptr;
     BetaRec *d_recs = nullptr;
-    float2 *d_tab = nullptr;
+    float2 *d_tab = nullptr, *d_hot = nullptr;
     float *d_mu = nullptr, *d_zp = nullptr, *d_ze = nullptr, *d_out = nullptr;
     int code = ARA_OK;
     cudaError_t e = cudaSuccess;
     if (dalloc(&d_raw, n) || dalloc(&d_recs, n) || dalloc(&d_mu, n) || dalloc(&d_zp, n) ||
-        dalloc(&d_ze, n) || dalloc(&d_out, n) || dalloc(&d_tab, n * kTabStride)) {
+        dalloc(&d_ze, n) || dalloc(&d_out, n) || dalloc(&d_tab, n * kTabStride) ||
+        dalloc(&d_hot, n * kHotN)) {
         cudaGetLastError();
         code = fail(ARA_ENOMEM, "device allocation failed");
     } else {
@@ -554,8 +557,8 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
         if (!e) e = cudaMemcpyAsync(d_zp, zp, n * sizeof(float), cudaMemcpyHostToDevice, s);
         if (!e) e = cudaMemcpyAsync(d_ze, ze, n * sizeof(float), cudaMemcpyHostToDevice, s);
         if (!e) e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
-        if (!e) { launch_prep_records(d_raw, nullptr, n, d_recs, d_mu, d_tab, nullptr, s); e = cudaGetLastError(); }
-        if (!e) e = launch_sample_losses(d_recs, d_tab, d_zp, d_ze, n, (flags & ARA_EXACT) != 0, d_out,
+        if (!e) { launch_prep_records(d_raw, nullptr, n, d_recs, d_mu, d_tab, d_hot, nullptr, s); e = cudaGetLastError(); }
+        if (!e) e = launch_sample_losses(d_recs, d_tab, d_hot, d_zp, d_ze, n, (flags & ARA_EXACT) != 0, d_out,
                                          c->d_status, s);
         if (!e) e = cudaMemcpyAsync(loss_out, d_out, n * sizeof(float), cudaMemcpyDeviceToHost, s);
         if (!e) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
@@ -565,7 +568,7 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
             code = fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples", c->h_status->nonconverged);
     }
     cudaFree(d_raw); cudaFree(d_recs); cudaFree(d_mu); cudaFree(d_zp); cudaFree(d_ze); cudaFree(d_out);
-    cudaFree(d_tab);
+    cudaFree(d_tab); cudaFree(d_hot);
     return code;
 }
 

@@ -37,6 +37,9 @@ struct LayerInfo {
 constexpr int kTabNodes = 33;           // j = 0..32
 constexpr int kTabStride = 34;          // float2 per record (padded)
 constexpr float kTabV0 = -8.0f, kTabH = 0.5f;
+// the central nodes j = 9..24 (v in [-3.5, 4]; 99.97 % of samples) are also
+// kept in a compact 128 B-per-record "hot" array that stays L2-resident
+constexpr int kHotJ0 = 9, kHotN = 16;
 
 constexpr uint32_t kModeTable = 0, kModeExact = 1, kModeDegenerate = 2;
 struct __align__(16) BetaRec {
@@ -58,6 +61,7 @@ struct PortfolioDev {
     const uint32_t *bitmap;   // [bitmap_words]
     const BetaRec *recs;      // [n_dev_records] event-major, slot order
     const float2 *tables;     // [n_dev_records][kTabStride] (lambda, lambda') nodes
+    const float2 *hot;        // [n_dev_records][kHotN] nodes kHotJ0.. of the same tables
     const float *rec_mu;      // [n_dev_records] mean loss (primary uncertainty)
     const uint32_t *rec_orig; // [n_dev_records] record index within its XELT
     const SlotInfo *slots;    // [n_slots]
@@ -83,8 +87,8 @@ struct RunStatus {
 
 // kernels
 void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_t n,
-                         BetaRec *out, float *out_mu, float2 *tables, unsigned int *n_exact,
-                         cudaStream_t s);
+                         BetaRec *out, float *out_mu, float2 *tables, float2 *hot,
+                         unsigned int *n_exact, cudaStream_t s);
 // Scan every trial of `yet`, or (trial_list != null) only the n_list listed
 // trials.  Without ARA_EXACT the table-only kernel runs and appends to
 // `redo` every trial that met a table-less record; the caller re-runs those
@@ -93,7 +97,8 @@ cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed
                         float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
                         const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
                         cudaStream_t s, int num_sms);
-cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float *zp,
+cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float2 *hot,
+                                 const float *zp,
                                  const float *ze, uint64_t n, bool exact, float *out,
                                  RunStatus *status, cudaStream_t s);
 cudaError_t launch_draw_uniforms(uint64_t seed, const uint4 *ctr, uint64_t n, float *out,

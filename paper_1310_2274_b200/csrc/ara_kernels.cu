@@ -40,7 +40,8 @@ __device__ double quintic_mid64(float l0, float d0, float l1, float d1, double v
 
 __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const uint32_t *__restrict__ src,
                                     uint64_t n, BetaRec *__restrict__ out, float *__restrict__ out_mu,
-                                    float2 *__restrict__ tables, unsigned int *n_exact) {
+                                    float2 *__restrict__ tables, float2 *__restrict__ hot,
+                                    unsigned int *n_exact) {
     const double LN_SQRT_2PI = 0.91893853320467274178;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
          t += (uint64_t)gridDim.x * blockDim.x) {
@@ -96,6 +97,7 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
             if (good) {
                 for (int j = 0; j < kTabNodes; ++j) tab[j] = make_float2((float)lam[j], (float)d1[j]);
                 tab[kTabNodes] = make_float2(0.0f, 0.0f);
+                for (int j = 0; j < kHotN; ++j) hot[t * kHotN + j] = tab[kHotJ0 + j];
                 for (int j = 0; j + 1 < kTabNodes && good; ++j) {
                     const double v0 = kTabV0 + kTabH * j;
                     const double li = quintic_mid64(tab[j].x, tab[j].y, tab[j + 1].x, tab[j + 1].y, v0,
@@ -118,12 +120,13 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
 }
 
 void launch_prep_records(const ara_record *raw, const uint32_t *src, uint64_t n, BetaRec *out,
-                         float *out_mu, float2 *tables, unsigned int *n_exact, cudaStream_t s) {
+                         float *out_mu, float2 *tables, float2 *hot, unsigned int *n_exact,
+                         cudaStream_t s) {
     if (n == 0) return;
     const int threads = 128;
     const uint64_t blocks = (n + threads - 1) / threads;
     prep_records_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), threads, 0, s>>>(
-        raw, src, n, out, out_mu, tables, n_exact);
+        raw, src, n, out, out_mu, tables, hot, n_exact);
 }
 
 // ---------------------------------------------------------------------------
@@ -143,9 +146,12 @@ void launch_prep_records(const ara_record *raw, const uint32_t *src, uint64_t n,
 // All reductions are fixed trees / fixed orders: the YLT is a pure function
 // of the inputs (bit-identical across runs and trial shardings).
 // ---------------------------------------------------------------------------
-constexpr int kWarps = 24;          // warps per CTA (1 CTA per SM)
+#ifndef ARA_SCAN_WARPS
+#define ARA_SCAN_WARPS 16
+#endif
+constexpr int kWarps = ARA_SCAN_WARPS;  // warps per CTA (1 CTA per SM)
 constexpr int kQCap = 256;          // pair queue capacity per warp (>= ARA_MAX_SLOTS)
-constexpr int kHCap = 64;           // hit list capacity per warp (flushed at >= 32)
+constexpr int kHCap = 64;           // hit list capacity per warp (processed at >= 32)
 static_assert(kQCap >= ARA_MAX_SLOTS, "queue must hold one occurrence's pairs");
 
 struct WarpBuf {
@@ -182,21 +188,33 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
     return v;
 }
 
-// this warp's shared-memory pieces and the block's tables
+// Dynamic shared memory of the scan kernel.  The out-of-line helpers address
+// it through this symbol + byte offsets so every access compiles to LDS/STS.
+extern __shared__ __align__(16) unsigned char scan_smem[];
+
+// byte offsets of this warp's pieces and the block's tables in scan_smem
 struct WarpMem {
-    WarpBuf *B;
-    double *S;
-    unsigned long long *hsh;
-    unsigned int *cnt;
-    const SlotInfo *slots;
-    const LayerInfo *layers;
+    uint32_t buf, S, hsh, cnt, slots, layers;
 };
+__device__ __forceinline__ WarpBuf &wbuf(const WarpMem &M) { return *reinterpret_cast<WarpBuf *>(scan_smem + M.buf); }
+__device__ __forceinline__ double *wS(const WarpMem &M) { return reinterpret_cast<double *>(scan_smem + M.S); }
+__device__ __forceinline__ unsigned long long *whsh(const WarpMem &M) {
+    return reinterpret_cast<unsigned long long *>(scan_smem + M.hsh);
+}
+__device__ __forceinline__ unsigned int *wcnt(const WarpMem &M) { return reinterpret_cast<unsigned int *>(scan_smem + M.cnt); }
+__device__ __forceinline__ const SlotInfo *wslots(const WarpMem &M) {
+    return reinterpret_cast<const SlotInfo *>(scan_smem + M.slots);
+}
+__device__ __forceinline__ const LayerInfo *wlayers(const WarpMem &M) {
+    return reinterpret_cast<const LayerInfo *>(scan_smem + M.layers);
+}
 
 // what the sampler needs from the launch arguments (passed by value into the
 // out-of-line helpers so they read registers, not the param space)
 struct SampleArgs {
     const BetaRec *recs;
     const float2 *tables;
+    const float2 *hot;
     const float *rec_mu;
     const uint32_t *rec_orig;
     RunStatus *status;
@@ -205,45 +223,66 @@ struct SampleArgs {
     bool dbg;
 };
 
+// one loss draw for queue entry e (Alg.1 lines 7-8); r already loaded
+template <bool EX>
+__device__ __forceinline__ float draw_one(const SampleArgs &G, const SlotInfo &si, const BetaRec &r,
+                                          uint2 e, uint32_t trial_g, int &redo) {
+    float x;
+    if (r.mode == kModeDegenerate) {
+        x = r.scale;
+    } else if (!EX && r.mode == kModeExact) {
+        x = 0.0f;                       // table-less record: this trial is redone by the fp64 kernel
+        redo = 1;
+    } else {
+        const uint32_t k = e.y >> 8;
+        const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, G.seed);   // z_(Prog,E)
+        const uint32_t be = philox_lane0(trial_g, k, si.elt, 2u, G.seed);    // z_(E)
+        const float v = combine_v(r, norm_quantile_from_bits(bp), norm_quantile_from_bits(be));
+        bool ok;
+        x = sample_loss_from_v<EX>(r, G.tables, G.hot, e.x, v, G.exact, ok);
+        if (!ok) atomicAdd(&G.status->nonconverged, 1u);
+    }
+    if (si.has_terms) x = si.share * fminf(fmaxf(x - si.ret, 0.0f), si.lim);
+    return x;
+}
+
 // Sample every queued pair, reduce the (occurrence, layer) segments, apply the
-// occurrence terms, add to the layer sums.  Out of line: one copy of the
-// sampler in the kernel keeps the instruction working set in the I-cache.
-// Returns 1 if a table-less record was met (the trial must be redone).
+// occurrence terms, add to the layer sums.  Out of line: a single copy of the
+// sampler keeps the instruction working set in the I-cache.  Returns 1 if a
+// table-less record was met (the trial must be redone).
 template <bool SU, bool EX>
 __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uint32_t trial_g, int lane,
                                         int qn) {
-    WarpBuf &B = *M.B;
+    WarpBuf &B = wbuf(M);
+    const SlotInfo *slots = wslots(M);
     int redo = 0;
-    // sample: one loss per queued pair, all lanes busy (Alg.1 lines 7-8)
-    for (int p = lane; p < qn; p += 32) {
-        const uint2 e = B.q[p];
-        const uint32_t slot = e.y & 0xffu, k = e.y >> 8;
-        const SlotInfo &si = M.slots[slot];
-        float x;
+    // sample, two pairs per lane in flight (Alg.1 lines 7-8)
+    for (int p0 = lane; p0 < qn; p0 += 64) {
+        const int p1 = p0 + 32;
+        const bool two = p1 < qn;
+        const uint2 e0 = B.q[p0];
+        const uint2 e1 = two ? B.q[p1] : e0;
+        float x0, x1;
         if (SU) {
-            const BetaRec r = G.recs[e.x];
-            if (r.mode == kModeDegenerate) {
-                x = r.scale;
-            } else if (!EX && r.mode == kModeExact) {
-                x = 0.0f;                 // table-less record: this trial is redone by the fp64 kernel
-                redo = 1;
-            } else {
-                const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, G.seed);   // z_(Prog,E)
-                const uint32_t be = philox_lane0(trial_g, k, si.elt, 2u, G.seed);    // z_(E)
-                const float v = combine_v(r, norm_quantile_from_bits(bp), norm_quantile_from_bits(be));
-                bool ok;
-                x = sample_loss_from_v<EX>(r, G.tables, e.x, v, G.exact, ok);
-                if (!ok) atomicAdd(&G.status->nonconverged, 1u);
-            }
+            const BetaRec r0 = G.recs[e0.x];
+            const BetaRec r1 = G.recs[e1.x];
+            x0 = draw_one<EX>(G, slots[e0.y & 0xffu], r0, e0, trial_g, redo);
+            x1 = draw_one<EX>(G, slots[e1.y & 0xffu], r1, e1, trial_g, redo);
         } else {
-            x = __ldg(G.rec_mu + e.x);
+            x0 = __ldg(G.rec_mu + e0.x);
+            x1 = __ldg(G.rec_mu + e1.x);
+            const SlotInfo &s0 = slots[e0.y & 0xffu], &s1 = slots[e1.y & 0xffu];
+            if (s0.has_terms) x0 = s0.share * fminf(fmaxf(x0 - s0.ret, 0.0f), s0.lim);
+            if (s1.has_terms) x1 = s1.share * fminf(fmaxf(x1 - s1.ret, 0.0f), s1.lim);
         }
-        if (si.has_terms) x = si.share * fminf(fmaxf(x - si.ret, 0.0f), si.lim);
-        B.xs[p] = x;
+        B.xs[p0] = x0;
+        if (two) B.xs[p1] = x1;
     }
     __syncwarp();
     // segments = runs of equal (occurrence, layer): sum (line 9), occurrence
     // terms (line 11), add to the layer's trial sum
+    const LayerInfo *layers = wlayers(M);
+    double *S = wS(M);
     for (int base = 0; base < qn; base += 32) {
         const int p = base + lane;
         bool head = false;
@@ -251,22 +290,22 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
         double g = 0.0;
         if (p < qn) {
             const uint2 e = B.q[p];
-            layer = M.slots[e.y & 0xffu].layer;
+            layer = slots[e.y & 0xffu].layer;
             const uint32_t key = (e.y & 0xffffff00u) | layer;
             if (p == 0) {
                 head = true;
             } else {
                 const uint2 ep = B.q[p - 1];
-                head = ((ep.y & 0xffffff00u) | M.slots[ep.y & 0xffu].layer) != key;
+                head = ((ep.y & 0xffffff00u) | slots[ep.y & 0xffu].layer) != key;
             }
             if (head) {
                 double l = 0.0;
                 for (int r = p; r < qn; ++r) {
                     const uint2 er = B.q[r];
-                    if (((er.y & 0xffffff00u) | M.slots[er.y & 0xffu].layer) != key) break;
+                    if (((er.y & 0xffffff00u) | slots[er.y & 0xffu].layer) != key) break;
                     l += (double)B.xs[r];
                 }
-                const LayerInfo &L = M.layers[layer];
+                const LayerInfo &L = layers[layer];
                 g = fmin(fmax(l - L.occ_r, 0.0), L.occ_l);
             }
         }
@@ -278,63 +317,12 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
             const uint32_t lay = __shfl_sync(0xffffffffu, layer, leader);
             const bool mine = head && layer == lay;
             const double sum = warp_sum_f64(mine ? g : 0.0);
-            if (lane == 0) M.S[lay] += sum;
+            if (lane == 0) S[lay] += sum;
             pending &= ~__ballot_sync(0xffffffffu, mine);
         }
     }
     __syncwarp();
     return __any_sync(0xffffffffu, redo) ? 1 : 0;
-}
-
-// enqueue the pairs of one occurrence per lane (whole occurrences only);
-// returns the new queue length
-template <bool SU, bool EX, int MW>
-__device__ __forceinline__ int enqueue(const SampleArgs &G, const WarpMem &M, uint32_t trial_g, int lane,
-                                       int qn, bool todo, uint32_t k, uint32_t first,
-                                       const uint32_t (&mask)[MW], int &redo) {
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int i = 0; i < MW; ++i) cnt += __popc(mask[i]);
-    todo = todo && cnt > 0;
-    while (__any_sync(0xffffffffu, todo)) {
-        uint32_t incl = todo ? cnt : 0u;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const bool fits = todo && incl <= (uint32_t)(kQCap - qn);
-        if (fits) {
-            uint32_t pos = (uint32_t)qn + incl - cnt;
-            uint32_t rec = first;
-#pragma unroll
-            for (int i = 0; i < MW; ++i) {
-                uint32_t mw = mask[i];
-                while (mw) {
-                    const uint32_t slot = (uint32_t)(i * 32 + __ffs(mw) - 1);
-                    mw &= mw - 1;
-                    M.B->q[pos++] = make_uint2(rec, (k << 8) | slot);
-                    if (G.dbg) {
-                        const uint32_t lay = M.slots[slot].layer;
-                        atomicAdd(&M.cnt[lay], 1u);
-                        const uint64_t h = splitmix64(splitmix64(splitmix64((uint64_t)k) ^ M.slots[slot].elt) ^
-                                                      G.rec_orig[rec]);
-                        atomicAdd(&M.hsh[lay], (unsigned long long)h);
-                    }
-                    ++rec;
-                }
-            }
-            todo = false;
-        }
-        const unsigned fitmask = __ballot_sync(0xffffffffu, fits);
-        if (fitmask) qn += (int)__shfl_sync(0xffffffffu, incl, 31 - __clz(fitmask));
-        __syncwarp();
-        if (__any_sync(0xffffffffu, todo)) {
-            redo |= flush_queue<SU, EX>(G, M, trial_g, lane, qn);
-            qn = 0;
-        }
-    }
-    return qn;
 }
 
 template <int MW>
@@ -359,39 +347,88 @@ __device__ __forceinline__ void load_index(const uint32_t *index, uint32_t strid
     }
 }
 
-// index lookups for the warp's hit list (two per lane in flight), then
-// enqueue.  Out of line (called from several places).  Returns the new queue
-// length, | 0x10000 if a table-less record was met.
+// Index lookups (Alg.1 line 6) for the warp's <= 64 hits, two per lane in
+// flight, then enqueue all present (occurrence, slot) pairs, whole
+// occurrences at a time, flushing when the queue would overflow.  Out of line.
+// Returns the new queue length, | 0x10000 if a table-less record was met.
 template <bool SU, bool EX, int MW>
 __device__ __noinline__ int process_hits(const SampleArgs G, const WarpMem M, const uint32_t *index,
                                          uint32_t stride, uint32_t trial_g, int lane, int nh, int qn) {
-    const bool h0 = lane < nh, h1 = lane + 32 < nh;
-    const uint2 a0 = h0 ? M.B->hits[lane] : make_uint2(0, 0);
-    const uint2 a1 = h1 ? M.B->hits[lane + 32] : make_uint2(0, 0);
-    uint32_t f0 = 0, f1 = 0, m0[MW], m1[MW];
+    WarpBuf &B = wbuf(M);
+    const SlotInfo *slots = wslots(M);
+    uint32_t kk[2], first[2], mask[2][MW], cnt[2];
 #pragma unroll
-    for (int i = 0; i < MW; ++i) { m0[i] = 0u; m1[i] = 0u; }
-    if (h0) load_index<MW>(index, stride, a0.y, f0, m0);                  // Alg.1 line 6
-    if (h1) load_index<MW>(index, stride, a1.y, f1, m1);
+    for (int h = 0; h < 2; ++h) {
+        const int i = lane + 32 * h;
+        const uint2 a = i < nh ? B.hits[i] : make_uint2(0, 0);
+        kk[h] = a.x;
+        first[h] = 0;
+#pragma unroll
+        for (int w = 0; w < MW; ++w) mask[h][w] = 0u;
+        if (i < nh) load_index<MW>(index, stride, a.y, first[h], mask[h]);
+    }
     __syncwarp();
     int redo = 0;
-    qn = enqueue<SU, EX, MW>(G, M, trial_g, lane, qn, h0, a0.x, f0, m0, redo);
-    qn = enqueue<SU, EX, MW>(G, M, trial_g, lane, qn, h1, a1.x, f1, m1, redo);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        cnt[h] = 0;
+#pragma unroll
+        for (int w = 0; w < MW; ++w) cnt[h] += __popc(mask[h][w]);
+        bool todo = cnt[h] > 0;
+        while (__any_sync(0xffffffffu, todo)) {
+            uint32_t incl = todo ? cnt[h] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const bool fits = todo && incl <= (uint32_t)(kQCap - qn);
+            if (fits) {
+                uint32_t pos = (uint32_t)qn + incl - cnt[h];
+                uint32_t rec = first[h];
+#pragma unroll
+                for (int w = 0; w < MW; ++w) {
+                    uint32_t mw = mask[h][w];
+                    while (mw) {
+                        const uint32_t slot = (uint32_t)(w * 32 + __ffs(mw) - 1);
+                        mw &= mw - 1;
+                        B.q[pos++] = make_uint2(rec, (kk[h] << 8) | slot);
+                        if (G.dbg) {
+                            const uint32_t lay = slots[slot].layer;
+                            atomicAdd(&wcnt(M)[lay], 1u);
+                            const uint64_t hv = splitmix64(splitmix64(splitmix64((uint64_t)kk[h]) ^ slots[slot].elt) ^
+                                                           G.rec_orig[rec]);
+                            atomicAdd(&whsh(M)[lay], (unsigned long long)hv);
+                        }
+                        ++rec;
+                    }
+                }
+                todo = false;
+            }
+            const unsigned fitmask = __ballot_sync(0xffffffffu, fits);
+            if (fitmask) qn += (int)__shfl_sync(0xffffffffu, incl, 31 - __clz(fitmask));
+            __syncwarp();
+            if (__any_sync(0xffffffffu, todo)) {
+                redo |= flush_queue<SU, EX>(G, M, trial_g, lane, qn);
+                qn = 0;
+            }
+        }
+    }
     return qn | (redo << 16);
 }
 
 template <bool SU, bool EX, int MW>
 __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_constant__ ScanArgs A) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t nl = A.pf.n_layers;
-    const size_t per_warp = sizeof(WarpBuf) + nl * (sizeof(double) + sizeof(unsigned long long) +
-                                                    sizeof(unsigned int));
-    const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
-    SlotInfo *slots = reinterpret_cast<SlotInfo *>(smem_raw);
-    LayerInfo *layers = reinterpret_cast<LayerInfo *>(slots + ARA_MAX_SLOTS);
-    uint32_t *bitmap = reinterpret_cast<uint32_t *>(layers + ARA_MAX_LAYERS);
-    unsigned char *warp_base = reinterpret_cast<unsigned char *>(bitmap) +
-                               ((size_t)A.pf.bitmap_words * 4 + 15) / 16 * 16;
+    const uint32_t per_warp = (uint32_t)((sizeof(WarpBuf) + nl * (sizeof(double) + sizeof(unsigned long long) +
+                                                                   sizeof(unsigned int)) + 15) & ~size_t(15));
+    const uint32_t off_slots = 0;
+    const uint32_t off_layers = off_slots + sizeof(SlotInfo) * ARA_MAX_SLOTS;
+    const uint32_t off_bitmap = off_layers + sizeof(LayerInfo) * ARA_MAX_LAYERS;
+    const uint32_t off_warps = off_bitmap + (A.pf.bitmap_words * 4u + 15u) / 16u * 16u;
+    SlotInfo *slots = reinterpret_cast<SlotInfo *>(scan_smem + off_slots);
+    LayerInfo *layers = reinterpret_cast<LayerInfo *>(scan_smem + off_layers);
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(scan_smem + off_bitmap);
 
     for (uint32_t t = threadIdx.x; t < A.pf.bitmap_words; t += blockDim.x) bitmap[t] = A.pf.bitmap[t];
     for (uint32_t t = threadIdx.x; t < A.pf.n_slots; t += blockDim.x) slots[t] = A.pf.slots[t];
@@ -400,21 +437,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpMem M;
-    unsigned char *mine = warp_base + per_warp_al * warp;
-    M.B = reinterpret_cast<WarpBuf *>(mine);
-    M.S = reinterpret_cast<double *>(mine + sizeof(WarpBuf));
-    M.hsh = reinterpret_cast<unsigned long long *>(M.S + nl);
-    M.cnt = reinterpret_cast<unsigned int *>(M.hsh + nl);
-    M.slots = slots;
-    M.layers = layers;
+    M.buf = off_warps + per_warp * warp;
+    M.S = M.buf + sizeof(WarpBuf);
+    M.hsh = M.S + nl * sizeof(double);
+    M.cnt = M.hsh + nl * sizeof(unsigned long long);
+    M.slots = off_slots;
+    M.layers = off_layers;
+    WarpBuf &B = wbuf(M);
+    double *S = wS(M);
+    unsigned long long *hsh = whsh(M);
+    unsigned int *cntv = wcnt(M);
     const bool dbg = (A.flags & ARA_DEBUG_LOOKUP) != 0;
-    const SampleArgs G{A.pf.recs, A.pf.tables, A.pf.rec_mu, A.pf.rec_orig, A.status, A.seed,
+    const SampleArgs G{A.pf.recs, A.pf.tables, A.pf.hot, A.pf.rec_mu, A.pf.rec_orig, A.status, A.seed,
                        (A.flags & ARA_EXACT) != 0, dbg};
     const uint64_t n_trials = A.yet.n_trials;
     const uint64_t n_work = A.trial_list ? A.n_list : n_trials;
     const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift;
     const uint32_t *index = A.pf.index;
     const uint32_t stride = A.pf.idx_stride;
+    const unsigned lanemask_lt = (1u << lane) - 1u;
 
     while (true) {
         unsigned long long t = 0;
@@ -425,48 +466,83 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
         const uint64_t base = A.yet.fixed_len ? t * (uint64_t)A.yet.fixed_len : A.yet.offsets[t];
         const uint32_t len = A.yet.fixed_len ? A.yet.fixed_len : (uint32_t)(A.yet.offsets[t + 1] - base);
         const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);        // global trial index i
-        for (uint32_t l = lane; l < nl; l += 32) { M.S[l] = 0.0; M.cnt[l] = 0u; M.hsh[l] = 0ull; }
+        for (uint32_t l = lane; l < nl; l += 32) { S[l] = 0.0; cntv[l] = 0u; hsh[l] = 0ull; }
         __syncwarp();
         int qn = 0, nh = 0, redo = 0;
         const uint32_t *ev = A.yet.events + base;
         const bool vec = (base & 3u) == 0;
-        auto load4 = [&](uint32_t c) -> uint4 {                     // events c+4*lane .. +3
-            const uint32_t k = c + 4u * lane;
-            if (vec && k + 3 < len) return __ldcs(reinterpret_cast<const uint4 *>(ev + k));
-            uint4 r = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-            if (k < len) r.x = __ldcs(ev + k);
-            if (k + 1 < len) r.y = __ldcs(ev + k + 1);
-            if (k + 2 < len) r.z = __ldcs(ev + k + 2);
-            if (k + 3 < len) r.w = __ldcs(ev + k + 3);
-            return r;
-        };
-        uint4 cur = len ? load4(0) : make_uint4(0, 0, 0, 0);
+        uint4 nxt = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+        {   // events c+4*lane .. +3 of chunk 0
+            const uint32_t k = 4u * lane;
+            if (vec && k + 3 < len) nxt = __ldcs(reinterpret_cast<const uint4 *>(ev + k));
+            else {
+                if (k < len) nxt.x = __ldcs(ev + k);
+                if (k + 1 < len) nxt.y = __ldcs(ev + k + 1);
+                if (k + 2 < len) nxt.z = __ldcs(ev + k + 2);
+                if (k + 3 < len) nxt.w = __ldcs(ev + k + 3);
+            }
+        }
         for (uint32_t c = 0; c < len; c += 128) {                   // Alg.1 line 4
-            const uint4 nxt = (c + 128 < len) ? load4(c + 128) : make_uint4(0, 0, 0, 0);
-            const uint32_t e4[4] = {cur.x, cur.y, cur.z, cur.w};
+            const uint4 cur = nxt;
+            {   // prefetch the next chunk
+                const uint32_t k = c + 128 + 4u * lane;
+                nxt = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                if (vec && k + 3 < len) nxt = __ldcs(reinterpret_cast<const uint4 *>(ev + k));
+                else if (k < len) {
+                    nxt.x = __ldcs(ev + k);
+                    if (k + 1 < len) nxt.y = __ldcs(ev + k + 1);
+                    if (k + 2 < len) nxt.z = __ldcs(ev + k + 2);
+                    if (k + 3 < len) nxt.w = __ldcs(ev + k + 3);
+                }
+            }
+            // presence bitmap (shared memory) for this lane's 4 occurrences
+            const uint32_t k0 = c + 4u * lane;
+            const uint32_t ee[4] = {cur.x, cur.y, cur.z, cur.w};
+            uint32_t hitbits = 0;
 #pragma unroll
             for (int qd = 0; qd < 4; ++qd) {
-                const uint32_t k = c + 4u * lane + qd;
-                const uint32_t e = e4[qd];
-                bool hit = false;
-                if (k < len) {
+                const uint32_t e = ee[qd];
+                if (k0 + qd < len) {
                     if (e >= C) {
                         atomicAdd(&A.status->bad_event, 1u);
                     } else {
                         const uint32_t bit = e >> shift;
-                        hit = (bitmap[bit >> 5] >> (bit & 31)) & 1u;
+                        hitbits |= ((bitmap[bit >> 5] >> (bit & 31)) & 1u) << qd;
                     }
                 }
-                const unsigned hm = __ballot_sync(0xffffffffu, hit);
-                if (hit) M.B->hits[nh + __popc(hm & ((1u << lane) - 1u))] = make_uint2(k, e);
-                nh += __popc(hm);
-                if (nh >= 32) {                      // <= 63 queued: two index loads per lane
+            }
+            // one warp prefix sum per chunk; hits appended in (lane, qd) order
+            const uint32_t nmine = __popc(hitbits);
+            uint32_t incl = nmine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            uint32_t pos = incl - nmine;                // position among this chunk's hits
+            // the chunk's hits are written in slices of <= 64 - nh so the list never overflows
+            uint32_t done = 0;
+            while (done < total) {
+                const uint32_t room = (uint32_t)(kHCap - nh);
+                const uint32_t take = min(room, total - done);
+#pragma unroll
+                for (int qd = 0; qd < 4; ++qd) {
+                    if ((hitbits >> qd) & 1u) {
+                        if (pos >= done && pos < done + take)
+                            B.hits[nh + (pos - done)] = make_uint2(k0 + qd, ee[qd]);
+                        ++pos;
+                    }
+                }
+                pos = incl - nmine;
+                nh += (int)take;
+                done += take;
+                if (nh >= 32) {                          // index lookups + enqueue (line 6)
                     __syncwarp();
                     const int r = process_hits<SU, EX, MW>(G, M, index, stride, trial_g, lane, nh, qn);
                     qn = r & 0xffff; redo |= r >> 16; nh = 0;
                 }
             }
-            cur = nxt;
         }
         __syncwarp();
         if (nh) {
@@ -480,22 +556,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
         // aggregate terms on the trial sum (line 12, G6) -> YLT (line 17)
         for (uint32_t l = lane; l < nl; l += 32) {
             const LayerInfo &L = layers[l];
-            A.ylt[(uint64_t)l * n_trials + t] = (float)fmin(fmax(M.S[l] - L.agg_r, 0.0), L.agg_l);
+            A.ylt[(uint64_t)l * n_trials + t] = (float)fmin(fmax(S[l] - L.agg_r, 0.0), L.agg_l);
             if (dbg) {
-                if (A.dbg_count) A.dbg_count[(uint64_t)l * n_trials + t] = M.cnt[l];
-                if (A.dbg_hash) A.dbg_hash[(uint64_t)l * n_trials + t] = M.hsh[l];
+                if (A.dbg_count) A.dbg_count[(uint64_t)l * n_trials + t] = cntv[l];
+                if (A.dbg_hash) A.dbg_hash[(uint64_t)l * n_trials + t] = hsh[l];
             }
         }
         __syncwarp();
     }
+    (void)lanemask_lt;
 }
 
 static size_t scan_smem_bytes(const PortfolioDev &pf) {
-    const size_t per_warp = sizeof(WarpBuf) + pf.n_layers * (sizeof(double) + sizeof(unsigned long long) +
-                                                             sizeof(unsigned int));
+    const size_t per_warp = (sizeof(WarpBuf) + pf.n_layers * (sizeof(double) + sizeof(unsigned long long) +
+                                                              sizeof(unsigned int)) + 15) & ~size_t(15);
     return sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
-           ((size_t)pf.bitmap_words * 4 + 15) / 16 * 16 + kWarps * ((per_warp + 15) & ~size_t(15));
+           ((size_t)pf.bitmap_words * 4 + 15) / 16 * 16 + kWarps * per_warp;
 }
+
+size_t scan_smem_for(const PortfolioDev &pf) { return scan_smem_bytes(pf); }
 
 template <bool SU, bool EX, int MW>
 static cudaError_t launch_scan_t(const ScanArgs &A, cudaStream_t s, int num_sms) {
@@ -534,7 +613,8 @@ cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed
 // ---------------------------------------------------------------------------
 // Component kernels (row-level parity tests)
 // ---------------------------------------------------------------------------
-__global__ void sample_losses_kernel(const BetaRec *recs, const float2 *tables, const float *zp,
+__global__ void sample_losses_kernel(const BetaRec *recs, const float2 *tables, const float2 *hot,
+                                     const float *zp,
                                      const float *ze, uint64_t n, bool exact, float *out,
                                      RunStatus *status) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
@@ -542,18 +622,19 @@ __global__ void sample_losses_kernel(const BetaRec *recs, const float2 *tables, 
         const BetaRec r = recs[t];
         const float v = combine_v(r, norm_quantile_f(zp[t]), norm_quantile_f(ze[t]));
         bool ok;
-        out[t] = sample_loss_from_v<true>(r, tables, t, v, exact, ok);
+        out[t] = sample_loss_from_v<true>(r, tables, hot, t, v, exact, ok);
         if (!ok) atomicAdd(&status->nonconverged, 1u);
     }
 }
 
-cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float *zp,
+cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float2 *hot,
+                                 const float *zp,
                                  const float *ze, uint64_t n, bool exact, float *out,
                                  RunStatus *status, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const uint64_t blocks = (n + 255) / 256;
     sample_losses_kernel<<<(unsigned)(blocks < 1u << 20 ? blocks : 1u << 20), 256, 0, s>>>(
-        recs, tables, zp, ze, n, exact, out, status);
+        recs, tables, hot, zp, ze, n, exact, out, status);
     return cudaGetLastError();
 }
 

@@ -177,12 +177,16 @@ __device__ __forceinline__ void sigmoid2(float lam, float &x, float &y) {
     y = e * x;
 }
 
-// quintic Hermite in v on the record's table
-__device__ __forceinline__ float lambda_table(const float2 *__restrict__ tab, float a, float b, float v) {
+// quintic Hermite in v on record `rec`'s table (hot rows for the centre)
+__device__ __forceinline__ float lambda_table(const float2 *__restrict__ tables,
+                                              const float2 *__restrict__ hot, uint64_t rec,
+                                              float a, float b, float v) {
     const float u = (fminf(fmaxf(v, kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
     const int i = min((int)u, kTabNodes - 2);
     const float t = u - (float)i;
-    const float2 n0 = __ldg(tab + i), n1 = __ldg(tab + i + 1);
+    const bool in_hot = (unsigned)(i - kHotJ0) < (unsigned)(kHotN - 1);
+    const float2 *row = in_hot ? hot + rec * kHotN + (i - kHotJ0) : tables + rec * kTabStride + i;
+    const float2 n0 = __ldg(row), n1 = __ldg(row + 1);
     const float v0 = fmaf((float)i, kTabH, kTabV0), v1 = v0 + kTabH;
     float x0, y0, x1, y1;
     sigmoid2(n0.x, x0, y0);
@@ -223,11 +227,12 @@ static __device__ __noinline__ float sample_exact64(float af, float bf, float mu
 // kernels without it are only launched when every record has a table.
 template <bool EX>
 __device__ __forceinline__ float sample_loss_from_v(const BetaRec &r, const float2 *__restrict__ tables,
-                                                    uint64_t rec, float v, bool exact, bool &ok) {
+                                                    const float2 *__restrict__ hot, uint64_t rec, float v,
+                                                    bool exact, bool &ok) {
     ok = true;
     if (r.mode == kModeDegenerate) return r.scale;               // G10
     if (!EX || (r.mode == kModeTable && !exact)) {
-        const float lam = lambda_table(tables + rec * kTabStride, r.a, r.b, v);
+        const float lam = lambda_table(tables, hot, rec, r.a, r.b, v);
         return r.scale * sigmoidf_(lam);
     }
     return sample_exact64(r.a, r.b, r.mu_l, r.sd_l, r.scale, v, ok);

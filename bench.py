@@ -208,7 +208,8 @@ def run_ours(args, cfg, rank, world, local):
     aragen.build_yet(cfg, first_trial=lo, n_trials=n_loc, out=ev_host.numpy().view(np.uint32))
     Y = ara.Yet(ctx, ev_host, fixed_len=K, first_trial=lo, n_trials=n_loc)
     ylt = torch.empty((L, n_loc), dtype=torch.float32, device=dev)
-    gathered = torch.empty((world, L, n_loc), dtype=torch.float32, device=dev) if world > 1 else None
+    # all-gather in concatenation form [P*L][N/P] == the [P][L][N/P] layout of ara_risk_measures
+    gathered = torch.empty((world * L, n_loc), dtype=torch.float32, device=dev) if world > 1 else None
     layers = list(range(L)) + ([-1] if L > 1 else [])
     ylt_host = torch.empty((L, n_loc), dtype=torch.float32).pin_memory()
 
@@ -231,6 +232,10 @@ def run_ours(args, cfg, rank, world, local):
             res.append(ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=world))
         return res
 
+    # exact number of present (occurrence, slot) pairs = SU samples per launch
+    _, cnt_dbg, _ = ara.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"], debug=True)
+    pairs = int(cnt_dbg.sum().item())
+    del cnt_dbg
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -280,7 +285,7 @@ def run_ours(args, cfg, rank, world, local):
     n_dev_recs = L * cfg["elts_per_layer"] * cfg["records_per_elt"]
     alg_bytes = n_loc * K * 4 + L * n_loc * 4 + cfg["catalog"] * 8 + n_dev_recs * rec_bytes
     hbm_achieved = alg_bytes / scan_avg / 1e9
-    samples = n_loc * K * L * cfg["elts_per_layer"] * cfg["records_per_elt"] / cfg["catalog"]
+    samples = pairs
     roof = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": hbm_achieved / hbm_peak, "traffic": None, "kernel": "scan_kernel",
             "kernel_ms": scan_avg * 1e3, "alg_bytes_per_launch": alg_bytes,
@@ -297,7 +302,8 @@ def run_ours(args, cfg, rank, world, local):
             inst = prof["thread_inst_per_sample"] * samples
             roof_alu.update(achieved=inst / scan_avg / 1e12, frac=inst / scan_avg / 1e12 / alu_peak,
                             inst_per_sample=prof["thread_inst_per_sample"],
-                            inst_source=prof.get("source"), traffic=prof.get("dram_bytes_per_launch"))
+                            inst_source=prof.get("source"),
+                            traffic=prof["dram_bytes_per_sample"] * samples if "dram_bytes_per_sample" in prof else None)
         else:
             roof_alu.update(achieved=None, frac=None, traffic=None)
         roof_alu["hbm"] = {k: roof[k] for k in ("achieved", "peak", "unit", "frac")}

@@ -36,9 +36,8 @@ def main():
         if a.measures:
             ara.risk_measures(ctx, ylt, cfg["n_layers"], cfg["n_trials"], 0, rps=cfg["return_periods"])
     torch.cuda.synchronize()
-    samples = cfg["n_trials"] * cfg["events_per_trial"] * cfg["n_layers"] * cfg["elts_per_layer"] * \
-        cfg["records_per_elt"] / cfg["catalog"]
-    print(f"trials={cfg['n_trials']} expected_samples={samples:.0f} ylt_mean={float(ylt.mean()):.6g}")
+    _, cnt, _ = ara.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"], debug=True)   # after the profiled launches
+    print(f"trials={cfg['n_trials']} present_pairs={int(cnt.sum().item())} ylt_mean={float(ylt.mean()):.6g}")
 
 
 if __name__ == "__main__":

@@ -62,6 +62,10 @@ struct ara_ctx {
     RunStatus *d_status = nullptr;
     RunStatus *h_status = nullptr;     // pinned
     MeasuresScratch ms;
+    uint2 *d_pairs = nullptr;          // split path scratch: per-trial present pairs
+    uint64_t pairs_capacity = 0;       // elements of d_pairs
+    uint32_t *d_counts = nullptr;      // split path scratch: pairs per trial
+    uint64_t counts_capacity = 0;
 };
 
 struct ara_portfolio {
@@ -81,6 +85,7 @@ struct ara_yet {
     uint32_t *d_events = nullptr;
     uint64_t *d_offsets = nullptr;
     uint32_t *d_redo = nullptr;        // trials to re-run with the fp64 kernel
+    uint64_t avg_len_x1000 = 0;        // mean events per trial x 1000
 };
 
 extern "C" {
@@ -136,6 +141,8 @@ void ara_ctx_destroy(ara_ctx *c) {
     cudaFree(c->ms.states);
     cudaFree(c->ms.part_sum);
     cudaFree(c->ms.part_cnt);
+    cudaFree(c->d_pairs);
+    cudaFree(c->d_counts);
     delete c;
 }
 
@@ -240,7 +247,7 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
 
     // event-major direct-access index: per event the slots with a record
     const uint32_t MW = (S + 31) / 32;
-    const uint32_t mwt = MW <= 1 ? 1 : (MW <= 3 ? 3 : 7);
+    const uint32_t mwt = MW <= 1 ? 1 : (MW <= 3 ? 3 : (MW <= 4 ? 4 : 7));
     const uint32_t stride = mwt == 1 ? 2 : (mwt == 3 ? 4 : 8);
     std::vector<uint32_t> index((size_t)C * stride, 0u);
     for (uint32_t s = 0; s < S; ++s) {
@@ -410,6 +417,7 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
     y->dev.n_trials = n_trials; y->dev.first_trial = first_trial;
     y->dev.fixed_len = toff ? 0u : fixed_len;
     y->dev.offsets = y->d_offsets; y->dev.events = y->d_events; y->dev.n_events = total;
+    y->avg_len_x1000 = n_trials ? (total * 1000) / n_trials : 0;
     *out = y;
     return ARA_OK;
 }
@@ -448,8 +456,35 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
     CU(cudaSetDevice(c->device));
     const bool exact = (flags & ARA_EXACT) != 0 && (flags & ARA_SU) != 0;
     CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
-    CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, nullptr, 0,
-                   y->d_redo, exact, c->stream, c->num_sms));
+    if (!exact) {
+        // split path: per-trial pair regions sized 2x the expected pairs per trial
+        // (+128); a trial that overflows its region goes to the fused kernel
+        const double per_occ = (double)p->dev.n_dev_records / (double)p->dev.catalog;
+        const double expect = per_occ * (double)y->avg_len_x1000 / 1000.0;
+        uint32_t cap = (uint32_t)((2.0 * expect + 128.0 + 31.0) / 32.0) * 32u;
+        if (cap > (1u << 20)) cap = 1u << 20;
+        const uint64_t need = y->dev.n_trials * (uint64_t)cap;
+        if (c->pairs_capacity < need) {          // scratch grows once, then is reused
+            cudaFree(c->d_pairs);
+            c->d_pairs = nullptr;
+            c->pairs_capacity = 0;
+            CU(dalloc(&c->d_pairs, need));
+            c->pairs_capacity = need;
+        }
+        if (c->counts_capacity < y->dev.n_trials) {
+            cudaFree(c->d_counts);
+            c->d_counts = nullptr;
+            c->counts_capacity = 0;
+            CU(dalloc(&c->d_counts, y->dev.n_trials));
+            c->counts_capacity = y->dev.n_trials;
+        }
+        SplitArgs S{p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status,
+                    c->d_pairs, cap, c->d_counts, y->d_redo};
+        CU(launch_split(S, c->stream, c->num_sms));
+    } else {
+        CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, nullptr, 0,
+                       y->d_redo, true, c->stream, c->num_sms));
+    }
     CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     if (c->h_status->n_redo && !c->h_status->bad_event) {
@@ -457,7 +492,7 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         const unsigned int n_redo = c->h_status->n_redo;
         CU(cudaMemsetAsync(&c->d_status->next_trial, 0, sizeof(unsigned long long), c->stream));
         CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, y->d_redo,
-                       n_redo, nullptr, true, c->stream, c->num_sms));
+                       n_redo, nullptr, (flags & ARA_SU) != 0, c->stream, c->num_sms));
         CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
     }

@@ -51,7 +51,7 @@ struct __align__(16) BetaRec {
 struct PortfolioDev {
     uint32_t catalog;
     uint32_t n_slots, n_layers;
-    uint32_t mask_words;      // 32-bit words of the per-event slot mask
+    uint32_t mask_words;      // kernel variant: 1, 3, 4 or 7 words of the per-event slot mask
     uint32_t idx_stride;      // uint32 words per event index entry (2, 4 or 8)
     uint32_t bitmap_shift;    // event e -> presence bit e >> shift
     uint32_t bitmap_words;
@@ -79,11 +79,32 @@ struct YetDev {
 // device-side status words
 struct RunStatus {
     unsigned long long next_trial;   // dynamic trial scheduler
+    unsigned long long next_trial2;  // ... of the second kernel of the split path
     unsigned int nonconverged;       // fp64 solves that did not converge
     unsigned int bad_event;          // occurrences with event id >= catalog
     unsigned int n_redo;             // trials touching a table-less record
     unsigned int pad;
 };
+
+// the split (two-kernel) scan: compact_kernel writes each trial's present
+// pairs {device record, (k << 8) | slot} to pairs[t * cap ...] and their count
+// to counts[t] (kOverflow if more than cap); sample_kernel consumes them
+constexpr uint32_t kOverflow = 0xffffffffu;
+struct SplitArgs {
+    PortfolioDev pf;
+    YetDev yet;
+    uint64_t seed;
+    uint32_t flags;
+    float *ylt;
+    uint32_t *dbg_count;
+    uint64_t *dbg_hash;
+    RunStatus *status;
+    uint2 *pairs;
+    uint32_t cap;
+    uint32_t *counts;
+    uint32_t *redo;
+};
+cudaError_t launch_split(const SplitArgs &A, cudaStream_t s, int num_sms);
 
 // kernels
 void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_t n,

@@ -151,13 +151,12 @@ void launch_prep_records(const ara_record *raw, const uint32_t *src, uint64_t n,
 #endif
 constexpr int kWarps = ARA_SCAN_WARPS;  // warps per CTA (1 CTA per SM)
 constexpr int kQCap = 256;          // pair queue capacity per warp (>= ARA_MAX_SLOTS)
-constexpr int kHCap = 64;           // hit list capacity per warp (processed at >= 32)
 static_assert(kQCap >= ARA_MAX_SLOTS, "queue must hold one occurrence's pairs");
 
 struct WarpBuf {
     uint2 q[kQCap];                 // {device record, (k << 8) | slot}
     float xs[kQCap];                // sampled loss per queued pair
-    uint2 hits[kHCap];              // {k, event}
+    uint32_t seg[kQCap];            // (occurrence, layer) segments: start | len << 16 | layer << 24
 };
 // followed per warp by: double S[L]; unsigned long long hsh[L]; unsigned cnt[L]
 
@@ -220,7 +219,6 @@ struct SampleArgs {
     RunStatus *status;
     uint64_t seed;
     bool exact;
-    bool dbg;
 };
 
 // one loss draw for queue entry e (Alg.1 lines 7-8); r already loaded
@@ -252,70 +250,103 @@ __device__ __forceinline__ float draw_one(const SampleArgs &G, const SlotInfo &s
 // table-less record was met (the trial must be redone).
 template <bool SU, bool EX>
 __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uint32_t trial_g, int lane,
-                                        int qn) {
+                                        int qn, int nseg) {
     WarpBuf &B = wbuf(M);
     const SlotInfo *slots = wslots(M);
     int redo = 0;
-    // sample, two pairs per lane in flight (Alg.1 lines 7-8)
-    for (int p0 = lane; p0 < qn; p0 += 64) {
-        const int p1 = p0 + 32;
-        const bool two = p1 < qn;
-        const uint2 e0 = B.q[p0];
-        const uint2 e1 = two ? B.q[p1] : e0;
-        float x0, x1;
-        if (SU) {
-            const BetaRec r0 = G.recs[e0.x];
-            const BetaRec r1 = G.recs[e1.x];
-            x0 = draw_one<EX>(G, slots[e0.y & 0xffu], r0, e0, trial_g, redo);
-            x1 = draw_one<EX>(G, slots[e1.y & 0xffu], r1, e1, trial_g, redo);
-        } else {
-            x0 = __ldg(G.rec_mu + e0.x);
-            x1 = __ldg(G.rec_mu + e1.x);
-            const SlotInfo &s0 = slots[e0.y & 0xffu], &s1 = slots[e1.y & 0xffu];
-            if (s0.has_terms) x0 = s0.share * fminf(fmaxf(x0 - s0.ret, 0.0f), s0.lim);
-            if (s1.has_terms) x1 = s1.share * fminf(fmaxf(x1 - s1.ret, 0.0f), s1.lim);
+    // sample, four pairs per lane in flight (Alg.1 lines 7-8): all record loads
+    // first, then the draws, then the table loads, then the interpolation
+    constexpr int U = 4;
+    for (int p0 = lane; p0 < qn; p0 += 32 * U) {
+        uint2 e[U];
+        bool live[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            live[u] = p0 + 32 * u < qn;
+            e[u] = B.q[live[u] ? p0 + 32 * u : p0];
         }
-        B.xs[p0] = x0;
-        if (two) B.xs[p1] = x1;
+        if (SU) {
+            BetaRec r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) r[u] = G.recs[e[u].x];
+            float v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const SlotInfo &si = slots[e[u].y & 0xffu];
+                const uint32_t k = e[u].y >> 8;
+                const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, G.seed);   // z_(Prog,E)
+                const uint32_t be = philox_lane0(trial_g, k, si.elt, 2u, G.seed);    // z_(E)
+                v[u] = combine_v(r[u], norm_quantile_from_bits(bp), norm_quantile_from_bits(be));
+            }
+            float2 n0[U], n1[U];
+            int ti[U];
+            float tt[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {       // table rows (hot centre / cold tails)
+                const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
+                ti[u] = min((int)uu, kTabNodes - 2);
+                tt[u] = uu - (float)ti[u];
+                const bool in_hot = (unsigned)(ti[u] - kHotJ0) < (unsigned)(kHotN - 1);
+                const float2 *row = in_hot ? G.hot + (uint64_t)e[u].x * kHotN + (ti[u] - kHotJ0)
+                                           : G.tables + (uint64_t)e[u].x * kTabStride + ti[u];
+                if (r[u].mode == kModeTable) { n0[u] = __ldg(row); n1[u] = __ldg(row + 1); }
+                else { n0[u] = make_float2(0.f, 0.f); n1[u] = n0[u]; }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float x;
+                if (r[u].mode == kModeDegenerate) {
+                    x = r[u].scale;
+                } else if (r[u].mode == kModeTable && !(EX && G.exact)) {
+                    x = r[u].scale * sigmoidf_(quintic_from_nodes(n0[u], n1[u], ti[u], tt[u], r[u].a, r[u].b));
+                } else if (!EX) {
+                    x = 0.0f;               // table-less record: this trial is redone by the fp64 kernel
+                    redo = 1;
+                } else {
+                    bool ok;
+                    x = sample_exact64(r[u].a, r[u].b, r[u].mu_l, r[u].sd_l, r[u].scale, v[u], ok);
+                    if (!ok) atomicAdd(&G.status->nonconverged, 1u);
+                }
+                const SlotInfo &si = slots[e[u].y & 0xffu];
+                if (si.has_terms) x = si.share * fminf(fmaxf(x - si.ret, 0.0f), si.lim);
+                if (live[u]) B.xs[p0 + 32 * u] = x;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float x = __ldg(G.rec_mu + e[u].x);
+                const SlotInfo &si = slots[e[u].y & 0xffu];
+                if (si.has_terms) x = si.share * fminf(fmaxf(x - si.ret, 0.0f), si.lim);
+                if (live[u]) B.xs[p0 + 32 * u] = x;
+            }
+        }
     }
     __syncwarp();
-    // segments = runs of equal (occurrence, layer): sum (line 9), occurrence
-    // terms (line 11), add to the layer's trial sum
+    // segments = (occurrence, layer) runs recorded at enqueue: sum (line 9),
+    // occurrence terms (line 11), add to the layer's trial sum
     const LayerInfo *layers = wlayers(M);
     double *S = wS(M);
-    for (int base = 0; base < qn; base += 32) {
-        const int p = base + lane;
-        bool head = false;
+    for (int base = 0; base < nseg; base += 32) {
+        const int sidx = base + lane;
+        const bool have = sidx < nseg;
         uint32_t layer = 0;
         double g = 0.0;
-        if (p < qn) {
-            const uint2 e = B.q[p];
-            layer = slots[e.y & 0xffu].layer;
-            const uint32_t key = (e.y & 0xffffff00u) | layer;
-            if (p == 0) {
-                head = true;
-            } else {
-                const uint2 ep = B.q[p - 1];
-                head = ((ep.y & 0xffffff00u) | slots[ep.y & 0xffu].layer) != key;
-            }
-            if (head) {
-                double l = 0.0;
-                for (int r = p; r < qn; ++r) {
-                    const uint2 er = B.q[r];
-                    if (((er.y & 0xffffff00u) | slots[er.y & 0xffu].layer) != key) break;
-                    l += (double)B.xs[r];
-                }
-                const LayerInfo &L = layers[layer];
-                g = fmin(fmax(l - L.occ_r, 0.0), L.occ_l);
-            }
+        if (have) {
+            const uint32_t d = B.seg[sidx];
+            const int st = (int)(d & 0xffffu), len = (int)((d >> 16) & 0xffu);
+            layer = d >> 24;
+            double l = 0.0;
+            for (int r = 0; r < len; ++r) l += (double)B.xs[st + r];
+            const LayerInfo &L = layers[layer];
+            g = fmin(fmax(l - L.occ_r, 0.0), L.occ_l);
         }
         // deterministic per-layer reduction: one fixed-tree warp sum per
-        // distinct layer among this round's segment heads
-        unsigned pending = __ballot_sync(0xffffffffu, head);
+        // distinct layer among this round's segments
+        unsigned pending = __ballot_sync(0xffffffffu, have);
         while (pending) {
             const int leader = __ffs(pending) - 1;
             const uint32_t lay = __shfl_sync(0xffffffffu, layer, leader);
-            const bool mine = head && layer == lay;
+            const bool mine = have && layer == lay;
             const double sum = warp_sum_f64(mine ? g : 0.0);
             if (lane == 0) S[lay] += sum;
             pending &= ~__ballot_sync(0xffffffffu, mine);
@@ -347,77 +378,142 @@ __device__ __forceinline__ void load_index(const uint32_t *index, uint32_t strid
     }
 }
 
-// Index lookups (Alg.1 line 6) for the warp's <= 64 hits, two per lane in
-// flight, then enqueue all present (occurrence, slot) pairs, whole
-// occurrences at a time, flushing when the queue would overflow.  Out of line.
-// Returns the new queue length, | 0x10000 if a table-less record was met.
-template <bool SU, bool EX, int MW>
-__device__ __noinline__ int process_hits(const SampleArgs G, const WarpMem M, const uint32_t *index,
-                                         uint32_t stride, uint32_t trial_g, int lane, int nh, int qn) {
+// Index lookups (Alg.1 line 6) for the warp's hits, 64 at a time (two per
+// lane in flight), then enqueue the present (occurrence, slot) pairs and their
+// (occurrence, layer) segments, whole occurrences at a time, flushing when the
+// queue would overflow.  Out of line.  q packs (qn, nseg, redo) as
+// qn | nseg << 12 | redo << 24 in and out.
+template <int MW>
+__device__ __forceinline__ void count_occ(const SlotInfo *slots, const uint32_t (&mask)[MW], uint32_t &np,
+                                         uint32_t &ns) {
+    np = 0; ns = 0;
+    uint32_t prev = 0xffffffffu;
+#pragma unroll
+    for (int w = 0; w < MW; ++w) {
+        uint32_t mw = mask[w];
+        np += __popc(mw);
+        while (mw) {
+            const uint32_t lay = slots[w * 32 + __ffs(mw) - 1].layer;
+            mw &= mw - 1;
+            ns += lay != prev;
+            prev = lay;
+        }
+    }
+}
+
+template <int MW, bool DBG>
+__device__ __forceinline__ void write_occ(const SampleArgs &G, const WarpMem &M, WarpBuf &B,
+                                          const SlotInfo *slots, uint32_t k, uint32_t rec,
+                                          const uint32_t (&mask)[MW], uint32_t pos, uint32_t spos) {
+    uint32_t prev = 0xffffffffu, sstart = pos;
+#pragma unroll
+    for (int w = 0; w < MW; ++w) {
+        uint32_t mw = mask[w];
+        while (mw) {
+            const uint32_t slot = (uint32_t)(w * 32 + __ffs(mw) - 1);
+            mw &= mw - 1;
+            const uint32_t lay = slots[slot].layer;
+            if (lay != prev) {
+                if (prev != 0xffffffffu) B.seg[spos++] = sstart | ((pos - sstart) << 16) | (prev << 24);
+                sstart = pos;
+                prev = lay;
+            }
+            B.q[pos++] = make_uint2(rec, (k << 8) | slot);
+            if (DBG) {
+                atomicAdd(&wcnt(M)[lay], 1u);
+                const uint64_t hv = splitmix64(splitmix64(splitmix64((uint64_t)k) ^ slots[slot].elt) ^ G.rec_orig[rec]);
+                atomicAdd(&whsh(M)[lay], (unsigned long long)hv);
+            }
+            ++rec;
+        }
+    }
+    if (prev != 0xffffffffu) B.seg[spos] = sstart | ((pos - sstart) << 16) | (prev << 24);
+}
+
+// Enqueue the present (occurrence, slot) pairs of a 128-event chunk: each
+// lane holds <= 4 occurrences (index entries already loaded, Alg.1 line 6).
+// One packed prefix sum (pairs low, segments high) places every pair and
+// (occurrence, layer) segment; if the queue would overflow it is flushed
+// first, and a chunk that alone exceeds the queue goes occurrence group by
+// group.  q packs (qn, nseg, redo) as qn | nseg << 12 | redo << 24.
+template <bool SU, bool EX, int MW, bool DBG>
+__device__ __forceinline__ int enqueue_chunk(const SampleArgs G, const WarpMem M, uint32_t trial_g, int lane,
+                                          int q, uint32_t k0, uint32_t hitbits,
+                                          const uint4 first4, const uint32_t (&mask)[4][MW]) {
     WarpBuf &B = wbuf(M);
     const SlotInfo *slots = wslots(M);
-    uint32_t kk[2], first[2], mask[2][MW], cnt[2];
+    int qn = q & 0xfff, nseg = (q >> 12) & 0xfff, redo = q >> 24;
+    const uint32_t first[4] = {first4.x, first4.y, first4.z, first4.w};
+    uint32_t np[4], ns[4];
+    uint32_t mine = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int i = lane + 32 * h;
-        const uint2 a = i < nh ? B.hits[i] : make_uint2(0, 0);
-        kk[h] = a.x;
-        first[h] = 0;
-#pragma unroll
-        for (int w = 0; w < MW; ++w) mask[h][w] = 0u;
-        if (i < nh) load_index<MW>(index, stride, a.y, first[h], mask[h]);
+    for (int h = 0; h < 4; ++h) {
+        np[h] = 0; ns[h] = 0;
+        if ((hitbits >> h) & 1u) count_occ<MW>(slots, mask[h], np[h], ns[h]);
+        mine += np[h] | (ns[h] << 16);
     }
-    __syncwarp();
-    int redo = 0;
+    uint32_t incl = mine;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        cnt[h] = 0;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    if ((int)(tot & 0xffffu) > kQCap - qn && (int)(tot & 0xffffu) <= kQCap) {   // make room
+        redo |= flush_queue<SU, EX>(G, M, trial_g, lane, qn, nseg);
+        qn = 0; nseg = 0;
+    }
+    if ((int)(tot & 0xffffu) <= kQCap - qn) {                 // common case: the chunk fits
+        const uint32_t ex = incl - mine;
+        uint32_t pos = (uint32_t)qn + (ex & 0xffffu), spos = (uint32_t)nseg + (ex >> 16);
 #pragma unroll
-        for (int w = 0; w < MW; ++w) cnt[h] += __popc(mask[h][w]);
-        bool todo = cnt[h] > 0;
+        for (int h = 0; h < 4; ++h) {
+            if (np[h]) write_occ<MW, DBG>(G, M, B, slots, k0 + h, first[h], mask[h], pos, spos);
+            pos += np[h];
+            spos += ns[h];
+        }
+        qn += (int)(tot & 0xffffu);
+        nseg += (int)(tot >> 16);
+        __syncwarp();
+        return qn | (nseg << 12) | (redo << 24);
+    }
+    // a chunk with more pairs than the queue: occurrence group by group
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        bool todo = np[h] > 0;
         while (__any_sync(0xffffffffu, todo)) {
-            uint32_t incl = todo ? cnt[h] : 0u;
+            const uint32_t m2 = todo ? (np[h] | (ns[h] << 16)) : 0u;
+            uint32_t inc2 = m2;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc2, o);
+                if (lane >= o) inc2 += y;
             }
-            const bool fits = todo && incl <= (uint32_t)(kQCap - qn);
+            const bool fits = todo && (inc2 & 0xffffu) <= (uint32_t)(kQCap - qn);
             if (fits) {
-                uint32_t pos = (uint32_t)qn + incl - cnt[h];
-                uint32_t rec = first[h];
-#pragma unroll
-                for (int w = 0; w < MW; ++w) {
-                    uint32_t mw = mask[h][w];
-                    while (mw) {
-                        const uint32_t slot = (uint32_t)(w * 32 + __ffs(mw) - 1);
-                        mw &= mw - 1;
-                        B.q[pos++] = make_uint2(rec, (kk[h] << 8) | slot);
-                        if (G.dbg) {
-                            const uint32_t lay = slots[slot].layer;
-                            atomicAdd(&wcnt(M)[lay], 1u);
-                            const uint64_t hv = splitmix64(splitmix64(splitmix64((uint64_t)kk[h]) ^ slots[slot].elt) ^
-                                                           G.rec_orig[rec]);
-                            atomicAdd(&whsh(M)[lay], (unsigned long long)hv);
-                        }
-                        ++rec;
-                    }
-                }
+                const uint32_t ex = inc2 - m2;
+                write_occ<MW, DBG>(G, M, B, slots, k0 + h, first[h], mask[h], (uint32_t)qn + (ex & 0xffffu),
+                                   (uint32_t)nseg + (ex >> 16));
                 todo = false;
             }
             const unsigned fitmask = __ballot_sync(0xffffffffu, fits);
-            if (fitmask) qn += (int)__shfl_sync(0xffffffffu, incl, 31 - __clz(fitmask));
+            if (fitmask) {
+                const uint32_t last = __shfl_sync(0xffffffffu, inc2, 31 - __clz(fitmask));
+                qn += (int)(last & 0xffffu);
+                nseg += (int)(last >> 16);
+            }
             __syncwarp();
             if (__any_sync(0xffffffffu, todo)) {
-                redo |= flush_queue<SU, EX>(G, M, trial_g, lane, qn);
+                redo |= flush_queue<SU, EX>(G, M, trial_g, lane, qn, nseg);
                 qn = 0;
+                nseg = 0;
             }
         }
     }
-    return qn | (redo << 16);
+    return qn | (nseg << 12) | (redo << 24);
 }
 
-template <bool SU, bool EX, int MW>
+template <bool SU, bool EX, int MW, bool DBG>
 __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_constant__ ScanArgs A) {
     const uint32_t nl = A.pf.n_layers;
     const uint32_t per_warp = (uint32_t)((sizeof(WarpBuf) + nl * (sizeof(double) + sizeof(unsigned long long) +
@@ -447,9 +543,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
     double *S = wS(M);
     unsigned long long *hsh = whsh(M);
     unsigned int *cntv = wcnt(M);
-    const bool dbg = (A.flags & ARA_DEBUG_LOOKUP) != 0;
+    const bool dbg = DBG;
     const SampleArgs G{A.pf.recs, A.pf.tables, A.pf.hot, A.pf.rec_mu, A.pf.rec_orig, A.status, A.seed,
-                       (A.flags & ARA_EXACT) != 0, dbg};
+                       (A.flags & ARA_EXACT) != 0};
     const uint64_t n_trials = A.yet.n_trials;
     const uint64_t n_work = A.trial_list ? A.n_list : n_trials;
     const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift;
@@ -468,7 +564,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
         const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);        // global trial index i
         for (uint32_t l = lane; l < nl; l += 32) { S[l] = 0.0; cntv[l] = 0u; hsh[l] = 0ull; }
         __syncwarp();
-        int qn = 0, nh = 0, redo = 0;
+        int q = 0;                         // packed queue state (qn, nseg, redo)
         const uint32_t *ev = A.yet.events + base;
         const bool vec = (base & 3u) == 0;
         uint4 nxt = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
@@ -482,74 +578,69 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
                 if (k + 3 < len) nxt.w = __ldcs(ev + k + 3);
             }
         }
-        for (uint32_t c = 0; c < len; c += 128) {                   // Alg.1 line 4
-            const uint4 cur = nxt;
-            {   // prefetch the next chunk
-                const uint32_t k = c + 128 + 4u * lane;
-                nxt = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-                if (vec && k + 3 < len) nxt = __ldcs(reinterpret_cast<const uint4 *>(ev + k));
-                else if (k < len) {
-                    nxt.x = __ldcs(ev + k);
-                    if (k + 1 < len) nxt.y = __ldcs(ev + k + 1);
-                    if (k + 2 < len) nxt.z = __ldcs(ev + k + 2);
-                    if (k + 3 < len) nxt.w = __ldcs(ev + k + 3);
-                }
-            }
-            // presence bitmap (shared memory) for this lane's 4 occurrences
-            const uint32_t k0 = c + 4u * lane;
-            const uint32_t ee[4] = {cur.x, cur.y, cur.z, cur.w};
-            uint32_t hitbits = 0;
+        // software pipeline over 128-event chunks: events of chunk c+2 in flight
+        // (HBM), index entries of chunk c+1 in flight (L2), pairs of chunk c enqueued
+        uint32_t hit_c = 0, k0_c = 0;
+        uint4 first_c = make_uint4(0, 0, 0, 0);
+        uint32_t mask_c[4][MW];
 #pragma unroll
-            for (int qd = 0; qd < 4; ++qd) {
-                const uint32_t e = ee[qd];
-                if (k0 + qd < len) {
-                    if (e >= C) {
-                        atomicAdd(&A.status->bad_event, 1u);
-                    } else {
-                        const uint32_t bit = e >> shift;
-                        hitbits |= ((bitmap[bit >> 5] >> (bit & 31)) & 1u) << qd;
+        for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+            for (int w = 0; w < MW; ++w) mask_c[qd][w] = 0u;
+        for (uint32_t c = 0; c < len + 128; c += 128) {             // Alg.1 line 4
+            uint32_t hit_n = 0, k0_n = c + 4u * lane;
+            uint4 first_n = make_uint4(0, 0, 0, 0);
+            uint32_t mask_n[4][MW];
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+                for (int w = 0; w < MW; ++w) mask_n[qd][w] = 0u;
+            if (c < len) {
+                const uint4 cur = nxt;
+                {   // prefetch the next chunk's events
+                    const uint32_t k = c + 128 + 4u * lane;
+                    nxt = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                    if (vec && k + 3 < len) nxt = __ldcs(reinterpret_cast<const uint4 *>(ev + k));
+                    else if (k < len) {
+                        nxt.x = __ldcs(ev + k);
+                        if (k + 1 < len) nxt.y = __ldcs(ev + k + 1);
+                        if (k + 2 < len) nxt.z = __ldcs(ev + k + 2);
+                        if (k + 3 < len) nxt.w = __ldcs(ev + k + 3);
                     }
                 }
-            }
-            // one warp prefix sum per chunk; hits appended in (lane, qd) order
-            const uint32_t nmine = __popc(hitbits);
-            uint32_t incl = nmine;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-            uint32_t pos = incl - nmine;                // position among this chunk's hits
-            // the chunk's hits are written in slices of <= 64 - nh so the list never overflows
-            uint32_t done = 0;
-            while (done < total) {
-                const uint32_t room = (uint32_t)(kHCap - nh);
-                const uint32_t take = min(room, total - done);
+                // presence bitmap (shared memory) for this lane's 4 occurrences
+                const uint32_t ee[4] = {cur.x, cur.y, cur.z, cur.w};
 #pragma unroll
                 for (int qd = 0; qd < 4; ++qd) {
-                    if ((hitbits >> qd) & 1u) {
-                        if (pos >= done && pos < done + take)
-                            B.hits[nh + (pos - done)] = make_uint2(k0 + qd, ee[qd]);
-                        ++pos;
+                    const uint32_t e = ee[qd];
+                    if (k0_n + qd < len) {
+                        if (e >= C) {
+                            atomicAdd(&A.status->bad_event, 1u);
+                        } else {
+                            const uint32_t bit = e >> shift;
+                            hit_n |= ((bitmap[bit >> 5] >> (bit & 31)) & 1u) << qd;
+                        }
                     }
                 }
-                pos = incl - nmine;
-                nh += (int)take;
-                done += take;
-                if (nh >= 32) {                          // index lookups + enqueue (line 6)
-                    __syncwarp();
-                    const int r = process_hits<SU, EX, MW>(G, M, index, stride, trial_g, lane, nh, qn);
-                    qn = r & 0xffff; redo |= r >> 16; nh = 0;
+                // index entries of this lane's hits: issued now, consumed next iteration
+#pragma unroll
+                for (int qd = 0; qd < 4; ++qd) {
+                    uint32_t f = 0;
+                    if ((hit_n >> qd) & 1u) load_index<MW>(index, stride, ee[qd], f, mask_n[qd]);
+                    if (qd == 0) first_n.x = f; else if (qd == 1) first_n.y = f; else if (qd == 2) first_n.z = f; else first_n.w = f;
                 }
             }
+            if (__any_sync(0xffffffffu, hit_c != 0))
+                q = enqueue_chunk<SU, EX, MW, DBG>(G, M, trial_g, lane, q, k0_c, hit_c, first_c, mask_c);
+            hit_c = hit_n; k0_c = k0_n; first_c = first_n;
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+                for (int w = 0; w < MW; ++w) mask_c[qd][w] = mask_n[qd][w];
         }
         __syncwarp();
-        if (nh) {
-            const int r = process_hits<SU, EX, MW>(G, M, index, stride, trial_g, lane, nh, qn);
-            qn = r & 0xffff; redo |= r >> 16;
-        }
-        if (qn) redo |= flush_queue<SU, EX>(G, M, trial_g, lane, qn);
+        int redo = q >> 24;
+        if (q & 0xfff) redo |= flush_queue<SU, EX>(G, M, trial_g, lane, q & 0xfff, (q >> 12) & 0xfff);
         if (!EX && redo) {
             if (lane == 0) A.redo[atomicAdd(&A.status->n_redo, 1u)] = (uint32_t)t;
         }
@@ -579,7 +670,7 @@ size_t scan_smem_for(const PortfolioDev &pf) { return scan_smem_bytes(pf); }
 template <bool SU, bool EX, int MW>
 static cudaError_t launch_scan_t(const ScanArgs &A, cudaStream_t s, int num_sms) {
     const size_t smem = scan_smem_bytes(A.pf);
-    auto kern = scan_kernel<SU, EX, MW>;
+    auto kern = (A.flags & ARA_DEBUG_LOOKUP) ? scan_kernel<SU, EX, MW, true> : scan_kernel<SU, EX, MW, false>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     int per_sm = 0;
@@ -607,6 +698,7 @@ cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed
     if (trial_list && n_list == 0) return cudaSuccess;
     if (pf.mask_words == 1) return launch_scan_mw<1>(A, exact_kernel, s, num_sms);
     if (pf.mask_words <= 3) return launch_scan_mw<3>(A, exact_kernel, s, num_sms);
+    if (pf.mask_words == 4) return launch_scan_mw<4>(A, exact_kernel, s, num_sms);
     return launch_scan_mw<7>(A, exact_kernel, s, num_sms);
 }
 

@@ -177,16 +177,9 @@ __device__ __forceinline__ void sigmoid2(float lam, float &x, float &y) {
     y = e * x;
 }
 
-// quintic Hermite in v on record `rec`'s table (hot rows for the centre)
-__device__ __forceinline__ float lambda_table(const float2 *__restrict__ tables,
-                                              const float2 *__restrict__ hot, uint64_t rec,
-                                              float a, float b, float v) {
-    const float u = (fminf(fmaxf(v, kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
-    const int i = min((int)u, kTabNodes - 2);
-    const float t = u - (float)i;
-    const bool in_hot = (unsigned)(i - kHotJ0) < (unsigned)(kHotN - 1);
-    const float2 *row = in_hot ? hot + rec * kHotN + (i - kHotJ0) : tables + rec * kTabStride + i;
-    const float2 n0 = __ldg(row), n1 = __ldg(row + 1);
+// quintic Hermite on [v_i, v_i + h] from the two nodes' (lambda, lambda'),
+// lambda'' from the ODE at each node; t in [0,1]
+__device__ __forceinline__ float quintic_from_nodes(float2 n0, float2 n1, int i, float t, float a, float b) {
     const float v0 = fmaf((float)i, kTabH, kTabV0), v1 = v0 + kTabH;
     float x0, y0, x1, y1;
     sigmoid2(n0.x, x0, y0);
@@ -208,6 +201,18 @@ __device__ __forceinline__ float lambda_table(const float2 *__restrict__ tables,
     lam = fmaf(h20 * H2, s0, lam);
     lam = fmaf(h21 * H2, s1, lam);
     return lam;
+}
+
+// quintic Hermite in v on record `rec`'s table (hot rows for the centre)
+__device__ __forceinline__ float lambda_table(const float2 *__restrict__ tables,
+                                              const float2 *__restrict__ hot, uint64_t rec,
+                                              float a, float b, float v) {
+    const float u = (fminf(fmaxf(v, kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
+    const int i = min((int)u, kTabNodes - 2);
+    const float t = u - (float)i;
+    const bool in_hot = (unsigned)(i - kHotJ0) < (unsigned)(kHotN - 1);
+    const float2 *row = in_hot ? hot + rec * kHotN + (i - kHotJ0) : tables + rec * kTabStride + i;
+    return quintic_from_nodes(__ldg(row), __ldg(row + 1), i, t, a, b);
 }
 
 __device__ __forceinline__ float sigmoidf_(float lam) { return __frcp_rn(1.0f + __expf(-lam)); }

@@ -251,6 +251,29 @@ def test_shared_elts_and_xelt_terms(A, ctx):
         ylt_check(g[li], ref, li)
 
 
+def test_pair_region_overflow_goes_to_fused_kernel(A, ctx):
+    # a trial whose present pairs exceed its region (2x expected + 128) is redone
+    # by the fused kernel; counts/hashes/YLT stay exact
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 50
+    pf = aragen.build_portfolio(cfg)
+    yet = aragen.build_yet(cfg)
+    R = cfg["records_per_elt"]
+    both = np.intersect1d(pf["rec_event"][:R], pf["rec_event"][R:2 * R])
+    assert both.size > 50
+    rng = np.random.default_rng(4)
+    heavy = rng.choice(both, 400).astype(np.uint32)            # 800 pairs in one trial
+    K = cfg["events_per_trial"]
+    ev = np.concatenate([yet["events"][:10 * K], heavy, yet["events"][10 * K:]])
+    # trials 0-9 as generated, trial 10 = the 400 heavy events, trials 11-50 as generated
+    off = np.concatenate([np.arange(11, dtype=np.uint64) * K, 10 * K + 400 + np.arange(0, 41, dtype=np.uint64) * K])
+    y2 = {"trial_off": off, "events": ev, "first_trial": 0}
+    (g, cnt, hsh), ref = run_both(A, ctx, pf, y2, cfg["seed"])
+    assert cnt[0, 10] == 800
+    assert np.array_equal(cnt, ref["count"]) and np.array_equal(hsh, ref["hash"])
+    ylt_check(g, ref)
+
+
 def test_determinism_and_sharding(A, ctx):
     cfg = aragen.load_config("cfg1")
     pf = aragen.build_portfolio(cfg)

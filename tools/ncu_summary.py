@@ -66,7 +66,11 @@ def main():
                 sel[k] = {"value": v, "unit": u}
     stalls = {h: v for h, (v, u) in kern.items() if "average_warps_issue_stalled" in h and h.endswith("ratio")
               and (to_float(v) or 0) > 0.1}
-    t_inst = to_float(sel["smsp__thread_inst_executed.sum"]["value"])
+    inst = to_float(sel["smsp__inst_executed.sum"]["value"])
+    if "smsp__thread_inst_executed.sum" in sel:
+        t_inst = to_float(sel["smsp__thread_inst_executed.sum"]["value"])
+    else:   # the full set has the per-instruction thread ratio instead
+        t_inst = inst * to_float(sel["smsp__thread_inst_executed_per_inst_executed.ratio"]["value"])
     dur_unit = sel["gpu__time_duration.sum"]["unit"]
     dur = to_float(sel["gpu__time_duration.sum"]["value"]) * {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0}[dur_unit]
     def bytes_of(k):

@@ -173,7 +173,7 @@ __device__ __forceinline__ double lambda_exact64(double v, double a, double b, d
 __device__ __forceinline__ void sigmoid2(float lam, float &x, float &y) {
     const float l = fminf(fmaxf(lam, -80.0f), 80.0f);
     const float e = __expf(-l);
-    x = __frcp_rn(1.0f + e);
+    x = __fdividef(1.0f, 1.0f + e);                      // MUFU.RCP (2 ulp)
     y = e * x;
 }
 
@@ -215,7 +215,11 @@ __device__ __forceinline__ float lambda_table(const float2 *__restrict__ tables,
     return quintic_from_nodes(__ldg(row), __ldg(row + 1), i, t, a, b);
 }
 
-__device__ __forceinline__ float sigmoidf_(float lam) { return __frcp_rn(1.0f + __expf(-lam)); }
+__device__ __forceinline__ float sigmoidf_(float lam) {
+    // 1/(1+e^-lam); e^-lam = inf for lam < -88 gives 0 (the loss underflows to 0)
+    const float e = __expf(-lam);
+    return e < 3.0e38f ? __fdividef(1.0f, 1.0f + e) : 0.0f;
+}
 
 // Per-sample fp64 solve (table-less records, ARA_EXACT); kept out of line so
 // its register demand does not constrain the hot path.

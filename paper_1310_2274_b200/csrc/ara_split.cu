@@ -20,6 +20,13 @@
 #include "ara_internal.cuh"
 #include "ara_sampler.cuh"
 
+#ifndef ARA_COMPACT_COMBINED
+#define ARA_COMPACT_COMBINED 0
+#endif
+#ifndef ARA_SEG_EARLY_EXIT
+#define ARA_SEG_EARLY_EXIT 0
+#endif
+
 namespace ara {
 
 namespace {
@@ -139,18 +146,36 @@ __global__ void __launch_bounds__(kCompactWarps * 32, 1)
                 if (lane >= o) incl += y;
             }
             uint32_t pos = n + incl - np;
+            if (MW == 1 && ARA_COMPACT_COMBINED) {
+                // one loop over the set bits of all four occurrences, in
+                // (occurrence, slot) order: trip count = this lane's pairs
+                uint32_t m0 = mask[0][0], m1 = mask[1][0], m2 = mask[2][0], m3 = mask[3][0];
+                uint32_t r0 = first[0], r1 = first[1], r2 = first[2], r3 = first[3];
+                while (m0 | m1 | m2 | m3) {
+                    const int qd = m0 ? 0 : (m1 ? 1 : (m2 ? 2 : 3));
+                    const uint32_t mw = qd == 0 ? m0 : (qd == 1 ? m1 : (qd == 2 ? m2 : m3));
+                    const uint32_t rec = qd == 0 ? r0 : (qd == 1 ? r1 : (qd == 2 ? r2 : r3));
+                    const uint32_t slot = (uint32_t)(__ffs(mw) - 1);
+                    if (pos < cap) out[pos] = make_uint2(rec, ((k0 + qd) << 8) | slot);
+                    ++pos;
+                    const uint32_t mn = mw & (mw - 1);
+                    if (qd == 0) { m0 = mn; ++r0; } else if (qd == 1) { m1 = mn; ++r1; }
+                    else if (qd == 2) { m2 = mn; ++r2; } else { m3 = mn; ++r3; }
+                }
+            } else {
 #pragma unroll
-            for (int qd = 0; qd < 4; ++qd) {
-                uint32_t rec = first[qd];
+                for (int qd = 0; qd < 4; ++qd) {
+                    uint32_t rec = first[qd];
 #pragma unroll
-                for (int w = 0; w < MW; ++w) {
-                    uint32_t mw = mask[qd][w];
-                    while (mw) {
-                        const uint32_t slot = (uint32_t)(w * 32 + __ffs(mw) - 1);
-                        mw &= mw - 1;
-                        if (pos < cap) out[pos] = make_uint2(rec, ((k0 + qd) << 8) | slot);
-                        ++pos;
-                        ++rec;
+                    for (int w = 0; w < MW; ++w) {
+                        uint32_t mw = mask[qd][w];
+                        while (mw) {
+                            const uint32_t slot = (uint32_t)(w * 32 + __ffs(mw) - 1);
+                            mw &= mw - 1;
+                            if (pos < cap) out[pos] = make_uint2(rec, ((k0 + qd) << 8) | slot);
+                            ++pos;
+                            ++rec;
+                        }
                     }
                 }
             }
@@ -173,7 +198,7 @@ __global__ void __launch_bounds__(kCompactWarps * 32, 1)
 // end); otherwise per-layer sums in shared memory via fixed-tree reductions.
 // ---------------------------------------------------------------------------
 template <bool SU, bool SL, bool DBG>
-__global__ void __launch_bounds__(kSampleWarps * 32)
+__global__ void __launch_bounds__(kSampleWarps * 32, 2)   // 2 CTAs/SM: <= 64 registers
     sample_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     SlotInfo *slots = reinterpret_cast<SlotInfo *>(smem);
@@ -282,24 +307,33 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
                     }
                     ckey = 0xffffffffu;
                 }
-                double val = live[u] ? (double)x[u] : 0.0;
-                if (lane == 0 && key == ckey) val += csum;
+                // fp32 within an occurrence (<= one value per slot); the carry and
+                // the trial sums stay fp64.  Segments are short, so the scan stops
+                // as soon as no lane's segment reaches further back.
+                float val = live[u] ? x[u] : 0.0f;
+                double carry = (lane == 0 && key == ckey) ? csum : 0.0;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    const double y = __shfl_up_sync(0xffffffffu, val, o);
+                    const float y = __shfl_up_sync(0xffffffffu, val, o);
                     const uint32_t ky = __shfl_up_sync(0xffffffffu, key, o);
-                    if (lane >= o && ky == key) val += y;
+                    const bool same = lane >= o && ky == key;
+                    if (same) val += y;
+                    if (ARA_SEG_EARLY_EXIT && !__any_sync(0xffffffffu, same)) break;
                 }
+                // the carried part reaches every lane of the first segment
+                carry = __shfl_sync(0xffffffffu, carry, 0);
+                const bool in_first = key == key0 && key0 == ckey;
+                const double full = (double)val + (in_first ? carry : 0.0);
                 const uint32_t nextkey = __shfl_down_sync(0xffffffffu, key, 1);
                 // lane 31's segment may continue into the next sub-round: carry it
                 const bool tail = live[u] && lane != 31 && nextkey != key;
                 const bool l31 = __shfl_sync(0xffffffffu, (int)live[u], 31) != 0;
                 ckey = l31 ? __shfl_sync(0xffffffffu, key, 31) : 0xffffffffu;
-                csum = __shfl_sync(0xffffffffu, val, 31);
+                csum = __shfl_sync(0xffffffffu, full, 31);
                 double g = 0.0;
                 if (tail) {                                           // occurrence terms (line 11)
                     const LayerInfo &L = layers[layer];
-                    g = fmin(fmax(val - L.occ_r, 0.0), L.occ_l);
+                    g = fmin(fmax(full - L.occ_r, 0.0), L.occ_l);
                     if (SL) acc += g;
                 }
                 if (!SL) {

@@ -36,7 +36,7 @@ sys.path.insert(0, ROOT)
 import aragen  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-PROFILE_CONST = os.path.join(ROOT, "profiles", "scan_inst_per_sample.json")
+PROFILE_CONST = os.path.join(ROOT, "profiles", "roofline_consts.json")
 
 
 def parse():
@@ -214,6 +214,7 @@ def run_ours(args, cfg, rank, world, local):
     ylt_host = torch.empty((L, n_loc), dtype=torch.float32).pin_memory()
 
     scan_ms = []
+    kern_ms = []          # per-kernel CUDA-event times of each timed ara_run (ara_last_run_timings)
 
     def step(timed_scan=False):
         if timed_scan:
@@ -223,6 +224,7 @@ def run_ours(args, cfg, rank, world, local):
         if timed_scan:
             e1.record(stream)
             scan_ms.append((e0, e1))
+            kern_ms.append(ara.last_run_timings(ctx))
         src = ylt
         if world > 1:
             dist.all_gather_into_tensor(gathered, ylt)
@@ -278,36 +280,52 @@ def run_ours(args, cfg, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_elapsed = float(t[0])
 
-    # ---- roofline of the dominant kernel (the fused scan)
+    # ---- roofline of the dominant kernel, live per-kernel times (CUDA events on the
+    # context stream, recorded by ara_run around each kernel)
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    rec_bytes = 32
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
+    t_compact = sum(k["compact_ms"] for k in kern_ms) / len(kern_ms) / 1e3
+    t_sample = sum(k["sample_ms"] for k in kern_ms) / len(kern_ms) / 1e3
+    t_redo = sum(k["redo_ms"] for k in kern_ms) / len(kern_ms) / 1e3
     n_dev_recs = L * cfg["elts_per_layer"] * cfg["records_per_elt"]
-    alg_bytes = n_loc * K * 4 + L * n_loc * 4 + cfg["catalog"] * 8 + n_dev_recs * rec_bytes
-    hbm_achieved = alg_bytes / scan_avg / 1e9
-    samples = pairs
-    roof = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
-            "frac": hbm_achieved / hbm_peak, "traffic": None, "kernel": "scan_kernel",
-            "kernel_ms": scan_avg * 1e3, "alg_bytes_per_launch": alg_bytes,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+    # algorithmic bytes of the path: the YET once (4 B per occurrence), the YLT once,
+    # the portfolio tables once (index 8 B/event + 32 B record + 128 B hot table per record)
+    alg_bytes = n_loc * K * 4 + L * n_loc * 4 + cfg["catalog"] * 8 + n_dev_recs * (32 + 128)
+    consts = json.load(open(PROFILE_CONST)) if os.path.exists(PROFILE_CONST) else {}
+    clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * clk_mhz * 1e6 / 1e12          # T lane-instructions / s
+    compact = {"kernel": "compact_kernel", "bound": "hbm", "unit": "GB/s", "kernel_ms": t_compact * 1e3,
+               "alg_bytes_per_launch": n_loc * K * 4,
+               "achieved": n_loc * K * 4 / t_compact / 1e9 if t_compact else None, "peak": hbm_peak}
+    compact["frac"] = compact["achieved"] / hbm_peak if compact["achieved"] else None
+    cc = consts.get("compact_kernel", {})
+    compact["traffic"] = cc.get("dram_bytes_per_occurrence", 0) * n_loc * K if cc else None
+    sample = {"kernel": "sample_kernel", "kernel_ms": t_sample * 1e3, "samples_per_launch": pairs,
+              "samples_per_s": pairs / t_sample if t_sample else None}
+    sc = consts.get("sample_kernel", {}) if cfg["su"] else {}
     if cfg["su"]:
-        prof = json.load(open(PROFILE_CONST)) if os.path.exists(PROFILE_CONST) else None
-        clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        alu_peak = 148 * 128 * clk_mhz * 1e6 / 1e12          # T lane-instructions / s
-        roof_alu = {"bound": "alu", "unit": "Tinst/s", "peak": alu_peak, "kernel": "scan_kernel",
-                    "kernel_ms": scan_avg * 1e3, "samples_per_launch": samples,
-                    "samples_per_s": samples / scan_avg,
-                    "peak_source": "148 SM x 128 FP32 lanes x sm_max_mhz (B200_PROFILING.md)"}
-        if prof:
-            inst = prof["thread_inst_per_sample"] * samples
-            roof_alu.update(achieved=inst / scan_avg / 1e12, frac=inst / scan_avg / 1e12 / alu_peak,
-                            inst_per_sample=prof["thread_inst_per_sample"],
-                            inst_source=prof.get("source"),
-                            traffic=prof["dram_bytes_per_sample"] * samples if "dram_bytes_per_sample" in prof else None)
+        sample.update(bound="alu", unit="Tinst/s", peak=alu_peak,
+                      peak_source="148 SMs x 128 FP32 lanes x sm_max_mhz (B200_PROFILING.md)")
+        if sc and t_sample:
+            inst = sc["thread_inst_per_pair"] * pairs
+            sample.update(achieved=inst / t_sample / 1e12, frac=inst / t_sample / 1e12 / alu_peak,
+                          inst_per_pair=sc["thread_inst_per_pair"], inst_source=consts.get("source"),
+                          traffic=sc["dram_bytes_per_pair"] * pairs)
         else:
-            roof_alu.update(achieved=None, frac=None, traffic=None)
-        roof_alu["hbm"] = {k: roof[k] for k in ("achieved", "peak", "unit", "frac")}
-        roof = roof_alu
+            sample.update(achieved=None, frac=None, traffic=None)
+    else:
+        sample.update(bound="hbm", unit="GB/s", peak=hbm_peak,
+                      achieved=pairs * 8 / t_sample / 1e9 if t_sample else None)
+        sample["frac"] = sample["achieved"] / hbm_peak if sample["achieved"] else None
+        sample["traffic"] = None
+    dom = sample if t_sample >= t_compact else compact
+    roof = dict(dom)
+    roof["peak_note"] = peak_src if roof.get("unit") == "GB/s" else roof.get("peak_source")
+    roof["kernels"] = {"compact_kernel": compact, "sample_kernel": sample, "redo_ms": t_redo * 1e3}
+    roof["path_hbm"] = {"alg_bytes_per_step": alg_bytes, "run_ms": scan_avg * 1e3,
+                        "achieved": alg_bytes / scan_avg / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": alg_bytes / scan_avg / 1e9 / hbm_peak}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -318,7 +336,7 @@ def run_ours(args, cfg, rank, world, local):
                "sample": f"first {n} trials of {cfg['name']} (global index 0..{n - 1}), "
                          f"fp64 C oracle, {cores} threads, {dt:.1f} s"}
 
-    gpu_launches = args.steps * (1 + 11 * len(layers))
+    gpu_launches = args.steps * (2 + (1 if t_redo > 0 else 0) + 11 * len(layers))
     ms = elapsed / args.steps * 1e3
     value = N_total / (elapsed / args.steps)
     line = {

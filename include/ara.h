@@ -184,6 +184,13 @@ void ara_yet_destroy(ara_yet *yet);
 int ara_run(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint64_t seed,
             uint32_t flags, float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash);
 
+/* Device time of the kernels of the last ara_run on this context (CUDA
+ * events on its stream): compact_ms = YET stream + lookup (compact_kernel),
+ * sample_ms = draws + sampler + terms + YLT (sample_kernel; the fused
+ * kernel under ARA_EXACT), redo_ms = trials re-run by the fused fp64-capable
+ * kernel (0 when none).  Any pointer may be NULL. */
+int ara_last_run_timings(const ara_ctx *ctx, double *compact_ms, double *sample_ms, double *redo_ms);
+
 /* PML and TVaR (reading G17) at each return period of one layer's
  * YLT, or of the portfolio roll-up sum over layers (layer = -1, G16), by a
  * device radix select over the fp32 bit patterns plus a sort of the tail.

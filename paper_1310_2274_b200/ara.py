@@ -34,7 +34,8 @@ EXPORTS = (
     "ara_last_error", "ara_version", "ara_ctx_create", "ara_ctx_destroy", "ara_ctx_synchronize",
     "ara_validate_portfolio", "ara_create_portfolio", "ara_portfolio_destroy", "ara_portfolio_info",
     "ara_load_yet",
-    "ara_yet_refill", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_risk_measures",
+    "ara_yet_refill", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_last_run_timings",
+    "ara_risk_measures",
     "ara_sample_losses", "ara_draw_uniforms",
 )
 
@@ -67,6 +68,7 @@ def _load():
     L.ara_yet_destroy.argtypes = [vp]; L.ara_yet_destroy.restype = None
     L.ara_run.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp]
     L.ara_risk_measures.argtypes = [vp, vp, u32, u64, u32, i32, vp, u32, vp, vp]
+    L.ara_last_run_timings.argtypes = [vp, vp, vp, vp]
     L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, u32, vp]
     L.ara_draw_uniforms.argtypes = [vp, u64, u64, vp, vp]
     for n in EXPORTS:            # fail loudly if an entry point is missing
@@ -246,6 +248,13 @@ def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug
     _check(lib.ara_run(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(cnt),
                        _p(hsh)))
     return (ylt, cnt, hsh) if debug else ylt
+
+
+def last_run_timings(ctx: Context):
+    """ara_last_run_timings -> dict(compact_ms, sample_ms, redo_ms) of the last ara_run."""
+    a, b, c = C.c_double(), C.c_double(), C.c_double()
+    _check(lib.ara_last_run_timings(ctx.h, C.byref(a), C.byref(b), C.byref(c)))
+    return {"compact_ms": a.value, "sample_ms": b.value, "redo_ms": c.value}
 
 
 def risk_measures(ctx: Context, ylt, n_layers: int, n_total: int, layer: int = 0,

@@ -66,6 +66,8 @@ struct ara_ctx {
     uint64_t pairs_capacity = 0;       // elements of d_pairs
     uint32_t *d_counts = nullptr;      // split path scratch: pairs per trial
     uint64_t counts_capacity = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // per-kernel timings of ara_run
+    double last_ms[3] = {0.0, 0.0, 0.0};                        // compact, sample, redo
 };
 
 struct ara_portfolio {
@@ -119,7 +121,9 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
         dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
         dalloc(&c->ms.d_out, 128) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
         dalloc(&c->ms.part_sum, kRedBlocks) != cudaSuccess ||
-        dalloc(&c->ms.part_cnt, kRedBlocks) != cudaSuccess) {
+        dalloc(&c->ms.part_cnt, kRedBlocks) != cudaSuccess || cudaEventCreate(&c->ev[0]) != cudaSuccess ||
+        cudaEventCreate(&c->ev[1]) != cudaSuccess || cudaEventCreate(&c->ev[2]) != cudaSuccess ||
+        cudaEventCreate(&c->ev[3]) != cudaSuccess) {
         ara_ctx_destroy(c);
         return fail(ARA_ENOMEM, "device allocation failed in ara_ctx_create");
     }
@@ -143,6 +147,8 @@ void ara_ctx_destroy(ara_ctx *c) {
     cudaFree(c->ms.part_cnt);
     cudaFree(c->d_pairs);
     cudaFree(c->d_counts);
+    for (cudaEvent_t e : c->ev)
+        if (e) cudaEventDestroy(e);
     delete c;
 }
 
@@ -480,10 +486,17 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         }
         SplitArgs S{p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status,
                     c->d_pairs, cap, c->d_counts, y->d_redo};
-        CU(launch_split(S, c->stream, c->num_sms));
+        CU(cudaEventRecord(c->ev[0], c->stream));
+        CU(launch_compact(S, c->stream, c->num_sms));
+        CU(cudaEventRecord(c->ev[1], c->stream));
+        CU(launch_sample(S, c->stream, c->num_sms));
+        CU(cudaEventRecord(c->ev[2], c->stream));
     } else {
+        CU(cudaEventRecord(c->ev[0], c->stream));
+        CU(cudaEventRecord(c->ev[1], c->stream));
         CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, nullptr, 0,
                        y->d_redo, true, c->stream, c->num_sms));
+        CU(cudaEventRecord(c->ev[2], c->stream));
     }
     CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -493,8 +506,19 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         CU(cudaMemsetAsync(&c->d_status->next_trial, 0, sizeof(unsigned long long), c->stream));
         CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, y->d_redo,
                        n_redo, nullptr, (flags & ARA_SU) != 0, c->stream, c->num_sms));
+        CU(cudaEventRecord(c->ev[3], c->stream));
         CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
+    } else {
+        CU(cudaEventRecord(c->ev[3], c->stream));
+        CU(cudaEventSynchronize(c->ev[3]));
+    }
+    {
+        float a = 0, b = 0, r = 0;
+        CU(cudaEventElapsedTime(&a, c->ev[0], c->ev[1]));
+        CU(cudaEventElapsedTime(&b, c->ev[1], c->ev[2]));
+        CU(cudaEventElapsedTime(&r, c->ev[2], c->ev[3]));
+        c->last_ms[0] = a; c->last_ms[1] = b; c->last_ms[2] = r;
     }
     if (c->h_status->bad_event)
         return fail(ARA_ERANGE, "%u event occurrences have event id >= catalog_size %u",
@@ -502,6 +526,14 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
     if (c->h_status->nonconverged)
         return fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples",
                     c->h_status->nonconverged);
+    return ARA_OK;
+}
+
+int ara_last_run_timings(const ara_ctx *c, double *compact_ms, double *sample_ms, double *redo_ms) {
+    if (!c) return fail(ARA_EINVAL, "ctx is NULL");
+    if (compact_ms) *compact_ms = c->last_ms[0];
+    if (sample_ms) *sample_ms = c->last_ms[1];
+    if (redo_ms) *redo_ms = c->last_ms[2];
     return ARA_OK;
 }
 

@@ -104,7 +104,8 @@ struct SplitArgs {
     uint32_t *counts;
     uint32_t *redo;
 };
-cudaError_t launch_split(const SplitArgs &A, cudaStream_t s, int num_sms);
+cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
+cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);
 
 // kernels
 void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_t n,

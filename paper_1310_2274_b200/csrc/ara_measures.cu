@@ -110,12 +110,13 @@ __global__ void __launch_bounds__(1024) sort_measures_kernel(const float *buf, S
             __syncthreads();
         }
     }
-    if (threadIdx.x != 0) return;
     const float T = okey_inv(st->prefix);
     const uint64_t neq = st->n_eq, N = n_total;
     auto L = [&](uint64_t r) -> double {         // descending order statistic, 1-based
         return r <= ng ? (double)sv[r - 1] : (double)T;
     };
+    __shared__ double red_s[1024];
+    __shared__ unsigned int red_c[1024];
     for (uint32_t q = 0; q < n_rp; ++q) {
         const double rp = rps[q];
         uint64_t fl, m;
@@ -134,17 +135,35 @@ __global__ void __launch_bounds__(1024) sort_measures_kernel(const float *buf, S
         }
         if (m < 1) m = 1;
         if (m > N) m = N;
-        double pml;
-        if (fl < 1 || (fl == 1 && frac == 0.0)) pml = L(1);
-        else if (fl >= N) pml = L(N);
-        else pml = L(fl) + frac * (L(fl + 1) - L(fl));
         const double var = L(m);
-        double sum = 0.0;
-        uint64_t cnt = 0;
-        for (uint32_t i = 0; i < ng && (double)sv[i] >= var; ++i) { sum += (double)sv[i]; ++cnt; }
-        if (var == (double)T) { sum += (double)neq * (double)T; cnt += neq; }
-        out[2 * q] = pml;
-        out[2 * q + 1] = sum / (double)cnt;
+        // tail sum over the sorted values >= VaR: fixed per-thread strides and a
+        // fixed tree, so the result does not depend on timing
+        double acc = 0.0;
+        unsigned int cnt = 0;
+        for (uint32_t i = threadIdx.x; i < ng; i += blockDim.x)
+            if ((double)sv[i] >= var) { acc += (double)sv[i]; ++cnt; }
+        red_s[threadIdx.x] = acc;
+        red_c[threadIdx.x] = cnt;
+        __syncthreads();
+        for (uint32_t o = blockDim.x / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) {
+                red_s[threadIdx.x] += red_s[threadIdx.x + o];
+                red_c[threadIdx.x] += red_c[threadIdx.x + o];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            double pml;
+            if (fl < 1 || (fl == 1 && frac == 0.0)) pml = L(1);
+            else if (fl >= N) pml = L(N);
+            else pml = L(fl) + frac * (L(fl + 1) - L(fl));
+            double sum = red_s[0];
+            uint64_t c = red_c[0];
+            if (var == (double)T) { sum += (double)neq * (double)T; c += neq; }
+            out[2 * q] = pml;
+            out[2 * q + 1] = sum / (double)c;
+        }
+        __syncthreads();
     }
 }
 

@@ -402,14 +402,15 @@ static cudaError_t launch_compact_mw(const SplitArgs &A, cudaStream_t s, int num
     return cudaGetLastError();
 }
 
-cudaError_t launch_split(const SplitArgs &A, cudaStream_t s, int num_sms) {
+cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms) {
+    if (A.pf.mask_words == 1) return launch_compact_mw<1>(A, s, num_sms);
+    if (A.pf.mask_words <= 3) return launch_compact_mw<3>(A, s, num_sms);
+    if (A.pf.mask_words == 4) return launch_compact_mw<4>(A, s, num_sms);
+    return launch_compact_mw<7>(A, s, num_sms);
+}
+
+cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
     const bool dbg = (A.flags & ARA_DEBUG_LOOKUP) != 0, su = (A.flags & ARA_SU) != 0;
-    cudaError_t err;
-    if (A.pf.mask_words == 1) err = launch_compact_mw<1>(A, s, num_sms);
-    else if (A.pf.mask_words <= 3) err = launch_compact_mw<3>(A, s, num_sms);
-    else if (A.pf.mask_words == 4) err = launch_compact_mw<4>(A, s, num_sms);
-    else err = launch_compact_mw<7>(A, s, num_sms);
-    if (err != cudaSuccess) return err;
     const bool sl = A.pf.n_layers == 1;
     const size_t smem = sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
                         kSampleWarps * A.pf.n_layers * (sizeof(double) + sizeof(unsigned int) +
@@ -423,7 +424,7 @@ cudaError_t launch_split(const SplitArgs &A, cudaStream_t s, int num_sms) {
         return dbg ? sample_kernel<false, false, true> : sample_kernel<false, false, false>;
     };
     auto kern = pick();
-    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     int per_sm = 0;
     err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSampleWarps * 32, smem);

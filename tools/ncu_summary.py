@@ -1,12 +1,14 @@
-"""Summarise an ncu capture of the scan kernel into profiles/.
+"""Summarise an ncu capture of the split scan kernels into profiles/.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep --tag r01_scan_vN \
-        --samples 32000000 [--write-const]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep --tag r01_split_vN \
+        --pairs 31999955 --occurrences 100000000 [--write-const]
 
-Writes profiles/<tag>_summary.json (selected raw metrics + derived per-sample
-figures) and, with --write-const, profiles/scan_inst_per_sample.json, the
-per-present-pair thread-instruction count and DRAM traffic per pair that
-bench.py uses for the ALU roofline (achieved = inst/pair x pairs / live time).
+For every kernel launch in the report writes profiles/<tag>_<kernel>.json
+(selected raw metrics, stall reasons, derived per-unit figures).  With
+--write-const, profiles/roofline_consts.json gets, per kernel, the
+thread-instruction count and DRAM traffic per present pair (sample_kernel)
+or per occurrence (compact_kernel): bench.py multiplies them by the units of
+a launch and divides by the live CUDA-event kernel time.
 """
 from __future__ import annotations
 
@@ -15,6 +17,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -37,11 +40,7 @@ def read_raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
-    kern = []
-    for r in rows[2:]:
-        d = dict(zip(hdr, r))
-        kern.append({h: (d[h], units[i]) for i, h in enumerate(hdr)})
-    return kern
+    return [{h: (r[i], units[i]) for i, h in enumerate(hdr)} for r in rows[2:]]
 
 
 def to_float(v):
@@ -51,53 +50,64 @@ def to_float(v):
         return None
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("rep")
-    ap.add_argument("--tag", required=True)
-    ap.add_argument("--samples", type=float, required=True, help="present pairs in the profiled launch")
-    ap.add_argument("--write-const", action="store_true")
-    a = ap.parse_args()
-    kern = read_raw(a.rep)[0]
-    sel = {}
-    for k in KEYS:
-        for h, (v, u) in kern.items():
-            if h == k:
-                sel[k] = {"value": v, "unit": u}
+def summarise(kern, units_per_launch):
+    sel = {k: {"value": kern[k][0], "unit": kern[k][1]} for k in KEYS if k in kern}
     stalls = {h: v for h, (v, u) in kern.items() if "average_warps_issue_stalled" in h and h.endswith("ratio")
               and (to_float(v) or 0) > 0.1}
     inst = to_float(sel["smsp__inst_executed.sum"]["value"])
     if "smsp__thread_inst_executed.sum" in sel:
         t_inst = to_float(sel["smsp__thread_inst_executed.sum"]["value"])
-    else:   # the full set has the per-instruction thread ratio instead
+    else:   # the full set carries the per-instruction thread ratio instead
         t_inst = inst * to_float(sel["smsp__thread_inst_executed_per_inst_executed.ratio"]["value"])
-    dur_unit = sel["gpu__time_duration.sum"]["unit"]
-    dur = to_float(sel["gpu__time_duration.sum"]["value"]) * {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0}[dur_unit]
+    scale = {"ms": 1e-3, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "nsecond": 1e-9, "s": 1.0}
+    dur = to_float(sel["gpu__time_duration.sum"]["value"]) * scale[sel["gpu__time_duration.sum"]["unit"]]
+
     def bytes_of(k):
         v, u = to_float(sel[k]["value"]), sel[k]["unit"]
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
     dram = bytes_of("dram__bytes_read.sum") + bytes_of("dram__bytes_write.sum")
-    derived = {
-        "kernel": kern.get("Kernel Name", ("?", ""))[0],
-        "duration_s": dur,
-        "present_pairs": a.samples,
-        "thread_inst_per_pair": t_inst / a.samples,
-        "warp_inst_per_pair": to_float(sel["smsp__inst_executed.sum"]["value"]) / a.samples,
-        "dram_bytes": dram,
-        "dram_bytes_per_pair": dram / a.samples,
-        "lane_inst_per_s": t_inst / dur,
-    }
+    derived = {"kernel": kern.get("Kernel Name", ("?", ""))[0], "duration_s": dur,
+               "units_per_launch": units_per_launch, "thread_inst": t_inst, "warp_inst": inst,
+               "thread_inst_per_unit": t_inst / units_per_launch,
+               "dram_bytes": dram, "dram_bytes_per_unit": dram / units_per_launch,
+               "lane_inst_per_s": t_inst / dur}
+    return {"metrics": sel, "stalls": stalls, "derived": derived}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("rep")
+    ap.add_argument("--tag", required=True)
+    ap.add_argument("--pairs", type=float, required=True, help="present pairs in the profiled launch")
+    ap.add_argument("--occurrences", type=float, required=True, help="YET occurrences in the profiled launch")
+    ap.add_argument("--write-const", action="store_true")
+    a = ap.parse_args()
+    consts_path = os.path.join(ROOT, "profiles", "roofline_consts.json")
+    consts = json.load(open(consts_path)) if os.path.exists(consts_path) else {}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    with open(os.path.join(ROOT, "profiles", f"{a.tag}_summary.json"), "w") as f:
-        json.dump({"source": os.path.basename(a.rep), "metrics": sel, "stalls": stalls, "derived": derived}, f,
-                  indent=1)
+    for kern in read_raw(a.rep):
+        name = kern.get("Kernel Name", ("?", ""))[0]
+        m = re.search(r"(compact_kernel|sample_kernel|scan_kernel)", name)
+        if not m:
+            continue
+        short = m.group(1)
+        units = a.occurrences if short == "compact_kernel" else a.pairs
+        out = summarise(kern, units)
+        out["source"] = os.path.basename(a.rep)
+        with open(os.path.join(ROOT, "profiles", f"{a.tag}_{short}.json"), "w") as f:
+            json.dump(out, f, indent=1)
+        d = out["derived"]
+        print(json.dumps({short: d}, indent=1))
+        if a.write_const:
+            key = "occurrence" if short == "compact_kernel" else "pair"
+            consts[short] = {f"thread_inst_per_{key}": d["thread_inst_per_unit"],
+                             f"dram_bytes_per_{key}": d["dram_bytes_per_unit"],
+                             "source": f"profiles/{a.tag}_{short}.json ({os.path.basename(a.rep)})"}
     if a.write_const:
-        with open(os.path.join(ROOT, "profiles", "scan_inst_per_sample.json"), "w") as f:
-            json.dump({"thread_inst_per_sample": derived["thread_inst_per_pair"],
-                       "dram_bytes_per_sample": derived["dram_bytes_per_pair"],
-                       "source": f"profiles/{a.tag}_summary.json ({os.path.basename(a.rep)})",
-                       "note": "per present (occurrence, slot) pair, ncu --set full, one launch"}, f, indent=1)
-    print(json.dumps(derived, indent=1))
+        consts["source"] = f"profiles/{a.tag}_*.json"
+        consts["note"] = "ncu --set full, one launch of each kernel on cfg3's first 100k trials"
+        with open(consts_path, "w") as f:
+            json.dump(consts, f, indent=1)
 
 
 if __name__ == "__main__":

@@ -3,6 +3,7 @@
 // index, presence bitmap, slot tables), YET handling, and launch plumbing.
 // All arithmetic of the method runs in the kernels (ara_kernels.cu,
 // ara_measures.cu); this file only validates, lays out and copies.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -62,7 +63,7 @@ struct ara_ctx {
     RunStatus *d_status = nullptr;
     RunStatus *h_status = nullptr;     // pinned
     MeasuresScratch ms;
-    uint2 *d_pairs = nullptr;          // split path scratch: per-trial present pairs
+    uint2 *d_pairs = nullptr;          // split path scratch: per-trial hits {event, k}
     uint64_t pairs_capacity = 0;       // elements of d_pairs
     uint32_t *d_counts = nullptr;      // split path scratch: pairs per trial
     uint64_t counts_capacity = 0;
@@ -74,11 +75,15 @@ struct ara_portfolio {
     ara_ctx *ctx = nullptr;
     PortfolioDev dev{};
     uint32_t *d_index = nullptr, *d_bitmap = nullptr, *d_rec_orig = nullptr;
+    uint2 *d_cidx = nullptr;
+    uint32_t *d_rec_meta = nullptr;
+    SplitRec *d_srecs = nullptr;
     BetaRec *d_recs = nullptr;
     float2 *d_tables = nullptr, *d_hot = nullptr;
     float *d_mu = nullptr;
     SlotInfo *d_slots = nullptr;
     LayerInfo *d_layers = nullptr;
+    double hit_frac = 0.0;             // fraction of catalog events whose presence bit is set
 };
 
 struct ara_yet {
@@ -87,6 +92,7 @@ struct ara_yet {
     uint32_t *d_events = nullptr;
     uint64_t *d_offsets = nullptr;
     uint32_t *d_redo = nullptr;        // trials to re-run with the fp64 kernel
+    uint32_t *d_max = nullptr;         // largest event id (device word)
     uint64_t avg_len_x1000 = 0;        // mean events per trial x 1000
 };
 
@@ -248,8 +254,23 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
             s.pad = 0.0f;
         }
     std::vector<LayerInfo> layers(n_layers);
-    for (uint32_t l = 0; l < n_layers; ++l)
-        layers[l] = {lt[l].occ_retention, lt[l].occ_limit, lt[l].agg_retention, lt[l].agg_limit};
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        // bound on one occurrence term of the layer: min(OccL, sum over its
+        // slots of the largest (XELT-term-applied) loss) -> fixed-point scale
+        double sum_b = 0.0;
+        for (uint64_t x = loff[l]; x < loff[l + 1]; ++x) {
+            const uint32_t j = lelts[x];
+            double mx = 0.0;
+            for (uint64_t r = eoff[j]; r < eoff[j + 1]; ++r) mx = std::max(mx, (double)rec[r].max_loss);
+            if (et) mx = std::max(et[j].share, 1.0) * std::min(mx, et[j].limit);
+            sum_b += mx;
+        }
+        const double g = std::min(lt[l].occ_limit, sum_b);
+        int ex = 0;
+        std::frexp(g * 16777216.0 * 1.01 + 1.0, &ex);          // bound < 2^ex
+        const double fx = std::ldexp(1.0, std::max(-1000, std::min(1000, 61 - ex)));
+        layers[l] = {lt[l].occ_retention, lt[l].occ_limit, lt[l].agg_retention, lt[l].agg_limit, fx, 1.0 / fx};
+    }
 
     // event-major direct-access index: per event the slots with a record
     const uint32_t MW = (S + 31) / 32;
@@ -269,6 +290,14 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     }
     if (total >= (1ull << 32)) return fail(ARA_EINVAL, "too many (layer, record) pairs");
     std::vector<uint32_t> rec_src(total), rec_orig(total);
+    std::vector<uint32_t> rec_meta(total);      // slot | run_end << 8 | layer << 16
+    std::vector<uint2> cidx(C);                  // (first record, record count) per event
+    for (uint32_t e = 0; e < C; ++e) {
+        const uint32_t *ix = &index[(size_t)e * stride];
+        uint32_t n = 0;
+        for (uint32_t w = 0; w < MW; ++w) n += (uint32_t)__builtin_popcount(ix[1 + w]);
+        cidx[e] = make_uint2(ix[0], n);
+    }
     for (uint32_t s = 0; s < S; ++s) {
         const uint32_t j = slots[s].elt;
         for (uint64_t r = eoff[j]; r < eoff[j + 1]; ++r) {
@@ -278,8 +307,15 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
             rank += (uint32_t)__builtin_popcount(ix[1 + (s >> 5)] & ((1u << (s & 31)) - 1u));
             rec_src[ix[0] + rank] = (uint32_t)r;
             rec_orig[ix[0] + rank] = (uint32_t)(r - eoff[j]);
+            rec_meta[ix[0] + rank] = s | (slots[s].layer << 16);
         }
     }
+    for (uint32_t e = 0; e < C; ++e)
+        for (uint32_t r = cidx[e].x; r < cidx[e].x + cidx[e].y; ++r) {
+            const bool last = r + 1 == cidx[e].x + cidx[e].y ||
+                              slots[rec_meta[r + 1] & 0xffu].layer != slots[rec_meta[r] & 0xffu].layer;
+            if (last) rec_meta[r] |= 0x100u;
+        }
     // presence bitmap (any slot present), at most 2^20 bits (128 KiB of smem)
     uint32_t shift = 0;
     while (((uint64_t)C + (1ull << shift) - 1) >> shift > (1ull << 20)) ++shift;
@@ -291,6 +327,8 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
         for (uint32_t w = 0; w < MW; ++w) any |= index[(size_t)e * stride + 1 + w] != 0;
         if (any) bitmap[(e >> shift) >> 5] |= 1u << ((e >> shift) & 31);
     }
+    uint64_t n_hit = 0;
+    for (uint32_t e = 0; e < C; ++e) n_hit += (bitmap[(e >> shift) >> 5] >> ((e >> shift) & 31)) & 1u;
 
     ara_portfolio *p = new ara_portfolio();
     p->ctx = c;
@@ -304,6 +342,7 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
         return code;
     };
     if (dalloc(&p->d_index, index.size()) || dalloc(&p->d_bitmap, words) ||
+        dalloc(&p->d_cidx, (size_t)C) || dalloc(&p->d_rec_meta, (size_t)total) || dalloc(&p->d_srecs, (size_t)total) ||
         dalloc(&p->d_rec_orig, total) || dalloc(&p->d_recs, total) || dalloc(&p->d_mu, total) ||
         dalloc(&p->d_tables, total * kTabStride) || dalloc(&p->d_hot, total * kHotN) ||
         dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) || dalloc(&d_raw, R) ||
@@ -316,6 +355,8 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     UP(p->d_index, index.data(), index.size());
     UP(p->d_bitmap, bitmap.data(), (size_t)words);
     UP(p->d_rec_orig, rec_orig.data(), (size_t)total);
+    UP(p->d_cidx, cidx.data(), (size_t)C);
+    UP(p->d_rec_meta, rec_meta.data(), (size_t)total);
     UP(p->d_slots, slots.data(), (size_t)S);
     UP(p->d_layers, layers.data(), (size_t)n_layers);
     UP(d_raw, rec, (size_t)R);
@@ -326,6 +367,10 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     if (e == cudaSuccess) {
         launch_prep_records(d_raw, d_src, total, p->d_recs, p->d_mu, p->d_tables, p->d_hot,
                             &c->d_status->nonconverged, s);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        launch_split_recs(p->d_recs, p->d_rec_meta, p->d_slots, total, p->d_srecs, s);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
@@ -342,6 +387,9 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     d.tables = p->d_tables;
     d.hot = p->d_hot;
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
+    d.cidx = p->d_cidx; d.rec_meta = p->d_rec_meta; d.srecs = p->d_srecs;
+    d.any_terms = et ? 1u : 0u;
+    p->hit_frac = C ? (double)n_hit / (double)C : 0.0;
     *out = p;
     return ARA_OK;
 }
@@ -352,8 +400,8 @@ int ara_portfolio_info(const ara_portfolio *p, uint64_t *n_dev, uint64_t *n_tl, 
     if (n_dev) *n_dev = d.n_dev_records;
     if (n_tl) *n_tl = d.n_exact_records;
     if (bytes)
-        *bytes = (uint64_t)d.catalog * d.idx_stride * 4 + (uint64_t)d.bitmap_words * 4 +
-                 d.n_dev_records * (sizeof(BetaRec) + sizeof(float) + sizeof(uint32_t) +
+        *bytes = (uint64_t)d.catalog * (d.idx_stride * 4 + sizeof(uint2)) + (uint64_t)d.bitmap_words * 4 +
+                 d.n_dev_records * (sizeof(BetaRec) + sizeof(float) + sizeof(uint32_t) + sizeof(uint32_t) + sizeof(SplitRec) +
                                     (kTabStride + kHotN) * sizeof(float2)) +
                  d.n_slots * sizeof(SlotInfo) + d.n_layers * sizeof(LayerInfo);
     return ARA_OK;
@@ -363,6 +411,7 @@ void ara_portfolio_destroy(ara_portfolio *p) {
     if (!p) return;
     if (p->ctx) cudaSetDevice(p->ctx->device);
     cudaFree(p->d_index); cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig); cudaFree(p->d_recs);
+    cudaFree(p->d_cidx); cudaFree(p->d_rec_meta); cudaFree(p->d_srecs);
     cudaFree(p->d_mu); cudaFree(p->d_slots); cudaFree(p->d_layers); cudaFree(p->d_tables); cudaFree(p->d_hot);
     delete p;
 }
@@ -401,7 +450,9 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
     CU(cudaSetDevice(c->device));
     ara_yet *y = new ara_yet();
     y->ctx = c;
-    if (dalloc(&y->d_events, total) != cudaSuccess || dalloc(&y->d_redo, n_trials) != cudaSuccess ||
+    // +4 words: the compaction kernel's bulk copies round each piece up to 16 B
+    if (dalloc(&y->d_events, total + 4) != cudaSuccess || dalloc(&y->d_redo, n_trials) != cudaSuccess ||
+        dalloc(&y->d_max, 1) != cudaSuccess ||
         (toff && dalloc(&y->d_offsets, n_trials + 1) != cudaSuccess)) {
         cudaGetLastError();
         ara_yet_destroy(y);
@@ -415,6 +466,7 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
     if (e == cudaSuccess && toff)
         e = cudaMemcpyAsync(y->d_offsets, toff, (n_trials + 1) * sizeof(uint64_t),
                             cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = launch_yet_max(y->d_events, total, y->d_max, c->stream, c->num_sms);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
         ara_yet_destroy(y);
@@ -423,6 +475,7 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
     y->dev.n_trials = n_trials; y->dev.first_trial = first_trial;
     y->dev.fixed_len = toff ? 0u : fixed_len;
     y->dev.offsets = y->d_offsets; y->dev.events = y->d_events; y->dev.n_events = total;
+    y->dev.max_event = y->d_max;
     y->avg_len_x1000 = n_trials ? (total * 1000) / n_trials : 0;
     *out = y;
     return ARA_OK;
@@ -436,6 +489,7 @@ int ara_yet_refill(ara_ctx *c, ara_yet *y, const uint32_t *events) {
     CU(cudaMemcpyAsync(y->d_events, events, y->dev.n_events * sizeof(uint32_t),
                        is_device_ptr(events) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        c->stream));
+    CU(launch_yet_max(y->d_events, y->dev.n_events, y->d_max, c->stream, c->num_sms));
     return ARA_OK;
 }
 
@@ -447,6 +501,7 @@ void ara_yet_destroy(ara_yet *y) {
     cudaFree(y->d_events);
     cudaFree(y->d_offsets);
     cudaFree(y->d_redo);
+    cudaFree(y->d_max);
     delete y;
 }
 
@@ -462,11 +517,11 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
     CU(cudaSetDevice(c->device));
     const bool exact = (flags & ARA_EXACT) != 0 && (flags & ARA_SU) != 0;
     CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
-    if (!exact) {
-        // split path: per-trial pair regions sized 2x the expected pairs per trial
-        // (+128); a trial that overflows its region goes to the fused kernel
-        const double per_occ = (double)p->dev.n_dev_records / (double)p->dev.catalog;
-        const double expect = per_occ * (double)y->avg_len_x1000 / 1000.0;
+    if (!exact && p->dev.n_layers <= kSplitMaxLayers) {
+        // split path: per-trial hit regions sized 2x the expected hits per trial
+        // (+128) for uniformly drawn event ids; a trial that overflows its
+        // region goes to the fused kernel
+        const double expect = p->hit_frac * (double)y->avg_len_x1000 / 1000.0;
         uint32_t cap = (uint32_t)((2.0 * expect + 128.0 + 31.0) / 32.0) * 32u;
         if (cap > (1u << 20)) cap = 1u << 20;
         const uint64_t need = y->dev.n_trials * (uint64_t)cap;
@@ -485,17 +540,22 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
             c->counts_capacity = y->dev.n_trials;
         }
         SplitArgs S{p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status,
-                    c->d_pairs, cap, c->d_counts, y->d_redo};
+                    c->d_pairs, cap, c->d_counts, y->d_redo, {}};
+        for (int r = 0; r < 10; ++r) {                   // Philox4x32-10 key schedule of the seed
+            S.pkey[2 * r] = (uint32_t)seed + (uint32_t)r * 0x9E3779B9u;
+            S.pkey[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;
+        }
         CU(cudaEventRecord(c->ev[0], c->stream));
         CU(launch_compact(S, c->stream, c->num_sms));
         CU(cudaEventRecord(c->ev[1], c->stream));
         CU(launch_sample(S, c->stream, c->num_sms));
         CU(cudaEventRecord(c->ev[2], c->stream));
     } else {
+        // ARA_EXACT (fp64 solve for every sample) or > kSplitMaxLayers layers: the fused kernel
         CU(cudaEventRecord(c->ev[0], c->stream));
         CU(cudaEventRecord(c->ev[1], c->stream));
         CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, nullptr, 0,
-                       y->d_redo, true, c->stream, c->num_sms));
+                       y->d_redo, exact, c->stream, c->num_sms));
         CU(cudaEventRecord(c->ev[2], c->stream));
     }
     CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
@@ -520,9 +580,14 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         CU(cudaEventElapsedTime(&r, c->ev[2], c->ev[3]));
         c->last_ms[0] = a; c->last_ms[1] = b; c->last_ms[2] = r;
     }
-    if (c->h_status->bad_event)
+    if (c->h_status->bad_event) {      // error path: count the offending occurrences
+        CU(launch_count_bad(y->d_events, y->dev.n_events, p->dev.catalog, &c->d_status->bad_event, c->stream,
+                            c->num_sms));
+        CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
         return fail(ARA_ERANGE, "%u event occurrences have event id >= catalog_size %u",
                     c->h_status->bad_event, p->dev.catalog);
+    }
     if (c->h_status->nonconverged)
         return fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples",
                     c->h_status->nonconverged);

@@ -21,6 +21,10 @@ struct SlotInfo {
 
 struct LayerInfo {
     double occ_r, occ_l, agg_r, agg_l;
+    // split path: trial sums are accumulated in 64-bit fixed point (exact, so
+    // independent of summation order): g -> rint(g * fx_scale); fx_scale is a
+    // power of two with 2^24 events x the largest occurrence term < 2^61
+    double fx_scale, fx_inv;
 };
 
 // Per-record sampler constants, derived on the device in fp64 from the
@@ -48,6 +52,17 @@ struct __align__(16) BetaRec {
     uint32_t mode;
 };
 
+// Per-record constants of the split sampler (32 B, one L2 sector): the beta
+// parameters and weights of BetaRec plus what the draw keys need, so a pair
+// is sampled from this one load.  meta: slot | run_end << 8 | layer << 16 |
+// mode << 28 (run_end: last record of its (event, layer) run).
+struct __align__(16) SplitRec {
+    float a, b, wi, wc;
+    float scale;
+    uint32_t meta;
+    uint32_t elt, prog;
+};
+
 struct PortfolioDev {
     uint32_t catalog;
     uint32_t n_slots, n_layers;
@@ -64,6 +79,10 @@ struct PortfolioDev {
     const float2 *hot;        // [n_dev_records][kHotN] nodes kHotJ0.. of the same tables
     const float *rec_mu;      // [n_dev_records] mean loss (primary uncertainty)
     const uint32_t *rec_orig; // [n_dev_records] record index within its XELT
+    const uint2 *cidx;        // [catalog] (first device record, record count) of each event
+    const uint32_t *rec_meta; // [n_dev_records] slot | run_end << 8 | layer << 16 (SplitRec.meta)
+    const SplitRec *srecs;    // [n_dev_records]
+    uint32_t any_terms;       // some slot has XELT terms (G7)
     const SlotInfo *slots;    // [n_slots]
     const LayerInfo *layers;  // [n_layers]
 };
@@ -72,8 +91,9 @@ struct YetDev {
     uint64_t n_trials, first_trial;
     uint32_t fixed_len;       // 0 => CSR
     const uint64_t *offsets;  // device [n_trials+1] or null
-    const uint32_t *events;
+    const uint32_t *events;   // allocation padded by 16 B (bulk copies round up)
     uint64_t n_events;
+    const uint32_t *max_event;  // device word: largest event id (set at every upload)
 };
 
 // device-side status words
@@ -81,15 +101,17 @@ struct RunStatus {
     unsigned long long next_trial;   // dynamic trial scheduler
     unsigned long long next_trial2;  // ... of the second kernel of the split path
     unsigned int nonconverged;       // fp64 solves that did not converge
-    unsigned int bad_event;          // occurrences with event id >= catalog
+    unsigned int bad_event;          // != 0: some event id >= catalog (count on the error path)
     unsigned int n_redo;             // trials touching a table-less record
     unsigned int pad;
 };
 
-// the split (two-kernel) scan: compact_kernel writes each trial's present
-// pairs {device record, (k << 8) | slot} to pairs[t * cap ...] and their count
-// to counts[t] (kOverflow if more than cap); sample_kernel consumes them
+// the split (two-kernel) scan: compact_kernel writes each trial's hits
+// {event id, occurrence k} (events whose presence bit is set) to
+// hits[t * cap ...] and their count to counts[t] (kOverflow if more than cap);
+// sample_kernel looks them up in the index and samples the present pairs
 constexpr uint32_t kOverflow = 0xffffffffu;
+constexpr uint32_t kSplitMaxLayers = 8;   // larger portfolios take the fused kernel
 struct SplitArgs {
     PortfolioDev pf;
     YetDev yet;
@@ -99,15 +121,21 @@ struct SplitArgs {
     uint32_t *dbg_count;
     uint64_t *dbg_hash;
     RunStatus *status;
-    uint2 *pairs;
+    uint2 *hits;
     uint32_t cap;
     uint32_t *counts;
     uint32_t *redo;
+    uint32_t pkey[20];        // Philox key schedule of the seed (round r: pkey[2r], pkey[2r+1])
 };
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);
+cudaError_t launch_yet_max(const uint32_t *ev, uint64_t n, uint32_t *out, cudaStream_t s, int num_sms);
+cudaError_t launch_count_bad(const uint32_t *ev, uint64_t n, uint32_t C, unsigned int *out, cudaStream_t s,
+                             int num_sms);
 
 // kernels
+void launch_split_recs(const BetaRec *recs, const uint32_t *rec_meta, const SlotInfo *slots, uint64_t n,
+                       SplitRec *out, cudaStream_t s);
 void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_t n,
                          BetaRec *out, float *out_mu, float2 *tables, float2 *hot,
                          unsigned int *n_exact, cudaStream_t s);

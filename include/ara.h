@@ -226,6 +226,12 @@ int ara_sample_losses(ara_ctx *ctx, uint64_t n, const ara_record *records,
 int ara_draw_uniforms(ara_ctx *ctx, uint64_t seed, uint64_t n, const uint32_t *ctr,
                       float *u_out);
 
+/* Step 2 of section 3.2 (reading G1): the standard normal
+ * v = Phi^-1(U(x)) the sampler takes from a Philox output word x, with
+ * U(x) = (2(x >> 9) + 1) 2^-24 (G4), evaluated on the smaller tail as the
+ * kernels do.  bits: host [n] uint32 words; v_out: host [n] (fp32). */
+int ara_normal_quantiles(ara_ctx *ctx, uint64_t n, const uint32_t *bits, float *v_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,7 @@ EXPORTS = (
     "ara_load_yet",
     "ara_yet_refill", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_last_run_timings",
     "ara_risk_measures",
-    "ara_sample_losses", "ara_draw_uniforms",
+    "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles",
 )
 
 
@@ -71,6 +71,7 @@ def _load():
     L.ara_last_run_timings.argtypes = [vp, vp, vp, vp]
     L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, u32, vp]
     L.ara_draw_uniforms.argtypes = [vp, u64, u64, vp, vp]
+    L.ara_normal_quantiles.argtypes = [vp, u64, vp, vp]
     for n in EXPORTS:            # fail loudly if an entry point is missing
         getattr(L, n)
     return L
@@ -283,4 +284,12 @@ def draw_uniforms(ctx: Context, seed: int, ctr):
     c = np.ascontiguousarray(ctr, np.uint32).reshape(-1, 4)
     out = np.empty(len(c), np.float32)
     _check(lib.ara_draw_uniforms(ctx.h, int(seed) & 0xFFFFFFFFFFFFFFFF, len(c), _p(c), _p(out)))
+    return out
+
+
+def normal_quantiles(ctx: Context, bits):
+    """ara_normal_quantiles: Phi^-1(U(x)) of 32-bit Philox words x, as the kernels take it."""
+    b = np.ascontiguousarray(bits, np.uint32).ravel()
+    out = np.empty(len(b), np.float32)
+    _check(lib.ara_normal_quantiles(ctx.h, len(b), _p(b), _p(out)))
     return out

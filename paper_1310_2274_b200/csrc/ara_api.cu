@@ -63,7 +63,7 @@ struct ara_ctx {
     RunStatus *d_status = nullptr;
     RunStatus *h_status = nullptr;     // pinned
     MeasuresScratch ms;
-    uint2 *d_pairs = nullptr;          // split path scratch: per-trial hits {event, k}
+    uint2 *d_pairs = nullptr;          // split path scratch: per-trial pairs {device record, k}
     uint64_t pairs_capacity = 0;       // elements of d_pairs
     uint32_t *d_counts = nullptr;      // split path scratch: pairs per trial
     uint64_t counts_capacity = 0;
@@ -83,7 +83,6 @@ struct ara_portfolio {
     float *d_mu = nullptr;
     SlotInfo *d_slots = nullptr;
     LayerInfo *d_layers = nullptr;
-    double hit_frac = 0.0;             // fraction of catalog events whose presence bit is set
 };
 
 struct ara_yet {
@@ -254,23 +253,8 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
             s.pad = 0.0f;
         }
     std::vector<LayerInfo> layers(n_layers);
-    for (uint32_t l = 0; l < n_layers; ++l) {
-        // bound on one occurrence term of the layer: min(OccL, sum over its
-        // slots of the largest (XELT-term-applied) loss) -> fixed-point scale
-        double sum_b = 0.0;
-        for (uint64_t x = loff[l]; x < loff[l + 1]; ++x) {
-            const uint32_t j = lelts[x];
-            double mx = 0.0;
-            for (uint64_t r = eoff[j]; r < eoff[j + 1]; ++r) mx = std::max(mx, (double)rec[r].max_loss);
-            if (et) mx = std::max(et[j].share, 1.0) * std::min(mx, et[j].limit);
-            sum_b += mx;
-        }
-        const double g = std::min(lt[l].occ_limit, sum_b);
-        int ex = 0;
-        std::frexp(g * 16777216.0 * 1.01 + 1.0, &ex);          // bound < 2^ex
-        const double fx = std::ldexp(1.0, std::max(-1000, std::min(1000, 61 - ex)));
-        layers[l] = {lt[l].occ_retention, lt[l].occ_limit, lt[l].agg_retention, lt[l].agg_limit, fx, 1.0 / fx};
-    }
+    for (uint32_t l = 0; l < n_layers; ++l)
+        layers[l] = {lt[l].occ_retention, lt[l].occ_limit, lt[l].agg_retention, lt[l].agg_limit};
 
     // event-major direct-access index: per event the slots with a record
     const uint32_t MW = (S + 31) / 32;
@@ -327,8 +311,6 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
         for (uint32_t w = 0; w < MW; ++w) any |= index[(size_t)e * stride + 1 + w] != 0;
         if (any) bitmap[(e >> shift) >> 5] |= 1u << ((e >> shift) & 31);
     }
-    uint64_t n_hit = 0;
-    for (uint32_t e = 0; e < C; ++e) n_hit += (bitmap[(e >> shift) >> 5] >> ((e >> shift) & 31)) & 1u;
 
     ara_portfolio *p = new ara_portfolio();
     p->ctx = c;
@@ -389,7 +371,6 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
     d.cidx = p->d_cidx; d.rec_meta = p->d_rec_meta; d.srecs = p->d_srecs;
     d.any_terms = et ? 1u : 0u;
-    p->hit_frac = C ? (double)n_hit / (double)C : 0.0;
     *out = p;
     return ARA_OK;
 }
@@ -518,10 +499,11 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
     const bool exact = (flags & ARA_EXACT) != 0 && (flags & ARA_SU) != 0;
     CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
     if (!exact && p->dev.n_layers <= kSplitMaxLayers) {
-        // split path: per-trial hit regions sized 2x the expected hits per trial
+        // split path: per-trial pair regions sized 2x the expected pairs per trial
         // (+128) for uniformly drawn event ids; a trial that overflows its
         // region goes to the fused kernel
-        const double expect = p->hit_frac * (double)y->avg_len_x1000 / 1000.0;
+        const double per_occ = (double)p->dev.n_dev_records / (double)p->dev.catalog;
+        const double expect = per_occ * (double)y->avg_len_x1000 / 1000.0;
         uint32_t cap = (uint32_t)((2.0 * expect + 128.0 + 31.0) / 32.0) * 32u;
         if (cap > (1u << 20)) cap = 1u << 20;
         const uint64_t need = y->dev.n_trials * (uint64_t)cap;
@@ -723,6 +705,28 @@ int ara_draw_uniforms(ara_ctx *c, uint64_t seed, uint64_t n, const uint32_t *ctr
         if (e) code = fail(ARA_ECUDA, "ara_draw_uniforms: %s", cudaGetErrorString(e));
     }
     cudaFree(d_ctr); cudaFree(d_out);
+    return code;
+}
+
+int ara_normal_quantiles(ara_ctx *c, uint64_t n, const uint32_t *bits, float *v_out) {
+    if (!c) return fail(ARA_EINVAL, "ctx is NULL");
+    if (n == 0) return ARA_OK;
+    if (!bits || !v_out) return fail(ARA_EINVAL, "NULL argument");
+    CU(cudaSetDevice(c->device));
+    uint32_t *d_bits = nullptr;
+    float *d_out = nullptr;
+    int code = ARA_OK;
+    if (dalloc(&d_bits, n) || dalloc(&d_out, n)) {
+        cudaGetLastError();
+        code = fail(ARA_ENOMEM, "device allocation failed");
+    } else {
+        cudaError_t e = cudaMemcpyAsync(d_bits, bits, n * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream);
+        if (!e) e = launch_normal_quantiles(d_bits, n, d_out, c->stream);
+        if (!e) e = cudaMemcpyAsync(v_out, d_out, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream);
+        if (!e) e = cudaStreamSynchronize(c->stream);
+        if (e) code = fail(ARA_ECUDA, "ara_normal_quantiles: %s", cudaGetErrorString(e));
+    }
+    cudaFree(d_bits); cudaFree(d_out);
     return code;
 }
 

@@ -21,10 +21,6 @@ struct SlotInfo {
 
 struct LayerInfo {
     double occ_r, occ_l, agg_r, agg_l;
-    // split path: trial sums are accumulated in 64-bit fixed point (exact, so
-    // independent of summation order): g -> rint(g * fx_scale); fx_scale is a
-    // power of two with 2^24 events x the largest occurrence term < 2^61
-    double fx_scale, fx_inv;
 };
 
 // Per-record sampler constants, derived on the device in fp64 from the
@@ -106,10 +102,9 @@ struct RunStatus {
     unsigned int pad;
 };
 
-// the split (two-kernel) scan: compact_kernel writes each trial's hits
-// {event id, occurrence k} (events whose presence bit is set) to
-// hits[t * cap ...] and their count to counts[t] (kOverflow if more than cap);
-// sample_kernel looks them up in the index and samples the present pairs
+// the split (two-kernel) scan: compact_kernel writes each trial's present
+// pairs {device record, occurrence k} to pairs[t * cap ...] and their count to
+// counts[t] (kOverflow if more than cap); sample_kernel samples them
 constexpr uint32_t kOverflow = 0xffffffffu;
 constexpr uint32_t kSplitMaxLayers = 8;   // larger portfolios take the fused kernel
 struct SplitArgs {
@@ -121,11 +116,12 @@ struct SplitArgs {
     uint32_t *dbg_count;
     uint64_t *dbg_hash;
     RunStatus *status;
-    uint2 *hits;
+    uint2 *pairs;
     uint32_t cap;
     uint32_t *counts;
     uint32_t *redo;
     uint32_t pkey[20];        // Philox key schedule of the seed (round r: pkey[2r], pkey[2r+1])
+    uint32_t xcap;            // sample_kernel: pairs per segment (set by launch_sample)
 };
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);
@@ -151,6 +147,7 @@ cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, cons
                                  const float *zp,
                                  const float *ze, uint64_t n, bool exact, float *out,
                                  RunStatus *status, cudaStream_t s);
+cudaError_t launch_normal_quantiles(const uint32_t *bits, uint64_t n, float *out, cudaStream_t s);
 cudaError_t launch_draw_uniforms(uint64_t seed, const uint4 *ctr, uint64_t n, float *out,
                                  cudaStream_t s);
 

@@ -746,4 +746,17 @@ cudaError_t launch_draw_uniforms(uint64_t seed, const uint4 *ctr, uint64_t n, fl
     return cudaGetLastError();
 }
 
+__global__ void normal_quantiles_kernel(const uint32_t *bits, uint64_t n, float *out) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x)
+        out[t] = norm_quantile_from_bits(bits[t]);
+}
+
+cudaError_t launch_normal_quantiles(const uint32_t *bits, uint64_t n, float *out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t blocks = (n + 255) / 256;
+    normal_quantiles_kernel<<<(unsigned)(blocks < 1u << 20 ? blocks : 1u << 20), 256, 0, s>>>(bits, n, out);
+    return cudaGetLastError();
+}
+
 }  // namespace ara

@@ -54,12 +54,44 @@ __device__ __forceinline__ float u01_from_bits(uint32_t x) {
 }
 
 // Phi^-1(U(x)) on the smaller tail: z = (2m+1) 2^-24 and min(z, 1-z) are exact.
+// Phi^-1(t) = -sqrt(2) erfinv(1 - 2t); erfinv by Giles' single-precision
+// approximation ("Approximating the erfinv function", GPU Computing Gems,
+// 2011): w = -ln(1 - y^2), a degree-8 polynomial in w - 2.5 (w < 5) or in
+// sqrt(w) - 3, times y.  Over the 2^22 tail values of U the relative error is
+// <= 3e-7 (tests/test_gpu_parity.py), like erfcinvf's 4 ulp, at half the
+// instructions and without erfcinvf's divergent tail branch on most warps.
 __device__ __forceinline__ float norm_quantile_from_bits(uint32_t x) {
     const uint32_t m = x >> 9;
     const bool low = m < (1u << 22);
     const uint32_t num = low ? 2u * m + 1u : (1u << 24) - 2u * m - 1u;
     const float p2 = (float)num * 1.1920928955078125e-07f;   // 2 * tail, exact
-    const float r = 1.41421356237f * erfcinvf(p2);            // -Phi^-1(tail) >= 0
+    const float y = 1.0f - p2;                                // exact
+    float w = -__logf(p2 * (2.0f - p2));                      // -ln((1-y)(1+y))
+    float p;
+    if (w < 5.0f) {
+        w = w - 2.5f;
+        p = 2.81022636e-08f;
+        p = fmaf(p, w, 3.43273939e-07f);
+        p = fmaf(p, w, -3.5233877e-06f);
+        p = fmaf(p, w, -4.39150654e-06f);
+        p = fmaf(p, w, 0.00021858087f);
+        p = fmaf(p, w, -0.00125372503f);
+        p = fmaf(p, w, -0.00417768164f);
+        p = fmaf(p, w, 0.246640727f);
+        p = fmaf(p, w, 1.50140941f);
+    } else {
+        w = sqrtf(w) - 3.0f;
+        p = -0.000200214257f;
+        p = fmaf(p, w, 0.000100950558f);
+        p = fmaf(p, w, 0.00134934322f);
+        p = fmaf(p, w, -0.00367342844f);
+        p = fmaf(p, w, 0.00573950773f);
+        p = fmaf(p, w, -0.0076224613f);
+        p = fmaf(p, w, 0.00943887047f);
+        p = fmaf(p, w, 1.00167406f);
+        p = fmaf(p, w, 2.83297682f);
+    }
+    const float r = 1.41421356237f * (p * y);                 // -Phi^-1(tail) >= 0
     return low ? -r : r;
 }
 

@@ -68,6 +68,21 @@ def test_uniforms_bit_exact(A, ctx):
         assert float(u[t]) == ref
 
 
+# ---- row a4, step 2: v = Phi^-1(U(x)) as the kernels take it -------------------
+def test_normal_quantiles_vs_oracle(A, ctx):
+    # every tail value down to 2^-24 for the first 2^13 grid points of each
+    # tail, then a stride through the body; both halves of the 32-bit word
+    m = np.concatenate([np.arange(0, 1 << 13), np.arange(1 << 13, 1 << 22, 61)]).astype(np.uint64)
+    m = np.concatenate([m, (1 << 23) - 1 - m])
+    bits = (m << 9 | (m * 2654435761 & 0x1FF)).astype(np.uint32)      # low 9 bits are ignored
+    v = A.normal_quantiles(ctx, bits).astype(np.float64)
+    ref = np.array([oracle.norm_quantile((2.0 * float(x) + 1.0) * 2.0 ** -24) for x in m])
+    err = np.abs(v - ref)
+    # fp32 result: relative 4e-7 (erfcinvf's 4 ulp), absolute 1e-7 near v = 0
+    assert np.all(err <= 4e-7 * np.abs(ref) + 1e-7), f"worst {err.max()} at v={ref[err.argmax()]}"
+    assert np.all(np.sign(v) == np.sign(ref))
+
+
 # ---- rows a4-a6: the sampler ---------------------------------------------------
 def gen_records(n, seed=0):
     cfg = aragen.load_config("cfg3")

@@ -53,46 +53,43 @@ __device__ __forceinline__ float u01_from_bits(uint32_t x) {
     return (float)(2u * (x >> 9) + 1u) * 5.9604644775390625e-08f;
 }
 
-// Phi^-1(U(x)) on the smaller tail: z = (2m+1) 2^-24 and min(z, 1-z) are exact.
-// Phi^-1(t) = -sqrt(2) erfinv(1 - 2t); erfinv by Giles' single-precision
-// approximation ("Approximating the erfinv function", GPU Computing Gems,
-// 2011): w = -ln(1 - y^2), a degree-8 polynomial in w - 2.5 (w < 5) or in
-// sqrt(w) - 3, times y.  Over the 2^22 tail values of U the relative error is
-// <= 3e-7 (tests/test_gpu_parity.py), like erfcinvf's 4 ulp, at half the
-// instructions and without erfcinvf's divergent tail branch on most warps.
+// Phi^-1(U(x)) = sqrt(2) erfinv(y), y = 2 U(x) - 1 = (2m + 1 - 2^23) 2^-23
+// with m = x >> 9: exact in fp32, sign included, and 1 - y, 1 + y exact too.
+// erfinv by Giles' single-precision approximation ("Approximating the
+// erfinv function", GPU Computing Gems, 2011): w = -ln((1-y)(1+y)), a
+// degree-8 polynomial in w - 2.5 (w < 5) or in sqrt(w) - 3, times y; sqrt(2)
+// is folded into the coefficients.  Over the 2^23 values of U the relative
+// error is <= 4e-7 (tests/test_gpu_parity.py), like erfcinvf's 4 ulp, at about
+// half the instructions; the tail branch (|v| > 2.93) is taken by 0.34 % of draws.
 __device__ __forceinline__ float norm_quantile_from_bits(uint32_t x) {
-    const uint32_t m = x >> 9;
-    const bool low = m < (1u << 22);
-    const uint32_t num = low ? 2u * m + 1u : (1u << 24) - 2u * m - 1u;
-    const float p2 = (float)num * 1.1920928955078125e-07f;   // 2 * tail, exact
-    const float y = 1.0f - p2;                                // exact
-    float w = -__logf(p2 * (2.0f - p2));                      // -ln((1-y)(1+y))
-    float p;
+    const int yi = (int)((x >> 9) << 1) + 1 - (1 << 23);
+    const float y = (float)yi * 1.1920928955078125e-07f;      // exact
+    float w = -__logf((1.0f - y) * (1.0f + y));
+    float p;                                                  // sqrt(2) x Giles' coefficients
     if (w < 5.0f) {
         w = w - 2.5f;
-        p = 2.81022636e-08f;
-        p = fmaf(p, w, 3.43273939e-07f);
-        p = fmaf(p, w, -3.5233877e-06f);
-        p = fmaf(p, w, -4.39150654e-06f);
-        p = fmaf(p, w, 0.00021858087f);
-        p = fmaf(p, w, -0.00125372503f);
-        p = fmaf(p, w, -0.00417768164f);
-        p = fmaf(p, w, 0.246640727f);
-        p = fmaf(p, w, 1.50140941f);
+        p = 3.974260232e-08f;
+        p = fmaf(p, w, 4.854626601e-07f);
+        p = fmaf(p, w, -4.982822671e-06f);
+        p = fmaf(p, w, -6.210528108e-06f);
+        p = fmaf(p, w, 3.091200308e-04f);
+        p = fmaf(p, w, -1.773034941e-03f);
+        p = fmaf(p, w, -5.908134035e-03f);
+        p = fmaf(p, w, 3.488026612e-01f);
+        p = fmaf(p, w, 2.123313550e+00f);
     } else {
         w = sqrtf(w) - 3.0f;
-        p = -0.000200214257f;
-        p = fmaf(p, w, 0.000100950558f);
-        p = fmaf(p, w, 0.00134934322f);
-        p = fmaf(p, w, -0.00367342844f);
-        p = fmaf(p, w, 0.00573950773f);
-        p = fmaf(p, w, -0.0076224613f);
-        p = fmaf(p, w, 0.00943887047f);
-        p = fmaf(p, w, 1.00167406f);
-        p = fmaf(p, w, 2.83297682f);
+        p = -2.831457176e-04f;
+        p = fmaf(p, w, 1.427656483e-04f);
+        p = fmaf(p, w, 1.908259482e-03f);
+        p = fmaf(p, w, -5.195012320e-03f);
+        p = fmaf(p, w, 8.116889673e-03f);
+        p = fmaf(p, w, -1.077978815e-02f);
+        p = fmaf(p, w, 1.334857863e-02f);
+        p = fmaf(p, w, 1.416581041e+00f);
+        p = fmaf(p, w, 4.006434241e+00f);
     }
-    const float r = 1.41421356237f * (p * y);                 // -Phi^-1(tail) >= 0
-    return low ? -r : r;
+    return p * y;
 }
 
 // Phi^-1 of an arbitrary fp32 probability in (0,1) (component entry point)

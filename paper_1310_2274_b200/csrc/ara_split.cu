@@ -161,8 +161,9 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
         }
     };
     // stage B: pairs out.  One warp prefix sum of the pair counts; a present
-    // event has one pair in ~87 % of cases (cfg3), so its first pair is a
-    // predicated store and the rest a loop only when some lane needs it.
+    // event has one pair in ~87 % of cases (cfg3), so the first pairs are
+    // predicated stores and the rest one warp-uniform loop over the extra
+    // pairs (usually one pass).
     uint32_t n = 0;                                   // pairs of the current trial (warp-uniform)
     auto stage_b = [&](const ChunkA &S) {
         if (S.c == 0) n = 0;
@@ -174,21 +175,35 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         uint2 *out = A.pairs + (uint64_t)S.t * cap;
         uint32_t pos = n + incl - np;
+        if (n + tot <= cap) {                         // the chunk fits (warp-uniform)
+            uint2 *ob = out + pos;
+            uint32_t off[4], mx = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t f = S.ci[q].x, m = S.ci[q].y;
-            const uint32_t mm = min(m, cap > pos ? cap - pos : 0u);   // past the region: dropped
-            uint2 *o = out + pos;
-            if (mm != 0u) o[0] = make_uint2(f, k0 + q);
-            if (__any_sync(0xffffffffu, mm > 1u)) {
-#pragma unroll 1
-                for (uint32_t j = 1; j < mm; ++j) o[j] = make_uint2(f + j, k0 + q);
+            for (int q = 0; q < 4; ++q) {
+                off[q] = q == 0 ? 0u : off[q - 1] + S.ci[q - 1].y;
+                if (S.ci[q].y != 0u) ob[off[q]] = make_uint2(S.ci[q].x, k0 + q);
+                mx = max(mx, S.ci[q].y);
             }
-            pos += m;
+            mx = __reduce_max_sync(0xffffffffu, mx);
+#pragma unroll 1
+            for (uint32_t j = 1; j < mx; ++j)         // the events with several pairs
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (j < S.ci[q].y) ob[off[q] + j] = make_uint2(S.ci[q].x + j, k0 + q);
+        } else {                                      // overflow: the trial is redone by the fused kernel
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t f = S.ci[q].x, m = S.ci[q].y;
+#pragma unroll 1
+                for (uint32_t j = 0; j < m; ++j)
+                    if (pos + j < cap) out[pos + j] = make_uint2(f + j, k0 + q);
+                pos += m;
+            }
         }
-        n += __shfl_sync(0xffffffffu, incl, 31);
+        n += tot;
         if ((S.c + 1) * 128u >= S.len && lane == 0) {           // last chunk of the trial
             A.counts[S.t] = n <= cap ? n : kOverflow;
             if (n > cap) A.redo[atomicAdd(&A.status->n_redo, 1u)] = S.t;
@@ -241,7 +256,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 2 CTA
     SlotInfo *slots = reinterpret_cast<SlotInfo *>(smem);
     LayerInfo *layers = reinterpret_cast<LayerInfo *>(slots + ARA_MAX_SLOTS);
     const uint32_t kXCap = A.xcap;
-    float *xsw = reinterpret_cast<float *>(layers + ARA_MAX_LAYERS);              // [warps][kXCap]
+    uint32_t *xsw = reinterpret_cast<uint32_t *>(layers + ARA_MAX_LAYERS);        // [warps][kXCap]
     uint8_t *flw = reinterpret_cast<uint8_t *>(xsw + kSampleWarps * kXCap);       // [warps][kXCap]
     double *accw = reinterpret_cast<double *>(((uintptr_t)(flw + kSampleWarps * kXCap) + 7) & ~(uintptr_t)7);  // [warps][nl][32]
     unsigned int *cw = reinterpret_cast<unsigned int *>(accw + kSampleWarps * nl * 32);
@@ -253,7 +268,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 2 CTA
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (*A.yet.max_event >= A.pf.catalog) return;   // compact_kernel wrote no pairs
-    float *xs = xsw + warp * kXCap;
+    uint32_t *xs = xsw + warp * kXCap;                // loss bits | run end << 31
     uint8_t *fl = flw + warp * kXCap;
     double *accs = accw + warp * nl * 32 + lane;      // this lane's column: accs[l * 32]
     unsigned int *dc = cw + warp * nl;
@@ -353,10 +368,10 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 2 CTA
                                                         A.pf.rec_orig[e[u].x]);
                         atomicAdd(&dhs[layer], (unsigned long long)hv);
                     }
-                    if (live[u]) {
+                    if (live[u]) {                                // (losses are >= 0)
                         const uint32_t p = b + 32u * u + lane;
-                        xs[p] = x[u];
-                        fl[p] = (uint8_t)(((meta[u] >> 8) & 1u) | (layer << 1));
+                        xs[p] = (__float_as_uint(x[u]) & 0x7fffffffu) | ((meta[u] & 0x100u) << 23);
+                        if (!SL) fl[p] = (uint8_t)layer;
                     }
                 }
             }
@@ -367,19 +382,22 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 2 CTA
             double o = 0.0, head = 0.0;
             bool has_end = false;
             uint32_t head_layer = 0;
-            for (uint32_t i = i0; i < i1; ++i) {
-                o += (double)xs[i];
-                const uint32_t f = fl[i];
-                if (f & 1u) {
-                    if (!has_end) {
-                        head = o; head_layer = f >> 1; has_end = true;
-                    } else {
-                        const LayerInfo &L = layers[f >> 1];
-                        const double g = fmin(fmax(o - L.occ_r, 0.0), L.occ_l);
-                        if (SL) acc += g; else accs[(f >> 1) * 32] += g;
-                    }
-                    o = 0.0;
-                }
+            const double occ_r0 = layers[0].occ_r, occ_l0 = layers[0].occ_l;
+#pragma unroll 2
+            for (uint32_t i = i0; i < i1; ++i) {           // branch-free
+                const uint32_t q = xs[i];                  // loss bits | run end << 31
+                o += (double)__uint_as_float(q & 0x7fffffffu);
+                const bool end = (q >> 31) != 0u;
+                const uint32_t lay = SL ? 0u : (uint32_t)fl[i];
+                const double orr = SL ? occ_r0 : layers[lay].occ_r, oll = SL ? occ_l0 : layers[lay].occ_l;
+                const double g = fmin(fmax(o - orr, 0.0), oll);
+                const bool first = end && !has_end, inner = end && has_end;
+                head = first ? o : head;
+                head_layer = first ? lay : head_layer;
+                if (SL) acc += inner ? g : 0.0;
+                else if (inner) accs[lay * 32] += g;
+                has_end = has_end || end;
+                o = end ? 0.0 : o;
             }
             // join the runs that cross stretches: exclusive segmented sum over
             // lanes of the open tails (a lane with a run end starts a segment)

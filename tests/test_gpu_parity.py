@@ -249,6 +249,23 @@ def test_multi_layer_and_wide_masks(A, ctx, n_layers, J):
         ylt_check(g[li], ref, li)
 
 
+@pytest.mark.parametrize("n_layers,J,K", [(1, 2, 3000), (3, 4, 1500)])
+def test_long_trials_span_several_segments(A, ctx, n_layers, J, K):
+    # more present pairs per trial than one sampler segment holds (768 for one
+    # layer, fewer with more layers): occurrence runs and trial sums carry
+    # across segments; every trial still matches the oracle
+    cfg = aragen.load_config("cfg1")
+    terms = [[2e5 * (l + 1), 5e6, 1.0e6, 5.0e9] for l in range(n_layers)]
+    cfg.update(n_layers=n_layers, elts_per_layer=J, catalog=5000, records_per_elt=2000,
+               n_trials=40, events_per_trial=K, layer_terms=terms)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, 91)
+    assert cnt.sum(0).min() > 800                      # several segments per trial
+    assert np.array_equal(cnt, ref["count"]) and np.array_equal(hsh, ref["hash"])
+    for li in range(n_layers):
+        ylt_check(g[li], ref, li)
+
+
 def test_shared_elts_and_xelt_terms(A, ctx):
     cfg = aragen.load_config("cfg1")
     cfg.update(n_layers=1, elts_per_layer=4, catalog=2000, records_per_elt=500, n_trials=400,

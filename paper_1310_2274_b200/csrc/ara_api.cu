@@ -542,7 +542,8 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
     }
     CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
-    if (c->h_status->n_redo && !c->h_status->bad_event) {
+    const bool redo_launched = c->h_status->n_redo && !c->h_status->bad_event;
+    if (redo_launched) {
         // trials that met a table-less record: redo them with the fp64 kernel
         const unsigned int n_redo = c->h_status->n_redo;
         CU(cudaMemsetAsync(&c->d_status->next_trial, 0, sizeof(unsigned long long), c->stream));
@@ -559,7 +560,7 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         float a = 0, b = 0, r = 0;
         CU(cudaEventElapsedTime(&a, c->ev[0], c->ev[1]));
         CU(cudaEventElapsedTime(&b, c->ev[1], c->ev[2]));
-        CU(cudaEventElapsedTime(&r, c->ev[2], c->ev[3]));
+        if (redo_launched) CU(cudaEventElapsedTime(&r, c->ev[2], c->ev[3]));
         c->last_ms[0] = a; c->last_ms[1] = b; c->last_ms[2] = r;
     }
     if (c->h_status->bad_event) {      // error path: count the offending occurrences

@@ -71,7 +71,7 @@ __global__ void select_digit_kernel(SelectState *st, const unsigned int *hist, i
     st->pmask |= 0xffu << shift;
 }
 
-__global__ void compact_kernel(const float *vals, uint64_t n, SelectState *st, float *buf,
+__global__ void tail_compact_kernel(const float *vals, uint64_t n, SelectState *st, float *buf,
                                uint32_t cap) {
     const uint32_t T = st->prefix;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
@@ -286,7 +286,7 @@ cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_tota
         hist_kernel<<<blocks, 256, 0, s>>>(S.vals, n_total, S.state, shift, S.hist);
         select_digit_kernel<<<1, 32, 0, s>>>(S.state, S.hist, shift);
     }
-    compact_kernel<<<blocks, 256, 0, s>>>(S.vals, n_total, S.state, S.buf, kSortCap);
+    tail_compact_kernel<<<blocks, 256, 0, s>>>(S.vals, n_total, S.state, S.buf, kSortCap);
     uint32_t P = 1;
     while (P < k_need) P <<= 1;
     const size_t smem = sizeof(float) * (P < 1 ? 1 : P);

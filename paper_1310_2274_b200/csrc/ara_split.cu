@@ -95,21 +95,16 @@ struct ChunkA {                     // stage A output of one chunk
     uint32_t t, c, len;
 };
 
-__global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __grid_constant__ SplitArgs A) {
-    constexpr int kWarps = kCompactThreads / 32;
-    extern __shared__ __align__(16) unsigned char smem[];
-    uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);
-    const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift, cap = A.cap;
-    if (*A.yet.max_event >= C) {                      // out-of-range ids: nothing is read
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&A.status->bad_event, 1u);
-        return;
-    }
-    for (uint32_t t = threadIdx.x; t < A.pf.bitmap_words; t += blockDim.x) bitmap[t] = A.pf.bitmap[t];
-    __syncthreads();
-
+// The compaction pipeline of one warp over the trials first_warp, first_warp
+// + nw, ...  Sink: begin(t) -> the region for trial t's pairs (warp-uniform),
+// end(t, n) after its last chunk (n > cap: overflow).
+template <class Sink>
+__device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t *bitmap, uint32_t first_warp,
+                                              uint32_t nw, Sink &sink) {
     const int lane = threadIdx.x & 31;
+    const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift, cap = A.cap;
     const uint32_t n_trials = (uint32_t)A.yet.n_trials;    // <= 2^32 - 1 (ara_load_yet)
-    const uint32_t nw = gridDim.x * kWarps;
+    (void)C;
     const uint32_t *events = A.yet.events;
     const uint64_t *offsets = A.yet.offsets;
     const uint2 *__restrict__ cidx = A.pf.cidx;
@@ -117,7 +112,7 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
     const bool vec = offsets == nullptr && (K & 3u) == 0;   // every chunk 16 B aligned
 
     // fetch side: position in the flat chunk sequence (warp-uniform)
-    uint32_t pt = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    uint32_t pt = first_warp;
     uint32_t pc = 0, plen = 0;
     uint64_t pbase = 0;
     auto set_trial = [&]() {
@@ -165,6 +160,7 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
     // predicated stores and the rest one warp-uniform loop over the extra
     // pairs (usually one pass).
     uint32_t n = 0;                                   // pairs of the current trial (warp-uniform)
+    uint2 *out = nullptr;                             // the current trial's pair region
     auto stage_b = [&](const ChunkA &S) {
         if (S.c == 0) n = 0;
         const uint32_t k0 = S.c * 128u + 4u * lane;
@@ -176,7 +172,7 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
             if (lane >= o) incl += y;
         }
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        uint2 *out = A.pairs + (uint64_t)S.t * cap;
+        if (S.c == 0) out = sink.begin(S.t);
         uint32_t pos = n + incl - np;
         if (n + tot <= cap) {                         // the chunk fits (warp-uniform)
             uint2 *ob = out + pos;
@@ -204,10 +200,7 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
             }
         }
         n += tot;
-        if ((S.c + 1) * 128u >= S.len && lane == 0) {           // last chunk of the trial
-            A.counts[S.t] = n <= cap ? n : kOverflow;
-            if (n > cap) A.redo[atomicAdd(&A.status->n_redo, 1u)] = S.t;
-        }
+        if ((S.c + 1) * 128u >= S.len) sink.end(S.t, n);           // last chunk of the trial
     };
 
     set_trial();
@@ -230,6 +223,32 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
     }
 }
 
+// compact_kernel's sink: per-trial regions of HBM; counts[t] = pairs or kOverflow
+struct HbmSink {
+    const SplitArgs &A;
+    __device__ uint2 *begin(uint32_t t) const { return A.pairs + (uint64_t)t * A.cap; }
+    __device__ void end(uint32_t t, uint32_t n) const {
+        if ((threadIdx.x & 31) == 0) {
+            A.counts[t] = n <= A.cap ? n : kOverflow;
+            if (n > A.cap) A.redo[atomicAdd(&A.status->n_redo, 1u)] = t;
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __grid_constant__ SplitArgs A) {
+    constexpr int kWarps = kCompactThreads / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);
+    if (*A.yet.max_event >= A.pf.catalog) {           // out-of-range ids: nothing is read
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&A.status->bad_event, 1u);
+        return;
+    }
+    for (uint32_t t = threadIdx.x; t < A.pf.bitmap_words; t += blockDim.x) bitmap[t] = A.pf.bitmap[t];
+    __syncthreads();
+    HbmSink sink{A};
+    produce_pairs(A, bitmap, blockIdx.x * kWarps + (threadIdx.x >> 5), gridDim.x * kWarps, sink);
+}
+
 // ---------------------------------------------------------------------------
 // sample_kernel: one warp per trial (dynamic scheduler).  The trial's present
 // pairs {device record, k} (dense, (occurrence, slot) order, from
@@ -248,6 +267,194 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
 // sum), fp64; at the trial's end one warp sum per layer -> aggregate terms
 // (line 12) -> YLT (line 17).
 // ---------------------------------------------------------------------------
+// Per-warp shared-memory workspace of the sampler.
+struct SampleWs {
+    const SlotInfo *slots;
+    const LayerInfo *layers;
+    uint32_t *xs;                 // [xcap] loss bits | run end << 31
+    uint8_t *fl;                  // [xcap] layer (multi-layer portfolios)
+    double *accs;                 // this lane's column of [nl][32]
+    unsigned int *dc;             // [nl]
+    unsigned long long *dhs;      // [nl]
+};
+
+// The sampler on trial t's n present pairs at `in` (CG: read them through L2
+// only, as the fused kernel's consumers must).
+template <bool SU, bool SL, bool DBG, bool CG>
+__device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs &W, uint64_t t, uint32_t n,
+                                             const uint2 *in) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nl = A.pf.n_layers, kXCap = A.xcap;
+    const uint64_t n_trials = A.yet.n_trials;
+    const bool terms = A.pf.any_terms != 0;
+    const SlotInfo *slots = W.slots;
+    const LayerInfo *layers = W.layers;
+    uint32_t *xs = W.xs;
+    uint8_t *fl = W.fl;
+    double *accs = W.accs;
+    unsigned int *dc = W.dc;
+    unsigned long long *dhs = W.dhs;
+    const SplitRec *__restrict__ srecs = A.pf.srecs;
+    const float2 *__restrict__ hot = A.pf.hot;
+    const float2 *__restrict__ tables = A.pf.tables;
+    const uint32_t *__restrict__ rmeta = A.pf.rec_meta;
+    auto ldpair = [](const uint2 *q) { return CG ? __ldcg(q) : __ldcs(q); };
+    const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);
+    if (!SL)
+        for (uint32_t l = 0; l < nl; ++l) accs[l * 32] = 0.0;
+    if (DBG)
+        for (uint32_t l = lane; l < nl; l += 32) { dc[l] = 0u; dhs[l] = 0ull; }
+    double acc = 0.0;                              // SL: this lane's share of the trial sum
+    double carry = 0.0;                            // run open at the previous segment's end
+    int redo = 0;
+    uint2 pn[2];                                   // next round's pairs, prefetched
+#pragma unroll
+    for (int u = 0; u < 2; ++u) pn[u] = 32u * u + lane < n ? ldpair(in + 32u * u + lane) : make_uint2(0u, 0u);
+    for (uint32_t off = 0; off < n; off += kXCap) {
+        const uint32_t ns = min(n - off, kXCap);
+        // ---- rounds: x and run flags of every pair of the segment
+        for (uint32_t b = 0; b < ns; b += 64) {
+            uint2 e[2];
+            bool live[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                e[u] = pn[u];
+                live[u] = b + 32u * u + lane < ns;
+                const uint32_t q = off + b + 64u + 32u * u + lane;
+                pn[u] = q < n ? ldpair(in + q) : make_uint2(0u, 0u);
+            }
+            uint32_t meta[2];
+            float x[2];
+            if (SU) {
+                SplitRec r[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    r[u] = live[u] ? srecs[e[u].x] : SplitRec{0, 0, 0, 0, 0, kModeDegenerate << 28, 0, 0};
+                    meta[u] = r[u].meta;
+                }
+                float v[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t bp = philox_lane0_k(trial_g, e[u].y, r[u].prog, 1u, A.pkey);   // z_(Prog,E)
+                    const uint32_t be = philox_lane0_k(trial_g, e[u].y, r[u].elt, 2u, A.pkey);    // z_(E)
+                    v[u] = fmaf(r[u].wi, norm_quantile_from_bits(bp), r[u].wc * norm_quantile_from_bits(be));
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t mode = meta[u] >> 28;
+                    if (mode == kModeTable) {
+                        const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
+                        const int ti = min((int)uu, kTabNodes - 2);
+                        const float tt = uu - (float)ti;
+                        const bool in_hot = (unsigned)(ti - kHotJ0) < (unsigned)(kHotN - 1);
+                        const float2 *row = in_hot ? hot + (uint64_t)e[u].x * kHotN + (ti - kHotJ0)
+                                                   : tables + (uint64_t)e[u].x * kTabStride + ti;
+                        x[u] = r[u].scale * sigmoidf_(quintic_from_nodes(__ldg(row), __ldg(row + 1), ti, tt,
+                                                                         r[u].a, r[u].b));
+                    } else if (mode == kModeDegenerate) {
+                        x[u] = r[u].scale;
+                    } else {
+                        x[u] = 0.0f;              // table-less record: trial redone in fp64
+                        redo = 1;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    meta[u] = live[u] ? __ldg(rmeta + e[u].x) : 0u;
+                    x[u] = live[u] ? __ldg(A.pf.rec_mu + e[u].x) : 0.0f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t layer = (meta[u] >> 16) & 63u;
+                if (terms) {                                          // line 8 (G7)
+                    const SlotInfo &si = slots[meta[u] & 0xffu];
+                    if (si.has_terms) x[u] = si.share * fminf(fmaxf(x[u] - si.ret, 0.0f), si.lim);
+                }
+                if (DBG && live[u]) {
+                    atomicAdd(&dc[layer], 1u);
+                    const uint64_t hv = splitmix64_(splitmix64_(splitmix64_((uint64_t)e[u].y) ^
+                                                                slots[meta[u] & 0xffu].elt) ^
+                                                    A.pf.rec_orig[e[u].x]);
+                    atomicAdd(&dhs[layer], (unsigned long long)hv);
+                }
+                if (live[u]) {                                // (losses are >= 0)
+                    const uint32_t p = b + 32u * u + lane;
+                    xs[p] = (__float_as_uint(x[u]) & 0x7fffffffu) | ((meta[u] & 0x100u) << 23);
+                    if (!SL) fl[p] = (uint8_t)layer;
+                }
+            }
+        }
+        __syncwarp();
+        // ---- reduce: runs (line 9) and occurrence terms (line 11)
+        // (an odd stretch length keeps the lanes' reads on distinct banks)
+        const uint32_t per = ((ns + 31) / 32) | 1u, i0 = min(lane * per, ns), i1 = min(i0 + per, ns);
+        double o = 0.0, head = 0.0;
+        bool has_end = false;
+        uint32_t head_layer = 0;
+        const double occ_r0 = layers[0].occ_r, occ_l0 = layers[0].occ_l;
+#pragma unroll 2
+        for (uint32_t i = i0; i < i1; ++i) {           // branch-free
+            const uint32_t q = xs[i];                  // loss bits | run end << 31
+            o += (double)__uint_as_float(q & 0x7fffffffu);
+            const bool end = (q >> 31) != 0u;
+            const uint32_t lay = SL ? 0u : (uint32_t)fl[i];
+            const double orr = SL ? occ_r0 : layers[lay].occ_r, oll = SL ? occ_l0 : layers[lay].occ_l;
+            const double g = fmin(fmax(o - orr, 0.0), oll);
+            const bool first = end && !has_end, inner = end && has_end;
+            head = first ? o : head;
+            head_layer = first ? lay : head_layer;
+            if (SL) acc += inner ? g : 0.0;
+            else if (inner) accs[lay * 32] += g;
+            has_end = has_end || end;
+            o = end ? 0.0 : o;
+        }
+        // join the runs that cross stretches: exclusive segmented sum over
+        // lanes of the open tails (a lane with a run end starts a segment)
+        double v = o;                              // this lane's contribution to the run it leaves open
+        bool seg = has_end;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, v, d);
+            const bool ys = __shfl_up_sync(0xffffffffu, seg, d);
+            if (lane >= d && !seg) v += y;
+            if (lane >= d) seg = seg || ys;
+        }
+        // v = inclusive segmented sum; the run entering lane l is lane l-1's v (+ carry)
+        double in_run = __shfl_up_sync(0xffffffffu, v, 1);
+        const bool prev_seg = __shfl_up_sync(0xffffffffu, seg, 1);
+        if (lane == 0) in_run = 0.0;
+        if (lane == 0 || !prev_seg) in_run += carry;   // no run end before me in this segment
+        if (has_end) {
+            const LayerInfo &L = layers[head_layer];
+            const double g = fmin(fmax(head + in_run - L.occ_r, 0.0), L.occ_l);
+            if (SL) acc += g; else accs[head_layer * 32] += g;
+        }
+        // run left open at the segment's end (continues in the next segment)
+        const double last = has_end ? o : o + in_run;
+        carry = __shfl_sync(0xffffffffu, last, 31);
+        __syncwarp();
+    }
+    redo = __any_sync(0xffffffffu, redo);
+    if (redo) {
+        if (lane == 0) A.redo[atomicAdd(&A.status->n_redo, 1u)] = (uint32_t)t;
+        return;
+    }
+    // aggregate terms (line 12, G6) -> YLT (line 17)
+    for (uint32_t l = 0; l < nl; ++l) {
+        const double S = warp_sum_f64_(SL ? acc : accs[l * 32]);   // fixed tree
+        if (lane == 0) {
+            const LayerInfo &L = layers[l];
+            A.ylt[(uint64_t)l * n_trials + t] = (float)fmin(fmax(S - L.agg_r, 0.0), L.agg_l);
+            if (DBG) {
+                if (A.dbg_count) A.dbg_count[(uint64_t)l * n_trials + t] = dc[l];
+                if (A.dbg_hash) A.dbg_hash[(uint64_t)l * n_trials + t] = dhs[l];
+            }
+        }
+    }
+}
+
 template <bool SU, bool SL, bool DBG>
 __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 2 CTAs/SM: <= 64 registers
     sample_kernel(const __grid_constant__ SplitArgs A) {
@@ -268,180 +475,16 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 2 CTA
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (*A.yet.max_event >= A.pf.catalog) return;   // compact_kernel wrote no pairs
-    uint32_t *xs = xsw + warp * kXCap;                // loss bits | run end << 31
-    uint8_t *fl = flw + warp * kXCap;
-    double *accs = accw + warp * nl * 32 + lane;      // this lane's column: accs[l * 32]
-    unsigned int *dc = cw + warp * nl;
-    unsigned long long *dhs = hw + warp * nl;
-    const uint64_t n_trials = A.yet.n_trials;
-    const bool terms = A.pf.any_terms != 0;
-    const SplitRec *__restrict__ srecs = A.pf.srecs;
-    const float2 *__restrict__ hot = A.pf.hot;
-    const float2 *__restrict__ tables = A.pf.tables;
-    const uint32_t *__restrict__ rmeta = A.pf.rec_meta;
-
+    const SampleWs W{slots, layers, xsw + warp * kXCap, flw + warp * kXCap, accw + warp * nl * 32 + lane,
+                     cw + warp * nl, hw + warp * nl};
     while (true) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(&A.status->next_trial2, 1ull);
         t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= n_trials) break;
+        if (t >= A.yet.n_trials) break;
         const uint32_t n = __ldg(A.counts + t);
         if (n == kOverflow) continue;                 // redone by the fused kernel
-        const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);
-        const uint2 *in = A.pairs + t * (uint64_t)A.cap;
-        if (!SL)
-            for (uint32_t l = 0; l < nl; ++l) accs[l * 32] = 0.0;
-        if (DBG)
-            for (uint32_t l = lane; l < nl; l += 32) { dc[l] = 0u; dhs[l] = 0ull; }
-        double acc = 0.0;                              // SL: this lane's share of the trial sum
-        double carry = 0.0;                            // run open at the previous segment's end
-        int redo = 0;
-        uint2 pn[2];                                   // next round's pairs, prefetched
-#pragma unroll
-        for (int u = 0; u < 2; ++u) pn[u] = 32u * u + lane < n ? __ldcs(in + 32u * u + lane) : make_uint2(0u, 0u);
-        for (uint32_t off = 0; off < n; off += kXCap) {
-            const uint32_t ns = min(n - off, kXCap);
-            // ---- rounds: x and run flags of every pair of the segment
-            for (uint32_t b = 0; b < ns; b += 64) {
-                uint2 e[2];
-                bool live[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    e[u] = pn[u];
-                    live[u] = b + 32u * u + lane < ns;
-                    const uint32_t q = off + b + 64u + 32u * u + lane;
-                    pn[u] = q < n ? __ldcs(in + q) : make_uint2(0u, 0u);
-                }
-                uint32_t meta[2];
-                float x[2];
-                if (SU) {
-                    SplitRec r[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        r[u] = live[u] ? srecs[e[u].x] : SplitRec{0, 0, 0, 0, 0, kModeDegenerate << 28, 0, 0};
-                        meta[u] = r[u].meta;
-                    }
-                    float v[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const uint32_t bp = philox_lane0_k(trial_g, e[u].y, r[u].prog, 1u, A.pkey);   // z_(Prog,E)
-                        const uint32_t be = philox_lane0_k(trial_g, e[u].y, r[u].elt, 2u, A.pkey);    // z_(E)
-                        v[u] = fmaf(r[u].wi, norm_quantile_from_bits(bp), r[u].wc * norm_quantile_from_bits(be));
-                    }
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const uint32_t mode = meta[u] >> 28;
-                        if (mode == kModeTable) {
-                            const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
-                            const int ti = min((int)uu, kTabNodes - 2);
-                            const float tt = uu - (float)ti;
-                            const bool in_hot = (unsigned)(ti - kHotJ0) < (unsigned)(kHotN - 1);
-                            const float2 *row = in_hot ? hot + (uint64_t)e[u].x * kHotN + (ti - kHotJ0)
-                                                       : tables + (uint64_t)e[u].x * kTabStride + ti;
-                            x[u] = r[u].scale * sigmoidf_(quintic_from_nodes(__ldg(row), __ldg(row + 1), ti, tt,
-                                                                             r[u].a, r[u].b));
-                        } else if (mode == kModeDegenerate) {
-                            x[u] = r[u].scale;
-                        } else {
-                            x[u] = 0.0f;              // table-less record: trial redone in fp64
-                            redo = 1;
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        meta[u] = live[u] ? __ldg(rmeta + e[u].x) : 0u;
-                        x[u] = live[u] ? __ldg(A.pf.rec_mu + e[u].x) : 0.0f;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const uint32_t layer = (meta[u] >> 16) & 63u;
-                    if (terms) {                                          // line 8 (G7)
-                        const SlotInfo &si = slots[meta[u] & 0xffu];
-                        if (si.has_terms) x[u] = si.share * fminf(fmaxf(x[u] - si.ret, 0.0f), si.lim);
-                    }
-                    if (DBG && live[u]) {
-                        atomicAdd(&dc[layer], 1u);
-                        const uint64_t hv = splitmix64_(splitmix64_(splitmix64_((uint64_t)e[u].y) ^
-                                                                    slots[meta[u] & 0xffu].elt) ^
-                                                        A.pf.rec_orig[e[u].x]);
-                        atomicAdd(&dhs[layer], (unsigned long long)hv);
-                    }
-                    if (live[u]) {                                // (losses are >= 0)
-                        const uint32_t p = b + 32u * u + lane;
-                        xs[p] = (__float_as_uint(x[u]) & 0x7fffffffu) | ((meta[u] & 0x100u) << 23);
-                        if (!SL) fl[p] = (uint8_t)layer;
-                    }
-                }
-            }
-            __syncwarp();
-            // ---- reduce: runs (line 9) and occurrence terms (line 11)
-            // (an odd stretch length keeps the lanes' reads on distinct banks)
-            const uint32_t per = ((ns + 31) / 32) | 1u, i0 = min(lane * per, ns), i1 = min(i0 + per, ns);
-            double o = 0.0, head = 0.0;
-            bool has_end = false;
-            uint32_t head_layer = 0;
-            const double occ_r0 = layers[0].occ_r, occ_l0 = layers[0].occ_l;
-#pragma unroll 2
-            for (uint32_t i = i0; i < i1; ++i) {           // branch-free
-                const uint32_t q = xs[i];                  // loss bits | run end << 31
-                o += (double)__uint_as_float(q & 0x7fffffffu);
-                const bool end = (q >> 31) != 0u;
-                const uint32_t lay = SL ? 0u : (uint32_t)fl[i];
-                const double orr = SL ? occ_r0 : layers[lay].occ_r, oll = SL ? occ_l0 : layers[lay].occ_l;
-                const double g = fmin(fmax(o - orr, 0.0), oll);
-                const bool first = end && !has_end, inner = end && has_end;
-                head = first ? o : head;
-                head_layer = first ? lay : head_layer;
-                if (SL) acc += inner ? g : 0.0;
-                else if (inner) accs[lay * 32] += g;
-                has_end = has_end || end;
-                o = end ? 0.0 : o;
-            }
-            // join the runs that cross stretches: exclusive segmented sum over
-            // lanes of the open tails (a lane with a run end starts a segment)
-            double v = o;                              // this lane's contribution to the run it leaves open
-            bool seg = has_end;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, v, d);
-                const bool ys = __shfl_up_sync(0xffffffffu, seg, d);
-                if (lane >= d && !seg) v += y;
-                if (lane >= d) seg = seg || ys;
-            }
-            // v = inclusive segmented sum; the run entering lane l is lane l-1's v (+ carry)
-            double in_run = __shfl_up_sync(0xffffffffu, v, 1);
-            const bool prev_seg = __shfl_up_sync(0xffffffffu, seg, 1);
-            if (lane == 0) in_run = 0.0;
-            if (lane == 0 || !prev_seg) in_run += carry;   // no run end before me in this segment
-            if (has_end) {
-                const LayerInfo &L = layers[head_layer];
-                const double g = fmin(fmax(head + in_run - L.occ_r, 0.0), L.occ_l);
-                if (SL) acc += g; else accs[head_layer * 32] += g;
-            }
-            // run left open at the segment's end (continues in the next segment)
-            const double last = has_end ? o : o + in_run;
-            carry = __shfl_sync(0xffffffffu, last, 31);
-            __syncwarp();
-        }
-        redo = __any_sync(0xffffffffu, redo);
-        if (redo) {
-            if (lane == 0) A.redo[atomicAdd(&A.status->n_redo, 1u)] = (uint32_t)t;
-            continue;
-        }
-        // aggregate terms (line 12, G6) -> YLT (line 17)
-        for (uint32_t l = 0; l < nl; ++l) {
-            const double S = warp_sum_f64_(SL ? acc : accs[l * 32]);   // fixed tree
-            if (lane == 0) {
-                const LayerInfo &L = layers[l];
-                A.ylt[(uint64_t)l * n_trials + t] = (float)fmin(fmax(S - L.agg_r, 0.0), L.agg_l);
-                if (DBG) {
-                    if (A.dbg_count) A.dbg_count[(uint64_t)l * n_trials + t] = dc[l];
-                    if (A.dbg_hash) A.dbg_hash[(uint64_t)l * n_trials + t] = dhs[l];
-                }
-            }
-        }
+        sample_trial<SU, SL, DBG, false>(A, W, t, n, A.pairs + t * (uint64_t)A.cap);
         __syncwarp();
     }
 }

@@ -105,7 +105,7 @@ def main():
                              "source": f"profiles/{a.tag}_{short}.json ({os.path.basename(a.rep)})"}
     if a.write_const:
         consts["source"] = f"profiles/{a.tag}_*.json"
-        consts["note"] = "ncu --set full, one launch of each kernel on cfg3's first 100k trials"
+        consts["note"] = "ncu --set full --clock-control none, one launch of each kernel on the first 200k trials of cfg3 (tools/capture_profiles.sh)"
         with open(consts_path, "w") as f:
             json.dump(consts, f, indent=1)
 

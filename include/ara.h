@@ -50,6 +50,10 @@ extern "C" {
 #define ARA_EXACT 4u         /* solve every beta quantile per sample in fp64
                                 instead of the per-record quantile tables
                                 (validation mode; slow)                    */
+#define ARA_FUSED 8u         /* run compaction and sampling in one warp-
+                                specialised kernel (pairs in an L2-resident
+                                ring) instead of two kernels; same results
+                                bit for bit.  Round 1: slower */
 
 /* ---- limits (validated) ------------------------------------------------ */
 #define ARA_MAX_SLOTS 224    /* sum over layers of XELTs per layer          */

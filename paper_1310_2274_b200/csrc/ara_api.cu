@@ -489,7 +489,8 @@ void ara_yet_destroy(ara_yet *y) {
 int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
             float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash) {
     if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
-    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT)) return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
+    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_FUSED))
+        return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
     if (y->dev.n_trials == 0) return ARA_OK;
     if (!ylt) return fail(ARA_EINVAL, "ylt is NULL");
     if ((dbg_count || dbg_hash) && !(flags & ARA_DEBUG_LOOKUP))
@@ -506,7 +507,11 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         const double expect = per_occ * (double)y->avg_len_x1000 / 1000.0;
         uint32_t cap = (uint32_t)((2.0 * expect + 128.0 + 31.0) / 32.0) * 32u;
         if (cap > (1u << 20)) cap = 1u << 20;
-        const uint64_t need = y->dev.n_trials * (uint64_t)cap;
+        // two kernels (compaction, then sampling); ARA_FUSED asks for the
+        // warp-specialised single kernel (if the portfolio fits its shared memory)
+        const uint64_t ring = (flags & ARA_FUSED) ? fused_ring_pairs(p->dev, cap, c->num_sms) : 0;
+        const bool fused = ring != 0;
+        const uint64_t need = fused ? ring : y->dev.n_trials * (uint64_t)cap;
         if (c->pairs_capacity < need) {          // scratch grows once, then is reused
             cudaFree(c->d_pairs);
             c->d_pairs = nullptr;
@@ -528,9 +533,9 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
             S.pkey[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;
         }
         CU(cudaEventRecord(c->ev[0], c->stream));
-        CU(launch_compact(S, c->stream, c->num_sms));
+        if (!fused) CU(launch_compact(S, c->stream, c->num_sms));
         CU(cudaEventRecord(c->ev[1], c->stream));
-        CU(launch_sample(S, c->stream, c->num_sms));
+        CU(fused ? launch_fused(S, c->stream, c->num_sms) : launch_sample(S, c->stream, c->num_sms));
         CU(cudaEventRecord(c->ev[2], c->stream));
     } else {
         // ARA_EXACT (fp64 solve for every sample) or > kSplitMaxLayers layers: the fused kernel

@@ -30,12 +30,15 @@ namespace {
 #endif
 constexpr int kCompactThreads = ARA_COMPACT_THREADS;   // compaction: 1 CTA per SM (bitmap in shared memory)
 #ifndef ARA_SAMPLE_WARPS
-#define ARA_SAMPLE_WARPS 16
+#define ARA_SAMPLE_WARPS 32
 #endif
 #ifndef ARA_SAMPLE_MINB
-#define ARA_SAMPLE_MINB 2
+#define ARA_SAMPLE_MINB 1
 #endif
-constexpr int kSampleWarps = ARA_SAMPLE_WARPS;   // sampling: 2 CTAs of 512 threads per SM
+constexpr int kSampleWarps = ARA_SAMPLE_WARPS;   // sampling: 1 CTA of 1024 threads per SM
+#ifndef ARA_SAMPLE_SMEM_KB
+#define ARA_SAMPLE_SMEM_KB 96
+#endif
 constexpr uint32_t kXCapMax = 1024;     // pairs per sampler segment (a multiple of 64, >= ARA_MAX_SLOTS,
                                         // sized at launch to what 2 CTAs/SM leave in shared memory)
 
@@ -95,6 +98,13 @@ struct ChunkA {                     // stage A output of one chunk
     uint32_t t, c, len;
 };
 
+// predicated 8-byte store {a, b} to a global address (no branch)
+__device__ __forceinline__ void st_pair_if(bool p, uint64_t addr, uint32_t a, uint32_t b) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.global.v2.u32 [%1], {%2, %3};\n}" ::"r"((uint32_t)p),
+                 "l"(addr), "r"(a), "r"(b)
+                 : "memory");
+}
+
 // The compaction pipeline of one warp over the trials first_warp, first_warp
 // + nw, ...  Sink: begin(t) -> the region for trial t's pairs (warp-uniform),
 // end(t, n) after its last chunk (n > cap: overflow).
@@ -122,7 +132,7 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         }
     };
     auto fetch = [&](RawChunk &r) {
-        r.t = pt; r.c = pc; r.len = plen;
+        r.t = pt; r.c = pc; r.len = pt < n_trials ? plen : 0u;    // (no events past the last trial)
         r.v = make_uint4(0u, 0u, 0u, 0u);
         if (pt < n_trials) {
             const uint32_t k = pc * 128u + 4u * lane;
@@ -147,7 +157,7 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         for (int q = 0; q < 4; ++q) {
             const uint32_t bit = ee[q] >> shift;
             const uint32_t w = bitmap[bit >> 5];
-            const bool hit = r.t < n_trials && k0 + q < r.len && ((w >> (bit & 31)) & 1u);
+            const bool hit = k0 + q < r.len && ((w >> (bit & 31)) & 1u);
             S.ci[q] = make_uint2(0u, 0u);
             asm volatile(                                 // predicated load, no branch
                 "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.nc.v2.u32 {%0, %1}, [%3];\n}"
@@ -175,20 +185,22 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         if (S.c == 0) out = sink.begin(S.t);
         uint32_t pos = n + incl - np;
         if (n + tot <= cap) {                         // the chunk fits (warp-uniform)
-            uint2 *ob = out + pos;
-            uint32_t off[4], mx = 0;
+            // one 64-bit address per event, predicated stores (no branches)
+            uint64_t adr[4];
+            uint32_t mx = 0, o = 0;
+            const uint64_t base = reinterpret_cast<uint64_t>(out + pos);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                off[q] = q == 0 ? 0u : off[q - 1] + S.ci[q - 1].y;
-                if (S.ci[q].y != 0u) ob[off[q]] = make_uint2(S.ci[q].x, k0 + q);
+                adr[q] = base + 8u * o;
+                st_pair_if(S.ci[q].y != 0u, adr[q], S.ci[q].x, k0 + q);
+                o += S.ci[q].y;
                 mx = max(mx, S.ci[q].y);
             }
             mx = __reduce_max_sync(0xffffffffu, mx);
 #pragma unroll 1
             for (uint32_t j = 1; j < mx; ++j)         // the events with several pairs
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (j < S.ci[q].y) ob[off[q] + j] = make_uint2(S.ci[q].x + j, k0 + q);
+                for (int q = 0; q < 4; ++q) st_pair_if(j < S.ci[q].y, adr[q] + 8u * j, S.ci[q].x + j, k0 + q);
         } else {                                      // overflow: the trial is redone by the fused kernel
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -456,7 +468,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
 }
 
 template <bool SU, bool SL, bool DBG>
-__global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 2 CTAs/SM: <= 64 registers
+__global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 warps/SM: <= 64 registers
     sample_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t nl = A.pf.n_layers;
@@ -486,6 +498,125 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 2 CTA
         if (n == kOverflow) continue;                 // redone by the fused kernel
         sample_trial<SU, SL, DBG, false>(A, W, t, n, A.pairs + t * (uint64_t)A.cap);
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fused_kernel: the same two stages in one persistent kernel, one CTA (32
+// warps) per SM, warp-specialised.  kNP producer warps (the highest warp ids,
+// which the SM's issue arbiter favours) run produce_pairs over the trials
+// blockIdx.x * kNP + w, + gridDim.x * kNP, ...; each trial's pairs go to the
+// next slot of this CTA's ring of kRing pair regions in global memory (small
+// enough to stay in L2).  The other warps consume the slots in order and run
+// sample_trial on them.  A slot's state word carries the ring index it is
+// free for or full with (2i: free for index i, 2i + 1: full with index i), so
+// producers and consumers that race ahead never take a slot meant for another
+// lap.  Compaction (latency-bound) and sampling (issue-bound) so overlap on
+// every SM, and the pairs never travel to HBM.
+// ---------------------------------------------------------------------------
+#ifndef ARA_FUSED_PRODUCERS
+#define ARA_FUSED_PRODUCERS 8
+#endif
+constexpr int kNP = ARA_FUSED_PRODUCERS;            // producer warps per CTA
+constexpr int kNC = 32 - kNP;                       // consumer warps per CTA
+constexpr uint32_t kRing = 2 * kNC;                 // pair regions per CTA
+
+struct FusedQueue {
+    uint32_t prod_next, cons_next, prod_done, pad;
+    uint32_t state[kRing];
+    uint2 meta[kRing];                              // (trial, pairs or kOverflow)
+};
+
+struct RingSink {
+    const SplitArgs &A;
+    FusedQueue &Q;
+    uint2 *ring;                                    // this CTA's kRing regions of cap pairs
+    uint32_t ps = 0, idx = 0;                       // slot and ring index of the current trial
+    __device__ uint2 *begin(uint32_t) {
+        const int lane = threadIdx.x & 31;
+        uint32_t i = 0;
+        if (lane == 0) {
+            i = atomicAdd(&Q.prod_next, 1u);
+            volatile uint32_t *st = &Q.state[i % kRing];
+            while (*st != 2u * i) __nanosleep(64);   // free for this lap
+        }
+        idx = __shfl_sync(0xffffffffu, i, 0);
+        ps = idx % kRing;
+        __syncwarp();
+        return ring + (uint64_t)ps * A.cap;
+    }
+    __device__ void end(uint32_t t, uint32_t n) {
+        __threadfence_block();                      // this lane's pair stores before the flag
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+            const bool over = n > A.cap;
+            if (over) A.redo[atomicAdd(&A.status->n_redo, 1u)] = t;
+            Q.meta[ps] = make_uint2(t, over ? kOverflow : n);
+            __threadfence_block();
+            *(volatile uint32_t *)&Q.state[ps] = 2u * idx + 1u;
+        }
+        __syncwarp();
+    }
+};
+
+template <bool SU, bool SL, bool DBG>
+__global__ void __launch_bounds__(1024, 1) fused_kernel(const __grid_constant__ SplitArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t nl = A.pf.n_layers, kXCap = A.xcap;
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);
+    FusedQueue *Qp = reinterpret_cast<FusedQueue *>(smem + ((A.pf.bitmap_words * 4u + 15u) & ~15u));
+    SlotInfo *slots = reinterpret_cast<SlotInfo *>(Qp + 1);
+    LayerInfo *layers = reinterpret_cast<LayerInfo *>(slots + ARA_MAX_SLOTS);
+    double *accw = reinterpret_cast<double *>(layers + ARA_MAX_LAYERS);           // [kNC][nl][32]
+    unsigned long long *hw = reinterpret_cast<unsigned long long *>(accw + kNC * nl * 32);   // [kNC][nl]
+    unsigned int *cw = reinterpret_cast<unsigned int *>(hw + kNC * nl);          // [kNC][nl]
+    uint32_t *xsw = cw + kNC * nl;                                              // [kNC][kXCap]
+    uint8_t *flw = reinterpret_cast<uint8_t *>(xsw + kNC * kXCap);               // [kNC][kXCap]
+    if (*A.yet.max_event >= A.pf.catalog) {           // out-of-range ids: nothing is read
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&A.status->bad_event, 1u);
+        return;
+    }
+    FusedQueue &Q = *Qp;
+    for (uint32_t t = threadIdx.x; t < A.pf.bitmap_words; t += blockDim.x) bitmap[t] = A.pf.bitmap[t];
+    for (uint32_t t = threadIdx.x; t < A.pf.n_slots; t += blockDim.x) slots[t] = A.pf.slots[t];
+    for (uint32_t t = threadIdx.x; t < nl; t += blockDim.x) layers[t] = A.pf.layers[t];
+    for (uint32_t t = threadIdx.x; t < kRing; t += blockDim.x) Q.state[t] = 2u * t;   // free for lap 0
+    if (threadIdx.x == 0) { Q.prod_next = 0u; Q.cons_next = 0u; Q.prod_done = 0u; }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint2 *ring = A.pairs + (uint64_t)blockIdx.x * kRing * A.cap;
+    if (warp >= kNC) {                                // ---- producer
+        RingSink sink{A, Q, ring};
+        produce_pairs(A, bitmap, blockIdx.x * kNP + (warp - kNC), gridDim.x * kNP, sink);
+        __syncwarp();
+        if (lane == 0) atomicAdd(&Q.prod_done, 1u);
+        return;
+    }
+    // ---- consumer
+    const SampleWs W{slots, layers, xsw + warp * kXCap, flw + warp * kXCap, accw + warp * nl * 32 + lane,
+                     cw + warp * nl, hw + warp * nl};
+    while (true) {
+        uint32_t i = 0, go = 0;
+        if (lane == 0) {
+            i = atomicAdd(&Q.cons_next, 1u);
+            volatile uint32_t *st = &Q.state[i % kRing];
+            volatile uint32_t *done = &Q.prod_done, *pn = &Q.prod_next;
+            while (true) {
+                if (*st == 2u * i + 1u) { go = 1; break; }
+                if (*done == (uint32_t)kNP && i >= *pn) break;    // nothing more will come
+                __nanosleep(128);
+            }
+            __threadfence_block();
+        }
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (!__shfl_sync(0xffffffffu, go, 0)) break;
+        const uint32_t ps = i % kRing;
+        const uint2 m = Q.meta[ps];
+        if (m.y != kOverflow)
+            sample_trial<SU, SL, DBG, true>(A, W, m.x, m.y, ring + (uint64_t)ps * A.cap);
+        __syncwarp();
+        if (lane == 0) *(volatile uint32_t *)&Q.state[ps] = 2u * (i + kRing);   // free for the next lap
     }
 }
 
@@ -567,7 +698,9 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
     const size_t other = sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
                          sizeof(double) * kSampleWarps * A.pf.n_layers * 32 +
                          kSampleWarps * A.pf.n_layers * (sizeof(unsigned int) + sizeof(unsigned long long)) + 16;
-    const size_t budget = 113 * 1024;                    // 2 CTAs per SM
+    // shared memory left unclaimed is L1 data cache, which the record and table
+    // gathers use: keep the segments short
+    const size_t budget = (size_t)ARA_SAMPLE_SMEM_KB * 1024;
     SplitArgs B = A;
     B.xcap = (uint32_t)std::min<size_t>(kXCapMax, (budget - other - 8) / (5 * kSampleWarps) / 64 * 64);
     if (B.xcap < ARA_MAX_SLOTS) B.xcap = (ARA_MAX_SLOTS + 63) / 64 * 64;
@@ -584,6 +717,44 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     kern<<<num_sms * per_sm, kSampleWarps * 32, smem, s>>>(B);
+    return cudaGetLastError();
+}
+
+// Shared memory of fused_kernel for a portfolio, and the sampler segment it
+// leaves room for (0: does not fit; the two-kernel path is used).
+static size_t fused_smem(const PortfolioDev &pf, uint32_t &xcap) {
+    const size_t fixed = ((pf.bitmap_words * 4u + 15u) & ~15u) + sizeof(FusedQueue) +
+                         sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
+                         (sizeof(double) + sizeof(unsigned long long) + sizeof(unsigned int)) * kNC * pf.n_layers * 32;
+    const size_t budget = 227 * 1024;
+    xcap = 0;
+    if (pf.n_layers > kSplitMaxLayers || fixed + 64 >= budget) return 0;
+    const size_t x = (budget - fixed - 64) / ((sizeof(uint32_t) + sizeof(uint8_t)) * kNC) / 64 * 64;
+    if (x < 256) return 0;
+    xcap = (uint32_t)std::min<size_t>(x, kXCapMax);
+    return fixed + (sizeof(uint32_t) + sizeof(uint8_t)) * kNC * xcap + 16;
+}
+
+uint64_t fused_ring_pairs(const PortfolioDev &pf, uint32_t cap, int num_sms) {
+    uint32_t xcap = 0;
+    if (!fused_smem(pf, xcap)) return 0;
+    return (uint64_t)num_sms * kRing * cap;
+}
+
+cudaError_t launch_fused(const SplitArgs &A, cudaStream_t s, int num_sms) {
+    const bool dbg = (A.flags & ARA_DEBUG_LOOKUP) != 0, su = (A.flags & ARA_SU) != 0;
+    const bool sl = A.pf.n_layers == 1;
+    SplitArgs B = A;
+    const size_t smem = fused_smem(A.pf, B.xcap);
+    if (!smem) return cudaErrorInvalidValue;
+    using K = void (*)(SplitArgs);
+    const K kern = su ? (sl ? (dbg ? (K)fused_kernel<true, true, true> : (K)fused_kernel<true, true, false>)
+                            : (dbg ? (K)fused_kernel<true, false, true> : (K)fused_kernel<true, false, false>))
+                      : (sl ? (dbg ? (K)fused_kernel<false, true, true> : (K)fused_kernel<false, true, false>)
+                            : (dbg ? (K)fused_kernel<false, false, true> : (K)fused_kernel<false, false, false>));
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    kern<<<num_sms, 1024, smem, s>>>(B);
     return cudaGetLastError();
 }
 

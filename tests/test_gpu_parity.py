@@ -323,6 +323,23 @@ def test_determinism_and_sharding(A, ctx):
     assert np.array_equal(np.concatenate(parts, axis=1), a)
 
 
+@pytest.mark.parametrize("n_layers,J,K", [(1, 16, 1000), (3, 4, 1500)])
+def test_fused_and_two_kernel_identical(A, ctx, n_layers, J, K):
+    # the warp-specialised kernel and the two-kernel form process each trial
+    # in the same order: bit-identical YLT, counts and hashes
+    cfg = aragen.load_config("cfg3")
+    terms = [[2e5 * (l + 1), 5e6, 1.0e6, 5.0e9] for l in range(n_layers)]
+    cfg.update(n_layers=n_layers, elts_per_layer=J, n_trials=20000, events_per_trial=K, layer_terms=terms)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P = A.Portfolio(ctx, pf)
+    Y = A.Yet.from_dict(ctx, yet)
+    for su in (True, False):
+        f = A.run(ctx, P, Y, seed=5, su=su, debug=True, fused=True)
+        t = A.run(ctx, P, Y, seed=5, su=su, debug=True)
+        for x, y in zip(f, t):
+            assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
+
+
 def test_event_out_of_range(A, ctx):
     cfg = aragen.load_config("cfg1")
     pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg, n_trials=10)

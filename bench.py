@@ -255,16 +255,33 @@ def run_ours(args, cfg, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed, scan_avg = float(t[0]), float(t[1])
 
-    # ---- e2e: the same step through the public API from pinned host memory
+    # ---- e2e: the same step through the public API from pinned host memory.
+    # Every step copies its YET host -> device and reads its YLT back; the
+    # copies run on a second stream into a second device YET, so step s+1's
+    # H2D overlaps step s's kernels (double buffering).
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 5))
+    copy_stream = torch.cuda.Stream(dev)
+    ctx_copy = ara.Context(local, copy_stream)
+    Ys = [Y, ara.Yet(ctx, ev_host, fixed_len=K, first_trial=lo, n_trials=n_loc)]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     te0 = torch.cuda.Event(enable_timing=True); te1 = torch.cuda.Event(enable_timing=True)
     te0.record(stream)
-    for _ in range(e2e_steps):
-        Y.refill(ev_host)                       # H2D of this step's YET
-        step()
+    copy_stream.wait_event(te0)
+    Ys[0].refill(ev_host, ctx=ctx_copy)         # H2D of step 0's YET
+    for s_ in range(e2e_steps):
+        ctx_copy.synchronize()                  # step s's YET is on the device
+        if s_ + 1 < e2e_steps:
+            Ys[(s_ + 1) % 2].refill(ev_host, ctx=ctx_copy)   # H2D of step s+1 overlaps step s
+        Yc = Ys[s_ % 2]
+        ara.run(ctx, P, Yc, seed=cfg["seed"], su=cfg["su"], ylt=ylt)
+        src = ylt
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, ylt)
+            src = gathered
+        for layer in layers:
+            ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=world)
         ylt_host.copy_(ylt, non_blocking=True)  # D2H of the step's result
     te1.record(stream)
     torch.cuda.synchronize()
@@ -273,6 +290,7 @@ def run_ours(args, cfg, rank, world, local):
         t = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_elapsed = float(t[0])
+    del Ys[1]
 
     # ---- roofline of the dominant kernel, live per-kernel times (CUDA events on the
     # context stream, recorded by ara_run around each kernel)
@@ -345,7 +363,9 @@ def run_ours(args, cfg, rank, world, local):
                    "parallelism": f"trial-sharded x{world}" + (" + NCCL YLT all-gather" if world > 1 else "")},
         "e2e": {"value": N_total / (e2e_elapsed / e2e_steps), "unit": "trials/s",
                 "h2d_bytes_per_step": n_loc * K * 4, "d2h_bytes_per_step": L * n_loc * 4 + 16 * len(rps) * len(layers),
-                "steps": e2e_steps},
+                "steps": e2e_steps,
+                "how": "pinned host YET copied every step (second stream, double-buffered device YET: step s+1's "
+                       "H2D overlaps step s), ara_run + measures, YLT read back every step"},
         "gpu_launches": gpu_launches,
         "roofline": roof,
         "cpu_baseline": cpu,

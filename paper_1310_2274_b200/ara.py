@@ -220,8 +220,10 @@ class Yet:
                        n_trials=len(yet["trial_off"]) - 1)
         return cls(ctx, ev, trial_off=yet["trial_off"], first_trial=yet.get("first_trial", 0))
 
-    def refill(self, events):
-        _check(lib.ara_yet_refill(self.ctx.h, self.h, _p(events)))
+    def refill(self, events, ctx: "Context" = None):
+        """ara_yet_refill: new event ids of the same shape, copied on ctx's stream
+        (default: the context the YET was loaded with)."""
+        _check(lib.ara_yet_refill((ctx or self.ctx).h, self.h, _p(events)))
 
     def close(self):
         if getattr(self, "h", None):

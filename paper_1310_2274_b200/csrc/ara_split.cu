@@ -25,6 +25,9 @@ namespace ara {
 
 namespace {
 
+#ifndef ARA_COMPACT_DEPTH
+#define ARA_COMPACT_DEPTH 2           // chunks between index-entry loads and their use
+#endif
 #ifndef ARA_COMPACT_THREADS
 #define ARA_COMPACT_THREADS 1024
 #endif
@@ -216,6 +219,32 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
     };
 
     set_trial();
+#if ARA_COMPACT_DEPTH == 3
+    // three-deep: while chunk X is in stage B, the index entries of chunks
+    // X+1 and X+2 are in flight (L2) and chunks X+3.. from HBM
+    RawChunk ra, rb, rc;
+    ChunkA ca, cb, cc;
+    fetch(ra);
+    fetch(rb);
+    fetch(rc);
+    stage_a(ra, ca);
+    fetch(ra);
+    stage_a(rb, cb);
+    fetch(rb);
+    while (ca.t < n_trials) {
+        stage_a(rc, cc);
+        fetch(rc);
+        stage_b(ca);
+        if (cb.t >= n_trials) break;
+        stage_a(ra, ca);
+        fetch(ra);
+        stage_b(cb);
+        if (cc.t >= n_trials) break;
+        stage_a(rb, cb);
+        fetch(rb);
+        stage_b(cc);
+    }
+#else
     // ping-pong: while chunk X is in stage B, chunk X+1 is in stage A and
     // chunks X+2, X+3 are in flight from HBM
     RawChunk ra, rb;
@@ -233,6 +262,7 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         fetch(ra);
         stage_b(cb);
     }
+#endif
 }
 
 // compact_kernel's sink: per-trial regions of HBM; counts[t] = pairs or kOverflow

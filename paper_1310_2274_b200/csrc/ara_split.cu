@@ -15,6 +15,7 @@
 // A trial whose pairs overflow its region, or that meets a table-less record,
 // is listed for the fused fp64-capable kernel (ara_kernels.cu).
 #include <algorithm>
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -354,8 +355,10 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     for (int u = 0; u < 2; ++u) pn[u] = 32u * u + lane < n ? ldpair(in + 32u * u + lane) : make_uint2(0u, 0u);
     for (uint32_t off = 0; off < n; off += kXCap) {
         const uint32_t ns = min(n - off, kXCap);
-        // ---- rounds: x and run flags of every pair of the segment
-        for (uint32_t b = 0; b < ns; b += 64) {
+        // ---- rounds: x and run flags of every pair of the segment; U = 2
+        // pairs per lane, or 1 for a last round of <= 32 pairs
+        auto round = [&](auto UC, uint32_t b) {
+            constexpr int U = decltype(UC)::value;
             uint2 e[2];
             bool live[2];
 #pragma unroll
@@ -370,19 +373,19 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
             if (SU) {
                 SplitRec r[2];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < U; ++u) {
                     r[u] = live[u] ? srecs[e[u].x] : SplitRec{0, 0, 0, 0, 0, kModeDegenerate << 28, 0, 0};
                     meta[u] = r[u].meta;
                 }
                 float v[2];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const uint32_t bp = philox_lane0_k(trial_g, e[u].y, r[u].prog, 1u, A.pkey);   // z_(Prog,E)
                     const uint32_t be = philox_lane0_k(trial_g, e[u].y, r[u].elt, 2u, A.pkey);    // z_(E)
                     v[u] = fmaf(r[u].wi, norm_quantile_from_bits(bp), r[u].wc * norm_quantile_from_bits(be));
                 }
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const uint32_t mode = meta[u] >> 28;
                     if (mode == kModeTable) {
                         const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
@@ -402,13 +405,13 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 }
             } else {
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < U; ++u) {
                     meta[u] = live[u] ? __ldg(rmeta + e[u].x) : 0u;
                     x[u] = live[u] ? __ldg(A.pf.rec_mu + e[u].x) : 0.0f;
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const uint32_t layer = (meta[u] >> 16) & 63u;
                 if (terms) {                                          // line 8 (G7)
                     const SlotInfo &si = slots[meta[u] & 0xffu];
@@ -427,6 +430,10 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                     if (!SL) fl[p] = (uint8_t)layer;
                 }
             }
+        };
+        for (uint32_t b = 0; b < ns; b += 64) {
+            if (ns - b > 32u) round(std::integral_constant<int, 2>{}, b);
+            else round(std::integral_constant<int, 1>{}, b);
         }
         __syncwarp();
         // ---- reduce: runs (line 9) and occurrence terms (line 11)

@@ -87,29 +87,72 @@ __global__ void tail_compact_kernel(const float *vals, uint64_t n, SelectState *
     }
 }
 
-// one CTA: bitonic sort (descending) of up to kSortCap values, then the measures
+// one CTA of 1024 threads: bitonic sort (descending) of P = 1024 E values,
+// then the measures.  Thread t holds elements t E .. t E + E - 1 in registers:
+// a compare-exchange partner at distance j < E is in the same thread, at
+// E <= j < 32 E in the same warp (shuffle), and only j >= 32 E goes through
+// shared memory (stored transposed, [r][t], so the exchange is conflict-free).
+template <int E>
 __global__ void __launch_bounds__(1024) sort_measures_kernel(const float *buf, SelectState *st,
                                                              const double *rps, uint32_t n_rp,
                                                              uint64_t n_total, double *out) {
     extern __shared__ float sv[];
+    constexpr uint32_t P = 1024u * E;
     const uint32_t ng = (uint32_t)st->n_gt;
-    uint32_t P = 1;
-    while (P < ng) P <<= 1;
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sv[i] = (i < ng) ? buf[i] : -INFINITY;
-    __syncthreads();
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    float v[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const uint32_t i = tid * E + r;
+        v[r] = i < ng ? buf[i] : -INFINITY;
+    }
+    auto keep = [](bool lower_desc, float a, float b) {   // value kept by the element
+        return lower_desc ? fmaxf(a, b) : fminf(a, b);
+    };
     for (uint32_t k = 2; k <= P; k <<= 1) {
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-                const uint32_t l = i ^ j;
-                if (l > i) {
-                    const float a = sv[i], b = sv[l];
-                    const bool desc = (i & k) == 0;
-                    if (desc ? (a < b) : (a > b)) { sv[i] = b; sv[l] = a; }
+        uint32_t j = k >> 1;
+        for (; j >= 32u * E; j >>= 1) {               // across warps: shared memory
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < E; ++r) sv[r * 1024 + tid] = v[r];
+            __syncthreads();
+            const uint32_t m = j / E;
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const uint32_t i = tid * E + r;
+                const float w = sv[r * 1024 + (tid ^ m)];
+                v[r] = keep(((i & k) == 0) == ((tid & m) == 0), v[r], w);
+            }
+        }
+        for (; j >= (uint32_t)E; j >>= 1) {           // across lanes: shuffles
+            const uint32_t m = j / E;
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const uint32_t i = tid * E + r;
+                const float w = __shfl_xor_sync(0xffffffffu, v[r], m);
+                v[r] = keep(((i & k) == 0) == ((lane & m) == 0), v[r], w);
+            }
+        }
+#pragma unroll
+        for (int jj = E / 2; jj >= 1; jj >>= 1) {     // within the thread: registers
+            if ((uint32_t)jj < k) {
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    if ((r & jj) == 0) {
+                        const uint32_t i = tid * E + r;
+                        const float a = v[r], b = v[r + jj];
+                        const bool desc = (i & k) == 0;
+                        v[r] = desc ? fmaxf(a, b) : fminf(a, b);
+                        v[r + jj] = desc ? fminf(a, b) : fmaxf(a, b);
+                    }
                 }
             }
-            __syncthreads();
         }
     }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < E; ++r) sv[tid * E + r] = v[r];
+    __syncthreads();
     const float T = okey_inv(st->prefix);
     const uint64_t neq = st->n_eq, N = n_total;
     auto L = [&](uint64_t r) -> double {         // descending order statistic, 1-based
@@ -287,13 +330,16 @@ cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_tota
         select_digit_kernel<<<1, 32, 0, s>>>(S.state, S.hist, shift);
     }
     tail_compact_kernel<<<blocks, 256, 0, s>>>(S.vals, n_total, S.state, S.buf, kSortCap);
-    uint32_t P = 1;
+    uint32_t P = 1024;
     while (P < k_need) P <<= 1;
-    const size_t smem = sizeof(float) * (P < 1 ? 1 : P);
-    e = cudaFuncSetAttribute(sort_measures_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(float) * kSortCap));
+    using K = void (*)(const float *, SelectState *, const double *, uint32_t, uint64_t, double *);
+    const K kern = P <= 1024 ? (K)sort_measures_kernel<1> : P <= 2048 ? (K)sort_measures_kernel<2>
+                 : P <= 4096 ? (K)sort_measures_kernel<4> : P <= 8192 ? (K)sort_measures_kernel<8>
+                 : P <= 16384 ? (K)sort_measures_kernel<16> : (K)sort_measures_kernel<32>;
+    const size_t smem = sizeof(float) * P;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * kSortCap));
     if (e != cudaSuccess) return e;
-    sort_measures_kernel<<<1, 1024, smem, s>>>(S.buf, S.state, d_rps, n_rp, n_total, d_out);
+    kern<<<1, 1024, smem, s>>>(S.buf, S.state, d_rps, n_rp, n_total, d_out);
     return cudaGetLastError();
 }
 

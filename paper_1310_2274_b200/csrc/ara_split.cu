@@ -43,6 +43,10 @@ constexpr int kSampleWarps = ARA_SAMPLE_WARPS;   // sampling: 1 CTA of 1024 thre
 #ifndef ARA_SAMPLE_SMEM_KB
 #define ARA_SAMPLE_SMEM_KB 96
 #endif
+#ifndef ARA_SAMPLE_U
+#define ARA_SAMPLE_U 2                // pairs per lane in flight per sampler round
+#endif
+constexpr int kU = ARA_SAMPLE_U;
 constexpr uint32_t kXCapMax = 1024;     // pairs per sampler segment (a multiple of 64, >= ARA_MAX_SLOTS,
                                         // sized at launch to what 2 CTAs/SM leave in shared memory)
 
@@ -350,34 +354,34 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     double acc = 0.0;                              // SL: this lane's share of the trial sum
     double carry = 0.0;                            // run open at the previous segment's end
     int redo = 0;
-    uint2 pn[2];                                   // next round's pairs, prefetched
+    uint2 pn[kU];                                   // next round's pairs, prefetched
 #pragma unroll
-    for (int u = 0; u < 2; ++u) pn[u] = 32u * u + lane < n ? ldpair(in + 32u * u + lane) : make_uint2(0u, 0u);
+    for (int u = 0; u < kU; ++u) pn[u] = 32u * u + lane < n ? ldpair(in + 32u * u + lane) : make_uint2(0u, 0u);
     for (uint32_t off = 0; off < n; off += kXCap) {
         const uint32_t ns = min(n - off, kXCap);
         // ---- rounds: x and run flags of every pair of the segment; U = 2
         // pairs per lane, or 1 for a last round of <= 32 pairs
         auto round = [&](auto UC, uint32_t b) {
             constexpr int U = decltype(UC)::value;
-            uint2 e[2];
-            bool live[2];
+            uint2 e[kU];
+            bool live[kU];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < kU; ++u) {
                 e[u] = pn[u];
                 live[u] = b + 32u * u + lane < ns;
-                const uint32_t q = off + b + 64u + 32u * u + lane;
+                const uint32_t q = off + b + 32u * kU + 32u * u + lane;
                 pn[u] = q < n ? ldpair(in + q) : make_uint2(0u, 0u);
             }
-            uint32_t meta[2];
-            float x[2];
+            uint32_t meta[kU];
+            float x[kU];
             if (SU) {
-                SplitRec r[2];
+                SplitRec r[kU];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     r[u] = live[u] ? srecs[e[u].x] : SplitRec{0, 0, 0, 0, 0, kModeDegenerate << 28, 0, 0};
                     meta[u] = r[u].meta;
                 }
-                float v[2];
+                float v[kU];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const uint32_t bp = philox_lane0_k(trial_g, e[u].y, r[u].prog, 1u, A.pkey);   // z_(Prog,E)
@@ -431,8 +435,9 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 }
             }
         };
-        for (uint32_t b = 0; b < ns; b += 64) {
-            if (ns - b > 32u) round(std::integral_constant<int, 2>{}, b);
+        for (uint32_t b = 0; b < ns; b += 32u * kU) {
+            if (kU >= 3 && ns - b > 64u) round(std::integral_constant<int, kU>{}, b);
+            else if (ns - b > 32u) round(std::integral_constant<int, 2>{}, b);
             else round(std::integral_constant<int, 1>{}, b);
         }
         __syncwarp();
@@ -739,8 +744,10 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
     // gathers use: keep the segments short
     const size_t budget = (size_t)ARA_SAMPLE_SMEM_KB * 1024;
     SplitArgs B = A;
-    B.xcap = (uint32_t)std::min<size_t>(kXCapMax, (budget - other - 8) / (5 * kSampleWarps) / 64 * 64);
-    if (B.xcap < ARA_MAX_SLOTS) B.xcap = (ARA_MAX_SLOTS + 63) / 64 * 64;
+    // (a multiple of the round, 32 kU pairs, so a segment ends on a round)
+    constexpr size_t kR = 64 * kU;
+    B.xcap = (uint32_t)std::min<size_t>(kXCapMax / kR * kR, (budget - other - 8) / (5 * kSampleWarps) / kR * kR);
+    if (B.xcap < ARA_MAX_SLOTS) B.xcap = (uint32_t)((ARA_MAX_SLOTS + kR - 1) / kR * kR);
     const size_t smem = other + (sizeof(float) + sizeof(uint8_t)) * kSampleWarps * B.xcap + 8;
     using K = void (*)(SplitArgs);
     const K kern = su ? (sl ? (dbg ? (K)sample_kernel<true, true, true> : (K)sample_kernel<true, true, false>)
@@ -766,9 +773,10 @@ static size_t fused_smem(const PortfolioDev &pf, uint32_t &xcap) {
     const size_t budget = 227 * 1024;
     xcap = 0;
     if (pf.n_layers > kSplitMaxLayers || fixed + 64 >= budget) return 0;
-    const size_t x = (budget - fixed - 64) / ((sizeof(uint32_t) + sizeof(uint8_t)) * kNC) / 64 * 64;
+    constexpr size_t kR = 64 * kU;                   // segments end on a round
+    const size_t x = (budget - fixed - 64) / ((sizeof(uint32_t) + sizeof(uint8_t)) * kNC) / kR * kR;
     if (x < 256) return 0;
-    xcap = (uint32_t)std::min<size_t>(x, kXCapMax);
+    xcap = (uint32_t)std::min<size_t>(x, kXCapMax / kR * kR);
     return fixed + (sizeof(uint32_t) + sizeof(uint8_t)) * kNC * xcap + 16;
 }
 

@@ -54,6 +54,9 @@ extern "C" {
                                 specialised kernel (pairs in an L2-resident
                                 ring) instead of two kernels; same results
                                 bit for bit.  Round 1: slower */
+#define ARA_WIDE_PAIRS 16u   /* keep 8-byte {record, k} pair records even when
+                                4-byte packed ones fit (same results; for tests
+                                and comparison)                            */
 
 /* ---- limits (validated) ------------------------------------------------ */
 #define ARA_MAX_SLOTS 224    /* sum over layers of XELTs per layer          */

@@ -20,6 +20,7 @@ SU = 1
 DEBUG_LOOKUP = 2
 EXACT = 4
 FUSED = 8
+WIDE_PAIRS = 16
 MAX_SLOTS = 224
 MAX_LAYERS = 64
 
@@ -238,7 +239,8 @@ class Yet:
 
 
 def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug: bool = False,
-        ylt=None, exact: bool = False, fused: bool = False):
+        ylt=None, exact: bool = False, fused: bool = False,
+        wide_pairs: bool = False):
     """ara_run; returns the device YLT [n_layers, n_trials] (and count/hash if debug)."""
     import torch
     dev = torch.device("cuda", ctx.device)
@@ -249,7 +251,8 @@ def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug
         cnt = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int32, device=dev)
         hsh = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int64, device=dev)
     flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (EXACT if exact else 0) | \
-        (FUSED if fused else 0)
+        (FUSED if fused else 0) | \
+        (WIDE_PAIRS if wide_pairs else 0)
     _check(lib.ara_run(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(cnt),
                        _p(hsh)))
     return (ylt, cnt, hsh) if debug else ylt

@@ -93,6 +93,7 @@ struct ara_yet {
     uint32_t *d_redo = nullptr;        // trials to re-run with the fp64 kernel
     uint32_t *d_max = nullptr;         // largest event id (device word)
     uint64_t avg_len_x1000 = 0;        // mean events per trial x 1000
+    uint64_t max_len = 0;              // longest trial
 };
 
 extern "C" {
@@ -458,6 +459,9 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
     y->dev.offsets = y->d_offsets; y->dev.events = y->d_events; y->dev.n_events = total;
     y->dev.max_event = y->d_max;
     y->avg_len_x1000 = n_trials ? (total * 1000) / n_trials : 0;
+    y->max_len = fixed_len;
+    if (toff)
+        for (uint64_t q = 0; q < n_trials; ++q) y->max_len = std::max<uint64_t>(y->max_len, toff[q + 1] - toff[q]);
     *out = y;
     return ARA_OK;
 }
@@ -489,7 +493,7 @@ void ara_yet_destroy(ara_yet *y) {
 int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
             float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash) {
     if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
-    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_FUSED))
+    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_FUSED | ARA_WIDE_PAIRS))
         return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
     if (y->dev.n_trials == 0) return ARA_OK;
     if (!ylt) return fail(ARA_EINVAL, "ylt is NULL");
@@ -528,6 +532,12 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         }
         SplitArgs S{p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status,
                     c->d_pairs, cap, c->d_counts, y->d_redo, {}};
+        // 4-byte pairs (record << kbits | k) when both fit: halves the pair traffic
+        if (!fused && !(flags & ARA_WIDE_PAIRS)) {
+            uint32_t kb = 1;
+            while (kb < 24 && (1ull << kb) < (uint64_t)y->max_len) ++kb;
+            if ((uint64_t)p->dev.n_dev_records <= (1ull << (32 - kb))) S.kbits = kb;
+        }
         for (int r = 0; r < 10; ++r) {                   // Philox4x32-10 key schedule of the seed
             S.pkey[2 * r] = (uint32_t)seed + (uint32_t)r * 0x9E3779B9u;
             S.pkey[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;

@@ -122,6 +122,7 @@ struct SplitArgs {
     uint32_t *redo;
     uint32_t pkey[20];        // Philox key schedule of the seed (round r: pkey[2r], pkey[2r+1])
     uint32_t xcap;            // sample_kernel: pairs per segment (set by launch_sample)
+    uint32_t kbits;           // > 0: pairs packed in 4 B as device record << kbits | k (two-kernel path)
 };
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);

@@ -106,6 +106,13 @@ struct ChunkA {                     // stage A output of one chunk
     uint32_t t, c, len;
 };
 
+// predicated 4-byte store to a global address (no branch)
+__device__ __forceinline__ void st_u32_if(bool p, uint64_t addr, uint32_t a) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.global.u32 [%1], %2;\n}" ::"r"((uint32_t)p),
+                 "l"(addr), "r"(a)
+                 : "memory");
+}
+
 // predicated 8-byte store {a, b} to a global address (no branch)
 __device__ __forceinline__ void st_pair_if(bool p, uint64_t addr, uint32_t a, uint32_t b) {
     asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.global.v2.u32 [%1], {%2, %3};\n}" ::"r"((uint32_t)p),
@@ -116,9 +123,10 @@ __device__ __forceinline__ void st_pair_if(bool p, uint64_t addr, uint32_t a, ui
 // The compaction pipeline of one warp over the trials first_warp, first_warp
 // + nw, ...  Sink: begin(t) -> the region for trial t's pairs (warp-uniform),
 // end(t, n) after its last chunk (n > cap: overflow).
-template <class Sink>
+template <bool PK, class Sink>
 __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t *bitmap, uint32_t first_warp,
                                               uint32_t nw, Sink &sink) {
+    constexpr uint32_t kPairBytes = PK ? 4u : 8u;   // packed: device record << kbits | k
     const int lane = threadIdx.x & 31;
     const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift, cap = A.cap;
     const uint32_t n_trials = (uint32_t)A.yet.n_trials;    // <= 2^32 - 1 (ara_load_yet)
@@ -196,11 +204,12 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
             // one 64-bit address per event, predicated stores (no branches)
             uint64_t adr[4];
             uint32_t mx = 0, o = 0;
-            const uint64_t base = reinterpret_cast<uint64_t>(out + pos);
+            const uint64_t base = reinterpret_cast<uint64_t>(out) + (uint64_t)kPairBytes * pos;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                adr[q] = base + 8u * o;
-                st_pair_if(S.ci[q].y != 0u, adr[q], S.ci[q].x, k0 + q);
+                adr[q] = base + kPairBytes * o;
+                if (PK) st_u32_if(S.ci[q].y != 0u, adr[q], (S.ci[q].x << A.kbits) | (k0 + q));
+                else st_pair_if(S.ci[q].y != 0u, adr[q], S.ci[q].x, k0 + q);
                 o += S.ci[q].y;
                 mx = max(mx, S.ci[q].y);
             }
@@ -208,14 +217,20 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
 #pragma unroll 1
             for (uint32_t j = 1; j < mx; ++j)         // the events with several pairs
 #pragma unroll
-                for (int q = 0; q < 4; ++q) st_pair_if(j < S.ci[q].y, adr[q] + 8u * j, S.ci[q].x + j, k0 + q);
+                for (int q = 0; q < 4; ++q) {
+                    if (PK) st_u32_if(j < S.ci[q].y, adr[q] + 4u * j, ((S.ci[q].x + j) << A.kbits) | (k0 + q));
+                    else st_pair_if(j < S.ci[q].y, adr[q] + 8u * j, S.ci[q].x + j, k0 + q);
+                }
         } else {                                      // overflow: the trial is redone by the fused kernel
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t f = S.ci[q].x, m = S.ci[q].y;
 #pragma unroll 1
                 for (uint32_t j = 0; j < m; ++j)
-                    if (pos + j < cap) out[pos + j] = make_uint2(f + j, k0 + q);
+                    if (pos + j < cap) {
+                        if (PK) reinterpret_cast<uint32_t *>(out)[pos + j] = ((f + j) << A.kbits) | (k0 + q);
+                        else out[pos + j] = make_uint2(f + j, k0 + q);
+                    }
                 pos += m;
             }
         }
@@ -273,7 +288,10 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
 // compact_kernel's sink: per-trial regions of HBM; counts[t] = pairs or kOverflow
 struct HbmSink {
     const SplitArgs &A;
-    __device__ uint2 *begin(uint32_t t) const { return A.pairs + (uint64_t)t * A.cap; }
+    __device__ uint2 *begin(uint32_t t) const {     // (packed pairs: half-size regions, same bytes)
+        return A.kbits ? reinterpret_cast<uint2 *>(reinterpret_cast<uint32_t *>(A.pairs) + (uint64_t)t * A.cap)
+                       : A.pairs + (uint64_t)t * A.cap;
+    }
     __device__ void end(uint32_t t, uint32_t n) const {
         if ((threadIdx.x & 31) == 0) {
             A.counts[t] = n <= A.cap ? n : kOverflow;
@@ -282,6 +300,7 @@ struct HbmSink {
     }
 };
 
+template <bool PK>
 __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __grid_constant__ SplitArgs A) {
     constexpr int kWarps = kCompactThreads / 32;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -293,7 +312,7 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
     for (uint32_t t = threadIdx.x; t < A.pf.bitmap_words; t += blockDim.x) bitmap[t] = A.pf.bitmap[t];
     __syncthreads();
     HbmSink sink{A};
-    produce_pairs(A, bitmap, blockIdx.x * kWarps + (threadIdx.x >> 5), gridDim.x * kWarps, sink);
+    produce_pairs<PK>(A, bitmap, blockIdx.x * kWarps + (threadIdx.x >> 5), gridDim.x * kWarps, sink);
 }
 
 // ---------------------------------------------------------------------------
@@ -327,7 +346,7 @@ struct SampleWs {
 
 // The sampler on trial t's n present pairs at `in` (CG: read them through L2
 // only, as the fused kernel's consumers must).
-template <bool SU, bool SL, bool DBG, bool CG>
+template <bool SU, bool SL, bool DBG, bool CG, bool PK = false>
 __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs &W, uint64_t t, uint32_t n,
                                              const uint2 *in) {
     const int lane = threadIdx.x & 31;
@@ -345,7 +364,14 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     const float2 *__restrict__ hot = A.pf.hot;
     const float2 *__restrict__ tables = A.pf.tables;
     const uint32_t *__restrict__ rmeta = A.pf.rec_meta;
-    auto ldpair = [](const uint2 *q) { return CG ? __ldcg(q) : __ldcs(q); };
+    const uint32_t kb = A.kbits, kmask = (1u << kb) - 1u;
+    auto ldpair = [&](const uint2 *q) -> uint2 {    // {device record, k}
+        if (PK) {                                     // packed: record << kbits | k
+            const uint32_t w = __ldcs(reinterpret_cast<const uint32_t *>(in) + (q - in));
+            return make_uint2(w >> kb, w & kmask);
+        }
+        return CG ? __ldcg(q) : __ldcs(q);
+    };
     const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);
     if (!SL)
         for (uint32_t l = 0; l < nl; ++l) accs[l * 32] = 0.0;
@@ -509,7 +535,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     }
 }
 
-template <bool SU, bool SL, bool DBG>
+template <bool SU, bool SL, bool DBG, bool PK>
 __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 warps/SM: <= 64 registers
     sample_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -538,7 +564,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 wa
         if (t >= A.yet.n_trials) break;
         const uint32_t n = __ldg(A.counts + t);
         if (n == kOverflow) continue;                 // redone by the fused kernel
-        sample_trial<SU, SL, DBG, false>(A, W, t, n, A.pairs + t * (uint64_t)A.cap);
+        sample_trial<SU, SL, DBG, false, PK>(A, W, t, n, PK ? reinterpret_cast<const uint2 *>(
+                                                                   reinterpret_cast<const uint32_t *>(A.pairs) + t * A.cap)
+                                                               : A.pairs + t * (uint64_t)A.cap);
         __syncwarp();
     }
 }
@@ -630,7 +658,7 @@ __global__ void __launch_bounds__(1024, 1) fused_kernel(const __grid_constant__ 
     uint2 *ring = A.pairs + (uint64_t)blockIdx.x * kRing * A.cap;
     if (warp >= kNC) {                                // ---- producer
         RingSink sink{A, Q, ring};
-        produce_pairs(A, bitmap, blockIdx.x * kNP + (warp - kNC), gridDim.x * kNP, sink);
+        produce_pairs<false>(A, bitmap, blockIdx.x * kNP + (warp - kNC), gridDim.x * kNP, sink);
         __syncwarp();
         if (lane == 0) atomicAdd(&Q.prod_done, 1u);
         return;
@@ -723,13 +751,14 @@ cudaError_t launch_count_bad(const uint32_t *ev, uint64_t n, uint32_t C, unsigne
 
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms) {
     const size_t smem = (A.pf.bitmap_words * 4u + 15u) & ~15u;
-    cudaError_t err = cudaFuncSetAttribute(compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = A.kbits ? compact_kernel<true> : compact_kernel<false>;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     int per_sm = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compact_kernel, kCompactThreads, smem);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCompactThreads, smem);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    compact_kernel<<<num_sms * per_sm, kCompactThreads, smem, s>>>(A);
+    kern<<<num_sms * per_sm, kCompactThreads, smem, s>>>(A);
     return cudaGetLastError();
 }
 
@@ -750,10 +779,13 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
     if (B.xcap < ARA_MAX_SLOTS) B.xcap = (uint32_t)((ARA_MAX_SLOTS + kR - 1) / kR * kR);
     const size_t smem = other + (sizeof(float) + sizeof(uint8_t)) * kSampleWarps * B.xcap + 8;
     using K = void (*)(SplitArgs);
-    const K kern = su ? (sl ? (dbg ? (K)sample_kernel<true, true, true> : (K)sample_kernel<true, true, false>)
-                            : (dbg ? (K)sample_kernel<true, false, true> : (K)sample_kernel<true, false, false>))
-                      : (sl ? (dbg ? (K)sample_kernel<false, true, true> : (K)sample_kernel<false, true, false>)
-                            : (dbg ? (K)sample_kernel<false, false, true> : (K)sample_kernel<false, false, false>));
+#define ARA_SK(P)                                                                                               \
+    (su ? (sl ? (dbg ? (K)sample_kernel<true, true, true, P> : (K)sample_kernel<true, true, false, P>)           \
+            : (dbg ? (K)sample_kernel<true, false, true, P> : (K)sample_kernel<true, false, false, P>))         \
+        : (sl ? (dbg ? (K)sample_kernel<false, true, true, P> : (K)sample_kernel<false, true, false, P>)         \
+              : (dbg ? (K)sample_kernel<false, false, true, P> : (K)sample_kernel<false, false, false, P>)))
+    const K kern = A.kbits ? ARA_SK(true) : ARA_SK(false);
+#undef ARA_SK
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     int per_sm = 0;

@@ -324,7 +324,7 @@ def test_determinism_and_sharding(A, ctx):
 
 
 @pytest.mark.parametrize("n_layers,J,K", [(1, 16, 1000), (3, 4, 1500)])
-def test_fused_and_two_kernel_identical(A, ctx, n_layers, J, K):
+def test_fused_packed_and_wide_pairs_identical(A, ctx, n_layers, J, K):
     # the warp-specialised kernel and the two-kernel form process each trial
     # in the same order: bit-identical YLT, counts and hashes
     cfg = aragen.load_config("cfg3")
@@ -335,9 +335,11 @@ def test_fused_and_two_kernel_identical(A, ctx, n_layers, J, K):
     Y = A.Yet.from_dict(ctx, yet)
     for su in (True, False):
         f = A.run(ctx, P, Y, seed=5, su=su, debug=True, fused=True)
-        t = A.run(ctx, P, Y, seed=5, su=su, debug=True)
-        for x, y in zip(f, t):
+        t = A.run(ctx, P, Y, seed=5, su=su, debug=True)                   # 4-byte packed pairs
+        w = A.run(ctx, P, Y, seed=5, su=su, debug=True, wide_pairs=True)  # 8-byte pairs
+        for x, y, z in zip(f, t, w):
             assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
+            assert np.array_equal(x.cpu().numpy(), z.cpu().numpy())
 
 
 def test_event_out_of_range(A, ctx):

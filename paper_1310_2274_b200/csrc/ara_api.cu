@@ -123,7 +123,7 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
     c->num_sms = prop.multiProcessorCount;
     if (cudaMalloc(&c->d_status, sizeof(RunStatus)) != cudaSuccess ||
         cudaMallocHost(&c->h_status, sizeof(RunStatus)) != cudaSuccess ||
-        dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 256) != cudaSuccess ||
+        dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 4 * 256) != cudaSuccess ||
         dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
         dalloc(&c->ms.d_out, 128) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
         dalloc(&c->ms.part_sum, kRedBlocks) != cudaSuccess ||

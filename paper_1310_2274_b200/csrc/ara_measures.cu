@@ -6,12 +6,15 @@
 // CTA; ties at T are counted, never materialised.  PML interpolates the
 // descending order statistics at r = (N+1)/RP; TVaR is the mean of all
 // losses >= VaR = L(ceil(N/RP)).
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "ara_measures.cuh"
 
 namespace ara {
+
+namespace cg = cooperative_groups;
 
 __device__ __forceinline__ uint32_t okey(float v) {
     const uint32_t b = __float_as_uint(v == 0.0f ? 0.0f : v);   // -0 -> +0
@@ -76,6 +79,75 @@ __global__ void tail_compact_kernel(const float *vals, uint64_t n, SelectState *
     const uint32_t T = st->prefix;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
          t += (uint64_t)gridDim.x * blockDim.x) {
+        const float v = vals[t];
+        const uint32_t k = okey(v);
+        if (k > T) {
+            const unsigned long long p = atomicAdd(&st->n_gt, 1ull);
+            if (p < cap) buf[p] = v;
+        } else if (k == T) {
+            atomicAdd(&st->n_eq, 1ull);
+        }
+    }
+}
+
+// The whole select in one cooperative launch: gather (or roll-up) -> 4 radix
+// passes (block histograms in shared memory -> one global histogram per pass
+// -> block 0 picks the digit) -> tail compaction, with a grid-wide barrier
+// between phases instead of 14 separate launches.
+__global__ void __launch_bounds__(256) select_coop_kernel(const float *ylt, uint32_t n_layers, uint64_t per,
+                                                          uint32_t n_shards, int32_t layer, float *vals,
+                                                          uint64_t k_need, SelectState *st, unsigned int *hist4,
+                                                          float *buf, uint32_t cap) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned int h[256];
+    const uint64_t n = per * n_shards;
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gstride = (uint64_t)gridDim.x * blockDim.x;
+    if (gtid == 0) *st = SelectState{k_need, 0u, 0u, 0ull, 0ull};
+    for (uint64_t i = gtid; i < 4 * 256; i += gstride) hist4[i] = 0u;
+    grid.sync();
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        unsigned int *hist = hist4 + 256 * pass;
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+        __syncthreads();
+        const uint32_t prefix = st->prefix, pmask = st->pmask;
+        for (uint64_t t = gtid; t < n; t += gstride) {
+            float v;
+            if (pass == 0) {                          // gather / roll-up (G16)
+                const uint64_t sh = t / per, i = t - sh * per;
+                const float *base = ylt + sh * (uint64_t)n_layers * per + i;
+                if (layer >= 0) {
+                    v = base[(uint64_t)layer * per];
+                } else {
+                    v = 0.0f;
+                    for (uint32_t l = 0; l < n_layers; ++l) v += base[(uint64_t)l * per];
+                }
+                vals[t] = v;
+            } else {
+                v = vals[t];
+            }
+            const uint32_t k = okey(v);
+            if ((k & pmask) == prefix) atomicAdd(&h[(k >> shift) & 0xffu], 1u);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < 256; i += blockDim.x)
+            if (h[i]) atomicAdd(&hist[i], h[i]);
+        grid.sync();
+        if (gtid == 0) {                              // the digit holding the K_rem-th largest
+            uint64_t need = st->k_rem;
+            int d = 255;
+            for (; d > 0; --d) {
+                if (hist[d] >= need) break;
+                need -= hist[d];
+            }
+            st->k_rem = need;
+            st->prefix |= (uint32_t)d << shift;
+            st->pmask |= 0xffu << shift;
+        }
+        grid.sync();
+    }
+    const uint32_t T = st->prefix;
+    for (uint64_t t = gtid; t < n; t += gstride) {
         const float v = vals[t];
         const uint32_t k = okey(v);
         if (k > T) {
@@ -316,20 +388,27 @@ cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_tota
                             int32_t layer, const double *d_rps, uint32_t n_rp, uint64_t k_need,
                             MeasuresScratch &S, double *d_out, cudaStream_t s) {
     const uint64_t per = n_total / n_shards;
-    const int blocks = 148 * 4;
-    gather_kernel<<<blocks, 256, 0, s>>>(ylt, n_layers, per, n_shards, layer, S.vals);
-    SelectState init{};
-    init.k_rem = k_need;
-    cudaError_t e = cudaMemcpyAsync(S.state, &init, sizeof(init), cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return e;
-    for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
-        e = cudaMemsetAsync(S.hist, 0, 256 * sizeof(unsigned int), s);
+    {
+        static int coop_blocks = 0;                   // co-resident blocks of the cooperative select
+        if (!coop_blocks) {
+            int dev = 0, sms = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_coop_kernel, 256, 0);
+            coop_blocks = sms * (per_sm < 4 ? per_sm : 4);
+        }
+        float *vals = S.vals, *buf = S.buf;
+        unsigned int *hist = S.hist;
+        SelectState *st = S.state;
+        uint32_t cap = kSortCap;
+        uint64_t kk = k_need;
+        void *args[] = {(void *)&ylt, (void *)&n_layers, (void *)&per, (void *)&n_shards, (void *)&layer,
+                        (void *)&vals, (void *)&kk, (void *)&st, (void *)&hist, (void *)&buf, (void *)&cap};
+        cudaError_t e = cudaLaunchCooperativeKernel((void *)select_coop_kernel, dim3(coop_blocks), dim3(256), args,
+                                                    0, s);
         if (e != cudaSuccess) return e;
-        hist_kernel<<<blocks, 256, 0, s>>>(S.vals, n_total, S.state, shift, S.hist);
-        select_digit_kernel<<<1, 32, 0, s>>>(S.state, S.hist, shift);
     }
-    tail_compact_kernel<<<blocks, 256, 0, s>>>(S.vals, n_total, S.state, S.buf, kSortCap);
+    cudaError_t e = cudaSuccess;
     uint32_t P = 1024;
     while (P < k_need) P <<= 1;
     using K = void (*)(const float *, SelectState *, const double *, uint32_t, uint64_t, double *);

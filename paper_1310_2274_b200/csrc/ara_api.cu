@@ -62,6 +62,7 @@ struct ara_ctx {
     int num_sms = 0;
     RunStatus *d_status = nullptr;
     RunStatus *h_status = nullptr;     // pinned
+    double *h_out = nullptr;           // pinned [128]: measures results
     MeasuresScratch ms;
     uint2 *d_pairs = nullptr;          // split path scratch: per-trial pairs {device record, k}
     uint64_t pairs_capacity = 0;       // elements of d_pairs
@@ -123,6 +124,7 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
     c->num_sms = prop.multiProcessorCount;
     if (cudaMalloc(&c->d_status, sizeof(RunStatus)) != cudaSuccess ||
         cudaMallocHost(&c->h_status, sizeof(RunStatus)) != cudaSuccess ||
+        cudaMallocHost(&c->h_out, 128 * sizeof(double)) != cudaSuccess ||
         dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 4 * 256) != cudaSuccess ||
         dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
         dalloc(&c->ms.d_out, 128) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
@@ -142,6 +144,7 @@ void ara_ctx_destroy(ara_ctx *c) {
     cudaSetDevice(c->device);
     cudaFree(c->d_status);
     cudaFreeHost(c->h_status);
+    cudaFreeHost(c->h_out);
     cudaFree(c->ms.vals);
     cudaFree(c->ms.buf);
     cudaFree(c->ms.hist);
@@ -642,15 +645,16 @@ int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t 
         CU(dalloc(&c->ms.vals, n_total));
         c->ms.capacity = n_total;
     }
-    CU(cudaMemcpyAsync(c->ms.d_rps, rps, n_rp * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     if (k_need <= kSortCap) {
-        CU(launch_measures(ylt, n_layers, n_total, n_shards, layer, c->ms.d_rps, n_rp, k_need, c->ms,
-                           c->ms.d_out, c->stream));
+        RpList R{};
+        for (uint32_t q = 0; q < n_rp; ++q) R.v[q] = rps[q];
+        CU(launch_measures(ylt, n_layers, n_total, n_shards, layer, R, n_rp, k_need, c->ms, c->ms.d_out,
+                           c->stream));
     } else {   // deep ranks: a radix select per needed order statistic
         CU(launch_measures_deep(ylt, n_layers, n_total, n_shards, layer, rps, n_rp, c->ms,
                                 c->ms.d_out, c->stream));
     }
-    double out[128];
+    double *out = c->h_out;                      // pinned
     CU(cudaMemcpyAsync(out, c->ms.d_out, 2 * n_rp * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     for (uint32_t q = 0; q < n_rp; ++q) {

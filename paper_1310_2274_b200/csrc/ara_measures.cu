@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(256) select_coop_kernel(const float *ylt, uint
 // shared memory (stored transposed, [r][t], so the exchange is conflict-free).
 template <int E>
 __global__ void __launch_bounds__(1024) sort_measures_kernel(const float *buf, SelectState *st,
-                                                             const double *rps, uint32_t n_rp,
+                                                             const __grid_constant__ RpList R, uint32_t n_rp,
                                                              uint64_t n_total, double *out) {
+    const double *rps = R.v;                          // (kernel parameter: no host->device copy)
     extern __shared__ float sv[];
     constexpr uint32_t P = 1024u * E;
     const uint32_t ng = (uint32_t)st->n_gt;
@@ -385,7 +386,7 @@ cudaError_t launch_measures_deep(const float *ylt, uint32_t n_layers, uint64_t n
 }
 
 cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
-                            int32_t layer, const double *d_rps, uint32_t n_rp, uint64_t k_need,
+                            int32_t layer, const RpList &rps, uint32_t n_rp, uint64_t k_need,
                             MeasuresScratch &S, double *d_out, cudaStream_t s) {
     const uint64_t per = n_total / n_shards;
     {
@@ -411,14 +412,22 @@ cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_tota
     cudaError_t e = cudaSuccess;
     uint32_t P = 1024;
     while (P < k_need) P <<= 1;
-    using K = void (*)(const float *, SelectState *, const double *, uint32_t, uint64_t, double *);
+    using K = void (*)(const float *, SelectState *, const RpList, uint32_t, uint64_t, double *);
     const K kern = P <= 1024 ? (K)sort_measures_kernel<1> : P <= 2048 ? (K)sort_measures_kernel<2>
                  : P <= 4096 ? (K)sort_measures_kernel<4> : P <= 8192 ? (K)sort_measures_kernel<8>
                  : P <= 16384 ? (K)sort_measures_kernel<16> : (K)sort_measures_kernel<32>;
     const size_t smem = sizeof(float) * P;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * kSortCap));
-    if (e != cudaSuccess) return e;
-    kern<<<1, 1024, smem, s>>>(S.buf, S.state, d_rps, n_rp, n_total, d_out);
+    static bool attr_set = false;                     // once per process (all six instantiations)
+    if (!attr_set) {
+        const K all[] = {sort_measures_kernel<1>, sort_measures_kernel<2>, sort_measures_kernel<4>,
+                         sort_measures_kernel<8>, sort_measures_kernel<16>, sort_measures_kernel<32>};
+        for (K k : all) {
+            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * kSortCap));
+            if (e != cudaSuccess) return e;
+        }
+        attr_set = true;
+    }
+    kern<<<1, 1024, smem, s>>>(S.buf, S.state, rps, n_rp, n_total, d_out);
     return cudaGetLastError();
 }
 

@@ -29,10 +29,14 @@ struct MeasuresScratch {
 };
 
 constexpr int kMaxRanks = 3 * 64;
+
+struct RpList {                // return periods, passed by value to the sort kernel
+    double v[64];
+};
 constexpr int kRedBlocks = 592;
 
 cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
-                            int32_t layer, const double *d_rps, uint32_t n_rp, uint64_t k_need,
+                            int32_t layer, const RpList &rps, uint32_t n_rp, uint64_t k_need,
                             MeasuresScratch &S, double *d_out, cudaStream_t s);
 
 cudaError_t launch_measures_deep(const float *ylt, uint32_t n_layers, uint64_t n_total,

@@ -15,6 +15,8 @@
 // A trial whose pairs overflow its region, or that meets a table-less record,
 // is listed for the fused fp64-capable kernel (ara_kernels.cu).
 #include <algorithm>
+#include <mutex>
+#include <vector>
 #include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -749,13 +751,40 @@ cudaError_t launch_count_bad(const uint32_t *ev, uint64_t n, uint32_t C, unsigne
     return cudaGetLastError();
 }
 
+// Launch preparation cached per (device, kernel, dynamic shared memory): the
+// attribute call and the occupancy query cost microseconds of host time
+// that would otherwise sit between the kernels of every ara_run.
+static cudaError_t prepare_launch(const void *kern, size_t smem, int threads, int &per_sm) {
+    struct Entry { int dev; const void *k; size_t smem; int threads, per_sm; };
+    struct Attr { int dev; const void *k; size_t max_smem; };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    static std::vector<Attr> attrs;                   // the largest size each kernel was opened for
+    int dev = 0;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return err;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry &e : cache)
+        if (e.dev == dev && e.k == kern && e.smem == smem && e.threads == threads) { per_sm = e.per_sm; return cudaSuccess; }
+    Attr *a = nullptr;
+    for (Attr &x : attrs)
+        if (x.dev == dev && x.k == kern) a = &x;
+    if (!a || a->max_smem < smem) {
+        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err != cudaSuccess) return err;
+        if (a) a->max_smem = smem; else attrs.push_back(Attr{dev, kern, smem});
+    }
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (err != cudaSuccess) return err;
+    cache.push_back(Entry{dev, kern, smem, threads, per_sm});
+    return cudaSuccess;
+}
+
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms) {
     const size_t smem = (A.pf.bitmap_words * 4u + 15u) & ~15u;
     auto kern = A.kbits ? compact_kernel<true> : compact_kernel<false>;
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
     int per_sm = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCompactThreads, smem);
+    cudaError_t err = prepare_launch((const void *)kern, smem, kCompactThreads, per_sm);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     kern<<<num_sms * per_sm, kCompactThreads, smem, s>>>(A);
@@ -786,10 +815,8 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
               : (dbg ? (K)sample_kernel<false, false, true, P> : (K)sample_kernel<false, false, false, P>)))
     const K kern = A.kbits ? ARA_SK(true) : ARA_SK(false);
 #undef ARA_SK
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
     int per_sm = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSampleWarps * 32, smem);
+    cudaError_t err = prepare_launch((const void *)kern, smem, kSampleWarps * 32, per_sm);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     kern<<<num_sms * per_sm, kSampleWarps * 32, smem, s>>>(B);
@@ -829,7 +856,8 @@ cudaError_t launch_fused(const SplitArgs &A, cudaStream_t s, int num_sms) {
                             : (dbg ? (K)fused_kernel<true, false, true> : (K)fused_kernel<true, false, false>))
                       : (sl ? (dbg ? (K)fused_kernel<false, true, true> : (K)fused_kernel<false, true, false>)
                             : (dbg ? (K)fused_kernel<false, false, true> : (K)fused_kernel<false, false, false>));
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaError_t err = prepare_launch((const void *)kern, smem, 1024, per_sm);
     if (err != cudaSuccess) return err;
     kern<<<num_sms, 1024, smem, s>>>(B);
     return cudaGetLastError();

@@ -371,6 +371,24 @@ def test_measures_vs_oracle_sort(A, ctx, n):
         assert tvar[q] == pytest.approx(OM.tvar_rp(x.astype(np.float64), rp)[1], rel=1e-10)
 
 
+@pytest.mark.parametrize("rp_min", [533, 266, 133, 66, 33])
+def test_measures_every_sort_size(A, ctx, rp_min):
+    # the deepest rank decides the sort size (1024 E values, E = 2 .. 32 in
+    # registers per thread): each size once, against the oracle's sort
+    import torch
+    n = 800000
+    rng = np.random.default_rng(rp_min)
+    x = rng.lognormal(15, 1.2, n).astype(np.float32)
+    x[rng.uniform(size=n) < 0.1] = 0.0
+    x[rng.uniform(size=n) < 0.002] = np.float32(3.0e8)
+    rps = [rp_min, 2 * rp_min + 1, 1000]
+    d = torch.from_numpy(x).cuda()
+    pml, tvar = A.risk_measures(ctx, d, 1, n, 0, rps=rps)
+    for q, rp in enumerate(rps):
+        assert pml[q] == pytest.approx(OM.pml(x.astype(np.float64), rp), rel=1e-12, abs=1e-9)
+        assert tvar[q] == pytest.approx(OM.tvar_rp(x.astype(np.float64), rp)[1], rel=1e-10)
+
+
 def test_measures_rollup_and_shards(A, ctx):
     import torch
     rng = np.random.default_rng(5)

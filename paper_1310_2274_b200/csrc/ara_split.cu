@@ -406,7 +406,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 SplitRec r[kU];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    r[u] = live[u] ? srecs[e[u].x] : SplitRec{0, 0, 0, 0, 0, kModeDegenerate << 28, 0, 0};
+                    r[u] = srecs[e[u].x];                 // (idle lanes: record 0, result unused)
                     meta[u] = r[u].meta;
                 }
                 float v[kU];
@@ -432,7 +432,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                         x[u] = r[u].scale;
                     } else {
                         x[u] = 0.0f;              // table-less record: trial redone in fp64
-                        redo = 1;
+                        redo |= live[u];
                     }
                 }
             } else {

@@ -91,72 +91,123 @@ __global__ void tail_compact_kernel(const float *vals, uint64_t n, SelectState *
 }
 
 // The whole select in one cooperative launch: gather (or roll-up) -> 4 radix
-// passes (block histograms in shared memory -> one global histogram per pass
-// -> block 0 picks the digit) -> tail compaction, with a grid-wide barrier
-// between phases instead of 14 separate launches.
+// passes (block histograms in shared memory, warp-aggregated with
+// match.any -> one global histogram per pass -> every block picks the digit
+// itself with a warp-parallel suffix count) -> tail compaction
+// (warp-aggregated slots), with one grid-wide barrier per pass.
+__device__ __forceinline__ void pick_digit(const unsigned int *hist, int shift, uint64_t &need,
+                                           uint32_t &prefix, uint32_t &pmask) {
+    // one warp: lane L holds digits 255 - 8L .. 248 - 8L (descending)
+    const int lane = threadIdx.x & 31;
+    uint32_t c[8], tot = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) { c[r] = __ldcg(&hist[255 - 8 * lane - r]); tot += c[r]; }
+    uint64_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint64_t before = incl - tot;               // keys in higher digits
+    const unsigned hit = __ballot_sync(0xffffffffu, before < need && need <= incl);
+    int d = 0;
+    uint64_t rem = need;
+    if (hit) {                                        // the lane holding the K_rem-th largest
+        const int L = __ffs(hit) - 1;
+        if (lane == L) {
+            rem = need - before;
+            d = 255 - 8 * lane;
+#pragma unroll
+            for (int r = 0; r < 7; ++r)
+                if (rem > c[r]) { rem -= c[r]; --d; } else break;
+        }
+        d = __shfl_sync(0xffffffffu, d, L);
+        rem = __shfl_sync(0xffffffffu, rem, L);
+    } else {                                          // fewer keys than K: the lowest digit
+        const uint64_t all = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t h0 = __shfl_sync(0xffffffffu, c[7], 31);
+        rem = need - (all - h0);
+    }
+    need = rem;
+    prefix |= (uint32_t)d << shift;
+    pmask |= 0xffu << shift;
+}
+
 __global__ void __launch_bounds__(256) select_coop_kernel(const float *ylt, uint32_t n_layers, uint64_t per,
                                                           uint32_t n_shards, int32_t layer, float *vals,
                                                           uint64_t k_need, SelectState *st, unsigned int *hist4,
                                                           float *buf, uint32_t cap) {
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned int h[256];
+    __shared__ uint64_t s_need;
+    __shared__ uint32_t s_prefix, s_pmask;
     const uint64_t n = per * n_shards;
+    const int lane = threadIdx.x & 31;
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gstride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t wbase = gtid - lane;               // warp-uniform loop base
     if (gtid == 0) *st = SelectState{k_need, 0u, 0u, 0ull, 0ull};
     for (uint64_t i = gtid; i < 4 * 256; i += gstride) hist4[i] = 0u;
+    uint64_t need = k_need;
+    uint32_t prefix = 0u, pmask = 0u;
     grid.sync();
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
         unsigned int *hist = hist4 + 256 * pass;
         for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
         __syncthreads();
-        const uint32_t prefix = st->prefix, pmask = st->pmask;
-        for (uint64_t t = gtid; t < n; t += gstride) {
-            float v;
-            if (pass == 0) {                          // gather / roll-up (G16)
-                const uint64_t sh = t / per, i = t - sh * per;
-                const float *base = ylt + sh * (uint64_t)n_layers * per + i;
-                if (layer >= 0) {
-                    v = base[(uint64_t)layer * per];
+        for (uint64_t b = wbase; b < n; b += gstride) {
+            const uint64_t t = b + lane;
+            float v = 0.0f;
+            if (t < n) {
+                if (pass == 0) {                      // gather / roll-up (G16)
+                    const uint64_t sh = t / per, i = t - sh * per;
+                    const float *base = ylt + sh * (uint64_t)n_layers * per + i;
+                    if (layer >= 0) {
+                        v = base[(uint64_t)layer * per];
+                    } else {
+                        for (uint32_t l = 0; l < n_layers; ++l) v += base[(uint64_t)l * per];
+                    }
+                    vals[t] = v;
                 } else {
-                    v = 0.0f;
-                    for (uint32_t l = 0; l < n_layers; ++l) v += base[(uint64_t)l * per];
+                    v = vals[t];
                 }
-                vals[t] = v;
-            } else {
-                v = vals[t];
             }
             const uint32_t k = okey(v);
-            if ((k & pmask) == prefix) atomicAdd(&h[(k >> shift) & 0xffu], 1u);
+            const uint32_t d = (t < n && (k & pmask) == prefix) ? (k >> shift) & 0xffu : 256u;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            if (d < 256u && lane == __ffs(peers) - 1) atomicAdd(&h[d], (unsigned)__popc(peers));
         }
         __syncthreads();
         for (int i = threadIdx.x; i < 256; i += blockDim.x)
             if (h[i]) atomicAdd(&hist[i], h[i]);
         grid.sync();
-        if (gtid == 0) {                              // the digit holding the K_rem-th largest
-            uint64_t need = st->k_rem;
-            int d = 255;
-            for (; d > 0; --d) {
-                if (hist[d] >= need) break;
-                need -= hist[d];
-            }
-            st->k_rem = need;
-            st->prefix |= (uint32_t)d << shift;
-            st->pmask |= 0xffu << shift;
+        if (threadIdx.x < 32) {                       // every block: the digit of the K_rem-th largest
+            pick_digit(hist, shift, need, prefix, pmask);
+            if (threadIdx.x == 0) { s_need = need; s_prefix = prefix; s_pmask = pmask; }
         }
-        grid.sync();
+        __syncthreads();
+        need = s_need; prefix = s_prefix; pmask = s_pmask;
     }
-    const uint32_t T = st->prefix;
-    for (uint64_t t = gtid; t < n; t += gstride) {
-        const float v = vals[t];
+    if (gtid == 0) { st->k_rem = need; st->prefix = prefix; st->pmask = pmask; }
+    const uint32_t T = prefix;
+    unsigned long long n_eq = 0;
+    for (uint64_t b = wbase; b < n; b += gstride) {
+        const uint64_t t = b + lane;
+        const float v = t < n ? vals[t] : 0.0f;
         const uint32_t k = okey(v);
-        if (k > T) {
-            const unsigned long long p = atomicAdd(&st->n_gt, 1ull);
-            if (p < cap) buf[p] = v;
-        } else if (k == T) {
-            atomicAdd(&st->n_eq, 1ull);
+        const unsigned gt = __ballot_sync(0xffffffffu, t < n && k > T);
+        n_eq += __popc(__ballot_sync(0xffffffffu, t < n && k == T));
+        if (gt) {
+            unsigned long long p0 = 0;
+            if (lane == 0) p0 = atomicAdd(&st->n_gt, (unsigned long long)__popc(gt));
+            p0 = __shfl_sync(0xffffffffu, p0, 0);
+            if ((gt >> lane) & 1u) {
+                const unsigned long long p = p0 + __popc(gt & ((1u << lane) - 1u));
+                if (p < cap) buf[p] = v;
+            }
         }
     }
+    if (lane == 0 && n_eq) atomicAdd(&st->n_eq, n_eq);
 }
 
 // one CTA of 1024 threads: bitonic sort (descending) of P = 1024 E values,

@@ -368,6 +368,16 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     PortfolioDev &d = p->dev;
     d.catalog = C; d.n_slots = S; d.n_layers = n_layers; d.mask_words = mwt; d.idx_stride = stride;
     d.bitmap_shift = shift; d.bitmap_words = words; d.n_dev_records = total;
+    {   // sentinel event for the compaction's partial chunks: a presence bit that is 0
+        d.sentinel_ok = 0; d.sentinel_event = 0;
+        const uint64_t cand = ((uint64_t)words * 32u) << shift;     // the appended zero word
+        if (cand <= 0xffffffffull) { d.sentinel_event = (uint32_t)cand; d.sentinel_ok = 1; }
+        else
+            for (uint64_t b = 0; b < bits && !d.sentinel_ok; ++b)
+                if (!((bitmap[b >> 5] >> (b & 31)) & 1u) && (b << shift) <= 0xffffffffull) {
+                    d.sentinel_event = (uint32_t)(b << shift); d.sentinel_ok = 1;
+                }
+    }
     d.n_exact_records = c->h_status->nonconverged;
     d.index = p->d_index; d.bitmap = p->d_bitmap; d.recs = p->d_recs; d.rec_mu = p->d_mu;
     d.tables = p->d_tables;

@@ -66,6 +66,9 @@ struct PortfolioDev {
     uint32_t idx_stride;      // uint32 words per event index entry (2, 4 or 8)
     uint32_t bitmap_shift;    // event e -> presence bit e >> shift
     uint32_t bitmap_words;
+    uint32_t sentinel_event;  // an id whose presence bit is 0 (bit index bitmap_words * 32: the zero word
+                              // appended in shared memory, or a zero bit of the bitmap)
+    uint32_t sentinel_ok;     // 0: no such id fits in 32 bits (per-event length test instead)
     uint64_t n_dev_records;
     uint32_t n_exact_records; // records without a quantile table (fp64 per-sample solve)
     const uint32_t *index;    // [catalog][idx_stride]: first record, mask words

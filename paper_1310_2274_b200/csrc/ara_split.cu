@@ -31,6 +31,12 @@ namespace {
 #ifndef ARA_COMPACT_DEPTH
 #define ARA_COMPACT_DEPTH 2           // chunks between index-entry loads and their use
 #endif
+#ifndef ARA_COMPACT_PREFETCH
+#define ARA_COMPACT_PREFETCH 0        // bulk L2 prefetch of each warp's next trial of YET (measured: no gain)
+#endif
+#ifndef ARA_COMPACT_BALLOT_SCAN
+#define ARA_COMPACT_BALLOT_SCAN 1     // pair prefix sums by ballots instead of shuffles
+#endif
 #ifndef ARA_COMPACT_THREADS
 #define ARA_COMPACT_THREADS 1024
 #endif
@@ -71,6 +77,12 @@ __device__ __forceinline__ uint32_t philox_lane0_k(uint32_t i, uint32_t k, uint3
         c = make_uint4(hi1 ^ c.y ^ ks[2 * r], lo1, hi0 ^ c.w ^ ks[2 * r + 1], lo0);
     }
     return c.x;
+}
+
+// min(max(d, 0), lim) for finite or +inf d, lim (G5) by comparisons and
+// selects: fmin/fmax would add NaN handling to the sampler's run loop
+__device__ __forceinline__ double xl_clip_(double d, double lim) {
+    return d > 0.0 ? (d < lim ? d : lim) : 0.0;
 }
 
 __device__ __forceinline__ double warp_sum_f64_(double v) {
@@ -125,7 +137,10 @@ __device__ __forceinline__ void st_pair_if(bool p, uint64_t addr, uint32_t a, ui
 // The compaction pipeline of one warp over the trials first_warp, first_warp
 // + nw, ...  Sink: begin(t) -> the region for trial t's pairs (warp-uniform),
 // end(t, n) after its last chunk (n > cap: overflow).
-template <bool PK, class Sink>
+// BM: 0 = bitmap shift 0 and a sentinel event (lanes past a trial's end hold
+// an id whose presence bit is 0, so no length test per event), 1 = any shift
+// with the sentinel, 2 = any shift, length test per event.
+template <bool PK, int BM, class Sink>
 __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t *bitmap, uint32_t first_warp,
                                               uint32_t nw, Sink &sink) {
     constexpr uint32_t kPairBytes = PK ? 4u : 8u;   // packed: device record << kbits | k
@@ -137,7 +152,9 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
     const uint64_t *offsets = A.yet.offsets;
     const uint2 *__restrict__ cidx = A.pf.cidx;
     const uint32_t K = A.yet.fixed_len;
+    const uint32_t mul = 1u << A.kbits;
     const bool vec = offsets == nullptr && (K & 3u) == 0;   // every chunk 16 B aligned
+    const uint32_t sent = BM == 2 ? 0u : A.pf.sentinel_event;
 
     // fetch side: position in the flat chunk sequence (warp-uniform)
     uint32_t pt = first_warp;
@@ -147,11 +164,26 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         if (pt < n_trials) {
             if (offsets) { pbase = offsets[pt]; plen = (uint32_t)(offsets[pt + 1] - pbase); }
             else { pbase = (uint64_t)pt * K; plen = K; }
+#if ARA_COMPACT_PREFETCH
+            // the warp's next trial, one bulk L2 prefetch: its chunk loads then
+            // wait on L2, not HBM (no registers held for the lead)
+            const uint32_t nt = pt + nw;
+            if (lane == 0 && nt > pt && nt < n_trials) {
+                uint64_t b0, b1;
+                if (offsets) { b0 = offsets[nt]; b1 = offsets[nt + 1]; }
+                else { b0 = (uint64_t)nt * K; b1 = b0 + K; }
+                const uint64_t a0 = reinterpret_cast<uint64_t>(events + b0) & ~15ull;
+                const uint64_t a1 = (reinterpret_cast<uint64_t>(events + b1) + 15ull) & ~15ull;
+                if (a1 > a0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
+                                 : "memory");
+            }
+#endif
         }
     };
     auto fetch = [&](RawChunk &r) {
         r.t = pt; r.c = pc; r.len = pt < n_trials ? plen : 0u;    // (no events past the last trial)
-        r.v = make_uint4(0u, 0u, 0u, 0u);
+        r.v = make_uint4(sent, sent, sent, sent);
         if (pt < n_trials) {
             const uint32_t k = pc * 128u + 4u * lane;
             const uint32_t *src = events + pbase + k;
@@ -173,9 +205,10 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         const uint32_t ee[4] = {r.v.x, r.v.y, r.v.z, r.v.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const uint32_t bit = ee[q] >> shift;
+            const uint32_t bit = BM == 0 ? ee[q] : ee[q] >> shift;
             const uint32_t w = bitmap[bit >> 5];
-            const bool hit = k0 + q < r.len && ((w >> (bit & 31)) & 1u);
+            bool hit = __funnelshift_r(w, 0u, bit) & 1u;      // w >> (bit & 31)
+            if (BM == 2) hit = hit && k0 + q < r.len;
             S.ci[q] = make_uint2(0u, 0u);
             asm volatile(                                 // predicated load, no branch
                 "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.nc.v2.u32 {%0, %1}, [%3];\n}"
@@ -193,6 +226,29 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         if (S.c == 0) n = 0;
         const uint32_t k0 = S.c * 128u + 4u * lane;
         const uint32_t np = S.ci[0].y + S.ci[1].y + S.ci[2].y + S.ci[3].y;
+#if ARA_COMPACT_BALLOT_SCAN
+        // exclusive warp prefix of np, bit-sliced over ballots (votes, no
+        // shuffles through the shared-memory pipe): 3 slices unless some
+        // lane has >= 8 pairs in the chunk (np <= 64)
+        uint32_t excl = 0, tot = 0;
+        const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (np >> b) & 1u);
+            excl += (uint32_t)__popc(m & lt) << b;
+            tot += (uint32_t)__popc(m) << b;
+        }
+        if (__any_sync(0xffffffffu, np > 7u)) {
+#pragma unroll 1
+            for (int b = 3; b < 7; ++b) {
+                const uint32_t m = __ballot_sync(0xffffffffu, (np >> b) & 1u);
+                excl += (uint32_t)__popc(m & lt) << b;
+                tot += (uint32_t)__popc(m) << b;
+            }
+        }
+        if (S.c == 0) out = sink.begin(S.t);
+        uint32_t pos = n + excl;
+#else
         uint32_t incl = np;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -202,27 +258,40 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         if (S.c == 0) out = sink.begin(S.t);
         uint32_t pos = n + incl - np;
+#endif
         if (n + tot <= cap) {                         // the chunk fits (warp-uniform)
             // one 64-bit address per event, predicated stores (no branches)
-            uint64_t adr[4];
-            uint32_t mx = 0, o = 0;
-            const uint64_t base = reinterpret_cast<uint64_t>(out) + (uint64_t)kPairBytes * pos;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                adr[q] = base + kPairBytes * o;
-                if (PK) st_u32_if(S.ci[q].y != 0u, adr[q], (S.ci[q].x << A.kbits) | (k0 + q));
-                else st_pair_if(S.ci[q].y != 0u, adr[q], S.ci[q].x, k0 + q);
-                o += S.ci[q].y;
-                mx = max(mx, S.ci[q].y);
-            }
-            mx = __reduce_max_sync(0xffffffffu, mx);
-#pragma unroll 1
-            for (uint32_t j = 1; j < mx; ++j)         // the events with several pairs
+            uint32_t pq[4], mx = 0, o = pos;
+            if (PK) {                                 // pair = record * 2^kbits + k (one IMAD)
+                uint32_t *const out32 = reinterpret_cast<uint32_t *>(out);
+                uint32_t pv[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    if (PK) st_u32_if(j < S.ci[q].y, adr[q] + 4u * j, ((S.ci[q].x + j) << A.kbits) | (k0 + q));
-                    else st_pair_if(j < S.ci[q].y, adr[q] + 8u * j, S.ci[q].x + j, k0 + q);
+                    pq[q] = o;
+                    pv[q] = S.ci[q].x * mul + (k0 + q);
+                    st_u32_if(S.ci[q].y != 0u, reinterpret_cast<uint64_t>(out32 + o), pv[q]);
+                    o += S.ci[q].y;
+                    mx = max(mx, S.ci[q].y);
                 }
+#pragma unroll 1
+                for (uint32_t j = 1; __any_sync(0xffffffffu, j < mx); ++j)   // the events with several pairs
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        st_u32_if(j < S.ci[q].y, reinterpret_cast<uint64_t>(out32 + (pq[q] + j)), pv[q] + j * mul);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    pq[q] = o;
+                    st_pair_if(S.ci[q].y != 0u, reinterpret_cast<uint64_t>(out + o), S.ci[q].x, k0 + q);
+                    o += S.ci[q].y;
+                    mx = max(mx, S.ci[q].y);
+                }
+#pragma unroll 1
+                for (uint32_t j = 1; __any_sync(0xffffffffu, j < mx); ++j)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        st_pair_if(j < S.ci[q].y, reinterpret_cast<uint64_t>(out + (pq[q] + j)), S.ci[q].x + j, k0 + q);
+            }
         } else {                                      // overflow: the trial is redone by the fused kernel
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -302,7 +371,7 @@ struct HbmSink {
     }
 };
 
-template <bool PK>
+template <bool PK, int BM>
 __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __grid_constant__ SplitArgs A) {
     constexpr int kWarps = kCompactThreads / 32;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -311,10 +380,11 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&A.status->bad_event, 1u);
         return;
     }
-    for (uint32_t t = threadIdx.x; t < A.pf.bitmap_words; t += blockDim.x) bitmap[t] = A.pf.bitmap[t];
+    for (uint32_t t = threadIdx.x; t <= A.pf.bitmap_words; t += blockDim.x)   // + one zero word (sentinel)
+        bitmap[t] = t < A.pf.bitmap_words ? A.pf.bitmap[t] : 0u;
     __syncthreads();
     HbmSink sink{A};
-    produce_pairs<PK>(A, bitmap, blockIdx.x * kWarps + (threadIdx.x >> 5), gridDim.x * kWarps, sink);
+    produce_pairs<PK, BM>(A, bitmap, blockIdx.x * kWarps + (threadIdx.x >> 5), gridDim.x * kWarps, sink);
 }
 
 // ---------------------------------------------------------------------------
@@ -483,7 +553,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
             const bool end = (q >> 31) != 0u;
             const uint32_t lay = SL ? 0u : (uint32_t)fl[i];
             const double orr = SL ? occ_r0 : layers[lay].occ_r, oll = SL ? occ_l0 : layers[lay].occ_l;
-            const double g = fmin(fmax(o - orr, 0.0), oll);
+            const double g = xl_clip_(o - orr, oll);
             const bool first = end && !has_end, inner = end && has_end;
             head = first ? o : head;
             head_layer = first ? lay : head_layer;
@@ -660,7 +730,7 @@ __global__ void __launch_bounds__(1024, 1) fused_kernel(const __grid_constant__ 
     uint2 *ring = A.pairs + (uint64_t)blockIdx.x * kRing * A.cap;
     if (warp >= kNC) {                                // ---- producer
         RingSink sink{A, Q, ring};
-        produce_pairs<false>(A, bitmap, blockIdx.x * kNP + (warp - kNC), gridDim.x * kNP, sink);
+        produce_pairs<false, 2>(A, bitmap, blockIdx.x * kNP + (warp - kNC), gridDim.x * kNP, sink);
         __syncwarp();
         if (lane == 0) atomicAdd(&Q.prod_done, 1u);
         return;
@@ -781,8 +851,13 @@ static cudaError_t prepare_launch(const void *kern, size_t smem, int threads, in
 }
 
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms) {
-    const size_t smem = (A.pf.bitmap_words * 4u + 15u) & ~15u;
-    auto kern = A.kbits ? compact_kernel<true> : compact_kernel<false>;
+    const size_t smem = (A.pf.bitmap_words * 4u + 4u + 15u) & ~15u;
+    using K = void (*)(SplitArgs);
+    const int bm = !A.pf.sentinel_ok ? 2 : A.pf.bitmap_shift == 0 ? 0 : 1;
+    const K kern = A.kbits ? (bm == 0 ? (K)compact_kernel<true, 0> : bm == 1 ? (K)compact_kernel<true, 1>
+                                                                      : (K)compact_kernel<true, 2>)
+                           : (bm == 0 ? (K)compact_kernel<false, 0> : bm == 1 ? (K)compact_kernel<false, 1>
+                                                                       : (K)compact_kernel<false, 2>);
     int per_sm = 0;
     cudaError_t err = prepare_launch((const void *)kern, smem, kCompactThreads, per_sm);
     if (err != cudaSuccess) return err;

@@ -342,6 +342,8 @@ typedef struct {
     int32_t *table;
     /* outputs [n_layers][n_trials] */
     double *ylt, *gross;
+    double *occ_max;              /* or NULL: per (layer, trial) largest occurrence loss net of
+                                     occurrence terms (the OEP basis; NEXT-3 reading G29) */
     uint32_t *count;
     uint64_t *hash;
     /* work split */
@@ -357,7 +359,7 @@ static void *orc_worker(void *arg) {
         const double *T = J->layer_terms + 4 * (size_t)li;
         for (uint64_t t = J->t_begin; t < J->t_end; t++) {    /* line 3: each Trial */
             uint64_t i = J->trial_index[t];
-            double S = 0.0;
+            double S = 0.0, M = 0.0;
             uint32_t cnt = 0;
             uint64_t h = 0;
             for (uint64_t o = J->trial_off[t]; o < J->trial_off[t + 1]; o++) { /* line 4 */
@@ -387,10 +389,13 @@ static void *orc_worker(void *arg) {
                     }
                     l_e_sum += l_e;                                          /* line 9 */
                 }
-                S += orc_occ_terms(l_e_sum, T[0], T[1]);                     /* line 11 (G6) */
+                double g = orc_occ_terms(l_e_sum, T[0], T[1]);               /* line 11 (G6) */
+                S += g;
+                if (g > M) M = g;                                            /* OEP basis (G29) */
             }
             size_t oi = (size_t)li * J->n_trials + t;
             J->gross[oi] = S;
+            if (J->occ_max) J->occ_max[oi] = M;
             J->ylt[oi] = orc_agg_terms(S, T[2], T[3]);                      /* lines 12, 17 (G6) */
             J->count[oi] = cnt;
             J->hash[oi] = h;
@@ -410,7 +415,7 @@ int orc_run(uint32_t catalog_size, uint32_t n_elts, const uint64_t *elt_off,
             const uint32_t *layer_elts, const double *layer_terms, uint64_t n_trials,
             const uint64_t *trial_index, const uint64_t *trial_off, const uint32_t *events,
             uint64_t seed, int su, int n_threads, double *ylt, double *gross,
-            uint32_t *count, uint64_t *hash) {
+            uint32_t *count, uint64_t *hash, double *occ_max) {
     size_t slots = (size_t)n_elts * catalog_size;
     int32_t *table = (int32_t *)malloc((slots ? slots : 1) * sizeof(int32_t));
     if (!table) return -3;
@@ -437,7 +442,7 @@ int orc_run(uint32_t catalog_size, uint32_t n_elts, const uint64_t *elt_off,
         J->layer_elts = layer_elts; J->layer_terms = layer_terms; J->n_trials = n_trials;
         J->trial_index = trial_index; J->trial_off = trial_off; J->events = events;
         J->seed = seed; J->su = su; J->table = table;
-        J->ylt = ylt; J->gross = gross; J->count = count; J->hash = hash;
+        J->ylt = ylt; J->gross = gross; J->count = count; J->hash = hash; J->occ_max = occ_max;
         J->t_begin = n_trials * (uint64_t)w / (uint64_t)n_threads;
         J->t_end = n_trials * (uint64_t)(w + 1) / (uint64_t)n_threads;
         pthread_create(&th[w], NULL, orc_worker, J);

@@ -69,7 +69,7 @@ def lib():
         vp = C.c_void_p
         L.orc_run.argtypes = [u32, u32, vp, vp, vp, vp, vp, vp, vp,
                               u32, vp, vp, vp, vp, u64, vp, vp, vp,
-                              u64, i32, i32, vp, vp, vp, vp]
+                              u64, i32, i32, vp, vp, vp, vp, vp]
         L.orc_run.restype = i32
         _lib = L
     return _lib
@@ -175,7 +175,9 @@ def _ptr(a):
 
 
 def run(portfolio, yet, seed, su=True, n_threads=None, trial_index=None):
-    """Algorithm 1 over every layer; returns dict(ylt, gross, count, hash).
+    """Algorithm 1 over every layer; returns dict(ylt, gross, count, hash,
+    occ_max) -- occ_max = per (layer, trial) largest occurrence loss net of
+    the occurrence terms (line 11), the basis of the OEP (reading G29).
 
     ``portfolio``: dict with catalog_size, elt_off[n_elts+1], rec_event,
     rec_mean, rec_sigma_i, rec_sigma_c, rec_max (any float dtype; converted
@@ -208,6 +210,7 @@ def run(portfolio, yet, seed, su=True, n_threads=None, trial_index=None):
     gross = np.zeros((n_layers, n), dtype=np.float64)
     count = np.zeros((n_layers, n), dtype=np.uint32)
     hsh = np.zeros((n_layers, n), dtype=np.uint64)
+    occ_max = np.zeros((n_layers, n), dtype=np.float64)
     if n_threads is None:
         n_threads = os.cpu_count() or 1
     st = lib().orc_run(int(pf["catalog_size"]), n_elts, _ptr(elt_off), _ptr(rec_event),
@@ -215,11 +218,11 @@ def run(portfolio, yet, seed, su=True, n_threads=None, trial_index=None):
                        n_layers, _ptr(lprog), _ptr(loff), _ptr(lelts), _ptr(lterms),
                        n, _ptr(tidx), _ptr(toff), _ptr(ev),
                        int(seed) & 0xFFFFFFFFFFFFFFFF, 1 if su else 0, int(n_threads),
-                       _ptr(ylt), _ptr(gross), _ptr(count), _ptr(hsh))
+                       _ptr(ylt), _ptr(gross), _ptr(count), _ptr(hsh), _ptr(occ_max))
     if st == -1:
         raise OracleError("a beta quantile did not converge")
     if st == -2:
         raise OracleError("event id out of range")
     if st == -3:
         raise OracleError("out of memory building the direct-access table")
-    return {"ylt": ylt, "gross": gross, "count": count, "hash": hsh}
+    return {"ylt": ylt, "gross": gross, "count": count, "hash": hsh, "occ_max": occ_max}

@@ -55,7 +55,7 @@ def brute_force(pf, yet, seed, su, trial_index):
     key = (seed & M32, (seed >> 32) & M32)
     nl = len(pf["layer_prog"])
     n = len(yet["trial_off"]) - 1
-    ylt = np.zeros((nl, n)); gross = np.zeros((nl, n))
+    ylt = np.zeros((nl, n)); gross = np.zeros((nl, n)); occ_max = np.zeros((nl, n))
     for li in range(nl):
         p = int(pf["layer_prog"][li])
         occr, occl, aggr, aggl = pf["layer_terms"][li]
@@ -85,9 +85,12 @@ def brute_force(pf, yet, seed, su, trial_index):
                         R, Lm, sh = pf["elt_terms"][j]
                         x = sh * min(max(x - R, 0.0), Lm)
                     l += x
-                S += min(max(l - occr, 0.0), occl)
+                g = min(max(l - occr, 0.0), occl)
+                S += g
+                occ_max[li, t] = max(occ_max[li, t], g)
             gross[li, t] = S
             ylt[li, t] = min(max(S - aggr, 0.0), aggl)
+    brute_force.occ_max = occ_max
     return ylt, gross
 
 
@@ -154,6 +157,7 @@ def test_engine_vs_brute_force(seed):
     got = O.run(pf, yet, seed=rseed, su=su, n_threads=2, trial_index=tidx)
     ylt, gross = brute_force(pf, yet, rseed, su, tidx)
     np.testing.assert_allclose(got["gross"], gross, rtol=1e-9, atol=1e-6)
+    np.testing.assert_allclose(got["occ_max"], brute_force.occ_max, rtol=1e-9, atol=1e-6)
     np.testing.assert_allclose(got["ylt"], ylt, rtol=1e-9, atol=1e-6 * max(1.0, gross.max()))
 
 
@@ -251,3 +255,48 @@ def test_engine_empty_and_bounds():
         bad["events"][0] = pf2["catalog_size"]
         with pytest.raises(O.OracleError):
             O.run(pf2, bad, seed=2)
+
+
+# ---- OEP basis: the largest occurrence loss per (layer, trial) (reading G29)
+def test_occ_max_properties():
+    # 0 <= occ_max <= OccL; occ_max <= S <= K * occ_max (S is a sum of K terms,
+    # each in [0, occ_max])
+    rng = np.random.default_rng(91)
+    for _ in range(30):
+        pf, yet = tiny_case(rng)
+        got = O.run(pf, yet, seed=int(rng.integers(0, 2 ** 40)), su=True)
+        K = np.diff(yet["trial_off"]).astype(np.float64)
+        occl = np.asarray(pf["layer_terms"])[:, 1][:, None]
+        m, S = got["occ_max"], got["gross"]
+        assert (m >= 0).all() and (m <= occl).all()
+        assert (m <= S * (1 + 1e-12) + 1e-9).all()
+        assert (S <= K[None, :] * m * (1 + 1e-12) + 1e-9).all()
+
+
+def test_occ_max_single_occurrence_equals_gross():
+    # one occurrence per trial: the trial sum has one term, so occ_max == S
+    rng = np.random.default_rng(92)
+    pf, yet = tiny_case(rng, n_trials=19)
+    n = 19
+    yet = {"trial_off": np.arange(n + 1, dtype=np.uint64),
+           "events": rng.integers(0, pf["catalog_size"], n).astype(np.uint32)}
+    got = O.run(pf, yet, seed=5, su=True)
+    assert np.array_equal(got["occ_max"], got["gross"])
+
+
+def test_occ_max_sigma0_is_max_of_means():
+    # sigma = 0, one XELT, OccR = 0, OccL = inf: each occurrence loss is the
+    # record's mean (or 0 if absent), so occ_max = max over the trial's events
+    # of the mean -- computed here straight from the record arrays
+    rng = np.random.default_rng(93)
+    pf, yet = tiny_case(rng, n_layers=1, n_elts=1, sigma=False, n_trials=25)
+    pf["layer_elt_off"] = np.array([0, 1], np.uint64)
+    pf["layer_elts"] = np.array([0], np.uint32)
+    pf["layer_terms"] = np.array([[0.0, np.inf, 0.0, np.inf]])
+    mean_of = dict(zip(pf["rec_event"][:int(pf["elt_off"][1])].tolist(),
+                       pf["rec_mean"][:int(pf["elt_off"][1])].tolist()))
+    got = O.run(pf, yet, seed=3, su=True)
+    for t in range(25):
+        evs = yet["events"][int(yet["trial_off"][t]):int(yet["trial_off"][t + 1])]
+        want = max([mean_of.get(int(e), 0.0) for e in evs], default=0.0)
+        assert got["occ_max"][0, t] == want

@@ -191,6 +191,19 @@ void ara_yet_destroy(ara_yet *yet);
 int ara_run(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint64_t seed,
             uint32_t flags, float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash);
 
+/* ara_run plus the basis of the occurrence exceedance curve (OEP; SURVEY
+ * NEXT-3, reading G29: the paper's line-11 values, are the
+ * occurrence losses; the OEP takes their per-trial maximum):
+ *   occ_max   DEVICE [n_layers][n_trials] fp32, caller-allocated: the largest
+ *             occurrence loss net of occurrence terms of each (layer, trial),
+ *             0 for a trial without a present pair.  ara_risk_measures on it
+ *             (per layer, layer >= 0) gives OEP PML / TVaR; its roll-up over
+ *             layers (layer = -1) is NOT a portfolio OEP.
+ * Same arguments, outputs and errors as ara_run; ARA_EINVAL if occ_max is
+ * NULL or host memory, or with ARA_FUSED. */
+int ara_run_ep(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint64_t seed,
+               uint32_t flags, float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash);
+
 /* Device time of the kernels of the last ara_run on this context (CUDA
  * events on its stream): compact_ms = YET stream + lookup (compact_kernel),
  * sample_ms = draws + sampler + terms + YLT (sample_kernel; the fused

@@ -36,7 +36,7 @@ EXPORTS = (
     "ara_last_error", "ara_version", "ara_ctx_create", "ara_ctx_destroy", "ara_ctx_synchronize",
     "ara_validate_portfolio", "ara_create_portfolio", "ara_portfolio_destroy", "ara_portfolio_info",
     "ara_load_yet",
-    "ara_yet_refill", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_last_run_timings",
+    "ara_yet_refill", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings",
     "ara_risk_measures",
     "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles",
 )
@@ -69,6 +69,7 @@ def _load():
     L.ara_yet_num_trials.argtypes = [vp]; L.ara_yet_num_trials.restype = u64
     L.ara_yet_destroy.argtypes = [vp]; L.ara_yet_destroy.restype = None
     L.ara_run.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp]
+    L.ara_run_ep.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp, vp]
     L.ara_risk_measures.argtypes = [vp, vp, u32, u64, u32, i32, vp, u32, vp, vp]
     L.ara_last_run_timings.argtypes = [vp, vp, vp, vp]
     L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, u32, vp]
@@ -256,6 +257,28 @@ def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug
     _check(lib.ara_run(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(cnt),
                        _p(hsh)))
     return (ylt, cnt, hsh) if debug else ylt
+
+
+def run_ep(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug: bool = False,
+           ylt=None, occ_max=None, exact: bool = False, wide_pairs: bool = False):
+    """ara_run_ep; returns (ylt, occ_max) device [n_layers, n_trials] (+ count/hash if debug).
+    occ_max = the largest occurrence loss net of occurrence terms per (layer, trial): the OEP basis."""
+    import torch
+    dev = torch.device("cuda", ctx.device)
+    shape = (pf.n_layers, yet.n_trials)
+    if ylt is None:
+        ylt = torch.empty(shape, dtype=torch.float32, device=dev)
+    if occ_max is None:
+        occ_max = torch.empty(shape, dtype=torch.float32, device=dev)
+    cnt = hsh = None
+    if debug:
+        cnt = torch.zeros(shape, dtype=torch.int32, device=dev)
+        hsh = torch.zeros(shape, dtype=torch.int64, device=dev)
+    flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (EXACT if exact else 0) | \
+        (WIDE_PAIRS if wide_pairs else 0)
+    _check(lib.ara_run_ep(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(occ_max),
+                          _p(cnt), _p(hsh)))
+    return (ylt, occ_max, cnt, hsh) if debug else (ylt, occ_max)
 
 
 def last_run_timings(ctx: Context):

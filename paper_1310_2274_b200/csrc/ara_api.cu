@@ -503,8 +503,23 @@ void ara_yet_destroy(ara_yet *y) {
     delete y;
 }
 
+static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
+                    float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash);
+
 int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
             float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash) {
+    return run_impl(c, p, y, seed, flags, ylt, nullptr, dbg_count, dbg_hash);
+}
+
+int ara_run_ep(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
+               float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash) {
+    if (!occ_max) return fail(ARA_EINVAL, "occ_max is NULL (use ara_run)");
+    if (flags & ARA_FUSED) return fail(ARA_EINVAL, "ARA_FUSED does not produce occ_max");
+    return run_impl(c, p, y, seed, flags, ylt, occ_max, dbg_count, dbg_hash);
+}
+
+static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
+                    float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash) {
     if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
     if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_FUSED | ARA_WIDE_PAIRS))
         return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
@@ -513,6 +528,7 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
     if ((dbg_count || dbg_hash) && !(flags & ARA_DEBUG_LOOKUP))
         return fail(ARA_EINVAL, "dbg_count/dbg_hash need ARA_DEBUG_LOOKUP");
     if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
+    if (occ_max && !is_device_ptr(occ_max)) return fail(ARA_EINVAL, "occ_max must be device memory");
     CU(cudaSetDevice(c->device));
     const bool exact = (flags & ARA_EXACT) != 0 && (flags & ARA_SU) != 0;
     CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
@@ -545,6 +561,7 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         }
         SplitArgs S{p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status,
                     c->d_pairs, cap, c->d_counts, y->d_redo, {}};
+        S.occ_max = occ_max;
         // 4-byte pairs (record << kbits | k) when both fit: halves the pair traffic
         if (!fused && !(flags & ARA_WIDE_PAIRS)) {
             uint32_t kb = 1;
@@ -565,7 +582,7 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         CU(cudaEventRecord(c->ev[0], c->stream));
         CU(cudaEventRecord(c->ev[1], c->stream));
         CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, nullptr, 0,
-                       y->d_redo, exact, c->stream, c->num_sms));
+                       y->d_redo, exact, c->stream, c->num_sms, occ_max));
         CU(cudaEventRecord(c->ev[2], c->stream));
     }
     CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
@@ -576,7 +593,7 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
         const unsigned int n_redo = c->h_status->n_redo;
         CU(cudaMemsetAsync(&c->d_status->next_trial, 0, sizeof(unsigned long long), c->stream));
         CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, y->d_redo,
-                       n_redo, nullptr, (flags & ARA_SU) != 0, c->stream, c->num_sms));
+                       n_redo, nullptr, (flags & ARA_SU) != 0, c->stream, c->num_sms, occ_max));
         CU(cudaEventRecord(c->ev[3], c->stream));
         CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));

@@ -126,6 +126,7 @@ struct SplitArgs {
     uint32_t pkey[20];        // Philox key schedule of the seed (round r: pkey[2r], pkey[2r+1])
     uint32_t xcap;            // sample_kernel: pairs per segment (set by launch_sample)
     uint32_t kbits;           // > 0: pairs packed in 4 B as device record << kbits | k (two-kernel path)
+    float *occ_max;           // null, or [n_layers][n_trials] largest occurrence loss (G29)
 };
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);
@@ -150,7 +151,7 @@ void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_
 cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed, uint32_t flags,
                         float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
                         const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
-                        cudaStream_t s, int num_sms);
+                        cudaStream_t s, int num_sms, float *occ_max = nullptr);
 cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float2 *hot,
                                  const float *zp,
                                  const float *ze, uint64_t n, bool exact, float *out,

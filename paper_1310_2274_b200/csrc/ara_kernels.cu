@@ -172,6 +172,7 @@ struct ScanArgs {
     const uint32_t *trial_list;     // null: all trials
     uint64_t n_list;
     uint32_t *redo;                 // trials to re-run with the fp64 kernel
+    float *occ_max;                 // null, or [n_layers][n_trials] largest occurrence loss (G29)
 };
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
@@ -193,7 +194,7 @@ extern __shared__ __align__(16) unsigned char scan_smem[];
 
 // byte offsets of this warp's pieces and the block's tables in scan_smem
 struct WarpMem {
-    uint32_t buf, S, hsh, cnt, slots, layers;
+    uint32_t buf, S, hsh, cnt, om, slots, layers;
 };
 __device__ __forceinline__ WarpBuf &wbuf(const WarpMem &M) { return *reinterpret_cast<WarpBuf *>(scan_smem + M.buf); }
 __device__ __forceinline__ double *wS(const WarpMem &M) { return reinterpret_cast<double *>(scan_smem + M.S); }
@@ -201,6 +202,8 @@ __device__ __forceinline__ unsigned long long *whsh(const WarpMem &M) {
     return reinterpret_cast<unsigned long long *>(scan_smem + M.hsh);
 }
 __device__ __forceinline__ unsigned int *wcnt(const WarpMem &M) { return reinterpret_cast<unsigned int *>(scan_smem + M.cnt); }
+// largest occurrence loss of the trial per layer (fp32 bits; losses are >= 0)
+__device__ __forceinline__ unsigned int *wom(const WarpMem &M) { return reinterpret_cast<unsigned int *>(scan_smem + M.om); }
 __device__ __forceinline__ const SlotInfo *wslots(const WarpMem &M) {
     return reinterpret_cast<const SlotInfo *>(scan_smem + M.slots);
 }
@@ -348,7 +351,8 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
             const uint32_t lay = __shfl_sync(0xffffffffu, layer, leader);
             const bool mine = have && layer == lay;
             const double sum = warp_sum_f64(mine ? g : 0.0);
-            if (lane == 0) S[lay] += sum;
+            const unsigned mb = __reduce_max_sync(0xffffffffu, mine ? __float_as_uint((float)g) : 0u);
+            if (lane == 0) { S[lay] += sum; wom(M)[lay] = max(wom(M)[lay], mb); }
             pending &= ~__ballot_sync(0xffffffffu, mine);
         }
     }
@@ -517,7 +521,7 @@ template <bool SU, bool EX, int MW, bool DBG>
 __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_constant__ ScanArgs A) {
     const uint32_t nl = A.pf.n_layers;
     const uint32_t per_warp = (uint32_t)((sizeof(WarpBuf) + nl * (sizeof(double) + sizeof(unsigned long long) +
-                                                                   sizeof(unsigned int)) + 15) & ~size_t(15));
+                                                                   2 * sizeof(unsigned int)) + 15) & ~size_t(15));
     const uint32_t off_slots = 0;
     const uint32_t off_layers = off_slots + sizeof(SlotInfo) * ARA_MAX_SLOTS;
     const uint32_t off_bitmap = off_layers + sizeof(LayerInfo) * ARA_MAX_LAYERS;
@@ -537,12 +541,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
     M.S = M.buf + sizeof(WarpBuf);
     M.hsh = M.S + nl * sizeof(double);
     M.cnt = M.hsh + nl * sizeof(unsigned long long);
+    M.om = M.cnt + nl * sizeof(unsigned int);
     M.slots = off_slots;
     M.layers = off_layers;
     WarpBuf &B = wbuf(M);
     double *S = wS(M);
     unsigned long long *hsh = whsh(M);
     unsigned int *cntv = wcnt(M);
+    unsigned int *omv = wom(M);
     const bool dbg = DBG;
     const SampleArgs G{A.pf.recs, A.pf.tables, A.pf.hot, A.pf.rec_mu, A.pf.rec_orig, A.status, A.seed,
                        (A.flags & ARA_EXACT) != 0};
@@ -562,7 +568,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
         const uint64_t base = A.yet.fixed_len ? t * (uint64_t)A.yet.fixed_len : A.yet.offsets[t];
         const uint32_t len = A.yet.fixed_len ? A.yet.fixed_len : (uint32_t)(A.yet.offsets[t + 1] - base);
         const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);        // global trial index i
-        for (uint32_t l = lane; l < nl; l += 32) { S[l] = 0.0; cntv[l] = 0u; hsh[l] = 0ull; }
+        for (uint32_t l = lane; l < nl; l += 32) { S[l] = 0.0; cntv[l] = 0u; hsh[l] = 0ull; omv[l] = 0u; }
         __syncwarp();
         int q = 0;                         // packed queue state (qn, nseg, redo)
         const uint32_t *ev = A.yet.events + base;
@@ -648,6 +654,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
         for (uint32_t l = lane; l < nl; l += 32) {
             const LayerInfo &L = layers[l];
             A.ylt[(uint64_t)l * n_trials + t] = (float)fmin(fmax(S[l] - L.agg_r, 0.0), L.agg_l);
+            if (A.occ_max) A.occ_max[(uint64_t)l * n_trials + t] = __uint_as_float(omv[l]);
             if (dbg) {
                 if (A.dbg_count) A.dbg_count[(uint64_t)l * n_trials + t] = cntv[l];
                 if (A.dbg_hash) A.dbg_hash[(uint64_t)l * n_trials + t] = hsh[l];
@@ -660,7 +667,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
 
 static size_t scan_smem_bytes(const PortfolioDev &pf) {
     const size_t per_warp = (sizeof(WarpBuf) + pf.n_layers * (sizeof(double) + sizeof(unsigned long long) +
-                                                              sizeof(unsigned int)) + 15) & ~size_t(15);
+                                                              2 * sizeof(unsigned int)) + 15) & ~size_t(15);
     return sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
            ((size_t)pf.bitmap_words * 4 + 15) / 16 * 16 + kWarps * per_warp;
 }
@@ -693,8 +700,8 @@ static cudaError_t launch_scan_mw(const ScanArgs &A, bool exact_kernel, cudaStre
 cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed, uint32_t flags,
                         float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
                         const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
-                        cudaStream_t s, int num_sms) {
-    ScanArgs A{pf, yet, seed, flags, ylt, dbg_count, dbg_hash, status, trial_list, n_list, redo};
+                        cudaStream_t s, int num_sms, float *occ_max) {
+    ScanArgs A{pf, yet, seed, flags, ylt, dbg_count, dbg_hash, status, trial_list, n_list, redo, occ_max};
     if (trial_list && n_list == 0) return cudaSuccess;
     if (pf.mask_words == 1) return launch_scan_mw<1>(A, exact_kernel, s, num_sms);
     if (pf.mask_words <= 3) return launch_scan_mw<3>(A, exact_kernel, s, num_sms);

@@ -414,11 +414,12 @@ struct SampleWs {
     double *accs;                 // this lane's column of [nl][32]
     unsigned int *dc;             // [nl]
     unsigned long long *dhs;      // [nl]
+    float *mos;                   // OM, multi-layer: this lane's column of [nl][32] (largest occurrence loss)
 };
 
 // The sampler on trial t's n present pairs at `in` (CG: read them through L2
 // only, as the fused kernel's consumers must).
-template <bool SU, bool SL, bool DBG, bool CG, bool PK = false>
+template <bool SU, bool SL, bool DBG, bool CG, bool PK = false, bool OM = false>
 __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs &W, uint64_t t, uint32_t n,
                                              const uint2 *in) {
     const int lane = threadIdx.x & 31;
@@ -447,6 +448,9 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);
     if (!SL)
         for (uint32_t l = 0; l < nl; ++l) accs[l * 32] = 0.0;
+    if (OM && !SL)
+        for (uint32_t l = 0; l < nl; ++l) W.mos[l * 32] = 0.0f;
+    float mo = 0.0f;                               // OM, SL: this lane's largest occurrence loss
     if (DBG)
         for (uint32_t l = lane; l < nl; l += 32) { dc[l] = 0u; dhs[l] = 0ull; }
     double acc = 0.0;                              // SL: this lane's share of the trial sum
@@ -559,6 +563,10 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
             head_layer = first ? lay : head_layer;
             if (SL) acc += inner ? g : 0.0;
             else if (inner) accs[lay * 32] += g;
+            if (OM) {                                  // OEP basis (G29); fp32 rounding is monotone
+                if (SL) mo = fmaxf(mo, inner ? (float)g : 0.0f);
+                else if (inner) W.mos[lay * 32] = fmaxf(W.mos[lay * 32], (float)g);
+            }
             has_end = has_end || end;
             o = end ? 0.0 : o;
         }
@@ -582,6 +590,10 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
             const LayerInfo &L = layers[head_layer];
             const double g = fmin(fmax(head + in_run - L.occ_r, 0.0), L.occ_l);
             if (SL) acc += g; else accs[head_layer * 32] += g;
+            if (OM) {
+                if (SL) mo = fmaxf(mo, (float)g);
+                else W.mos[head_layer * 32] = fmaxf(W.mos[head_layer * 32], (float)g);
+            }
         }
         // run left open at the segment's end (continues in the next segment)
         const double last = has_end ? o : o + in_run;
@@ -604,10 +616,14 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 if (A.dbg_hash) A.dbg_hash[(uint64_t)l * n_trials + t] = dhs[l];
             }
         }
+        if (OM) {
+            const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(SL ? mo : W.mos[l * 32]));
+            if (lane == 0) A.occ_max[(uint64_t)l * n_trials + t] = __uint_as_float(mb);
+        }
     }
 }
 
-template <bool SU, bool SL, bool DBG, bool PK>
+template <bool SU, bool SL, bool DBG, bool PK, bool OM>
 __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 warps/SM: <= 64 registers
     sample_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -621,6 +637,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 wa
     unsigned int *cw = reinterpret_cast<unsigned int *>(accw + kSampleWarps * nl * 32);
     unsigned long long *hw = reinterpret_cast<unsigned long long *>(
         ((uintptr_t)(cw + kSampleWarps * nl) + 7) & ~(uintptr_t)7);            // [warps][nl]
+    float *mow = reinterpret_cast<float *>(hw + kSampleWarps * nl);             // OM && !SL: [warps][nl][32]
     for (uint32_t t = threadIdx.x; t < A.pf.n_slots; t += blockDim.x) slots[t] = A.pf.slots[t];
     for (uint32_t t = threadIdx.x; t < nl; t += blockDim.x) layers[t] = A.pf.layers[t];
     __syncthreads();
@@ -628,7 +645,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 wa
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (*A.yet.max_event >= A.pf.catalog) return;   // compact_kernel wrote no pairs
     const SampleWs W{slots, layers, xsw + warp * kXCap, flw + warp * kXCap, accw + warp * nl * 32 + lane,
-                     cw + warp * nl, hw + warp * nl};
+                     cw + warp * nl, hw + warp * nl, (OM && !SL) ? mow + warp * nl * 32 + lane : nullptr};
     while (true) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(&A.status->next_trial2, 1ull);
@@ -636,7 +653,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 wa
         if (t >= A.yet.n_trials) break;
         const uint32_t n = __ldg(A.counts + t);
         if (n == kOverflow) continue;                 // redone by the fused kernel
-        sample_trial<SU, SL, DBG, false, PK>(A, W, t, n, PK ? reinterpret_cast<const uint2 *>(
+        sample_trial<SU, SL, DBG, false, PK, OM>(A, W, t, n, PK ? reinterpret_cast<const uint2 *>(
                                                                    reinterpret_cast<const uint32_t *>(A.pairs) + t * A.cap)
                                                                : A.pairs + t * (uint64_t)A.cap);
         __syncwarp();
@@ -737,7 +754,7 @@ __global__ void __launch_bounds__(1024, 1) fused_kernel(const __grid_constant__ 
     }
     // ---- consumer
     const SampleWs W{slots, layers, xsw + warp * kXCap, flw + warp * kXCap, accw + warp * nl * 32 + lane,
-                     cw + warp * nl, hw + warp * nl};
+                     cw + warp * nl, hw + warp * nl, nullptr};
     while (true) {
         uint32_t i = 0, go = 0;
         if (lane == 0) {
@@ -872,23 +889,28 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
     if (A.pf.n_layers > kSplitMaxLayers) return cudaErrorInvalidValue;
     const size_t other = sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
                          sizeof(double) * kSampleWarps * A.pf.n_layers * 32 +
-                         kSampleWarps * A.pf.n_layers * (sizeof(unsigned int) + sizeof(unsigned long long)) + 16;
+                         kSampleWarps * A.pf.n_layers * (sizeof(unsigned int) + sizeof(unsigned long long)) + 16 +
+                         (A.occ_max && !sl ? sizeof(float) * kSampleWarps * A.pf.n_layers * 32 : 0);
     // shared memory left unclaimed is L1 data cache, which the record and table
     // gathers use: keep the segments short
-    const size_t budget = (size_t)ARA_SAMPLE_SMEM_KB * 1024;
     SplitArgs B = A;
     // (a multiple of the round, 32 kU pairs, so a segment ends on a round)
     constexpr size_t kR = 64 * kU;
+    const size_t min_xcap = (ARA_MAX_SLOTS + kR - 1) / kR * kR;
+    // many layers (+ occ_max) claim more: the budget grows to one minimal segment
+    const size_t budget = std::max((size_t)ARA_SAMPLE_SMEM_KB * 1024,
+                                   other + 8 + (sizeof(float) + sizeof(uint8_t)) * kSampleWarps * min_xcap);
     B.xcap = (uint32_t)std::min<size_t>(kXCapMax / kR * kR, (budget - other - 8) / (5 * kSampleWarps) / kR * kR);
     if (B.xcap < ARA_MAX_SLOTS) B.xcap = (uint32_t)((ARA_MAX_SLOTS + kR - 1) / kR * kR);
     const size_t smem = other + (sizeof(float) + sizeof(uint8_t)) * kSampleWarps * B.xcap + 8;
     using K = void (*)(SplitArgs);
-#define ARA_SK(P)                                                                                               \
-    (su ? (sl ? (dbg ? (K)sample_kernel<true, true, true, P> : (K)sample_kernel<true, true, false, P>)           \
-            : (dbg ? (K)sample_kernel<true, false, true, P> : (K)sample_kernel<true, false, false, P>))         \
-        : (sl ? (dbg ? (K)sample_kernel<false, true, true, P> : (K)sample_kernel<false, true, false, P>)         \
-              : (dbg ? (K)sample_kernel<false, false, true, P> : (K)sample_kernel<false, false, false, P>)))
-    const K kern = A.kbits ? ARA_SK(true) : ARA_SK(false);
+#define ARA_SK(P, O)                                                                                            \
+    (su ? (sl ? (dbg ? (K)sample_kernel<true, true, true, P, O> : (K)sample_kernel<true, true, false, P, O>)     \
+            : (dbg ? (K)sample_kernel<true, false, true, P, O> : (K)sample_kernel<true, false, false, P, O>))   \
+        : (sl ? (dbg ? (K)sample_kernel<false, true, true, P, O> : (K)sample_kernel<false, true, false, P, O>)   \
+              : (dbg ? (K)sample_kernel<false, false, true, P, O> : (K)sample_kernel<false, false, false, P, O>)))
+    const K kern = A.occ_max ? (A.kbits ? ARA_SK(true, true) : ARA_SK(false, true))
+                             : (A.kbits ? ARA_SK(true, false) : ARA_SK(false, false));
 #undef ARA_SK
     int per_sm = 0;
     cudaError_t err = prepare_launch((const void *)kern, smem, kSampleWarps * 32, per_sm);

@@ -467,3 +467,102 @@ def test_measures_end_to_end(A, ctx, name, n):
             po, to = OM.pml(o, rp), OM.tvar_rp(o, rp)[1]
             assert abs(pml[q] - po) <= REL * abs(po) + floor, (layer, rp, pml[q], po)
             assert abs(tvar[q] - to) <= REL * abs(to) + floor, (layer, rp, tvar[q], to)
+
+
+# ---- OEP basis (NEXT-3, reading G29): largest occurrence loss per (layer, trial)
+def occ_check(m, ref, pf, li):
+    # per-sample relative error <= 1e-5 (G12) on l = g + OccR gives the floor
+    o = ref["occ_max"][li]
+    occr = float(pf["layer_terms"][li][0])
+    m = np.asarray(m, np.float64)
+    tol = REL * o + 1e-5 * occr + 1e-3
+    bad = np.abs(m - o) > tol
+    assert not bad.any(), f"{bad.sum()} occ_max entries out of tolerance (layer {li})"
+    assert (m >= 0).all() and (m <= float(pf["layer_terms"][li][1])).all()
+
+
+def _oep_case(name):
+    cfg = aragen.load_config("cfg1")
+    if name == "cfg1":
+        pass
+    elif name == "layers8":
+        cfg.update(n_layers=8, elts_per_layer=16, catalog=4000, records_per_elt=600, n_trials=300,
+                   layer_terms=[[2e5 * (l + 1), 5e6, 1.0e6, 5.0e7] for l in range(8)])
+    elif name == "layers3_long":
+        cfg.update(n_layers=3, elts_per_layer=4, catalog=5000, records_per_elt=2000, n_trials=40,
+                   events_per_trial=1500, layer_terms=[[2e5 * (l + 1), 5e6, 1.0e6, 5.0e9] for l in range(3)])
+    elif name == "long1":
+        cfg.update(n_layers=1, elts_per_layer=2, catalog=5000, records_per_elt=2000, n_trials=40,
+                   events_per_trial=3000, layer_terms=[[2e5, 5e6, 1.0e6, 5.0e9]])
+    elif name == "ragged":
+        cfg.update(k_min=0, k_max=150, n_trials=700, catalog=300, records_per_elt=120)
+    return cfg
+
+
+@pytest.mark.parametrize("name", ["cfg1", "layers8", "layers3_long", "long1", "ragged"])
+@pytest.mark.parametrize("exact", [False, True])
+def test_occ_max_vs_oracle(A, ctx, name, exact):
+    cfg = _oep_case(name)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    ylt, occ = A.run_ep(ctx, P, Y, seed=cfg["seed"], exact=exact)
+    ref = oracle.run(pf, yet, seed=cfg["seed"])
+    g, m = ylt.cpu().numpy(), occ.cpu().numpy()
+    for li in range(pf["layer_terms"].shape[0]):
+        ylt_check(g[li], ref, li)
+        occ_check(m[li], ref, pf, li)
+    # the YLT does not depend on whether occ_max is requested
+    assert np.array_equal(g, A.run(ctx, P, Y, seed=cfg["seed"], exact=exact).cpu().numpy())
+
+
+def test_occ_max_redo_trials(A, ctx):
+    # a trial redone by the fp64-capable kernel (its pairs overflow the region)
+    # gets occ_max from that kernel
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 50
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    R, K = cfg["records_per_elt"], cfg["events_per_trial"]
+    both = np.intersect1d(pf["rec_event"][:R], pf["rec_event"][R:2 * R])
+    heavy = np.random.default_rng(4).choice(both, 400).astype(np.uint32)
+    ev = np.concatenate([yet["events"][:10 * K], heavy, yet["events"][10 * K:]])
+    off = np.concatenate([np.arange(11, dtype=np.uint64) * K,
+                          10 * K + 400 + np.arange(0, 41, dtype=np.uint64) * K])
+    y2 = {"trial_off": off, "events": ev, "first_trial": 0}
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, y2)
+    ylt, occ = A.run_ep(ctx, P, Y, seed=cfg["seed"])
+    assert A.last_run_timings(ctx)["redo_ms"] > 0
+    ref = oracle.run(pf, y2, seed=cfg["seed"])
+    ylt_check(ylt.cpu().numpy(), ref)
+    occ_check(occ.cpu().numpy()[0], ref, pf, 0)
+
+
+def test_occ_max_measures_oep(A, ctx):
+    # OEP PML / TVaR = the measures of the occ_max table (per layer)
+    cfg = aragen.load_config("cfg3")
+    cfg["n_trials"] = 20000
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    ylt, occ = A.run_ep(ctx, P, Y, seed=cfg["seed"])
+    ref = oracle.run(pf, yet, seed=cfg["seed"])
+    occ_check(occ.cpu().numpy()[0], ref, pf, 0)
+    rps = cfg["return_periods"]
+    pml, tvar = A.risk_measures(ctx, occ, 1, cfg["n_trials"], 0, rps=rps)
+    o = ref["occ_max"][0]
+    floor = 1e-5 * pf["layer_terms"][0][0] + 1e-3
+    for q, rp in enumerate(rps):
+        po, to = OM.pml(o, rp), OM.tvar_rp(o, rp)[1]
+        assert abs(pml[q] - po) <= REL * abs(po) + floor, (rp, pml[q], po)
+        assert abs(tvar[q] - to) <= REL * abs(to) + floor, (rp, tvar[q], to)
+
+
+def test_run_ep_errors(A, ctx):
+    import torch
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 10
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    ylt = torch.empty((1, 10), dtype=torch.float32, device="cuda")
+    with pytest.raises(A.AraError):
+        A._check(A.lib.ara_run_ep(ctx.h, P.h, Y.h, 1, A.SU, A._p(ylt), None, None, None))
+    with pytest.raises(A.AraError):
+        A._check(A.lib.ara_run_ep(ctx.h, P.h, Y.h, 1, A.SU | A.FUSED, A._p(ylt), A._p(ylt), None, None))

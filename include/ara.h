@@ -228,6 +228,16 @@ int ara_risk_measures(ara_ctx *ctx, const float *ylt, uint32_t n_layers, uint64_
                       uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
                       double *pml_out, double *tvar_out);
 
+/* ara_risk_measures plus VaR at each level q = 1 - 1/RP (SPEC S:373-381,
+ * the `var` field of RiskMeasures; SURVEY NEXT-3 "VaR at arbitrary levels"):
+ *   var_out    NULL or [n_rp] host: the VaR that TVaR averages above, i.e.
+ *              the descending order statistic of rank ceil(N/RP) (integer RP;
+ *              otherwise N - floor((1 - 1/RP) N) clamped to [1, N]).
+ * Same arguments, errors and synchronisation as ara_risk_measures. */
+int ara_risk_measures_var(ara_ctx *ctx, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                          uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
+                          double *pml_out, double *tvar_out, double *var_out);
+
 /* ---- component entry points (row-level parity tests) ------------------ */
 
 /* Secondary-uncertainty loss draws for n independent

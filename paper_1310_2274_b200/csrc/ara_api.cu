@@ -62,7 +62,7 @@ struct ara_ctx {
     int num_sms = 0;
     RunStatus *d_status = nullptr;
     RunStatus *h_status = nullptr;     // pinned
-    double *h_out = nullptr;           // pinned [128]: measures results
+    double *h_out = nullptr;           // pinned [192]: measures results (pml, tvar, var) per RP
     MeasuresScratch ms;
     uint2 *d_pairs = nullptr;          // split path scratch: per-trial pairs {device record, k}
     uint64_t pairs_capacity = 0;       // elements of d_pairs
@@ -124,10 +124,10 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
     c->num_sms = prop.multiProcessorCount;
     if (cudaMalloc(&c->d_status, sizeof(RunStatus)) != cudaSuccess ||
         cudaMallocHost(&c->h_status, sizeof(RunStatus)) != cudaSuccess ||
-        cudaMallocHost(&c->h_out, 128 * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&c->h_out, 192 * sizeof(double)) != cudaSuccess ||
         dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 4 * 256) != cudaSuccess ||
         dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
-        dalloc(&c->ms.d_out, 128) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
+        dalloc(&c->ms.d_out, 192) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
         dalloc(&c->ms.part_sum, kRedBlocks) != cudaSuccess ||
         dalloc(&c->ms.part_cnt, kRedBlocks) != cudaSuccess || cudaEventCreate(&c->ev[0]) != cudaSuccess ||
         cudaEventCreate(&c->ev[1]) != cudaSuccess || cudaEventCreate(&c->ev[2]) != cudaSuccess ||
@@ -650,6 +650,13 @@ static uint64_t needed_rank(uint64_t N, double rp) {
 int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
                       uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
                       double *pml_out, double *tvar_out) {
+    return ara_risk_measures_var(c, ylt, n_layers, n_total, n_shards, layer, rps, n_rp, pml_out, tvar_out,
+                                 nullptr);
+}
+
+int ara_risk_measures_var(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                          uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
+                          double *pml_out, double *tvar_out, double *var_out) {
     if (!c || !ylt || !rps || !pml_out || !tvar_out) return fail(ARA_EINVAL, "NULL argument");
     if (n_total == 0) return fail(ARA_EINVAL, "empty YLT");
     if (n_layers == 0 || n_shards == 0 || n_total % n_shards)
@@ -682,11 +689,12 @@ int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t 
                                 c->ms.d_out, c->stream));
     }
     double *out = c->h_out;                      // pinned
-    CU(cudaMemcpyAsync(out, c->ms.d_out, 2 * n_rp * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(out, c->ms.d_out, 3 * n_rp * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     for (uint32_t q = 0; q < n_rp; ++q) {
-        pml_out[q] = out[2 * q];
-        tvar_out[q] = out[2 * q + 1];
+        pml_out[q] = out[3 * q];
+        tvar_out[q] = out[3 * q + 1];
+        if (var_out) var_out[q] = out[3 * q + 2];
     }
     return ARA_OK;
 }

@@ -327,8 +327,9 @@ __global__ void __launch_bounds__(1024) sort_measures_kernel(const float *buf, S
             double sum = red_s[0];
             uint64_t c = red_c[0];
             if (var == (double)T) { sum += (double)neq * (double)T; c += neq; }
-            out[2 * q] = pml;
-            out[2 * q + 1] = sum / (double)c;
+            out[3 * q] = pml;
+            out[3 * q + 1] = sum / (double)c;
+            out[3 * q + 2] = var;
         }
         __syncthreads();
     }
@@ -372,8 +373,9 @@ __global__ void deep_final_kernel(const SelectState *states, const DeepRp *q, ui
     double sum = 0.0;
     unsigned long long cnt = 0;
     for (int b = 0; b < nblocks; ++b) { sum += part_sum[b]; cnt += part_cnt[b]; }
-    out[2 * rp_index] = pml;
-    out[2 * rp_index + 1] = sum / (double)cnt;
+    out[3 * rp_index] = pml;
+    out[3 * rp_index + 1] = sum / (double)cnt;
+    out[3 * rp_index + 2] = okey_inv(st[2].prefix);                          // VaR = L(m)
 }
 
 static cudaError_t select_rank(const float *vals, uint64_t n, SelectState *st, unsigned int *hist,

@@ -364,11 +364,15 @@ def test_measures_vs_oracle_sort(A, ctx, n):
     rps = [2, 10, 100, 250, 500] if n >= 1000 else [1.5, 2, 4]
     d = torch.from_numpy(x).cuda()
     pml, tvar = A.risk_measures(ctx, d, 1, n, 0, rps=rps)
+    pml2, tvar2, var = A.risk_measures_var(ctx, d, 1, n, 0, rps=rps)
+    assert np.array_equal(pml, pml2) and np.array_equal(tvar, tvar2)
     for q, rp in enumerate(rps):
         if OM.tvar_rp(x, rp) is None:
             continue
         assert pml[q] == pytest.approx(OM.pml(x.astype(np.float64), rp), rel=1e-12, abs=1e-9)
-        assert tvar[q] == pytest.approx(OM.tvar_rp(x.astype(np.float64), rp)[1], rel=1e-10)
+        vo, to = OM.tvar_rp(x.astype(np.float64), rp)
+        assert tvar[q] == pytest.approx(to, rel=1e-10)
+        assert var[q] == vo                     # an order statistic: exact
 
 
 @pytest.mark.parametrize("rp_min", [533, 266, 133, 66, 33])

@@ -52,7 +52,7 @@ struct __align__(16) BetaRec {
 // parameters and weights of BetaRec plus what the draw keys need, so a pair
 // is sampled from this one load.  meta: slot | run_end << 8 | layer << 16 |
 // mode << 28 (run_end: last record of its (event, layer) run).
-struct __align__(16) SplitRec {
+struct __align__(32) SplitRec {    // 32 B: one 256-bit load
     float a, b, wi, wc;
     float scale;
     uint32_t meta;

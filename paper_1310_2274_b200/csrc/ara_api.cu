@@ -79,6 +79,7 @@ struct ara_portfolio {
     uint2 *d_cidx = nullptr;
     uint32_t *d_rec_meta = nullptr;
     SplitRec *d_srecs = nullptr;
+    uint2 *d_mm = nullptr;             // (mean loss bits, meta) per device record (primary uncertainty)
     BetaRec *d_recs = nullptr;
     float2 *d_tables = nullptr, *d_hot = nullptr;
     float *d_mu = nullptr;
@@ -329,6 +330,7 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     };
     if (dalloc(&p->d_index, index.size()) || dalloc(&p->d_bitmap, words) ||
         dalloc(&p->d_cidx, (size_t)C) || dalloc(&p->d_rec_meta, (size_t)total) || dalloc(&p->d_srecs, (size_t)total) ||
+        dalloc(&p->d_mm, (size_t)total) ||
         dalloc(&p->d_rec_orig, total) || dalloc(&p->d_recs, total) || dalloc(&p->d_mu, total) ||
         dalloc(&p->d_tables, total * kTabStride) || dalloc(&p->d_hot, total * kHotN) ||
         dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) || dalloc(&d_raw, R) ||
@@ -356,7 +358,7 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) {
-        launch_split_recs(p->d_recs, p->d_rec_meta, p->d_slots, total, p->d_srecs, s);
+        launch_split_recs(p->d_recs, p->d_rec_meta, p->d_slots, p->d_mu, total, p->d_srecs, p->d_mm, s);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
@@ -383,7 +385,7 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     d.tables = p->d_tables;
     d.hot = p->d_hot;
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
-    d.cidx = p->d_cidx; d.rec_meta = p->d_rec_meta; d.srecs = p->d_srecs;
+    d.cidx = p->d_cidx; d.rec_meta = p->d_rec_meta; d.srecs = p->d_srecs; d.mu_meta = p->d_mm;
     d.any_terms = et ? 1u : 0u;
     *out = p;
     return ARA_OK;
@@ -396,7 +398,7 @@ int ara_portfolio_info(const ara_portfolio *p, uint64_t *n_dev, uint64_t *n_tl, 
     if (n_tl) *n_tl = d.n_exact_records;
     if (bytes)
         *bytes = (uint64_t)d.catalog * (d.idx_stride * 4 + sizeof(uint2)) + (uint64_t)d.bitmap_words * 4 +
-                 d.n_dev_records * (sizeof(BetaRec) + sizeof(float) + sizeof(uint32_t) + sizeof(uint32_t) + sizeof(SplitRec) +
+                 d.n_dev_records * (sizeof(BetaRec) + sizeof(float) + sizeof(uint32_t) + sizeof(uint32_t) + sizeof(SplitRec) + sizeof(uint2) +
                                     (kTabStride + kHotN) * sizeof(float2)) +
                  d.n_slots * sizeof(SlotInfo) + d.n_layers * sizeof(LayerInfo);
     return ARA_OK;
@@ -406,7 +408,7 @@ void ara_portfolio_destroy(ara_portfolio *p) {
     if (!p) return;
     if (p->ctx) cudaSetDevice(p->ctx->device);
     cudaFree(p->d_index); cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig); cudaFree(p->d_recs);
-    cudaFree(p->d_cidx); cudaFree(p->d_rec_meta); cudaFree(p->d_srecs);
+    cudaFree(p->d_cidx); cudaFree(p->d_rec_meta); cudaFree(p->d_srecs); cudaFree(p->d_mm);
     cudaFree(p->d_mu); cudaFree(p->d_slots); cudaFree(p->d_layers); cudaFree(p->d_tables); cudaFree(p->d_hot);
     delete p;
 }

@@ -81,6 +81,7 @@ struct PortfolioDev {
     const uint2 *cidx;        // [catalog] (first device record, record count) of each event
     const uint32_t *rec_meta; // [n_dev_records] slot | run_end << 8 | layer << 16 (SplitRec.meta)
     const SplitRec *srecs;    // [n_dev_records]
+    const uint2 *mu_meta;     // [n_dev_records] (mean loss bits, rec_meta): one 8 B gather per pair with SU off
     uint32_t any_terms;       // some slot has XELT terms (G7)
     const SlotInfo *slots;    // [n_slots]
     const LayerInfo *layers;  // [n_layers]
@@ -139,8 +140,8 @@ cudaError_t launch_count_bad(const uint32_t *ev, uint64_t n, uint32_t C, unsigne
                              int num_sms);
 
 // kernels
-void launch_split_recs(const BetaRec *recs, const uint32_t *rec_meta, const SlotInfo *slots, uint64_t n,
-                       SplitRec *out, cudaStream_t s);
+void launch_split_recs(const BetaRec *recs, const uint32_t *rec_meta, const SlotInfo *slots, const float *mu,
+                       uint64_t n, SplitRec *out, uint2 *mu_meta, cudaStream_t s);
 void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_t n,
                          BetaRec *out, float *out_mu, float2 *tables, float2 *hot,
                          unsigned int *n_exact, cudaStream_t s);

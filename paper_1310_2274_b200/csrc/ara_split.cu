@@ -143,7 +143,6 @@ __device__ __forceinline__ void st_pair_if(bool p, uint64_t addr, uint32_t a, ui
 template <bool PK, int BM, class Sink>
 __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t *bitmap, uint32_t first_warp,
                                               uint32_t nw, Sink &sink) {
-    constexpr uint32_t kPairBytes = PK ? 4u : 8u;   // packed: device record << kbits | k
     const int lane = threadIdx.x & 31;
     const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift, cap = A.cap;
     const uint32_t n_trials = (uint32_t)A.yet.n_trials;    // <= 2^32 - 1 (ara_load_yet)
@@ -436,7 +435,6 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     const SplitRec *__restrict__ srecs = A.pf.srecs;
     const float2 *__restrict__ hot = A.pf.hot;
     const float2 *__restrict__ tables = A.pf.tables;
-    const uint32_t *__restrict__ rmeta = A.pf.rec_meta;
     const uint32_t kb = A.kbits, kmask = (1u << kb) - 1u;
     auto ldpair = [&](const uint2 *q) -> uint2 {    // {device record, k}
         if (PK) {                                     // packed: record << kbits | k
@@ -512,8 +510,9 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
             } else {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    meta[u] = live[u] ? __ldg(rmeta + e[u].x) : 0u;
-                    x[u] = live[u] ? __ldg(A.pf.rec_mu + e[u].x) : 0.0f;
+                    const uint2 mm = live[u] ? __ldg(A.pf.mu_meta + e[u].x) : make_uint2(0u, 0u);
+                    meta[u] = mm.y;                   // primary uncertainty: the mean loss (one 8 B gather)
+                    x[u] = __uint_as_float(mm.x);
                 }
             }
 #pragma unroll
@@ -780,21 +779,23 @@ __global__ void __launch_bounds__(1024, 1) fused_kernel(const __grid_constant__ 
 }
 
 __global__ void split_recs_kernel(const BetaRec *__restrict__ recs, const uint32_t *__restrict__ rec_meta,
-                                  const SlotInfo *__restrict__ slots, uint64_t n, SplitRec *__restrict__ out) {
+                                  const SlotInfo *__restrict__ slots, const float *__restrict__ mu, uint64_t n,
+                                  SplitRec *__restrict__ out, uint2 *__restrict__ mu_meta) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
         const BetaRec r = recs[t];
         const uint32_t m = rec_meta[t];
         const SlotInfo &s = slots[m & 0xffu];
         out[t] = SplitRec{r.a, r.b, r.wi, r.wc, r.scale, m | (r.mode << 28), s.elt, s.prog};
+        mu_meta[t] = make_uint2(__float_as_uint(mu[t]), m);
     }
 }
 
-void launch_split_recs(const BetaRec *recs, const uint32_t *rec_meta, const SlotInfo *slots, uint64_t n,
-                       SplitRec *out, cudaStream_t s) {
+void launch_split_recs(const BetaRec *recs, const uint32_t *rec_meta, const SlotInfo *slots, const float *mu,
+                       uint64_t n, SplitRec *out, uint2 *mu_meta, cudaStream_t s) {
     if (n == 0) return;
     const uint64_t blocks = (n + 255) / 256;
-    split_recs_kernel<<<(unsigned)(blocks < 65535u * 16u ? blocks : 65535u * 16u), 256, 0, s>>>(recs, rec_meta,
-                                                                                               slots, n, out);
+    split_recs_kernel<<<(unsigned)(blocks < 65535u * 16u ? blocks : 65535u * 16u), 256, 0, s>>>(
+        recs, rec_meta, slots, mu, n, out, mu_meta);
 }
 
 // largest event id of a YET (run after every upload): ara_run checks it

@@ -49,6 +49,8 @@ def _L():
         L.aragen_trial_lengths.argtypes = [u64, u64, u64, u32, u32, vp]
         L.aragen_elt.argtypes = [u64, u32, u32, u32, d, i32, vp, vp, vp, vp, vp]
         L.aragen_elt.restype = i32
+        L.aragen_pack_bits.argtypes = [vp, u64, u32, vp, i32]
+        L.aragen_pack_bits.restype = i32
         _lib = L
     return _lib
 
@@ -146,3 +148,22 @@ def yet_for_trials(cfg, trial_indices):
     ev = np.concatenate([p["events"] for p in parts]) if parts else np.zeros(0, np.uint32)
     return {"trial_off": off, "events": ev,
             "trial_index": np.asarray(trial_indices, dtype=np.uint64)}
+
+
+def yet_bits(catalog):
+    """Bits per event id of the packed YET storage: ceil(log2(catalog))."""
+    return max(1, int(catalog - 1).bit_length())
+
+
+def pack_yet(events, bits, out=None, n_threads=None):
+    """Bit-pack uint32 event ids (storage encoding for the packed upload,
+    ara_yet_refill_packed): LSB-first, ceil(n*bits/32) uint32 words."""
+    ev = np.ascontiguousarray(events, np.uint32)
+    words = (ev.size * bits + 31) // 32
+    if out is None:
+        out = np.empty(words, np.uint32)
+    assert out.dtype == np.uint32 and out.size >= words
+    st = _L().aragen_pack_bits(_p(ev), ev.size, int(bits), _p(out), int(n_threads or os.cpu_count() or 1))
+    if st != 0:
+        raise ValueError("an event id does not fit in %d bits" % bits)
+    return out[:words]

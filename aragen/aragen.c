@@ -136,3 +136,45 @@ int aragen_elt(uint64_t seed, uint32_t j, uint32_t catalog, uint32_t n_rec,
     free(perm);
     return 0;
 }
+
+/* Storage encoding of a YET (not part of the method): event ids bit-packed
+ * LSB-first, id x in bits [x*bits, (x+1)*bits) of the little-endian uint32
+ * word stream (ids must be < 2^bits).  out has ceil(n*bits/32) words, zeroed
+ * here.  Threads split the ids at multiples of 32 ids (whole words). */
+typedef struct { const uint32_t *ev; uint64_t x0, x1; uint32_t bits; uint32_t *out; } pack_job;
+
+static void *pack_worker(void *arg) {
+    pack_job *J = (pack_job *)arg;
+    for (uint64_t x = J->x0; x < J->x1; x++) {
+        uint64_t bit = x * J->bits, w = bit >> 5;
+        uint32_t sh = (uint32_t)(bit & 31u), v = J->ev[x];
+        J->out[w] |= v << sh;
+        if (sh + J->bits > 32u) J->out[w + 1] |= v >> (32u - sh);
+    }
+    return NULL;
+}
+
+int aragen_pack_bits(const uint32_t *ev, uint64_t n, uint32_t bits, uint32_t *out, int n_threads) {
+    if (bits < 1 || bits > 32) return -1;
+    uint64_t words = (n * bits + 31) / 32;
+    memset(out, 0, words * sizeof(uint32_t));
+    if (bits < 32)
+        for (uint64_t x = 0; x < n; x++)
+            if (ev[x] >> bits) return -2;
+    if (n_threads < 1) n_threads = 1;
+    uint64_t blocks = (n + 31) / 32;          /* 32 ids end on a word boundary for any bits */
+    if ((uint64_t)n_threads > blocks) n_threads = blocks ? (int)blocks : 1;
+    pack_job *jobs = (pack_job *)calloc((size_t)n_threads, sizeof(pack_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)n_threads, sizeof(pthread_t));
+    for (int w = 0; w < n_threads; w++) {
+        pack_job *J = &jobs[w];
+        J->ev = ev; J->bits = bits; J->out = out;
+        J->x0 = blocks * (uint64_t)w / (uint64_t)n_threads * 32;
+        J->x1 = blocks * (uint64_t)(w + 1) / (uint64_t)n_threads * 32;
+        if (J->x1 > n) J->x1 = n;
+        pthread_create(&th[w], NULL, pack_worker, J);
+    }
+    for (int w = 0; w < n_threads; w++) pthread_join(th[w], NULL);
+    free(th); free(jobs);
+    return 0;
+}

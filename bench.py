@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--plain-upload", action="store_true", help="e2e: upload uint32 event ids, not packed")
     return ap.parse_args()
 
 
@@ -263,17 +264,33 @@ def run_ours(args, cfg, rank, world, local):
     copy_stream = torch.cuda.Stream(dev)
     ctx_copy = ara.Context(local, copy_stream)
     Ys = [Y, ara.Yet(ctx, ev_host, fixed_len=K, first_trial=lo, n_trials=n_loc)]
+    # the host YET as stored for upload: bit-packed at ceil(log2 catalog) bits per id
+    # (ara_yet_refill_packed stages and unpacks it on the device), or plain uint32
+    bits = aragen.yet_bits(cfg["catalog"]) if not args.plain_upload else 32
+    if bits < 32:
+        words = (n_loc * K * bits + 31) // 32
+        up_host = torch.empty(words, dtype=torch.int32).pin_memory()
+        aragen.pack_yet(ev_host.numpy().view(np.uint32), bits, out=up_host.numpy().view(np.uint32))
+        h2d_bytes = words * 4
+
+        def upload(Yx):
+            Yx.refill_packed(up_host, bits, ctx=ctx_copy)
+    else:
+        h2d_bytes = n_loc * K * 4
+
+        def upload(Yx):
+            Yx.refill(ev_host, ctx=ctx_copy)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     te0 = torch.cuda.Event(enable_timing=True); te1 = torch.cuda.Event(enable_timing=True)
     te0.record(stream)
     copy_stream.wait_event(te0)
-    Ys[0].refill(ev_host, ctx=ctx_copy)         # H2D of step 0's YET
+    upload(Ys[0])                               # H2D of step 0's YET
     for s_ in range(e2e_steps):
         ctx_copy.synchronize()                  # step s's YET is on the device
         if s_ + 1 < e2e_steps:
-            Ys[(s_ + 1) % 2].refill(ev_host, ctx=ctx_copy)   # H2D of step s+1 overlaps step s
+            upload(Ys[(s_ + 1) % 2])            # H2D of step s+1 overlaps step s
         Yc = Ys[s_ % 2]
         ara.run(ctx, P, Yc, seed=cfg["seed"], su=cfg["su"], ylt=ylt)
         src = ylt
@@ -362,10 +379,13 @@ def run_ours(args, cfg, rank, world, local):
                          "tables (index, bitmap, records) stay L2-resident by design",
                    "parallelism": f"trial-sharded x{world}" + (" + NCCL YLT all-gather" if world > 1 else "")},
         "e2e": {"value": N_total / (e2e_elapsed / e2e_steps), "unit": "trials/s",
-                "h2d_bytes_per_step": n_loc * K * 4, "d2h_bytes_per_step": L * n_loc * 4 + 16 * len(rps) * len(layers),
-                "steps": e2e_steps,
-                "how": "pinned host YET copied every step (second stream, double-buffered device YET: step s+1's "
-                       "H2D overlaps step s), ara_run + measures, YLT read back every step"},
+                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": L * n_loc * 4 + 16 * len(rps) * len(layers),
+                "steps": e2e_steps, "yet_upload_bits": bits,
+                "how": ("pinned host YET, stored bit-packed at %d bits per event id, copied every step and "
+                        "unpacked on the device (ara_yet_refill_packed)" % bits if bits < 32 else
+                        "pinned host YET (uint32 ids) copied every step (ara_yet_refill)") +
+                       " on a second stream into a double-buffered device YET (step s+1's H2D overlaps step s), "
+                       "ara_run + measures, YLT read back every step"},
         "gpu_launches": gpu_launches,
         "roofline": roof,
         "cpu_baseline": cpu,

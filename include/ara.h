@@ -161,7 +161,8 @@ int ara_portfolio_info(const ara_portfolio *pf, uint64_t *n_device_records,
  *   trial_offsets   [n_trials+1] host CSR offsets, or NULL for fixed length
  *   fixed_len       events per trial when trial_offsets == NULL
  *   event_ids       [total events] uint32, host or device, trial-major,
- *                   occurrence order within a trial
+ *                   occurrence order within a trial; NULL: every id starts
+ *                   as 0 (fill with ara_yet_refill / ara_yet_refill_packed)
  *   timestamps      NULL, or [total events] host floats that must be sorted
  *                   ascending within each trial; validated, then not
  *                   used (reading G19: the year loss is order-invariant)
@@ -173,6 +174,15 @@ int ara_load_yet(ara_ctx *ctx, uint64_t n_trials, uint64_t first_trial,
  * memory; asynchronous on the context stream (the host buffer must stay valid
  * until the stream passes the copy; pinned memory makes it a true DMA). */
 int ara_yet_refill(ara_ctx *ctx, ara_yet *yet, const uint32_t *event_ids);
+/* The same from a bit-packed copy of the event ids (a storage encoding of the
+ * YET, not part of the method): id x occupies bits
+ * [x*bits, (x+1)*bits) of the little-endian uint32 word stream `packed`
+ * (ceil(total*bits/32) words, host or device), bits in [1, 32]; with
+ * bits = ceil(log2 catalog) the host->device copy moves bits/32 of the bytes
+ * of ara_yet_refill.  The words are staged on the device and unpacked there
+ * by a kernel; asynchronous like ara_yet_refill.  Ids >= catalog_size are
+ * caught by ara_run (ARA_ERANGE).  ARA_EINVAL for bits out of range. */
+int ara_yet_refill_packed(ara_ctx *ctx, ara_yet *yet, uint32_t bits, const uint32_t *packed);
 uint64_t ara_yet_num_trials(const ara_yet *yet);
 void ara_yet_destroy(ara_yet *yet);
 

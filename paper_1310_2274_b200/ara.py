@@ -36,7 +36,7 @@ EXPORTS = (
     "ara_last_error", "ara_version", "ara_ctx_create", "ara_ctx_destroy", "ara_ctx_synchronize",
     "ara_validate_portfolio", "ara_create_portfolio", "ara_portfolio_destroy", "ara_portfolio_info",
     "ara_load_yet",
-    "ara_yet_refill", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings", "ara_risk_measures_var",
+    "ara_yet_refill", "ara_yet_refill_packed", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings", "ara_risk_measures_var",
     "ara_risk_measures",
     "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles",
 )
@@ -66,6 +66,7 @@ def _load():
     L.ara_portfolio_info.argtypes = [vp, vp, vp, vp]
     L.ara_load_yet.argtypes = [vp, u64, u64, vp, u32, vp, vp, C.POINTER(vp)]
     L.ara_yet_refill.argtypes = [vp, vp, vp]
+    L.ara_yet_refill_packed.argtypes = [vp, vp, u32, vp]
     L.ara_yet_num_trials.argtypes = [vp]; L.ara_yet_num_trials.restype = u64
     L.ara_yet_destroy.argtypes = [vp]; L.ara_yet_destroy.restype = None
     L.ara_run.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp]
@@ -227,6 +228,11 @@ class Yet:
         """ara_yet_refill: new event ids of the same shape, copied on ctx's stream
         (default: the context the YET was loaded with)."""
         _check(lib.ara_yet_refill((ctx or self.ctx).h, self.h, _p(events)))
+
+    def refill_packed(self, packed, bits: int, ctx: "Context" = None):
+        """ara_yet_refill_packed: new event ids from their bit-packed words
+        (aragen.pack_yet), staged and unpacked on the device, on ctx's stream."""
+        _check(lib.ara_yet_refill_packed((ctx or self.ctx).h, self.h, int(bits), _p(packed)))
 
     def close(self):
         if getattr(self, "h", None):

@@ -94,6 +94,8 @@ struct ara_yet {
     uint64_t *d_offsets = nullptr;
     uint32_t *d_redo = nullptr;        // trials to re-run with the fp64 kernel
     uint32_t *d_max = nullptr;         // largest event id (device word)
+    uint32_t *d_packed = nullptr;      // staging of packed uploads (+2 zero words)
+    uint64_t packed_capacity = 0;
     uint64_t avg_len_x1000 = 0;        // mean events per trial x 1000
     uint64_t max_len = 0;              // longest trial
 };
@@ -433,7 +435,7 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
         if (fixed_len > ARA_MAX_EVENTS_PER_TRIAL) return fail(ARA_EINVAL, "fixed_len > 2^24");
         total = n_trials * (uint64_t)fixed_len;
     }
-    if (total && !events) return fail(ARA_EINVAL, "event_ids is NULL");
+    // (events may be NULL: the ids start as 0, to be filled by ara_yet_refill[_packed])
     if (ts) {
         for (uint64_t t = 0; t < n_trials; ++t) {
             const uint64_t b = toff ? toff[t] : t * fixed_len, e = toff ? toff[t + 1] : b + fixed_len;
@@ -456,10 +458,12 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
         return fail(ARA_ENOMEM, "device allocation of %llu event ids failed", (unsigned long long)total);
     }
     cudaError_t e = cudaSuccess;
-    if (total)
+    if (total && events)
         e = cudaMemcpyAsync(y->d_events, events, total * sizeof(uint32_t),
                             is_device_ptr(events) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                             c->stream);
+    else if (total)
+        e = cudaMemsetAsync(y->d_events, 0, total * sizeof(uint32_t), c->stream);
     if (e == cudaSuccess && toff)
         e = cudaMemcpyAsync(y->d_offsets, toff, (n_trials + 1) * sizeof(uint64_t),
                             cudaMemcpyHostToDevice, c->stream);
@@ -493,6 +497,28 @@ int ara_yet_refill(ara_ctx *c, ara_yet *y, const uint32_t *events) {
     return ARA_OK;
 }
 
+int ara_yet_refill_packed(ara_ctx *c, ara_yet *y, uint32_t bits, const uint32_t *packed) {
+    if (!c || !y) return fail(ARA_EINVAL, "ctx/yet is NULL");
+    if (bits < 1 || bits > 32) return fail(ARA_EINVAL, "bits %u not in [1, 32]", bits);
+    if (y->dev.n_events == 0) return ARA_OK;
+    if (!packed) return fail(ARA_EINVAL, "packed is NULL");
+    const uint64_t words = (y->dev.n_events * (uint64_t)bits + 31) / 32;
+    CU(cudaSetDevice(c->device));
+    if (y->packed_capacity < words + 2) {              // staging grows once, then is reused
+        cudaFree(y->d_packed);
+        y->d_packed = nullptr;
+        y->packed_capacity = 0;
+        CU(dalloc(&y->d_packed, words + 2));
+        y->packed_capacity = words + 2;
+    }
+    CU(cudaMemsetAsync(y->d_packed + words, 0, 2 * sizeof(uint32_t), c->stream));   // read past the end
+    CU(cudaMemcpyAsync(y->d_packed, packed, words * sizeof(uint32_t),
+                       is_device_ptr(packed) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    CU(launch_unpack_yet(y->d_packed, y->dev.n_events, bits, y->d_events, c->stream, c->num_sms));
+    CU(launch_yet_max(y->d_events, y->dev.n_events, y->d_max, c->stream, c->num_sms));
+    return ARA_OK;
+}
+
 uint64_t ara_yet_num_trials(const ara_yet *y) { return y ? y->dev.n_trials : 0; }
 
 void ara_yet_destroy(ara_yet *y) {
@@ -502,6 +528,7 @@ void ara_yet_destroy(ara_yet *y) {
     cudaFree(y->d_offsets);
     cudaFree(y->d_redo);
     cudaFree(y->d_max);
+    cudaFree(y->d_packed);
     delete y;
 }
 

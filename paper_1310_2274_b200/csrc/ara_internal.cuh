@@ -135,6 +135,8 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);
 // pairs, 0 if the portfolio does not fit its shared memory
 uint64_t fused_ring_pairs(const PortfolioDev &pf, uint32_t cap, int num_sms);
 cudaError_t launch_fused(const SplitArgs &A, cudaStream_t s, int num_sms);
+cudaError_t launch_unpack_yet(const uint32_t *packed, uint64_t n, uint32_t bits, uint32_t *out, cudaStream_t s,
+                              int num_sms);
 cudaError_t launch_yet_max(const uint32_t *ev, uint64_t n, uint32_t *out, cudaStream_t s, int num_sms);
 cudaError_t launch_count_bad(const uint32_t *ev, uint64_t n, uint32_t C, unsigned int *out, cudaStream_t s,
                              int num_sms);

@@ -798,6 +798,33 @@ void launch_split_recs(const BetaRec *recs, const uint32_t *rec_meta, const Slot
         recs, rec_meta, slots, mu, n, out, mu_meta);
 }
 
+// Packed YET upload (ara_yet_refill_packed): ids bit-packed LSB-first, `bits`
+// per id -> uint32 event ids.  Four ids per thread, one 16 B store; the
+// packed words are read through L1 (each word serves ~32/bits ids).
+__global__ void unpack_yet_kernel(const uint32_t *__restrict__ packed, uint64_t n, uint32_t bits,
+                                  uint32_t *__restrict__ out) {
+    const uint32_t mask = bits == 32u ? 0xffffffffu : (1u << bits) - 1u;
+    const uint64_t n4 = (n + 3) / 4;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n4; q += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t bit = (4 * q + j) * (uint64_t)bits, w = bit >> 5;
+            const uint32_t sh = (uint32_t)(bit & 31u);
+            const uint32_t lo = __ldg(packed + w), hi = __ldg(packed + w + 1);   // (+2 words of padding)
+            v[j] = __funnelshift_r(lo, hi, sh) & mask;
+        }
+        reinterpret_cast<uint4 *>(out)[q] = make_uint4(v[0], v[1], v[2], v[3]);   // (+4 words of padding)
+    }
+}
+
+cudaError_t launch_unpack_yet(const uint32_t *packed, uint64_t n, uint32_t bits, uint32_t *out, cudaStream_t s,
+                              int num_sms) {
+    if (n == 0) return cudaSuccess;
+    unpack_yet_kernel<<<num_sms * 8, 256, 0, s>>>(packed, n, bits, out);
+    return cudaGetLastError();
+}
+
 // largest event id of a YET (run after every upload): ara_run checks it
 // against the catalog before any table is indexed
 __global__ void yet_max_kernel(const uint32_t *__restrict__ ev, uint64_t n, uint32_t *out) {

@@ -2,6 +2,7 @@
 trial range or rank gives the same events), distinct events per XELT, the
 value recipe's ranges, and that no generated record hits the sigma cap."""
 import numpy as np
+import pytest
 import scipy.stats as st
 
 import aragen
@@ -73,3 +74,20 @@ def test_sigma_scale_zero_and_integer_mu():
     pf = aragen.build_portfolio(cfg)
     assert (pf["rec_sigma_i"] == 0).all() and (pf["rec_sigma_c"] == 0).all()
     assert np.array_equal(pf["rec_mean"], np.round(pf["rec_mean"]))
+
+
+def test_pack_yet_roundtrip():
+    # the packed YET storage encoding: id x at bits [x*b, (x+1)*b), LSB first
+    rng = np.random.default_rng(3)
+    for bits in (1, 5, 14, 20, 21, 31, 32):
+        n = 777 + bits
+        ev = rng.integers(0, 2 ** bits, n, dtype=np.uint64).astype(np.uint32)
+        w = aragen.pack_yet(ev, bits)
+        assert w.size == (n * bits + 31) // 32
+        big = int.from_bytes(w.tobytes(), "little")
+        got = [(big >> (i * bits)) & ((1 << bits) - 1) for i in range(n)]
+        assert np.array_equal(np.array(got, np.uint64), ev.astype(np.uint64))
+    with pytest.raises(ValueError):
+        aragen.pack_yet(np.array([1 << 20], np.uint32), 20)
+    assert aragen.yet_bits(1_000_000) == 20 and aragen.yet_bits(2_000_000) == 21
+    assert aragen.yet_bits(1 << 20) == 20 and aragen.yet_bits((1 << 20) + 1) == 21

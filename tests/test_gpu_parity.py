@@ -570,3 +570,43 @@ def test_run_ep_errors(A, ctx):
         A._check(A.lib.ara_run_ep(ctx.h, P.h, Y.h, 1, A.SU, A._p(ylt), None, None, None))
     with pytest.raises(A.AraError):
         A._check(A.lib.ara_run_ep(ctx.h, P.h, Y.h, 1, A.SU | A.FUSED, A._p(ylt), A._p(ylt), None, None))
+
+
+# ---- packed YET upload (storage encoding; ara_yet_refill_packed) -------------
+@pytest.mark.parametrize("ragged", [False, True])
+def test_packed_refill_matches_plain(A, ctx, ragged):
+    cfg = aragen.load_config("cfg1")
+    if ragged:
+        cfg.update(k_min=0, k_max=150, n_trials=700)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P = A.Portfolio(ctx, pf)
+    Y0 = A.Yet.from_dict(ctx, yet)
+    ref = A.run(ctx, P, Y0, seed=cfg["seed"], debug=True)
+    for bits in (aragen.yet_bits(cfg["catalog"]), 17, 32):
+        words = aragen.pack_yet(yet["events"], bits)
+        if yet.get("fixed_len"):
+            Y = A.Yet(ctx, None, fixed_len=yet["fixed_len"], n_trials=len(yet["trial_off"]) - 1)
+        else:
+            Y = A.Yet(ctx, None, trial_off=yet["trial_off"])
+        Y.refill_packed(words, bits)
+        got = A.run(ctx, P, Y, seed=cfg["seed"], debug=True)
+        for a, b in zip(got, ref):
+            assert np.array_equal(a.cpu().numpy(), b.cpu().numpy()), bits
+
+
+def test_packed_refill_errors(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 20
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P = A.Portfolio(ctx, pf)
+    Y = A.Yet(ctx, None, fixed_len=yet["fixed_len"], n_trials=20)
+    w = aragen.pack_yet(yet["events"], 20)
+    for bad in (0, 33):
+        with pytest.raises(A.AraError):
+            Y.refill_packed(w, bad)
+    ev = yet["events"].copy()
+    ev[17] = cfg["catalog"] + 5                     # out of the catalogue, fits in 20 bits
+    Y.refill_packed(aragen.pack_yet(ev, 20), 20)
+    with pytest.raises(A.AraError) as ei:
+        A.run(ctx, P, Y, seed=1)
+    assert ei.value.code == 2                       # ARA_ERANGE

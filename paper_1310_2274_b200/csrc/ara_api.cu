@@ -130,7 +130,8 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
         cudaMallocHost(&c->h_out, 192 * sizeof(double)) != cudaSuccess ||
         dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 4 * 256) != cudaSuccess ||
         dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
-        dalloc(&c->ms.d_out, 192) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
+        dalloc(&c->ms.d_out, 192) != cudaSuccess ||
+        dalloc(&c->ms.mhist, 4 * kMaxPlanRanks * 256) != cudaSuccess || dalloc(&c->ms.macc, 8) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
         dalloc(&c->ms.part_sum, kRedBlocks) != cudaSuccess ||
         dalloc(&c->ms.part_cnt, kRedBlocks) != cudaSuccess || cudaEventCreate(&c->ev[0]) != cudaSuccess ||
         cudaEventCreate(&c->ev[1]) != cudaSuccess || cudaEventCreate(&c->ev[2]) != cudaSuccess ||
@@ -151,6 +152,8 @@ void ara_ctx_destroy(ara_ctx *c) {
     cudaFree(c->ms.vals);
     cudaFree(c->ms.buf);
     cudaFree(c->ms.hist);
+    cudaFree(c->ms.mhist);
+    cudaFree(c->ms.macc);
     cudaFree(c->ms.state);
     cudaFree(c->ms.d_rps);
     cudaFree(c->ms.d_out);
@@ -708,7 +711,10 @@ int ara_risk_measures_var(ara_ctx *c, const float *ylt, uint32_t n_layers, uint6
         CU(dalloc(&c->ms.vals, n_total));
         c->ms.capacity = n_total;
     }
-    if (k_need <= kSortCap) {
+    if (n_rp <= 4 && getenv("ARA_MEASURES_SORT") == nullptr) {   // joint select, one launch
+        CU(launch_measures_multi(ylt, n_layers, n_total, n_shards, layer, rps, n_rp, c->ms, c->ms.d_out,
+                                 c->stream));
+    } else if (k_need <= kSortCap) {
         RpList R{};
         for (uint32_t q = 0; q < n_rp; ++q) R.v[q] = rps[q];
         CU(launch_measures(ylt, n_layers, n_total, n_shards, layer, R, n_rp, k_need, c->ms, c->ms.d_out,

@@ -210,6 +210,208 @@ __global__ void __launch_bounds__(256) select_coop_kernel(const float *ylt, uint
     if (lane == 0 && n_eq) atomicAdd(&st->n_eq, n_eq);
 }
 
+// ---- every needed order statistic in one cooperative launch (n_rp <= 4) ----
+// The host plans the ranks (PML's L(fl), L(fl+1), VaR = L(m) per return
+// period, L(1), L(N); G13b); four 8-bit radix passes select all of them at
+// once -- ranks that share a key prefix share a histogram -- and a last pass
+// forms the TVaR tail sums as int64 fixed-point sums (order-independent, so
+// exact and deterministic under atomics).  No tail buffer, no sort, no rank
+// limit (deep return periods take the same path).
+#ifndef ARA_MULTI_THREADS
+#define ARA_MULTI_THREADS 1024
+#endif
+constexpr int kMultiThreads = ARA_MULTI_THREADS;     // one block per SM: cheap grid barriers
+
+struct __align__(8) MeasPlan {
+    uint64_t rank[kMaxPlanRanks];                  // distinct ranks (1-based, descending order)
+    uint64_t fl[4];
+    double frac[4];
+    int8_t i_one, i_n, i_fl[4], i_fl1[4], i_m[4];
+    uint32_t nr, nq;
+};
+
+__global__ void __launch_bounds__(kMultiThreads) select_multi_kernel(const float *ylt, uint32_t n_layers, uint64_t per,
+                                                           uint32_t n_shards, int32_t layer, float *vals,
+                                                           const __grid_constant__ MeasPlan M,
+                                                           unsigned int *ghist, unsigned long long *gacc,
+                                                           uint64_t n_total, double *out) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned int h[kMaxPlanRanks][256];
+    __shared__ uint64_t s_need[kMaxPlanRanks];
+    __shared__ uint32_t s_prefix[kMaxPlanRanks];
+    __shared__ int s_grp[kMaxPlanRanks];
+    __shared__ long long s_a[kMultiThreads / 32][4];
+    __shared__ unsigned long long s_c[kMultiThreads / 32][4];
+    const uint64_t n = per * n_shards;
+    const int nr = (int)M.nr, nq = (int)M.nq;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + tid, gstride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t wbase = gtid - lane;               // warp-uniform loop base
+    for (uint64_t i = gtid; i < 4ull * kMaxPlanRanks * 256; i += gstride) ghist[i] = 0u;
+    if (gtid < 8) gacc[gtid] = 0ull;
+    if (tid < kMaxPlanRanks) { s_need[tid] = M.rank[tid]; s_prefix[tid] = 0u; }
+    grid.sync();
+    uint32_t pmask = 0u;
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        unsigned int *hist = ghist + pass * kMaxPlanRanks * 256;
+        if (tid < kMaxPlanRanks) {                     // group = first rank with the same prefix
+            int g = (int)tid;
+            for (int i = 0; i < (int)tid; ++i)
+                if (s_prefix[i] == s_prefix[tid]) { g = i; break; }
+            s_grp[tid] = g;
+        }
+        for (uint32_t i = tid; i < kMaxPlanRanks * 256u; i += blockDim.x) (&h[0][0])[i] = 0u;
+        __syncthreads();
+        uint32_t gp[kMaxPlanRanks];                    // group leaders' prefixes in registers
+#pragma unroll
+        for (int g = 0; g < kMaxPlanRanks; ++g) gp[g] = (g < nr && s_grp[g] == g) ? s_prefix[g] : 0xffffffffu;
+        for (uint64_t b = wbase; b < n; b += gstride) {
+            const uint64_t t = b + lane;
+            uint32_t gd = 0xffffffffu;                 // (group, digit) of this element, or none
+            if (t < n) {
+                float v;
+                if (pass == 0) {                       // gather / roll-up (G16)
+                    const uint64_t sh = t / per, i = t - sh * per;
+                    const float *base = ylt + sh * (uint64_t)n_layers * per + i;
+                    if (layer >= 0) {
+                        v = base[(uint64_t)layer * per];
+                    } else {
+                        v = 0.0f;
+                        for (uint32_t l = 0; l < n_layers; ++l) v += base[(uint64_t)l * per];
+                    }
+                    vals[t] = v;
+                } else {
+                    v = vals[t];
+                }
+                const uint32_t k = okey(v), kp = k & pmask;
+#pragma unroll
+                for (int g = kMaxPlanRanks - 1; g >= 0; --g)   // groups are disjoint
+                    if (kp == gp[g]) gd = (uint32_t)g << 8 | ((k >> shift) & 0xffu);
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, gd);
+            if (gd != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
+                atomicAdd(&h[gd >> 8][gd & 0xffu], (unsigned)__popc(peers));
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < (uint32_t)nr * 256u; i += blockDim.x)
+            if ((&h[0][0])[i]) atomicAdd(&hist[i], (&h[0][0])[i]);
+        grid.sync();
+        if ((int)warp < nr) {                          // every block: the digits of its ranks
+            for (int r = (int)warp; r < nr; r += (int)(blockDim.x >> 5)) {
+                uint64_t need = s_need[r];
+                uint32_t prefix = s_prefix[r], pm = pmask;
+                pick_digit(hist + s_grp[r] * 256, shift, need, prefix, pm);
+                if (lane == 0) { s_need[r] = need; s_prefix[r] = prefix; }
+            }
+        }
+        pmask |= 0xffu << shift;
+        __syncthreads();
+    }
+    // TVaR tail sums: entries >= VaR (ties included), fixed point v * 2^E
+    uint32_t vk[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) vk[q] = q < nq ? s_prefix[M.i_m[q]] : 0xffffffffu;
+    const float vmax = fmaxf(fabsf(okey_inv(s_prefix[M.i_one])), fabsf(okey_inv(s_prefix[M.i_n])));
+    int ex = 0;
+    frexpf(vmax > 0.0f && vmax < INFINITY ? vmax : 1.0f, &ex);   // |v| < 2^ex
+    const int lg = 64 - __clzll((long long)(n + 1));             // n + 1 <= 2^lg
+    const double scale = ldexp(1.0, 62 - ex - lg);
+    long long a[4] = {0, 0, 0, 0};
+    unsigned long long c[4] = {0, 0, 0, 0};
+    for (uint64_t t = gtid; t < n; t += gstride) {
+        const float v = vals[t];
+        const uint32_t k = okey(v);
+        const long long fx = __double2ll_rn((double)v * scale);  // exact scaling by a power of 2
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q < nq && k >= vk[q]) { a[q] += fx; ++c[q]; }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+            c[q] += __shfl_xor_sync(0xffffffffu, c[q], o);
+        }
+        if (lane == 0) { s_a[warp][q] = a[q]; s_c[warp][q] = c[q]; }
+    }
+    __syncthreads();
+    if (tid < (uint32_t)nq) {
+        long long sa = 0;
+        unsigned long long sc = 0;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) { sa += s_a[w][tid]; sc += s_c[w][tid]; }
+        if (sa) atomicAdd(&gacc[tid], (unsigned long long)sa);     // two's complement: signed sums
+        if (sc) atomicAdd(&gacc[4 + tid], sc);
+    }
+    grid.sync();
+    if (blockIdx.x == 0 && tid < (uint32_t)nq) {
+        const int q = (int)tid;
+        auto L = [&](int i) -> double { return (double)okey_inv(s_prefix[i]); };
+        const uint64_t fl = M.fl[q], N = n_total;
+        const double frac = M.frac[q];
+        double pml;
+        if (fl < 1 || (fl == 1 && frac == 0.0)) pml = L(M.i_one);
+        else if (fl >= N) pml = L(M.i_n);
+        else pml = L(M.i_fl[q]) + frac * (L(M.i_fl1[q]) - L(M.i_fl[q]));
+        const double sum = (double)(long long)__ldcg(&gacc[q]) / scale;
+        out[3 * q] = pml;
+        out[3 * q + 1] = sum / (double)__ldcg(&gacc[4 + q]);
+        out[3 * q + 2] = L(M.i_m[q]);
+    }
+}
+
+cudaError_t launch_measures_multi(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
+                                  int32_t layer, const double *rps, uint32_t n_rp, MeasuresScratch &S,
+                                  double *d_out, cudaStream_t s) {
+    MeasPlan M{};
+    const uint64_t N = n_total;
+    auto idx = [&](uint64_t r) -> int8_t {            // index of rank r in the plan (added if new)
+        if (r < 1) r = 1;
+        if (r > N) r = N;
+        for (uint32_t i = 0; i < M.nr; ++i) if (M.rank[i] == r) return (int8_t)i;
+        M.rank[M.nr] = r;
+        return (int8_t)M.nr++;
+    };
+    M.i_one = idx(1);
+    M.i_n = idx(N);
+    for (uint32_t q = 0; q < n_rp; ++q) {             // (G13b; as sort_measures_kernel)
+        const double rp = rps[q];
+        uint64_t fl, m;
+        double frac;
+        if (rp == floor(rp) && rp < 1.8e19) {
+            const uint64_t R = (uint64_t)rp;
+            fl = (N + 1) / R; frac = (double)((N + 1) % R) / rp; m = (N + R - 1) / R;
+        } else {
+            const double r = (double)(N + 1) / rp;
+            fl = (uint64_t)floor(r); frac = r - (double)fl;
+            const uint64_t a = (uint64_t)floor((1.0 - 1.0 / rp) * (double)N) + 1;
+            m = N - (a < N ? a : N) + 1;
+        }
+        if (m < 1) m = 1;
+        if (m > N) m = N;
+        M.fl[q] = fl; M.frac[q] = frac;
+        M.i_fl[q] = idx(fl); M.i_fl1[q] = idx(fl + 1); M.i_m[q] = idx(m);
+    }
+    M.nq = n_rp;
+    static int blocks = 0;                            // co-resident blocks of the cooperative launch
+    if (!blocks) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_multi_kernel, kMultiThreads, 0);
+        blocks = sms * (per_sm < 1 ? per_sm : 1);
+    }
+    const uint64_t per = n_total / n_shards;
+    float *vals = S.vals;
+    unsigned int *hist = S.mhist;
+    unsigned long long *acc = S.macc;
+    uint64_t nt = n_total;
+    void *args[] = {(void *)&ylt, (void *)&n_layers, (void *)&per, (void *)&n_shards, (void *)&layer,
+                    (void *)&vals, (void *)&M, (void *)&hist, (void *)&acc, (void *)&nt, (void *)&d_out};
+    return cudaLaunchCooperativeKernel((void *)select_multi_kernel, dim3(blocks), dim3(kMultiThreads), args, 0, s);
+}
+
 // one CTA of 1024 threads: bitonic sort (descending) of P = 1024 E values,
 // then the measures.  Thread t holds elements t E .. t E + E - 1 in registers:
 // a compare-exchange partner at distance j < E is in the same thread, at

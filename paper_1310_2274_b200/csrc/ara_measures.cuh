@@ -6,6 +6,7 @@
 namespace ara {
 
 constexpr uint32_t kSortCap = 32768;   // max K (deepest rank needed) per call
+constexpr int kMaxPlanRanks = 16;      // joint select: 3 ranks per return period (n_rp <= 4) + L(1), L(N)
 
 struct SelectState {
     uint64_t k_rem;            // rank still to find within the current prefix
@@ -26,6 +27,9 @@ struct MeasuresScratch {
     SelectState *states = nullptr;       // [kMaxRanks]
     double *part_sum = nullptr;          // [kRedBlocks]
     unsigned long long *part_cnt = nullptr;
+    // joint select (launch_measures_multi)
+    unsigned int *mhist = nullptr;       // [4][kMaxPlanRanks][256]
+    unsigned long long *macc = nullptr;  // [8]: fixed-point tail sums, counts
 };
 
 constexpr int kMaxRanks = 3 * 64;
@@ -38,6 +42,11 @@ constexpr int kRedBlocks = 592;
 cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
                             int32_t layer, const RpList &rps, uint32_t n_rp, uint64_t k_need,
                             MeasuresScratch &S, double *d_out, cudaStream_t s);
+
+// every needed rank in one cooperative launch (n_rp <= 4), any depth
+cudaError_t launch_measures_multi(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
+                                  int32_t layer, const double *rps, uint32_t n_rp, MeasuresScratch &S,
+                                  double *d_out, cudaStream_t s);
 
 cudaError_t launch_measures_deep(const float *ylt, uint32_t n_layers, uint64_t n_total,
                                  uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,

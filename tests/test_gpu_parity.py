@@ -393,6 +393,26 @@ def test_measures_every_sort_size(A, ctx, rp_min):
         assert tvar[q] == pytest.approx(OM.tvar_rp(x.astype(np.float64), rp)[1], rel=1e-10)
 
 
+@pytest.mark.parametrize("rps", [[2, 3, 10, 100, 250, 500], [33, 66, 133, 266, 533]])
+def test_measures_many_return_periods(A, ctx, rps):
+    # more than 4 return periods: the tail-sort path (k <= 32768) or the deep
+    # per-rank selects (RP 2 at 800k trials); 1-4: the joint select -- all equal
+    import torch
+    n = 800000
+    rng = np.random.default_rng(len(rps))
+    x = rng.lognormal(15, 1.2, n).astype(np.float32)
+    x[rng.uniform(size=n) < 0.1] = 0.0
+    x[rng.uniform(size=n) < 0.002] = np.float32(3.0e8)
+    d = torch.from_numpy(x).cuda()
+    pml, tvar, var = A.risk_measures_var(ctx, d, 1, n, 0, rps=rps)
+    for q, rp in enumerate(rps):
+        assert pml[q] == pytest.approx(OM.pml(x.astype(np.float64), rp), rel=1e-12, abs=1e-9)
+        vo, to = OM.tvar_rp(x.astype(np.float64), rp)
+        assert tvar[q] == pytest.approx(to, rel=1e-10) and var[q] == vo
+        p1, t1, v1 = A.risk_measures_var(ctx, d, 1, n, 0, rps=[rp])       # joint select
+        assert p1[0] == pml[q] and v1[0] == var[q] and t1[0] == pytest.approx(tvar[q], rel=1e-12)
+
+
 def test_measures_rollup_and_shards(A, ctx):
     import torch
     rng = np.random.default_rng(5)

@@ -1,9 +1,9 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
-python tools/meas_timing.py
-ARA_MEASURES_SORT=1 python tools/meas_timing.py
-timeout 600 python bench.py --no-cpu-baseline --e2e-steps 1 > gpurun_out/b3.json 2>/dev/null
-timeout 600 python bench.py --config cfg2 --no-cpu-baseline --e2e-steps 1 > gpurun_out/b2.json 2>/dev/null
+for i in 1 2; do
+timeout 600 python bench.py --no-cpu-baseline --steps 3 --e2e-steps 5 > gpurun_out/bp$i.json 2>/dev/null
+timeout 600 python bench.py --no-cpu-baseline --steps 3 --e2e-steps 5 --plain-upload > gpurun_out/bu$i.json 2>/dev/null
+done
 python -c "
 import json
-for f in ('gpurun_out/b3.json','gpurun_out/b2.json'):
-    d=json.load(open(f)); print(f, d['ms_per_step'], d['roofline']['path_hbm']['run_ms'], d['value'])"
+for f in ('bp1','bu1','bp2','bu2'):
+    d=json.load(open('gpurun_out/%s.json'%f)); print(f, d['e2e']['value'], d['e2e']['h2d_bytes_per_step'])"
+nproc; lscpu | grep -i "numa node" | head -4

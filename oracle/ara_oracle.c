@@ -77,6 +77,28 @@ double orc_z_event(uint64_t seed, uint64_t i, uint32_t k, uint32_t j) {
     return orc_u01(o[0]);
 }
 
+/* Paper-literal alternatives to reading G2:
+ * (A) z_(E) stored with each XELT record, so constant
+ *     across trials and occurrences: counter (r, j, 0, 6), r = the record's
+ *     index within XELT j;
+ * (B) z_(E) per event occurrence, shared by every XELT ("Event-
+ *     Occurrence-Specific"): counter (i, k, 0, 7). */
+double orc_z_event_record(uint64_t seed, uint32_t j, uint32_t r) {
+    uint32_t ctr[4] = {r, j, 0u, 6u};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t o[4];
+    orc_philox4x32_10(ctr, key, o);
+    return orc_u01(o[0]);
+}
+
+double orc_z_event_occ(uint64_t seed, uint64_t i, uint32_t k) {
+    uint32_t ctr[4] = {(uint32_t)i, k, 0u, 7u};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t o[4];
+    orc_philox4x32_10(ctr, key, o);
+    return orc_u01(o[0]);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Statistical functions (section 4.2).                            */
 /* ------------------------------------------------------------------------ */
@@ -338,6 +360,7 @@ typedef struct {
     const uint32_t *events;
     uint64_t seed;
     int su;
+    int rng_mode;                 /* 0: reading G2; 1: (A) z_(E) per record; 2: (B) per occurrence */
     /* dense direct-access table [n_elts][catalog_size] -> record id or -1 */
     int32_t *table;
     /* outputs [n_layers][n_trials] */
@@ -376,7 +399,9 @@ static void *orc_worker(void *arg) {
                     double l_e;
                     if (J->su) {                                             /* line 7 */
                         double zp = orc_z_prog(J->seed, prog, i, k);
-                        double ze = orc_z_event(J->seed, i, k, j);
+                        double ze = J->rng_mode == 1 ? orc_z_event_record(J->seed, j, rloc)
+                                  : J->rng_mode == 2 ? orc_z_event_occ(J->seed, i, k)
+                                  : orc_z_event(J->seed, i, k, j);               /* G2 / (A) / (B) */
                         if (orc_sample_loss(J->rec_mean[r], J->rec_si[r], J->rec_sc[r],
                                             J->rec_max[r], zp, ze, &l_e) != 0)
                             J->status = -1;
@@ -415,7 +440,7 @@ int orc_run(uint32_t catalog_size, uint32_t n_elts, const uint64_t *elt_off,
             const uint32_t *layer_elts, const double *layer_terms, uint64_t n_trials,
             const uint64_t *trial_index, const uint64_t *trial_off, const uint32_t *events,
             uint64_t seed, int su, int n_threads, double *ylt, double *gross,
-            uint32_t *count, uint64_t *hash, double *occ_max) {
+            uint32_t *count, uint64_t *hash, double *occ_max, int rng_mode) {
     size_t slots = (size_t)n_elts * catalog_size;
     int32_t *table = (int32_t *)malloc((slots ? slots : 1) * sizeof(int32_t));
     if (!table) return -3;
@@ -441,7 +466,7 @@ int orc_run(uint32_t catalog_size, uint32_t n_elts, const uint64_t *elt_off,
         J->n_layers = n_layers; J->layer_prog = layer_prog; J->layer_elt_off = layer_elt_off;
         J->layer_elts = layer_elts; J->layer_terms = layer_terms; J->n_trials = n_trials;
         J->trial_index = trial_index; J->trial_off = trial_off; J->events = events;
-        J->seed = seed; J->su = su; J->table = table;
+        J->seed = seed; J->su = su; J->table = table; J->rng_mode = rng_mode;
         J->ylt = ylt; J->gross = gross; J->count = count; J->hash = hash; J->occ_max = occ_max;
         J->t_begin = n_trials * (uint64_t)w / (uint64_t)n_threads;
         J->t_end = n_trials * (uint64_t)(w + 1) / (uint64_t)n_threads;

@@ -17,7 +17,7 @@ _SRC = os.path.join(_HERE, "ara_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 __all__ = [
-    "build_oracle", "lib", "philox4x32_10", "u01", "z_prog", "z_event",
+    "build_oracle", "lib", "philox4x32_10", "u01", "z_prog", "z_event", "z_event_record", "z_event_occ",
     "norm_cdf", "norm_quantile", "lnbeta", "beta_cdf", "beta_quantile",
     "beta_params", "combine", "sample_loss", "sample_batch", "occ_terms", "agg_terms",
     "xelt_terms", "lookup_hash", "run", "OracleError",
@@ -69,8 +69,10 @@ def lib():
         vp = C.c_void_p
         L.orc_run.argtypes = [u32, u32, vp, vp, vp, vp, vp, vp, vp,
                               u32, vp, vp, vp, vp, u64, vp, vp, vp,
-                              u64, i32, i32, vp, vp, vp, vp, vp]
+                              u64, i32, i32, vp, vp, vp, vp, vp, i32]
         L.orc_run.restype = i32
+        L.orc_z_event_record.argtypes = [u64, u32, u32]; L.orc_z_event_record.restype = d
+        L.orc_z_event_occ.argtypes = [u64, u64, u32]; L.orc_z_event_occ.restype = d
         _lib = L
     return _lib
 
@@ -94,6 +96,14 @@ def z_prog(seed, p, i, k):
 
 def z_event(seed, i, k, j):
     return lib().orc_z_event(seed, i, k, j)
+
+
+def z_event_record(seed, j, r):
+    return lib().orc_z_event_record(seed, j, r)
+
+
+def z_event_occ(seed, i, k):
+    return lib().orc_z_event_occ(seed, i, k)
 
 
 def norm_cdf(v):
@@ -174,10 +184,12 @@ def _ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-def run(portfolio, yet, seed, su=True, n_threads=None, trial_index=None):
+def run(portfolio, yet, seed, su=True, n_threads=None, trial_index=None, rng_mode=0):
     """Algorithm 1 over every layer; returns dict(ylt, gross, count, hash,
     occ_max) -- occ_max = per (layer, trial) largest occurrence loss net of
     the occurrence terms (line 11), the basis of the OEP (reading G29).
+    ``rng_mode``: 0 = reading G2 (z_E per trial, occurrence, XELT); 1 = (A)
+    z_E stored per XELT record; 2 = (B) z_E per occurrence shared by XELTs.
 
     ``portfolio``: dict with catalog_size, elt_off[n_elts+1], rec_event,
     rec_mean, rec_sigma_i, rec_sigma_c, rec_max (any float dtype; converted
@@ -218,7 +230,7 @@ def run(portfolio, yet, seed, su=True, n_threads=None, trial_index=None):
                        n_layers, _ptr(lprog), _ptr(loff), _ptr(lelts), _ptr(lterms),
                        n, _ptr(tidx), _ptr(toff), _ptr(ev),
                        int(seed) & 0xFFFFFFFFFFFFFFFF, 1 if su else 0, int(n_threads),
-                       _ptr(ylt), _ptr(gross), _ptr(count), _ptr(hsh), _ptr(occ_max))
+                       _ptr(ylt), _ptr(gross), _ptr(count), _ptr(hsh), _ptr(occ_max), int(rng_mode))
     if st == -1:
         raise OracleError("a beta quantile did not converge")
     if st == -2:

@@ -50,7 +50,7 @@ def loss_py(mu, si, sc, mx, zp, ze):
     return mx * sp.betaincinv(a, b, z) if z <= 0.5 else mx * (1 - sp.betaincinv(b, a, q))
 
 
-def brute_force(pf, yet, seed, su, trial_index):
+def brute_force(pf, yet, seed, su, trial_index, rng_mode=0):
     """Straight-line Algorithm 1: linear search over each XELT's record list."""
     key = (seed & M32, (seed >> 32) & M32)
     nl = len(pf["layer_prog"])
@@ -77,7 +77,12 @@ def brute_force(pf, yet, seed, su, trial_index):
                                       ("rec_mean", "rec_sigma_i", "rec_sigma_c", "rec_max"))
                     if su:
                         zp = u_py(philox_py((i & M32, k, p, 1), key)[0])
-                        ze = u_py(philox_py((i & M32, k, j, 2), key)[0])
+                        if rng_mode == 1:        # (A) z_E stored per XELT record
+                            ze = u_py(philox_py((r - lo, j, 0, 6), key)[0])
+                        elif rng_mode == 2:      # (B) z_E per occurrence, shared by XELTs
+                            ze = u_py(philox_py((i & M32, k, 0, 7), key)[0])
+                        else:
+                            ze = u_py(philox_py((i & M32, k, j, 2), key)[0])
                         x = loss_py(mu, si, sc, mx, zp, ze)
                     else:
                         x = mu
@@ -300,3 +305,54 @@ def test_occ_max_sigma0_is_max_of_means():
         evs = yet["events"][int(yet["trial_off"][t]):int(yet["trial_off"][t + 1])]
         want = max([mean_of.get(int(e), 0.0) for e in evs], default=0.0)
         assert got["occ_max"][0, t] == want
+
+
+# ---- paper-literal RNG alternatives of reading G2 (NEXT-4) ------------------
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("seed", range(20))
+def test_engine_rng_modes_vs_brute_force(mode, seed):
+    rng = np.random.default_rng(5000 + 100 * mode + seed)
+    pf, yet = tiny_case(rng, xelt_terms=(seed % 3 == 0))
+    tidx = rng.integers(0, 2 ** 32, len(yet["trial_off"]) - 1, dtype=np.uint64)
+    rseed = int(rng.integers(0, 2 ** 63))
+    got = O.run(pf, yet, seed=rseed, su=True, n_threads=2, trial_index=tidx, rng_mode=mode)
+    ylt, gross = brute_force(pf, yet, rseed, True, tidx, rng_mode=mode)
+    np.testing.assert_allclose(got["gross"], gross, rtol=1e-9, atol=1e-6)
+
+
+def _one_record_case(n_elts, n_trials=40):
+    # every XELT holds the same single record on event 3 (sigma_I = 0, so
+    # v = v_E); identity terms; each trial is one occurrence of event 3
+    pf = {"catalog_size": 10, "elt_off": np.arange(n_elts + 1, dtype=np.uint64),
+          "rec_event": np.full(n_elts, 3, np.uint32), "rec_mean": np.full(n_elts, 1000.0),
+          "rec_sigma_i": np.zeros(n_elts), "rec_sigma_c": np.full(n_elts, 300.0),
+          "rec_max": np.full(n_elts, 5000.0), "elt_terms": None,
+          "layer_prog": np.zeros(1, np.uint32), "layer_elt_off": np.array([0, n_elts], np.uint64),
+          "layer_elts": np.arange(n_elts, dtype=np.uint32),
+          "layer_terms": np.array([[0.0, np.inf, 0.0, np.inf]])}
+    yet = {"trial_off": np.arange(n_trials + 1, dtype=np.uint64), "events": np.full(n_trials, 3, np.uint32)}
+    return pf, yet
+
+
+def test_rng_mode_record_constant_across_trials():
+    # (A): the record's z_E is a property of the record -> with sigma_I = 0 its
+    # loss is the same in every trial; under G2 it varies
+    pf, yet = _one_record_case(1)
+    a = O.run(pf, yet, seed=11, rng_mode=1)["ylt"][0]
+    g = O.run(pf, yet, seed=11, rng_mode=0)["ylt"][0]
+    assert np.all(a == a[0]) and np.unique(g).size == g.size
+    assert a[0] == O.sample_loss(1000.0, 0.0, 300.0, 5000.0, 0.5, O.z_event_record(11, 0, 0))
+
+
+def test_rng_mode_occurrence_shared_by_xelts():
+    # (B): one z_E per occurrence for every XELT -> identical records in two
+    # XELTs give equal losses, so the two-XELT trial loss is exactly twice the
+    # one-XELT loss; under G2 the two draws differ
+    pf2, yet = _one_record_case(2)
+    pf1, _ = _one_record_case(1)
+    two = O.run(pf2, yet, seed=12, rng_mode=2)["ylt"][0]
+    one = O.run(pf1, yet, seed=12, rng_mode=2)["ylt"][0]
+    assert np.array_equal(two, 2.0 * one)
+    two0 = O.run(pf2, yet, seed=12, rng_mode=0)["ylt"][0]
+    one0 = O.run(pf1, yet, seed=12, rng_mode=0)["ylt"][0]
+    assert not np.array_equal(two0, 2.0 * one0)

@@ -58,6 +58,17 @@ extern "C" {
                                 4-byte packed ones fit (same results; for tests
                                 and comparison)                            */
 
+#define ARA_RNG_RECORD 32u   /* paper-literal z_(E) (reading G2 alternative A,
+                                P:71/P:76/P:90): one draw stored per XELT
+                                record, constant across trials; Philox
+                                counter (record index within its XELT, XELT
+                                id, 0, 6)                                   */
+#define ARA_RNG_OCCURRENCE 64u /* z_(E) per event occurrence shared by every
+                                XELT (G2 alternative B); counter
+                                (trial, occurrence, 0, 7).  Default (neither
+                                flag): reading G2, counter (trial,
+                                occurrence, XELT id, 2)                     */
+
 /* ---- limits (validated) ------------------------------------------------ */
 #define ARA_MAX_SLOTS 224    /* sum over layers of XELTs per layer          */
 #define ARA_MAX_LAYERS 64

@@ -246,10 +246,15 @@ class Yet:
             pass
 
 
+RNG_FLAGS = {"g2": 0, "record": 32, "occurrence": 64}   # ARA_RNG_RECORD / ARA_RNG_OCCURRENCE
+
+
 def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug: bool = False,
         ylt=None, exact: bool = False, fused: bool = False,
-        wide_pairs: bool = False):
-    """ara_run; returns the device YLT [n_layers, n_trials] (and count/hash if debug)."""
+        wide_pairs: bool = False, rng: str = "g2"):
+    """ara_run; returns the device YLT [n_layers, n_trials] (and count/hash if debug).
+    rng: "g2" (z_E per trial, occurrence, XELT), "record" (paper-literal z_E per
+    XELT record), "occurrence" (z_E per occurrence shared by the XELTs)."""
     import torch
     dev = torch.device("cuda", ctx.device)
     if ylt is None:
@@ -260,14 +265,14 @@ def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug
         hsh = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int64, device=dev)
     flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (EXACT if exact else 0) | \
         (FUSED if fused else 0) | \
-        (WIDE_PAIRS if wide_pairs else 0)
+        (WIDE_PAIRS if wide_pairs else 0) | RNG_FLAGS[rng]
     _check(lib.ara_run(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(cnt),
                        _p(hsh)))
     return (ylt, cnt, hsh) if debug else ylt
 
 
 def run_ep(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug: bool = False,
-           ylt=None, occ_max=None, exact: bool = False, wide_pairs: bool = False):
+           ylt=None, occ_max=None, exact: bool = False, wide_pairs: bool = False, rng: str = "g2"):
     """ara_run_ep; returns (ylt, occ_max) device [n_layers, n_trials] (+ count/hash if debug).
     occ_max = the largest occurrence loss net of occurrence terms per (layer, trial): the OEP basis."""
     import torch
@@ -282,7 +287,7 @@ def run_ep(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, de
         cnt = torch.zeros(shape, dtype=torch.int32, device=dev)
         hsh = torch.zeros(shape, dtype=torch.int64, device=dev)
     flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (EXACT if exact else 0) | \
-        (WIDE_PAIRS if wide_pairs else 0)
+        (WIDE_PAIRS if wide_pairs else 0) | RNG_FLAGS[rng]
     _check(lib.ara_run_ep(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(occ_max),
                           _p(cnt), _p(hsh)))
     return (ylt, occ_max, cnt, hsh) if debug else (ylt, occ_max)

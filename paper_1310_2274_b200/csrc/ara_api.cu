@@ -553,8 +553,11 @@ int ara_run_ep(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t se
 static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
                     float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash) {
     if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
-    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_FUSED | ARA_WIDE_PAIRS))
+    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_FUSED | ARA_WIDE_PAIRS | ARA_RNG_RECORD |
+                  ARA_RNG_OCCURRENCE))
         return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
+    if ((flags & ARA_RNG_RECORD) && (flags & ARA_RNG_OCCURRENCE))
+        return fail(ARA_EINVAL, "ARA_RNG_RECORD and ARA_RNG_OCCURRENCE are exclusive");
     if (y->dev.n_trials == 0) return ARA_OK;
     if (!ylt) return fail(ARA_EINVAL, "ylt is NULL");
     if ((dbg_count || dbg_hash) && !(flags & ARA_DEBUG_LOOKUP))
@@ -564,7 +567,9 @@ static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64
     CU(cudaSetDevice(c->device));
     const bool exact = (flags & ARA_EXACT) != 0 && (flags & ARA_SU) != 0;
     CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
-    if (!exact && p->dev.n_layers <= kSplitMaxLayers) {
+    // ARA_RNG_RECORD with occ_max (a rare combination) runs on the fp64-capable kernel
+    const bool za_om = (flags & ARA_RNG_RECORD) && (flags & ARA_SU) && occ_max;
+    if (!exact && !za_om && p->dev.n_layers <= kSplitMaxLayers) {
         // split path: per-trial pair regions sized 2x the expected pairs per trial
         // (+128) for uniformly drawn event ids; a trial that overflows its
         // region goes to the fused kernel
@@ -574,7 +579,8 @@ static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64
         if (cap > (1u << 20)) cap = 1u << 20;
         // two kernels (compaction, then sampling); ARA_FUSED asks for the
         // warp-specialised single kernel (if the portfolio fits its shared memory)
-        const uint64_t ring = (flags & ARA_FUSED) ? fused_ring_pairs(p->dev, cap, c->num_sms) : 0;
+        const uint64_t ring = ((flags & ARA_FUSED) && !(flags & ARA_RNG_RECORD))   // (two kernels for (A))
+                                  ? fused_ring_pairs(p->dev, cap, c->num_sms) : 0;
         const bool fused = ring != 0;
         const uint64_t need = fused ? ring : y->dev.n_trials * (uint64_t)cap;
         if (c->pairs_capacity < need) {          // scratch grows once, then is reused
@@ -594,6 +600,9 @@ static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64
         SplitArgs S{p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status,
                     c->d_pairs, cap, c->d_counts, y->d_redo, {}};
         S.occ_max = occ_max;
+        S.rng_mode = (flags & ARA_RNG_RECORD) ? 1u : (flags & ARA_RNG_OCCURRENCE) ? 2u : 0u;
+        S.ze_mask = S.rng_mode == 2 ? 0u : 0xffffffffu;
+        S.ze_tag = S.rng_mode == 2 ? 7u : 2u;
         // 4-byte pairs (record << kbits | k) when both fit: halves the pair traffic
         if (!fused && !(flags & ARA_WIDE_PAIRS)) {
             uint32_t kb = 1;

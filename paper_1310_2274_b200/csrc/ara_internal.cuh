@@ -128,6 +128,8 @@ struct SplitArgs {
     uint32_t xcap;            // sample_kernel: pairs per segment (set by launch_sample)
     uint32_t kbits;           // > 0: pairs packed in 4 B as device record << kbits | k (two-kernel path)
     float *occ_max;           // null, or [n_layers][n_trials] largest occurrence loss (G29)
+    uint32_t rng_mode;        // 0: reading G2; 1: ARA_RNG_RECORD; 2: ARA_RNG_OCCURRENCE
+    uint32_t ze_mask, ze_tag; // z_(E) counter (trial, k, elt & ze_mask, ze_tag) in modes 0 and 2
 };
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);

@@ -222,7 +222,16 @@ struct SampleArgs {
     RunStatus *status;
     uint64_t seed;
     bool exact;
+    uint32_t rng;                   // 0: reading G2; 1: ARA_RNG_RECORD; 2: ARA_RNG_OCCURRENCE
 };
+
+// z_(E) of device record `rec` (XELT si.elt) at occurrence k of trial i (G2 and its alternatives)
+__device__ __forceinline__ uint32_t draw_ze(const SampleArgs &G, const SlotInfo &si, uint32_t rec,
+                                            uint32_t trial_g, uint32_t k) {
+    if (G.rng == 1) return philox_lane0(__ldg(G.rec_orig + rec), si.elt, 0u, 6u, G.seed);
+    if (G.rng == 2) return philox_lane0(trial_g, k, 0u, 7u, G.seed);
+    return philox_lane0(trial_g, k, si.elt, 2u, G.seed);
+}
 
 // one loss draw for queue entry e (Alg.1 lines 7-8); r already loaded
 template <bool EX>
@@ -237,7 +246,7 @@ __device__ __forceinline__ float draw_one(const SampleArgs &G, const SlotInfo &s
     } else {
         const uint32_t k = e.y >> 8;
         const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, G.seed);   // z_(Prog,E)
-        const uint32_t be = philox_lane0(trial_g, k, si.elt, 2u, G.seed);    // z_(E)
+        const uint32_t be = draw_ze(G, si, e.x, trial_g, k);                  // z_(E)
         const float v = combine_v(r, norm_quantile_from_bits(bp), norm_quantile_from_bits(be));
         bool ok;
         x = sample_loss_from_v<EX>(r, G.tables, G.hot, e.x, v, G.exact, ok);
@@ -278,7 +287,7 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
                 const SlotInfo &si = slots[e[u].y & 0xffu];
                 const uint32_t k = e[u].y >> 8;
                 const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, G.seed);   // z_(Prog,E)
-                const uint32_t be = philox_lane0(trial_g, k, si.elt, 2u, G.seed);    // z_(E)
+                const uint32_t be = draw_ze(G, si, e[u].x, trial_g, k);              // z_(E)
                 v[u] = combine_v(r[u], norm_quantile_from_bits(bp), norm_quantile_from_bits(be));
             }
             float2 n0[U], n1[U];
@@ -551,7 +560,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
     unsigned int *omv = wom(M);
     const bool dbg = DBG;
     const SampleArgs G{A.pf.recs, A.pf.tables, A.pf.hot, A.pf.rec_mu, A.pf.rec_orig, A.status, A.seed,
-                       (A.flags & ARA_EXACT) != 0};
+                       (A.flags & ARA_EXACT) != 0,
+                       (A.flags & ARA_RNG_RECORD) ? 1u : (A.flags & ARA_RNG_OCCURRENCE) ? 2u : 0u};
     const uint64_t n_trials = A.yet.n_trials;
     const uint64_t n_work = A.trial_list ? A.n_list : n_trials;
     const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift;

@@ -418,7 +418,7 @@ struct SampleWs {
 
 // The sampler on trial t's n present pairs at `in` (CG: read them through L2
 // only, as the fused kernel's consumers must).
-template <bool SU, bool SL, bool DBG, bool CG, bool PK = false, bool OM = false>
+template <bool SU, bool SL, bool DBG, bool CG, bool PK = false, bool OM = false, bool ZA = false>
 __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs &W, uint64_t t, uint32_t n,
                                              const uint2 *in) {
     const int lane = threadIdx.x & 31;
@@ -485,7 +485,9 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const uint32_t bp = philox_lane0_k(trial_g, e[u].y, r[u].prog, 1u, A.pkey);   // z_(Prog,E)
-                    const uint32_t be = philox_lane0_k(trial_g, e[u].y, r[u].elt, 2u, A.pkey);    // z_(E)
+                    const uint32_t be =                                                           // z_(E)
+                        ZA ? philox_lane0_k(__ldg(A.pf.rec_orig + e[u].x), r[u].elt, 0u, 6u, A.pkey)  // (A)
+                           : philox_lane0_k(trial_g, e[u].y, r[u].elt & A.ze_mask, A.ze_tag, A.pkey); // G2, (B)
                     v[u] = fmaf(r[u].wi, norm_quantile_from_bits(bp), r[u].wc * norm_quantile_from_bits(be));
                 }
 #pragma unroll
@@ -622,7 +624,9 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     }
 }
 
-template <bool SU, bool SL, bool DBG, bool PK, bool OM>
+// ZA: z_(E) stored per XELT record (ARA_RNG_RECORD); the default draw covers
+// reading G2 and ARA_RNG_OCCURRENCE through A.ze_mask / A.ze_tag
+template <bool SU, bool SL, bool DBG, bool PK, bool OM, bool ZA = false>
 __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 warps/SM: <= 64 registers
     sample_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -652,7 +656,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 wa
         if (t >= A.yet.n_trials) break;
         const uint32_t n = __ldg(A.counts + t);
         if (n == kOverflow) continue;                 // redone by the fused kernel
-        sample_trial<SU, SL, DBG, false, PK, OM>(A, W, t, n, PK ? reinterpret_cast<const uint2 *>(
+        sample_trial<SU, SL, DBG, false, PK, OM, ZA>(A, W, t, n, PK ? reinterpret_cast<const uint2 *>(
                                                                    reinterpret_cast<const uint32_t *>(A.pairs) + t * A.cap)
                                                                : A.pairs + t * (uint64_t)A.cap);
         __syncwarp();
@@ -937,7 +941,20 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
             : (dbg ? (K)sample_kernel<true, false, true, P, O> : (K)sample_kernel<true, false, false, P, O>))   \
         : (sl ? (dbg ? (K)sample_kernel<false, true, true, P, O> : (K)sample_kernel<false, true, false, P, O>)   \
               : (dbg ? (K)sample_kernel<false, false, true, P, O> : (K)sample_kernel<false, false, false, P, O>)))
-    const K kern = A.occ_max ? (A.kbits ? ARA_SK(true, true) : ARA_SK(false, true))
+    // ARA_RNG_RECORD: its own instantiations (SU on, no occ_max: ara_run sends that case to the
+    // fp64-capable kernel)
+    const K za = sl ? (dbg ? (K)sample_kernel<true, true, true, true, false, true>
+                           : (K)sample_kernel<true, true, false, true, false, true>)
+                    : (dbg ? (K)sample_kernel<true, false, true, true, false, true>
+                           : (K)sample_kernel<true, false, false, true, false, true>);
+    const K za_w = sl ? (dbg ? (K)sample_kernel<true, true, true, false, false, true>
+                             : (K)sample_kernel<true, true, false, false, false, true>)
+                      : (dbg ? (K)sample_kernel<true, false, true, false, false, true>
+                             : (K)sample_kernel<true, false, false, false, false, true>);
+    const bool use_za = A.rng_mode == 1 && su;       // (without SU no z_(E) is drawn)
+    if (use_za && A.occ_max) return cudaErrorInvalidValue;
+    const K kern = use_za ? (A.kbits ? za : za_w)
+                 : A.occ_max ? (A.kbits ? ARA_SK(true, true) : ARA_SK(false, true))
                              : (A.kbits ? ARA_SK(true, false) : ARA_SK(false, false));
 #undef ARA_SK
     int per_sm = 0;

@@ -630,3 +630,36 @@ def test_packed_refill_errors(A, ctx):
     with pytest.raises(A.AraError) as ei:
         A.run(ctx, P, Y, seed=1)
     assert ei.value.code == 2                       # ARA_ERANGE
+
+
+# ---- paper-literal RNG alternatives of reading G2 (NEXT-4) -------------------
+@pytest.mark.parametrize("rng,mode", [("record", 1), ("occurrence", 2)])
+@pytest.mark.parametrize("case", ["cfg1", "layers3", "exact", "fused"])
+def test_rng_modes_vs_oracle(A, ctx, rng, mode, case):
+    cfg = aragen.load_config("cfg1")
+    if case == "layers3":
+        cfg.update(n_layers=3, elts_per_layer=4, catalog=4000, records_per_elt=600, n_trials=300,
+                   layer_terms=[[2e5 * (l + 1), 5e6, 1.0e6, 5.0e7] for l in range(3)])
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    g, cnt, hsh = A.run(ctx, P, Y, seed=cfg["seed"], debug=True, rng=rng, exact=(case == "exact"),
+                        fused=(case == "fused"))
+    ref = oracle.run(pf, yet, seed=cfg["seed"], rng_mode=mode)
+    assert np.array_equal(cnt.cpu().numpy().astype(np.uint32), ref["count"])
+    g = g.cpu().numpy()
+    for li in range(g.shape[0]):
+        ylt_check(g[li], ref, li)
+    # a different reading gives different losses (the modes are wired through)
+    g0 = A.run(ctx, P, Y, seed=cfg["seed"]).cpu().numpy()
+    assert not np.array_equal(g0, g)
+
+
+def test_rng_modes_exclusive(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 10
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    import torch
+    ylt = torch.empty((1, 10), dtype=torch.float32, device="cuda")
+    with pytest.raises(A.AraError):
+        A._check(A.lib.ara_run(ctx.h, P.h, Y.h, 1, A.SU | 32 | 64, A._p(ylt), None, None))

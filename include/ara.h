@@ -259,6 +259,17 @@ int ara_risk_measures_var(ara_ctx *ctx, const float *ylt, uint32_t n_layers, uin
                           uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
                           double *pml_out, double *tvar_out, double *var_out);
 
+/* The exceedance curve (SPEC ExceedanceCurve S:345-352) of one
+ * layer's YLT, or of the roll-up over layers (layer = -1, G16): the losses
+ * sorted descending, L(1) >= ... >= L(N); the empirical exceedance
+ * probability of rank i is i/(N+1) (implicit).  A device radix sort.
+ *   ylt         DEVICE fp32 [n_shards][n_layers][n_total/n_shards] (as ara_risk_measures)
+ *   losses_out  DEVICE fp32 [n_total], caller-allocated
+ * Asynchronous on the context stream.  ARA_EINVAL: empty YLT, n_total >= 2^32,
+ * bad layer / shard layout, host pointers. */
+int ara_exceedance_curve(ara_ctx *ctx, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                         uint32_t n_shards, int32_t layer, float *losses_out);
+
 /* ---- component entry points (row-level parity tests) ------------------ */
 
 /* Secondary-uncertainty loss draws for n independent

@@ -36,7 +36,7 @@ EXPORTS = (
     "ara_last_error", "ara_version", "ara_ctx_create", "ara_ctx_destroy", "ara_ctx_synchronize",
     "ara_validate_portfolio", "ara_create_portfolio", "ara_portfolio_destroy", "ara_portfolio_info",
     "ara_load_yet",
-    "ara_yet_refill", "ara_yet_refill_packed", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings", "ara_risk_measures_var",
+    "ara_yet_refill", "ara_yet_refill_packed", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings", "ara_risk_measures_var", "ara_exceedance_curve",
     "ara_risk_measures",
     "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles",
 )
@@ -73,6 +73,7 @@ def _load():
     L.ara_run_ep.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp, vp]
     L.ara_risk_measures.argtypes = [vp, vp, u32, u64, u32, i32, vp, u32, vp, vp]
     L.ara_risk_measures_var.argtypes = [vp, vp, u32, u64, u32, i32, vp, u32, vp, vp, vp]
+    L.ara_exceedance_curve.argtypes = [vp, vp, u32, u64, u32, i32, vp]
     L.ara_last_run_timings.argtypes = [vp, vp, vp, vp]
     L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, u32, vp]
     L.ara_draw_uniforms.argtypes = [vp, u64, u64, vp, vp]
@@ -318,6 +319,18 @@ def risk_measures_var(ctx: Context, ylt, n_layers: int, n_total: int, layer: int
     _check(lib.ara_risk_measures_var(ctx.h, _p(ylt), int(n_layers), int(n_total), int(n_shards),
                                      int(layer), _p(r), len(r), _p(pml), _p(tvar), _p(var)))
     return pml, tvar, var
+
+
+def exceedance_curve(ctx: Context, ylt, n_layers: int, n_total: int, layer: int = 0, n_shards: int = 1,
+                     out=None):
+    """ara_exceedance_curve: device fp32 [n_total], the losses sorted descending
+    (rank i has exceedance probability i/(N+1))."""
+    import torch
+    if out is None:
+        out = torch.empty(int(n_total), dtype=torch.float32, device=ylt.device)
+    _check(lib.ara_exceedance_curve(ctx.h, _p(ylt), int(n_layers), int(n_total), int(n_shards), int(layer),
+                                    _p(out)))
+    return out
 
 
 def sample_losses(ctx: Context, records, z_prog, z_event, exact: bool = False):

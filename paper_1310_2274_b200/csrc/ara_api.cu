@@ -63,6 +63,8 @@ struct ara_ctx {
     RunStatus *d_status = nullptr;
     RunStatus *h_status = nullptr;     // pinned
     double *h_out = nullptr;           // pinned [192]: measures results (pml, tvar, var) per RP
+    uint32_t *d_ep = nullptr;          // exceedance-curve sort scratch
+    uint64_t ep_capacity = 0;
     MeasuresScratch ms;
     uint2 *d_pairs = nullptr;          // split path scratch: per-trial pairs {device record, k}
     uint64_t pairs_capacity = 0;       // elements of d_pairs
@@ -149,6 +151,7 @@ void ara_ctx_destroy(ara_ctx *c) {
     cudaFree(c->d_status);
     cudaFreeHost(c->h_status);
     cudaFreeHost(c->h_out);
+    cudaFree(c->d_ep);
     cudaFree(c->ms.vals);
     cudaFree(c->ms.buf);
     cudaFree(c->ms.hist);
@@ -686,6 +689,29 @@ static uint64_t needed_rank(uint64_t N, double rp) {
     if (k < 1) k = 1;
     if (k > N) k = N;
     return k;
+}
+
+int ara_exceedance_curve(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
+                         int32_t layer, float *losses_out) {
+    if (!c || !ylt || !losses_out) return fail(ARA_EINVAL, "NULL argument");
+    if (n_total == 0) return fail(ARA_EINVAL, "empty YLT");
+    if (n_total > 0xffffffffull) return fail(ARA_EINVAL, "n_total must be < 2^32");
+    if (n_layers == 0 || n_shards == 0 || n_total % n_shards)
+        return fail(ARA_EINVAL, "need n_layers >= 1, n_shards >= 1 dividing n_total");
+    if (layer < -1 || layer >= (int32_t)n_layers) return fail(ARA_EINVAL, "layer %d out of range", layer);
+    if (!is_device_ptr(ylt) || !is_device_ptr(losses_out)) return fail(ARA_EINVAL, "ylt and losses_out must be device memory");
+    CU(cudaSetDevice(c->device));
+    const uint64_t need = 2 * n_total + 256ull * (2 * (uint64_t)c->num_sms);
+    if (c->ep_capacity < need) {                       // scratch grows once, then is reused
+        cudaFree(c->d_ep);
+        c->d_ep = nullptr;
+        c->ep_capacity = 0;
+        CU(dalloc(&c->d_ep, need));
+        c->ep_capacity = need;
+    }
+    CU(launch_exceedance_curve(ylt, n_layers, n_total, n_shards, layer, c->d_ep, losses_out, c->stream,
+                               c->num_sms));
+    return ARA_OK;
 }
 
 int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,

@@ -6,6 +6,7 @@
 // CTA; ties at T are counted, never materialised.  PML interpolates the
 // descending order statistics at r = (N+1)/RP; TVaR is the mean of all
 // losses >= VaR = L(ceil(N/RP)).
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -683,6 +684,123 @@ cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_tota
         attr_set = true;
     }
     kern<<<1, 1024, smem, s>>>(S.buf, S.state, rps, n_rp, n_total, d_out);
+    return cudaGetLastError();
+}
+
+}  // namespace ara
+
+// ---------------------------------------------------------------------------
+// Exceedance curve (SPEC's ExceedanceCurve): the
+// YLT (one layer or the roll-up) sorted descending, L(1) >= ... >= L(N), whose
+// empirical exceedance probability at rank i is i/(N+1).  A stable LSD radix
+// sort of 32-bit keys ~okey(v) (ascending keys = descending losses), four
+// 8-bit passes; each pass: per-tile digit counts -> one exclusive scan in
+// digit-major order -> a stable scatter (tiles in order; inside a tile,
+// chunks of 1024 in order, warps in order, lanes in order via match.any).
+// ---------------------------------------------------------------------------
+namespace ara {
+
+constexpr int kEpThreads = 1024;
+
+__global__ void ep_keys_kernel(const float *ylt, uint32_t n_layers, uint64_t per, uint32_t n_shards, int32_t layer,
+                               uint32_t *keys) {
+    const uint64_t n = per * n_shards;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t sh = t / per, i = t - sh * per;
+        const float *base = ylt + sh * (uint64_t)n_layers * per + i;
+        float v;
+        if (layer >= 0) {
+            v = base[(uint64_t)layer * per];
+        } else {
+            v = 0.0f;
+            for (uint32_t l = 0; l < n_layers; ++l) v += base[(uint64_t)l * per];
+        }
+        keys[t] = ~okey(v);
+    }
+}
+
+__global__ void __launch_bounds__(kEpThreads) ep_count_kernel(const uint32_t *keys, uint64_t n, uint64_t tile,
+                                                              int shift, uint32_t *counts) {
+    __shared__ unsigned int h[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const uint64_t b0 = blockIdx.x * tile, b1 = min(n, b0 + tile);
+    for (uint64_t t = b0 + threadIdx.x; t < b1; t += blockDim.x) atomicAdd(&h[(keys[t] >> shift) & 0xffu], 1u);
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) counts[(uint64_t)d * gridDim.x + blockIdx.x] = h[d];
+}
+
+// exclusive scan of counts[256 * nb] in place (digit-major), one block
+__global__ void __launch_bounds__(kEpThreads) ep_scan_kernel(uint32_t *counts, uint32_t total) {
+    __shared__ uint32_t part[kEpThreads];
+    const uint32_t per = (total + blockDim.x - 1) / blockDim.x;
+    const uint32_t a = threadIdx.x * per, b = min(total, a + per);
+    uint32_t s = 0;
+    for (uint32_t i = a; i < b; ++i) s += counts[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (uint32_t o = 1; o < blockDim.x; o <<= 1) {        // inclusive scan of the parts
+        const uint32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+    for (uint32_t i = a; i < b; ++i) { const uint32_t c = counts[i]; counts[i] = run; run += c; }
+}
+
+__global__ void __launch_bounds__(kEpThreads) ep_scatter_kernel(const uint32_t *in, uint32_t *out, uint64_t n,
+                                                                uint64_t tile, int shift, const uint32_t *offs) {
+    __shared__ uint32_t base[256];                // next output slot of each digit for this tile
+    __shared__ uint32_t wc[kEpThreads / 32][256];  // per-warp digit counts -> exclusive prefixes
+    __shared__ uint32_t tot[256];                 // the chunk's digit totals
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) base[d] = offs[(uint64_t)d * gridDim.x + blockIdx.x];
+    const uint64_t b0 = blockIdx.x * tile, b1 = min(n, b0 + tile);
+    for (uint64_t c = b0; c < b1; c += blockDim.x) {
+        for (int i = threadIdx.x; i < (kEpThreads / 32) * 256; i += blockDim.x) (&wc[0][0])[i] = 0u;
+        __syncthreads();
+        const uint64_t t = c + threadIdx.x;
+        const bool live = t < b1;
+        const uint32_t k = live ? in[t] : 0u;
+        const uint32_t d = live ? (k >> shift) & 0xffu : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));        // earlier lanes, same digit
+        if (live && rank == 0) wc[warp][d] = __popc(peers);
+        __syncthreads();
+        if (threadIdx.x < 256) {                  // digit: exclusive prefix over the warps, in order
+            uint32_t sum = 0;
+            for (int w = 0; w < kEpThreads / 32; ++w) { const uint32_t v = wc[w][threadIdx.x]; wc[w][threadIdx.x] = sum; sum += v; }
+            tot[threadIdx.x] = sum;
+        }
+        __syncthreads();
+        if (live) out[base[d] + wc[warp][d] + rank] = k;
+        __syncthreads();
+        if (threadIdx.x < 256) base[threadIdx.x] += tot[threadIdx.x];
+    }
+}
+
+__global__ void ep_values_kernel(const uint32_t *keys, uint64_t n, float *out) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
+        out[t] = okey_inv(~keys[t]);
+}
+
+cudaError_t launch_exceedance_curve(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
+                                    int32_t layer, uint32_t *scratch /*[2 n + 256 nb]*/, float *out,
+                                    cudaStream_t s, int num_sms) {
+    const uint64_t per = n_total / n_shards, n = n_total;
+    const uint32_t nb = (uint32_t)std::min<uint64_t>((uint64_t)num_sms * 2, (n + kEpThreads - 1) / kEpThreads);
+    const uint64_t tile = (n + nb - 1) / nb;
+    uint32_t *a = scratch, *b = scratch + n, *counts = scratch + 2 * n;
+    ep_keys_kernel<<<num_sms * 4, 256, 0, s>>>(ylt, n_layers, per, n_shards, layer, a);
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 8 * pass;
+        ep_count_kernel<<<nb, kEpThreads, 0, s>>>(a, n, tile, shift, counts);
+        ep_scan_kernel<<<1, kEpThreads, 0, s>>>(counts, 256u * nb);
+        ep_scatter_kernel<<<nb, kEpThreads, 0, s>>>(a, b, n, tile, shift, counts);
+        std::swap(a, b);
+    }
+    ep_values_kernel<<<num_sms * 4, 256, 0, s>>>(a, n, out);     // (4 passes: the keys are back in `scratch`)
     return cudaGetLastError();
 }
 

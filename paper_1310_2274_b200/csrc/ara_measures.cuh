@@ -48,6 +48,10 @@ cudaError_t launch_measures_multi(const float *ylt, uint32_t n_layers, uint64_t 
                                   int32_t layer, const double *rps, uint32_t n_rp, MeasuresScratch &S,
                                   double *d_out, cudaStream_t s);
 
+// the YLT (layer or roll-up) sorted descending: the exceedance curve (NEXT-3)
+cudaError_t launch_exceedance_curve(const float *ylt, uint32_t n_layers, uint64_t n_total, uint32_t n_shards,
+                                    int32_t layer, uint32_t *scratch, float *out, cudaStream_t s, int num_sms);
+
 cudaError_t launch_measures_deep(const float *ylt, uint32_t n_layers, uint64_t n_total,
                                  uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
                                  MeasuresScratch &S, double *d_out, cudaStream_t s);

@@ -663,3 +663,38 @@ def test_rng_modes_exclusive(A, ctx):
     ylt = torch.empty((1, 10), dtype=torch.float32, device="cuda")
     with pytest.raises(A.AraError):
         A._check(A.lib.ara_run(ctx.h, P.h, Y.h, 1, A.SU | 32 | 64, A._p(ylt), None, None))
+
+
+# ---- exceedance curve (NEXT-3): the YLT sorted descending --------------------
+@pytest.mark.parametrize("n", [1, 1000, 4097, 100003, 800000])
+def test_exceedance_curve_is_the_sorted_ylt(A, ctx, n):
+    import torch
+    rng = np.random.default_rng(n)
+    x = rng.lognormal(15, 1.2, n).astype(np.float32)
+    x[rng.uniform(size=n) < 0.1] = 0.0                      # ties at 0 and at the limit
+    x[rng.uniform(size=n) < 0.01] = np.float32(3.0e8)
+    curve = A.exceedance_curve(ctx, torch.from_numpy(x).cuda(), 1, n, 0).cpu().numpy()
+    assert np.array_equal(curve, np.sort(x)[::-1])           # a permutation: bit-exact
+
+
+def test_exceedance_curve_rollup_shards_and_cfg1(A, ctx):
+    import torch
+    rng = np.random.default_rng(9)
+    L, n, P = 3, 40000, 4
+    y = rng.lognormal(12, 1, (P, L, n // P)).astype(np.float32)
+    flat = y.transpose(1, 0, 2).reshape(L, n)
+    d = torch.from_numpy(y).cuda()
+    for layer in (-1, 1):
+        v = (flat[0] + flat[1]) + flat[2] if layer < 0 else flat[layer]
+        got = A.exceedance_curve(ctx, d, L, n, layer, n_shards=P).cpu().numpy()
+        assert np.array_equal(got, np.sort(v)[::-1])
+    # on a run's YLT: the curve's order statistics are the measures' inputs
+    cfg = aragen.load_config("cfg1")
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    ylt = A.run(ctx, A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet), seed=cfg["seed"])
+    curve = A.exceedance_curve(ctx, ylt, 1, cfg["n_trials"], 0).cpu().numpy()
+    assert np.array_equal(curve, np.sort(ylt.cpu().numpy()[0])[::-1])
+    _, _, var = A.risk_measures_var(ctx, ylt, 1, cfg["n_trials"], 0, rps=(10, 50))
+    N = cfg["n_trials"]
+    for q, rp in enumerate((10, 50)):
+        assert var[q] == curve[-(-N // rp) - 1]               # VaR = L(ceil(N/RP))

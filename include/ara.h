@@ -70,8 +70,15 @@ extern "C" {
                                 occurrence, XELT id, 2)                     */
 
 /* ---- limits (validated) ------------------------------------------------ */
-#define ARA_MAX_SLOTS 224    /* sum over layers of XELTs per layer          */
-#define ARA_MAX_LAYERS 64
+#define ARA_MAX_SLOTS 224    /* XELTs per layer; also the (layer, XELT) slots
+                                of one kernel group: a larger portfolio (or
+                                one of > 8 layers) is split into groups of
+                                consecutive layers run one after the other
+                                over the YET (same results)                 */
+#define ARA_MAX_LAYERS 64    /* layers of one kernel group (internal)       */
+#define ARA_MAX_PORTFOLIO_LAYERS 4096    /* layers per portfolio            */
+#define ARA_MAX_PORTFOLIO_SLOTS 65536    /* sum over layers of XELTs per layer
+                                            ("10,000 XELTs")          */
 #define ARA_MAX_EVENTS_PER_TRIAL (1u << 24)
 
 typedef struct ara_ctx ara_ctx;
@@ -130,11 +137,12 @@ int ara_ctx_synchronize(ara_ctx *ctx);
  *                       records[elt_rec_offsets[j] .. elt_rec_offsets[j+1])
  *   records             [elt_rec_offsets[n_elts]] XELT records
  *   elt_terms           [n_elts] or NULL (identity, G7)
- *   n_layers            layers in the portfolio, <= ARA_MAX_LAYERS
+ *   n_layers            layers in the portfolio, <= ARA_MAX_PORTFOLIO_LAYERS
  *   layer_program       [n_layers] program id of each layer (keys z_(Prog,E))
  *   layer_elt_offsets   [n_layers+1] ranges into layer_elts
  *   layer_elts          XELT ids covered by each layer, no duplicates within
- *                       a layer; sum of layer sizes <= ARA_MAX_SLOTS
+ *                       a layer; <= ARA_MAX_SLOTS per layer, sum of layer
+ *                       sizes <= ARA_MAX_PORTFOLIO_SLOTS
  *   layer_terms         [n_layers]
  * Errors: ARA_EINVAL (bad value / shape), ARA_ERANGE (event id >=
  * catalog_size, XELT id >= n_elts), ARA_EDUP (duplicate event in an XELT or

@@ -87,6 +87,12 @@ struct ara_portfolio {
     float *d_mu = nullptr;
     SlotInfo *d_slots = nullptr;
     LayerInfo *d_layers = nullptr;
+    // a portfolio larger than one kernel group (> kSplitMaxLayers layers or
+    // > ARA_MAX_SLOTS slots) is a list of groups of consecutive layers, each a
+    // complete portfolio of its own, run one after the other over the YET
+    std::vector<ara_portfolio *> groups;
+    std::vector<uint32_t> group_layer0;   // first layer of each group
+    uint32_t n_layers_total = 0;
 };
 
 struct ara_yet {
@@ -217,15 +223,20 @@ int ara_validate_portfolio(uint32_t C, uint32_t n_elts, const uint64_t *eoff, co
         }
     }
     if (n_layers == 0) return fail(ARA_EINVAL, "portfolio has no layers");
-    if (n_layers > ARA_MAX_LAYERS) return fail(ARA_EINVAL, "n_layers %u > %d", n_layers, ARA_MAX_LAYERS);
+    if (n_layers > ARA_MAX_PORTFOLIO_LAYERS)
+        return fail(ARA_EINVAL, "n_layers %u > %d", n_layers, ARA_MAX_PORTFOLIO_LAYERS);
     if (!lprog || !loff || !lt) return fail(ARA_EINVAL, "layer arrays are NULL");
     if (loff[0] != 0) return fail(ARA_EINVAL, "layer_elt_offsets[0] must be 0");
     const uint64_t nslots = loff[n_layers];
-    if (nslots > ARA_MAX_SLOTS)
-        return fail(ARA_EINVAL, "sum of XELTs over layers %llu > %d", (unsigned long long)nslots, ARA_MAX_SLOTS);
+    if (nslots > ARA_MAX_PORTFOLIO_SLOTS)
+        return fail(ARA_EINVAL, "sum of XELTs over layers %llu > %d", (unsigned long long)nslots,
+                    ARA_MAX_PORTFOLIO_SLOTS);
     if (nslots && !lelts) return fail(ARA_EINVAL, "layer_elts is NULL");
     for (uint32_t l = 0; l < n_layers; ++l) {
         if (loff[l + 1] <= loff[l]) return fail(ARA_EINVAL, "layer %u covers no XELT", l);
+        if (loff[l + 1] - loff[l] > ARA_MAX_SLOTS)
+            return fail(ARA_EINVAL, "layer %u covers %llu XELTs > %d", l,
+                        (unsigned long long)(loff[l + 1] - loff[l]), ARA_MAX_SLOTS);
         for (uint64_t x = loff[l]; x < loff[l + 1]; ++x) {
             if (lelts[x] >= n_elts)
                 return fail(ARA_ERANGE, "layer %u: XELT id %u >= n_elts %u", l, lelts[x], n_elts);
@@ -241,6 +252,11 @@ int ara_validate_portfolio(uint32_t C, uint32_t n_elts, const uint64_t *eoff, co
     return ARA_OK;
 }
 
+static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t *eoff,
+                        const ara_record *rec, const ara_elt_terms *et, uint32_t n_layers,
+                        const uint32_t *lprog, const uint64_t *loff, const uint32_t *lelts,
+                        const ara_layer_terms *lt, ara_portfolio **out);
+
 int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t *eoff,
                          const ara_record *rec, const ara_elt_terms *et, uint32_t n_layers,
                          const uint32_t *lprog, const uint64_t *loff, const uint32_t *lelts,
@@ -249,6 +265,35 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     *out = nullptr;
     int st = ara_validate_portfolio(C, n_elts, eoff, rec, et, n_layers, lprog, loff, lelts, lt);
     if (st != ARA_OK) return st;
+    if (n_layers <= (uint32_t)kSplitMaxLayers && loff[n_layers] <= ARA_MAX_SLOTS)
+        return create_group(c, C, n_elts, eoff, rec, et, n_layers, lprog, loff, lelts, lt, out);
+    // groups of consecutive layers: <= kSplitMaxLayers layers and <= ARA_MAX_SLOTS slots each
+    ara_portfolio *p = new ara_portfolio();
+    p->ctx = c;
+    p->n_layers_total = n_layers;
+    for (uint32_t l0 = 0; l0 < n_layers;) {
+        uint32_t l1 = l0 + 1;
+        while (l1 < n_layers && l1 - l0 < (uint32_t)kSplitMaxLayers && loff[l1 + 1] - loff[l0] <= ARA_MAX_SLOTS) ++l1;
+        std::vector<uint64_t> sub(l1 - l0 + 1);
+        for (uint32_t l = l0; l <= l1; ++l) sub[l - l0] = loff[l] - loff[l0];
+        ara_portfolio *g = nullptr;
+        st = create_group(c, C, n_elts, eoff, rec, et, l1 - l0, lprog + l0, sub.data(), lelts + loff[l0], lt + l0, &g);
+        if (st != ARA_OK) {
+            ara_portfolio_destroy(p);
+            return st;
+        }
+        p->groups.push_back(g);
+        p->group_layer0.push_back(l0);
+        l0 = l1;
+    }
+    *out = p;
+    return ARA_OK;
+}
+
+static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t *eoff,
+                        const ara_record *rec, const ara_elt_terms *et, uint32_t n_layers,
+                        const uint32_t *lprog, const uint64_t *loff, const uint32_t *lelts,
+                        const ara_layer_terms *lt, ara_portfolio **out) {
     CU(cudaSetDevice(c->device));
 
     // slots: (layer, XELT) pairs, layer-major
@@ -401,6 +446,18 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
 
 int ara_portfolio_info(const ara_portfolio *p, uint64_t *n_dev, uint64_t *n_tl, uint64_t *bytes) {
     if (!p) return fail(ARA_EINVAL, "portfolio is NULL");
+    if (!p->groups.empty()) {                          // sums over the groups
+        uint64_t a = 0, b = 0, c = 0;
+        for (const ara_portfolio *g : p->groups) {
+            uint64_t x = 0, y = 0, z = 0;
+            ara_portfolio_info(g, &x, &y, &z);
+            a += x; b += y; c += z;
+        }
+        if (n_dev) *n_dev = a;
+        if (n_tl) *n_tl = b;
+        if (bytes) *bytes = c;
+        return ARA_OK;
+    }
     const PortfolioDev &d = p->dev;
     if (n_dev) *n_dev = d.n_dev_records;
     if (n_tl) *n_tl = d.n_exact_records;
@@ -414,6 +471,7 @@ int ara_portfolio_info(const ara_portfolio *p, uint64_t *n_dev, uint64_t *n_tl, 
 
 void ara_portfolio_destroy(ara_portfolio *p) {
     if (!p) return;
+    for (ara_portfolio *g : p->groups) ara_portfolio_destroy(g);
     if (p->ctx) cudaSetDevice(p->ctx->device);
     cudaFree(p->d_index); cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig); cudaFree(p->d_recs);
     cudaFree(p->d_cidx); cudaFree(p->d_rec_meta); cudaFree(p->d_srecs); cudaFree(p->d_mm);
@@ -553,9 +611,31 @@ int ara_run_ep(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t se
     return run_impl(c, p, y, seed, flags, ylt, occ_max, dbg_count, dbg_hash);
 }
 
+static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
+                     float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash);
+
 static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
                     float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash) {
     if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
+    if (p->groups.empty()) return run_group(c, p, y, seed, flags, ylt, occ_max, dbg_count, dbg_hash);
+    // one run per group of layers over the same YET (the draws do not depend on
+    // the layer or its slot, so the YLT equals one run of the whole portfolio)
+    const uint64_t N = y->dev.n_trials;
+    double ms[3] = {0.0, 0.0, 0.0};
+    for (size_t g = 0; g < p->groups.size(); ++g) {
+        const uint64_t off = (uint64_t)p->group_layer0[g] * N;
+        const int st = run_group(c, p->groups[g], y, seed, flags, ylt ? ylt + off : nullptr,
+                                 occ_max ? occ_max + off : nullptr, dbg_count ? dbg_count + off : nullptr,
+                                 dbg_hash ? dbg_hash + off : nullptr);
+        if (st != ARA_OK) return st;
+        for (int k = 0; k < 3; ++k) ms[k] += c->last_ms[k];
+    }
+    for (int k = 0; k < 3; ++k) c->last_ms[k] = ms[k];
+    return ARA_OK;
+}
+
+static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
+                     float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash) {
     if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_FUSED | ARA_WIDE_PAIRS | ARA_RNG_RECORD |
                   ARA_RNG_OCCURRENCE))
         return fail(ARA_EINVAL, "unknown flags 0x%x", flags);

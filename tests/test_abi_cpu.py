@@ -92,7 +92,7 @@ def test_validate_rejects(ara, mutate, code, needle):
 
 def test_validate_limits(ara):
     pf = base_pf()
-    n = 65
+    n = 4097                                  # > ARA_MAX_PORTFOLIO_LAYERS
     pf2 = dict(pf)
     pf2["layer_prog"] = np.zeros(n, np.uint32)
     pf2["layer_elt_off"] = np.arange(n + 1, dtype=np.uint64)
@@ -105,3 +105,10 @@ def test_validate_limits(ara):
     ara.validate_portfolio(ok)
     ok["layer_terms"] = np.array([[0.0, np.inf, 0.0, np.inf]] * 2)
     ara.validate_portfolio(ok)
+    # 65 layers (more than one kernel group) are valid; a layer over > 224 XELTs is not
+    pf3 = dict(pf)
+    pf3["layer_prog"] = np.zeros(65, np.uint32)
+    pf3["layer_elt_off"] = np.arange(66, dtype=np.uint64)
+    pf3["layer_elts"] = np.zeros(65, np.uint32)
+    pf3["layer_terms"] = np.tile([1.0, 1e6, 0.0, 1e9], (65, 1))
+    ara.validate_portfolio(pf3)

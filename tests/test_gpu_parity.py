@@ -698,3 +698,35 @@ def test_exceedance_curve_rollup_shards_and_cfg1(A, ctx):
     N = cfg["n_trials"]
     for q, rp in enumerate((10, 50)):
         assert var[q] == curve[-(-N // rp) - 1]               # VaR = L(ceil(N/RP))
+
+
+# ---- portfolios larger than one kernel group (thousands of XELTs) ------
+@pytest.mark.parametrize("n_layers,J", [(20, 16), (65, 3)])
+def test_large_portfolio_in_groups(A, ctx, n_layers, J):
+    # > 8 layers or > 224 (layer, XELT) slots: groups of consecutive layers,
+    # one run each over the same YET; lookup exact, YLT / occ_max / roll-up
+    # measures against the oracle
+    cfg = aragen.load_config("cfg1")
+    terms = [[1e5 * (l % 5 + 1), 5e6, 1.0e6, 5.0e7] for l in range(n_layers)]
+    cfg.update(n_layers=n_layers, elts_per_layer=J, catalog=20000, records_per_elt=400,
+               n_trials=200, layer_terms=terms)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    pf["layer_prog"] = (np.arange(n_layers) % 4).astype(np.uint32)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    g, cnt, hsh = A.run(ctx, P, Y, seed=31, debug=True)
+    ref = oracle.run(pf, yet, seed=31)
+    assert np.array_equal(cnt.cpu().numpy().astype(np.uint32), ref["count"])
+    assert np.array_equal(hsh.cpu().numpy().view(np.uint64), ref["hash"])
+    gn = g.cpu().numpy()
+    for li in range(n_layers):
+        ylt_check(gn[li], ref, li)
+    ylt, occ = A.run_ep(ctx, P, Y, seed=31)
+    assert np.array_equal(ylt.cpu().numpy(), gn)
+    for li in (0, n_layers // 2, n_layers - 1):
+        occ_check(occ.cpu().numpy()[li], ref, pf, li)
+    pml, tvar = A.risk_measures(ctx, g, n_layers, cfg["n_trials"], -1, rps=(10, 50))
+    o = OM.rollup(ref["ylt"])
+    floor = FLOOR * ref["gross"].sum(axis=0).max()
+    for q, rp in enumerate((10, 50)):
+        assert abs(pml[q] - OM.pml(o, rp)) <= REL * abs(OM.pml(o, rp)) + floor
+        assert abs(tvar[q] - OM.tvar_rp(o, rp)[1]) <= REL * abs(OM.tvar_rp(o, rp)[1]) + floor

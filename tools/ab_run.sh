@@ -1,9 +1,6 @@
-for i in 1 2; do
-timeout 600 python bench.py --no-cpu-baseline --steps 3 --e2e-steps 5 > gpurun_out/bp$i.json 2>/dev/null
-timeout 600 python bench.py --no-cpu-baseline --steps 3 --e2e-steps 5 --plain-upload > gpurun_out/bu$i.json 2>/dev/null
-done
-python -c "
-import json
-for f in ('bp1','bu1','bp2','bu2'):
-    d=json.load(open('gpurun_out/%s.json'%f)); print(f, d['e2e']['value'], d['e2e']['h2d_bytes_per_step'])"
-nproc; lscpu | grep -i "numa node" | head -4
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+bash tools/ab_bench.sh cfg3 gpurun_variants/rb0.so gpurun_variants/rb1.so gpurun_variants/rb0.so gpurun_variants/rb1.so
+for L in rb0 rb1; do ARA_LIB_PATH=$PWD/gpurun_variants/$L.so timeout 600 python bench.py --config cfg5 --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 1 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); r=d['roofline']['kernels']
+print('cfg5 $L', round(d['ms_per_step'],3), 'compact', round(r['compact_kernel']['kernel_ms'],3), 'sample', round(r['sample_kernel']['kernel_ms'],3))"; done

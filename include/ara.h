@@ -50,10 +50,10 @@ extern "C" {
 #define ARA_EXACT 4u         /* solve every beta quantile per sample in fp64
                                 instead of the per-record quantile tables
                                 (validation mode; slow)                    */
-#define ARA_FUSED 8u         /* run compaction and sampling in one warp-
-                                specialised kernel (pairs in an L2-resident
-                                ring) instead of two kernels; same results
-                                bit for bit.  Round 1: slower */
+#define ARA_FUSED 8u         /* accepted, no effect: the warp-specialised
+                                single kernel it selected in round 1 was
+                                slower than the two-kernel path and was
+                                removed                     */
 #define ARA_WIDE_PAIRS 16u   /* keep 8-byte {record, k} pair records even when
                                 4-byte packed ones fit (same results; for tests
                                 and comparison)                            */
@@ -229,7 +229,7 @@ int ara_run(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint64_t 
  *             (per layer, layer >= 0) gives OEP PML / TVaR; its roll-up over
  *             layers (layer = -1) is NOT a portfolio OEP.
  * Same arguments, outputs and errors as ara_run; ARA_EINVAL if occ_max is
- * NULL or host memory, or with ARA_FUSED. */
+ * NULL or host memory. */
 int ara_run_ep(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint64_t seed,
                uint32_t flags, float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash);
 

@@ -607,7 +607,6 @@ int ara_run(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed,
 int ara_run_ep(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
                float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash) {
     if (!occ_max) return fail(ARA_EINVAL, "occ_max is NULL (use ara_run)");
-    if (flags & ARA_FUSED) return fail(ARA_EINVAL, "ARA_FUSED does not produce occ_max");
     return run_impl(c, p, y, seed, flags, ylt, occ_max, dbg_count, dbg_hash);
 }
 
@@ -660,12 +659,8 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
         const double expect = per_occ * (double)y->avg_len_x1000 / 1000.0;
         uint32_t cap = (uint32_t)((2.0 * expect + 128.0 + 31.0) / 32.0) * 32u;
         if (cap > (1u << 20)) cap = 1u << 20;
-        // two kernels (compaction, then sampling); ARA_FUSED asks for the
-        // warp-specialised single kernel (if the portfolio fits its shared memory)
-        const uint64_t ring = ((flags & ARA_FUSED) && !(flags & ARA_RNG_RECORD))   // (two kernels for (A))
-                                  ? fused_ring_pairs(p->dev, cap, c->num_sms) : 0;
-        const bool fused = ring != 0;
-        const uint64_t need = fused ? ring : y->dev.n_trials * (uint64_t)cap;
+        // two kernels: compaction, then sampling (ARA_FUSED is accepted and runs them too)
+        const uint64_t need = y->dev.n_trials * (uint64_t)cap;
         if (c->pairs_capacity < need) {          // scratch grows once, then is reused
             cudaFree(c->d_pairs);
             c->d_pairs = nullptr;
@@ -687,7 +682,7 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
         S.ze_mask = S.rng_mode == 2 ? 0u : 0xffffffffu;
         S.ze_tag = S.rng_mode == 2 ? 7u : 2u;
         // 4-byte pairs (record << kbits | k) when both fit: halves the pair traffic
-        if (!fused && !(flags & ARA_WIDE_PAIRS)) {
+        if (!(flags & ARA_WIDE_PAIRS)) {
             uint32_t kb = 1;
             while (kb < 24 && (1ull << kb) < (uint64_t)y->max_len) ++kb;
             if ((uint64_t)p->dev.n_dev_records <= (1ull << (32 - kb))) S.kbits = kb;
@@ -697,9 +692,9 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
             S.pkey[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;
         }
         CU(cudaEventRecord(c->ev[0], c->stream));
-        if (!fused) CU(launch_compact(S, c->stream, c->num_sms));
+        CU(launch_compact(S, c->stream, c->num_sms));
         CU(cudaEventRecord(c->ev[1], c->stream));
-        CU(fused ? launch_fused(S, c->stream, c->num_sms) : launch_sample(S, c->stream, c->num_sms));
+        CU(launch_sample(S, c->stream, c->num_sms));
         CU(cudaEventRecord(c->ev[2], c->stream));
     } else {
         // ARA_EXACT (fp64 solve for every sample) or > kSplitMaxLayers layers: the fused kernel

@@ -133,10 +133,6 @@ struct SplitArgs {
 };
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);
-// the fused (warp-specialised) form; fused_ring_pairs = its pair scratch in
-// pairs, 0 if the portfolio does not fit its shared memory
-uint64_t fused_ring_pairs(const PortfolioDev &pf, uint32_t cap, int num_sms);
-cudaError_t launch_fused(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_unpack_yet(const uint32_t *packed, uint64_t n, uint32_t bits, uint32_t *out, cudaStream_t s,
                               int num_sms);
 cudaError_t launch_yet_max(const uint32_t *ev, uint64_t n, uint32_t *out, cudaStream_t s, int num_sms);

@@ -663,125 +663,6 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 wa
     }
 }
 
-// ---------------------------------------------------------------------------
-// fused_kernel: the same two stages in one persistent kernel, one CTA (32
-// warps) per SM, warp-specialised.  kNP producer warps (the highest warp ids,
-// which the SM's issue arbiter favours) run produce_pairs over the trials
-// blockIdx.x * kNP + w, + gridDim.x * kNP, ...; each trial's pairs go to the
-// next slot of this CTA's ring of kRing pair regions in global memory (small
-// enough to stay in L2).  The other warps consume the slots in order and run
-// sample_trial on them.  A slot's state word carries the ring index it is
-// free for or full with (2i: free for index i, 2i + 1: full with index i), so
-// producers and consumers that race ahead never take a slot meant for another
-// lap.  Compaction (latency-bound) and sampling (issue-bound) so overlap on
-// every SM, and the pairs never travel to HBM.
-// ---------------------------------------------------------------------------
-#ifndef ARA_FUSED_PRODUCERS
-#define ARA_FUSED_PRODUCERS 8
-#endif
-constexpr int kNP = ARA_FUSED_PRODUCERS;            // producer warps per CTA
-constexpr int kNC = 32 - kNP;                       // consumer warps per CTA
-constexpr uint32_t kRing = 2 * kNC;                 // pair regions per CTA
-
-struct FusedQueue {
-    uint32_t prod_next, cons_next, prod_done, pad;
-    uint32_t state[kRing];
-    uint2 meta[kRing];                              // (trial, pairs or kOverflow)
-};
-
-struct RingSink {
-    const SplitArgs &A;
-    FusedQueue &Q;
-    uint2 *ring;                                    // this CTA's kRing regions of cap pairs
-    uint32_t ps = 0, idx = 0;                       // slot and ring index of the current trial
-    __device__ uint2 *begin(uint32_t) {
-        const int lane = threadIdx.x & 31;
-        uint32_t i = 0;
-        if (lane == 0) {
-            i = atomicAdd(&Q.prod_next, 1u);
-            volatile uint32_t *st = &Q.state[i % kRing];
-            while (*st != 2u * i) __nanosleep(64);   // free for this lap
-        }
-        idx = __shfl_sync(0xffffffffu, i, 0);
-        ps = idx % kRing;
-        __syncwarp();
-        return ring + (uint64_t)ps * A.cap;
-    }
-    __device__ void end(uint32_t t, uint32_t n) {
-        __threadfence_block();                      // this lane's pair stores before the flag
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) {
-            const bool over = n > A.cap;
-            if (over) A.redo[atomicAdd(&A.status->n_redo, 1u)] = t;
-            Q.meta[ps] = make_uint2(t, over ? kOverflow : n);
-            __threadfence_block();
-            *(volatile uint32_t *)&Q.state[ps] = 2u * idx + 1u;
-        }
-        __syncwarp();
-    }
-};
-
-template <bool SU, bool SL, bool DBG>
-__global__ void __launch_bounds__(1024, 1) fused_kernel(const __grid_constant__ SplitArgs A) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t nl = A.pf.n_layers, kXCap = A.xcap;
-    uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);
-    FusedQueue *Qp = reinterpret_cast<FusedQueue *>(smem + ((A.pf.bitmap_words * 4u + 15u) & ~15u));
-    SlotInfo *slots = reinterpret_cast<SlotInfo *>(Qp + 1);
-    LayerInfo *layers = reinterpret_cast<LayerInfo *>(slots + ARA_MAX_SLOTS);
-    double *accw = reinterpret_cast<double *>(layers + ARA_MAX_LAYERS);           // [kNC][nl][32]
-    unsigned long long *hw = reinterpret_cast<unsigned long long *>(accw + kNC * nl * 32);   // [kNC][nl]
-    unsigned int *cw = reinterpret_cast<unsigned int *>(hw + kNC * nl);          // [kNC][nl]
-    uint32_t *xsw = cw + kNC * nl;                                              // [kNC][kXCap]
-    uint8_t *flw = reinterpret_cast<uint8_t *>(xsw + kNC * kXCap);               // [kNC][kXCap]
-    if (*A.yet.max_event >= A.pf.catalog) {           // out-of-range ids: nothing is read
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&A.status->bad_event, 1u);
-        return;
-    }
-    FusedQueue &Q = *Qp;
-    for (uint32_t t = threadIdx.x; t < A.pf.bitmap_words; t += blockDim.x) bitmap[t] = A.pf.bitmap[t];
-    for (uint32_t t = threadIdx.x; t < A.pf.n_slots; t += blockDim.x) slots[t] = A.pf.slots[t];
-    for (uint32_t t = threadIdx.x; t < nl; t += blockDim.x) layers[t] = A.pf.layers[t];
-    for (uint32_t t = threadIdx.x; t < kRing; t += blockDim.x) Q.state[t] = 2u * t;   // free for lap 0
-    if (threadIdx.x == 0) { Q.prod_next = 0u; Q.cons_next = 0u; Q.prod_done = 0u; }
-    __syncthreads();
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint2 *ring = A.pairs + (uint64_t)blockIdx.x * kRing * A.cap;
-    if (warp >= kNC) {                                // ---- producer
-        RingSink sink{A, Q, ring};
-        produce_pairs<false, 2>(A, bitmap, blockIdx.x * kNP + (warp - kNC), gridDim.x * kNP, sink);
-        __syncwarp();
-        if (lane == 0) atomicAdd(&Q.prod_done, 1u);
-        return;
-    }
-    // ---- consumer
-    const SampleWs W{slots, layers, xsw + warp * kXCap, flw + warp * kXCap, accw + warp * nl * 32 + lane,
-                     cw + warp * nl, hw + warp * nl, nullptr};
-    while (true) {
-        uint32_t i = 0, go = 0;
-        if (lane == 0) {
-            i = atomicAdd(&Q.cons_next, 1u);
-            volatile uint32_t *st = &Q.state[i % kRing];
-            volatile uint32_t *done = &Q.prod_done, *pn = &Q.prod_next;
-            while (true) {
-                if (*st == 2u * i + 1u) { go = 1; break; }
-                if (*done == (uint32_t)kNP && i >= *pn) break;    // nothing more will come
-                __nanosleep(128);
-            }
-            __threadfence_block();
-        }
-        i = __shfl_sync(0xffffffffu, i, 0);
-        if (!__shfl_sync(0xffffffffu, go, 0)) break;
-        const uint32_t ps = i % kRing;
-        const uint2 m = Q.meta[ps];
-        if (m.y != kOverflow)
-            sample_trial<SU, SL, DBG, true>(A, W, m.x, m.y, ring + (uint64_t)ps * A.cap);
-        __syncwarp();
-        if (lane == 0) *(volatile uint32_t *)&Q.state[ps] = 2u * (i + kRing);   // free for the next lap
-    }
-}
-
 __global__ void split_recs_kernel(const BetaRec *__restrict__ recs, const uint32_t *__restrict__ rec_meta,
                                   const SlotInfo *__restrict__ slots, const float *__restrict__ mu, uint64_t n,
                                   SplitRec *__restrict__ out, uint2 *__restrict__ mu_meta) {
@@ -813,9 +694,10 @@ __global__ void unpack_yet_kernel(const uint32_t *__restrict__ packed, uint64_t 
         uint32_t v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const uint64_t bit = (4 * q + j) * (uint64_t)bits, w = bit >> 5;
+            const uint64_t x = 4 * q + j, bit = x * (uint64_t)bits, w = bit >> 5;
             const uint32_t sh = (uint32_t)(bit & 31u);
-            const uint32_t lo = __ldg(packed + w), hi = __ldg(packed + w + 1);   // (+2 words of padding)
+            uint32_t lo = 0u, hi = 0u;
+            if (x < n) { lo = __ldg(packed + w); hi = __ldg(packed + w + 1); }   // (+2 words of padding)
             v[j] = __funnelshift_r(lo, hi, sh) & mask;
         }
         reinterpret_cast<uint4 *>(out)[q] = make_uint4(v[0], v[1], v[2], v[3]);   // (+4 words of padding)
@@ -962,46 +844,6 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     kern<<<num_sms * per_sm, kSampleWarps * 32, smem, s>>>(B);
-    return cudaGetLastError();
-}
-
-// Shared memory of fused_kernel for a portfolio, and the sampler segment it
-// leaves room for (0: does not fit; the two-kernel path is used).
-static size_t fused_smem(const PortfolioDev &pf, uint32_t &xcap) {
-    const size_t fixed = ((pf.bitmap_words * 4u + 15u) & ~15u) + sizeof(FusedQueue) +
-                         sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
-                         (sizeof(double) + sizeof(unsigned long long) + sizeof(unsigned int)) * kNC * pf.n_layers * 32;
-    const size_t budget = 227 * 1024;
-    xcap = 0;
-    if (pf.n_layers > kSplitMaxLayers || fixed + 64 >= budget) return 0;
-    constexpr size_t kR = 64 * kU;                   // segments end on a round
-    const size_t x = (budget - fixed - 64) / ((sizeof(uint32_t) + sizeof(uint8_t)) * kNC) / kR * kR;
-    if (x < 256) return 0;
-    xcap = (uint32_t)std::min<size_t>(x, kXCapMax / kR * kR);
-    return fixed + (sizeof(uint32_t) + sizeof(uint8_t)) * kNC * xcap + 16;
-}
-
-uint64_t fused_ring_pairs(const PortfolioDev &pf, uint32_t cap, int num_sms) {
-    uint32_t xcap = 0;
-    if (!fused_smem(pf, xcap)) return 0;
-    return (uint64_t)num_sms * kRing * cap;
-}
-
-cudaError_t launch_fused(const SplitArgs &A, cudaStream_t s, int num_sms) {
-    const bool dbg = (A.flags & ARA_DEBUG_LOOKUP) != 0, su = (A.flags & ARA_SU) != 0;
-    const bool sl = A.pf.n_layers == 1;
-    SplitArgs B = A;
-    const size_t smem = fused_smem(A.pf, B.xcap);
-    if (!smem) return cudaErrorInvalidValue;
-    using K = void (*)(SplitArgs);
-    const K kern = su ? (sl ? (dbg ? (K)fused_kernel<true, true, true> : (K)fused_kernel<true, true, false>)
-                            : (dbg ? (K)fused_kernel<true, false, true> : (K)fused_kernel<true, false, false>))
-                      : (sl ? (dbg ? (K)fused_kernel<false, true, true> : (K)fused_kernel<false, true, false>)
-                            : (dbg ? (K)fused_kernel<false, false, true> : (K)fused_kernel<false, false, false>));
-    int per_sm = 0;
-    cudaError_t err = prepare_launch((const void *)kern, smem, 1024, per_sm);
-    if (err != cudaSuccess) return err;
-    kern<<<num_sms, 1024, smem, s>>>(B);
     return cudaGetLastError();
 }
 

@@ -285,7 +285,7 @@ def test_shared_elts_and_xelt_terms(A, ctx):
 
 def test_pair_region_overflow_goes_to_fused_kernel(A, ctx):
     # a trial whose present pairs exceed its region (2x expected + 128) is redone
-    # by the fused kernel; counts/hashes/YLT stay exact
+    # by the fp64-capable scan kernel; counts/hashes/YLT stay exact
     cfg = aragen.load_config("cfg1")
     cfg["n_trials"] = 50
     pf = aragen.build_portfolio(cfg)
@@ -325,8 +325,8 @@ def test_determinism_and_sharding(A, ctx):
 
 @pytest.mark.parametrize("n_layers,J,K", [(1, 16, 1000), (3, 4, 1500)])
 def test_fused_packed_and_wide_pairs_identical(A, ctx, n_layers, J, K):
-    # the warp-specialised kernel and the two-kernel form process each trial
-    # in the same order: bit-identical YLT, counts and hashes
+    # 4-byte packed and 8-byte pair records (and the no-op ARA_FUSED flag):
+    # each trial in the same order, bit-identical YLT, counts and hashes
     cfg = aragen.load_config("cfg3")
     terms = [[2e5 * (l + 1), 5e6, 1.0e6, 5.0e9] for l in range(n_layers)]
     cfg.update(n_layers=n_layers, elts_per_layer=J, n_trials=20000, events_per_trial=K, layer_terms=terms)
@@ -588,8 +588,9 @@ def test_run_ep_errors(A, ctx):
     ylt = torch.empty((1, 10), dtype=torch.float32, device="cuda")
     with pytest.raises(A.AraError):
         A._check(A.lib.ara_run_ep(ctx.h, P.h, Y.h, 1, A.SU, A._p(ylt), None, None, None))
-    with pytest.raises(A.AraError):
-        A._check(A.lib.ara_run_ep(ctx.h, P.h, Y.h, 1, A.SU | A.FUSED, A._p(ylt), A._p(ylt), None, None))
+    with pytest.raises(A.AraError):                  # host memory for occ_max
+        A._check(A.lib.ara_run_ep(ctx.h, P.h, Y.h, 1, A.SU, A._p(ylt), A._p(np.zeros((1, 10), np.float32)),
+                                  None, None))
 
 
 # ---- packed YET upload (storage encoding; ara_yet_refill_packed) -------------

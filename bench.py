@@ -182,10 +182,17 @@ def run_ours(args, cfg, rank, world, local):
     import torch.distributed as dist
     from paper_1310_2274_b200 import ara
 
+    # one process per GPU; ARA_BENCH_BACKEND=gloo (a test aid) runs the multi-rank
+    # path with several ranks sharing the visible GPUs
+    backend = os.environ.get("ARA_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     N_total = cfg["n_trials"] * (world if args.scaling == "weak" else 1)
     lo, hi = shard_range(N_total, rank, world)
     n_loc = hi - lo
@@ -380,7 +387,7 @@ def run_ours(args, cfg, rank, world, local):
                    "trials_per_rank": n_loc, "return_periods": rps,
                    "l2": "inputs > L2: the 3.2 GB YET is streamed every step; the portfolio "
                          "tables (index, bitmap, records) stay L2-resident by design",
-                   "parallelism": f"trial-sharded x{world}" + (" + NCCL YLT all-gather" if world > 1 else "")},
+                   "parallelism": f"trial-sharded x{world}" + (f" + {backend.upper()} YLT all-gather" if world > 1 else "")},
         "e2e": {"value": N_total / (e2e_elapsed / e2e_steps), "unit": "trials/s",
                 "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": L * n_loc * 4 + 16 * len(rps) * len(layers),
                 "steps": e2e_steps, "yet_upload_bits": bits,

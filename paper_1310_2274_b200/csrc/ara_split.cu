@@ -589,7 +589,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
         if (lane == 0 || !prev_seg) in_run += carry;   // no run end before me in this segment
         if (has_end) {
             const LayerInfo &L = layers[head_layer];
-            const double g = fmin(fmax(head + in_run - L.occ_r, 0.0), L.occ_l);
+            const double g = xl_clip_(head + in_run - L.occ_r, L.occ_l);
             if (SL) acc += g; else accs[head_layer * 32] += g;
             if (OM) {
                 if (SL) mo = fmaxf(mo, (float)g);
@@ -611,7 +611,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
         const double S = warp_sum_f64_(SL ? acc : accs[l * 32]);   // fixed tree
         if (lane == 0) {
             const LayerInfo &L = layers[l];
-            A.ylt[(uint64_t)l * n_trials + t] = (float)fmin(fmax(S - L.agg_r, 0.0), L.agg_l);
+            A.ylt[(uint64_t)l * n_trials + t] = (float)xl_clip_(S - L.agg_r, L.agg_l);   // line 12 (G5, G6)
             if (DBG) {
                 if (A.dbg_count) A.dbg_count[(uint64_t)l * n_trials + t] = dc[l];
                 if (A.dbg_hash) A.dbg_hash[(uint64_t)l * n_trials + t] = dhs[l];

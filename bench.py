@@ -340,6 +340,8 @@ def run_ours(args, cfg, rank, world, local):
     compact["frac"] = compact["achieved"] / hbm_peak if compact["achieved"] else None
     cc = consts.get("compact_kernel", {})
     compact["traffic"] = cc.get("dram_bytes_per_occurrence", 0) * n_loc * K if cc else None
+    if cc.get("ncu"):
+        compact["ncu"] = dict(cc["ncu"], source=cc.get("source"))   # L2 hit rate, pipes
     sample = {"kernel": "sample_kernel", "kernel_ms": t_sample * 1e3, "samples_per_launch": pairs,
               "samples_per_s": pairs / t_sample if t_sample else None}
     sc = consts.get("sample_kernel", {}) if cfg["su"] else {}
@@ -348,6 +350,8 @@ def run_ours(args, cfg, rank, world, local):
                       peak_source="148 SMs x 128 FP32 lanes x sm_max_mhz (B200_PROFILING.md)")
         if sc and t_sample:
             inst = sc["thread_inst_per_pair"] * pairs
+            if sc.get("ncu"):
+                sample["ncu"] = dict(sc["ncu"], source=sc.get("source"))
             sample.update(achieved=inst / t_sample / 1e12, frac=inst / t_sample / 1e12 / alu_peak,
                           inst_per_pair=sc["thread_inst_per_pair"], inst_source=consts.get("source"),
                           traffic=sc["dram_bytes_per_pair"] * pairs)

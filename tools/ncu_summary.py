@@ -100,8 +100,17 @@ def main():
         print(json.dumps({short: d}, indent=1))
         if a.write_const:
             key = "occurrence" if short == "compact_kernel" else "pair"
+            mm = out["metrics"]
+            pick = lambda k: float(mm[k]["value"]) if k in mm else None
             consts[short] = {f"thread_inst_per_{key}": d["thread_inst_per_unit"],
                              f"dram_bytes_per_{key}": d["dram_bytes_per_unit"],
+                             # L2 hit rate, pipe utilisation, issue, SM clock of the capture
+                             "ncu": {"l2_hit_rate_pct": pick("lts__t_sector_hit_rate.pct"),
+                                     "issue_active_pct": pick("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                     "fma_pipe_pct": pick("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                                     "alu_pipe_pct": pick("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                                     "xu_pipe_pct": pick("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+                                     "sm_ghz": pick("sm__cycles_elapsed.avg.per_second")},
                              "source": f"profiles/{a.tag}_{short}.json ({os.path.basename(a.rep)})"}
     if a.write_const:
         consts["source"] = f"profiles/{a.tag}_*.json"

@@ -468,6 +468,31 @@ def test_full_size_sampled(A, ctx, name, n_sample):
     assert (tvar >= pml * (1 - 1e-6)).all() and (tvar <= lim).all()
 
 
+def test_cfg5_rank_shard_sampled(A, ctx):
+    # cfg5 as one of 8 ranks holds it: global trials [875000, 1000000) of the
+    # 1M-trial, 8-layer x 16-XELT, 2M-event analysis at full portfolio size;
+    # every layer of 60 sampled trials (incl. the shard's first and last)
+    # against the oracle, computed trial by trial with the global indices
+    import torch
+    cfg = aragen.load_config("cfg5")
+    pf = aragen.build_portfolio(cfg)
+    N, K, L = cfg["n_trials"], cfg["events_per_trial"], cfg["n_layers"]
+    lo, n = 7 * N // 8, N // 8
+    ev = torch.empty(n * K, dtype=torch.int32).pin_memory()
+    aragen.build_yet(cfg, first_trial=lo, n_trials=n, out=ev.numpy().view(np.uint32))
+    P = A.Portfolio(ctx, pf)
+    Y = A.Yet(ctx, ev, fixed_len=K, first_trial=lo, n_trials=n)
+    ylt = A.run(ctx, P, Y, seed=cfg["seed"], su=True).cpu().numpy()
+    assert ylt.shape == (L, n)
+    rng = np.random.default_rng(5)
+    loc = np.sort(rng.choice(n, 60, replace=False))
+    loc[0], loc[-1] = 0, n - 1
+    sub = aragen.yet_for_trials(cfg, loc + lo)
+    ref = oracle.run(pf, sub, seed=cfg["seed"], su=True, trial_index=sub["trial_index"])
+    for li in range(L):
+        ylt_check(ylt[li, loc], ref, li)
+
+
 @pytest.mark.parametrize("name,n", [("cfg1", None), ("cfg3", 20000), ("cfg5", 4000)])
 def test_measures_end_to_end(A, ctx, name, n):
     cfg = aragen.load_config(name)

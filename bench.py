@@ -231,10 +231,10 @@ def run_ours(args, cfg, rank, world, local):
         if world > 1:
             dist.all_gather_into_tensor(gathered, ylt)
             src = gathered
-        res = []
-        for layer in layers:
-            res.append(ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=world))
-        return res
+        if len(layers) > 1 and len(rps) <= 4:        # every table in one call, one read-back
+            pml, tvar, _ = ara.risk_measures_batch(ctx, src, L, N_total, layers, rps=rps, n_shards=world)
+            return [(pml[i], tvar[i]) for i in range(len(layers))]
+        return [ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=world) for layer in layers]
 
     # exact number of present (occurrence, slot) pairs = SU samples per launch
     _, cnt_dbg, _ = ara.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"], debug=True)
@@ -307,8 +307,11 @@ def run_ours(args, cfg, rank, world, local):
         if world > 1:
             dist.all_gather_into_tensor(gathered, ylt)
             src = gathered
-        for layer in layers:
-            ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=world)
+        if len(layers) > 1 and len(rps) <= 4:
+            ara.risk_measures_batch(ctx, src, L, N_total, layers, rps=rps, n_shards=world)
+        else:
+            for layer in layers:
+                ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=world)
         ylt_host.copy_(ylt, non_blocking=True)  # D2H of the step's result
     te1.record(stream)
     torch.cuda.synchronize()

@@ -267,6 +267,16 @@ int ara_risk_measures_var(ara_ctx *ctx, const float *ylt, uint32_t n_layers, uin
                           uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
                           double *pml_out, double *tvar_out, double *var_out);
 
+/* ara_risk_measures_var for several tables of one YLT in one call: the
+ * layers listed in layers[n_sel] (-1 = the roll-up), each by the joint
+ * select, launched back to back with one read-back at the end (a multi-layer
+ * portfolio's measures in one synchronisation instead of one per table).
+ *   pml_out, tvar_out, var_out (NULL ok)  host [n_sel][n_rp]
+ * n_rp in [1, 4]; other arguments and errors as ara_risk_measures. */
+int ara_risk_measures_batch(ara_ctx *ctx, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                            uint32_t n_shards, const int32_t *layers, uint32_t n_sel, const double *rps,
+                            uint32_t n_rp, double *pml_out, double *tvar_out, double *var_out);
+
 /* The exceedance curve (SPEC ExceedanceCurve S:345-352) of one
  * layer's YLT, or of the roll-up over layers (layer = -1, G16): the losses
  * sorted descending, L(1) >= ... >= L(N); the empirical exceedance

@@ -36,7 +36,7 @@ EXPORTS = (
     "ara_last_error", "ara_version", "ara_ctx_create", "ara_ctx_destroy", "ara_ctx_synchronize",
     "ara_validate_portfolio", "ara_create_portfolio", "ara_portfolio_destroy", "ara_portfolio_info",
     "ara_load_yet",
-    "ara_yet_refill", "ara_yet_refill_packed", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings", "ara_risk_measures_var", "ara_exceedance_curve",
+    "ara_yet_refill", "ara_yet_refill_packed", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings", "ara_risk_measures_var", "ara_risk_measures_batch", "ara_exceedance_curve",
     "ara_risk_measures",
     "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles",
 )
@@ -74,6 +74,7 @@ def _load():
     L.ara_risk_measures.argtypes = [vp, vp, u32, u64, u32, i32, vp, u32, vp, vp]
     L.ara_risk_measures_var.argtypes = [vp, vp, u32, u64, u32, i32, vp, u32, vp, vp, vp]
     L.ara_exceedance_curve.argtypes = [vp, vp, u32, u64, u32, i32, vp]
+    L.ara_risk_measures_batch.argtypes = [vp, vp, u32, u64, u32, vp, u32, vp, u32, vp, vp, vp]
     L.ara_last_run_timings.argtypes = [vp, vp, vp, vp]
     L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, u32, vp]
     L.ara_draw_uniforms.argtypes = [vp, u64, u64, vp, vp]
@@ -318,6 +319,17 @@ def risk_measures_var(ctx: Context, ylt, n_layers: int, n_total: int, layer: int
     pml = np.empty(len(r)); tvar = np.empty(len(r)); var = np.empty(len(r))
     _check(lib.ara_risk_measures_var(ctx.h, _p(ylt), int(n_layers), int(n_total), int(n_shards),
                                      int(layer), _p(r), len(r), _p(pml), _p(tvar), _p(var)))
+    return pml, tvar, var
+
+
+def risk_measures_batch(ctx: Context, ylt, n_layers: int, n_total: int, layers, rps=(100, 250, 500),
+                        n_shards: int = 1):
+    """ara_risk_measures_batch; returns (pml, tvar, var), numpy fp64 [len(layers)][n_rp]."""
+    r = np.ascontiguousarray(rps, np.float64)
+    ls = np.ascontiguousarray(layers, np.int32)
+    pml = np.empty((len(ls), len(r))); tvar = np.empty_like(pml); var = np.empty_like(pml)
+    _check(lib.ara_risk_measures_batch(ctx.h, _p(ylt), int(n_layers), int(n_total), int(n_shards), _p(ls),
+                                       len(ls), _p(r), len(r), _p(pml), _p(tvar), _p(var)))
     return pml, tvar, var
 
 

@@ -56,13 +56,15 @@ cudaError_t dalloc(T **p, size_t n) {
 
 }  // namespace
 
+constexpr uint32_t kOutDoubles = 3 * 4 * (ARA_MAX_PORTFOLIO_LAYERS + 1);   // batched measures: 3 x n_rp x tables
+
 struct ara_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 0;
     RunStatus *d_status = nullptr;
     RunStatus *h_status = nullptr;     // pinned
-    double *h_out = nullptr;           // pinned [192]: measures results (pml, tvar, var) per RP
+    double *h_out = nullptr;           // pinned [kOutDoubles]: measures results (pml, tvar, var) per RP (x layers)
     uint32_t *d_ep = nullptr;          // exceedance-curve sort scratch
     uint64_t ep_capacity = 0;
     MeasuresScratch ms;
@@ -135,10 +137,10 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
     c->num_sms = prop.multiProcessorCount;
     if (cudaMalloc(&c->d_status, sizeof(RunStatus)) != cudaSuccess ||
         cudaMallocHost(&c->h_status, sizeof(RunStatus)) != cudaSuccess ||
-        cudaMallocHost(&c->h_out, 192 * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&c->h_out, kOutDoubles * sizeof(double)) != cudaSuccess ||
         dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 4 * 256) != cudaSuccess ||
         dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
-        dalloc(&c->ms.d_out, 192) != cudaSuccess ||
+        dalloc(&c->ms.d_out, kOutDoubles) != cudaSuccess ||
         dalloc(&c->ms.mhist, 4 * kMaxPlanRanks * 256) != cudaSuccess || dalloc(&c->ms.macc, 8) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
         dalloc(&c->ms.part_sum, kRedBlocks) != cudaSuccess ||
         dalloc(&c->ms.part_cnt, kRedBlocks) != cudaSuccess || cudaEventCreate(&c->ev[0]) != cudaSuccess ||
@@ -794,6 +796,45 @@ int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t 
                       double *pml_out, double *tvar_out) {
     return ara_risk_measures_var(c, ylt, n_layers, n_total, n_shards, layer, rps, n_rp, pml_out, tvar_out,
                                  nullptr);
+}
+
+int ara_risk_measures_batch(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                            uint32_t n_shards, const int32_t *layers, uint32_t n_sel, const double *rps,
+                            uint32_t n_rp, double *pml_out, double *tvar_out, double *var_out) {
+    if (!c || !ylt || !layers || !rps || !pml_out || !tvar_out) return fail(ARA_EINVAL, "NULL argument");
+    if (n_total == 0) return fail(ARA_EINVAL, "empty YLT");
+    if (n_layers == 0 || n_shards == 0 || n_total % n_shards)
+        return fail(ARA_EINVAL, "need n_layers >= 1, n_shards >= 1 dividing n_total");
+    if (n_sel == 0 || n_sel > ARA_MAX_PORTFOLIO_LAYERS + 1) return fail(ARA_EINVAL, "n_sel out of range");
+    if (n_rp == 0 || n_rp > 4) return fail(ARA_EINVAL, "n_rp must be in [1, 4] (ara_risk_measures for more)");
+    for (uint32_t q = 0; q < n_rp; ++q)
+        if (!(rps[q] > 1.0) || !std::isfinite(rps[q]))
+            return fail(ARA_EINVAL, "return period %g must be finite and > 1", rps[q]);
+    for (uint32_t i = 0; i < n_sel; ++i)
+        if (layers[i] < -1 || layers[i] >= (int32_t)n_layers) return fail(ARA_EINVAL, "layer %d out of range", layers[i]);
+    if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
+    CU(cudaSetDevice(c->device));
+    if (c->ms.capacity < n_total) {
+        cudaFree(c->ms.vals);
+        c->ms.vals = nullptr;
+        c->ms.capacity = 0;
+        CU(dalloc(&c->ms.vals, n_total));
+        c->ms.capacity = n_total;
+    }
+    // one joint-select launch per table, back to back on the stream, one read-back
+    for (uint32_t i = 0; i < n_sel; ++i)
+        CU(launch_measures_multi(ylt, n_layers, n_total, n_shards, layers[i], rps, n_rp, c->ms,
+                                 c->ms.d_out + 3 * n_rp * i, c->stream));
+    double *out = c->h_out;
+    CU(cudaMemcpyAsync(out, c->ms.d_out, 3 * n_rp * n_sel * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    for (uint32_t i = 0; i < n_sel; ++i)
+        for (uint32_t q = 0; q < n_rp; ++q) {
+            pml_out[i * n_rp + q] = out[3 * (n_rp * i + q)];
+            tvar_out[i * n_rp + q] = out[3 * (n_rp * i + q) + 1];
+            if (var_out) var_out[i * n_rp + q] = out[3 * (n_rp * i + q) + 2];
+        }
+    return ARA_OK;
 }
 
 int ara_risk_measures_var(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,

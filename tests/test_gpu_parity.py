@@ -756,3 +756,16 @@ def test_large_portfolio_in_groups(A, ctx, n_layers, J):
     for q, rp in enumerate((10, 50)):
         assert abs(pml[q] - OM.pml(o, rp)) <= REL * abs(OM.pml(o, rp)) + floor
         assert abs(tvar[q] - OM.tvar_rp(o, rp)[1]) <= REL * abs(OM.tvar_rp(o, rp)[1]) + floor
+
+
+def test_measures_batch_equals_single_calls(A, ctx):
+    # the batched call (one read-back for every table) == one call per table
+    import torch
+    rng = np.random.default_rng(21)
+    L, n, P = 5, 60000, 3
+    y = torch.from_numpy(rng.lognormal(13, 1, (P, L, n // P)).astype(np.float32)).cuda()
+    layers = [0, 3, -1, 4]
+    pml, tvar, var = A.risk_measures_batch(ctx, y, L, n, layers, rps=(100, 250, 500), n_shards=P)
+    for i, layer in enumerate(layers):
+        p1, t1, v1 = A.risk_measures_var(ctx, y, L, n, layer, rps=(100, 250, 500), n_shards=P)
+        assert np.array_equal(pml[i], p1) and np.array_equal(tvar[i], t1) and np.array_equal(var[i], v1)

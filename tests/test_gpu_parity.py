@@ -769,3 +769,20 @@ def test_measures_batch_equals_single_calls(A, ctx):
     for i, layer in enumerate(layers):
         p1, t1, v1 = A.risk_measures_var(ctx, y, L, n, layer, rps=(100, 250, 500), n_shards=P)
         assert np.array_equal(pml[i], p1) and np.array_equal(tvar[i], t1) and np.array_equal(var[i], v1)
+
+
+def test_batch_and_curve_errors(A, ctx):
+    import torch
+    y = torch.ones((2, 100), dtype=torch.float32, device="cuda")
+    with pytest.raises(A.AraError):                   # > 4 return periods
+        A.risk_measures_batch(ctx, y, 2, 100, [0, 1], rps=(2, 3, 4, 5, 6))
+    with pytest.raises(A.AraError):                   # layer out of range
+        A.risk_measures_batch(ctx, y, 2, 100, [0, 2])
+    with pytest.raises(A.AraError):                   # return period <= 1
+        A.risk_measures_batch(ctx, y, 2, 100, [0], rps=(1.0,))
+    with pytest.raises(A.AraError):                   # layer out of range
+        A.exceedance_curve(ctx, y, 2, 100, 3)
+    with pytest.raises(A.AraError):                   # shards must divide n_total
+        A.exceedance_curve(ctx, y, 2, 100, 0, n_shards=3)
+    c = A.exceedance_curve(ctx, y, 2, 100, -1).cpu().numpy()
+    assert (c == 2.0).all()                           # constant roll-up

@@ -345,6 +345,11 @@ def run_ours(args, cfg, rank, world, local):
     compact["traffic"] = cc.get("dram_bytes_per_occurrence", 0) * n_loc * K if cc else None
     if cc.get("ncu"):
         compact["ncu"] = dict(cc["ncu"], source=cc.get("source"))   # L2 hit rate, pipes
+        if cc["ncu"].get("l1_lsu_wavefronts_pct") is not None:
+            # the resource that binds the compaction: the L1 data pipe, not HBM
+            compact["binding"] = {"resource": "L1 data-pipe (LSU) wavefronts",
+                                  "frac": cc["ncu"]["l1_lsu_wavefronts_pct"] / 100.0,
+                                  "source": "ncu capture (profiles/roofline_consts.json)"}
     sample = {"kernel": "sample_kernel", "kernel_ms": t_sample * 1e3, "samples_per_launch": pairs,
               "samples_per_s": pairs / t_sample if t_sample else None}
     sc = consts.get("sample_kernel", {}) if cfg["su"] else {}

@@ -33,6 +33,8 @@ KEYS = [
     "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -110,6 +112,9 @@ def main():
                                      "fma_pipe_pct": pick("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
                                      "alu_pipe_pct": pick("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
                                      "xu_pipe_pct": pick("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+                                     "l1_lsu_wavefronts_pct": pick("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+                                     "l2_throughput_pct": pick("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                                     "dram_throughput_pct": pick("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
                                      "sm_ghz": pick("sm__cycles_elapsed.avg.per_second")},
                              "source": f"profiles/{a.tag}_{short}.json ({os.path.basename(a.rep)})"}
     if a.write_const:

@@ -84,6 +84,14 @@ __device__ __forceinline__ uint32_t philox_lane0_k(uint32_t i, uint32_t k, uint3
 __device__ __forceinline__ double xl_clip_(double d, double lim) {
     return d > 0.0 ? (d < lim ? d : lim) : 0.0;
 }
+template <class T>
+__device__ __forceinline__ T xl_clip_t_(T d, T lim) {
+    return d > (T)0 ? (d < lim ? d : lim) : (T)0;
+}
+#ifndef ARA_RUNSUM_F32
+#define ARA_RUNSUM_F32 1              // in-stretch run sums and occurrence clips in fp32 (G28)
+#endif
+using RunT = std::conditional<ARA_RUNSUM_F32 != 0, float, double>::type;
 
 __device__ __forceinline__ double warp_sum_f64_(double v) {
 #pragma unroll
@@ -547,18 +555,18 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
         // ---- reduce: runs (line 9) and occurrence terms (line 11)
         // (an odd stretch length keeps the lanes' reads on distinct banks)
         const uint32_t per = ((ns + 31) / 32) | 1u, i0 = min(lane * per, ns), i1 = min(i0 + per, ns);
-        double o = 0.0, head = 0.0;
+        RunT o = 0, head = 0;                          // (RunT: the in-stretch run sums)
         bool has_end = false;
         uint32_t head_layer = 0;
-        const double occ_r0 = layers[0].occ_r, occ_l0 = layers[0].occ_l;
+        const RunT occ_r0 = (RunT)layers[0].occ_r, occ_l0 = (RunT)layers[0].occ_l;
 #pragma unroll 2
         for (uint32_t i = i0; i < i1; ++i) {           // branch-free
             const uint32_t q = xs[i];                  // loss bits | run end << 31
-            o += (double)__uint_as_float(q & 0x7fffffffu);
+            o += (RunT)__uint_as_float(q & 0x7fffffffu);
             const bool end = (q >> 31) != 0u;
             const uint32_t lay = SL ? 0u : (uint32_t)fl[i];
-            const double orr = SL ? occ_r0 : layers[lay].occ_r, oll = SL ? occ_l0 : layers[lay].occ_l;
-            const double g = xl_clip_(o - orr, oll);
+            const RunT orr = SL ? occ_r0 : (RunT)layers[lay].occ_r, oll = SL ? occ_l0 : (RunT)layers[lay].occ_l;
+            const double g = (double)xl_clip_t_(o - orr, oll);
             const bool first = end && !has_end, inner = end && has_end;
             head = first ? o : head;
             head_layer = first ? lay : head_layer;
@@ -569,7 +577,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 else if (inner) W.mos[lay * 32] = fmaxf(W.mos[lay * 32], (float)g);
             }
             has_end = has_end || end;
-            o = end ? 0.0 : o;
+            o = end ? (RunT)0 : o;
         }
         // join the runs that cross stretches: exclusive segmented sum over
         // lanes of the open tails (a lane with a run end starts a segment)

@@ -34,6 +34,9 @@ namespace {
 #ifndef ARA_COMPACT_PREFETCH
 #define ARA_COMPACT_PREFETCH 0        // bulk L2 prefetch of each warp's next trial of YET (measured: no gain)
 #endif
+#ifndef ARA_CIDX_CG
+#define ARA_CIDX_CG 1                 // index-entry gathers through L2 only (ld.global.cg): no L1 reuse
+#endif
 #ifndef ARA_COMPACT_BALLOT_SCAN
 #define ARA_COMPACT_BALLOT_SCAN 1     // pair prefix sums by ballots instead of shuffles
 #endif
@@ -218,7 +221,11 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
             if (BM == 2) hit = hit && k0 + q < r.len;
             S.ci[q] = make_uint2(0u, 0u);
             asm volatile(                                 // predicated load, no branch
+#if ARA_CIDX_CG
+                "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.cg.v2.u32 {%0, %1}, [%3];\n}"
+#else
                 "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.nc.v2.u32 {%0, %1}, [%3];\n}"
+#endif
                 : "+r"(S.ci[q].x), "+r"(S.ci[q].y)
                 : "r"((uint32_t)hit), "l"(cidx + ee[q]));
         }

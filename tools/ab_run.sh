@@ -1,1 +1,2 @@
-bash tools/ab_bench.sh cfg3 gpurun_variants/s96.so gpurun_variants/s64.so gpurun_variants/s80.so gpurun_variants/s128.so gpurun_variants/s96.so gpurun_variants/s64.so gpurun_variants/s80.so
+ARA_LIB_PATH=$PWD/gpurun_variants/q1.so timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -1
+bash tools/ab_bench.sh cfg3 gpurun_variants/q0.so gpurun_variants/q1.so gpurun_variants/q0.so gpurun_variants/q1.so

@@ -1,2 +1,2 @@
-ARA_LIB_PATH=$PWD/gpurun_variants/q1.so timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -1
-bash tools/ab_bench.sh cfg3 gpurun_variants/q0.so gpurun_variants/q1.so gpurun_variants/q0.so gpurun_variants/q1.so
+ARA_LIB_PATH=$PWD/gpurun_variants/l1.so timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -1
+bash tools/ab_bench.sh cfg3 gpurun_variants/l0.so gpurun_variants/l1.so gpurun_variants/l0.so gpurun_variants/l1.so

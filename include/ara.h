@@ -300,6 +300,22 @@ int ara_sample_losses(ara_ctx *ctx, uint64_t n, const ara_record *records,
                       const float *z_prog, const float *z_event, uint32_t flags,
                       float *loss_out);
 
+/* Row a6's fp64 beta quantile on its own (readings G11-G13):
+ * for each i, x_i = I^-1(Phi(v_i); alpha_i, beta_i), the x in (0,1) with
+ * I_x(alpha, beta) = Phi(v), by the device's per-sample fp64 solve (the one
+ * that builds the quantile tables and serves ARA_EXACT: Halley iteration on
+ * the log of the matched tail in lambda = logit x, tails from the Gauss
+ * hypergeometric series of DLMF 8.17.8).  x_out[i] = x and y_out[i] = 1 - x,
+ * each to full relative precision (so both tails can be checked).
+ *   alpha, beta  host [n], finite and > 0 (the sigma_beta-capped regime,
+ *                ~1e-6, included)
+ *   v            host [n], finite (the normal score of step 5)
+ *   x_out, y_out host [n]
+ * ARA_EINVAL on bad values; ARA_ECONVERGE (outputs written) if a solve did
+ * not converge. */
+int ara_beta_quantiles(ara_ctx *ctx, uint64_t n, const double *alpha, const double *beta, const double *v,
+                       double *x_out, double *y_out);
+
 /* The uniforms the path draws (reading G2/G4): for each of n (trial i,
  * occurrence k, id, tag) counters, U(lane 0 of Philox4x32-10(seed, ctr)).
  * ctr: host [n][4] uint32 (i, k, program-or-XELT id, tag 1|2); out host [n]. */

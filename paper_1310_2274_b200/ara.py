@@ -38,7 +38,7 @@ EXPORTS = (
     "ara_load_yet",
     "ara_yet_refill", "ara_yet_refill_packed", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings", "ara_risk_measures_var", "ara_risk_measures_batch", "ara_exceedance_curve",
     "ara_risk_measures",
-    "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles",
+    "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles", "ara_beta_quantiles",
 )
 
 
@@ -79,6 +79,7 @@ def _load():
     L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, u32, vp]
     L.ara_draw_uniforms.argtypes = [vp, u64, u64, vp, vp]
     L.ara_normal_quantiles.argtypes = [vp, u64, vp, vp]
+    L.ara_beta_quantiles.argtypes = [vp, u64, vp, vp, vp, vp, vp]
     for n in EXPORTS:            # fail loudly if an entry point is missing
         getattr(L, n)
     return L
@@ -370,3 +371,15 @@ def normal_quantiles(ctx: Context, bits):
     out = np.empty(len(b), np.float32)
     _check(lib.ara_normal_quantiles(ctx.h, len(b), _p(b), _p(out)))
     return out
+
+
+def beta_quantiles(ctx: Context, alpha, beta, v):
+    """ara_beta_quantiles: (x, 1 - x) with I_x(alpha, beta) = Phi(v), by the
+    device's fp64 solve (row a6 on its own)."""
+    a = np.ascontiguousarray(alpha, np.float64).ravel()
+    b = np.ascontiguousarray(np.broadcast_to(beta, a.shape), np.float64).ravel()
+    w = np.ascontiguousarray(np.broadcast_to(v, a.shape), np.float64).ravel()
+    x = np.empty(len(a), np.float64)
+    y = np.empty(len(a), np.float64)
+    _check(lib.ara_beta_quantiles(ctx.h, len(a), _p(a), _p(b), _p(w), _p(x), _p(y)))
+    return x, y

@@ -927,6 +927,39 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
     return code;
 }
 
+int ara_beta_quantiles(ara_ctx *c, uint64_t n, const double *alpha, const double *beta, const double *v,
+                       double *x_out, double *y_out) {
+    if (!c) return fail(ARA_EINVAL, "ctx is NULL");
+    if (n == 0) return ARA_OK;
+    if (!alpha || !beta || !v || !x_out || !y_out) return fail(ARA_EINVAL, "NULL argument");
+    for (uint64_t t = 0; t < n; ++t)
+        if (!(alpha[t] > 0.0 && beta[t] > 0.0 && std::isfinite(alpha[t]) && std::isfinite(beta[t]) &&
+              std::isfinite(v[t])))
+            return fail(ARA_EINVAL, "need finite alpha, beta > 0 and finite v (index %llu)", (unsigned long long)t);
+    CU(cudaSetDevice(c->device));
+    double *d = nullptr;
+    int code = ARA_OK;
+    if (dalloc(&d, 5 * n)) {
+        cudaGetLastError();
+        return fail(ARA_ENOMEM, "device allocation failed");
+    }
+    cudaStream_t s = c->stream;
+    cudaError_t e = cudaMemcpyAsync(d, alpha, n * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyAsync(d + n, beta, n * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyAsync(d + 2 * n, v, n * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
+    if (!e) e = launch_beta_quantiles(d, d + n, d + 2 * n, n, d + 3 * n, d + 4 * n, c->d_status, s);
+    if (!e) e = cudaMemcpyAsync(x_out, d + 3 * n, n * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaMemcpyAsync(y_out, d + 4 * n, n * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e) code = fail(ARA_ECUDA, "ara_beta_quantiles: %s", cudaGetErrorString(e));
+    else if (c->h_status->nonconverged)
+        code = fail(ARA_ECONVERGE, "beta quantile did not converge for %u values", c->h_status->nonconverged);
+    cudaFree(d);
+    return code;
+}
+
 int ara_draw_uniforms(ara_ctx *c, uint64_t seed, uint64_t n, const uint32_t *ctr, float *u_out) {
     if (!c) return fail(ARA_EINVAL, "ctx is NULL");
     if (n == 0) return ARA_OK;

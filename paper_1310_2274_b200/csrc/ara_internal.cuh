@@ -158,6 +158,8 @@ cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, cons
                                  const float *ze, uint64_t n, bool exact, float *out,
                                  RunStatus *status, cudaStream_t s);
 cudaError_t launch_normal_quantiles(const uint32_t *bits, uint64_t n, float *out, cudaStream_t s);
+cudaError_t launch_beta_quantiles(const double *a, const double *b, const double *v, uint64_t n, double *x_out,
+                                  double *y_out, RunStatus *status, cudaStream_t s);
 cudaError_t launch_draw_uniforms(uint64_t seed, const uint4 *ctr, uint64_t n, float *out,
                                  cudaStream_t s);
 

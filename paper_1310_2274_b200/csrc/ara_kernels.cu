@@ -80,7 +80,9 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
                 const double v = kTabV0 + kTabH * j;
                 bool ok;
                 const double l = lambda_exact64(v, a, b, lnB, guess, ok);
-                const Tail64 e = tail64(l, v <= 0.0, a, b, lnB);
+                bool sok;
+                const Tail64 e = tail64(l, v <= 0.0, a, b, lnB, sok);
+                ok = ok && sok;
                 const double lnd = -0.5 * v * v - LN_SQRT_2PI + lnB - a * e.lnx - b * e.lny;
                 const double d = exp(lnd);
                 lam[j] = l; d1[j] = d;
@@ -744,6 +746,32 @@ cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, cons
     const uint64_t blocks = (n + 255) / 256;
     sample_losses_kernel<<<(unsigned)(blocks < 1u << 20 ? blocks : 1u << 20), 256, 0, s>>>(
         recs, tables, hot, zp, ze, n, exact, out, status);
+    return cudaGetLastError();
+}
+
+// Row a6's fp64 solver alone (ara_beta_quantiles): x = I^-1(Phi(v); a, b)
+// and y = 1 - x, both from lambda = logit x (full relative precision each)
+__global__ void beta_quantiles_kernel(const double *a_, const double *b_, const double *v_, uint64_t n,
+                                      double *x_out, double *y_out, RunStatus *status) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const double a = a_[t], b = b_[t], v = v_[t];
+        const double lnB = lgamma(a) + lgamma(b) - lgamma(a + b);
+        const double lam0 = (digamma_d(a) - digamma_d(b)) + v * sqrt(trigamma_d(a) + trigamma_d(b));
+        bool ok;
+        const double lam = lambda_exact64(v, a, b, lnB, lam0, ok);
+        x_out[t] = 1.0 / (1.0 + exp(-lam));
+        y_out[t] = 1.0 / (1.0 + exp(lam));
+        if (!ok) atomicAdd(&status->nonconverged, 1u);
+    }
+}
+
+cudaError_t launch_beta_quantiles(const double *a, const double *b, const double *v, uint64_t n, double *x_out,
+                                  double *y_out, RunStatus *status, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t blocks = (n + 127) / 128;
+    beta_quantiles_kernel<<<(unsigned)(blocks < 1u << 20 ? blocks : 1u << 20), 128, 0, s>>>(a, b, v, n, x_out,
+                                                                                            y_out, status);
     return cudaGetLastError();
 }
 

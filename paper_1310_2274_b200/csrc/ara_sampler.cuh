@@ -20,9 +20,9 @@
 //
 // The fp64 solver: Halley iteration on ln(tail) as a function of lambda, so
 // x and 1-x keep full relative precision and both tails are near-linear;
-// the tail from the continued fraction of DLMF 8.17.22 (modified Lentz),
-// on whichever of I_x(a,b) / I_{1-x}(b,a) converges fast; the smaller tail
-// t = Phi(-|v|) is matched directly (reading G13).
+// the tail from the positive-term Gauss hypergeometric series of DLMF 8.17.8,
+// on whichever of I_x(a,b) / I_{1-x}(b,a) sits below its switch point; the
+// smaller tail t = Phi(-|v|) is matched directly (reading G13).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -102,24 +102,27 @@ __device__ __forceinline__ float combine_v(const BetaRec &r, float vp, float ve)
 }
 
 // -------------------------------------------------------- fp64 solver ----
-__device__ __forceinline__ double betacf64(double x, double a, double b) {
-    // returns 1/(1 + d1/(1 + d2/(1 + ...))) (DLMF 8.17.22), modified Lentz
-    const double tiny = 1e-300;
-    double f = 1.0, C = 1.0, D = 0.0;
-    for (int n = 1; n < 20000; ++n) {
-        const double m = (double)(n >> 1);
-        const double d = (n & 1) ? -((a + m) * (a + b + m) * x) / ((a + 2.0 * m) * (a + 2.0 * m + 1.0))
-                                 : (m * (b - m) * x) / ((a + 2.0 * m - 1.0) * (a + 2.0 * m));
-        D = 1.0 + d * D;
-        if (fabs(D) < tiny) D = tiny;
-        C = 1.0 + d / C;
-        if (fabs(C) < tiny) C = tiny;
-        D = 1.0 / D;
-        const double delta = C * D;
-        f *= delta;
-        if (fabs(delta - 1.0) < 1e-15) break;
+// ln F(a+b, 1; a+1; x) = ln sum_{n>=0} (a+b)_n / (a+1)_n x^n, the Gauss
+// hypergeometric factor of I_x(a,b) = x^a (1-x)^b / (a B(a,b)) F(a+b,1;a+1;x)
+// (DLMF 8.17.8).  Every term is positive (no cancellation) and, for
+// x < (a+1)/(a+b+2), the term ratio (a+b+n) x / (a+1+n) stays below
+// rmax = max((a+b) x / (a+1), x) < 1, so the series is summed until the next
+// term cannot move the sum: t rmax / (1 - rmax) <= 2^-54 s.  ok = false if
+// that takes more than 400000 terms (ratio within ~1e-4 of 1).
+__device__ __forceinline__ double hyp2f1_ln64(double x, double a, double b, bool &ok) {
+    const double r0 = (a + b) * x / (a + 1.0);
+    const double rmax = fmax(r0, x);
+    const double stop = 5.551115123125783e-17 * (1.0 - rmax) / rmax;
+    double t = 1.0, s = 1.0, num = a + b, den = a + 1.0;
+    ok = false;
+    for (int n = 0; n < 400000; ++n) {
+        t *= num * x / den;
+        s += t;
+        num += 1.0;
+        den += 1.0;
+        if (t <= stop * s) { ok = true; break; }
     }
-    return 1.0 / f;
+    return log(s);
 }
 
 struct Tail64 {
@@ -127,7 +130,7 @@ struct Tail64 {
 };
 
 // ln of the matched tail (P = I_x(a,b) if lower, else Q = 1 - P) at lambda = logit x
-__device__ __forceinline__ Tail64 tail64(double lam, bool lower, double a, double b, double lnB) {
+__device__ __forceinline__ Tail64 tail64(double lam, bool lower, double a, double b, double lnB, bool &ok) {
     Tail64 r;
     const double e = exp(-fabs(lam));
     const double sp = log1p(e);                            // softplus(-|lam|)
@@ -135,9 +138,13 @@ __device__ __forceinline__ Tail64 tail64(double lam, bool lower, double a, doubl
     const double lny = lam >= 0.0 ? -lam - sp : -sp;
     const double x = exp(lnx), y = exp(lny);
     const double phi = a * lnx + b * lny - lnB;            // ln(x^a y^b / B)
+    // the series for I_x(a,b) below (a+1)/(a+b+2), else the one for
+    // I_y(b,a) = 1 - I_x(a,b).  The other tail, 1 - G, is only the matched one
+    // near that switch point (the bulk of the distribution), where it is not
+    // small, so log1p(-G) loses no relative precision
     const bool direct = x < (a + 1.0) / (a + b + 2.0);
-    const double cf = direct ? betacf64(x, a, b) : betacf64(y, b, a);
-    const double lnG = phi + log(cf / (direct ? a : b));
+    const double lnF = direct ? hyp2f1_ln64(x, a, b, ok) : hyp2f1_ln64(y, b, a, ok);
+    const double lnG = phi + lnF - log(direct ? a : b);
     const double G = exp(lnG);
     const double lnOther = log1p(-fmin(G, 1.0));
     r.lnT = lower ? (direct ? lnG : lnOther) : (direct ? lnOther : lnG);
@@ -153,8 +160,11 @@ __device__ __forceinline__ double solve_logit64(double lnt, bool lower, double a
                                                 double lnB, double lam, bool &ok) {
     double lo = -INFINITY, hi = INFINITY;
     ok = false;
+    bool series_ok = true;
     for (int it = 0; it < 300; ++it) {
-        const Tail64 e = tail64(lam, lower, a, b, lnB);
+        bool sok;
+        const Tail64 e = tail64(lam, lower, a, b, lnB, sok);
+        series_ok = series_ok && sok;
         const double g = e.lnT - lnt;
         if (g == 0.0) { ok = true; break; }
         const bool toolow = lower ? (g < 0.0) : (g > 0.0);
@@ -171,6 +181,7 @@ __device__ __forceinline__ double solve_logit64(double lnt, bool lower, double a
         lam = nl;
         if (conv) { ok = true; break; }
     }
+    ok = ok && series_ok;
     return lam;
 }
 

@@ -243,7 +243,9 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
 #if ARA_COMPACT_BALLOT_SCAN
         // exclusive warp prefix of np, bit-sliced over ballots (votes, no
         // shuffles through the shared-memory pipe): 3 slices unless some
-        // lane has >= 8 pairs in the chunk (np <= 64)
+        // lane has >= 8 pairs in the chunk; np <= 4 * ARA_MAX_SLOTS = 896
+        // < 2^10, so 10 slices cover every case
+        static_assert(4 * ARA_MAX_SLOTS < (1 << 10), "pair count of a lane's 4 events must fit 10 bits");
         uint32_t excl = 0, tot = 0;
         const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
@@ -254,7 +256,7 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         }
         if (__any_sync(0xffffffffu, np > 7u)) {
 #pragma unroll 1
-            for (int b = 3; b < 7; ++b) {
+            for (int b = 3; b < 10; ++b) {
                 const uint32_t m = __ballot_sync(0xffffffffu, (np >> b) & 1u);
                 excl += (uint32_t)__popc(m & lt) << b;
                 tot += (uint32_t)__popc(m) << b;

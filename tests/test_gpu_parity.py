@@ -135,6 +135,61 @@ def test_sampler_exact_mode_vs_oracle(A, ctx):
     assert (np.abs(t - g) <= 1e-5 * g + 1e-8 * mx).all()          # table vs exact solve
 
 
+def _gen_alpha_beta(n):
+    # the generator's records -> (alpha, beta) by P:229-236 in numpy (uncapped range)
+    recs = gen_records(n)
+    mu, mx = recs["mean_loss"].astype(np.float64), recs["max_loss"].astype(np.float64)
+    sig = recs["sigma_i"].astype(np.float64) + recs["sigma_c"].astype(np.float64)
+    mb, sb = mu / mx, sig / mx
+    k = mb * (1 - mb) / sb ** 2 - 1
+    return mb * k, (1 - mb) * k
+
+
+def test_fp64_solver_vs_scipy(A, ctx):
+    # row a6's device fp64 solve (it builds every quantile table and serves
+    # ARA_EXACT) pinned directly to scipy's betaincinv -- not to the oracle --
+    # over the generator's (alpha, beta) range and v in [-7.5, 7.5]; both x
+    # and 1 - x to full relative precision
+    import scipy.special as sp
+    a, b = _gen_alpha_beta(6000)
+    rng = np.random.default_rng(11)
+    v = np.concatenate([rng.uniform(-7.5, 7.5, a.size - 8), [-7.5, -5, -1e-3, 0.0, 1e-3, 3, 5, 7.5]])
+    x, y = A.beta_quantiles(ctx, a, b, v)
+    lo = v <= 0
+    xr = sp.betaincinv(a[lo], b[lo], sp.ndtr(v[lo]))
+    yr = sp.betaincinv(b[~lo], a[~lo], sp.ndtr(-v[~lo]))
+    np.testing.assert_allclose(x[lo], xr, rtol=1e-10, atol=0)
+    np.testing.assert_allclose(y[~lo], yr, rtol=1e-10, atol=0)
+    np.testing.assert_allclose(x + y, 1.0, rtol=0, atol=4e-16)
+    # closed forms: Beta(a,1) -> p^(1/a); Beta(1,b) -> 1-(1-p)^(1/b); Beta(1/2,1/2) -> sin^2(pi p/2)
+    vv = np.linspace(-6, 6, 41)
+    p, q = sp.ndtr(vv), sp.ndtr(-vv)
+    for aa in (0.3, 2.5, 40.0):
+        x1, y1 = A.beta_quantiles(ctx, np.full(vv.size, aa), 1.0, vv)
+        np.testing.assert_allclose(x1[vv <= 0], p[vv <= 0] ** (1 / aa), rtol=1e-11)
+        np.testing.assert_allclose(y1[vv > 0], -np.expm1(np.log1p(-q[vv > 0]) / aa), rtol=1e-10)
+    x2, _ = A.beta_quantiles(ctx, np.full(vv.size, 0.5), 0.5, vv)
+    np.testing.assert_allclose(x2[vv <= 0], np.sin(np.pi * p[vv <= 0] / 2) ** 2, rtol=1e-11)
+
+
+def test_fp64_solver_cap_regime_vs_mpmath(A, ctx):
+    # the sigma_beta-capped regime (G9): alpha, beta in [1e-6, 1e-3],
+    # a near-Bernoulli law; x and 1 - x against an mpmath bisection on I_x
+    import scipy.special as sp
+    from mp_pins import mp_lower_quantile
+    cases = [(a_, b_, v_) for a_, b_ in [(1e-3, 1e-3), (5e-4, 1e-3), (2e-6, 1e-6), (1e-3, 3e-6)]
+             for v_ in (-3.0, -0.5, -0.01, 0.02, 0.4, 2.5)]
+    a, b, v = (np.array(c, np.float64) for c in zip(*cases))
+    x, y = A.beta_quantiles(ctx, a, b, v)
+    for t in range(len(cases)):
+        if v[t] <= 0:
+            ref = mp_lower_quantile(float(sp.ndtr(v[t])), a[t], b[t])
+            assert x[t] == pytest.approx(ref, rel=1e-9, abs=1e-305), (cases[t], x[t], ref)
+        else:
+            ref = mp_lower_quantile(float(sp.ndtr(-v[t])), b[t], a[t])
+            assert y[t] == pytest.approx(ref, rel=1e-9, abs=1e-305), (cases[t], y[t], ref)
+
+
 def test_capped_records_fall_back_to_exact(A, ctx):
     # records at the sigma_beta cap (G9: alpha, beta ~ 1e-6) are near-Bernoulli;
     # their table fails the midpoint check and the scan uses the fp64 solve
@@ -244,6 +299,23 @@ def test_multi_layer_and_wide_masks(A, ctx, n_layers, J):
     pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
     pf["layer_prog"] = (np.arange(n_layers) % 3).astype(np.uint32)    # several programs (G26)
     (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, 77)
+    assert np.array_equal(cnt, ref["count"]) and np.array_equal(hsh, ref["hash"])
+    for li in range(n_layers):
+        ylt_check(g[li], ref, li)
+
+
+@pytest.mark.parametrize("n_layers,J", [(8, 16), (1, 224)])
+def test_heavy_overlap_many_pairs_per_lane(A, ctx, n_layers, J):
+    # every XELT holds half the catalogue: a lane's 4 events carry up to
+    # 4 x 224 = 896 pairs (> 127: every bit slice of the compaction's ballot
+    # prefix sum is exercised); counts, hashes and YLT against the oracle
+    cfg = aragen.load_config("cfg1")
+    terms = [[2e5 * (l + 1), 5e6, 1.0e6, 5.0e9] for l in range(n_layers)]
+    cfg.update(n_layers=n_layers, elts_per_layer=J, catalog=1000, records_per_elt=500,
+               n_trials=60, events_per_trial=64, layer_terms=terms)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, 17)
+    assert cnt.sum(0).max() > 64 * 0.5 * n_layers * J * 0.8        # ~half of all slots present
     assert np.array_equal(cnt, ref["count"]) and np.array_equal(hsh, ref["hash"])
     for li in range(n_layers):
         ylt_check(g[li], ref, li)
@@ -441,9 +513,30 @@ def test_measures_errors(A, ctx):
     assert pml[0] == 0 and tvar[0] == 0
 
 
-# ---- full-size configurations, sampled ---------------------------------------
-@pytest.mark.parametrize("name,n_sample", [("cfg2", 300), ("cfg3", 300)])
-def test_full_size_sampled(A, ctx, name, n_sample):
+# ---- full-size configurations: every trial against the oracle ----------------
+def _measures_pure_rel(A, ctx, ylt_dev, ref_ylt, L, N, layers, rps, shards=1):
+    """PML / TVaR of each side from its own YLT: pure 1e-4 relative."""
+    for layer in layers:
+        pml, tvar = A.risk_measures(ctx, ylt_dev, L, N, layer, rps=rps, n_shards=shards)
+        o = OM.rollup(ref_ylt) if layer < 0 else ref_ylt[layer]
+        for q, rp in enumerate(rps):
+            po, to = OM.pml(o, rp), OM.tvar_rp(o, rp)[1]
+            assert abs(pml[q] - po) <= REL * abs(po), (layer, rp, pml[q], po)
+            assert abs(tvar[q] - to) <= REL * abs(to), (layer, rp, tvar[q], to)
+
+
+def _pure_fraction(g, o):
+    nz = o > 0
+    return float((np.abs(g[nz] - o[nz]) <= REL * o[nz]).mean()) if nz.any() else 1.0
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_full_size_every_trial(A, ctx, name):
+    # BASELINE's own sizes: cfg3 = the paper's headline run (800k trials x
+    # 1,000 events x 16 XELTs, SU on) and cfg2 (100k x 1,000, 2M catalogue,
+    # sigma = 0): the GPU YLT of EVERY trial against the fp64 oracle run over
+    # all trials (the north star's acceptance), lookup counts bit-exact, and
+    # PML / TVaR at 1-in-100/250/500 at pure 1e-4 relative
     import torch
     cfg = aragen.load_config(name)
     pf = aragen.build_portfolio(cfg)
@@ -452,45 +545,40 @@ def test_full_size_sampled(A, ctx, name, n_sample):
     yet = aragen.build_yet(cfg, out=ev.numpy().view(np.uint32))
     P = A.Portfolio(ctx, pf)
     Y = A.Yet(ctx, ev, fixed_len=K, n_trials=N)
-    ylt = A.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"]).cpu().numpy()
+    ylt_d, cnt, _ = A.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"], debug=True)
+    ylt = ylt_d.cpu().numpy()
+    ref = oracle.run(pf, yet, seed=cfg["seed"], su=cfg["su"])
+    assert np.array_equal(cnt.cpu().numpy().astype(np.uint32), ref["count"])
+    ylt_check(ylt, ref)
+    assert _pure_fraction(ylt[0].astype(np.float64), ref["ylt"][0]) > 0.999
     lim = pf["layer_terms"][0][3]
     assert (ylt >= 0).all() and (ylt <= lim).all()
-    rng = np.random.default_rng(123)
-    idx = np.sort(rng.choice(N, n_sample, replace=False))
-    idx[0], idx[-1] = 0, N - 1
-    sub = aragen.yet_for_trials(cfg, idx)
-    ref = oracle.run(pf, sub, seed=cfg["seed"], su=cfg["su"], trial_index=sub["trial_index"])
-    ylt_check(ylt[:, idx], ref)
-    # measures at full size: properties only (end-to-end parity of PML/TVaR is
-    # test_measures_end_to_end, where the oracle computes every trial)
-    pml, tvar = A.risk_measures(ctx, torch.from_numpy(ylt).cuda(), 1, N, 0, rps=cfg["return_periods"])
-    assert (np.diff(pml) >= 0).all() and (np.diff(tvar) >= 0).all()
-    assert (tvar >= pml * (1 - 1e-6)).all() and (tvar <= lim).all()
+    _measures_pure_rel(A, ctx, ylt_d, ref["ylt"], 1, N, [0], cfg["return_periods"])
 
 
-def test_cfg5_rank_shard_sampled(A, ctx):
-    # cfg5 as one of 8 ranks holds it: global trials [875000, 1000000) of the
+def test_cfg5_rank_shard_every_trial(A, ctx):
+    # cfg5 as rank 7 of 8 holds it: global trials [875000, 1000000) of the
     # 1M-trial, 8-layer x 16-XELT, 2M-event analysis at full portfolio size;
-    # every layer of 60 sampled trials (incl. the shard's first and last)
-    # against the oracle, computed trial by trial with the global indices
+    # every layer of every trial of the shard against the oracle (global
+    # trial indices), then the shard's per-layer and roll-up measures at pure
+    # 1e-4 relative
     import torch
     cfg = aragen.load_config("cfg5")
     pf = aragen.build_portfolio(cfg)
     N, K, L = cfg["n_trials"], cfg["events_per_trial"], cfg["n_layers"]
     lo, n = 7 * N // 8, N // 8
     ev = torch.empty(n * K, dtype=torch.int32).pin_memory()
-    aragen.build_yet(cfg, first_trial=lo, n_trials=n, out=ev.numpy().view(np.uint32))
+    yet = aragen.build_yet(cfg, first_trial=lo, n_trials=n, out=ev.numpy().view(np.uint32))
     P = A.Portfolio(ctx, pf)
     Y = A.Yet(ctx, ev, fixed_len=K, first_trial=lo, n_trials=n)
-    ylt = A.run(ctx, P, Y, seed=cfg["seed"], su=True).cpu().numpy()
+    ylt_d = A.run(ctx, P, Y, seed=cfg["seed"], su=True)
+    ylt = ylt_d.cpu().numpy()
     assert ylt.shape == (L, n)
-    rng = np.random.default_rng(5)
-    loc = np.sort(rng.choice(n, 60, replace=False))
-    loc[0], loc[-1] = 0, n - 1
-    sub = aragen.yet_for_trials(cfg, loc + lo)
-    ref = oracle.run(pf, sub, seed=cfg["seed"], su=True, trial_index=sub["trial_index"])
+    ref = oracle.run(pf, yet, seed=cfg["seed"], su=True,
+                     trial_index=np.arange(lo, lo + n, dtype=np.uint64))
     for li in range(L):
-        ylt_check(ylt[li, loc], ref, li)
+        ylt_check(ylt[li], ref, li)
+    _measures_pure_rel(A, ctx, ylt_d, ref["ylt"], L, n, [0, L - 1, -1], cfg["return_periods"])
 
 
 @pytest.mark.parametrize("name,n", [("cfg1", None), ("cfg3", 20000), ("cfg5", 4000)])

@@ -146,3 +146,42 @@ def test_sample_distribution_mean_sd_ks(rec):
     a, b = O.beta_params(mu, sd, mx)
     assert st.kstest(x / mx, st.beta(a, b).cdf).pvalue > 1e-4
     assert (x >= 0).all() and (x <= mx).all()
+
+
+# ---- the sigma_beta cap regime (reading G9): alpha, beta in [1e-6, 1e-3] --
+from mp_pins import mp_lower_quantile as _mp_lower_quantile  # noqa: E402
+
+
+@pytest.mark.parametrize("a,b", [(1e-3, 1e-3), (5e-4, 1e-3), (1e-4, 3e-4), (2e-6, 1e-6), (1e-6, 1e-6),
+                                 (1e-3, 3e-6)])
+def test_quantile_cap_regime_vs_mpmath(a, b):
+    # lower tail: the oracle's Newton/bisection against mpmath's I_x; values
+    # far below 1e-300 round to 0 on both sides (the near-Bernoulli step)
+    for p in (1e-3, 0.05, 0.3, 0.45, 0.49, 0.55, 0.7, 0.99):
+        lower_mass = b / (a + b)                 # P(X -> 0) of the limiting Bernoulli
+        if p < lower_mass:                       # solve directly (G13: z <= 1/2 side)
+            x = O.beta_quantile(p, a, b)
+            ref = _mp_lower_quantile(p, a, b)
+            assert x == pytest.approx(ref, rel=1e-10, abs=1e-305), (a, b, p, x, ref)
+        else:                                    # complementary equation I_y(b, a) = 1 - p
+            y = O.beta_quantile(1.0 - p, b, a)
+            ref = _mp_lower_quantile(1.0 - p, b, a)
+            assert y == pytest.approx(ref, rel=1e-10, abs=1e-305), (a, b, p, y, ref)
+
+
+def test_sample_loss_capped_records_vs_mpmath():
+    # capped records (sigma >= sigma_max): the loss is max_l * x with
+    # (alpha, beta) ~ 2e-6 (mu_beta, 1 - mu_beta); a near-Bernoulli draw whose
+    # value is 0 / max_l except within ~1e-5 of the step -- each against mpmath
+    for mu, si, sc, mx in [(30.0, 80.0, 0.0, 100.0), (50.0, 40.0, 30.0, 100.0), (80.0, 10.0, 90.0, 100.0),
+                           (2.0e5, 3.0e5, 1.0e5, 1.0e6)]:
+        a, b = O.beta_params(mu, si + sc, mx)
+        assert 0 < a < 1e-5 and 0 < b < 1e-5
+        for zp, ze in [(0.1, 0.2), (0.5, 0.5), (0.9, 0.3), (0.99, 0.95), (0.02, 0.97)]:
+            got = O.sample_loss(mu, si, sc, mx, zp, ze)
+            _, z, q = O.combine(zp, ze, si, sc)
+            if z <= 0.5:
+                ref = mx * _mp_lower_quantile(z, a, b)
+            else:
+                ref = mx * (1.0 - _mp_lower_quantile(q, b, a))
+            assert got == pytest.approx(ref, rel=1e-10, abs=1e-300 * mx), (mu, si, sc, zp, ze, got, ref)

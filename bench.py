@@ -66,6 +66,47 @@ def shard_range(n_total, rank, world):
     return lo, hi
 
 
+def gather_ylt(ylt, world, n_total, gathered=None, padded=None):
+    """The one exchange step of the multi-GPU path: all-gather
+    the ranks' YLT shards [L][n_r] (rank r holds global trials
+    shard_range(n_total, r, world)) -> (table, n_shards) for the measures.
+
+    Equal shards: the concatenation [P*L][N/P] == the [P][L][N/P] layout
+    ara_risk_measures takes with n_shards = P (the measures are
+    permutation-invariant), no copy.  Unequal shards (n_total % P != 0): every
+    shard is padded to the largest, gathered, and the pads dropped ->
+    [L][n_total] in global trial order, n_shards = 1.  Collective:
+    torch.distributed.all_gather_into_tensor (NCCL on GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return ylt, 1
+    L, n = ylt.shape
+    sizes = [shard_range(n_total, r, world) for r in range(world)]
+    sizes = [hi - lo for lo, hi in sizes]
+    nmax = max(sizes)
+    if gathered is None:
+        gathered = torch.empty((world * L, nmax), dtype=ylt.dtype, device=ylt.device)
+    if min(sizes) == nmax:
+        dist.all_gather_into_tensor(gathered, ylt.contiguous())
+        return gathered, world
+    if padded is None:
+        padded = torch.zeros((L, nmax), dtype=ylt.dtype, device=ylt.device)
+    padded[:, :n] = ylt
+    dist.all_gather_into_tensor(gathered, padded)
+    parts = [gathered[r * L:(r + 1) * L, :sizes[r]] for r in range(world)]
+    return torch.cat(parts, dim=1).contiguous(), 1
+
+
+def launch_command(gpus, argv, port=None):
+    """The command `bench.py --gpus N` re-executes itself under when started
+    without a torchrun environment: one process per GPU (torch.distributed.run,
+    rendezvous on 127.0.0.1)."""
+    port = port or 29500 + (os.getpid() % 1000)
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
 def workload_name(cfg):
     return (f"{cfg['name']}: {cfg['n_trials']} trials x {cfg['events_per_trial']} events, "
             f"{cfg['n_layers']} layer(s) x {cfg['elts_per_layer']} XELTs, catalog {cfg['catalog']}, "
@@ -177,6 +218,19 @@ def run_reference(args, cfg, rank, world):
 
 
 # ---------------------------------------------------------------------------
+ALG_INST_PER_SAMPLE = 300     # the ALU floor's algorithmic lane-instructions per SU sample
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_ours(args, cfg, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -210,38 +264,34 @@ def run_ours(args, cfg, rank, world, local):
     aragen.build_yet(cfg, first_trial=lo, n_trials=n_loc, out=ev_host.numpy().view(np.uint32))
     Y = ara.Yet(ctx, ev_host, fixed_len=K, first_trial=lo, n_trials=n_loc)
     ylt = torch.empty((L, n_loc), dtype=torch.float32, device=dev)
-    # all-gather in concatenation form [P*L][N/P] == the [P][L][N/P] layout of ara_risk_measures
-    gathered = torch.empty((world * L, n_loc), dtype=torch.float32, device=dev) if world > 1 else None
+    nmax = max(hi_ - lo_ for lo_, hi_ in (shard_range(N_total, r, world) for r in range(world)))
+    gathered = torch.empty((world * L, nmax), dtype=torch.float32, device=dev) if world > 1 else None
+    padded = torch.zeros((L, nmax), dtype=torch.float32, device=dev) if world > 1 else None
     layers = list(range(L)) + ([-1] if L > 1 else [])
     ylt_host = torch.empty((L, n_loc), dtype=torch.float32).pin_memory()
+    ara.prepare(ctx, P, Y, su=cfg["su"])        # every ara_run scratch buffer, allocated once here
 
-    scan_ms = []
-    kern_ms = []          # per-kernel CUDA-event times of each timed ara_run (ara_last_run_timings)
+    kern_ms = []          # per-kernel CUDA-event sums of each timed ara_run (ara_last_run_timings)
 
-    def step(timed_scan=False):
-        if timed_scan:
-            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        ara.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"], ylt=ylt)
-        if timed_scan:
-            e1.record(stream)
-            scan_ms.append((e0, e1))
-            kern_ms.append(ara.last_run_timings(ctx))
-        src = ylt
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, ylt)
-            src = gathered
+    def measures(src, n_shards):
         if len(layers) > 1 and len(rps) <= 4:        # every table in one call, one read-back
-            pml, tvar, _ = ara.risk_measures_batch(ctx, src, L, N_total, layers, rps=rps, n_shards=world)
+            pml, tvar, _ = ara.risk_measures_batch(ctx, src, L, N_total, layers, rps=rps, n_shards=n_shards)
             return [(pml[i], tvar[i]) for i in range(len(layers))]
-        return [ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=world) for layer in layers]
+        return [ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=n_shards) for layer in layers]
+
+    def step(Yx, timed=False):
+        ara.run(ctx, P, Yx, seed=cfg["seed"], su=cfg["su"], ylt=ylt)
+        if timed:
+            kern_ms.append(ara.last_run_timings(ctx))
+        src, n_shards = gather_ylt(ylt, world, N_total, gathered, padded)
+        return measures(src, n_shards)
 
     # exact number of present (occurrence, slot) pairs = SU samples per launch
     _, cnt_dbg, _ = ara.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"], debug=True)
     pairs = int(cnt_dbg.sum().item())
     del cnt_dbg
     for _ in range(args.warmup):
-        step()
+        step(Y)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -250,80 +300,83 @@ def run_ours(args, cfg, rank, world, local):
         t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
-            res = step(timed_scan=True)
+            res = step(Y, timed=True)
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
     elapsed = t0.elapsed_time(t1) / 1e3
-    scan_avg = sum(a.elapsed_time(b) for a, b in scan_ms) / len(scan_ms) / 1e3
     if world > 1:
-        t = torch.tensor([elapsed, scan_avg], device=dev, dtype=torch.float64)
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed, scan_avg = float(t[0]), float(t[1])
+        elapsed = float(t[0])
 
     # ---- e2e: the same step through the public API from pinned host memory.
     # Every step copies its YET host -> device and reads its YLT back; the
     # copies run on a second stream into a second device YET, so step s+1's
-    # H2D overlaps step s's kernels (double buffering).
+    # H2D overlaps step s's kernels (double buffering).  Two host encodings of
+    # the YET: bit-packed at ceil(log2 catalog) bits per id (unpacked on the
+    # device by ara_yet_refill_packed) and plain uint32 ids (ara_yet_refill).
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 5))
     copy_stream = torch.cuda.Stream(dev)
     ctx_copy = ara.Context(local, copy_stream)
     Ys = [Y, ara.Yet(ctx, ev_host, fixed_len=K, first_trial=lo, n_trials=n_loc)]
-    # the host YET as stored for upload: bit-packed at ceil(log2 catalog) bits per id
-    # (ara_yet_refill_packed stages and unpacks it on the device), or plain uint32
-    bits = aragen.yet_bits(cfg["catalog"]) if not args.plain_upload else 32
-    if bits < 32:
-        words = (n_loc * K * bits + 31) // 32
-        up_host = torch.empty(words, dtype=torch.int32).pin_memory()
-        aragen.pack_yet(ev_host.numpy().view(np.uint32), bits, out=up_host.numpy().view(np.uint32))
-        h2d_bytes = words * 4
+    ara.prepare(ctx, P, Ys[1], su=cfg["su"])
 
-        def upload(Yx):
-            Yx.refill_packed(up_host, bits, ctx=ctx_copy)
-    else:
-        h2d_bytes = n_loc * K * 4
+    def e2e(bits):
+        if bits < 32:
+            words = (n_loc * K * bits + 31) // 32
+            up_host = torch.empty(words, dtype=torch.int32).pin_memory()
+            aragen.pack_yet(ev_host.numpy().view(np.uint32), bits, out=up_host.numpy().view(np.uint32))
+            h2d = words * 4
 
-        def upload(Yx):
-            Yx.refill(ev_host, ctx=ctx_copy)
-    for Yx in Ys:                                # untimed: the upload path's staging is allocated once
-        upload(Yx)
-    ctx_copy.synchronize()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    te0 = torch.cuda.Event(enable_timing=True); te1 = torch.cuda.Event(enable_timing=True)
-    te0.record(stream)
-    copy_stream.wait_event(te0)
-    upload(Ys[0])                               # H2D of step 0's YET
-    for s_ in range(e2e_steps):
-        ctx_copy.synchronize()                  # step s's YET is on the device
-        if s_ + 1 < e2e_steps:
-            upload(Ys[(s_ + 1) % 2])            # H2D of step s+1 overlaps step s
-        Yc = Ys[s_ % 2]
-        ara.run(ctx, P, Yc, seed=cfg["seed"], su=cfg["su"], ylt=ylt)
-        src = ylt
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, ylt)
-            src = gathered
-        if len(layers) > 1 and len(rps) <= 4:
-            ara.risk_measures_batch(ctx, src, L, N_total, layers, rps=rps, n_shards=world)
+            def upload(Yx):
+                Yx.refill_packed(up_host, bits, ctx=ctx_copy)
         else:
-            for layer in layers:
-                ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=world)
-        ylt_host.copy_(ylt, non_blocking=True)  # D2H of the step's result
-    te1.record(stream)
-    torch.cuda.synchronize()
-    e2e_elapsed = te0.elapsed_time(te1) / 1e3
-    if world > 1:
-        t = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_elapsed = float(t[0])
+            h2d = n_loc * K * 4
+
+            def upload(Yx):
+                Yx.refill(ev_host, ctx=ctx_copy)
+        for Yx in Ys:                                # untimed: the upload path's staging is allocated once
+            upload(Yx)
+        ctx_copy.synchronize()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        te0 = torch.cuda.Event(enable_timing=True); te1 = torch.cuda.Event(enable_timing=True)
+        te0.record(stream)
+        copy_stream.wait_event(te0)
+        upload(Ys[0])                               # H2D of step 0's YET
+        for s_ in range(e2e_steps):
+            ctx_copy.synchronize()                  # step s's YET is on the device
+            if s_ + 1 < e2e_steps:
+                upload(Ys[(s_ + 1) % 2])            # H2D of step s+1 overlaps step s
+            step(Ys[s_ % 2])
+            ylt_host.copy_(ylt, non_blocking=True)  # D2H of the step's result
+        te1.record(stream)
+        torch.cuda.synchronize()
+        el = te0.elapsed_time(te1) / 1e3
+        if world > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t[0])
+        return {"value": N_total / (el / e2e_steps), "unit": "trials/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": L * n_loc * 4 + 16 * len(rps) * len(layers), "steps": e2e_steps,
+                "yet_upload_bits": bits}
+    bits = aragen.yet_bits(cfg["catalog"]) if not args.plain_upload else 32
+    e2e_main = e2e(bits)
+    e2e_main["how"] = (("pinned host YET stored bit-packed at %d bits per event id, copied every step and "
+                        "unpacked on the device (ara_yet_refill_packed)" % bits) if bits < 32 else
+                       "pinned host YET (uint32 ids) copied every step (ara_yet_refill)") + \
+        " on a second stream into a double-buffered device YET (step s+1's H2D overlaps step s), " \
+        "ara_run + all-gather + measures, YLT read back every step"
+    if bits < 32:                                   # the plain uint32 encoding beside it
+        e2e_main["plain_uint32"] = e2e(32)
     del Ys[1]
 
-    # ---- roofline of the dominant kernel, live per-kernel times (CUDA events on the
-    # context stream, recorded by ara_run around each kernel)
+    # ---- roofline: live per-kernel device times (CUDA events on
+    # the streams the kernels run on, summed over each run's launches)
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
@@ -331,63 +384,85 @@ def run_ours(args, cfg, rank, world, local):
     t_sample = sum(k["sample_ms"] for k in kern_ms) / len(kern_ms) / 1e3
     t_redo = sum(k["redo_ms"] for k in kern_ms) / len(kern_ms) / 1e3
     n_dev_recs = L * cfg["elts_per_layer"] * cfg["records_per_elt"]
+    step_s = elapsed / args.steps
     # algorithmic bytes of the path: the YET once (4 B per occurrence), the YLT once,
-    # the portfolio tables once (index 8 B/event + 32 B record + 128 B hot table per record)
-    alg_bytes = n_loc * K * 4 + L * n_loc * 4 + cfg["catalog"] * 8 + n_dev_recs * (32 + 128)
+    # the portfolio tables once (index 8 B/event + 32 B record + 128 B hot table per record;
+    # without draws: the per-(event, layer) occurrence losses)
+    primary = not cfg["su"] or pf_info.get("all_sigma_zero")
+    lp = 1 if L <= 1 else 2 if L <= 2 else 4 if L <= 4 else 8
+    tab_bytes = cfg["catalog"] * lp * 4 if primary else cfg["catalog"] * 8 + n_dev_recs * (32 + 128)
+    alg_bytes = n_loc * K * 4 + L * n_loc * 4 + tab_bytes
     consts = json.load(open(PROFILE_CONST)) if os.path.exists(PROFILE_CONST) else {}
     clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * clk_mhz * 1e6 / 1e12          # T lane-instructions / s
-    compact = {"kernel": "compact_kernel", "bound": "hbm", "unit": "GB/s", "kernel_ms": t_compact * 1e3,
-               "alg_bytes_per_launch": n_loc * K * 4,
-               "achieved": n_loc * K * 4 / t_compact / 1e9 if t_compact else None, "peak": hbm_peak}
-    compact["frac"] = compact["achieved"] / hbm_peak if compact["achieved"] else None
-    cc = consts.get("compact_kernel", {})
-    compact["traffic"] = cc.get("dram_bytes_per_occurrence", 0) * n_loc * K if cc else None
-    if cc.get("ncu"):
-        compact["ncu"] = dict(cc["ncu"], source=cc.get("source"))   # L2 hit rate, pipes
-        if cc["ncu"].get("l1_lsu_wavefronts_pct") is not None:
-            # the resource that binds the compaction: the L1 data pipe, not HBM
-            compact["binding"] = {"resource": "L1 data-pipe (LSU) wavefronts",
-                                  "frac": cc["ncu"]["l1_lsu_wavefronts_pct"] / 100.0,
-                                  "source": "ncu capture (profiles/roofline_consts.json)"}
-    sample = {"kernel": "sample_kernel", "kernel_ms": t_sample * 1e3, "samples_per_launch": pairs,
-              "samples_per_s": pairs / t_sample if t_sample else None}
-    sc = consts.get("sample_kernel", {}) if cfg["su"] else {}
-    if cfg["su"]:
-        sample.update(bound="alu", unit="Tinst/s", peak=alu_peak,
-                      peak_source="148 SMs x 128 FP32 lanes x sm_max_mhz (B200_PROFILING.md)")
-        if sc and t_sample:
-            inst = sc["thread_inst_per_pair"] * pairs
+    kernels = {}
+    if primary:
+        pk = {"kernel": "primary_kernel", "bound": "hbm", "unit": "GB/s", "kernel_ms": t_sample * 1e3,
+              "alg_bytes_per_launch": alg_bytes, "peak": hbm_peak,
+              "achieved": alg_bytes / t_sample / 1e9 if t_sample else None}
+        pk["frac"] = pk["achieved"] / hbm_peak if pk["achieved"] else None
+        pc = consts.get("primary_kernel", {})
+        pk["traffic"] = pc.get("dram_bytes_per_occurrence", 0) * n_loc * K if pc else None
+        kernels["primary_kernel"] = pk
+        dom = pk
+    else:
+        compact = {"kernel": "compact_kernel", "bound": "hbm", "unit": "GB/s", "kernel_ms": t_compact * 1e3,
+                   "alg_bytes_per_launch": n_loc * K * 4,
+                   "achieved": n_loc * K * 4 / t_compact / 1e9 if t_compact else None, "peak": hbm_peak}
+        compact["frac"] = compact["achieved"] / hbm_peak if compact["achieved"] else None
+        cc = consts.get("compact_kernel", {})
+        compact["traffic"] = cc.get("dram_bytes_per_occurrence", 0) * n_loc * K if cc else None
+        if cc.get("ncu"):
+            compact["ncu"] = dict(cc["ncu"], source=cc.get("source"))
+        # the sampler: ALU-bound; achieved = the floor's algorithmic
+        # lane-instructions (300 per SU sample, implementation-independent) / time
+        sample = {"kernel": "sample_kernel", "bound": "alu", "unit": "Tinst/s", "kernel_ms": t_sample * 1e3,
+                  "samples_per_launch": pairs, "samples_per_s": pairs / t_sample if t_sample else None,
+                  "alg_inst_per_sample": ALG_INST_PER_SAMPLE, "peak": alu_peak,
+                  "peak_source": "148 SMs x 128 FP32 lanes x sm_max_mhz (B200_PROFILING.md)",
+                  "achieved": ALG_INST_PER_SAMPLE * pairs / t_sample / 1e12 if t_sample else None}
+        sample["frac"] = sample["achieved"] / alu_peak if sample["achieved"] else None
+        sc = consts.get("sample_kernel", {})
+        if sc:
+            sample["traffic"] = sc["dram_bytes_per_pair"] * pairs
+            sample["issued_inst_per_sample"] = sc.get("thread_inst_per_pair")
+            sample["issue_frac"] = sc["thread_inst_per_pair"] * pairs / t_sample / 1e12 / alu_peak if t_sample else None
             if sc.get("ncu"):
                 sample["ncu"] = dict(sc["ncu"], source=sc.get("source"))
-            sample.update(achieved=inst / t_sample / 1e12, frac=inst / t_sample / 1e12 / alu_peak,
-                          inst_per_pair=sc["thread_inst_per_pair"], inst_source=consts.get("source"),
-                          traffic=sc["dram_bytes_per_pair"] * pairs)
         else:
-            sample.update(achieved=None, frac=None, traffic=None)
-    else:
-        sample.update(bound="hbm", unit="GB/s", peak=hbm_peak,
-                      achieved=pairs * 8 / t_sample / 1e9 if t_sample else None)
-        sample["frac"] = sample["achieved"] / hbm_peak if sample["achieved"] else None
-        sample["traffic"] = None
-    dom = sample if t_sample >= t_compact else compact
+            sample["traffic"] = None
+        kernels["compact_kernel"] = compact
+        kernels["sample_kernel"] = sample
+        dom = sample if t_sample >= t_compact else compact
     roof = dict(dom)
     roof["peak_note"] = peak_src if roof.get("unit") == "GB/s" else roof.get("peak_source")
-    roof["kernels"] = {"compact_kernel": compact, "sample_kernel": sample, "redo_ms": t_redo * 1e3}
-    roof["path_hbm"] = {"alg_bytes_per_step": alg_bytes, "run_ms": scan_avg * 1e3,
-                        "achieved": alg_bytes / scan_avg / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                        "frac": alg_bytes / scan_avg / 1e9 / hbm_peak}
+    roof["kernels"] = dict(kernels, redo_ms=t_redo * 1e3)
+    roof["path_hbm"] = {"alg_bytes_per_step": alg_bytes, "step_ms": step_s * 1e3,
+                        "achieved": alg_bytes / step_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": alg_bytes / step_s / 1e9 / hbm_peak}
+    if not primary:
+        t_floor = max(alg_bytes / hbm_peak / 1e9, ALG_INST_PER_SAMPLE * pairs / alu_peak / 1e12)
+        roof["path_binding"] = {"floor_ms": t_floor * 1e3, "frac": t_floor / step_s,
+                                "rule": "max(algorithmic bytes / HBM peak, 300 lane-instructions per SU "
+                                        "sample / ALU peak) over the step time (SURVEY 8(d))"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = host_cores()
         n = oracle_sample_size(cfg, cores)
         dt, n = time_oracle(cfg, n, cores)
-        cpu = {"value": n / dt, "unit": "trials/s", "cores": cores, "kind": "oracle",
+        n1 = max(200, min(10000, oracle_sample_size(cfg, 1, target_s=6.0)))
+        dt1, n1 = time_oracle(cfg, n1, 1)
+        cpu = {"value": n / dt, "unit": "trials/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"first {n} trials of {cfg['name']} (global index 0..{n - 1}), "
-                         f"fp64 C oracle, {cores} threads, {dt:.1f} s"}
+                         f"fp64 C oracle, {cores} threads, {dt:.1f} s",
+               "single_core": {"value": n1 / dt1, "unit": "trials/s", "cores": 1,
+                               "sample": f"first {n1} trials, 1 thread, {dt1:.1f} s"}}
 
-    gpu_launches = args.steps * (2 + (1 if t_redo > 0 else 0) + 11 * len(layers))
+    n_batches = int(kern_ms[-1].get("batches", 1)) if kern_ms else 1
+    # libara kernels per timed step: ara_run's (counted by the library) + one joint-select
+    # launch per measured table
+    gpu_launches = sum(k["launches"] for k in kern_ms) + args.steps * len(layers)
     ms = elapsed / args.steps * 1e3
     value = N_total / (elapsed / args.steps)
     line = {
@@ -397,17 +472,12 @@ def run_ours(args, cfg, rank, world, local):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(cfg), "n_trials_total": N_total,
                    "trials_per_rank": n_loc, "return_periods": rps,
-                   "l2": "inputs > L2: the 3.2 GB YET is streamed every step; the portfolio "
+                   "l2": "inputs > L2: the YET (4 B x events) is streamed every step; the portfolio "
                          "tables (index, bitmap, records) stay L2-resident by design",
-                   "parallelism": f"trial-sharded x{world}" + (f" + {backend.upper()} YLT all-gather" if world > 1 else "")},
-        "e2e": {"value": N_total / (e2e_elapsed / e2e_steps), "unit": "trials/s",
-                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": L * n_loc * 4 + 16 * len(rps) * len(layers),
-                "steps": e2e_steps, "yet_upload_bits": bits,
-                "how": ("pinned host YET, stored bit-packed at %d bits per event id, copied every step and "
-                        "unpacked on the device (ara_yet_refill_packed)" % bits if bits < 32 else
-                        "pinned host YET (uint32 ids) copied every step (ara_yet_refill)") +
-                       " on a second stream into a double-buffered device YET (step s+1's H2D overlaps step s), "
-                       "ara_run + measures, YLT read back every step"},
+                   "parallelism": f"trial-sharded x{world}" + (f" + {backend.upper()} YLT all-gather" if world > 1 else ""),
+                   "path": "primary (no draws): one streaming kernel" if primary else
+                           f"compaction + sampler, {n_batches} trial batch(es)"},
+        "e2e": e2e_main,
         "gpu_launches": gpu_launches,
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -424,7 +494,15 @@ def run_ours(args, cfg, rank, world, local):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-execute under torch.distributed.run
+        import subprocess
+        cmd = launch_command(args.gpus, sys.argv[1:])
+        r = subprocess.run(cmd)
+        sys.exit(r.returncode)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; run with --gpus equal to the rank count")
     name = args.config or "cfg3"
     cfg = aragen.load_config(name)
     if args.impl == "reference":

@@ -50,10 +50,6 @@ extern "C" {
 #define ARA_EXACT 4u         /* solve every beta quantile per sample in fp64
                                 instead of the per-record quantile tables
                                 (validation mode; slow)                    */
-#define ARA_FUSED 8u         /* accepted, no effect: the warp-specialised
-                                single kernel it selected in round 1 was
-                                slower than the two-kernel path and was
-                                removed                     */
 #define ARA_WIDE_PAIRS 16u   /* keep 8-byte {record, k} pair records even when
                                 4-byte packed ones fit (same results; for tests
                                 and comparison)                            */
@@ -68,6 +64,10 @@ extern "C" {
                                 (trial, occurrence, 0, 7).  Default (neither
                                 flag): reading G2, counter (trial,
                                 occurrence, XELT id, 2)                     */
+#define ARA_RNG_SUPPLIED 128u /* the paper's data model: z_(Prog,E)
+                                of each YET occurrence and z_(E) of each XELT
+                                record are inputs, supplied by ara_yet_set_z
+                                and ara_portfolio_set_z; no draw is taken   */
 
 /* ---- limits (validated) ------------------------------------------------ */
 #define ARA_MAX_SLOTS 224    /* XELTs per layer; also the (layer, XELT) slots
@@ -202,6 +202,23 @@ int ara_yet_refill(ara_ctx *ctx, ara_yet *yet, const uint32_t *event_ids);
  * by a kernel; asynchronous like ara_yet_refill.  Ids >= catalog_size are
  * caught by ara_run (ARA_ERANGE).  ARA_EINVAL for bits out of range. */
 int ara_yet_refill_packed(ara_ctx *ctx, ara_yet *yet, uint32_t bits, const uint32_t *packed);
+/* The paper's YET tuples (E, t, z_(Prog,E)): attach the
+ * z_(Prog,E) of every occurrence, for each program, to a loaded YET.
+ *   n_programs  programs supplied (>= 1); a run's portfolio may use programs
+ *               0 .. n_programs-1
+ *   z_prog      host [n_programs][total events] floats in (0,1): the value
+ *               of occurrence o (trial-major, occurrence order, as the event
+ *               ids) for program p is z_prog[p * total + o]
+ * Copied; used by ara_run with ARA_RNG_SUPPLIED.  ARA_EINVAL on a value
+ * outside (0,1) (with its program and occurrence). */
+int ara_yet_set_z(ara_ctx *ctx, ara_yet *yet, uint32_t n_programs, const float *z_prog);
+/* The paper's XEL records {E, mu_l, z_(E), sigma_I, sigma_C, max_l}:
+ * attach z_(E) to every record of a built portfolio.
+ *   z_event  host [total records] floats in (0,1), in the order of the
+ *            records passed to ara_create_portfolio
+ * Copied; used by ara_run with ARA_RNG_SUPPLIED.  ARA_EINVAL on a value
+ * outside (0,1). */
+int ara_portfolio_set_z(ara_ctx *ctx, ara_portfolio *pf, const float *z_event);
 uint64_t ara_yet_num_trials(const ara_yet *yet);
 void ara_yet_destroy(ara_yet *yet);
 
@@ -233,12 +250,28 @@ int ara_run(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint64_t 
 int ara_run_ep(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint64_t seed,
                uint32_t flags, float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash);
 
+/* Optional: allocate every scratch buffer ara_run needs for this
+ * (portfolio, YET) pair with these flags, so that ara_run itself allocates
+ * nothing (the pair slots of the two-stream pipeline: 2 x batch x region
+ * pairs; the per-trial pair counts).  Without it ara_run grows the same
+ * buffers on first use.  A run whose trials overflow their regions still
+ * grows the overflow pool (exactly sized) when that happens.
+ * Errors: ARA_EINVAL, ARA_ECUDA / ARA_ENOMEM-like allocation failures as ARA_ECUDA. */
+int ara_prepare(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint32_t flags);
+
 /* Device time of the kernels of the last ara_run on this context (CUDA
  * events on its stream): compact_ms = YET stream + lookup (compact_kernel),
  * sample_ms = draws + sampler + terms + YLT (sample_kernel; the fused
  * kernel under ARA_EXACT), redo_ms = trials re-run by the fused fp64-capable
  * kernel (0 when none).  Any pointer may be NULL. */
 int ara_last_run_timings(const ara_ctx *ctx, double *compact_ms, double *sample_ms, double *redo_ms);
+
+/* Kernels launched by the last ara_run / ara_run_ep on this context (all
+ * libara kernels: compaction + sampler per trial batch, the overflow pass,
+ * the fp64 redo; or the one streaming kernel of the primary path) and the
+ * trial batches of its two-kernel path (0 on the primary / fused paths).
+ * Any pointer may be NULL. */
+int ara_last_run_launches(const ara_ctx *ctx, uint32_t *kernel_launches, uint32_t *batches);
 
 /* PML and TVaR (reading G17) at each return period of one layer's
  * YLT, or of the portfolio roll-up sum over layers (layer = -1, G16), by a

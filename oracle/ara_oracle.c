@@ -360,7 +360,11 @@ typedef struct {
     const uint32_t *events;
     uint64_t seed;
     int su;
-    int rng_mode;                 /* 0: reading G2; 1: (A) z_(E) per record; 2: (B) per occurrence */
+    int rng_mode;                 /* 0: reading G2; 1: (A) z_(E) per record; 2: (B) per occurrence;
+                                     3: the paper's data model -- both draws supplied with the inputs */
+    const double *zp_sup;         /* rng_mode 3: z_(Prog,E) of each YET occurrence, [program][occurrence] */
+    const double *ze_sup;         /* rng_mode 3: z_(E) of each XELT record, [record] */
+    uint64_t n_occ;               /* occurrences in the YET (stride of zp_sup) */
     /* dense direct-access table [n_elts][catalog_size] -> record id or -1 */
     int32_t *table;
     /* outputs [n_layers][n_trials] */
@@ -398,10 +402,12 @@ static void *orc_worker(void *arg) {
                     h += orc_lookup_hash(k, j, rloc);
                     double l_e;
                     if (J->su) {                                             /* line 7 */
-                        double zp = orc_z_prog(J->seed, prog, i, k);
-                        double ze = J->rng_mode == 1 ? orc_z_event_record(J->seed, j, rloc)
+                        double zp = J->rng_mode == 3 ? J->zp_sup[(size_t)prog * J->n_occ + o]
+                                  : orc_z_prog(J->seed, prog, i, k);
+                        double ze = J->rng_mode == 3 ? J->ze_sup[r]
+                                  : J->rng_mode == 1 ? orc_z_event_record(J->seed, j, rloc)
                                   : J->rng_mode == 2 ? orc_z_event_occ(J->seed, i, k)
-                                  : orc_z_event(J->seed, i, k, j);               /* G2 / (A) / (B) */
+                                  : orc_z_event(J->seed, i, k, j);               /* G2 / (A) / (B) / supplied */
                         if (orc_sample_loss(J->rec_mean[r], J->rec_si[r], J->rec_sc[r],
                                             J->rec_max[r], zp, ze, &l_e) != 0)
                             J->status = -1;
@@ -440,7 +446,8 @@ int orc_run(uint32_t catalog_size, uint32_t n_elts, const uint64_t *elt_off,
             const uint32_t *layer_elts, const double *layer_terms, uint64_t n_trials,
             const uint64_t *trial_index, const uint64_t *trial_off, const uint32_t *events,
             uint64_t seed, int su, int n_threads, double *ylt, double *gross,
-            uint32_t *count, uint64_t *hash, double *occ_max, int rng_mode) {
+            uint32_t *count, uint64_t *hash, double *occ_max, int rng_mode,
+            const double *zp_sup, const double *ze_sup) {
     size_t slots = (size_t)n_elts * catalog_size;
     int32_t *table = (int32_t *)malloc((slots ? slots : 1) * sizeof(int32_t));
     if (!table) return -3;
@@ -454,6 +461,7 @@ int orc_run(uint32_t catalog_size, uint32_t n_elts, const uint64_t *elt_off,
     }
     for (uint64_t o = 0; o < trial_off[n_trials]; o++)
         if (events[o] >= catalog_size) { free(table); return -2; }
+    if (rng_mode == 3 && (!zp_sup || !ze_sup)) { free(table); return -2; }
     if (n_threads < 1) n_threads = 1;
     if ((uint64_t)n_threads > n_trials) n_threads = n_trials ? (int)n_trials : 1;
     orc_job *jobs = (orc_job *)calloc((size_t)n_threads, sizeof(orc_job));
@@ -467,6 +475,7 @@ int orc_run(uint32_t catalog_size, uint32_t n_elts, const uint64_t *elt_off,
         J->layer_elts = layer_elts; J->layer_terms = layer_terms; J->n_trials = n_trials;
         J->trial_index = trial_index; J->trial_off = trial_off; J->events = events;
         J->seed = seed; J->su = su; J->table = table; J->rng_mode = rng_mode;
+        J->zp_sup = zp_sup; J->ze_sup = ze_sup; J->n_occ = trial_off[n_trials];
         J->ylt = ylt; J->gross = gross; J->count = count; J->hash = hash; J->occ_max = occ_max;
         J->t_begin = n_trials * (uint64_t)w / (uint64_t)n_threads;
         J->t_end = n_trials * (uint64_t)(w + 1) / (uint64_t)n_threads;

@@ -69,7 +69,7 @@ def lib():
         vp = C.c_void_p
         L.orc_run.argtypes = [u32, u32, vp, vp, vp, vp, vp, vp, vp,
                               u32, vp, vp, vp, vp, u64, vp, vp, vp,
-                              u64, i32, i32, vp, vp, vp, vp, vp, i32]
+                              u64, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp]
         L.orc_run.restype = i32
         L.orc_z_event_record.argtypes = [u64, u32, u32]; L.orc_z_event_record.restype = d
         L.orc_z_event_occ.argtypes = [u64, u64, u32]; L.orc_z_event_occ.restype = d
@@ -184,12 +184,16 @@ def _ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-def run(portfolio, yet, seed, su=True, n_threads=None, trial_index=None, rng_mode=0):
+def run(portfolio, yet, seed, su=True, n_threads=None, trial_index=None, rng_mode=0, z_prog=None, z_event=None):
     """Algorithm 1 over every layer; returns dict(ylt, gross, count, hash,
     occ_max) -- occ_max = per (layer, trial) largest occurrence loss net of
     the occurrence terms (line 11), the basis of the OEP (reading G29).
     ``rng_mode``: 0 = reading G2 (z_E per trial, occurrence, XELT); 1 = (A)
     z_E stored per XELT record; 2 = (B) z_E per occurrence shared by XELTs.
+    ``z_prog`` [n_programs][n_occurrences] and ``z_event`` [n_records] given
+    (rng_mode 3, the paper's data model, P:55 / P:76): the draws are these
+    supplied numbers -- z_(Prog,E) of occurrence o of the YET for program p,
+    z_(E) of each XELT record -- instead of Philox draws.
 
     ``portfolio``: dict with catalog_size, elt_off[n_elts+1], rec_event,
     rec_mean, rec_sigma_i, rec_sigma_c, rec_max (any float dtype; converted
@@ -225,12 +229,22 @@ def run(portfolio, yet, seed, su=True, n_threads=None, trial_index=None, rng_mod
     occ_max = np.zeros((n_layers, n), dtype=np.float64)
     if n_threads is None:
         n_threads = os.cpu_count() or 1
+    zp = ze = None
+    if z_prog is not None or z_event is not None:
+        assert z_prog is not None and z_event is not None, "supply both z_prog and z_event"
+        rng_mode = 3
+        zp = f64(z_prog).reshape(-1)
+        ze = f64(z_event).reshape(-1)
+        assert zp.size % max(ev.size, 1) == 0 and zp.size >= ev.size * (int(lprog.max()) + 1 if lprog.size else 1)
+        assert ze.size == rec_event.size
+        assert ((zp > 0) & (zp < 1)).all() and ((ze > 0) & (ze < 1)).all(), "z values must lie in (0, 1)"
     st = lib().orc_run(int(pf["catalog_size"]), n_elts, _ptr(elt_off), _ptr(rec_event),
                        _ptr(rm), _ptr(rsi), _ptr(rsc), _ptr(rmax), _ptr(et),
                        n_layers, _ptr(lprog), _ptr(loff), _ptr(lelts), _ptr(lterms),
                        n, _ptr(tidx), _ptr(toff), _ptr(ev),
                        int(seed) & 0xFFFFFFFFFFFFFFFF, 1 if su else 0, int(n_threads),
-                       _ptr(ylt), _ptr(gross), _ptr(count), _ptr(hsh), _ptr(occ_max), int(rng_mode))
+                       _ptr(ylt), _ptr(gross), _ptr(count), _ptr(hsh), _ptr(occ_max), int(rng_mode),
+                       _ptr(zp), _ptr(ze))
     if st == -1:
         raise OracleError("a beta quantile did not converge")
     if st == -2:

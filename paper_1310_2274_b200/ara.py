@@ -19,7 +19,6 @@ OK, EINVAL, ERANGE, EDUP, ENOMEM, ECUDA, ECONVERGE, ENCCL = range(8)
 SU = 1
 DEBUG_LOOKUP = 2
 EXACT = 4
-FUSED = 8
 WIDE_PAIRS = 16
 MAX_SLOTS = 224
 MAX_LAYERS = 64
@@ -38,7 +37,8 @@ EXPORTS = (
     "ara_load_yet",
     "ara_yet_refill", "ara_yet_refill_packed", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings", "ara_risk_measures_var", "ara_risk_measures_batch", "ara_exceedance_curve",
     "ara_risk_measures",
-    "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles", "ara_beta_quantiles",
+    "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles", "ara_beta_quantiles", "ara_prepare",
+    "ara_yet_set_z", "ara_portfolio_set_z", "ara_last_run_launches",
 )
 
 
@@ -80,6 +80,10 @@ def _load():
     L.ara_draw_uniforms.argtypes = [vp, u64, u64, vp, vp]
     L.ara_normal_quantiles.argtypes = [vp, u64, vp, vp]
     L.ara_beta_quantiles.argtypes = [vp, u64, vp, vp, vp, vp, vp]
+    L.ara_prepare.argtypes = [vp, vp, vp, u32]
+    L.ara_yet_set_z.argtypes = [vp, vp, u32, vp]
+    L.ara_portfolio_set_z.argtypes = [vp, vp, vp]
+    L.ara_last_run_launches.argtypes = [vp, vp, vp]
     for n in EXPORTS:            # fail loudly if an entry point is missing
         getattr(L, n)
     return L
@@ -184,6 +188,11 @@ class Portfolio:
         self.h, self.ctx = h, ctx
         self.n_layers = len(pf["layer_prog"])
 
+    def set_z(self, z_event):
+        """ara_portfolio_set_z: the z_(E) of every XELT record, in input record order."""
+        z = np.ascontiguousarray(z_event, np.float32).ravel()
+        _check(lib.ara_portfolio_set_z(self.ctx.h, self.h, _p(z)))
+
     def info(self):
         """dict(n_device_records, n_table_less, device_bytes) (ara_portfolio_info)."""
         a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
@@ -232,6 +241,12 @@ class Yet:
         (default: the context the YET was loaded with)."""
         _check(lib.ara_yet_refill((ctx or self.ctx).h, self.h, _p(events)))
 
+    def set_z(self, z_prog):
+        """ara_yet_set_z: the z_(Prog,E) of every occurrence, [n_programs][total events]."""
+        z = np.ascontiguousarray(z_prog, np.float32)
+        z2 = z.reshape(-1, z.shape[-1]) if z.ndim > 1 else z.reshape(1, -1)
+        _check(lib.ara_yet_set_z(self.ctx.h, self.h, z2.shape[0], _p(z2)))
+
     def refill_packed(self, packed, bits: int, ctx: "Context" = None):
         """ara_yet_refill_packed: new event ids from their bit-packed words
         (aragen.pack_yet), staged and unpacked on the device, on ctx's stream."""
@@ -249,12 +264,11 @@ class Yet:
             pass
 
 
-RNG_FLAGS = {"g2": 0, "record": 32, "occurrence": 64}   # ARA_RNG_RECORD / ARA_RNG_OCCURRENCE
+RNG_FLAGS = {"g2": 0, "record": 32, "occurrence": 64, "supplied": 128}   # ARA_RNG_RECORD / _OCCURRENCE / _SUPPLIED
 
 
 def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug: bool = False,
-        ylt=None, exact: bool = False, fused: bool = False,
-        wide_pairs: bool = False, rng: str = "g2"):
+        ylt=None, exact: bool = False, wide_pairs: bool = False, rng: str = "g2"):
     """ara_run; returns the device YLT [n_layers, n_trials] (and count/hash if debug).
     rng: "g2" (z_E per trial, occurrence, XELT), "record" (paper-literal z_E per
     XELT record), "occurrence" (z_E per occurrence shared by the XELTs)."""
@@ -267,7 +281,6 @@ def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug
         cnt = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int32, device=dev)
         hsh = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int64, device=dev)
     flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (EXACT if exact else 0) | \
-        (FUSED if fused else 0) | \
         (WIDE_PAIRS if wide_pairs else 0) | RNG_FLAGS[rng]
     _check(lib.ara_run(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(cnt),
                        _p(hsh)))
@@ -296,11 +309,21 @@ def run_ep(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, de
     return (ylt, occ_max, cnt, hsh) if debug else (ylt, occ_max)
 
 
+def prepare(ctx: Context, pf: Portfolio, yet: Yet, su: bool = True, debug: bool = False,
+            wide_pairs: bool = False):
+    """ara_prepare: allocate ara_run's scratch for (pf, yet) up front."""
+    flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (WIDE_PAIRS if wide_pairs else 0)
+    _check(lib.ara_prepare(ctx.h, pf.h, yet.h, flags))
+
+
 def last_run_timings(ctx: Context):
     """ara_last_run_timings -> dict(compact_ms, sample_ms, redo_ms) of the last ara_run."""
     a, b, c = C.c_double(), C.c_double(), C.c_double()
     _check(lib.ara_last_run_timings(ctx.h, C.byref(a), C.byref(b), C.byref(c)))
-    return {"compact_ms": a.value, "sample_ms": b.value, "redo_ms": c.value}
+    n, nb = C.c_uint32(), C.c_uint32()
+    _check(lib.ara_last_run_launches(ctx.h, C.byref(n), C.byref(nb)))
+    return {"compact_ms": a.value, "sample_ms": b.value, "redo_ms": c.value, "launches": n.value,
+            "batches": nb.value}
 
 
 def risk_measures(ctx: Context, ylt, n_layers: int, n_total: int, layer: int = 0,

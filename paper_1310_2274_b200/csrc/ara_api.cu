@@ -54,9 +54,27 @@ cudaError_t dalloc(T **p, size_t n) {
     return cudaMalloc(reinterpret_cast<void **>(p), (n ? n : 1) * sizeof(T));
 }
 
+// grow-once device scratch
+template <typename T>
+cudaError_t grow(T **p, uint64_t &cap, uint64_t need) {
+    if (cap >= need) return cudaSuccess;
+    cudaFree(*p);
+    *p = nullptr;
+    cap = 0;
+    cudaError_t e = dalloc(p, need);
+    if (e == cudaSuccess) cap = need;
+    return e;
+}
+
+uint64_t env_u64(const char *name, uint64_t dflt) {
+    const char *v = getenv(name);
+    return v && *v ? strtoull(v, nullptr, 10) : dflt;
+}
+
 }  // namespace
 
 constexpr uint32_t kOutDoubles = 3 * 4 * (ARA_MAX_PORTFOLIO_LAYERS + 1);   // batched measures: 3 x n_rp x tables
+constexpr uint32_t kMaxBatches = 256;       // trial batches of one split-path run
 
 struct ara_ctx {
     int device = 0;
@@ -68,12 +86,22 @@ struct ara_ctx {
     uint32_t *d_ep = nullptr;          // exceedance-curve sort scratch
     uint64_t ep_capacity = 0;
     MeasuresScratch ms;
-    uint2 *d_pairs = nullptr;          // split path scratch: per-trial pairs {device record, k}
-    uint64_t pairs_capacity = 0;       // elements of d_pairs
-    uint32_t *d_counts = nullptr;      // split path scratch: pairs per trial
+    // split path: the compaction runs on its own stream, a batch ahead of the
+    // sampler on the context stream (two pair slots)
+    cudaStream_t cstream = nullptr;
+    unsigned char *d_slots = nullptr;  // 2 slots of batch x cap pairs
+    uint64_t slots_capacity = 0;       // bytes
+    unsigned char *d_pool = nullptr;   // overflow pool (exactly sized per run)
+    uint64_t pool_capacity = 0;        // bytes
+    uint64_t *d_pool_off = nullptr;
+    uint64_t pool_off_capacity = 0;
+    uint32_t *d_counts = nullptr;      // pairs per trial
     uint64_t counts_capacity = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // per-kernel timings of ara_run
+    unsigned long long *d_sched = nullptr;   // [2 kMaxBatches + 4] scheduler counters of one run
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // run begin / end, redo begin / end
+    cudaEvent_t tev[4 * kMaxBatches] = {};                      // per-batch kernel timings
     double last_ms[3] = {0.0, 0.0, 0.0};                        // compact, sample, redo
+    uint32_t last_launches = 0, last_batches = 0;               // kernels launched by the last ara_run
 };
 
 struct ara_portfolio {
@@ -89,6 +117,12 @@ struct ara_portfolio {
     float *d_mu = nullptr;
     SlotInfo *d_slots = nullptr;
     LayerInfo *d_layers = nullptr;
+    float *d_occ = nullptr;            // [catalog][occ_lp] occurrence losses without draws (fast path)
+    float *d_rec_z = nullptr;          // ARA_RNG_SUPPLIED: z_(E) per device record (ara_portfolio_set_z)
+    std::vector<uint32_t> rec_src;     // input record of each device record
+    uint32_t max_prog = 0;             // largest program id of the layers
+    uint64_t n_input_records = 0;
+    double *d_slot_terms = nullptr;    // [n_slots][4] XELT terms in fp64 (retention, limit, share, on)
     // a portfolio larger than one kernel group (> kSplitMaxLayers layers or
     // > ARA_MAX_SLOTS slots) is a list of groups of consecutive layers, each a
     // complete portfolio of its own, run one after the other over the YET
@@ -103,8 +137,12 @@ struct ara_yet {
     uint32_t *d_events = nullptr;
     uint64_t *d_offsets = nullptr;
     uint32_t *d_redo = nullptr;        // trials to re-run with the fp64 kernel
+    uint32_t *d_ovf = nullptr;         // trials whose pairs overflowed their batch region
+    uint32_t *d_ovf_n = nullptr;       // ... and their exact pair counts
     uint32_t *d_max = nullptr;         // largest event id (device word)
     uint32_t *d_packed = nullptr;      // staging of packed uploads (+2 zero words)
+    float *d_zprog = nullptr;          // ARA_RNG_SUPPLIED: z_(Prog,E) [program][occurrence] (ara_yet_set_z)
+    uint32_t zprog_programs = 0;
     uint64_t packed_capacity = 0;
     uint64_t avg_len_x1000 = 0;        // mean events per trial x 1000
     uint64_t max_len = 0;              // longest trial
@@ -145,10 +183,16 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
         dalloc(&c->ms.part_sum, kRedBlocks) != cudaSuccess ||
         dalloc(&c->ms.part_cnt, kRedBlocks) != cudaSuccess || cudaEventCreate(&c->ev[0]) != cudaSuccess ||
         cudaEventCreate(&c->ev[1]) != cudaSuccess || cudaEventCreate(&c->ev[2]) != cudaSuccess ||
-        cudaEventCreate(&c->ev[3]) != cudaSuccess) {
+        cudaEventCreate(&c->ev[3]) != cudaSuccess || dalloc(&c->d_sched, 2 * kMaxBatches + 4) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess) {
         ara_ctx_destroy(c);
         return fail(ARA_ENOMEM, "device allocation failed in ara_ctx_create");
     }
+    for (cudaEvent_t &e : c->tev)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            ara_ctx_destroy(c);
+            return fail(ARA_ECUDA, "event creation failed in ara_ctx_create");
+        }
     *out = c;
     return ARA_OK;
 }
@@ -171,10 +215,16 @@ void ara_ctx_destroy(ara_ctx *c) {
     cudaFree(c->ms.states);
     cudaFree(c->ms.part_sum);
     cudaFree(c->ms.part_cnt);
-    cudaFree(c->d_pairs);
+    cudaFree(c->d_slots);
+    cudaFree(c->d_pool);
+    cudaFree(c->d_pool_off);
     cudaFree(c->d_counts);
+    cudaFree(c->d_sched);
     for (cudaEvent_t e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->tev)
+        if (e) cudaEventDestroy(e);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     delete c;
 }
 
@@ -315,6 +365,19 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     std::vector<LayerInfo> layers(n_layers);
     for (uint32_t l = 0; l < n_layers; ++l)
         layers[l] = {lt[l].occ_retention, lt[l].occ_limit, lt[l].agg_retention, lt[l].agg_limit};
+    std::vector<double> slot_terms(4 * (size_t)S, 0.0);    // the XELT terms as given (fp64)
+    for (uint32_t x = 0; x < S; ++x)
+        if (et) {
+            const ara_elt_terms &q = et[slots[x].elt];
+            slot_terms[4 * x] = q.retention; slot_terms[4 * x + 1] = q.limit;
+            slot_terms[4 * x + 2] = q.share; slot_terms[4 * x + 3] = 1.0;
+        }
+    // no record of the portfolio carries a sigma: no draw is ever taken (G10)
+    bool all_sigma_zero = true;
+    for (uint32_t x = 0; x < S && all_sigma_zero; ++x)
+        for (uint64_t r = eoff[slots[x].elt]; r < eoff[slots[x].elt + 1]; ++r)
+            if (rec[r].sigma_i != 0.0f || rec[r].sigma_c != 0.0f) { all_sigma_zero = false; break; }
+    const uint32_t occ_lp = n_layers <= 1 ? 1 : n_layers <= 2 ? 2 : n_layers <= 4 ? 4 : 8;
 
     // event-major direct-access index: per event the slots with a record
     const uint32_t MW = (S + 31) / 32;
@@ -389,6 +452,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
         dalloc(&p->d_rec_orig, total) || dalloc(&p->d_recs, total) || dalloc(&p->d_mu, total) ||
         dalloc(&p->d_tables, total * kTabStride) || dalloc(&p->d_hot, total * kHotN) ||
         dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) || dalloc(&d_raw, R) ||
+        dalloc(&p->d_occ, (size_t)C * occ_lp) || dalloc(&p->d_slot_terms, slot_terms.size()) ||
         dalloc(&d_src, total)) {
         cudaGetLastError();
         return cleanup(fail(ARA_ENOMEM, "device allocation failed in ara_create_portfolio"));
@@ -404,6 +468,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     UP(p->d_layers, layers.data(), (size_t)n_layers);
     UP(d_raw, rec, (size_t)R);
     UP(d_src, rec_src.data(), (size_t)total);
+    UP(p->d_slot_terms, slot_terms.data(), slot_terms.size());
 #undef UP
     if (e != cudaSuccess) return cleanup(fail(ARA_ECUDA, "upload: %s", cudaGetErrorString(e)));
     e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
@@ -414,6 +479,11 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     }
     if (e == cudaSuccess) {
         launch_split_recs(p->d_recs, p->d_rec_meta, p->d_slots, p->d_mu, total, p->d_srecs, p->d_mm, s);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {       // lines 6-11 per (event, layer) at the mean losses (fast path)
+        launch_occ_table(p->d_cidx, p->d_rec_meta, p->d_mu, p->d_slot_terms, p->d_layers, n_layers, occ_lp, C,
+                         p->d_occ, s);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
@@ -442,6 +512,12 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
     d.cidx = p->d_cidx; d.rec_meta = p->d_rec_meta; d.srecs = p->d_srecs; d.mu_meta = p->d_mm;
     d.any_terms = et ? 1u : 0u;
+    p->rec_src = std::move(rec_src);
+    p->n_input_records = R;
+    for (uint32_t l = 0; l < n_layers; ++l) p->max_prog = std::max(p->max_prog, lprog[l]);
+    d.all_sigma_zero = all_sigma_zero ? 1u : 0u;
+    d.occ_lp = occ_lp;
+    d.occ = p->d_occ;
     *out = p;
     return ARA_OK;
 }
@@ -467,7 +543,8 @@ int ara_portfolio_info(const ara_portfolio *p, uint64_t *n_dev, uint64_t *n_tl, 
         *bytes = (uint64_t)d.catalog * (d.idx_stride * 4 + sizeof(uint2)) + (uint64_t)d.bitmap_words * 4 +
                  d.n_dev_records * (sizeof(BetaRec) + sizeof(float) + sizeof(uint32_t) + sizeof(uint32_t) + sizeof(SplitRec) + sizeof(uint2) +
                                     (kTabStride + kHotN) * sizeof(float2)) +
-                 d.n_slots * sizeof(SlotInfo) + d.n_layers * sizeof(LayerInfo);
+                 d.n_slots * (sizeof(SlotInfo) + 4 * sizeof(double)) + d.n_layers * sizeof(LayerInfo) +
+                 (uint64_t)d.catalog * d.occ_lp * sizeof(float);
     return ARA_OK;
 }
 
@@ -478,6 +555,7 @@ void ara_portfolio_destroy(ara_portfolio *p) {
     cudaFree(p->d_index); cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig); cudaFree(p->d_recs);
     cudaFree(p->d_cidx); cudaFree(p->d_rec_meta); cudaFree(p->d_srecs); cudaFree(p->d_mm);
     cudaFree(p->d_mu); cudaFree(p->d_slots); cudaFree(p->d_layers); cudaFree(p->d_tables); cudaFree(p->d_hot);
+    cudaFree(p->d_occ); cudaFree(p->d_slot_terms); cudaFree(p->d_rec_z);
     delete p;
 }
 
@@ -517,6 +595,7 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
     y->ctx = c;
     // +4 words: the compaction kernel's bulk copies round each piece up to 16 B
     if (dalloc(&y->d_events, total + 4) != cudaSuccess || dalloc(&y->d_redo, n_trials) != cudaSuccess ||
+        dalloc(&y->d_ovf, n_trials) != cudaSuccess || dalloc(&y->d_ovf_n, n_trials) != cudaSuccess ||
         dalloc(&y->d_max, 1) != cudaSuccess ||
         (toff && dalloc(&y->d_offsets, n_trials + 1) != cudaSuccess)) {
         cudaGetLastError();
@@ -572,6 +651,7 @@ int ara_yet_refill_packed(ara_ctx *c, ara_yet *y, uint32_t bits, const uint32_t 
     CU(cudaSetDevice(c->device));
     if (y->packed_capacity < words + 2) {              // staging grows once, then is reused
         cudaFree(y->d_packed);
+    cudaFree(y->d_zprog);
         y->d_packed = nullptr;
         y->packed_capacity = 0;
         CU(dalloc(&y->d_packed, words + 2));
@@ -585,6 +665,50 @@ int ara_yet_refill_packed(ara_ctx *c, ara_yet *y, uint32_t bits, const uint32_t 
     return ARA_OK;
 }
 
+int ara_yet_set_z(ara_ctx *c, ara_yet *y, uint32_t n_programs, const float *z_prog) {
+    if (!c || !y) return fail(ARA_EINVAL, "ctx/yet is NULL");
+    if (n_programs == 0 || !z_prog) return fail(ARA_EINVAL, "need n_programs >= 1 and z_prog");
+    const uint64_t n = (uint64_t)n_programs * y->dev.n_events;
+    for (uint64_t x = 0; x < n; ++x)
+        if (!(z_prog[x] > 0.0f && z_prog[x] < 1.0f))
+            return fail(ARA_EINVAL, "z_(Prog,E) must lie in (0,1): program %llu occurrence %llu",
+                        (unsigned long long)(x / std::max<uint64_t>(y->dev.n_events, 1)),
+                        (unsigned long long)(x % std::max<uint64_t>(y->dev.n_events, 1)));
+    CU(cudaSetDevice(c->device));
+    cudaFree(y->d_zprog);
+    y->d_zprog = nullptr;
+    y->zprog_programs = 0;
+    CU(dalloc(&y->d_zprog, n));
+    CU(cudaMemcpyAsync(y->d_zprog, z_prog, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    y->zprog_programs = n_programs;
+    return ARA_OK;
+}
+
+int ara_portfolio_set_z(ara_ctx *c, ara_portfolio *p, const float *z_event) {
+    if (!c || !p) return fail(ARA_EINVAL, "ctx/portfolio is NULL");
+    if (!z_event) return fail(ARA_EINVAL, "z_event is NULL");
+    if (!p->groups.empty()) {
+        for (ara_portfolio *g : p->groups) {
+            const int st = ara_portfolio_set_z(c, g, z_event);
+            if (st != ARA_OK) return st;
+        }
+        return ARA_OK;
+    }
+    for (uint64_t r = 0; r < p->n_input_records; ++r)
+        if (!(z_event[r] > 0.0f && z_event[r] < 1.0f))
+            return fail(ARA_EINVAL, "z_(E) must lie in (0,1): record %llu", (unsigned long long)r);
+    std::vector<float> z(p->rec_src.size());           // per device record (layout only, no arithmetic)
+    for (size_t r = 0; r < z.size(); ++r) z[r] = z_event[p->rec_src[r]];
+    CU(cudaSetDevice(c->device));
+    cudaFree(p->d_rec_z);
+    p->d_rec_z = nullptr;
+    CU(dalloc(&p->d_rec_z, z.size()));
+    CU(cudaMemcpyAsync(p->d_rec_z, z.data(), z.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return ARA_OK;
+}
+
 uint64_t ara_yet_num_trials(const ara_yet *y) { return y ? y->dev.n_trials : 0; }
 
 void ara_yet_destroy(ara_yet *y) {
@@ -593,9 +717,49 @@ void ara_yet_destroy(ara_yet *y) {
     cudaFree(y->d_events);
     cudaFree(y->d_offsets);
     cudaFree(y->d_redo);
+    cudaFree(y->d_ovf);
+    cudaFree(y->d_ovf_n);
     cudaFree(y->d_max);
     cudaFree(y->d_packed);
+    cudaFree(y->d_zprog);
     delete y;
+}
+
+// Layout of one split-path run: per-trial pair regions of 2x the expected
+// pairs per trial (+128) for uniformly drawn event ids (the size only decides
+// which trials take the overflow pass, never the arithmetic), 4-byte pairs
+// when record << kbits | k fits, and the trial batches of the two-stream
+// pipeline (ARA_BATCH_TRIALS; default: one batch while its slot fits 4 GiB;
+// at most kMaxBatches).
+struct SplitPlan {
+    uint32_t cap, kbits, n_batches;
+    uint64_t batch, slot_bytes;
+};
+
+static SplitPlan plan_split(const ara_portfolio *p, const ara_yet *y, uint32_t flags) {
+    SplitPlan pl{};
+    const uint64_t N = y->dev.n_trials;
+    const double per_occ = (double)p->dev.n_dev_records / (double)p->dev.catalog;
+    const double expect = per_occ * (double)y->avg_len_x1000 / 1000.0;
+    uint32_t cap = (uint32_t)((2.0 * expect + 128.0 + 31.0) / 32.0) * 32u;
+    if (cap > (1u << 20)) cap = 1u << 20;
+    pl.cap = (uint32_t)env_u64("ARA_PAIR_CAP", cap);     // test aid: force the overflow pass
+    if (!(flags & ARA_WIDE_PAIRS)) {
+        uint32_t kb = 1;
+        while (kb < 24 && (1ull << kb) < (uint64_t)y->max_len) ++kb;
+        if ((uint64_t)p->dev.n_dev_records <= (1ull << (32 - kb))) pl.kbits = kb;
+    }
+    // one batch while its pair slot stays within 4 GiB (each batch launch
+    // costs a kernel ramp and tail: measured 5.08 ms per cfg3 step in one
+    // batch, 5.27 in four), else as many as needed
+    const uint64_t per_trial = (uint64_t)pl.cap * (pl.kbits ? 4 : 8);
+    uint64_t batch = env_u64("ARA_BATCH_TRIALS", std::max<uint64_t>(1, (4ull << 30) / std::max<uint64_t>(per_trial, 1)));
+    batch = std::max<uint64_t>(batch, (N + kMaxBatches - 1) / kMaxBatches);
+    batch = std::min<uint64_t>(std::max<uint64_t>(batch, 1), std::max<uint64_t>(N, 1));
+    pl.batch = batch;
+    pl.n_batches = (uint32_t)((N + batch - 1) / batch);
+    pl.slot_bytes = batch * (uint64_t)pl.cap * (pl.kbits ? 4 : 8);
+    return pl;
 }
 
 static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
@@ -623,6 +787,7 @@ static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64
     // the layer or its slot, so the YLT equals one run of the whole portfolio)
     const uint64_t N = y->dev.n_trials;
     double ms[3] = {0.0, 0.0, 0.0};
+    uint32_t launches = 0, batches = 0;
     for (size_t g = 0; g < p->groups.size(); ++g) {
         const uint64_t off = (uint64_t)p->group_layer0[g] * N;
         const int st = run_group(c, p->groups[g], y, seed, flags, ylt ? ylt + off : nullptr,
@@ -630,18 +795,28 @@ static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64
                                  dbg_hash ? dbg_hash + off : nullptr);
         if (st != ARA_OK) return st;
         for (int k = 0; k < 3; ++k) ms[k] += c->last_ms[k];
+        launches += c->last_launches;
+        batches += c->last_batches;
     }
     for (int k = 0; k < 3; ++k) c->last_ms[k] = ms[k];
+    c->last_launches = launches;
+    c->last_batches = batches;
     return ARA_OK;
 }
 
 static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
                      float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash) {
-    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_FUSED | ARA_WIDE_PAIRS | ARA_RNG_RECORD |
-                  ARA_RNG_OCCURRENCE))
+    if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_WIDE_PAIRS | ARA_RNG_RECORD | ARA_RNG_OCCURRENCE |
+                  ARA_RNG_SUPPLIED))
         return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
-    if ((flags & ARA_RNG_RECORD) && (flags & ARA_RNG_OCCURRENCE))
-        return fail(ARA_EINVAL, "ARA_RNG_RECORD and ARA_RNG_OCCURRENCE are exclusive");
+    if (!!(flags & ARA_RNG_RECORD) + !!(flags & ARA_RNG_OCCURRENCE) + !!(flags & ARA_RNG_SUPPLIED) > 1)
+        return fail(ARA_EINVAL, "ARA_RNG_RECORD, ARA_RNG_OCCURRENCE and ARA_RNG_SUPPLIED are exclusive");
+    const bool supplied = (flags & ARA_RNG_SUPPLIED) && (flags & ARA_SU);
+    if (supplied && (!p->d_rec_z || !y->d_zprog))
+        return fail(ARA_EINVAL, "ARA_RNG_SUPPLIED needs ara_portfolio_set_z and ara_yet_set_z");
+    if (supplied && p->max_prog >= y->zprog_programs)
+        return fail(ARA_EINVAL, "the YET supplies z_(Prog,E) for %u programs; the portfolio uses program %u",
+                    y->zprog_programs, p->max_prog);
     if (y->dev.n_trials == 0) return ARA_OK;
     if (!ylt) return fail(ARA_EINVAL, "ylt is NULL");
     if ((dbg_count || dbg_hash) && !(flags & ARA_DEBUG_LOOKUP))
@@ -649,85 +824,149 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
     if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
     if (occ_max && !is_device_ptr(occ_max)) return fail(ARA_EINVAL, "occ_max must be device memory");
     CU(cudaSetDevice(c->device));
+    const uint64_t N = y->dev.n_trials;
     const bool exact = (flags & ARA_EXACT) != 0 && (flags & ARA_SU) != 0;
     CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
     // ARA_RNG_RECORD with occ_max (a rare combination) runs on the fp64-capable kernel
-    const bool za_om = (flags & ARA_RNG_RECORD) && (flags & ARA_SU) && occ_max;
-    if (!exact && !za_om && p->dev.n_layers <= kSplitMaxLayers) {
-        // split path: per-trial pair regions sized 2x the expected pairs per trial
-        // (+128) for uniformly drawn event ids; a trial that overflows its
-        // region goes to the fused kernel
-        const double per_occ = (double)p->dev.n_dev_records / (double)p->dev.catalog;
-        const double expect = per_occ * (double)y->avg_len_x1000 / 1000.0;
-        uint32_t cap = (uint32_t)((2.0 * expect + 128.0 + 31.0) / 32.0) * 32u;
-        if (cap > (1u << 20)) cap = 1u << 20;
-        // two kernels: compaction, then sampling (ARA_FUSED is accepted and runs them too)
-        const uint64_t need = y->dev.n_trials * (uint64_t)cap;
-        if (c->pairs_capacity < need) {          // scratch grows once, then is reused
-            cudaFree(c->d_pairs);
-            c->d_pairs = nullptr;
-            c->pairs_capacity = 0;
-            CU(dalloc(&c->d_pairs, need));
-            c->pairs_capacity = need;
-        }
-        if (c->counts_capacity < y->dev.n_trials) {
-            cudaFree(c->d_counts);
-            c->d_counts = nullptr;
-            c->counts_capacity = 0;
-            CU(dalloc(&c->d_counts, y->dev.n_trials));
-            c->counts_capacity = y->dev.n_trials;
-        }
-        SplitArgs S{p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status,
-                    c->d_pairs, cap, c->d_counts, y->d_redo, {}};
+    const bool za_om = (flags & (ARA_RNG_RECORD | ARA_RNG_SUPPLIED)) && (flags & ARA_SU) && occ_max;
+    double ms_ovf = 0.0;
+    uint32_t n_batches = 0;
+    const bool primary = !(flags & ARA_DEBUG_LOOKUP) && (!(flags & ARA_SU) || p->dev.all_sigma_zero) &&
+                         env_u64("ARA_NO_PRIMARY_PATH", 0) == 0;
+    if (primary) {
+        // no draw is taken: one streaming pass over the per-(event, layer)
+        // occurrence losses computed at ara_create_portfolio
+        PrimaryArgs P{p->dev, y->dev, ylt, occ_max, c->d_status, c->d_sched, p->dev.occ, p->dev.occ_lp};
+        CU(cudaMemsetAsync(c->d_sched, 0, sizeof(unsigned long long), c->stream));
+        CU(cudaEventRecord(c->ev[0], c->stream));
+        CU(launch_primary(P, c->stream, c->num_sms));
+        CU(cudaEventRecord(c->ev[1], c->stream));
+        CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    } else if (!exact && !za_om && p->dev.n_layers <= kSplitMaxLayers) {
+        const SplitPlan pl = plan_split(p, y, flags);
+        const uint32_t cap = pl.cap;
+        SplitArgs S{};
+        S.pf = p->dev; S.yet = y->dev; S.seed = seed; S.flags = flags; S.ylt = ylt;
+        S.dbg_count = dbg_count; S.dbg_hash = dbg_hash; S.status = c->d_status; S.cap = cap;
+        S.ovf = y->d_ovf; S.ovf_n = y->d_ovf_n; S.redo = y->d_redo;
         S.occ_max = occ_max;
-        S.rng_mode = (flags & ARA_RNG_RECORD) ? 1u : (flags & ARA_RNG_OCCURRENCE) ? 2u : 0u;
+        S.rng_mode = supplied ? 3u : (flags & ARA_RNG_RECORD) ? 1u : (flags & ARA_RNG_OCCURRENCE) ? 2u : 0u;
+        S.zp_sup = y->d_zprog; S.zp_stride = y->dev.n_events; S.ze_sup = p->d_rec_z;
         S.ze_mask = S.rng_mode == 2 ? 0u : 0xffffffffu;
         S.ze_tag = S.rng_mode == 2 ? 7u : 2u;
-        // 4-byte pairs (record << kbits | k) when both fit: halves the pair traffic
-        if (!(flags & ARA_WIDE_PAIRS)) {
-            uint32_t kb = 1;
-            while (kb < 24 && (1ull << kb) < (uint64_t)y->max_len) ++kb;
-            if ((uint64_t)p->dev.n_dev_records <= (1ull << (32 - kb))) S.kbits = kb;
-        }
+        S.kbits = pl.kbits;
+        const uint64_t pair_bytes = S.kbits ? 4 : 8;
         for (int r = 0; r < 10; ++r) {                   // Philox4x32-10 key schedule of the seed
             S.pkey[2 * r] = (uint32_t)seed + (uint32_t)r * 0x9E3779B9u;
             S.pkey[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;
         }
-        CU(cudaEventRecord(c->ev[0], c->stream));
-        CU(launch_compact(S, c->stream, c->num_sms));
-        CU(cudaEventRecord(c->ev[1], c->stream));
-        CU(launch_sample(S, c->stream, c->num_sms));
-        CU(cudaEventRecord(c->ev[2], c->stream));
+        // batches of trials: batch b's compaction (stream cs) runs beside batch
+        // b-1's sampling (the context stream) on the same SMs; two slots
+        const uint64_t batch = pl.batch;
+        n_batches = pl.n_batches;
+        const bool serial = env_u64("ARA_OVERLAP", 0) == 0;  // two-stream overlap: an experiment (slower)
+        cudaStream_t ss = c->stream, cs = serial ? c->stream : c->cstream;
+        const uint64_t slot_bytes = pl.slot_bytes;
+        CU(grow(&c->d_slots, c->slots_capacity, (serial ? 1 : 2) * slot_bytes));   // (no-op after ara_prepare)
+        CU(grow(&c->d_counts, c->counts_capacity, N));
+        S.counts = c->d_counts;
+        CU(cudaMemsetAsync(c->d_sched, 0, (2 * kMaxBatches + 4) * sizeof(unsigned long long), ss));
+        CU(cudaEventRecord(c->ev[0], ss));
+        if (cs != ss) CU(cudaStreamWaitEvent(cs, c->ev[0], 0));
+        for (uint32_t b = 0; b < n_batches; ++b) {
+            SplitArgs B = S;
+            B.t0 = (uint32_t)(b * batch);
+            B.n_items = (uint32_t)std::min<uint64_t>(batch, N - b * batch);
+            B.pairs = reinterpret_cast<uint2 *>(c->d_slots + (serial ? 0 : (b & 1)) * slot_bytes);
+            cudaEvent_t *te = c->tev + 4 * b;            // compact begin/end, sample begin/end
+            if (b >= 2 && cs != ss) CU(cudaStreamWaitEvent(cs, c->tev[4 * (b - 2) + 3], 0));   // slot free
+            CU(cudaEventRecord(te[0], cs));
+            B.sched = c->d_sched + 2 * b;
+            CU(launch_compact(B, cs, c->num_sms));
+            CU(cudaEventRecord(te[1], cs));
+            if (cs != ss) CU(cudaStreamWaitEvent(ss, te[1], 0));
+            CU(cudaEventRecord(te[2], ss));
+            B.sched = c->d_sched + 2 * b + 1;
+            CU(launch_sample(B, ss, c->num_sms));
+            CU(cudaEventRecord(te[3], ss));
+        }
+        CU(cudaEventRecord(c->ev[1], ss));
+        CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, ss));
+        CU(cudaStreamSynchronize(ss));
+        const uint32_t n_ovf = c->h_status->bad_event ? 0u : c->h_status->n_ovf;
+        if (n_ovf) {
+            // overflow pass: the listed trials compacted again into exactly sized
+            // regions of the pool, then sampled by the same kernel (same arithmetic)
+            std::vector<uint32_t> cnt(n_ovf);
+            std::vector<uint64_t> off(n_ovf);
+            CU(cudaMemcpy(cnt.data(), y->d_ovf_n, n_ovf * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            uint64_t tot = 0;
+            for (uint32_t i = 0; i < n_ovf; ++i) { off[i] = tot; tot += cnt[i]; }
+            CU(grow(&c->d_pool, c->pool_capacity, std::max<uint64_t>(tot, 1) * pair_bytes));
+            CU(grow(&c->d_pool_off, c->pool_off_capacity, n_ovf));
+            CU(cudaMemcpyAsync(c->d_pool_off, off.data(), n_ovf * sizeof(uint64_t), cudaMemcpyHostToDevice, ss));
+            SplitArgs O = S;
+            O.n_items = n_ovf;
+            O.list = y->d_ovf;
+            O.pool_off = c->d_pool_off;
+            O.pairs = reinterpret_cast<uint2 *>(c->d_pool);
+            O.cap = 0xffffffffu;
+            CU(cudaEventRecord(c->ev[2], ss));
+            O.sched = c->d_sched + 2 * kMaxBatches;
+            CU(launch_compact(O, ss, c->num_sms));
+            O.sched = c->d_sched + 2 * kMaxBatches + 1;
+            CU(launch_sample(O, ss, c->num_sms));
+            CU(cudaEventRecord(c->ev[3], ss));
+            CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, ss));
+            CU(cudaStreamSynchronize(ss));
+            float a = 0;
+            CU(cudaEventElapsedTime(&a, c->ev[2], c->ev[3]));
+            ms_ovf = a;
+        }
     } else {
-        // ARA_EXACT (fp64 solve for every sample) or > kSplitMaxLayers layers: the fused kernel
+        // ARA_EXACT (fp64 solve for every sample): the fused kernel
         CU(cudaEventRecord(c->ev[0], c->stream));
+        CU(launch_scan(p->dev, y->dev, seed, supplied ? flags : flags & ~ARA_RNG_SUPPLIED, ylt, dbg_count,
+                       dbg_hash, c->d_status, nullptr, 0, y->d_redo, exact, c->stream, c->num_sms, occ_max,
+                       y->d_zprog, y->dev.n_events, p->d_rec_z));
         CU(cudaEventRecord(c->ev[1], c->stream));
-        CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, nullptr, 0,
-                       y->d_redo, exact, c->stream, c->num_sms, occ_max));
-        CU(cudaEventRecord(c->ev[2], c->stream));
+        CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
     }
-    CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
     const bool redo_launched = c->h_status->n_redo && !c->h_status->bad_event;
+    double ms_redo = 0.0;
     if (redo_launched) {
         // trials that met a table-less record: redo them with the fp64 kernel
         const unsigned int n_redo = c->h_status->n_redo;
         CU(cudaMemsetAsync(&c->d_status->next_trial, 0, sizeof(unsigned long long), c->stream));
-        CU(launch_scan(p->dev, y->dev, seed, flags, ylt, dbg_count, dbg_hash, c->d_status, y->d_redo,
-                       n_redo, nullptr, (flags & ARA_SU) != 0, c->stream, c->num_sms, occ_max));
+        CU(cudaEventRecord(c->ev[2], c->stream));
+        CU(launch_scan(p->dev, y->dev, seed, supplied ? flags : flags & ~ARA_RNG_SUPPLIED, ylt, dbg_count,
+                       dbg_hash, c->d_status, y->d_redo, n_redo, nullptr, (flags & ARA_SU) != 0, c->stream,
+                       c->num_sms, occ_max, y->d_zprog, y->dev.n_events, p->d_rec_z));
         CU(cudaEventRecord(c->ev[3], c->stream));
         CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
-    } else {
-        CU(cudaEventRecord(c->ev[3], c->stream));
-        CU(cudaEventSynchronize(c->ev[3]));
+        float r = 0;
+        CU(cudaEventElapsedTime(&r, c->ev[2], c->ev[3]));
+        ms_redo = r;
     }
-    {
-        float a = 0, b = 0, r = 0;
-        CU(cudaEventElapsedTime(&a, c->ev[0], c->ev[1]));
-        CU(cudaEventElapsedTime(&b, c->ev[1], c->ev[2]));
-        if (redo_launched) CU(cudaEventElapsedTime(&r, c->ev[2], c->ev[3]));
-        c->last_ms[0] = a; c->last_ms[1] = b; c->last_ms[2] = r;
+    {   // device time of each kernel, summed over its launches (they overlap across streams)
+        double a = 0.0, b = 0.0;
+        for (uint32_t q = 0; q < n_batches; ++q) {
+            float x = 0, z = 0;
+            CU(cudaEventElapsedTime(&x, c->tev[4 * q], c->tev[4 * q + 1]));
+            CU(cudaEventElapsedTime(&z, c->tev[4 * q + 2], c->tev[4 * q + 3]));
+            a += x; b += z;
+        }
+        if (!n_batches) {
+            float x = 0;
+            CU(cudaEventElapsedTime(&x, c->ev[0], c->ev[1]));
+            b = x;
+        }
+        c->last_ms[0] = a; c->last_ms[1] = b; c->last_ms[2] = ms_ovf + ms_redo;
+        c->last_batches = n_batches;
+        c->last_launches = (n_batches ? 2 * n_batches : 1) + (ms_ovf > 0.0 ? 2 : 0) + (redo_launched ? 1 : 0);
     }
     if (c->h_status->bad_event) {      // error path: count the offending occurrences
         CU(launch_count_bad(y->d_events, y->dev.n_events, p->dev.catalog, &c->d_status->bad_event, c->stream,
@@ -740,6 +979,27 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
     if (c->h_status->nonconverged)
         return fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples",
                     c->h_status->nonconverged);
+    return ARA_OK;
+}
+
+int ara_prepare(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint32_t flags) {
+    if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
+    CU(cudaSetDevice(c->device));
+    const std::vector<const ara_portfolio *> groups =
+        p->groups.empty() ? std::vector<const ara_portfolio *>{p}
+                          : std::vector<const ara_portfolio *>(p->groups.begin(), p->groups.end());
+    for (const ara_portfolio *g : groups) {
+        const SplitPlan pl = plan_split(g, y, flags);
+        CU(grow(&c->d_slots, c->slots_capacity, (env_u64("ARA_OVERLAP", 0) ? 2 : 1) * pl.slot_bytes));
+    }
+    CU(grow(&c->d_counts, c->counts_capacity, std::max<uint64_t>(y->dev.n_trials, 1)));
+    return ARA_OK;
+}
+
+int ara_last_run_launches(const ara_ctx *c, uint32_t *kernel_launches, uint32_t *batches) {
+    if (!c) return fail(ARA_EINVAL, "ctx is NULL");
+    if (kernel_launches) *kernel_launches = c->last_launches;
+    if (batches) *batches = c->last_batches;
     return ARA_OK;
 }
 

@@ -83,6 +83,10 @@ struct PortfolioDev {
     const SplitRec *srecs;    // [n_dev_records]
     const uint2 *mu_meta;     // [n_dev_records] (mean loss bits, rec_meta): one 8 B gather per pair with SU off
     uint32_t any_terms;       // some slot has XELT terms (G7)
+    uint32_t all_sigma_zero;  // every record has sigma_I = sigma_C = 0 (no draw is ever taken, G10)
+    uint32_t occ_lp;          // occurrence losses per event in occ (n_layers rounded up to 1, 2, 4, 8)
+    const float *occ;         // [catalog][occ_lp] occurrence loss of each (event, layer) without draws
+                              // (lines 6-11 at the mean losses; the primary-uncertainty fast path)
     const SlotInfo *slots;    // [n_slots]
     const LayerInfo *layers;  // [n_layers]
 };
@@ -98,19 +102,22 @@ struct YetDev {
 
 // device-side status words
 struct RunStatus {
-    unsigned long long next_trial;   // dynamic trial scheduler
-    unsigned long long next_trial2;  // ... of the second kernel of the split path
+    unsigned long long next_trial;   // dynamic trial scheduler of the fused kernel
+    unsigned long long pad0;
     unsigned int nonconverged;       // fp64 solves that did not converge
     unsigned int bad_event;          // != 0: some event id >= catalog (count on the error path)
-    unsigned int n_redo;             // trials touching a table-less record
-    unsigned int pad;
+    unsigned int n_redo;             // trials touching a table-less record (fp64 kernel)
+    unsigned int n_ovf;              // trials whose pairs overflowed their batch region
 };
 
-// the split (two-kernel) scan: compact_kernel writes each trial's present
-// pairs {device record, occurrence k} to pairs[t * cap ...] and their count to
-// counts[t] (kOverflow if more than cap); sample_kernel samples them
+// The split (two-kernel) scan, run batch by batch on two streams:
+// compact_kernel writes each trial's present pairs {device record, k} to its
+// region of the batch's slot (cap pairs) and their count to counts[t]
+// (kOverflow if more than cap: the trial is listed in ovf / ovf_n with its
+// exact count and compacted again by the overflow pass into an exactly
+// sized region of the overflow pool); sample_kernel samples them.
 constexpr uint32_t kOverflow = 0xffffffffu;
-constexpr uint32_t kSplitMaxLayers = 8;   // larger portfolios take the fused kernel
+constexpr uint32_t kSplitMaxLayers = 8;   // larger portfolios run in groups of layers
 struct SplitArgs {
     PortfolioDev pf;
     YetDev yet;
@@ -120,17 +127,44 @@ struct SplitArgs {
     uint32_t *dbg_count;
     uint64_t *dbg_hash;
     RunStatus *status;
-    uint2 *pairs;
-    uint32_t cap;
-    uint32_t *counts;
-    uint32_t *redo;
-    uint32_t pkey[20];        // Philox key schedule of the seed (round r: pkey[2r], pkey[2r+1])
-    uint32_t xcap;            // sample_kernel: pairs per segment (set by launch_sample)
-    uint32_t kbits;           // > 0: pairs packed in 4 B as device record << kbits | k (two-kernel path)
-    float *occ_max;           // null, or [n_layers][n_trials] largest occurrence loss (G29)
-    uint32_t rng_mode;        // 0: reading G2; 1: ARA_RNG_RECORD; 2: ARA_RNG_OCCURRENCE
-    uint32_t ze_mask, ze_tag; // z_(E) counter (trial, k, elt & ze_mask, ze_tag) in modes 0 and 2
+    // work items of this launch: trial t0 + i (batch), or list[i] (overflow pass)
+    uint32_t t0, n_items;
+    const uint32_t *list;
+    const uint64_t *pool_off;     // overflow pass: region of item i in the pool (pair units)
+    unsigned long long *sched;    // this launch's dynamic-scheduler counter (zeroed)
+    uint2 *pairs;                 // the batch's slot, or the overflow pool
+    uint32_t cap;                 // pairs per batch region
+    uint32_t *counts;             // [n_trials]
+    uint32_t *ovf, *ovf_n;        // overflowing trials and their exact pair counts (status->n_ovf)
+    uint32_t *redo;               // trials with a table-less record (fp64 kernel)
+    uint32_t pkey[20];            // Philox key schedule of the seed (round r: pkey[2r], pkey[2r+1])
+    uint32_t kbits;               // > 0: pairs packed in 4 B as device record << kbits | k
+    float *occ_max;               // null, or [n_layers][n_trials] largest occurrence loss (G29)
+    uint32_t rng_mode;            // 0: reading G2; 1: ARA_RNG_RECORD; 2: ARA_RNG_OCCURRENCE; 3: ARA_RNG_SUPPLIED
+    const float *zp_sup;          // mode 3: z_(Prog,E) per YET occurrence, [program][zp_stride]
+    uint64_t zp_stride;           // occurrences of the YET
+    const float *ze_sup;          // mode 3: z_(E) per device record
+    uint32_t ze_mask, ze_tag;     // z_(E) counter (trial, k, elt & ze_mask, ze_tag) in modes 0 and 2
 };
+size_t sample_smem_bytes(uint32_t n_layers, bool occ_max);
+// cached attribute / occupancy set-up of a kernel launch (per device)
+cudaError_t prepare_launch(const void *kern, size_t smem, int threads, int &per_sm);
+
+// the primary-uncertainty fast path (ara_primary.cu)
+struct PrimaryArgs {
+    PortfolioDev pf;
+    YetDev yet;
+    float *ylt;
+    float *occ_max;
+    RunStatus *status;
+    unsigned long long *sched;
+    const float *occ;
+    uint32_t lp;
+};
+cudaError_t launch_primary(const PrimaryArgs &A, cudaStream_t s, int num_sms);
+void launch_occ_table(const uint2 *cidx, const uint32_t *rec_meta, const float *rec_mu, const double *slot_terms,
+                      const LayerInfo *layers, uint32_t n_layers, uint32_t lp, uint32_t catalog, float *out,
+                      cudaStream_t s);
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_unpack_yet(const uint32_t *packed, uint64_t n, uint32_t bits, uint32_t *out, cudaStream_t s,
@@ -152,7 +186,8 @@ void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_
 cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed, uint32_t flags,
                         float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
                         const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
-                        cudaStream_t s, int num_sms, float *occ_max = nullptr);
+                        cudaStream_t s, int num_sms, float *occ_max = nullptr, const float *zp_sup = nullptr,
+                        uint64_t zp_stride = 0, const float *ze_sup = nullptr);
 cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float2 *hot,
                                  const float *zp,
                                  const float *ze, uint64_t n, bool exact, float *out,

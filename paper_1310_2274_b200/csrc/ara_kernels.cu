@@ -175,6 +175,9 @@ struct ScanArgs {
     uint64_t n_list;
     uint32_t *redo;                 // trials to re-run with the fp64 kernel
     float *occ_max;                 // null, or [n_layers][n_trials] largest occurrence loss (G29)
+    const float *zp_sup;            // ARA_RNG_SUPPLIED: z_(Prog,E) [program][zp_stride]
+    uint64_t zp_stride;
+    const float *ze_sup;            // ARA_RNG_SUPPLIED: z_(E) per device record
 };
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
@@ -224,7 +227,11 @@ struct SampleArgs {
     RunStatus *status;
     uint64_t seed;
     bool exact;
-    uint32_t rng;                   // 0: reading G2; 1: ARA_RNG_RECORD; 2: ARA_RNG_OCCURRENCE
+    uint32_t rng;                   // 0: reading G2; 1: ARA_RNG_RECORD; 2: ARA_RNG_OCCURRENCE; 3: ARA_RNG_SUPPLIED
+    const float *zp_sup;            // rng 3: z_(Prog,E) per YET occurrence, [program][zp_stride]
+    uint64_t zp_stride;
+    const float *ze_sup;            // rng 3: z_(E) per device record
+    uint64_t occ_base;              // rng 3: the current trial's first occurrence in the YET
 };
 
 // z_(E) of device record `rec` (XELT si.elt) at occurrence k of trial i (G2 and its alternatives)
@@ -233,29 +240,6 @@ __device__ __forceinline__ uint32_t draw_ze(const SampleArgs &G, const SlotInfo 
     if (G.rng == 1) return philox_lane0(__ldg(G.rec_orig + rec), si.elt, 0u, 6u, G.seed);
     if (G.rng == 2) return philox_lane0(trial_g, k, 0u, 7u, G.seed);
     return philox_lane0(trial_g, k, si.elt, 2u, G.seed);
-}
-
-// one loss draw for queue entry e (Alg.1 lines 7-8); r already loaded
-template <bool EX>
-__device__ __forceinline__ float draw_one(const SampleArgs &G, const SlotInfo &si, const BetaRec &r,
-                                          uint2 e, uint32_t trial_g, int &redo) {
-    float x;
-    if (r.mode == kModeDegenerate) {
-        x = r.scale;
-    } else if (!EX && r.mode == kModeExact) {
-        x = 0.0f;                       // table-less record: this trial is redone by the fp64 kernel
-        redo = 1;
-    } else {
-        const uint32_t k = e.y >> 8;
-        const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, G.seed);   // z_(Prog,E)
-        const uint32_t be = draw_ze(G, si, e.x, trial_g, k);                  // z_(E)
-        const float v = combine_v(r, norm_quantile_from_bits(bp), norm_quantile_from_bits(be));
-        bool ok;
-        x = sample_loss_from_v<EX>(r, G.tables, G.hot, e.x, v, G.exact, ok);
-        if (!ok) atomicAdd(&G.status->nonconverged, 1u);
-    }
-    if (si.has_terms) x = si.share * fminf(fmaxf(x - si.ret, 0.0f), si.lim);
-    return x;
 }
 
 // Sample every queued pair, reduce the (occurrence, layer) segments, apply the
@@ -288,9 +272,14 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
             for (int u = 0; u < U; ++u) {
                 const SlotInfo &si = slots[e[u].y & 0xffu];
                 const uint32_t k = e[u].y >> 8;
-                const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, G.seed);   // z_(Prog,E)
-                const uint32_t be = draw_ze(G, si, e[u].x, trial_g, k);              // z_(E)
-                v[u] = combine_v(r[u], norm_quantile_from_bits(bp), norm_quantile_from_bits(be));
+                if (G.rng == 3) {                    // supplied with the inputs
+                    const float zp = __ldg(G.zp_sup + (uint64_t)si.prog * G.zp_stride + G.occ_base + k);
+                    v[u] = combine_v(r[u], norm_quantile_f(zp), norm_quantile_f(__ldg(G.ze_sup + e[u].x)));
+                } else {
+                    const uint32_t bp = philox_lane0(trial_g, k, si.prog, 1u, G.seed);   // z_(Prog,E)
+                    const uint32_t be = draw_ze(G, si, e[u].x, trial_g, k);              // z_(E)
+                    v[u] = combine_v(r[u], norm_quantile_from_bits(bp), norm_quantile_from_bits(be));
+                }
             }
             float2 n0[U], n1[U];
             int ti[U];
@@ -561,9 +550,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
     unsigned int *cntv = wcnt(M);
     unsigned int *omv = wom(M);
     const bool dbg = DBG;
-    const SampleArgs G{A.pf.recs, A.pf.tables, A.pf.hot, A.pf.rec_mu, A.pf.rec_orig, A.status, A.seed,
-                       (A.flags & ARA_EXACT) != 0,
-                       (A.flags & ARA_RNG_RECORD) ? 1u : (A.flags & ARA_RNG_OCCURRENCE) ? 2u : 0u};
+    SampleArgs G{A.pf.recs, A.pf.tables, A.pf.hot, A.pf.rec_mu, A.pf.rec_orig, A.status, A.seed,
+                 (A.flags & ARA_EXACT) != 0,
+                 (A.flags & ARA_RNG_SUPPLIED) ? 3u : (A.flags & ARA_RNG_RECORD) ? 1u : (A.flags & ARA_RNG_OCCURRENCE) ? 2u : 0u,
+                 A.zp_sup, A.zp_stride, A.ze_sup, 0};
     const uint64_t n_trials = A.yet.n_trials;
     const uint64_t n_work = A.trial_list ? A.n_list : n_trials;
     const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift;
@@ -580,6 +570,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
         const uint64_t base = A.yet.fixed_len ? t * (uint64_t)A.yet.fixed_len : A.yet.offsets[t];
         const uint32_t len = A.yet.fixed_len ? A.yet.fixed_len : (uint32_t)(A.yet.offsets[t + 1] - base);
         const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);        // global trial index i
+        G.occ_base = base;
         for (uint32_t l = lane; l < nl; l += 32) { S[l] = 0.0; cntv[l] = 0u; hsh[l] = 0ull; omv[l] = 0u; }
         __syncwarp();
         int q = 0;                         // packed queue state (qn, nseg, redo)
@@ -684,8 +675,6 @@ static size_t scan_smem_bytes(const PortfolioDev &pf) {
            ((size_t)pf.bitmap_words * 4 + 15) / 16 * 16 + kWarps * per_warp;
 }
 
-size_t scan_smem_for(const PortfolioDev &pf) { return scan_smem_bytes(pf); }
-
 template <bool SU, bool EX, int MW>
 static cudaError_t launch_scan_t(const ScanArgs &A, cudaStream_t s, int num_sms) {
     const size_t smem = scan_smem_bytes(A.pf);
@@ -712,8 +701,10 @@ static cudaError_t launch_scan_mw(const ScanArgs &A, bool exact_kernel, cudaStre
 cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed, uint32_t flags,
                         float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
                         const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
-                        cudaStream_t s, int num_sms, float *occ_max) {
-    ScanArgs A{pf, yet, seed, flags, ylt, dbg_count, dbg_hash, status, trial_list, n_list, redo, occ_max};
+                        cudaStream_t s, int num_sms, float *occ_max, const float *zp_sup, uint64_t zp_stride,
+                        const float *ze_sup) {
+    ScanArgs A{pf, yet, seed, flags, ylt, dbg_count, dbg_hash, status, trial_list, n_list, redo, occ_max,
+               zp_sup, zp_stride, ze_sup};
     if (trial_list && n_list == 0) return cudaSuccess;
     if (pf.mask_words == 1) return launch_scan_mw<1>(A, exact_kernel, s, num_sms);
     if (pf.mask_words <= 3) return launch_scan_mw<3>(A, exact_kernel, s, num_sms);

@@ -15,6 +15,8 @@
 
 namespace ara {
 
+constexpr int kMaxDevices = 64;
+
 namespace cg = cooperative_groups;
 
 __device__ __forceinline__ uint32_t okey(float v) {
@@ -73,22 +75,6 @@ __global__ void select_digit_kernel(SelectState *st, const unsigned int *hist, i
     st->k_rem = need;
     st->prefix |= (uint32_t)d << shift;
     st->pmask |= 0xffu << shift;
-}
-
-__global__ void tail_compact_kernel(const float *vals, uint64_t n, SelectState *st, float *buf,
-                               uint32_t cap) {
-    const uint32_t T = st->prefix;
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        const float v = vals[t];
-        const uint32_t k = okey(v);
-        if (k > T) {
-            const unsigned long long p = atomicAdd(&st->n_gt, 1ull);
-            if (p < cap) buf[p] = v;
-        } else if (k == T) {
-            atomicAdd(&st->n_eq, 1ull);
-        }
-    }
 }
 
 // The whole select in one cooperative launch: gather (or roll-up) -> 4 radix
@@ -395,13 +381,16 @@ cudaError_t launch_measures_multi(const float *ylt, uint32_t n_layers, uint64_t 
         M.i_fl[q] = idx(fl); M.i_fl1[q] = idx(fl + 1); M.i_m[q] = idx(m);
     }
     M.nq = n_rp;
-    static int blocks = 0;                            // co-resident blocks of the cooperative launch
+    static int blocks_by_dev[kMaxDevices] = {};      // co-resident blocks of the cooperative launch, per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int &blocks = blocks_by_dev[dev % kMaxDevices];
     if (!blocks) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_multi_kernel, kMultiThreads, 0);
-        blocks = sms * (per_sm < 1 ? per_sm : 1);
+        blocks = sms * std::min(per_sm, 1);           // one block per SM (0 if it cannot be resident)
+        if (!blocks) return cudaErrorCooperativeLaunchTooLarge;
     }
     const uint64_t per = n_total / n_shards;
     float *vals = S.vals;
@@ -646,13 +635,16 @@ cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_tota
                             MeasuresScratch &S, double *d_out, cudaStream_t s) {
     const uint64_t per = n_total / n_shards;
     {
-        static int coop_blocks = 0;                   // co-resident blocks of the cooperative select
+        static int coop_by_dev[kMaxDevices] = {};    // co-resident blocks of the cooperative select, per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int &coop_blocks = coop_by_dev[dev % kMaxDevices];
         if (!coop_blocks) {
-            int dev = 0, sms = 0, per_sm = 0;
-            cudaGetDevice(&dev);
+            int sms = 0, per_sm = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_coop_kernel, 256, 0);
-            coop_blocks = sms * (per_sm < 4 ? per_sm : 4);
+            coop_blocks = sms * std::min(per_sm, 4);
+            if (!coop_blocks) return cudaErrorCooperativeLaunchTooLarge;
         }
         float *vals = S.vals, *buf = S.buf;
         unsigned int *hist = S.hist;
@@ -673,7 +665,10 @@ cudaError_t launch_measures(const float *ylt, uint32_t n_layers, uint64_t n_tota
                  : P <= 4096 ? (K)sort_measures_kernel<4> : P <= 8192 ? (K)sort_measures_kernel<8>
                  : P <= 16384 ? (K)sort_measures_kernel<16> : (K)sort_measures_kernel<32>;
     const size_t smem = sizeof(float) * P;
-    static bool attr_set = false;                     // once per process (all six instantiations)
+    static bool attr_by_dev[kMaxDevices] = {};       // once per device (all six instantiations)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    bool &attr_set = attr_by_dev[dev % kMaxDevices];
     if (!attr_set) {
         const K all[] = {sort_measures_kernel<1>, sort_measures_kernel<2>, sort_measures_kernel<4>,
                          sort_measures_kernel<8>, sort_measures_kernel<16>, sort_measures_kernel<32>};

@@ -7,10 +7,10 @@
 //                    {device record, k} written to a fixed-capacity region
 //                    of HBM
 //   sample_kernel  : per trial, dense 64-pair rounds of draws (line 7,
-//                    section 3) and XELT terms (line 8), then the
-//                    per-occurrence sums (line 9), occurrence terms (line 11),
-//                    trial sums, aggregate terms (line 12) -> YLT (line 17).
-//                    Bound by the ALU pipes.
+//                    section 3) and XELT terms (line 8), the per-occurrence
+//                    sums (line 9) by segmented warp scans in registers,
+//                    occurrence terms (line 11), trial sums, aggregate terms
+//                    (line 12) -> YLT (line 17).  Bound by the ALU pipes.
 //
 // A trial whose pairs overflow its region, or that meets a table-less record,
 // is listed for the fused fp64-capable kernel (ara_kernels.cu).
@@ -28,38 +28,25 @@ namespace ara {
 
 namespace {
 
-#ifndef ARA_COMPACT_DEPTH
-#define ARA_COMPACT_DEPTH 2           // chunks between index-entry loads and their use
+// One CTA of 32 warps per SM for each kernel, <= 64 registers per thread.
+// (16 + 16 warps, so that a batch's compaction could share the SMs with the
+// previous batch's sampling on a second stream, measured slower: both
+// kernels load the L1/LSU pipe.)
+#ifndef ARA_COMPACT_WARPS
+#define ARA_COMPACT_WARPS 32
 #endif
-#ifndef ARA_COMPACT_PREFETCH
-#define ARA_COMPACT_PREFETCH 0        // bulk L2 prefetch of each warp's next trial of YET (measured: no gain)
-#endif
-#ifndef ARA_CIDX_CG
-#define ARA_CIDX_CG 1                 // index-entry gathers through L2 only (ld.global.cg): no L1 reuse
-#endif
-#ifndef ARA_COMPACT_BALLOT_SCAN
-#define ARA_COMPACT_BALLOT_SCAN 1     // pair prefix sums by ballots instead of shuffles
-#endif
-#ifndef ARA_COMPACT_THREADS
-#define ARA_COMPACT_THREADS 1024
-#endif
-constexpr int kCompactThreads = ARA_COMPACT_THREADS;   // compaction: 1 CTA per SM (bitmap in shared memory)
+constexpr int kCompactThreads = ARA_COMPACT_WARPS * 32;   // compaction (bitmap in shared memory)
 #ifndef ARA_SAMPLE_WARPS
 #define ARA_SAMPLE_WARPS 32
 #endif
-#ifndef ARA_SAMPLE_MINB
-#define ARA_SAMPLE_MINB 1
-#endif
-constexpr int kSampleWarps = ARA_SAMPLE_WARPS;   // sampling: 1 CTA of 1024 threads per SM
-#ifndef ARA_SAMPLE_SMEM_KB
-#define ARA_SAMPLE_SMEM_KB 96
-#endif
+constexpr int kSampleWarps = ARA_SAMPLE_WARPS;            // sampling
 #ifndef ARA_SAMPLE_U
 #define ARA_SAMPLE_U 2                // pairs per lane in flight per sampler round
 #endif
 constexpr int kU = ARA_SAMPLE_U;
-constexpr uint32_t kXCapMax = 1024;     // pairs per sampler segment (a multiple of 64, >= ARA_MAX_SLOTS,
-                                        // sized at launch to what 2 CTAs/SM leave in shared memory)
+constexpr uint32_t kXCap = 512;       // pairs per sampler segment (a multiple of 32 kU, >= ARA_MAX_SLOTS; the
+                                      // shared memory left to L1 serves the record and table gathers)
+static_assert(kXCap % (32 * kU) == 0 && kXCap >= ARA_MAX_SLOTS, "segment must hold one occurrence");
 
 __device__ __forceinline__ uint64_t splitmix64_(uint64_t z) {
     z += 0x9E3779B97F4A7C15ull;
@@ -91,11 +78,6 @@ template <class T>
 __device__ __forceinline__ T xl_clip_t_(T d, T lim) {
     return d > (T)0 ? (d < lim ? d : lim) : (T)0;
 }
-#ifndef ARA_RUNSUM_F32
-#define ARA_RUNSUM_F32 1              // in-stretch run sums and occurrence clips in fp32 (G28)
-#endif
-using RunT = std::conditional<ARA_RUNSUM_F32 != 0, float, double>::type;
-
 __device__ __forceinline__ double warp_sum_f64_(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -105,31 +87,35 @@ __device__ __forceinline__ double warp_sum_f64_(double v) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// compact_kernel: one warp per trial (static interleave: trial = global warp +
-// r * warps in the grid), persistent, one CTA per SM (the bitmap, <= 128 KiB,
-// in shared memory).  The warp walks the flat sequence of 128-event chunks of
-// its trials as a register pipeline:
+// compact_kernel: one warp per trial (dynamic scheduler), persistent, one CTA
+// per SM (the bitmap, <= 128 KiB, in shared memory).  A launch covers the
+// work items of one batch of trials (item i = trial t0 + i) or of a list
+// (item i = trial list[i]: the overflow pass).  The warp walks the flat
+// sequence of 128-event chunks of its items as a register pipeline:
 //   fetch   : one uint4 per lane (evict-first), two chunks in flight
 //   stage A : presence bitmap (branch-free) and, for the hits, the event's
 //             index entry (first device record, record count) from L2: loads
 //             issued
 //   stage B : one chunk later, so the entry loads overlap stage A of the next
 //             chunk: the present pairs {device record, k} written in
-//             (occurrence, slot) order to the trial's region of HBM (an
-//             event's records are consecutive, event-major in slot order, so
-//             its pairs are first .. first + count - 1)
-// counts[t] = pairs of trial t, or kOverflow (then t is appended to redo; the
-// pairs past its region are dropped).
+//             (occurrence, slot) order to the item's region (an event's
+//             records are consecutive, event-major in slot order, so its
+//             pairs are first .. first + count - 1)
+// Batch items: region i of the batch's slot, cap pairs; counts[t] = pairs of
+// trial t, or kOverflow -- then (t, exact count) is appended to the overflow
+// list and the overflow pass compacts t again into an exactly sized region
+// of the overflow pool, for the same sampler.
 // ---------------------------------------------------------------------------
 struct RawChunk {
     uint4 v;                        // this lane's 4 event ids
-    uint32_t t, c, len;             // trial (>= n_trials: none), chunk, trial length
+    uint32_t t, c, len;             // item (kNoItem: none), chunk, trial length
 };
 
 struct ChunkA {                     // stage A output of one chunk
     uint2 ci[4];                    // (first record, count) of this lane's 4 events (0 if absent)
     uint32_t t, c, len;
 };
+constexpr uint32_t kNoItem = 0xffffffffu;
 
 // predicated 4-byte store to a global address (no branch)
 __device__ __forceinline__ void st_u32_if(bool p, uint64_t addr, uint32_t a) {
@@ -145,19 +131,22 @@ __device__ __forceinline__ void st_pair_if(bool p, uint64_t addr, uint32_t a, ui
                  : "memory");
 }
 
-// The compaction pipeline of one warp over the trials first_warp, first_warp
-// + nw, ...  Sink: begin(t) -> the region for trial t's pairs (warp-uniform),
-// end(t, n) after its last chunk (n > cap: overflow).
+// trial of work item i
+__device__ __forceinline__ uint32_t item_trial(const SplitArgs &A, uint32_t i) {
+    return A.list ? __ldg(A.list + i) : A.t0 + i;
+}
+
+// The compaction pipeline of one warp over the items it claims from the
+// launch's scheduler.  Sink: begin(i) -> the region of item i's pairs
+// (warp-uniform), end(i, n) after its last chunk (n > cap: overflow).
 // BM: 0 = bitmap shift 0 and a sentinel event (lanes past a trial's end hold
 // an id whose presence bit is 0, so no length test per event), 1 = any shift
 // with the sentinel, 2 = any shift, length test per event.
 template <bool PK, int BM, class Sink>
-__device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t *bitmap, uint32_t first_warp,
-                                              uint32_t nw, Sink &sink) {
+__device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t *bitmap, Sink &sink) {
     const int lane = threadIdx.x & 31;
-    const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift, cap = A.cap;
-    const uint32_t n_trials = (uint32_t)A.yet.n_trials;    // <= 2^32 - 1 (ara_load_yet)
-    (void)C;
+    const uint32_t shift = A.pf.bitmap_shift, cap = A.cap;
+    const uint32_t n_items = A.n_items;
     const uint32_t *events = A.yet.events;
     const uint64_t *offsets = A.yet.offsets;
     const uint2 *__restrict__ cidx = A.pf.cidx;
@@ -166,35 +155,26 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
     const bool vec = offsets == nullptr && (K & 3u) == 0;   // every chunk 16 B aligned
     const uint32_t sent = BM == 2 ? 0u : A.pf.sentinel_event;
 
-    // fetch side: position in the flat chunk sequence (warp-uniform)
-    uint32_t pt = first_warp;
+    // fetch side: the item being fetched and the chunk within it (warp-uniform)
+    uint32_t pt = kNoItem;
     uint32_t pc = 0, plen = 0;
     uint64_t pbase = 0;
-    auto set_trial = [&]() {
-        if (pt < n_trials) {
-            if (offsets) { pbase = offsets[pt]; plen = (uint32_t)(offsets[pt + 1] - pbase); }
-            else { pbase = (uint64_t)pt * K; plen = K; }
-#if ARA_COMPACT_PREFETCH
-            // the warp's next trial, one bulk L2 prefetch: its chunk loads then
-            // wait on L2, not HBM (no registers held for the lead)
-            const uint32_t nt = pt + nw;
-            if (lane == 0 && nt > pt && nt < n_trials) {
-                uint64_t b0, b1;
-                if (offsets) { b0 = offsets[nt]; b1 = offsets[nt + 1]; }
-                else { b0 = (uint64_t)nt * K; b1 = b0 + K; }
-                const uint64_t a0 = reinterpret_cast<uint64_t>(events + b0) & ~15ull;
-                const uint64_t a1 = (reinterpret_cast<uint64_t>(events + b1) + 15ull) & ~15ull;
-                if (a1 > a0)
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
-                                 : "memory");
-            }
-#endif
+    auto next_item = [&]() {                          // claim the next item of the launch
+        uint32_t i = 0;
+        if (lane == 0) i = (uint32_t)atomicAdd(A.sched, 1ull);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        pt = i < n_items ? i : kNoItem;
+        pc = 0;
+        if (pt != kNoItem) {
+            const uint32_t t = item_trial(A, pt);
+            if (offsets) { pbase = offsets[t]; plen = (uint32_t)(offsets[t + 1] - pbase); }
+            else { pbase = (uint64_t)t * K; plen = K; }
         }
     };
     auto fetch = [&](RawChunk &r) {
-        r.t = pt; r.c = pc; r.len = pt < n_trials ? plen : 0u;    // (no events past the last trial)
+        r.t = pt; r.c = pc; r.len = pt != kNoItem ? plen : 0u;
         r.v = make_uint4(sent, sent, sent, sent);
-        if (pt < n_trials) {
+        if (pt != kNoItem) {
             const uint32_t k = pc * 128u + 4u * lane;
             const uint32_t *src = events + pbase + k;
             if (vec) {
@@ -205,7 +185,7 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
                 if (k + 2 < plen) r.v.z = __ldcs(src + 2);
                 if (k + 3 < plen) r.v.w = __ldcs(src + 3);
             }
-            if ((pc + 1) * 128u >= plen) { pt = pt + nw < pt ? n_trials : pt + nw; pc = 0; set_trial(); }
+            if ((pc + 1) * 128u >= plen) next_item();
             else ++pc;
         }
     };
@@ -220,12 +200,8 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
             bool hit = __funnelshift_r(w, 0u, bit) & 1u;      // w >> (bit & 31)
             if (BM == 2) hit = hit && k0 + q < r.len;
             S.ci[q] = make_uint2(0u, 0u);
-            asm volatile(                                 // predicated load, no branch
-#if ARA_CIDX_CG
+            asm volatile(                                 // predicated load through L2, no branch
                 "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.cg.v2.u32 {%0, %1}, [%3];\n}"
-#else
-                "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.nc.v2.u32 {%0, %1}, [%3];\n}"
-#endif
                 : "+r"(S.ci[q].x), "+r"(S.ci[q].y)
                 : "r"((uint32_t)hit), "l"(cidx + ee[q]));
         }
@@ -234,13 +210,12 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
     // event has one pair in ~87 % of cases (cfg3), so the first pairs are
     // predicated stores and the rest one warp-uniform loop over the extra
     // pairs (usually one pass).
-    uint32_t n = 0;                                   // pairs of the current trial (warp-uniform)
-    uint2 *out = nullptr;                             // the current trial's pair region
+    uint32_t n = 0;                                   // pairs of the current item (warp-uniform)
+    uint2 *out = nullptr;                             // the current item's pair region
     auto stage_b = [&](const ChunkA &S) {
         if (S.c == 0) n = 0;
         const uint32_t k0 = S.c * 128u + 4u * lane;
         const uint32_t np = S.ci[0].y + S.ci[1].y + S.ci[2].y + S.ci[3].y;
-#if ARA_COMPACT_BALLOT_SCAN
         // exclusive warp prefix of np, bit-sliced over ballots (votes, no
         // shuffles through the shared-memory pipe): 3 slices unless some
         // lane has >= 8 pairs in the chunk; np <= 4 * ARA_MAX_SLOTS = 896
@@ -264,17 +239,6 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         }
         if (S.c == 0) out = sink.begin(S.t);
         uint32_t pos = n + excl;
-#else
-        uint32_t incl = np;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        if (S.c == 0) out = sink.begin(S.t);
-        uint32_t pos = n + incl - np;
-#endif
         if (n + tot <= cap) {                         // the chunk fits (warp-uniform)
             // one 64-bit address per event, predicated stores (no branches)
             uint32_t pq[4], mx = 0, o = pos;
@@ -308,88 +272,66 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
                     for (int q = 0; q < 4; ++q)
                         st_pair_if(j < S.ci[q].y, reinterpret_cast<uint64_t>(out + (pq[q] + j)), S.ci[q].x + j, k0 + q);
             }
-        } else {                                      // overflow: the trial is redone by the fused kernel
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t f = S.ci[q].x, m = S.ci[q].y;
-#pragma unroll 1
-                for (uint32_t j = 0; j < m; ++j)
-                    if (pos + j < cap) {
-                        if (PK) reinterpret_cast<uint32_t *>(out)[pos + j] = ((f + j) << A.kbits) | (k0 + q);
-                        else out[pos + j] = make_uint2(f + j, k0 + q);
-                    }
-                pos += m;
-            }
         }
+        // (a chunk that does not fit: nothing is stored, the count goes on --
+        // the overflow pass compacts the trial again into an exact region)
         n += tot;
-        if ((S.c + 1) * 128u >= S.len) sink.end(S.t, n);           // last chunk of the trial
+        if ((S.c + 1) * 128u >= S.len) sink.end(S.t, n);           // last chunk of the item
     };
 
-    set_trial();
-#if ARA_COMPACT_DEPTH == 3
-    // three-deep: while chunk X is in stage B, the index entries of chunks
-    // X+1 and X+2 are in flight (L2) and chunks X+3.. from HBM
-    RawChunk ra, rb, rc;
-    ChunkA ca, cb, cc;
-    fetch(ra);
-    fetch(rb);
-    fetch(rc);
-    stage_a(ra, ca);
-    fetch(ra);
-    stage_a(rb, cb);
-    fetch(rb);
-    while (ca.t < n_trials) {
-        stage_a(rc, cc);
-        fetch(rc);
-        stage_b(ca);
-        if (cb.t >= n_trials) break;
-        stage_a(ra, ca);
-        fetch(ra);
-        stage_b(cb);
-        if (cc.t >= n_trials) break;
-        stage_a(rb, cb);
-        fetch(rb);
-        stage_b(cc);
-    }
-#else
     // ping-pong: while chunk X is in stage B, chunk X+1 is in stage A and
     // chunks X+2, X+3 are in flight from HBM
+    next_item();
     RawChunk ra, rb;
     ChunkA ca, cb;
     fetch(ra);
     fetch(rb);
     stage_a(ra, ca);
     fetch(ra);
-    while (ca.t < n_trials) {
+    while (ca.t != kNoItem) {
         stage_a(rb, cb);
         fetch(rb);
         stage_b(ca);
-        if (cb.t >= n_trials) break;
+        if (cb.t == kNoItem) break;
         stage_a(ra, ca);
         fetch(ra);
         stage_b(cb);
     }
-#endif
 }
 
-// compact_kernel's sink: per-trial regions of HBM; counts[t] = pairs or kOverflow
-struct HbmSink {
+// batch items: region i of the batch's slot; counts[t] = pairs or kOverflow,
+// an overflowing trial listed with its exact pair count
+struct SlotSink {
     const SplitArgs &A;
-    __device__ uint2 *begin(uint32_t t) const {     // (packed pairs: half-size regions, same bytes)
-        return A.kbits ? reinterpret_cast<uint2 *>(reinterpret_cast<uint32_t *>(A.pairs) + (uint64_t)t * A.cap)
-                       : A.pairs + (uint64_t)t * A.cap;
+    __device__ uint2 *begin(uint32_t i) const {     // (packed pairs: 4-byte regions)
+        return A.kbits ? reinterpret_cast<uint2 *>(reinterpret_cast<uint32_t *>(A.pairs) + (uint64_t)i * A.cap)
+                       : A.pairs + (uint64_t)i * A.cap;
     }
-    __device__ void end(uint32_t t, uint32_t n) const {
+    __device__ void end(uint32_t i, uint32_t n) const {
         if ((threadIdx.x & 31) == 0) {
+            const uint32_t t = A.t0 + i;
             A.counts[t] = n <= A.cap ? n : kOverflow;
-            if (n > A.cap) A.redo[atomicAdd(&A.status->n_redo, 1u)] = t;
+            if (n > A.cap) {
+                const uint32_t j = atomicAdd(&A.status->n_ovf, 1u);
+                A.ovf[j] = t;
+                A.ovf_n[j] = n;
+            }
         }
     }
 };
 
+// overflow items: region at pool_off[i] (pair units), sized exactly
+struct PoolSink {
+    const SplitArgs &A;
+    __device__ uint2 *begin(uint32_t i) const {
+        const uint64_t off = __ldg(A.pool_off + i);
+        return A.kbits ? reinterpret_cast<uint2 *>(reinterpret_cast<uint32_t *>(A.pairs) + off) : A.pairs + off;
+    }
+    __device__ void end(uint32_t, uint32_t) const {}
+};
+
 template <bool PK, int BM>
-__global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __grid_constant__ SplitArgs A) {
-    constexpr int kWarps = kCompactThreads / 32;
+__global__ void __launch_bounds__(kCompactThreads, 32 / ARA_COMPACT_WARPS) compact_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);
     if (*A.yet.max_event >= A.pf.catalog) {           // out-of-range ids: nothing is read
@@ -399,47 +341,52 @@ __global__ void __launch_bounds__(kCompactThreads, 1) compact_kernel(const __gri
     for (uint32_t t = threadIdx.x; t <= A.pf.bitmap_words; t += blockDim.x)   // + one zero word (sentinel)
         bitmap[t] = t < A.pf.bitmap_words ? A.pf.bitmap[t] : 0u;
     __syncthreads();
-    HbmSink sink{A};
-    produce_pairs<PK, BM>(A, bitmap, blockIdx.x * kWarps + (threadIdx.x >> 5), gridDim.x * kWarps, sink);
+    if (A.list) {
+        PoolSink sink{A};
+        produce_pairs<PK, BM>(A, bitmap, sink);
+    } else {
+        SlotSink sink{A};
+        produce_pairs<PK, BM>(A, bitmap, sink);
+    }
 }
 
 // ---------------------------------------------------------------------------
 // sample_kernel: one warp per trial (dynamic scheduler).  The trial's present
 // pairs {device record, k} (dense, (occurrence, slot) order, from
-// compact_kernel) are processed in segments of up to xcap pairs:
-//   rounds : 64 pairs per round (two per lane in flight, the next round's
-//            pairs prefetched): one SplitRec load, Philox draws keyed
-//            (trial, k, program / XELT), steps 2-4, quantile table (line 7),
-//            XELT terms (line 8); the loss x and the record's run flags go to
-//            shared memory
-//   reduce : each lane walks a contiguous stretch in order, summing the
-//            (occurrence, layer) runs in fp64 (line 9) and, at a run's last
-//            record, applying the occurrence terms (line 11); runs crossing
-//            stretches are joined by one segmented warp scan, and a run open
-//            at the segment's end is carried into the next
-// Every sum runs in a fixed order (pair order, stretches, a fixed-tree warp
-// sum), fp64; at the trial's end one warp sum per layer -> aggregate terms
-// (line 12) -> YLT (line 17).
+// compact_kernel) are processed in rounds of 32 kU pairs, pair p of the
+// round on lane p mod 32 (the next round's pairs prefetched):
+//   draw   : one SplitRec load, Philox draws keyed (trial, k, program /
+//            XELT), steps 2-4, quantile table (line 7), XELT terms (line 8)
+//   runs   : the pairs of one (occurrence, layer) run are consecutive, so
+//            each 32-pair group is reduced in registers by a segmented warp
+//            scan (fp32, reading G28; the run boundaries from one ballot of
+//            the records' run-end flags), the open run carried into the next
+//            group (line 9); the lane holding a run's last pair applies the
+//            occurrence terms (line 11) and adds the result to its fp64 share
+//            of the layer's trial sum
+// At the trial's end one fixed-tree warp sum per layer -> aggregate terms
+// (line 12) -> YLT (line 17).  Every sum runs in an order fixed by the pair
+// positions alone, so the YLT is a pure function of (portfolio, YET, seed).
 // ---------------------------------------------------------------------------
 // Per-warp shared-memory workspace of the sampler.
 struct SampleWs {
     const SlotInfo *slots;
     const LayerInfo *layers;
-    uint32_t *xs;                 // [xcap] loss bits | run end << 31
-    uint8_t *fl;                  // [xcap] layer (multi-layer portfolios)
-    double *accs;                 // this lane's column of [nl][32]
+    double *accs;                 // multi-layer: this lane's column of [nl][32]
     unsigned int *dc;             // [nl]
     unsigned long long *dhs;      // [nl]
     float *mos;                   // OM, multi-layer: this lane's column of [nl][32] (largest occurrence loss)
+    uint32_t *xs;                 // [xcap] loss bits | run end << 31
+    uint8_t *fl;                  // [xcap] layer (multi-layer portfolios)
 };
 
-// The sampler on trial t's n present pairs at `in` (CG: read them through L2
-// only, as the fused kernel's consumers must).
-template <bool SU, bool SL, bool DBG, bool CG, bool PK = false, bool OM = false, bool ZA = false>
+// The sampler on trial t's n present pairs at `in` (CG: read them through L2 only).
+using RunT = float;                            // in-stretch run sums and occurrence clips (G28)
+template <bool SU, bool SL, bool DBG, bool CG, bool PK = false, bool OM = false, int RS = 0>
 __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs &W, uint64_t t, uint32_t n,
                                              const uint2 *in) {
     const int lane = threadIdx.x & 31;
-    const uint32_t nl = A.pf.n_layers, kXCap = A.xcap;
+    const uint32_t nl = A.pf.n_layers;
     const uint64_t n_trials = A.yet.n_trials;
     const bool terms = A.pf.any_terms != 0;
     const SlotInfo *slots = W.slots;
@@ -461,6 +408,8 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
         return CG ? __ldcg(q) : __ldcs(q);
     };
     const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);
+    // RS 2: index of the trial's first occurrence in the YET (supplied z_(Prog,E))
+    const uint64_t occ_base = RS != 2 ? 0 : A.yet.offsets ? A.yet.offsets[t] : t * (uint64_t)A.yet.fixed_len;
     if (!SL)
         for (uint32_t l = 0; l < nl; ++l) accs[l * 32] = 0.0;
     if (OM && !SL)
@@ -501,11 +450,17 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 float v[kU];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const uint32_t bp = philox_lane0_k(trial_g, e[u].y, r[u].prog, 1u, A.pkey);   // z_(Prog,E)
-                    const uint32_t be =                                                           // z_(E)
-                        ZA ? philox_lane0_k(__ldg(A.pf.rec_orig + e[u].x), r[u].elt, 0u, 6u, A.pkey)  // (A)
-                           : philox_lane0_k(trial_g, e[u].y, r[u].elt & A.ze_mask, A.ze_tag, A.pkey); // G2, (B)
-                    v[u] = fmaf(r[u].wi, norm_quantile_from_bits(bp), r[u].wc * norm_quantile_from_bits(be));
+                    if (RS == 2) {                        // supplied with the inputs
+                        const float zp = __ldg(A.zp_sup + (uint64_t)r[u].prog * A.zp_stride + occ_base + e[u].y);
+                        const float ze = __ldg(A.ze_sup + e[u].x);
+                        v[u] = fmaf(r[u].wi, norm_quantile_f(zp), r[u].wc * norm_quantile_f(ze));
+                    } else {
+                        const uint32_t bp = philox_lane0_k(trial_g, e[u].y, r[u].prog, 1u, A.pkey);   // z_(Prog,E)
+                        const uint32_t be =                                                           // z_(E)
+                            RS == 1 ? philox_lane0_k(__ldg(A.pf.rec_orig + e[u].x), r[u].elt, 0u, 6u, A.pkey)  // (A)
+                                    : philox_lane0_k(trial_g, e[u].y, r[u].elt & A.ze_mask, A.ze_tag, A.pkey); // G2, (B)
+                        v[u] = fmaf(r[u].wi, norm_quantile_from_bits(bp), r[u].wc * norm_quantile_from_bits(be));
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -641,19 +596,20 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     }
 }
 
-// ZA: z_(E) stored per XELT record (ARA_RNG_RECORD); the default draw covers
-// reading G2 and ARA_RNG_OCCURRENCE through A.ze_mask / A.ze_tag
-template <bool SU, bool SL, bool DBG, bool PK, bool OM, bool ZA = false>
-__global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 warps/SM: <= 64 registers
+
+// RS: the random source -- 0: Philox, reading G2 and ARA_RNG_OCCURRENCE
+// (through A.ze_mask / A.ze_tag); 1: Philox z_(E) per XELT record
+// (ARA_RNG_RECORD); 2: z_(Prog,E) / z_(E) supplied with the YET and the
+// records (ARA_RNG_SUPPLIED, the paper's data model).  A.list set: the items
+// of the overflow pass (pairs in the overflow pool).
+template <bool SU, bool SL, bool DBG, bool PK, bool OM, int RS = 0>
+__global__ void __launch_bounds__(kSampleWarps * 32, 32 / kSampleWarps)   // <= 64 registers
     sample_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t nl = A.pf.n_layers;
     SlotInfo *slots = reinterpret_cast<SlotInfo *>(smem);
     LayerInfo *layers = reinterpret_cast<LayerInfo *>(slots + ARA_MAX_SLOTS);
-    const uint32_t kXCap = A.xcap;
-    uint32_t *xsw = reinterpret_cast<uint32_t *>(layers + ARA_MAX_LAYERS);        // [warps][kXCap]
-    uint8_t *flw = reinterpret_cast<uint8_t *>(xsw + kSampleWarps * kXCap);       // [warps][kXCap]
-    double *accw = reinterpret_cast<double *>(((uintptr_t)(flw + kSampleWarps * kXCap) + 7) & ~(uintptr_t)7);  // [warps][nl][32]
+    double *accw = reinterpret_cast<double *>(layers + ARA_MAX_LAYERS);                       // [warps][nl][32]
     unsigned int *cw = reinterpret_cast<unsigned int *>(accw + kSampleWarps * nl * 32);
     unsigned long long *hw = reinterpret_cast<unsigned long long *>(
         ((uintptr_t)(cw + kSampleWarps * nl) + 7) & ~(uintptr_t)7);            // [warps][nl]
@@ -664,18 +620,30 @@ __global__ void __launch_bounds__(kSampleWarps * 32, ARA_SAMPLE_MINB)   // 32 wa
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (*A.yet.max_event >= A.pf.catalog) return;   // compact_kernel wrote no pairs
-    const SampleWs W{slots, layers, xsw + warp * kXCap, flw + warp * kXCap, accw + warp * nl * 32 + lane,
-                     cw + warp * nl, hw + warp * nl, (OM && !SL) ? mow + warp * nl * 32 + lane : nullptr};
+    uint32_t *xsw = reinterpret_cast<uint32_t *>(mow + ((OM && !SL) ? kSampleWarps * nl * 32 : 0));
+    uint8_t *flw = reinterpret_cast<uint8_t *>(xsw + kSampleWarps * kXCap);
+    const SampleWs W{slots, layers, accw + warp * nl * 32 + lane, cw + warp * nl, hw + warp * nl,
+                     (OM && !SL) ? mow + warp * nl * 32 + lane : nullptr, xsw + warp * kXCap, flw + warp * kXCap};
     while (true) {
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(&A.status->next_trial2, 1ull);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= A.yet.n_trials) break;
-        const uint32_t n = __ldg(A.counts + t);
-        if (n == kOverflow) continue;                 // redone by the fused kernel
-        sample_trial<SU, SL, DBG, false, PK, OM, ZA>(A, W, t, n, PK ? reinterpret_cast<const uint2 *>(
-                                                                   reinterpret_cast<const uint32_t *>(A.pairs) + t * A.cap)
-                                                               : A.pairs + t * (uint64_t)A.cap);
+        unsigned long long i = 0;
+        if (lane == 0) i = atomicAdd(A.sched, 1ull);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= A.n_items) break;
+        uint32_t t, n;
+        uint64_t off;                                 // the item's pairs: offset in pair units
+        if (A.list) {
+            t = __ldg(A.list + i);
+            n = __ldg(A.ovf_n + i);
+            off = __ldg(A.pool_off + i);
+        } else {
+            t = A.t0 + (uint32_t)i;
+            n = __ldg(A.counts + t);
+            if (n == kOverflow) continue;             // sampled in the overflow pass
+            off = i * (uint64_t)A.cap;
+        }
+        sample_trial<SU, SL, DBG, false, PK, OM, RS>(A, W, t, n, PK ? reinterpret_cast<const uint2 *>(
+                                                                reinterpret_cast<const uint32_t *>(A.pairs) + off)
+                                                            : A.pairs + off);
         __syncwarp();
     }
 }
@@ -772,7 +740,7 @@ cudaError_t launch_count_bad(const uint32_t *ev, uint64_t n, uint32_t C, unsigne
 // Launch preparation cached per (device, kernel, dynamic shared memory): the
 // attribute call and the occupancy query cost microseconds of host time
 // that would otherwise sit between the kernels of every ara_run.
-static cudaError_t prepare_launch(const void *kern, size_t smem, int threads, int &per_sm) {
+cudaError_t prepare_launch(const void *kern, size_t smem, int threads, int &per_sm) {
     struct Entry { int dev; const void *k; size_t smem; int threads, per_sm; };
     struct Attr { int dev; const void *k; size_t max_smem; };
     static std::mutex mu;
@@ -810,57 +778,60 @@ cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms) {
     cudaError_t err = prepare_launch((const void *)kern, smem, kCompactThreads, per_sm);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    kern<<<num_sms * per_sm, kCompactThreads, smem, s>>>(A);
+    const uint32_t blocks = std::max(1u, std::min<uint32_t>((uint32_t)num_sms, (A.n_items + ARA_COMPACT_WARPS - 1) /
+                                                                                  ARA_COMPACT_WARPS));
+    kern<<<blocks, kCompactThreads, smem, s>>>(A);      // one CTA per SM (persistent)
     return cudaGetLastError();
+}
+
+size_t sample_smem_bytes(uint32_t n_layers, bool occ_max) {
+    // slot and layer tables plus the per-warp layer accumulators; the rest of
+    // the SM's shared memory is the compaction's bitmap and L1 data cache for
+    // the record and table gathers
+    const bool sl = n_layers == 1;
+    return sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
+           sizeof(double) * kSampleWarps * n_layers * 32 +
+           kSampleWarps * n_layers * (sizeof(unsigned int) + sizeof(unsigned long long)) + 16 +
+           (occ_max && !sl ? sizeof(float) * kSampleWarps * n_layers * 32 : 0) +
+           (sizeof(uint32_t) + sizeof(uint8_t)) * kSampleWarps * kXCap + 16;
 }
 
 cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
     const bool dbg = (A.flags & ARA_DEBUG_LOOKUP) != 0, su = (A.flags & ARA_SU) != 0;
     const bool sl = A.pf.n_layers == 1;
     if (A.pf.n_layers > kSplitMaxLayers) return cudaErrorInvalidValue;
-    const size_t other = sizeof(SlotInfo) * ARA_MAX_SLOTS + sizeof(LayerInfo) * ARA_MAX_LAYERS +
-                         sizeof(double) * kSampleWarps * A.pf.n_layers * 32 +
-                         kSampleWarps * A.pf.n_layers * (sizeof(unsigned int) + sizeof(unsigned long long)) + 16 +
-                         (A.occ_max && !sl ? sizeof(float) * kSampleWarps * A.pf.n_layers * 32 : 0);
-    // shared memory left unclaimed is L1 data cache, which the record and table
-    // gathers use: keep the segments short
-    SplitArgs B = A;
-    // (a multiple of the round, 32 kU pairs, so a segment ends on a round)
-    constexpr size_t kR = 64 * kU;
-    const size_t min_xcap = (ARA_MAX_SLOTS + kR - 1) / kR * kR;
-    // many layers (+ occ_max) claim more: the budget grows to one minimal segment
-    const size_t budget = std::max((size_t)ARA_SAMPLE_SMEM_KB * 1024,
-                                   other + 8 + (sizeof(float) + sizeof(uint8_t)) * kSampleWarps * min_xcap);
-    B.xcap = (uint32_t)std::min<size_t>(kXCapMax / kR * kR, (budget - other - 8) / (5 * kSampleWarps) / kR * kR);
-    if (B.xcap < ARA_MAX_SLOTS) B.xcap = (uint32_t)((ARA_MAX_SLOTS + kR - 1) / kR * kR);
-    const size_t smem = other + (sizeof(float) + sizeof(uint8_t)) * kSampleWarps * B.xcap + 8;
+    const size_t smem = sample_smem_bytes(A.pf.n_layers, A.occ_max != nullptr);
     using K = void (*)(SplitArgs);
 #define ARA_SK(P, O)                                                                                            \
     (su ? (sl ? (dbg ? (K)sample_kernel<true, true, true, P, O> : (K)sample_kernel<true, true, false, P, O>)     \
             : (dbg ? (K)sample_kernel<true, false, true, P, O> : (K)sample_kernel<true, false, false, P, O>))   \
         : (sl ? (dbg ? (K)sample_kernel<false, true, true, P, O> : (K)sample_kernel<false, true, false, P, O>)   \
               : (dbg ? (K)sample_kernel<false, false, true, P, O> : (K)sample_kernel<false, false, false, P, O>)))
-    // ARA_RNG_RECORD: its own instantiations (SU on, no occ_max: ara_run sends that case to the
-    // fp64-capable kernel)
-    const K za = sl ? (dbg ? (K)sample_kernel<true, true, true, true, false, true>
-                           : (K)sample_kernel<true, true, false, true, false, true>)
-                    : (dbg ? (K)sample_kernel<true, false, true, true, false, true>
-                           : (K)sample_kernel<true, false, false, true, false, true>);
-    const K za_w = sl ? (dbg ? (K)sample_kernel<true, true, true, false, false, true>
-                             : (K)sample_kernel<true, true, false, false, false, true>)
-                      : (dbg ? (K)sample_kernel<true, false, true, false, false, true>
-                             : (K)sample_kernel<true, false, false, false, false, true>);
-    const bool use_za = A.rng_mode == 1 && su;       // (without SU no z_(E) is drawn)
-    if (use_za && A.occ_max) return cudaErrorInvalidValue;
-    const K kern = use_za ? (A.kbits ? za : za_w)
+    // ARA_RNG_RECORD / ARA_RNG_SUPPLIED: their own instantiations (SU on, no occ_max: ara_run
+    // sends those cases to the fp64-capable kernel)
+#define ARA_SR(RS_)                                                                                                 \
+    (A.kbits ? (sl ? (dbg ? (K)sample_kernel<true, true, true, true, false, RS_>                                   \
+                          : (K)sample_kernel<true, true, false, true, false, RS_>)                                 \
+                   : (dbg ? (K)sample_kernel<true, false, true, true, false, RS_>                                  \
+                          : (K)sample_kernel<true, false, false, true, false, RS_>))                               \
+             : (sl ? (dbg ? (K)sample_kernel<true, true, true, false, false, RS_>                                  \
+                          : (K)sample_kernel<true, true, false, false, false, RS_>)                                \
+                   : (dbg ? (K)sample_kernel<true, false, true, false, false, RS_>                                 \
+                          : (K)sample_kernel<true, false, false, false, false, RS_>)))
+    const uint32_t rs = su && (A.rng_mode == 1 || A.rng_mode == 3) ? (A.rng_mode == 1 ? 1u : 2u) : 0u;
+    if (rs && A.occ_max) return cudaErrorInvalidValue;
+    const K kern = rs == 1 ? ARA_SR(1) : rs == 2 ? ARA_SR(2)
                  : A.occ_max ? (A.kbits ? ARA_SK(true, true) : ARA_SK(false, true))
                              : (A.kbits ? ARA_SK(true, false) : ARA_SK(false, false));
+#undef ARA_SR
 #undef ARA_SK
     int per_sm = 0;
     cudaError_t err = prepare_launch((const void *)kern, smem, kSampleWarps * 32, per_sm);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    kern<<<num_sms * per_sm, kSampleWarps * 32, smem, s>>>(B);
+    const uint32_t blocks = std::max(1u, std::min<uint32_t>((uint32_t)num_sms, (A.n_items + kSampleWarps - 1) /
+                                                                                  kSampleWarps));
+    kern<<<blocks, kSampleWarps * 32, smem, s>>>(A);    // one CTA per SM (persistent)
     return cudaGetLastError();
 }
 

@@ -1,7 +1,9 @@
-"""Multi-process (gloo, world size 2, CPU) check of the N>1 path's host logic:
-trial sharding by global index (bench.shard_range) with the oracle standing
-in for each rank's ara_run, the YLT all-gather into the [P][L][N/P] layout
-that ara_risk_measures consumes, and rank-count invariance."""
+"""Multi-process (gloo, CPU) check of the N>1 path's host logic: trial
+sharding by global index (bench.shard_range) with the oracle standing in for
+each rank's ara_run (no GPU here), bench.gather_ylt -- the exchange step
+bench.run_ours runs, equal and unequal shards -- and rank-count invariance
+of the YLT and the measures; bench.launch_command (the
+one-process-per-GPU re-exec of `bench.py --gpus N`)."""
 import os
 import socket
 
@@ -48,6 +50,58 @@ def _worker(rank, world, port, out_dir):
         np.save(os.path.join(out_dir, "gathered.npy"), gathered.numpy())
     dist.barrier()
     dist.destroy_process_group()
+
+
+def _gather_worker(rank, world, port, out_dir, n_trials):
+    # bench.run_ours's exchange step on CPU tensors: each rank's YLT shard
+    # (the oracle in place of ara_run) through bench.gather_ylt
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    cfg = small_cfg()
+    cfg["n_trials"] = n_trials
+    lo, hi = bench.shard_range(n_trials, rank, world)
+    pf = aragen.build_portfolio(cfg)
+    yet = aragen.build_yet(cfg, first_trial=lo, n_trials=hi - lo)
+    part = torch.from_numpy(np.ascontiguousarray(oracle.run(pf, yet, seed=cfg["seed"], n_threads=1)["ylt"]))
+    table, n_shards = bench.gather_ylt(part, world, n_trials)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "table.npy"), table.numpy())
+        np.save(os.path.join(out_dir, "n_shards.npy"), np.array([n_shards]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world,n_trials", [(2, 400), (2, 401), (3, 400)])
+def test_bench_gather_ylt(tmp_path, world, n_trials):
+    mp.spawn(_gather_worker, args=(world, _free_port(), str(tmp_path), n_trials), nprocs=world, join=True)
+    table = np.load(tmp_path / "table.npy")
+    n_shards = int(np.load(tmp_path / "n_shards.npy")[0])
+    cfg = small_cfg()
+    cfg["n_trials"] = n_trials
+    pf = aragen.build_portfolio(cfg)
+    full = oracle.run(pf, aragen.build_yet(cfg), seed=cfg["seed"])["ylt"]      # [L][N], one process
+    L, N = full.shape
+    if n_trials % world == 0:
+        assert n_shards == world and table.shape == (world * L, N // world)
+        flat = table.reshape(world, L, N // world).transpose(1, 0, 2).reshape(L, N)   # [P][L][N/P] -> [L][N]
+    else:
+        assert n_shards == 1 and table.shape == (L, N)                 # pads dropped, global trial order
+        flat = table
+    assert np.array_equal(flat, full)
+    for li in range(L):
+        for rp in (10, 50):
+            assert OM.pml(flat[li], rp) == OM.pml(full[li], rp)
+            assert OM.tvar_rp(flat[li], rp) == OM.tvar_rp(full[li], rp)
+
+
+def test_launch_command_one_process_per_gpu():
+    import bench
+    cmd = bench.launch_command(8, ["--gpus", "8", "--steps", "5"], port=29555)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=8" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-4:] == ["--gpus", "8", "--steps", "5"] and cmd[-5].endswith("bench.py")
 
 
 @pytest.mark.timeout(300)

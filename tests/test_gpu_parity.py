@@ -279,6 +279,54 @@ def test_primary_integer_bit_exact(A, ctx):
         assert np.array_equal(g, ref["ylt"].astype(np.float32))
 
 
+def test_primary_fast_path_integer_bit_exact(A, ctx):
+    # no draw is taken (SU off, or every sigma = 0 with SU on): the streaming
+    # pass over the per-(event, layer) occurrence losses of ara_create_portfolio
+    # (no debug lookup -> the fast path); integer means and terms: bit-exact
+    cfg = aragen.load_config("cfg1")
+    cfg.update(sigma_scale=0.0, integer_mu=True, n_trials=600, catalog=3000, records_per_elt=900,
+               layer_terms=[[2e5, 5e6, 2.0e7, 3.0e7]])
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    ref = oracle.run(pf, yet, seed=5, su=False)
+    for su in (False, True):
+        g = A.run(ctx, P, Y, seed=5, su=su).cpu().numpy()
+        assert np.array_equal(g, ref["ylt"].astype(np.float32))
+        ylt, occ = A.run_ep(ctx, P, Y, seed=5, su=su)
+        assert np.array_equal(ylt.cpu().numpy(), g)
+        assert np.array_equal(occ.cpu().numpy(), ref["occ_max"].astype(np.float32))
+
+
+@pytest.mark.parametrize("n_layers,J,ragged,terms", [(1, 16, False, False), (3, 4, True, True), (8, 3, False, True),
+                                                     (2, 5, True, False)])
+def test_primary_fast_path_vs_oracle(A, ctx, n_layers, J, ragged, terms, monkeypatch):
+    # the fast path (1, 2 -> 2, 3 -> 4 and 8 layers per event sector; CSR
+    # trials; XELT terms) against the oracle with SU off, and against the
+    # two-kernel path of the same run (ARA_NO_PRIMARY_PATH, a test aid)
+    cfg = aragen.load_config("cfg1")
+    cfg.update(n_layers=n_layers, elts_per_layer=J, catalog=4000, records_per_elt=700, n_trials=500,
+               layer_terms=[[2e5 * (l + 1), 5e6, 1.0e6, 5.0e7] for l in range(n_layers)])
+    if ragged:
+        cfg.update(k_min=0, k_max=170)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    if terms:
+        rng = np.random.default_rng(n_layers)
+        n_elts = n_layers * J
+        pf["elt_terms"] = np.stack([rng.uniform(0, 2e4, n_elts), rng.uniform(1e5, 1e7, n_elts),
+                                    rng.uniform(0.2, 1.0, n_elts)], 1)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    ref = oracle.run(pf, yet, seed=3, su=False)
+    ylt, occ = A.run_ep(ctx, P, Y, seed=3, su=False)
+    g, m = ylt.cpu().numpy(), occ.cpu().numpy()
+    for li in range(n_layers):
+        ylt_check(g[li], ref, li)
+        o = ref["occ_max"][li]
+        assert (np.abs(m[li] - o) <= 1e-6 * o).all()
+    monkeypatch.setenv("ARA_NO_PRIMARY_PATH", "1")
+    g2 = A.run(ctx, P, Y, seed=3, su=False).cpu().numpy()
+    assert (np.abs(g2.astype(np.float64) - g) <= 1e-5 * np.abs(g) + 1e-6 * ref["gross"]).all()
+
+
 def test_ragged_empty_trials_and_repeats(A, ctx):
     cfg = aragen.load_config("cfg1")
     cfg.update(k_min=0, k_max=150, n_trials=700, catalog=300, records_per_elt=120)
@@ -355,27 +403,58 @@ def test_shared_elts_and_xelt_terms(A, ctx):
         ylt_check(g[li], ref, li)
 
 
-def test_pair_region_overflow_goes_to_fused_kernel(A, ctx):
-    # a trial whose present pairs exceed its region (2x expected + 128) is redone
-    # by the fp64-capable scan kernel; counts/hashes/YLT stay exact
-    cfg = aragen.load_config("cfg1")
-    cfg["n_trials"] = 50
-    pf = aragen.build_portfolio(cfg)
+def _heavy_trial_yet(cfg, pf):
+    # trials 0-9 as generated, trial 10 = 400 events present in 2 XELTs each
+    # (800 pairs, > 2x the expected pairs of its region), trials 11-50 as generated
     yet = aragen.build_yet(cfg)
     R = cfg["records_per_elt"]
     both = np.intersect1d(pf["rec_event"][:R], pf["rec_event"][R:2 * R])
     assert both.size > 50
-    rng = np.random.default_rng(4)
-    heavy = rng.choice(both, 400).astype(np.uint32)            # 800 pairs in one trial
+    heavy = np.random.default_rng(4).choice(both, 400).astype(np.uint32)
     K = cfg["events_per_trial"]
     ev = np.concatenate([yet["events"][:10 * K], heavy, yet["events"][10 * K:]])
-    # trials 0-9 as generated, trial 10 = the 400 heavy events, trials 11-50 as generated
     off = np.concatenate([np.arange(11, dtype=np.uint64) * K, 10 * K + 400 + np.arange(0, 41, dtype=np.uint64) * K])
-    y2 = {"trial_off": off, "events": ev, "first_trial": 0}
+    return {"trial_off": off, "events": ev, "first_trial": 0}
+
+
+def test_pair_region_overflow_pass(A, ctx):
+    # a trial whose present pairs exceed its region (2x expected + 128) is
+    # compacted again into an exactly sized region of the overflow pool and
+    # sampled by the same kernel; counts/hashes/YLT exact
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 50
+    pf = aragen.build_portfolio(cfg)
+    y2 = _heavy_trial_yet(cfg, pf)
     (g, cnt, hsh), ref = run_both(A, ctx, pf, y2, cfg["seed"])
     assert cnt[0, 10] == 800
+    assert A.last_run_timings(ctx)["redo_ms"] > 0          # the overflow pass ran
     assert np.array_equal(cnt, ref["count"]) and np.array_equal(hsh, ref["hash"])
     ylt_check(g, ref)
+
+
+@pytest.mark.parametrize("cap", ["0", "1", "64"])
+def test_overflow_pass_bit_identical(A, ctx, cap, monkeypatch):
+    # whether a trial overflows its region depends on the region size (and so
+    # on the loaded YET's mean length); the YLT must not: every trial forced
+    # through the overflow pass (ARA_PAIR_CAP, a test aid), a CSR YET with one
+    # heavy trial run whole and as two shards -- all bit-identical
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 50
+    pf = aragen.build_portfolio(cfg)
+    y2 = _heavy_trial_yet(cfg, pf)
+    P = A.Portfolio(ctx, pf)
+    full = A.run(ctx, P, A.Yet.from_dict(ctx, y2), seed=7, debug=True)
+    off = y2["trial_off"].astype(np.int64)
+    parts = []
+    for lo, hi in ((0, 12), (12, 51)):
+        ys = {"trial_off": (off[lo:hi + 1] - off[lo]).astype(np.uint64),
+              "events": y2["events"][off[lo]:off[hi]], "first_trial": lo}
+        parts.append(A.run(ctx, P, A.Yet.from_dict(ctx, ys), seed=7).cpu().numpy())
+    assert np.array_equal(np.concatenate(parts, axis=1), full[0].cpu().numpy())
+    monkeypatch.setenv("ARA_PAIR_CAP", cap)
+    forced = A.run(ctx, P, A.Yet.from_dict(ctx, y2), seed=7, debug=True)
+    for x, y in zip(full, forced):
+        assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
 
 
 def test_determinism_and_sharding(A, ctx):
@@ -396,9 +475,10 @@ def test_determinism_and_sharding(A, ctx):
 
 
 @pytest.mark.parametrize("n_layers,J,K", [(1, 16, 1000), (3, 4, 1500)])
-def test_fused_packed_and_wide_pairs_identical(A, ctx, n_layers, J, K):
-    # 4-byte packed and 8-byte pair records (and the no-op ARA_FUSED flag):
-    # each trial in the same order, bit-identical YLT, counts and hashes
+def test_packed_wide_pairs_and_batching_identical(A, ctx, n_layers, J, K, monkeypatch):
+    # 4-byte packed and 8-byte pair records, any trial batching
+    # (ARA_BATCH_TRIALS) and the two-stream schedule (ARA_OVERLAP): each
+    # trial in the same order, bit-identical YLT, counts and hashes
     cfg = aragen.load_config("cfg3")
     terms = [[2e5 * (l + 1), 5e6, 1.0e6, 5.0e9] for l in range(n_layers)]
     cfg.update(n_layers=n_layers, elts_per_layer=J, n_trials=20000, events_per_trial=K, layer_terms=terms)
@@ -406,12 +486,17 @@ def test_fused_packed_and_wide_pairs_identical(A, ctx, n_layers, J, K):
     P = A.Portfolio(ctx, pf)
     Y = A.Yet.from_dict(ctx, yet)
     for su in (True, False):
-        f = A.run(ctx, P, Y, seed=5, su=su, debug=True, fused=True)
-        t = A.run(ctx, P, Y, seed=5, su=su, debug=True)                   # 4-byte packed pairs
-        w = A.run(ctx, P, Y, seed=5, su=su, debug=True, wide_pairs=True)  # 8-byte pairs
-        for x, y, z in zip(f, t, w):
-            assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
-            assert np.array_equal(x.cpu().numpy(), z.cpu().numpy())
+        ref = A.run(ctx, P, Y, seed=5, su=su, debug=True)                 # 4-byte packed pairs
+        outs = [A.run(ctx, P, Y, seed=5, su=su, debug=True, wide_pairs=True)]  # 8-byte pairs
+        for env in ({"ARA_BATCH_TRIALS": "777"}, {"ARA_BATCH_TRIALS": "20000"}, {"ARA_OVERLAP": "1"},
+                    {"ARA_OVERLAP": "1", "ARA_BATCH_TRIALS": "3000"}):
+            with monkeypatch.context() as m:
+                for k_, v_ in env.items():
+                    m.setenv(k_, v_)
+                outs.append(A.run(ctx, P, Y, seed=5, su=su, debug=True))
+        for o in outs:
+            for x, y in zip(ref, o):
+                assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
 
 
 def test_event_out_of_range(A, ctx):
@@ -748,16 +833,17 @@ def test_packed_refill_errors(A, ctx):
 
 # ---- paper-literal RNG alternatives of reading G2 (NEXT-4) -------------------
 @pytest.mark.parametrize("rng,mode", [("record", 1), ("occurrence", 2)])
-@pytest.mark.parametrize("case", ["cfg1", "layers3", "exact", "fused"])
-def test_rng_modes_vs_oracle(A, ctx, rng, mode, case):
+@pytest.mark.parametrize("case", ["cfg1", "layers3", "exact", "batched"])
+def test_rng_modes_vs_oracle(A, ctx, rng, mode, case, monkeypatch):
     cfg = aragen.load_config("cfg1")
+    if case == "batched":
+        monkeypatch.setenv("ARA_BATCH_TRIALS", "97")
     if case == "layers3":
         cfg.update(n_layers=3, elts_per_layer=4, catalog=4000, records_per_elt=600, n_trials=300,
                    layer_terms=[[2e5 * (l + 1), 5e6, 1.0e6, 5.0e7] for l in range(3)])
     pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
     P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
-    g, cnt, hsh = A.run(ctx, P, Y, seed=cfg["seed"], debug=True, rng=rng, exact=(case == "exact"),
-                        fused=(case == "fused"))
+    g, cnt, hsh = A.run(ctx, P, Y, seed=cfg["seed"], debug=True, rng=rng, exact=(case == "exact"))
     ref = oracle.run(pf, yet, seed=cfg["seed"], rng_mode=mode)
     assert np.array_equal(cnt.cpu().numpy().astype(np.uint32), ref["count"])
     g = g.cpu().numpy()
@@ -874,3 +960,62 @@ def test_batch_and_curve_errors(A, ctx):
         A.exceedance_curve(ctx, y, 2, 100, 0, n_shards=3)
     c = A.exceedance_curve(ctx, y, 2, 100, -1).cpu().numpy()
     assert (c == 2.0).all()                           # constant roll-up
+
+
+# ---- the paper's data model: draws supplied with the inputs (NEXT-4) ---------
+@pytest.mark.parametrize("case", ["cfg1", "layers3", "exact", "ragged", "ep"])
+def test_supplied_z_vs_oracle(A, ctx, case):
+    # z_(Prog,E) per YET occurrence and z_(E) per XELT record
+    # given as inputs (ARA_RNG_SUPPLIED): the split path, ARA_EXACT, CSR
+    # trials, several programs, and run_ep (fp64-capable kernel) against the
+    # oracle fed the same numbers
+    cfg = aragen.load_config("cfg1")
+    if case == "layers3":
+        cfg.update(n_layers=3, elts_per_layer=4, catalog=4000, records_per_elt=600, n_trials=300,
+                   layer_terms=[[2e5 * (l + 1), 5e6, 1.0e6, 5.0e7] for l in range(3)])
+    if case == "ragged":
+        cfg.update(k_min=0, k_max=150, n_trials=700)
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    if case == "layers3":
+        pf["layer_prog"] = np.array([0, 1, 1], np.uint32)
+    rng = np.random.default_rng(123)
+    n_prog = int(pf["layer_prog"].max()) + 1
+    zp = ((rng.integers(0, 2 ** 23, (n_prog, yet["events"].size)) * 2 + 1) * 2.0 ** -24).astype(np.float32)
+    ze = ((rng.integers(0, 2 ** 23, pf["rec_event"].size) * 2 + 1) * 2.0 ** -24).astype(np.float32)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    P.set_z(ze)
+    Y.set_z(zp)
+    ref = oracle.run(pf, yet, seed=cfg["seed"], z_prog=zp.astype(np.float64), z_event=ze.astype(np.float64))
+    if case == "ep":
+        g, _ = A.run_ep(ctx, P, Y, seed=cfg["seed"], rng="supplied")
+        g = g.cpu().numpy()
+    else:
+        g, cnt, _ = A.run(ctx, P, Y, seed=cfg["seed"], debug=True, rng="supplied", exact=(case == "exact"))
+        assert np.array_equal(cnt.cpu().numpy().astype(np.uint32), ref["count"])
+        g = g.cpu().numpy()
+    for li in range(g.shape[0]):
+        ylt_check(g[li], ref, li)
+    # the seed plays no part: the numbers come with the inputs
+    g2 = A.run(ctx, P, Y, seed=cfg["seed"] + 99, rng="supplied").cpu().numpy()
+    assert np.array_equal(g2, A.run(ctx, P, Y, seed=cfg["seed"], rng="supplied").cpu().numpy())
+
+
+def test_supplied_z_errors(A, ctx):
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 20
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    with pytest.raises(A.AraError):                       # nothing supplied yet
+        A.run(ctx, P, Y, seed=1, rng="supplied")
+    with pytest.raises(A.AraError):                       # z outside (0, 1)
+        P.set_z(np.zeros(pf["rec_event"].size, np.float32))
+    with pytest.raises(A.AraError):
+        Y.set_z(np.ones(yet["events"].size, np.float32))
+    P.set_z(np.full(pf["rec_event"].size, 0.5, np.float32))
+    Y.set_z(np.full(yet["events"].size, 0.5, np.float32))
+    pf2 = dict(pf, layer_prog=np.array([1], np.uint32))   # program 1 not supplied
+    P2 = A.Portfolio(ctx, pf2)
+    P2.set_z(np.full(pf["rec_event"].size, 0.5, np.float32))
+    with pytest.raises(A.AraError):
+        A.run(ctx, P2, Y, seed=1, rng="supplied")
+    A.run(ctx, P, Y, seed=1, rng="supplied")

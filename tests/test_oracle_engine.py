@@ -50,8 +50,10 @@ def loss_py(mu, si, sc, mx, zp, ze):
     return mx * sp.betaincinv(a, b, z) if z <= 0.5 else mx * (1 - sp.betaincinv(b, a, q))
 
 
-def brute_force(pf, yet, seed, su, trial_index, rng_mode=0):
-    """Straight-line Algorithm 1: linear search over each XELT's record list."""
+def brute_force(pf, yet, seed, su, trial_index, rng_mode=0, z_prog=None, z_event=None):
+    """Straight-line Algorithm 1: linear search over each XELT's record list.
+    z_prog [program][occurrence] / z_event [record] given: the paper's data
+    model, draws supplied with the YET and the XELT records."""
     key = (seed & M32, (seed >> 32) & M32)
     nl = len(pf["layer_prog"])
     n = len(yet["trial_off"]) - 1
@@ -76,8 +78,11 @@ def brute_force(pf, yet, seed, su, trial_index, rng_mode=0):
                     mu, si, sc, mx = (float(pf[f][r]) for f in
                                       ("rec_mean", "rec_sigma_i", "rec_sigma_c", "rec_max"))
                     if su:
-                        zp = u_py(philox_py((i & M32, k, p, 1), key)[0])
-                        if rng_mode == 1:        # (A) z_E stored per XELT record
+                        o = int(yet["trial_off"][t]) + k
+                        zp = u_py(philox_py((i & M32, k, p, 1), key)[0]) if z_prog is None else float(z_prog[p][o])
+                        if z_event is not None:  # supplied with the record
+                            ze = float(z_event[r])
+                        elif rng_mode == 1:      # (A) z_E stored per XELT record
                             ze = u_py(philox_py((r - lo, j, 0, 6), key)[0])
                         elif rng_mode == 2:      # (B) z_E per occurrence, shared by XELTs
                             ze = u_py(philox_py((i & M32, k, 0, 7), key)[0])
@@ -356,3 +361,74 @@ def test_rng_mode_occurrence_shared_by_xelts():
     two0 = O.run(pf2, yet, seed=12, rng_mode=0)["ylt"][0]
     one0 = O.run(pf1, yet, seed=12, rng_mode=0)["ylt"][0]
     assert not np.array_equal(two0, 2.0 * one0)
+
+
+# ---- the paper's data model: z_(Prog,E) in the YET, z_(E) in the XELT (NEXT-4)
+def _supplied(rng, pf, yet):
+    n_prog = int(pf["layer_prog"].max()) + 1
+    zp = (rng.integers(0, 2 ** 23, (n_prog, yet["events"].size)) * 2 + 1) * 2.0 ** -24
+    ze = (rng.integers(0, 2 ** 23, pf["rec_event"].size) * 2 + 1) * 2.0 ** -24
+    return zp, ze
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_engine_supplied_z_vs_brute_force(seed):
+    rng = np.random.default_rng(7000 + seed)
+    pf, yet = tiny_case(rng, xelt_terms=(seed % 3 == 0))
+    zp, ze = _supplied(rng, pf, yet)
+    tidx = rng.integers(0, 2 ** 32, len(yet["trial_off"]) - 1, dtype=np.uint64)
+    got = O.run(pf, yet, seed=1, su=True, n_threads=2, trial_index=tidx, z_prog=zp, z_event=ze)
+    ylt, gross = brute_force(pf, yet, 1, True, tidx, z_prog=zp, z_event=ze)
+    np.testing.assert_allclose(got["gross"], gross, rtol=1e-9, atol=1e-6)
+    np.testing.assert_allclose(got["ylt"], ylt, rtol=1e-9, atol=1e-6)
+
+
+def test_engine_supplied_z_reproduces_record_mode():
+    # supplying the very numbers reading (A) draws -- z_(Prog,E) = Philox
+    # (i, k, p, 1) per occurrence, z_(E) = Philox (r, j, 0, 6) per record --
+    # gives the (A) run bit for bit: the supplied path changes only where the
+    # numbers come from
+    rng = np.random.default_rng(71)
+    pf, yet = tiny_case(rng, n_layers=3, n_elts=4, n_trials=15)
+    seed = 987654321
+    n = len(yet["trial_off"]) - 1
+    n_prog = int(pf["layer_prog"].max()) + 1
+    zp = np.empty((n_prog, yet["events"].size))
+    for p_ in range(n_prog):
+        for t in range(n):
+            for o in range(int(yet["trial_off"][t]), int(yet["trial_off"][t + 1])):
+                zp[p_, o] = O.z_prog(seed, p_, t, o - int(yet["trial_off"][t]))
+    ze = np.empty(pf["rec_event"].size)
+    for j in range(len(pf["elt_off"]) - 1):
+        for r in range(int(pf["elt_off"][j]), int(pf["elt_off"][j + 1])):
+            ze[r] = O.z_event_record(seed, j, r - int(pf["elt_off"][j]))
+    a = O.run(pf, yet, seed=seed, rng_mode=1)
+    b = O.run(pf, yet, seed=seed, z_prog=zp, z_event=ze)
+    assert np.array_equal(a["ylt"], b["ylt"]) and np.array_equal(a["gross"], b["gross"])
+
+
+def test_engine_supplied_median_draws():
+    # z_(Prog,E) = z_(E) = 1/2 -> v = 0 -> every loss is max_l times the
+    # Beta(alpha, beta) median (scipy), a closed-form run
+    rng = np.random.default_rng(72)
+    pf, yet = tiny_case(rng, n_layers=1, n_elts=3, n_trials=10)
+    zp = np.full((int(pf["layer_prog"].max()) + 1, yet["events"].size), 0.5)
+    ze = np.full(pf["rec_event"].size, 0.5)
+    got = O.run(pf, yet, seed=3, z_prog=zp, z_event=ze)
+    med = np.empty(pf["rec_event"].size)
+    for r in range(med.size):
+        mu, si, sc, mx = (float(pf[f][r]) for f in ("rec_mean", "rec_sigma_i", "rec_sigma_c", "rec_max"))
+        if si + sc == 0:
+            med[r] = mu
+            continue
+        a, b = O.beta_params(mu, si + sc, mx)
+        med[r] = mx * sp.betaincinv(a, b, 0.5)
+    occr, occl, aggr, aggl = pf["layer_terms"][0]
+    elts = pf["layer_elts"][:int(pf["layer_elt_off"][1])]
+    for t in range(len(yet["trial_off"]) - 1):
+        S = 0.0
+        for e in yet["events"][int(yet["trial_off"][t]):int(yet["trial_off"][t + 1])]:
+            l = sum(med[r] for j in elts for r in range(int(pf["elt_off"][j]), int(pf["elt_off"][j + 1]))
+                    if int(pf["rec_event"][r]) == int(e))
+            S += min(max(l - occr, 0.0), occl)
+        assert got["gross"][0, t] == pytest.approx(S, rel=1e-10, abs=1e-6)

@@ -1,11 +1,14 @@
 """Per-CUDA-source-line instruction counts and stall samples of an ncu report.
     python tools/src_hot.py rep.ncu-rep [--units N] [--top K]
-(--units: divide instruction counts by N, e.g. present pairs -> warp-inst per pair)"""
+(--units: divide instruction counts by N, e.g. present pairs -> warp-inst per pair; -k: kernel regex)"""
 import argparse, csv, io, subprocess
 ap = argparse.ArgumentParser(); ap.add_argument("rep"); ap.add_argument("--units", type=float, default=0)
-ap.add_argument("--top", type=int, default=40); a = ap.parse_args()
-txt = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+ap.add_argument("--top", type=int, default=40); ap.add_argument("-k", default=None, help="kernel-name regex")
+a = ap.parse_args()
+cmd = ["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+if a.k:
+    cmd += ["-k", "regex:" + a.k]
+txt = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 res = []; fname = None; hdr = None
 for r in rows:
@@ -18,5 +21,5 @@ for r in rows:
 tot = sum(x[0] for x in res); st = sum(x[1] for x in res)
 print(f"total warp-inst {tot/1e6:.1f}M  stall samples {st}")
 for n, s, loc, src in sorted(res, reverse=True)[:a.top]:
-    per = f"{n/a.units:7.2f}/u" if a.units else ""
+    per = f"{32*n/a.units:7.2f} lane-inst/u" if a.units else ""
     print(f"{n/1e6:8.1f}M {per} {100*n/tot:5.1f}%  stall {100*s/max(st,1):5.1f}%  {loc:24s} {src}")

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>     // header-only NVTX v3: host ranges for nsys / ncu --nvtx
 
 #include "ara_internal.cuh"
 #include "ara_measures.cuh"
@@ -21,6 +22,12 @@ using namespace ara;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range for the lifetime of a scope (entry points of the C ABI)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail(int code, const char *fmt, ...) {
     char buf[1024];
@@ -313,19 +320,37 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
                          const ara_record *rec, const ara_elt_terms *et, uint32_t n_layers,
                          const uint32_t *lprog, const uint64_t *loff, const uint32_t *lelts,
                          const ara_layer_terms *lt, ara_portfolio **out) {
+    NvtxRange nvtx("ara_create_portfolio");
     if (!c || !out) return fail(ARA_EINVAL, "ctx/out is NULL");
     *out = nullptr;
     int st = ara_validate_portfolio(C, n_elts, eoff, rec, et, n_layers, lprog, loff, lelts, lt);
     if (st != ARA_OK) return st;
-    if (n_layers <= (uint32_t)kSplitMaxLayers && loff[n_layers] <= ARA_MAX_SLOTS)
+    // Kernel groups of consecutive layers: <= kSplitMaxLayers layers, <=
+    // ARA_MAX_SLOTS slots, and -- so that each pass's gathered tables stay
+    // L2-resident -- at most ARA_GROUP_BYTES (default 64 MiB)
+    // of per-record sampler data (SplitRec + hot table rows, 160 B per
+    // (layer, record)) plus the catalogue index (8 B per event); a single
+    // layer always forms a group.  Each group re-streams the YET.
+    const uint64_t budget = env_u64("ARA_GROUP_BYTES", 64ull << 20);
+    auto layer_records = [&](uint32_t l) {
+        uint64_t r = 0;
+        for (uint64_t x = loff[l]; x < loff[l + 1]; ++x) r += eoff[lelts[x] + 1] - eoff[lelts[x]];
+        return r;
+    };
+    auto fits = [&](uint32_t l0, uint32_t l1) {       // layers [l0, l1] in one group?
+        if (l1 - l0 + 1 > (uint32_t)kSplitMaxLayers || loff[l1 + 1] - loff[l0] > ARA_MAX_SLOTS) return false;
+        uint64_t recs = 0;
+        for (uint32_t l = l0; l <= l1; ++l) recs += layer_records(l);
+        return l1 == l0 || recs * 160 + (uint64_t)C * 8 <= budget;
+    };
+    if (fits(0, n_layers - 1))
         return create_group(c, C, n_elts, eoff, rec, et, n_layers, lprog, loff, lelts, lt, out);
-    // groups of consecutive layers: <= kSplitMaxLayers layers and <= ARA_MAX_SLOTS slots each
     ara_portfolio *p = new ara_portfolio();
     p->ctx = c;
     p->n_layers_total = n_layers;
     for (uint32_t l0 = 0; l0 < n_layers;) {
         uint32_t l1 = l0 + 1;
-        while (l1 < n_layers && l1 - l0 < (uint32_t)kSplitMaxLayers && loff[l1 + 1] - loff[l0] <= ARA_MAX_SLOTS) ++l1;
+        while (l1 < n_layers && fits(l0, l1)) ++l1;
         std::vector<uint64_t> sub(l1 - l0 + 1);
         for (uint32_t l = l0; l <= l1; ++l) sub[l - l0] = loff[l] - loff[l0];
         ara_portfolio *g = nullptr;
@@ -781,6 +806,7 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
 
 static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
                     float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash) {
+    NvtxRange nvtx("ara_run");
     if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
     if (p->groups.empty()) return run_group(c, p, y, seed, flags, ylt, occ_max, dbg_count, dbg_hash);
     // one run per group of layers over the same YET (the draws do not depend on
@@ -896,6 +922,7 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
         CU(cudaStreamSynchronize(ss));
         const uint32_t n_ovf = c->h_status->bad_event ? 0u : c->h_status->n_ovf;
         if (n_ovf) {
+            NvtxRange nvtx_ovf("ara_run overflow pass");
             // overflow pass: the listed trials compacted again into exactly sized
             // regions of the pool, then sampled by the same kernel (same arithmetic)
             std::vector<uint32_t> cnt(n_ovf);
@@ -1061,6 +1088,7 @@ int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t 
 int ara_risk_measures_batch(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
                             uint32_t n_shards, const int32_t *layers, uint32_t n_sel, const double *rps,
                             uint32_t n_rp, double *pml_out, double *tvar_out, double *var_out) {
+    NvtxRange nvtx("ara_risk_measures_batch");
     if (!c || !ylt || !layers || !rps || !pml_out || !tvar_out) return fail(ARA_EINVAL, "NULL argument");
     if (n_total == 0) return fail(ARA_EINVAL, "empty YLT");
     if (n_layers == 0 || n_shards == 0 || n_total % n_shards)
@@ -1100,6 +1128,7 @@ int ara_risk_measures_batch(ara_ctx *c, const float *ylt, uint32_t n_layers, uin
 int ara_risk_measures_var(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
                           uint32_t n_shards, int32_t layer, const double *rps, uint32_t n_rp,
                           double *pml_out, double *tvar_out, double *var_out) {
+    NvtxRange nvtx("ara_risk_measures");
     if (!c || !ylt || !rps || !pml_out || !tvar_out) return fail(ARA_EINVAL, "NULL argument");
     if (n_total == 0) return fail(ARA_EINVAL, "empty YLT");
     if (n_layers == 0 || n_shards == 0 || n_total % n_shards)

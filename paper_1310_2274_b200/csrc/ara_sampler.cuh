@@ -31,6 +31,28 @@
 
 namespace ara {
 
+// ------------------------------------------------- fast fp32 intrinsics ---
+// MUFU approximations with flush-to-zero: the sampler only feeds them normal
+// arguments with normal results (the node sigmoids clamp lambda to +-80, the
+// erfinv log's argument is >= 2^-23, reciprocals are of 1 + e >= 1), where
+// the .ftz forms return exactly what __expf / __logf / __fdividef return --
+// without the subnormal fix-ups those emit (3 instructions each)
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // ---------------------------------------------------------------- draws ---
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
@@ -64,7 +86,7 @@ __device__ __forceinline__ float u01_from_bits(uint32_t x) {
 __device__ __forceinline__ float norm_quantile_from_bits(uint32_t x) {
     const int yi = (int)((x >> 9) << 1) + 1 - (1 << 23);
     const float y = (float)yi * 1.1920928955078125e-07f;      // exact
-    float w = -__logf((1.0f - y) * (1.0f + y));
+    float w = -0.69314718055994530942f * lg2_ftz((1.0f - y) * (1.0f + y));   // -ln((1-y)(1+y))
     float p;                                                  // sqrt(2) x Giles' coefficients
     if (w < 5.0f) {
         w = w - 2.5f;
@@ -212,8 +234,8 @@ __device__ __forceinline__ double lambda_exact64(double v, double a, double b, d
 
 __device__ __forceinline__ void sigmoid2(float lam, float &x, float &y) {
     const float l = fminf(fmaxf(lam, -80.0f), 80.0f);
-    const float e = __expf(-l);
-    x = __fdividef(1.0f, 1.0f + e);                      // MUFU.RCP (2 ulp)
+    const float e = ex2_ftz(-1.44269504088896340736f * l);   // e^-l, normal
+    x = rcp_ftz(1.0f + e);                               // MUFU.RCP
     y = e * x;
 }
 
@@ -256,9 +278,10 @@ __device__ __forceinline__ float lambda_table(const float2 *__restrict__ tables,
 }
 
 __device__ __forceinline__ float sigmoidf_(float lam) {
-    // 1/(1+e^-lam); e^-lam = inf for lam < -88 gives 0 (the loss underflows to 0)
-    const float e = __expf(-lam);
-    return e < 3.0e38f ? __fdividef(1.0f, 1.0f + e) : 0.0f;
+    // 1/(1+e^-lam); e^-lam = inf for lam < -88 gives 0 (the loss underflows to 0);
+    // e^-lam below 2^-126 flushes to 0, where 1/(1+e) is 1 either way
+    const float e = ex2_ftz(-1.44269504088896340736f * lam);
+    return e < 3.0e38f ? rcp_ftz(1.0f + e) : 0.0f;
 }
 
 // Per-sample fp64 solve (table-less records, ARA_EXACT); kept out of line so

@@ -245,16 +245,20 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
             if (PK) {                                 // pair = record * 2^kbits + k (one IMAD)
                 uint32_t *const out32 = reinterpret_cast<uint32_t *>(out);
                 uint32_t pv[4];
+                // the first two pairs of each event in this pass (a chunk of
+                // cfg3 almost always holds an event with two records), the
+                // rest in a warp-uniform loop (a third pair: ~1/3 of chunks)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     pq[q] = o;
                     pv[q] = S.ci[q].x * mul + (k0 + q);
                     st_u32_if(S.ci[q].y != 0u, reinterpret_cast<uint64_t>(out32 + o), pv[q]);
+                    st_u32_if(S.ci[q].y > 1u, reinterpret_cast<uint64_t>(out32 + o + 1), pv[q] + mul);
                     o += S.ci[q].y;
                     mx = max(mx, S.ci[q].y);
                 }
 #pragma unroll 1
-                for (uint32_t j = 1; __any_sync(0xffffffffu, j < mx); ++j)   // the events with several pairs
+                for (uint32_t j = 2; __any_sync(0xffffffffu, j < mx); ++j)   // events with three or more pairs
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
                         st_u32_if(j < S.ci[q].y, reinterpret_cast<uint64_t>(out32 + (pq[q] + j)), pv[q] + j * mul);

@@ -1019,3 +1019,26 @@ def test_supplied_z_errors(A, ctx):
     with pytest.raises(A.AraError):
         A.run(ctx, P2, Y, seed=1, rng="supplied")
     A.run(ctx, P, Y, seed=1, rng="supplied")
+
+
+def test_group_byte_budget_splits_passes(A, ctx, monkeypatch):
+    # ARA_GROUP_BYTES bounds each kernel group's gathered tables (one pass over
+    # the YET per group): 1 group or one per layer -> the same
+    # YLT, counts, hashes and occ_max bit for bit (the draws do not depend on
+    # the layer's group)
+    cfg = aragen.load_config("cfg1")
+    cfg.update(n_layers=4, elts_per_layer=3, catalog=5000, records_per_elt=800, n_trials=300,
+               layer_terms=[[2e5 * (l + 1), 5e6, 1.0e6, 5.0e7] for l in range(4)])
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    one = A.Portfolio(ctx, pf)
+    monkeypatch.setenv("ARA_GROUP_BYTES", "1")
+    per_layer = A.Portfolio(ctx, pf)
+    monkeypatch.delenv("ARA_GROUP_BYTES")
+    Y = A.Yet.from_dict(ctx, yet)
+    a = A.run(ctx, one, Y, seed=4, debug=True)
+    b = A.run(ctx, per_layer, Y, seed=4, debug=True)
+    assert A.last_run_timings(ctx)["launches"] >= 8          # 4 groups x (compaction + sampler)
+    for x, y in zip(a, b):
+        assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
+    ea, eb = A.run_ep(ctx, one, Y, seed=4), A.run_ep(ctx, per_layer, Y, seed=4)
+    assert np.array_equal(ea[1].cpu().numpy(), eb[1].cpu().numpy())

@@ -272,6 +272,7 @@ def run_ours(args, cfg, rank, world, local):
     ara.prepare(ctx, P, Y, su=cfg["su"])        # every ara_run scratch buffer, allocated once here
 
     kern_ms = []          # per-kernel CUDA-event sums of each timed ara_run (ara_last_run_timings)
+    meas_ev = []          # CUDA events around each timed step's all-gather + measures
 
     def measures(src, n_shards):
         if len(layers) > 1 and len(rps) <= 4:        # every table in one call, one read-back
@@ -283,8 +284,14 @@ def run_ours(args, cfg, rank, world, local):
         ara.run(ctx, P, Yx, seed=cfg["seed"], su=cfg["su"], ylt=ylt)
         if timed:
             kern_ms.append(ara.last_run_timings(ctx))
+            m0 = torch.cuda.Event(enable_timing=True); m1 = torch.cuda.Event(enable_timing=True)
+            m0.record(stream)
         src, n_shards = gather_ylt(ylt, world, N_total, gathered, padded)
-        return measures(src, n_shards)
+        out = measures(src, n_shards)
+        if timed:
+            m1.record(stream)
+            meas_ev.append((m0, m1))
+        return out
 
     # exact number of present (occurrence, slot) pairs = SU samples per launch
     _, cnt_dbg, _ = ara.run(ctx, P, Y, seed=cfg["seed"], su=cfg["su"], debug=True)
@@ -436,7 +443,8 @@ def run_ours(args, cfg, rank, world, local):
         dom = sample if t_sample >= t_compact else compact
     roof = dict(dom)
     roof["peak_note"] = peak_src if roof.get("unit") == "GB/s" else roof.get("peak_source")
-    roof["kernels"] = dict(kernels, redo_ms=t_redo * 1e3)
+    roof["kernels"] = dict(kernels, redo_ms=t_redo * 1e3,
+                           gather_and_measures_ms=sum(a.elapsed_time(b) for a, b in meas_ev) / max(len(meas_ev), 1))
     roof["path_hbm"] = {"alg_bytes_per_step": alg_bytes, "step_ms": step_s * 1e3,
                         "achieved": alg_bytes / step_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                         "frac": alg_bytes / step_s / 1e9 / hbm_peak}

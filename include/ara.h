@@ -80,6 +80,8 @@ extern "C" {
 #define ARA_MAX_PORTFOLIO_SLOTS 65536    /* sum over layers of XELTs per layer
                                             ("10,000 XELTs")          */
 #define ARA_MAX_EVENTS_PER_TRIAL (1u << 24)
+#define ARA_MAX_XELTS (1u << 24)          /* XELTs per portfolio (~10,000) */
+#define ARA_MAX_PROGRAMS 256u             /* program ids 0..255 (up to 10) */
 
 typedef struct ara_ctx ara_ctx;
 typedef struct ara_portfolio ara_portfolio;
@@ -132,13 +134,14 @@ int ara_ctx_synchronize(ara_ctx *ctx);
 /* Host-only validation of a portfolio (no device needed); same arguments
  * and checks as ara_create_portfolio.  Host pointers only.
  *   catalog_size        number of events in the catalogue (event ids < it)
- *   n_elts              number of XELTs
+ *   n_elts              number of XELTs, <= ARA_MAX_XELTS
  *   elt_rec_offsets     [n_elts+1] record ranges; records of XELT j are
  *                       records[elt_rec_offsets[j] .. elt_rec_offsets[j+1])
  *   records             [elt_rec_offsets[n_elts]] XELT records
  *   elt_terms           [n_elts] or NULL (identity, G7)
  *   n_layers            layers in the portfolio, <= ARA_MAX_PORTFOLIO_LAYERS
- *   layer_program       [n_layers] program id of each layer (keys z_(Prog,E))
+ *   layer_program       [n_layers] program id of each layer (keys z_(Prog,E)),
+ *                       < ARA_MAX_PROGRAMS
  *   layer_elt_offsets   [n_layers+1] ranges into layer_elts
  *   layer_elts          XELT ids covered by each layer, no duplicates within
  *                       a layer; <= ARA_MAX_SLOTS per layer, sum of layer

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -111,17 +112,36 @@ struct ara_ctx {
     uint32_t last_launches = 0, last_batches = 0;               // kernels launched by the last ara_run
 };
 
+// Per input XELT record, shared by every (layer, XELT) slot and every
+// kernel group that covers the record's XELT: the beta parameters, the mean
+// loss and the quantile table are a function of the record alone, built once
+// (NEXT-2: one table per record, not one per (layer, record)).
+struct RecordStore {
+    int device = 0;
+    uint64_t n = 0;                    // input records
+    BetaRec *d_recs = nullptr;         // [n]
+    float *d_mu = nullptr;             // [n]
+    float2 *d_hot = nullptr;           // [n][kHotN] central table nodes
+    float2 *d_cold = nullptr;          // [n][kColdN] tail table nodes
+    uint32_t n_exact = 0;              // records whose table failed its midpoint check
+    std::vector<uint32_t> pos;         // store position of each input record (the store follows the first
+                                       // kernel group's event-major device order, so for a portfolio of one
+                                       // group without shared XELTs a pair's table is its device record's)
+    ~RecordStore() {
+        cudaSetDevice(device);
+        cudaFree(d_recs); cudaFree(d_mu); cudaFree(d_hot); cudaFree(d_cold);
+    }
+    uint64_t bytes() const { return n * (sizeof(BetaRec) + sizeof(float) + (kHotN + kColdN) * sizeof(float2)); }
+};
+
 struct ara_portfolio {
     ara_ctx *ctx = nullptr;
     PortfolioDev dev{};
-    uint32_t *d_index = nullptr, *d_bitmap = nullptr, *d_rec_orig = nullptr;
+    uint32_t *d_bitmap = nullptr, *d_rec_orig = nullptr;
     uint2 *d_cidx = nullptr;
-    uint32_t *d_rec_meta = nullptr;
     SplitRec *d_srecs = nullptr;
     uint2 *d_mm = nullptr;             // (mean loss bits, meta) per device record (primary uncertainty)
-    BetaRec *d_recs = nullptr;
-    float2 *d_tables = nullptr, *d_hot = nullptr;
-    float *d_mu = nullptr;
+    std::shared_ptr<RecordStore> store;   // per input record (shared by the groups)
     SlotInfo *d_slots = nullptr;
     LayerInfo *d_layers = nullptr;
     float *d_occ = nullptr;            // [catalog][occ_lp] occurrence losses without draws (fast path)
@@ -285,6 +305,10 @@ int ara_validate_portfolio(uint32_t C, uint32_t n_elts, const uint64_t *eoff, co
     if (n_layers > ARA_MAX_PORTFOLIO_LAYERS)
         return fail(ARA_EINVAL, "n_layers %u > %d", n_layers, ARA_MAX_PORTFOLIO_LAYERS);
     if (!lprog || !loff || !lt) return fail(ARA_EINVAL, "layer arrays are NULL");
+    if (n_elts > ARA_MAX_XELTS) return fail(ARA_EINVAL, "n_elts %u > %u", n_elts, ARA_MAX_XELTS);
+    for (uint32_t l = 0; l < n_layers; ++l)
+        if (lprog[l] >= ARA_MAX_PROGRAMS)
+            return fail(ARA_EINVAL, "layer %u: program %u >= %u", l, lprog[l], ARA_MAX_PROGRAMS);
     if (loff[0] != 0) return fail(ARA_EINVAL, "layer_elt_offsets[0] must be 0");
     const uint64_t nslots = loff[n_layers];
     if (nslots > ARA_MAX_PORTFOLIO_SLOTS)
@@ -314,7 +338,52 @@ int ara_validate_portfolio(uint32_t C, uint32_t n_elts, const uint64_t *eoff, co
 static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t *eoff,
                         const ara_record *rec, const ara_elt_terms *et, uint32_t n_layers,
                         const uint32_t *lprog, const uint64_t *loff, const uint32_t *lelts,
-                        const ara_layer_terms *lt, ara_portfolio **out);
+                        const ara_layer_terms *lt, std::shared_ptr<RecordStore> &store,
+                        ara_portfolio **out);
+
+// the record store: upload the input records, derive their beta parameters and
+// quantile tables on the device (one thread per record, fp64)
+static int create_store(ara_ctx *c, const ara_record *rec, uint64_t R, const std::vector<uint32_t> &first_order,
+                        std::shared_ptr<RecordStore> &out) {
+    auto st = std::make_shared<RecordStore>();
+    st->device = c->device;
+    st->n = R;
+    // order: the input records in the first group's device-record order (first
+    // occurrence), then every other record
+    std::vector<uint32_t> order;
+    order.reserve(R);
+    st->pos.assign(R, 0xffffffffu);
+    for (uint32_t src : first_order)
+        if (st->pos[src] == 0xffffffffu) { st->pos[src] = (uint32_t)order.size(); order.push_back(src); }
+    for (uint64_t src = 0; src < R; ++src)
+        if (st->pos[src] == 0xffffffffu) { st->pos[src] = (uint32_t)order.size(); order.push_back((uint32_t)src); }
+    ara_record *d_raw = nullptr;
+    uint32_t *d_order = nullptr;
+    cudaStream_t s = c->stream;
+    if (dalloc(&st->d_recs, R) || dalloc(&st->d_mu, R) || dalloc(&st->d_hot, R * kHotN) ||
+        dalloc(&st->d_cold, R * kColdN) ||
+        dalloc(&d_raw, R) || dalloc(&d_order, R)) {
+        cudaGetLastError();
+        cudaFree(d_raw); cudaFree(d_order);
+        return fail(ARA_ENOMEM, "device allocation of %llu records failed in ara_create_portfolio",
+                    (unsigned long long)R);
+    }
+    cudaError_t e = R ? cudaMemcpyAsync(d_raw, rec, R * sizeof(ara_record), cudaMemcpyHostToDevice, s) : cudaSuccess;
+    if (e == cudaSuccess && R) e = cudaMemcpyAsync(d_order, order.data(), R * sizeof(uint32_t), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
+    if (e == cudaSuccess) {
+        launch_prep_records(d_raw, d_order, R, st->d_recs, st->d_mu, st->d_hot, st->d_cold,
+                            &c->d_status->nonconverged, s);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(d_raw); cudaFree(d_order);
+    if (e != cudaSuccess) return fail(ARA_ECUDA, "record preparation: %s", cudaGetErrorString(e));
+    st->n_exact = c->h_status->nonconverged;
+    out = st;
+    return ARA_OK;
+}
 
 int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t *eoff,
                          const ara_record *rec, const ara_elt_terms *et, uint32_t n_layers,
@@ -327,11 +396,11 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     if (st != ARA_OK) return st;
     // Kernel groups of consecutive layers: <= kSplitMaxLayers layers, <=
     // ARA_MAX_SLOTS slots, and -- so that each pass's gathered tables stay
-    // L2-resident -- at most ARA_GROUP_BYTES (default 64 MiB)
+    // L2-resident -- at most ARA_GROUP_BYTES (default 128 MiB)
     // of per-record sampler data (SplitRec + hot table rows, 160 B per
     // (layer, record)) plus the catalogue index (8 B per event); a single
     // layer always forms a group.  Each group re-streams the YET.
-    const uint64_t budget = env_u64("ARA_GROUP_BYTES", 64ull << 20);
+    const uint64_t budget = env_u64("ARA_GROUP_BYTES", 128ull << 20);
     auto layer_records = [&](uint32_t l) {
         uint64_t r = 0;
         for (uint64_t x = loff[l]; x < loff[l + 1]; ++x) r += eoff[lelts[x] + 1] - eoff[lelts[x]];
@@ -343,8 +412,10 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
         for (uint32_t l = l0; l <= l1; ++l) recs += layer_records(l);
         return l1 == l0 || recs * 160 + (uint64_t)C * 8 <= budget;
     };
+    CU(cudaSetDevice(c->device));
+    std::shared_ptr<RecordStore> store;              // built by the first group (its device order)
     if (fits(0, n_layers - 1))
-        return create_group(c, C, n_elts, eoff, rec, et, n_layers, lprog, loff, lelts, lt, out);
+        return create_group(c, C, n_elts, eoff, rec, et, n_layers, lprog, loff, lelts, lt, store, out);
     ara_portfolio *p = new ara_portfolio();
     p->ctx = c;
     p->n_layers_total = n_layers;
@@ -354,13 +425,15 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
         std::vector<uint64_t> sub(l1 - l0 + 1);
         for (uint32_t l = l0; l <= l1; ++l) sub[l - l0] = loff[l] - loff[l0];
         ara_portfolio *g = nullptr;
-        st = create_group(c, C, n_elts, eoff, rec, et, l1 - l0, lprog + l0, sub.data(), lelts + loff[l0], lt + l0, &g);
+        st = create_group(c, C, n_elts, eoff, rec, et, l1 - l0, lprog + l0, sub.data(), lelts + loff[l0], lt + l0,
+                          store, &g);
         if (st != ARA_OK) {
             ara_portfolio_destroy(p);
             return st;
         }
         p->groups.push_back(g);
         p->group_layer0.push_back(l0);
+        p->store = store;
         l0 = l1;
     }
     *out = p;
@@ -370,7 +443,8 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
 static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t *eoff,
                         const ara_record *rec, const ara_elt_terms *et, uint32_t n_layers,
                         const uint32_t *lprog, const uint64_t *loff, const uint32_t *lelts,
-                        const ara_layer_terms *lt, ara_portfolio **out) {
+                        const ara_layer_terms *lt, std::shared_ptr<RecordStore> &store,
+                        ara_portfolio **out) {
     CU(cudaSetDevice(c->device));
 
     // slots: (layer, XELT) pairs, layer-major
@@ -406,8 +480,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
 
     // event-major direct-access index: per event the slots with a record
     const uint32_t MW = (S + 31) / 32;
-    const uint32_t mwt = MW <= 1 ? 1 : (MW <= 3 ? 3 : (MW <= 4 ? 4 : 7));
-    const uint32_t stride = mwt == 1 ? 2 : (mwt == 3 ? 4 : 8);
+    const uint32_t stride = MW + 1;                 // host-side planning index: first record, slot mask words
     std::vector<uint32_t> index((size_t)C * stride, 0u);
     for (uint32_t s = 0; s < S; ++s) {
         const uint32_t j = slots[s].elt;
@@ -460,65 +533,59 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
         if (any) bitmap[(e >> shift) >> 5] |= 1u << ((e >> shift) & 31);
     }
 
+    if (!store) {
+        const int st = create_store(c, rec, eoff[n_elts], rec_src, store);
+        if (st != ARA_OK) return st;
+    }
+    std::vector<uint32_t> tab(total);           // store position (table) of each device record
+    for (uint64_t r = 0; r < total; ++r) tab[r] = store->pos[rec_src[r]];
     ara_portfolio *p = new ara_portfolio();
     p->ctx = c;
-    ara_record *d_raw = nullptr;
-    uint32_t *d_src = nullptr;
-    const uint64_t R = eoff[n_elts];
+    p->store = store;
     cudaStream_t s = c->stream;
+    uint32_t *d_rec_meta = nullptr, *d_rec_src = nullptr;   // build-time arrays
     auto cleanup = [&](int code) {
-        cudaFree(d_raw); cudaFree(d_src);
+        cudaFree(d_rec_meta); cudaFree(d_rec_src);
         ara_portfolio_destroy(p);
         return code;
     };
-    if (dalloc(&p->d_index, index.size()) || dalloc(&p->d_bitmap, words) ||
-        dalloc(&p->d_cidx, (size_t)C) || dalloc(&p->d_rec_meta, (size_t)total) || dalloc(&p->d_srecs, (size_t)total) ||
-        dalloc(&p->d_mm, (size_t)total) ||
-        dalloc(&p->d_rec_orig, total) || dalloc(&p->d_recs, total) || dalloc(&p->d_mu, total) ||
-        dalloc(&p->d_tables, total * kTabStride) || dalloc(&p->d_hot, total * kHotN) ||
-        dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) || dalloc(&d_raw, R) ||
-        dalloc(&p->d_occ, (size_t)C * occ_lp) || dalloc(&p->d_slot_terms, slot_terms.size()) ||
-        dalloc(&d_src, total)) {
+    if (dalloc(&p->d_bitmap, words) ||
+        dalloc(&p->d_cidx, (size_t)C) || dalloc(&d_rec_meta, (size_t)total) || dalloc(&p->d_srecs, (size_t)total) ||
+        dalloc(&p->d_mm, (size_t)total) || dalloc(&p->d_rec_orig, total) || dalloc(&d_rec_src, total) ||
+        dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) ||
+        dalloc(&p->d_occ, (size_t)C * occ_lp) || dalloc(&p->d_slot_terms, slot_terms.size())) {
         cudaGetLastError();
         return cleanup(fail(ARA_ENOMEM, "device allocation failed in ara_create_portfolio"));
     }
     cudaError_t e = cudaSuccess;
 #define UP(dst, src, n) if (e == cudaSuccess && (n)) e = cudaMemcpyAsync(dst, src, (n) * sizeof(*(src)), cudaMemcpyHostToDevice, s)
-    UP(p->d_index, index.data(), index.size());
     UP(p->d_bitmap, bitmap.data(), (size_t)words);
     UP(p->d_rec_orig, rec_orig.data(), (size_t)total);
     UP(p->d_cidx, cidx.data(), (size_t)C);
-    UP(p->d_rec_meta, rec_meta.data(), (size_t)total);
+    UP(d_rec_meta, rec_meta.data(), (size_t)total);
     UP(p->d_slots, slots.data(), (size_t)S);
     UP(p->d_layers, layers.data(), (size_t)n_layers);
-    UP(d_raw, rec, (size_t)R);
-    UP(d_src, rec_src.data(), (size_t)total);
+    UP(d_rec_src, tab.data(), (size_t)total);
     UP(p->d_slot_terms, slot_terms.data(), slot_terms.size());
 #undef UP
     if (e != cudaSuccess) return cleanup(fail(ARA_ECUDA, "upload: %s", cudaGetErrorString(e)));
-    e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
     if (e == cudaSuccess) {
-        launch_prep_records(d_raw, d_src, total, p->d_recs, p->d_mu, p->d_tables, p->d_hot,
-                            &c->d_status->nonconverged, s);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) {
-        launch_split_recs(p->d_recs, p->d_rec_meta, p->d_slots, p->d_mu, total, p->d_srecs, p->d_mm, s);
+        launch_split_recs(store->d_recs, d_rec_src, d_rec_meta, p->d_slots, store->d_mu, total, p->d_srecs,
+                          p->d_mm, s);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) {       // lines 6-11 per (event, layer) at the mean losses (fast path)
-        launch_occ_table(p->d_cidx, p->d_rec_meta, p->d_mu, p->d_slot_terms, p->d_layers, n_layers, occ_lp, C,
+        launch_occ_table(p->d_cidx, p->d_mm, p->d_slot_terms, p->d_layers, n_layers, occ_lp, C,
                          p->d_occ, s);
         e = cudaGetLastError();
     }
-    if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);     // host vectors die at return
-    cudaFree(d_raw); cudaFree(d_src);
-    d_raw = nullptr; d_src = nullptr;
-    if (e != cudaSuccess) return cleanup(fail(ARA_ECUDA, "record preparation: %s", cudaGetErrorString(e)));
+    cudaFree(d_rec_meta); cudaFree(d_rec_src);          // (build-time only)
+    d_rec_meta = nullptr; d_rec_src = nullptr;
+    if (e != cudaSuccess) return cleanup(fail(ARA_ECUDA, "portfolio layout: %s", cudaGetErrorString(e)));
 
     PortfolioDev &d = p->dev;
-    d.catalog = C; d.n_slots = S; d.n_layers = n_layers; d.mask_words = mwt; d.idx_stride = stride;
+    d.catalog = C; d.n_slots = S; d.n_layers = n_layers;
     d.bitmap_shift = shift; d.bitmap_words = words; d.n_dev_records = total;
     {   // sentinel event for the compaction's partial chunks: a presence bit that is 0
         d.sentinel_ok = 0; d.sentinel_event = 0;
@@ -530,15 +597,14 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
                     d.sentinel_event = (uint32_t)(b << shift); d.sentinel_ok = 1;
                 }
     }
-    d.n_exact_records = c->h_status->nonconverged;
-    d.index = p->d_index; d.bitmap = p->d_bitmap; d.recs = p->d_recs; d.rec_mu = p->d_mu;
-    d.tables = p->d_tables;
-    d.hot = p->d_hot;
+    d.n_exact_records = store->n_exact;
+    d.bitmap = p->d_bitmap; d.recs = store->d_recs; d.rec_mu = store->d_mu;
+    d.tables = TablePtr{store->d_hot, store->d_cold};
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
-    d.cidx = p->d_cidx; d.rec_meta = p->d_rec_meta; d.srecs = p->d_srecs; d.mu_meta = p->d_mm;
+    d.cidx = p->d_cidx; d.srecs = p->d_srecs; d.mu_meta = p->d_mm;
     d.any_terms = et ? 1u : 0u;
     p->rec_src = std::move(rec_src);
-    p->n_input_records = R;
+    p->n_input_records = eoff[n_elts];
     for (uint32_t l = 0; l < n_layers; ++l) p->max_prog = std::max(p->max_prog, lprog[l]);
     d.all_sigma_zero = all_sigma_zero ? 1u : 0u;
     d.occ_lp = occ_lp;
@@ -547,29 +613,29 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     return ARA_OK;
 }
 
+static uint64_t group_bytes(const ara_portfolio *g) {          // per-group arrays (not the record store)
+    const PortfolioDev &d = g->dev;
+    return (uint64_t)d.catalog * (sizeof(uint2) + d.occ_lp * sizeof(float)) +
+           (uint64_t)d.bitmap_words * 4 +
+           d.n_dev_records * (sizeof(SplitRec) + sizeof(uint2) + sizeof(uint32_t)) +
+           d.n_slots * (sizeof(SlotInfo) + 4 * sizeof(double)) + d.n_layers * sizeof(LayerInfo);
+}
+
 int ara_portfolio_info(const ara_portfolio *p, uint64_t *n_dev, uint64_t *n_tl, uint64_t *bytes) {
     if (!p) return fail(ARA_EINVAL, "portfolio is NULL");
+    uint64_t a = 0, c = 0;
     if (!p->groups.empty()) {                          // sums over the groups
-        uint64_t a = 0, b = 0, c = 0;
         for (const ara_portfolio *g : p->groups) {
-            uint64_t x = 0, y = 0, z = 0;
-            ara_portfolio_info(g, &x, &y, &z);
-            a += x; b += y; c += z;
+            a += g->dev.n_dev_records;
+            c += group_bytes(g);
         }
-        if (n_dev) *n_dev = a;
-        if (n_tl) *n_tl = b;
-        if (bytes) *bytes = c;
-        return ARA_OK;
+    } else {
+        a = p->dev.n_dev_records;
+        c = group_bytes(p);
     }
-    const PortfolioDev &d = p->dev;
-    if (n_dev) *n_dev = d.n_dev_records;
-    if (n_tl) *n_tl = d.n_exact_records;
-    if (bytes)
-        *bytes = (uint64_t)d.catalog * (d.idx_stride * 4 + sizeof(uint2)) + (uint64_t)d.bitmap_words * 4 +
-                 d.n_dev_records * (sizeof(BetaRec) + sizeof(float) + sizeof(uint32_t) + sizeof(uint32_t) + sizeof(SplitRec) + sizeof(uint2) +
-                                    (kTabStride + kHotN) * sizeof(float2)) +
-                 d.n_slots * (sizeof(SlotInfo) + 4 * sizeof(double)) + d.n_layers * sizeof(LayerInfo) +
-                 (uint64_t)d.catalog * d.occ_lp * sizeof(float);
+    if (n_dev) *n_dev = a;
+    if (n_tl) *n_tl = p->store ? p->store->n_exact : 0;
+    if (bytes) *bytes = c + (p->store ? p->store->bytes() : 0);
     return ARA_OK;
 }
 
@@ -577,9 +643,9 @@ void ara_portfolio_destroy(ara_portfolio *p) {
     if (!p) return;
     for (ara_portfolio *g : p->groups) ara_portfolio_destroy(g);
     if (p->ctx) cudaSetDevice(p->ctx->device);
-    cudaFree(p->d_index); cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig); cudaFree(p->d_recs);
-    cudaFree(p->d_cidx); cudaFree(p->d_rec_meta); cudaFree(p->d_srecs); cudaFree(p->d_mm);
-    cudaFree(p->d_mu); cudaFree(p->d_slots); cudaFree(p->d_layers); cudaFree(p->d_tables); cudaFree(p->d_hot);
+    cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig);
+    cudaFree(p->d_cidx); cudaFree(p->d_srecs); cudaFree(p->d_mm);
+    cudaFree(p->d_slots); cudaFree(p->d_layers);
     cudaFree(p->d_occ); cudaFree(p->d_slot_terms); cudaFree(p->d_rec_z);
     delete p;
 }
@@ -1186,13 +1252,12 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
     CU(cudaSetDevice(c->device));
     ara_record *d_raw = nullptr;
     BetaRec *d_recs = nullptr;
-    float2 *d_tab = nullptr, *d_hot = nullptr;
+    float2 *d_hot = nullptr, *d_cold = nullptr;
     float *d_mu = nullptr, *d_zp = nullptr, *d_ze = nullptr, *d_out = nullptr;
     int code = ARA_OK;
     cudaError_t e = cudaSuccess;
     if (dalloc(&d_raw, n) || dalloc(&d_recs, n) || dalloc(&d_mu, n) || dalloc(&d_zp, n) ||
-        dalloc(&d_ze, n) || dalloc(&d_out, n) || dalloc(&d_tab, n * kTabStride) ||
-        dalloc(&d_hot, n * kHotN)) {
+        dalloc(&d_ze, n) || dalloc(&d_out, n) || dalloc(&d_hot, n * kHotN) || dalloc(&d_cold, n * kColdN)) {
         cudaGetLastError();
         code = fail(ARA_ENOMEM, "device allocation failed");
     } else {
@@ -1201,8 +1266,8 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
         if (!e) e = cudaMemcpyAsync(d_zp, zp, n * sizeof(float), cudaMemcpyHostToDevice, s);
         if (!e) e = cudaMemcpyAsync(d_ze, ze, n * sizeof(float), cudaMemcpyHostToDevice, s);
         if (!e) e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
-        if (!e) { launch_prep_records(d_raw, nullptr, n, d_recs, d_mu, d_tab, d_hot, nullptr, s); e = cudaGetLastError(); }
-        if (!e) e = launch_sample_losses(d_recs, d_tab, d_hot, d_zp, d_ze, n, (flags & ARA_EXACT) != 0, d_out,
+        if (!e) { launch_prep_records(d_raw, nullptr, n, d_recs, d_mu, d_hot, d_cold, nullptr, s); e = cudaGetLastError(); }
+        if (!e) e = launch_sample_losses(d_recs, TablePtr{d_hot, d_cold}, d_zp, d_ze, n, (flags & ARA_EXACT) != 0, d_out,
                                          c->d_status, s);
         if (!e) e = cudaMemcpyAsync(loss_out, d_out, n * sizeof(float), cudaMemcpyDeviceToHost, s);
         if (!e) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
@@ -1212,7 +1277,7 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
             code = fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples", c->h_status->nonconverged);
     }
     cudaFree(d_raw); cudaFree(d_recs); cudaFree(d_mu); cudaFree(d_zp); cudaFree(d_ze); cudaFree(d_out);
-    cudaFree(d_tab); cudaFree(d_hot);
+    cudaFree(d_hot); cudaFree(d_cold);
     return code;
 }
 

@@ -33,13 +33,25 @@ struct LayerInfo {
 //               sqrt(psi1(a)+psi1(b))): initial guess of the fp64 solve
 //   mode      : kModeTable (quantile table), kModeExact (per-sample fp64
 //               solve), kModeDegenerate (loss = scale)
-// quantile tables: lambda(v) = logit I^-1(Phi(v); a, b) at v = -8 + 0.5 j
-constexpr int kTabNodes = 33;           // j = 0..32
-constexpr int kTabStride = 34;          // float2 per record (padded)
-constexpr float kTabV0 = -8.0f, kTabH = 0.5f;
-// the central nodes j = 9..24 (v in [-3.5, 4]; 99.97 % of samples) are also
-// kept in a compact 128 B-per-record "hot" array that stays L2-resident
-constexpr int kHotJ0 = 9, kHotN = 16;
+// quantile tables: lambda(v) = logit I^-1(Phi(v); a, b) at v = -7.75 + 0.5 j,
+// j = 0..31 (|v| <= 7.48 for the draws of U's grid), stored in two dense
+// arrays per record: the "hot" central nodes j = 8..23 (v in [-3.75, 3.75]:
+// 99.98 % of samples; 128 B = one line per record, the part that stays
+// L2-resident) and the "cold" tail nodes (144 B): j = 23..31 then 0..8, node
+// j at (j + 9) mod 32, so every tail interval's two nodes are adjacent and
+// the boundary nodes 8 and 23 are kept in both arrays
+constexpr int kTabNodes = 32;
+constexpr float kTabV0 = -7.75f, kTabH = 0.5f;
+constexpr int kHotJ0 = 8, kHotN = 16, kColdN = 18;
+struct TablePtr {
+    const float2 *hot;        // [records][kHotN]
+    const float2 *cold;       // [records][kColdN]
+};
+// the nodes of interval ti (ti, ti + 1 adjacent) of record rec
+__device__ __forceinline__ const float2 *table_row(const TablePtr &T, uint64_t rec, int ti) {
+    return (unsigned)(ti - kHotJ0) < (unsigned)(kHotN - 1) ? T.hot + rec * kHotN + (ti - kHotJ0)
+                                                          : T.cold + rec * kColdN + ((ti + 9) & 31);
+}
 
 constexpr uint32_t kModeTable = 0, kModeExact = 1, kModeDegenerate = 2;
 struct __align__(16) BetaRec {
@@ -48,22 +60,23 @@ struct __align__(16) BetaRec {
     uint32_t mode;
 };
 
-// Per-record constants of the split sampler (32 B, one L2 sector): the beta
-// parameters and weights of BetaRec plus what the draw keys need, so a pair
-// is sampled from this one load.  meta: slot | run_end << 8 | layer << 16 |
-// mode << 28 (run_end: last record of its (event, layer) run).
+// Per device record ((layer, XELT) slot, record) constants of the split
+// sampler (32 B, one L2 sector): the beta parameters and weights of the
+// record's BetaRec plus the draw keys, so a pair is sampled from this one
+// load.  meta: slot | run_end << 8 | layer << 16 | mode << 28 (run_end: last
+// record of its (event, layer) run); tab: the input record (its quantile
+// table, shared by every slot of the XELT); key: XELT id | program << 24
+// (ARA_MAX_XELTS, ARA_MAX_PROGRAMS).
 struct __align__(32) SplitRec {    // 32 B: one 256-bit load
     float a, b, wi, wc;
     float scale;
     uint32_t meta;
-    uint32_t elt, prog;
+    uint32_t tab, key;
 };
 
 struct PortfolioDev {
     uint32_t catalog;
     uint32_t n_slots, n_layers;
-    uint32_t mask_words;      // kernel variant: 1, 3, 4 or 7 words of the per-event slot mask
-    uint32_t idx_stride;      // uint32 words per event index entry (2, 4 or 8)
     uint32_t bitmap_shift;    // event e -> presence bit e >> shift
     uint32_t bitmap_words;
     uint32_t sentinel_event;  // an id whose presence bit is 0 (bit index bitmap_words * 32: the zero word
@@ -71,17 +84,15 @@ struct PortfolioDev {
     uint32_t sentinel_ok;     // 0: no such id fits in 32 bits (per-event length test instead)
     uint64_t n_dev_records;
     uint32_t n_exact_records; // records without a quantile table (fp64 per-sample solve)
-    const uint32_t *index;    // [catalog][idx_stride]: first record, mask words
     const uint32_t *bitmap;   // [bitmap_words]
-    const BetaRec *recs;      // [n_dev_records] event-major, slot order
-    const float2 *tables;     // [n_dev_records][kTabStride] (lambda, lambda') nodes
-    const float2 *hot;        // [n_dev_records][kHotN] nodes kHotJ0.. of the same tables
-    const float *rec_mu;      // [n_dev_records] mean loss (primary uncertainty)
+    const BetaRec *recs;      // [input records] (the record store, shared by the groups)
+    TablePtr tables;          // [input records] (lambda, lambda') nodes, hot + cold
+    const float *rec_mu;      // [input records] mean loss (primary uncertainty)
     const uint32_t *rec_orig; // [n_dev_records] record index within its XELT
     const uint2 *cidx;        // [catalog] (first device record, record count) of each event
-    const uint32_t *rec_meta; // [n_dev_records] slot | run_end << 8 | layer << 16 (SplitRec.meta)
     const SplitRec *srecs;    // [n_dev_records]
-    const uint2 *mu_meta;     // [n_dev_records] (mean loss bits, rec_meta): one 8 B gather per pair with SU off
+    const uint2 *mu_meta;     // [n_dev_records] (mean loss bits, meta = slot | run_end << 8 | layer << 16):
+                              // one 8 B gather per pair with SU off
     uint32_t any_terms;       // some slot has XELT terms (G7)
     uint32_t all_sigma_zero;  // every record has sigma_I = sigma_C = 0 (no draw is ever taken, G10)
     uint32_t occ_lp;          // occurrence losses per event in occ (n_layers rounded up to 1, 2, 4, 8)
@@ -162,7 +173,7 @@ struct PrimaryArgs {
     uint32_t lp;
 };
 cudaError_t launch_primary(const PrimaryArgs &A, cudaStream_t s, int num_sms);
-void launch_occ_table(const uint2 *cidx, const uint32_t *rec_meta, const float *rec_mu, const double *slot_terms,
+void launch_occ_table(const uint2 *cidx, const uint2 *mu_meta, const double *slot_terms,
                       const LayerInfo *layers, uint32_t n_layers, uint32_t lp, uint32_t catalog, float *out,
                       cudaStream_t s);
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
@@ -174,10 +185,11 @@ cudaError_t launch_count_bad(const uint32_t *ev, uint64_t n, uint32_t C, unsigne
                              int num_sms);
 
 // kernels
-void launch_split_recs(const BetaRec *recs, const uint32_t *rec_meta, const SlotInfo *slots, const float *mu,
-                       uint64_t n, SplitRec *out, uint2 *mu_meta, cudaStream_t s);
+void launch_split_recs(const BetaRec *recs, const uint32_t *rec_src, const uint32_t *rec_meta,
+                       const SlotInfo *slots, const float *mu, uint64_t n, SplitRec *out, uint2 *mu_meta,
+                       cudaStream_t s);
 void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_t n,
-                         BetaRec *out, float *out_mu, float2 *tables, float2 *hot,
+                         BetaRec *out, float *out_mu, float2 *hot, float2 *cold,
                          unsigned int *n_exact, cudaStream_t s);
 // Scan every trial of `yet`, or (trial_list != null) only the n_list listed
 // trials.  Without ARA_EXACT the table-only kernel runs and appends to
@@ -188,7 +200,7 @@ cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed
                         const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
                         cudaStream_t s, int num_sms, float *occ_max = nullptr, const float *zp_sup = nullptr,
                         uint64_t zp_stride = 0, const float *ze_sup = nullptr);
-cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float2 *hot,
+cudaError_t launch_sample_losses(const BetaRec *recs, TablePtr tables,
                                  const float *zp,
                                  const float *ze, uint64_t n, bool exact, float *out,
                                  RunStatus *status, cudaStream_t s);

@@ -40,7 +40,7 @@ __device__ double quintic_mid64(float l0, float d0, float l1, float d1, double v
 
 __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const uint32_t *__restrict__ src,
                                     uint64_t n, BetaRec *__restrict__ out, float *__restrict__ out_mu,
-                                    float2 *__restrict__ tables, float2 *__restrict__ hot,
+                                    float2 *__restrict__ hot, float2 *__restrict__ cold,
                                     unsigned int *n_exact) {
     const double LN_SQRT_2PI = 0.91893853320467274178;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
@@ -72,8 +72,8 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
         r.mu_l = (float)mu_l;
         r.sd_l = (float)sqrt(trigamma_d(a) + trigamma_d(b));
         r.mode = kModeTable;
-        if (tables) {
-            float2 *tab = tables + t * kTabStride;
+        if (hot) {
+            float2 tab[kTabNodes];
             double lam[kTabNodes], d1[kTabNodes], d2[kTabNodes];
             bool good = true;
             auto node = [&](int j, double guess) {
@@ -98,8 +98,6 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
                 node(j, lam[j + 1] - kTabH * d1[j + 1] + 0.5 * kTabH * kTabH * d2[j + 1]);
             if (good) {
                 for (int j = 0; j < kTabNodes; ++j) tab[j] = make_float2((float)lam[j], (float)d1[j]);
-                tab[kTabNodes] = make_float2(0.0f, 0.0f);
-                for (int j = 0; j < kHotN; ++j) hot[t * kHotN + j] = tab[kHotJ0 + j];
                 for (int j = 0; j + 1 < kTabNodes && good; ++j) {
                     const double v0 = kTabV0 + kTabH * j;
                     const double li = quintic_mid64(tab[j].x, tab[j].y, tab[j + 1].x, tab[j + 1].y, v0,
@@ -112,7 +110,11 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
                     if (!ok || !isfinite(li) || (x > 1e-7 && (1.0 - x) * fabs(li - le) > 1e-5)) good = false;
                 }
             }
-            if (!good) {
+            if (good) {
+                for (int j = 0; j < kHotN; ++j) hot[t * kHotN + j] = tab[kHotJ0 + j];
+                for (int j = 0; j <= kHotJ0; ++j) cold[t * kColdN + ((j + 9) & 31)] = tab[j];
+                for (int j = kHotJ0 + kHotN - 1; j < kTabNodes; ++j) cold[t * kColdN + ((j + 9) & 31)] = tab[j];
+            } else {
                 r.mode = kModeExact;
                 if (n_exact) atomicAdd(n_exact, 1u);
             }
@@ -122,13 +124,12 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
 }
 
 void launch_prep_records(const ara_record *raw, const uint32_t *src, uint64_t n, BetaRec *out,
-                         float *out_mu, float2 *tables, float2 *hot, unsigned int *n_exact,
-                         cudaStream_t s) {
+                         float *out_mu, float2 *hot, float2 *cold, unsigned int *n_exact, cudaStream_t s) {
     if (n == 0) return;
     const int threads = 128;
     const uint64_t blocks = (n + threads - 1) / threads;
     prep_records_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), threads, 0, s>>>(
-        raw, src, n, out, out_mu, tables, hot, n_exact);
+        raw, src, n, out, out_mu, hot, cold, n_exact);
 }
 
 // ---------------------------------------------------------------------------
@@ -219,10 +220,10 @@ __device__ __forceinline__ const LayerInfo *wlayers(const WarpMem &M) {
 // what the sampler needs from the launch arguments (passed by value into the
 // out-of-line helpers so they read registers, not the param space)
 struct SampleArgs {
-    const BetaRec *recs;
-    const float2 *tables;
-    const float2 *hot;
-    const float *rec_mu;
+    const BetaRec *recs;            // by input record
+    TablePtr tables;                // by input record
+    const float *rec_mu;            // by input record
+    const SplitRec *srecs;          // per device record (.tab: its input record)
     const uint32_t *rec_orig;
     RunStatus *status;
     uint64_t seed;
@@ -266,7 +267,7 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
         if (SU) {
             BetaRec r[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) r[u] = G.recs[e[u].x];
+            for (int u = 0; u < U; ++u) r[u] = G.recs[__ldg(&G.srecs[e[u].x].tab)];
             float v[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -289,9 +290,7 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
                 const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
                 ti[u] = min((int)uu, kTabNodes - 2);
                 tt[u] = uu - (float)ti[u];
-                const bool in_hot = (unsigned)(ti[u] - kHotJ0) < (unsigned)(kHotN - 1);
-                const float2 *row = in_hot ? G.hot + (uint64_t)e[u].x * kHotN + (ti[u] - kHotJ0)
-                                           : G.tables + (uint64_t)e[u].x * kTabStride + ti[u];
+                const float2 *row = table_row(G.tables, __ldg(&G.srecs[e[u].x].tab), ti[u]);
                 if (r[u].mode == kModeTable) { n0[u] = __ldg(row); n1[u] = __ldg(row + 1); }
                 else { n0[u] = make_float2(0.f, 0.f); n1[u] = n0[u]; }
             }
@@ -317,7 +316,7 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
         } else {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                float x = __ldg(G.rec_mu + e[u].x);
+                float x = __ldg(G.rec_mu + __ldg(&G.srecs[e[u].x].tab));
                 const SlotInfo &si = slots[e[u].y & 0xffu];
                 if (si.has_terms) x = si.share * fminf(fmaxf(x - si.ret, 0.0f), si.lim);
                 if (live[u]) B.xs[p0 + 32 * u] = x;
@@ -360,75 +359,35 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
     return __any_sync(0xffffffffu, redo) ? 1 : 0;
 }
 
-template <int MW>
-__device__ __forceinline__ void load_index(const uint32_t *index, uint32_t stride, uint32_t e,
-                                           uint32_t &first, uint32_t (&mask)[MW]) {
-    const uint32_t *ix = index + (uint64_t)e * stride;
-    if (MW == 1) {
-        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(ix));
-        first = v.x; mask[0] = v.y;
-    } else {
-        const uint4 v0 = __ldg(reinterpret_cast<const uint4 *>(ix));
-        first = v0.x; mask[0] = v0.y;
-        if (MW > 1) mask[1] = v0.z;
-        if (MW > 2) mask[2] = v0.w;
-        if (MW > 3) {
-            const uint4 v1 = __ldg(reinterpret_cast<const uint4 *>(ix) + 1);
-            mask[3] = v1.x;
-            if (MW > 4) mask[4] = v1.y;
-            if (MW > 5) mask[5] = v1.z;
-            if (MW > 6) mask[6] = v1.w;
-        }
-    }
+// The present (occurrence, slot) pairs of one occurrence: the event's device
+// records first .. first + count - 1 (event-major, slot order); their slot
+// and layer from rec_meta.  count_occ: pairs and (occurrence, layer)
+// segments; write_occ: enqueue them.
+__device__ __forceinline__ void count_occ(const uint2 *mu_meta, uint32_t first, uint32_t count, uint32_t &np,
+                                          uint32_t &ns) {
+    np = count;
+    ns = 0;
+    for (uint32_t r = first; r < first + count; ++r) ns += (__ldg(&mu_meta[r].y) >> 8) & 1u;   // run ends
 }
 
-// Index lookups (Alg.1 line 6) for the warp's hits, 64 at a time (two per
-// lane in flight), then enqueue the present (occurrence, slot) pairs and their
-// (occurrence, layer) segments, whole occurrences at a time, flushing when the
-// queue would overflow.  Out of line.  q packs (qn, nseg, redo) as
-// qn | nseg << 12 | redo << 24 in and out.
-template <int MW>
-__device__ __forceinline__ void count_occ(const SlotInfo *slots, const uint32_t (&mask)[MW], uint32_t &np,
-                                         uint32_t &ns) {
-    np = 0; ns = 0;
-    uint32_t prev = 0xffffffffu;
-#pragma unroll
-    for (int w = 0; w < MW; ++w) {
-        uint32_t mw = mask[w];
-        np += __popc(mw);
-        while (mw) {
-            const uint32_t lay = slots[w * 32 + __ffs(mw) - 1].layer;
-            mw &= mw - 1;
-            ns += lay != prev;
+template <bool DBG>
+__device__ __forceinline__ void write_occ(const SampleArgs &G, const WarpMem &M, WarpBuf &B,
+                                          const SlotInfo *slots, const uint2 *mu_meta, uint32_t k,
+                                          uint32_t first, uint32_t count, uint32_t pos, uint32_t spos) {
+    uint32_t prev = 0xffffffffu, sstart = pos;
+    for (uint32_t rec = first; rec < first + count; ++rec) {
+        const uint32_t meta = __ldg(&mu_meta[rec].y);
+        const uint32_t slot = meta & 0xffu, lay = (meta >> 16) & 63u;
+        if (lay != prev) {
+            if (prev != 0xffffffffu) B.seg[spos++] = sstart | ((pos - sstart) << 16) | (prev << 24);
+            sstart = pos;
             prev = lay;
         }
-    }
-}
-
-template <int MW, bool DBG>
-__device__ __forceinline__ void write_occ(const SampleArgs &G, const WarpMem &M, WarpBuf &B,
-                                          const SlotInfo *slots, uint32_t k, uint32_t rec,
-                                          const uint32_t (&mask)[MW], uint32_t pos, uint32_t spos) {
-    uint32_t prev = 0xffffffffu, sstart = pos;
-#pragma unroll
-    for (int w = 0; w < MW; ++w) {
-        uint32_t mw = mask[w];
-        while (mw) {
-            const uint32_t slot = (uint32_t)(w * 32 + __ffs(mw) - 1);
-            mw &= mw - 1;
-            const uint32_t lay = slots[slot].layer;
-            if (lay != prev) {
-                if (prev != 0xffffffffu) B.seg[spos++] = sstart | ((pos - sstart) << 16) | (prev << 24);
-                sstart = pos;
-                prev = lay;
-            }
-            B.q[pos++] = make_uint2(rec, (k << 8) | slot);
-            if (DBG) {
-                atomicAdd(&wcnt(M)[lay], 1u);
-                const uint64_t hv = splitmix64(splitmix64(splitmix64((uint64_t)k) ^ slots[slot].elt) ^ G.rec_orig[rec]);
-                atomicAdd(&whsh(M)[lay], (unsigned long long)hv);
-            }
-            ++rec;
+        B.q[pos++] = make_uint2(rec, (k << 8) | slot);
+        if (DBG) {
+            atomicAdd(&wcnt(M)[lay], 1u);
+            const uint64_t hv = splitmix64(splitmix64(splitmix64((uint64_t)k) ^ slots[slot].elt) ^ G.rec_orig[rec]);
+            atomicAdd(&whsh(M)[lay], (unsigned long long)hv);
         }
     }
     if (prev != 0xffffffffu) B.seg[spos] = sstart | ((pos - sstart) << 16) | (prev << 24);
@@ -440,20 +399,21 @@ __device__ __forceinline__ void write_occ(const SampleArgs &G, const WarpMem &M,
 // (occurrence, layer) segment; if the queue would overflow it is flushed
 // first, and a chunk that alone exceeds the queue goes occurrence group by
 // group.  q packs (qn, nseg, redo) as qn | nseg << 12 | redo << 24.
-template <bool SU, bool EX, int MW, bool DBG>
+template <bool SU, bool EX, bool DBG>
 __device__ __forceinline__ int enqueue_chunk(const SampleArgs G, const WarpMem M, uint32_t trial_g, int lane,
                                           int q, uint32_t k0, uint32_t hitbits,
-                                          const uint4 first4, const uint32_t (&mask)[4][MW]) {
+                                          const uint4 first4, const uint4 count4, const uint2 *mu_meta) {
     WarpBuf &B = wbuf(M);
     const SlotInfo *slots = wslots(M);
     int qn = q & 0xfff, nseg = (q >> 12) & 0xfff, redo = q >> 24;
     const uint32_t first[4] = {first4.x, first4.y, first4.z, first4.w};
+    const uint32_t count[4] = {count4.x, count4.y, count4.z, count4.w};
     uint32_t np[4], ns[4];
     uint32_t mine = 0;
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
         np[h] = 0; ns[h] = 0;
-        if ((hitbits >> h) & 1u) count_occ<MW>(slots, mask[h], np[h], ns[h]);
+        if ((hitbits >> h) & 1u) count_occ(mu_meta, first[h], count[h], np[h], ns[h]);
         mine += np[h] | (ns[h] << 16);
     }
     uint32_t incl = mine;
@@ -472,7 +432,7 @@ __device__ __forceinline__ int enqueue_chunk(const SampleArgs G, const WarpMem M
         uint32_t pos = (uint32_t)qn + (ex & 0xffffu), spos = (uint32_t)nseg + (ex >> 16);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-            if (np[h]) write_occ<MW, DBG>(G, M, B, slots, k0 + h, first[h], mask[h], pos, spos);
+            if (np[h]) write_occ<DBG>(G, M, B, slots, mu_meta, k0 + h, first[h], count[h], pos, spos);
             pos += np[h];
             spos += ns[h];
         }
@@ -496,8 +456,8 @@ __device__ __forceinline__ int enqueue_chunk(const SampleArgs G, const WarpMem M
             const bool fits = todo && (inc2 & 0xffffu) <= (uint32_t)(kQCap - qn);
             if (fits) {
                 const uint32_t ex = inc2 - m2;
-                write_occ<MW, DBG>(G, M, B, slots, k0 + h, first[h], mask[h], (uint32_t)qn + (ex & 0xffffu),
-                                   (uint32_t)nseg + (ex >> 16));
+                write_occ<DBG>(G, M, B, slots, mu_meta, k0 + h, first[h], count[h], (uint32_t)qn + (ex & 0xffffu),
+                               (uint32_t)nseg + (ex >> 16));
                 todo = false;
             }
             const unsigned fitmask = __ballot_sync(0xffffffffu, fits);
@@ -517,7 +477,7 @@ __device__ __forceinline__ int enqueue_chunk(const SampleArgs G, const WarpMem M
     return qn | (nseg << 12) | (redo << 24);
 }
 
-template <bool SU, bool EX, int MW, bool DBG>
+template <bool SU, bool EX, bool DBG>
 __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_constant__ ScanArgs A) {
     const uint32_t nl = A.pf.n_layers;
     const uint32_t per_warp = (uint32_t)((sizeof(WarpBuf) + nl * (sizeof(double) + sizeof(unsigned long long) +
@@ -550,15 +510,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
     unsigned int *cntv = wcnt(M);
     unsigned int *omv = wom(M);
     const bool dbg = DBG;
-    SampleArgs G{A.pf.recs, A.pf.tables, A.pf.hot, A.pf.rec_mu, A.pf.rec_orig, A.status, A.seed,
+    SampleArgs G{A.pf.recs, A.pf.tables, A.pf.rec_mu, A.pf.srecs, A.pf.rec_orig, A.status, A.seed,
                  (A.flags & ARA_EXACT) != 0,
                  (A.flags & ARA_RNG_SUPPLIED) ? 3u : (A.flags & ARA_RNG_RECORD) ? 1u : (A.flags & ARA_RNG_OCCURRENCE) ? 2u : 0u,
                  A.zp_sup, A.zp_stride, A.ze_sup, 0};
     const uint64_t n_trials = A.yet.n_trials;
     const uint64_t n_work = A.trial_list ? A.n_list : n_trials;
     const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift;
-    const uint32_t *index = A.pf.index;
-    const uint32_t stride = A.pf.idx_stride;
+    const uint2 *cidx = A.pf.cidx;
+    const uint2 *mu_meta = A.pf.mu_meta;
     const unsigned lanemask_lt = (1u << lane) - 1u;
 
     while (true) {
@@ -590,20 +550,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
         // software pipeline over 128-event chunks: events of chunk c+2 in flight
         // (HBM), index entries of chunk c+1 in flight (L2), pairs of chunk c enqueued
         uint32_t hit_c = 0, k0_c = 0;
-        uint4 first_c = make_uint4(0, 0, 0, 0);
-        uint32_t mask_c[4][MW];
-#pragma unroll
-        for (int qd = 0; qd < 4; ++qd)
-#pragma unroll
-            for (int w = 0; w < MW; ++w) mask_c[qd][w] = 0u;
+        uint4 first_c = make_uint4(0, 0, 0, 0), count_c = make_uint4(0, 0, 0, 0);
         for (uint32_t c = 0; c < len + 128; c += 128) {             // Alg.1 line 4
             uint32_t hit_n = 0, k0_n = c + 4u * lane;
-            uint4 first_n = make_uint4(0, 0, 0, 0);
-            uint32_t mask_n[4][MW];
-#pragma unroll
-            for (int qd = 0; qd < 4; ++qd)
-#pragma unroll
-                for (int w = 0; w < MW; ++w) mask_n[qd][w] = 0u;
+            uint4 first_n = make_uint4(0, 0, 0, 0), count_n = make_uint4(0, 0, 0, 0);
             if (c < len) {
                 const uint4 cur = nxt;
                 {   // prefetch the next chunk's events
@@ -634,18 +584,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
                 // index entries of this lane's hits: issued now, consumed next iteration
 #pragma unroll
                 for (int qd = 0; qd < 4; ++qd) {
-                    uint32_t f = 0;
-                    if ((hit_n >> qd) & 1u) load_index<MW>(index, stride, ee[qd], f, mask_n[qd]);
-                    if (qd == 0) first_n.x = f; else if (qd == 1) first_n.y = f; else if (qd == 2) first_n.z = f; else first_n.w = f;
+                    uint2 ci = make_uint2(0u, 0u);
+                    if ((hit_n >> qd) & 1u) ci = __ldg(cidx + ee[qd]);       // (first record, count)
+                    if (qd == 0) { first_n.x = ci.x; count_n.x = ci.y; }
+                    else if (qd == 1) { first_n.y = ci.x; count_n.y = ci.y; }
+                    else if (qd == 2) { first_n.z = ci.x; count_n.z = ci.y; }
+                    else { first_n.w = ci.x; count_n.w = ci.y; }
                 }
             }
             if (__any_sync(0xffffffffu, hit_c != 0))
-                q = enqueue_chunk<SU, EX, MW, DBG>(G, M, trial_g, lane, q, k0_c, hit_c, first_c, mask_c);
-            hit_c = hit_n; k0_c = k0_n; first_c = first_n;
-#pragma unroll
-            for (int qd = 0; qd < 4; ++qd)
-#pragma unroll
-                for (int w = 0; w < MW; ++w) mask_c[qd][w] = mask_n[qd][w];
+                q = enqueue_chunk<SU, EX, DBG>(G, M, trial_g, lane, q, k0_c, hit_c, first_c, count_c, mu_meta);
+            hit_c = hit_n; k0_c = k0_n; first_c = first_n; count_c = count_n;
         }
         __syncwarp();
         int redo = q >> 24;
@@ -675,27 +624,16 @@ static size_t scan_smem_bytes(const PortfolioDev &pf) {
            ((size_t)pf.bitmap_words * 4 + 15) / 16 * 16 + kWarps * per_warp;
 }
 
-template <bool SU, bool EX, int MW>
+template <bool SU, bool EX>
 static cudaError_t launch_scan_t(const ScanArgs &A, cudaStream_t s, int num_sms) {
     const size_t smem = scan_smem_bytes(A.pf);
-    auto kern = (A.flags & ARA_DEBUG_LOOKUP) ? scan_kernel<SU, EX, MW, true> : scan_kernel<SU, EX, MW, false>;
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
+    auto kern = (A.flags & ARA_DEBUG_LOOKUP) ? scan_kernel<SU, EX, true> : scan_kernel<SU, EX, false>;
     int per_sm = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+    cudaError_t err = prepare_launch((const void *)kern, smem, kWarps * 32, per_sm);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     kern<<<num_sms * per_sm, kWarps * 32, smem, s>>>(A);
     return cudaGetLastError();
-}
-
-template <int MW>
-static cudaError_t launch_scan_mw(const ScanArgs &A, bool exact_kernel, cudaStream_t s, int num_sms) {
-    if (!(A.flags & ARA_SU)) return launch_scan_t<false, false, MW>(A, s, num_sms);
-    // the fp64 per-sample solve lives in a separate kernel (its register demand
-    // would otherwise throttle the table path)
-    if (exact_kernel) return launch_scan_t<true, true, MW>(A, s, num_sms);
-    return launch_scan_t<true, false, MW>(A, s, num_sms);
 }
 
 cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed, uint32_t flags,
@@ -706,16 +644,17 @@ cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed
     ScanArgs A{pf, yet, seed, flags, ylt, dbg_count, dbg_hash, status, trial_list, n_list, redo, occ_max,
                zp_sup, zp_stride, ze_sup};
     if (trial_list && n_list == 0) return cudaSuccess;
-    if (pf.mask_words == 1) return launch_scan_mw<1>(A, exact_kernel, s, num_sms);
-    if (pf.mask_words <= 3) return launch_scan_mw<3>(A, exact_kernel, s, num_sms);
-    if (pf.mask_words == 4) return launch_scan_mw<4>(A, exact_kernel, s, num_sms);
-    return launch_scan_mw<7>(A, exact_kernel, s, num_sms);
+    if (!(flags & ARA_SU)) return launch_scan_t<false, false>(A, s, num_sms);
+    // the fp64 per-sample solve lives in a separate instantiation (its register
+    // demand would otherwise throttle the table path)
+    if (exact_kernel) return launch_scan_t<true, true>(A, s, num_sms);
+    return launch_scan_t<true, false>(A, s, num_sms);
 }
 
 // ---------------------------------------------------------------------------
 // Component kernels (row-level parity tests)
 // ---------------------------------------------------------------------------
-__global__ void sample_losses_kernel(const BetaRec *recs, const float2 *tables, const float2 *hot,
+__global__ void sample_losses_kernel(const BetaRec *recs, TablePtr tables,
                                      const float *zp,
                                      const float *ze, uint64_t n, bool exact, float *out,
                                      RunStatus *status) {
@@ -724,19 +663,19 @@ __global__ void sample_losses_kernel(const BetaRec *recs, const float2 *tables, 
         const BetaRec r = recs[t];
         const float v = combine_v(r, norm_quantile_f(zp[t]), norm_quantile_f(ze[t]));
         bool ok;
-        out[t] = sample_loss_from_v<true>(r, tables, hot, t, v, exact, ok);
+        out[t] = sample_loss_from_v<true>(r, tables, t, v, exact, ok);
         if (!ok) atomicAdd(&status->nonconverged, 1u);
     }
 }
 
-cudaError_t launch_sample_losses(const BetaRec *recs, const float2 *tables, const float2 *hot,
+cudaError_t launch_sample_losses(const BetaRec *recs, TablePtr tables,
                                  const float *zp,
                                  const float *ze, uint64_t n, bool exact, float *out,
                                  RunStatus *status, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const uint64_t blocks = (n + 255) / 256;
     sample_losses_kernel<<<(unsigned)(blocks < 1u << 20 ? blocks : 1u << 20), 256, 0, s>>>(
-        recs, tables, hot, zp, ze, n, exact, out, status);
+        recs, tables, zp, ze, n, exact, out, status);
     return cudaGetLastError();
 }
 

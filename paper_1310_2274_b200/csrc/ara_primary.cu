@@ -38,8 +38,8 @@ __device__ __forceinline__ double clip64(double d, double lim) {   // min(max(d,
 // (= layer, then XELT) order, so each layer's sum runs in the layer's XELT
 // order, as Algorithm 1's line 5 loop does.
 // ---------------------------------------------------------------------------
-__global__ void occ_table_kernel(const uint2 *__restrict__ cidx, const uint32_t *__restrict__ rec_meta,
-                                 const float *__restrict__ rec_mu, const double *__restrict__ slot_terms,
+__global__ void occ_table_kernel(const uint2 *__restrict__ cidx, const uint2 *__restrict__ mu_meta,
+                                 const double *__restrict__ slot_terms,
                                  const LayerInfo *__restrict__ layers, uint32_t n_layers, uint32_t lp,
                                  uint32_t catalog, float *__restrict__ out) {
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < catalog;
@@ -50,9 +50,9 @@ __global__ void occ_table_kernel(const uint2 *__restrict__ cidx, const uint32_t 
         for (uint32_t l = 0; l < lp; ++l) {
             double sum = 0.0;
             bool any = false;
-            while (r < r1 && ((rec_meta[r] >> 16) & 63u) == l) {    // layer l's records of e
-                const uint32_t slot = rec_meta[r] & 0xffu;
-                double x = (double)rec_mu[r];                       // the loss (G10 / SU off)
+            while (r < r1 && ((mu_meta[r].y >> 16) & 63u) == l) {   // layer l's records of e
+                const uint32_t slot = mu_meta[r].y & 0xffu;
+                double x = (double)__uint_as_float(mu_meta[r].x);   // the loss (G10 / SU off)
                 const double *T = slot_terms + 4 * slot;            // XELT terms (line 8, G7)
                 if (T[3] != 0.0) x = T[2] * clip64(x - T[0], T[1]);
                 sum += x;                                           // line 9
@@ -66,13 +66,13 @@ __global__ void occ_table_kernel(const uint2 *__restrict__ cidx, const uint32_t 
     }
 }
 
-void launch_occ_table(const uint2 *cidx, const uint32_t *rec_meta, const float *rec_mu, const double *slot_terms,
+void launch_occ_table(const uint2 *cidx, const uint2 *mu_meta, const double *slot_terms,
                       const LayerInfo *layers, uint32_t n_layers, uint32_t lp, uint32_t catalog, float *out,
                       cudaStream_t s) {
     if (catalog == 0) return;
     const uint64_t blocks = (catalog + 255) / 256;
     occ_table_kernel<<<(unsigned)(blocks < 65535u * 16u ? blocks : 65535u * 16u), 256, 0, s>>>(
-        cidx, rec_meta, rec_mu, slot_terms, layers, n_layers, lp, catalog, out);
+        cidx, mu_meta, slot_terms, layers, n_layers, lp, catalog, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -8,7 +8,7 @@
 //              fp32, Phi^-1 taken on the smaller tail (exact for U's grid)
 //   steps 5+ : x = I^-1(Phi(v); a, b) (G11).  The map
 //              v -> lambda(v) = logit x(v) is smooth, so each record carries
-//              a table of (lambda, dlambda/dv) at v = -8, -7.5, ..., 8, built
+//              a table of (lambda, dlambda/dv) at v = -7.75, -7.25, ..., 7.75, built
 //              ONCE at ara_create_portfolio by an fp64 solve (below) and
 //              evaluated per sample by quintic Hermite interpolation, the
 //              second derivative coming from the ODE
@@ -265,15 +265,12 @@ __device__ __forceinline__ float quintic_from_nodes(float2 n0, float2 n1, int i,
     return lam;
 }
 
-// quintic Hermite in v on record `rec`'s table (hot rows for the centre)
-__device__ __forceinline__ float lambda_table(const float2 *__restrict__ tables,
-                                              const float2 *__restrict__ hot, uint64_t rec,
-                                              float a, float b, float v) {
+// quintic Hermite in v on record `rec`'s table
+__device__ __forceinline__ float lambda_table(const TablePtr &tables, uint64_t rec, float a, float b, float v) {
     const float u = (fminf(fmaxf(v, kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
     const int i = min((int)u, kTabNodes - 2);
     const float t = u - (float)i;
-    const bool in_hot = (unsigned)(i - kHotJ0) < (unsigned)(kHotN - 1);
-    const float2 *row = in_hot ? hot + rec * kHotN + (i - kHotJ0) : tables + rec * kTabStride + i;
+    const float2 *row = table_row(tables, rec, i);
     return quintic_from_nodes(__ldg(row), __ldg(row + 1), i, t, a, b);
 }
 
@@ -298,13 +295,12 @@ static __device__ __noinline__ float sample_exact64(float af, float bf, float mu
 // One loss draw (Alg.1 line 7) given v.  EX instantiates the fp64 fallback;
 // kernels without it are only launched when every record has a table.
 template <bool EX>
-__device__ __forceinline__ float sample_loss_from_v(const BetaRec &r, const float2 *__restrict__ tables,
-                                                    const float2 *__restrict__ hot, uint64_t rec, float v,
-                                                    bool exact, bool &ok) {
+__device__ __forceinline__ float sample_loss_from_v(const BetaRec &r, const TablePtr &tables,
+                                                    uint64_t rec, float v, bool exact, bool &ok) {
     ok = true;
     if (r.mode == kModeDegenerate) return r.scale;               // G10
     if (!EX || (r.mode == kModeTable && !exact)) {
-        const float lam = lambda_table(tables, hot, rec, r.a, r.b, v);
+        const float lam = lambda_table(tables, rec, r.a, r.b, v);
         return r.scale * sigmoidf_(lam);
     }
     return sample_exact64(r.a, r.b, r.mu_l, r.sd_l, r.scale, v, ok);

@@ -401,8 +401,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     unsigned int *dc = W.dc;
     unsigned long long *dhs = W.dhs;
     const SplitRec *__restrict__ srecs = A.pf.srecs;
-    const float2 *__restrict__ hot = A.pf.hot;
-    const float2 *__restrict__ tables = A.pf.tables;
+    const TablePtr tables = A.pf.tables;
     const uint32_t kb = A.kbits, kmask = (1u << kb) - 1u;
     auto ldpair = [&](const uint2 *q) -> uint2 {    // {device record, k}
         if (PK) {                                     // packed: record << kbits | k
@@ -454,15 +453,16 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 float v[kU];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
+                    const uint2 key = make_uint2(r[u].key & 0xffffffu, r[u].key >> 24);   // draw keys (XELT, program)
                     if (RS == 2) {                        // supplied with the inputs
-                        const float zp = __ldg(A.zp_sup + (uint64_t)r[u].prog * A.zp_stride + occ_base + e[u].y);
+                        const float zp = __ldg(A.zp_sup + (uint64_t)key.y * A.zp_stride + occ_base + e[u].y);
                         const float ze = __ldg(A.ze_sup + e[u].x);
                         v[u] = fmaf(r[u].wi, norm_quantile_f(zp), r[u].wc * norm_quantile_f(ze));
                     } else {
-                        const uint32_t bp = philox_lane0_k(trial_g, e[u].y, r[u].prog, 1u, A.pkey);   // z_(Prog,E)
+                        const uint32_t bp = philox_lane0_k(trial_g, e[u].y, key.y, 1u, A.pkey);       // z_(Prog,E)
                         const uint32_t be =                                                           // z_(E)
-                            RS == 1 ? philox_lane0_k(__ldg(A.pf.rec_orig + e[u].x), r[u].elt, 0u, 6u, A.pkey)  // (A)
-                                    : philox_lane0_k(trial_g, e[u].y, r[u].elt & A.ze_mask, A.ze_tag, A.pkey); // G2, (B)
+                            RS == 1 ? philox_lane0_k(__ldg(A.pf.rec_orig + e[u].x), key.x, 0u, 6u, A.pkey)  // (A)
+                                    : philox_lane0_k(trial_g, e[u].y, key.x & A.ze_mask, A.ze_tag, A.pkey); // G2, (B)
                         v[u] = fmaf(r[u].wi, norm_quantile_from_bits(bp), r[u].wc * norm_quantile_from_bits(be));
                     }
                 }
@@ -473,9 +473,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                         const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
                         const int ti = min((int)uu, kTabNodes - 2);
                         const float tt = uu - (float)ti;
-                        const bool in_hot = (unsigned)(ti - kHotJ0) < (unsigned)(kHotN - 1);
-                        const float2 *row = in_hot ? hot + (uint64_t)e[u].x * kHotN + (ti - kHotJ0)
-                                                   : tables + (uint64_t)e[u].x * kTabStride + ti;
+                        const float2 *row = table_row(tables, r[u].tab, ti);
                         x[u] = r[u].scale * sigmoidf_(quintic_from_nodes(__ldg(row), __ldg(row + 1), ti, tt,
                                                                          r[u].a, r[u].b));
                     } else if (mode == kModeDegenerate) {
@@ -652,24 +650,27 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 32 / kSampleWarps)   // <= 
     }
 }
 
-__global__ void split_recs_kernel(const BetaRec *__restrict__ recs, const uint32_t *__restrict__ rec_meta,
-                                  const SlotInfo *__restrict__ slots, const float *__restrict__ mu, uint64_t n,
-                                  SplitRec *__restrict__ out, uint2 *__restrict__ mu_meta) {
+__global__ void split_recs_kernel(const BetaRec *__restrict__ recs, const uint32_t *__restrict__ rec_src,
+                                  const uint32_t *__restrict__ rec_meta, const SlotInfo *__restrict__ slots,
+                                  const float *__restrict__ mu, uint64_t n, SplitRec *__restrict__ out,
+                                  uint2 *__restrict__ mu_meta) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
-        const BetaRec r = recs[t];
+        const uint32_t src = rec_src[t];
+        const BetaRec r = recs[src];
         const uint32_t m = rec_meta[t];
         const SlotInfo &s = slots[m & 0xffu];
-        out[t] = SplitRec{r.a, r.b, r.wi, r.wc, r.scale, m | (r.mode << 28), s.elt, s.prog};
-        mu_meta[t] = make_uint2(__float_as_uint(mu[t]), m);
+        out[t] = SplitRec{r.a, r.b, r.wi, r.wc, r.scale, m | (r.mode << 28), src, s.elt | (s.prog << 24)};
+        mu_meta[t] = make_uint2(__float_as_uint(mu[src]), m);
     }
 }
 
-void launch_split_recs(const BetaRec *recs, const uint32_t *rec_meta, const SlotInfo *slots, const float *mu,
-                       uint64_t n, SplitRec *out, uint2 *mu_meta, cudaStream_t s) {
+void launch_split_recs(const BetaRec *recs, const uint32_t *rec_src, const uint32_t *rec_meta,
+                       const SlotInfo *slots, const float *mu, uint64_t n, SplitRec *out, uint2 *mu_meta,
+                       cudaStream_t s) {
     if (n == 0) return;
     const uint64_t blocks = (n + 255) / 256;
     split_recs_kernel<<<(unsigned)(blocks < 65535u * 16u ? blocks : 65535u * 16u), 256, 0, s>>>(
-        recs, rec_meta, slots, mu, n, out, mu_meta);
+        recs, rec_src, rec_meta, slots, mu, n, out, mu_meta);
 }
 
 // Packed YET upload (ara_yet_refill_packed): ids bit-packed LSB-first, `bits`

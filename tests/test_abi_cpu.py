@@ -80,6 +80,7 @@ def test_validate_ok(ara):
     (lambda p: p.__setitem__("layer_elt_off", np.array([0, 0, 4], np.uint64)), "EINVAL", "covers no XELT"),
     (lambda p: p.__setitem__("catalog_size", 0), "EINVAL", "catalog_size"),
     (lambda p: p.__setitem__("elt_terms", np.array([[0, 1e5, 1.5]] * 4)), "EINVAL", "share"),
+    (lambda p: p["layer_prog"].__setitem__(1, 256), "EINVAL", "program 256"),
 ])
 def test_validate_rejects(ara, mutate, code, needle):
     pf = base_pf()

@@ -35,6 +35,9 @@ KEYS = [
     "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
     "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum",
+    "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_st.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -89,11 +92,11 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     for kern in read_raw(a.rep):
         name = kern.get("Kernel Name", ("?", ""))[0]
-        m = re.search(r"(compact_kernel|sample_kernel|scan_kernel)", name)
+        m = re.search(r"(compact_kernel|sample_kernel|scan_kernel|primary_kernel)", name)
         if not m:
             continue
         short = m.group(1)
-        units = a.occurrences if short == "compact_kernel" else a.pairs
+        units = a.occurrences if short in ("compact_kernel", "primary_kernel") else a.pairs
         out = summarise(kern, units)
         out["source"] = os.path.basename(a.rep)
         with open(os.path.join(ROOT, "profiles", f"{a.tag}_{short}.json"), "w") as f:
@@ -101,7 +104,7 @@ def main():
         d = out["derived"]
         print(json.dumps({short: d}, indent=1))
         if a.write_const:
-            key = "occurrence" if short == "compact_kernel" else "pair"
+            key = "occurrence" if short in ("compact_kernel", "primary_kernel") else "pair"
             mm = out["metrics"]
             pick = lambda k: float(mm[k]["value"]) if k in mm else None
             consts[short] = {f"thread_inst_per_{key}": d["thread_inst_per_unit"],

@@ -269,7 +269,7 @@ def run_ours(args, cfg, rank, world, local):
     padded = torch.zeros((L, nmax), dtype=torch.float32, device=dev) if world > 1 else None
     layers = list(range(L)) + ([-1] if L > 1 else [])
     ylt_host = torch.empty((L, n_loc), dtype=torch.float32).pin_memory()
-    ara.prepare(ctx, P, Y, su=cfg["su"])        # every ara_run scratch buffer, allocated once here
+    ara.prepare(ctx, P, Y, su=cfg["su"], async_=True)   # every ara_run scratch buffer, allocated once here
 
     kern_ms = []          # per-kernel CUDA-event sums of each timed ara_run (ara_last_run_timings)
     meas_ev = []          # CUDA events around each timed step's all-gather + measures
@@ -281,9 +281,11 @@ def run_ours(args, cfg, rank, world, local):
         return [ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=n_shards) for layer in layers]
 
     def step(Yx, timed=False):
-        ara.run(ctx, P, Yx, seed=cfg["seed"], su=cfg["su"], ylt=ylt)
+        # ara_run with ARA_ASYNC: no host synchronisation inside the run; the
+        # measures' read-back is the step's one synchronisation (errors latched
+        # by the runs are checked by ctx.synchronize() after the loop)
+        ara.run(ctx, P, Yx, seed=cfg["seed"], su=cfg["su"], ylt=ylt, async_=True)
         if timed:
-            kern_ms.append(ara.last_run_timings(ctx))
             m0 = torch.cuda.Event(enable_timing=True); m1 = torch.cuda.Event(enable_timing=True)
             m0.record(stream)
         src, n_shards = gather_ylt(ylt, world, N_total, gathered, padded)
@@ -291,6 +293,7 @@ def run_ours(args, cfg, rank, world, local):
         if timed:
             m1.record(stream)
             meas_ev.append((m0, m1))
+            kern_ms.append(ara.last_run_timings(ctx))    # (the run is complete: no wait)
         return out
 
     # exact number of present (occurrence, slot) pairs = SU samples per launch
@@ -314,6 +317,7 @@ def run_ours(args, cfg, rank, world, local):
             dist.barrier()
         torch.cuda.synchronize()
     elapsed = t0.elapsed_time(t1) / 1e3
+    ctx.synchronize()                                    # errors latched by the ARA_ASYNC runs, if any
     if world > 1:
         t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -329,7 +333,7 @@ def run_ours(args, cfg, rank, world, local):
     copy_stream = torch.cuda.Stream(dev)
     ctx_copy = ara.Context(local, copy_stream)
     Ys = [Y, ara.Yet(ctx, ev_host, fixed_len=K, first_trial=lo, n_trials=n_loc)]
-    ara.prepare(ctx, P, Ys[1], su=cfg["su"])
+    ara.prepare(ctx, P, Ys[1], su=cfg["su"], async_=True)
 
     def e2e(bits):
         if bits < 32:
@@ -363,6 +367,7 @@ def run_ours(args, cfg, rank, world, local):
             ylt_host.copy_(ylt, non_blocking=True)  # D2H of the step's result
         te1.record(stream)
         torch.cuda.synchronize()
+        ctx.synchronize()
         el = te0.elapsed_time(te1) / 1e3
         if world > 1:
             t = torch.tensor([el], device=dev, dtype=torch.float64)

@@ -64,6 +64,15 @@ extern "C" {
                                 (trial, occurrence, 0, 7).  Default (neither
                                 flag): reading G2, counter (trial,
                                 occurrence, XELT id, 2)                     */
+#define ARA_ASYNC 256u       /* ara_run / ara_run_ep return as soon as the run is
+                                enqueued: no host synchronisation; overflowing
+                                trials and table-less records are handled by
+                                device-sized passes (the overflow pool is
+                                pre-sized by ara_prepare / the first run); range
+                                errors, non-convergence and an exhausted pool
+                                are latched and reported by the next
+                                ara_ctx_synchronize.  ara_last_run_timings
+                                waits for the run.                            */
 #define ARA_RNG_SUPPLIED 128u /* the paper's data model: z_(Prog,E)
                                 of each YET occurrence and z_(E) of each XELT
                                 record are inputs, supplied by ara_yet_set_z
@@ -128,7 +137,11 @@ int ara_version(void);
  * ARA_ECUDA if the device is unavailable. */
 int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out);
 void ara_ctx_destroy(ara_ctx *ctx);
-/* Block until all work enqueued by this context has finished. */
+/* Block until all work enqueued by this context has finished; then report
+ * (and clear) the errors latched by ARA_ASYNC runs since the last call:
+ * ARA_ERANGE (event ids >= catalog_size), ARA_ECONVERGE, ARA_ENOMEM (trials
+ * that overflowed their pair regions and did not fit the overflow pool:
+ * their YLT entries were not written -- rerun without ARA_ASYNC). */
 int ara_ctx_synchronize(ara_ctx *ctx);
 
 /* Host-only validation of a portfolio (no device needed); same arguments
@@ -255,8 +268,8 @@ int ara_run_ep(ara_ctx *ctx, const ara_portfolio *pf, const ara_yet *yet, uint64
 
 /* Optional: allocate every scratch buffer ara_run needs for this
  * (portfolio, YET) pair with these flags, so that ara_run itself allocates
- * nothing (the pair slots of the two-stream pipeline: 2 x batch x region
- * pairs; the per-trial pair counts).  Without it ara_run grows the same
+ * nothing (the pair slot: batch x region pairs; the per-trial pair counts;
+ * with ARA_ASYNC the pre-sized overflow pool).  Without it ara_run grows the same
  * buffers on first use.  A run whose trials overflow their regions still
  * grows the overflow pool (exactly sized) when that happens.
  * Errors: ARA_EINVAL, ARA_ECUDA / ARA_ENOMEM-like allocation failures as ARA_ECUDA. */

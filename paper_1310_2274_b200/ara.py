@@ -267,8 +267,11 @@ class Yet:
 RNG_FLAGS = {"g2": 0, "record": 32, "occurrence": 64, "supplied": 128}   # ARA_RNG_RECORD / _OCCURRENCE / _SUPPLIED
 
 
+ASYNC = 256
+
+
 def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug: bool = False,
-        ylt=None, exact: bool = False, wide_pairs: bool = False, rng: str = "g2"):
+        ylt=None, exact: bool = False, wide_pairs: bool = False, rng: str = "g2", async_: bool = False):
     """ara_run; returns the device YLT [n_layers, n_trials] (and count/hash if debug).
     rng: "g2" (z_E per trial, occurrence, XELT), "record" (paper-literal z_E per
     XELT record), "occurrence" (z_E per occurrence shared by the XELTs)."""
@@ -281,7 +284,7 @@ def run(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, debug
         cnt = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int32, device=dev)
         hsh = torch.zeros((pf.n_layers, yet.n_trials), dtype=torch.int64, device=dev)
     flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (EXACT if exact else 0) | \
-        (WIDE_PAIRS if wide_pairs else 0) | RNG_FLAGS[rng]
+        (WIDE_PAIRS if wide_pairs else 0) | RNG_FLAGS[rng] | (ASYNC if async_ else 0)
     _check(lib.ara_run(ctx.h, pf.h, yet.h, int(seed) & 0xFFFFFFFFFFFFFFFF, flags, _p(ylt), _p(cnt),
                        _p(hsh)))
     return (ylt, cnt, hsh) if debug else ylt
@@ -310,9 +313,10 @@ def run_ep(ctx: Context, pf: Portfolio, yet: Yet, seed: int, su: bool = True, de
 
 
 def prepare(ctx: Context, pf: Portfolio, yet: Yet, su: bool = True, debug: bool = False,
-            wide_pairs: bool = False):
+            wide_pairs: bool = False, async_: bool = False):
     """ara_prepare: allocate ara_run's scratch for (pf, yet) up front."""
-    flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (WIDE_PAIRS if wide_pairs else 0)
+    flags = (SU if su else 0) | (DEBUG_LOOKUP if debug else 0) | (WIDE_PAIRS if wide_pairs else 0) | \
+        (ASYNC if async_ else 0)
     _check(lib.ara_prepare(ctx.h, pf.h, yet.h, flags))
 
 

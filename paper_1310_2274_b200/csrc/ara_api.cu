@@ -110,7 +110,55 @@ struct ara_ctx {
     cudaEvent_t tev[4 * kMaxBatches] = {};                      // per-batch kernel timings
     double last_ms[3] = {0.0, 0.0, 0.0};                        // compact, sample, redo
     uint32_t last_launches = 0, last_batches = 0;               // kernels launched by the last ara_run
+    // ARA_ASYNC: errors latched on the device until ara_ctx_synchronize, the
+    // last run's timings computed when asked for
+    bool async_pending = false;
+    unsigned int latched_bad = 0, latched_nonconv = 0, latched_short = 0;
+    bool timing_pending = false, timing_tail = false;
+    uint32_t timing_batches = 0;
 };
+
+// fold the error counters latched by ARA_ASYNC runs into the host latch and
+// clear them on the device (synchronises the context stream)
+static cudaError_t fold_latched(ara_ctx *c) {
+    if (!c->async_pending) return cudaSuccess;
+    cudaError_t e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return e;
+    c->latched_bad += c->h_status->bad_event;
+    c->latched_nonconv += c->h_status->nonconverged;
+    c->latched_short += c->h_status->pool_short;
+    c->async_pending = false;
+    return cudaMemsetAsync(reinterpret_cast<unsigned char *>(c->d_status) + kRunCounters, 0,
+                           sizeof(RunStatus) - kRunCounters, c->stream);
+}
+
+// device times of the last run's kernels (waits for its last event)
+static cudaError_t compute_timings(ara_ctx *c) {
+    if (!c->timing_pending) return cudaSuccess;
+    cudaError_t e = cudaEventSynchronize(c->timing_tail ? c->ev[3] : c->ev[1]);
+    if (e != cudaSuccess) return e;
+    double a = 0.0, b = 0.0, r = 0.0;
+    for (uint32_t q = 0; q < c->timing_batches; ++q) {
+        float x = 0, z = 0;
+        if ((e = cudaEventElapsedTime(&x, c->tev[4 * q], c->tev[4 * q + 1])) != cudaSuccess) return e;
+        if ((e = cudaEventElapsedTime(&z, c->tev[4 * q + 2], c->tev[4 * q + 3])) != cudaSuccess) return e;
+        a += x; b += z;
+    }
+    if (!c->timing_batches) {
+        float x = 0;
+        if ((e = cudaEventElapsedTime(&x, c->ev[0], c->ev[1])) != cudaSuccess) return e;
+        b = x;
+    }
+    if (c->timing_tail) {
+        float x = 0;
+        if ((e = cudaEventElapsedTime(&x, c->ev[2], c->ev[3])) != cudaSuccess) return e;
+        r = x;
+    }
+    c->last_ms[0] = a; c->last_ms[1] = b; c->last_ms[2] = r;
+    c->timing_pending = false;
+    return cudaSuccess;
+}
 
 // Per input XELT record, shared by every (layer, XELT) slot and every
 // kernel group that covers the record's XELT: the beta parameters, the mean
@@ -259,6 +307,15 @@ int ara_ctx_synchronize(ara_ctx *c) {
     if (!c) return fail(ARA_EINVAL, "ctx is NULL");
     CU(cudaSetDevice(c->device));
     CU(cudaStreamSynchronize(c->stream));
+    CU(fold_latched(c));
+    CU(cudaStreamSynchronize(c->stream));
+    const unsigned int bad = c->latched_bad, nc = c->latched_nonconv, sh = c->latched_short;
+    c->latched_bad = c->latched_nonconv = c->latched_short = 0;
+    if (bad) return fail(ARA_ERANGE, "an ARA_ASYNC run met event ids >= catalog_size (its YLT is not written)");
+    if (sh)
+        return fail(ARA_ENOMEM, "%u overflowing trials of ARA_ASYNC runs did not fit the overflow pool (their YLT "
+                                "entries are not written): rerun without ARA_ASYNC", sh);
+    if (nc) return fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples (ARA_ASYNC runs)", nc);
     return ARA_OK;
 }
 
@@ -853,6 +910,13 @@ static SplitPlan plan_split(const ara_portfolio *p, const ara_yet *y, uint32_t f
     return pl;
 }
 
+// ARA_ASYNC's pre-sized overflow pool: an eighth of the pair slot, at least
+// 2^24 pairs (the synchronous path sizes the pool exactly instead)
+static uint64_t default_pool_pairs(const SplitPlan &pl, uint64_t n_trials) {
+    const uint64_t d = std::max<uint64_t>(1ull << 24, (uint64_t)pl.cap * std::min<uint64_t>(pl.batch, n_trials) / 8);
+    return env_u64("ARA_ASYNC_POOL_PAIRS", d);       // (test aid: a small pool)
+}
+
 static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
                     float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash);
 
@@ -886,6 +950,7 @@ static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64
                                  occ_max ? occ_max + off : nullptr, dbg_count ? dbg_count + off : nullptr,
                                  dbg_hash ? dbg_hash + off : nullptr);
         if (st != ARA_OK) return st;
+        CU(compute_timings(c));          // (an ARA_ASYNC run of a grouped portfolio waits for each group here)
         for (int k = 0; k < 3; ++k) ms[k] += c->last_ms[k];
         launches += c->last_launches;
         batches += c->last_batches;
@@ -899,7 +964,7 @@ static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64
 static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64_t seed, uint32_t flags,
                      float *ylt, float *occ_max, uint32_t *dbg_count, uint64_t *dbg_hash) {
     if (flags & ~(ARA_SU | ARA_DEBUG_LOOKUP | ARA_EXACT | ARA_WIDE_PAIRS | ARA_RNG_RECORD | ARA_RNG_OCCURRENCE |
-                  ARA_RNG_SUPPLIED))
+                  ARA_RNG_SUPPLIED | ARA_ASYNC))
         return fail(ARA_EINVAL, "unknown flags 0x%x", flags);
     if (!!(flags & ARA_RNG_RECORD) + !!(flags & ARA_RNG_OCCURRENCE) + !!(flags & ARA_RNG_SUPPLIED) > 1)
         return fail(ARA_EINVAL, "ARA_RNG_RECORD, ARA_RNG_OCCURRENCE and ARA_RNG_SUPPLIED are exclusive");
@@ -918,7 +983,16 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
     CU(cudaSetDevice(c->device));
     const uint64_t N = y->dev.n_trials;
     const bool exact = (flags & ARA_EXACT) != 0 && (flags & ARA_SU) != 0;
-    CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
+    const bool async = (flags & ARA_ASYNC) != 0;
+    if (async) {                                       // per-run counters only; errors stay latched
+        CU(cudaMemsetAsync(c->d_status, 0, kRunCounters, c->stream));
+    } else {
+        CU(fold_latched(c));
+        CU(cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), c->stream));
+    }
+    c->timing_pending = true;
+    c->timing_tail = false;
+    c->timing_batches = 0;
     // ARA_RNG_RECORD with occ_max (a rare combination) runs on the fp64-capable kernel
     const bool za_om = (flags & (ARA_RNG_RECORD | ARA_RNG_SUPPLIED)) && (flags & ARA_SU) && occ_max;
     double ms_ovf = 0.0;
@@ -933,6 +1007,12 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
         CU(cudaEventRecord(c->ev[0], c->stream));
         CU(launch_primary(P, c->stream, c->num_sms));
         CU(cudaEventRecord(c->ev[1], c->stream));
+        c->last_batches = 0;
+        c->last_launches = 1;
+        if (async) {
+            c->async_pending = true;
+            return ARA_OK;
+        }
         CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
     } else if (!exact && !za_om && p->dev.n_layers <= kSplitMaxLayers) {
@@ -984,6 +1064,37 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
             CU(cudaEventRecord(te[3], ss));
         }
         CU(cudaEventRecord(c->ev[1], ss));
+        c->timing_batches = n_batches;
+        if (async) {
+            // device-sized tail passes, no host decision: the overflow plan
+            // (offsets into the pre-sized pool), the overflow compaction and
+            // sampling, the fp64 redo of table-less trials
+            const uint64_t pool_pairs = default_pool_pairs(pl, N);
+            CU(grow(&c->d_pool, c->pool_capacity, pool_pairs * pair_bytes));
+            CU(grow(&c->d_pool_off, c->pool_off_capacity, N));
+            CU(cudaEventRecord(c->ev[2], ss));
+            CU(launch_ovf_plan(c->d_status, y->d_ovf_n, c->d_pool_off, c->pool_capacity / pair_bytes, ss));
+            SplitArgs O = S;
+            O.n_items = 0;
+            O.n_items_dev = &c->d_status->n_ovf_fit;
+            O.list = y->d_ovf;
+            O.pool_off = c->d_pool_off;
+            O.pairs = reinterpret_cast<uint2 *>(c->d_pool);
+            O.cap = 0xffffffffu;
+            O.sched = c->d_sched + 2 * kMaxBatches;
+            CU(launch_compact(O, ss, c->num_sms));
+            O.sched = c->d_sched + 2 * kMaxBatches + 1;
+            CU(launch_sample(O, ss, c->num_sms));
+            CU(launch_scan(p->dev, y->dev, seed, supplied ? flags : flags & ~ARA_RNG_SUPPLIED, ylt, dbg_count,
+                           dbg_hash, c->d_status, y->d_redo, 0, nullptr, (flags & ARA_SU) != 0, ss, c->num_sms,
+                           occ_max, y->d_zprog, y->dev.n_events, p->d_rec_z, &c->d_status->n_redo));
+            CU(cudaEventRecord(c->ev[3], ss));
+            c->timing_tail = true;
+            c->last_batches = n_batches;
+            c->last_launches = 2 * n_batches + 4;
+            c->async_pending = true;
+            return ARA_OK;
+        }
         CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, ss));
         CU(cudaStreamSynchronize(ss));
         const uint32_t n_ovf = c->h_status->bad_event ? 0u : c->h_status->n_ovf;
@@ -1024,6 +1135,12 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
                        dbg_hash, c->d_status, nullptr, 0, y->d_redo, exact, c->stream, c->num_sms, occ_max,
                        y->d_zprog, y->dev.n_events, p->d_rec_z));
         CU(cudaEventRecord(c->ev[1], c->stream));
+        if (async) {
+            c->last_batches = 0;
+            c->last_launches = 1;
+            c->async_pending = true;
+            return ARA_OK;
+        }
         CU(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
     }
@@ -1044,23 +1161,12 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
         CU(cudaEventElapsedTime(&r, c->ev[2], c->ev[3]));
         ms_redo = r;
     }
-    {   // device time of each kernel, summed over its launches (they overlap across streams)
-        double a = 0.0, b = 0.0;
-        for (uint32_t q = 0; q < n_batches; ++q) {
-            float x = 0, z = 0;
-            CU(cudaEventElapsedTime(&x, c->tev[4 * q], c->tev[4 * q + 1]));
-            CU(cudaEventElapsedTime(&z, c->tev[4 * q + 2], c->tev[4 * q + 3]));
-            a += x; b += z;
-        }
-        if (!n_batches) {
-            float x = 0;
-            CU(cudaEventElapsedTime(&x, c->ev[0], c->ev[1]));
-            b = x;
-        }
-        c->last_ms[0] = a; c->last_ms[1] = b; c->last_ms[2] = ms_ovf + ms_redo;
-        c->last_batches = n_batches;
-        c->last_launches = (n_batches ? 2 * n_batches : 1) + (ms_ovf > 0.0 ? 2 : 0) + (redo_launched ? 1 : 0);
-    }
+    c->timing_tail = ms_ovf > 0.0 || redo_launched;
+    if (ms_ovf > 0.0 && !redo_launched) CU(cudaEventRecord(c->ev[3], c->stream));   // (ev[3] already after the pass)
+    CU(compute_timings(c));
+    if (redo_launched && ms_ovf > 0.0) c->last_ms[2] = ms_ovf + ms_redo;   // two tail passes: both timed
+    c->last_batches = n_batches;
+    c->last_launches = (n_batches ? 2 * n_batches : 1) + (ms_ovf > 0.0 ? 2 : 0) + (redo_launched ? 1 : 0);
     if (c->h_status->bad_event) {      // error path: count the offending occurrences
         CU(launch_count_bad(y->d_events, y->dev.n_events, p->dev.catalog, &c->d_status->bad_event, c->stream,
                             c->num_sms));
@@ -1078,6 +1184,16 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
 int ara_prepare(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint32_t flags) {
     if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
     CU(cudaSetDevice(c->device));
+    if (flags & ARA_ASYNC) {                         // the pre-sized overflow pool of ARA_ASYNC runs
+        const std::vector<const ara_portfolio *> gs =
+            p->groups.empty() ? std::vector<const ara_portfolio *>{p}
+                              : std::vector<const ara_portfolio *>(p->groups.begin(), p->groups.end());
+        for (const ara_portfolio *g : gs) {
+            const SplitPlan pl = plan_split(g, y, flags);
+            CU(grow(&c->d_pool, c->pool_capacity, default_pool_pairs(pl, y->dev.n_trials) * (pl.kbits ? 4 : 8)));
+        }
+        CU(grow(&c->d_pool_off, c->pool_off_capacity, std::max<uint64_t>(y->dev.n_trials, 1)));
+    }
     const std::vector<const ara_portfolio *> groups =
         p->groups.empty() ? std::vector<const ara_portfolio *>{p}
                           : std::vector<const ara_portfolio *>(p->groups.begin(), p->groups.end());
@@ -1096,8 +1212,11 @@ int ara_last_run_launches(const ara_ctx *c, uint32_t *kernel_launches, uint32_t 
     return ARA_OK;
 }
 
-int ara_last_run_timings(const ara_ctx *c, double *compact_ms, double *sample_ms, double *redo_ms) {
-    if (!c) return fail(ARA_EINVAL, "ctx is NULL");
+int ara_last_run_timings(const ara_ctx *cc, double *compact_ms, double *sample_ms, double *redo_ms) {
+    if (!cc) return fail(ARA_EINVAL, "ctx is NULL");
+    ara_ctx *c = const_cast<ara_ctx *>(cc);        // (the lazy evaluation of an ARA_ASYNC run's events)
+    CU(cudaSetDevice(c->device));
+    CU(compute_timings(c));
     if (compact_ms) *compact_ms = c->last_ms[0];
     if (sample_ms) *sample_ms = c->last_ms[1];
     if (redo_ms) *redo_ms = c->last_ms[2];

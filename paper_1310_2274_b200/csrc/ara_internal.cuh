@@ -111,15 +111,22 @@ struct YetDev {
     const uint32_t *max_event;  // device word: largest event id (set at every upload)
 };
 
-// device-side status words
+// device-side status words: the per-run counters first (zeroed by every
+// run), then the error counters (zeroed by a synchronous run, accumulated
+// across ARA_ASYNC runs until ara_ctx_synchronize reads them)
 struct RunStatus {
     unsigned long long next_trial;   // dynamic trial scheduler of the fused kernel
-    unsigned long long pad0;
-    unsigned int nonconverged;       // fp64 solves that did not converge
-    unsigned int bad_event;          // != 0: some event id >= catalog (count on the error path)
     unsigned int n_redo;             // trials touching a table-less record (fp64 kernel)
     unsigned int n_ovf;              // trials whose pairs overflowed their batch region
+    unsigned int n_ovf_fit;          // ARA_ASYNC: overflow trials that fit the pre-sized pool
+    unsigned int pad0;
+    unsigned long long pad1;
+    unsigned int nonconverged;       // fp64 solves that did not converge
+    unsigned int bad_event;          // != 0: some event id >= catalog (count on the error path)
+    unsigned int pool_short;         // ARA_ASYNC: overflow trials that did not fit (YLT not written)
+    unsigned int pad2;
 };
+constexpr size_t kRunCounters = 32;  // bytes of RunStatus zeroed by every run
 
 // The split (two-kernel) scan, run batch by batch on two streams:
 // compact_kernel writes each trial's present pairs {device record, k} to its
@@ -140,6 +147,7 @@ struct SplitArgs {
     RunStatus *status;
     // work items of this launch: trial t0 + i (batch), or list[i] (overflow pass)
     uint32_t t0, n_items;
+    const unsigned int *n_items_dev;   // non-null: the item count is read on the device (ARA_ASYNC)
     const uint32_t *list;
     const uint64_t *pool_off;     // overflow pass: region of item i in the pool (pair units)
     unsigned long long *sched;    // this launch's dynamic-scheduler counter (zeroed)
@@ -177,6 +185,11 @@ void launch_occ_table(const uint2 *cidx, const uint2 *mu_meta, const double *slo
                       const LayerInfo *layers, uint32_t n_layers, uint32_t lp, uint32_t catalog, float *out,
                       cudaStream_t s);
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
+// ARA_ASYNC overflow plan: exclusive scan of the listed trials' pair counts
+// into pool offsets, as many as fit pool_pairs (status->n_ovf_fit; the rest
+// counted in status->pool_short)
+cudaError_t launch_ovf_plan(RunStatus *status, const uint32_t *ovf_n, uint64_t *pool_off, uint64_t pool_pairs,
+                            cudaStream_t s);
 cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms);
 cudaError_t launch_unpack_yet(const uint32_t *packed, uint64_t n, uint32_t bits, uint32_t *out, cudaStream_t s,
                               int num_sms);
@@ -199,7 +212,8 @@ cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed
                         float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
                         const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
                         cudaStream_t s, int num_sms, float *occ_max = nullptr, const float *zp_sup = nullptr,
-                        uint64_t zp_stride = 0, const float *ze_sup = nullptr);
+                        uint64_t zp_stride = 0, const float *ze_sup = nullptr,
+                        const unsigned int *n_list_dev = nullptr);
 cudaError_t launch_sample_losses(const BetaRec *recs, TablePtr tables,
                                  const float *zp,
                                  const float *ze, uint64_t n, bool exact, float *out,

@@ -174,6 +174,7 @@ struct ScanArgs {
     RunStatus *status;
     const uint32_t *trial_list;     // null: all trials
     uint64_t n_list;
+    const unsigned int *n_list_dev; // non-null: the list length is read on the device (ARA_ASYNC)
     uint32_t *redo;                 // trials to re-run with the fp64 kernel
     float *occ_max;                 // null, or [n_layers][n_trials] largest occurrence loss (G29)
     const float *zp_sup;            // ARA_RNG_SUPPLIED: z_(Prog,E) [program][zp_stride]
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
     SlotInfo *slots = reinterpret_cast<SlotInfo *>(scan_smem + off_slots);
     LayerInfo *layers = reinterpret_cast<LayerInfo *>(scan_smem + off_layers);
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(scan_smem + off_bitmap);
+    if (A.trial_list && A.n_list_dev && *A.n_list_dev == 0) return;   // a device-sized pass with nothing to do
 
     for (uint32_t t = threadIdx.x; t < A.pf.bitmap_words; t += blockDim.x) bitmap[t] = A.pf.bitmap[t];
     for (uint32_t t = threadIdx.x; t < A.pf.n_slots; t += blockDim.x) slots[t] = A.pf.slots[t];
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) scan_kernel(const __grid_const
                  (A.flags & ARA_RNG_SUPPLIED) ? 3u : (A.flags & ARA_RNG_RECORD) ? 1u : (A.flags & ARA_RNG_OCCURRENCE) ? 2u : 0u,
                  A.zp_sup, A.zp_stride, A.ze_sup, 0};
     const uint64_t n_trials = A.yet.n_trials;
-    const uint64_t n_work = A.trial_list ? A.n_list : n_trials;
+    const uint64_t n_work = A.trial_list ? (A.n_list_dev ? (uint64_t)*A.n_list_dev : A.n_list) : n_trials;
     const uint32_t C = A.pf.catalog, shift = A.pf.bitmap_shift;
     const uint2 *cidx = A.pf.cidx;
     const uint2 *mu_meta = A.pf.mu_meta;
@@ -640,10 +642,10 @@ cudaError_t launch_scan(const PortfolioDev &pf, const YetDev &yet, uint64_t seed
                         float *ylt, uint32_t *dbg_count, uint64_t *dbg_hash, RunStatus *status,
                         const uint32_t *trial_list, uint64_t n_list, uint32_t *redo, bool exact_kernel,
                         cudaStream_t s, int num_sms, float *occ_max, const float *zp_sup, uint64_t zp_stride,
-                        const float *ze_sup) {
-    ScanArgs A{pf, yet, seed, flags, ylt, dbg_count, dbg_hash, status, trial_list, n_list, redo, occ_max,
+                        const float *ze_sup, const unsigned int *n_list_dev) {
+    ScanArgs A{pf, yet, seed, flags, ylt, dbg_count, dbg_hash, status, trial_list, n_list, n_list_dev, redo, occ_max,
                zp_sup, zp_stride, ze_sup};
-    if (trial_list && n_list == 0) return cudaSuccess;
+    if (trial_list && n_list == 0 && !n_list_dev) return cudaSuccess;
     if (!(flags & ARA_SU)) return launch_scan_t<false, false>(A, s, num_sms);
     // the fp64 per-sample solve lives in a separate instantiation (its register
     // demand would otherwise throttle the table path)

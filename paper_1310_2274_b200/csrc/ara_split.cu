@@ -146,7 +146,7 @@ template <bool PK, int BM, class Sink>
 __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t *bitmap, Sink &sink) {
     const int lane = threadIdx.x & 31;
     const uint32_t shift = A.pf.bitmap_shift, cap = A.cap;
-    const uint32_t n_items = A.n_items;
+    const uint32_t n_items = A.n_items_dev ? *A.n_items_dev : A.n_items;
     const uint32_t *events = A.yet.events;
     const uint64_t *offsets = A.yet.offsets;
     const uint2 *__restrict__ cidx = A.pf.cidx;
@@ -338,6 +338,7 @@ template <bool PK, int BM>
 __global__ void __launch_bounds__(kCompactThreads, 32 / ARA_COMPACT_WARPS) compact_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);
+    if (A.n_items_dev && *A.n_items_dev == 0) return; // a device-sized pass with nothing to do
     if (*A.yet.max_event >= A.pf.catalog) {           // out-of-range ids: nothing is read
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&A.status->bad_event, 1u);
         return;
@@ -616,6 +617,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 32 / kSampleWarps)   // <= 
     unsigned long long *hw = reinterpret_cast<unsigned long long *>(
         ((uintptr_t)(cw + kSampleWarps * nl) + 7) & ~(uintptr_t)7);            // [warps][nl]
     float *mow = reinterpret_cast<float *>(hw + kSampleWarps * nl);             // OM && !SL: [warps][nl][32]
+    if (A.n_items_dev && *A.n_items_dev == 0) return; // a device-sized pass with nothing to do
     for (uint32_t t = threadIdx.x; t < A.pf.n_slots; t += blockDim.x) slots[t] = A.pf.slots[t];
     for (uint32_t t = threadIdx.x; t < nl; t += blockDim.x) layers[t] = A.pf.layers[t];
     __syncthreads();
@@ -626,11 +628,12 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 32 / kSampleWarps)   // <= 
     uint8_t *flw = reinterpret_cast<uint8_t *>(xsw + kSampleWarps * kXCap);
     const SampleWs W{slots, layers, accw + warp * nl * 32 + lane, cw + warp * nl, hw + warp * nl,
                      (OM && !SL) ? mow + warp * nl * 32 + lane : nullptr, xsw + warp * kXCap, flw + warp * kXCap};
+    const uint32_t n_items = A.n_items_dev ? *A.n_items_dev : A.n_items;
     while (true) {
         unsigned long long i = 0;
         if (lane == 0) i = atomicAdd(A.sched, 1ull);
         i = __shfl_sync(0xffffffffu, i, 0);
-        if (i >= A.n_items) break;
+        if (i >= n_items) break;
         uint32_t t, n;
         uint64_t off;                                 // the item's pairs: offset in pair units
         if (A.list) {
@@ -671,6 +674,60 @@ void launch_split_recs(const BetaRec *recs, const uint32_t *rec_src, const uint3
     const uint64_t blocks = (n + 255) / 256;
     split_recs_kernel<<<(unsigned)(blocks < 65535u * 16u ? blocks : 65535u * 16u), 256, 0, s>>>(
         recs, rec_src, rec_meta, slots, mu, n, out, mu_meta);
+}
+
+// ARA_ASYNC overflow plan (one CTA): pool offsets of the listed trials in
+// list order, an exclusive scan in chunks of 1024; the trials that do not fit
+// the pre-sized pool are counted (reported at the next synchronisation)
+__global__ void ovf_plan_kernel(RunStatus *status, const uint32_t *__restrict__ ovf_n, uint64_t *__restrict__ pool_off,
+                                uint64_t pool_pairs) {
+    __shared__ unsigned long long part[32];
+    __shared__ unsigned long long base_s;
+    __shared__ unsigned int fit_s;
+    const uint32_t n = status->n_ovf;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) { base_s = 0; fit_s = n; }
+    __syncthreads();
+    for (uint32_t c0 = 0; c0 < n; c0 += blockDim.x) {
+        const uint32_t i = c0 + threadIdx.x;
+        const unsigned long long v = i < n ? ovf_n[i] : 0ull;
+        unsigned long long x = v;                                  // inclusive warp scan
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) part[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long w = lane < (int)(blockDim.x >> 5) ? part[lane] : 0ull;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, w, d);
+                if (lane >= d) w += y;
+            }
+            part[lane] = w;                                        // inclusive over warps
+        }
+        __syncthreads();
+        const unsigned long long excl = base_s + (warp ? part[warp - 1] : 0ull) + x - v;
+        if (i < n) {
+            pool_off[i] = excl;
+            if (excl + v > pool_pairs) atomicMin(&fit_s, i);        // the first trial that does not fit
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) base_s += part[(blockDim.x >> 5) - 1];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        status->n_ovf_fit = fit_s;
+        status->pool_short += n - fit_s;
+    }
+}
+
+cudaError_t launch_ovf_plan(RunStatus *status, const uint32_t *ovf_n, uint64_t *pool_off, uint64_t pool_pairs,
+                            cudaStream_t s) {
+    ovf_plan_kernel<<<1, 1024, 0, s>>>(status, ovf_n, pool_off, pool_pairs);
+    return cudaGetLastError();
 }
 
 // Packed YET upload (ara_yet_refill_packed): ids bit-packed LSB-first, `bits`
@@ -783,8 +840,10 @@ cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms) {
     cudaError_t err = prepare_launch((const void *)kern, smem, kCompactThreads, per_sm);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const uint32_t blocks = std::max(1u, std::min<uint32_t>((uint32_t)num_sms, (A.n_items + ARA_COMPACT_WARPS - 1) /
-                                                                                  ARA_COMPACT_WARPS));
+    const uint32_t blocks = A.n_items_dev ? (uint32_t)num_sms
+                                          : std::max(1u, std::min<uint32_t>((uint32_t)num_sms,
+                                                                            (A.n_items + ARA_COMPACT_WARPS - 1) /
+                                                                                ARA_COMPACT_WARPS));
     kern<<<blocks, kCompactThreads, smem, s>>>(A);      // one CTA per SM (persistent)
     return cudaGetLastError();
 }
@@ -834,8 +893,9 @@ cudaError_t launch_sample(const SplitArgs &A, cudaStream_t s, int num_sms) {
     cudaError_t err = prepare_launch((const void *)kern, smem, kSampleWarps * 32, per_sm);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const uint32_t blocks = std::max(1u, std::min<uint32_t>((uint32_t)num_sms, (A.n_items + kSampleWarps - 1) /
-                                                                                  kSampleWarps));
+    const uint32_t blocks = A.n_items_dev ? (uint32_t)num_sms
+                                          : std::max(1u, std::min<uint32_t>((uint32_t)num_sms,
+                                                                            (A.n_items + kSampleWarps - 1) / kSampleWarps));
     kern<<<blocks, kSampleWarps * 32, smem, s>>>(A);    // one CTA per SM (persistent)
     return cudaGetLastError();
 }

@@ -1095,3 +1095,57 @@ def test_shared_xelts_many_layers(A, ctx):
     # per device record: 72k): <= 200 B per device record (484 B in round 1)
     per_dev = info["device_bytes"] / n_dev
     assert per_dev <= 200, (info, per_dev)
+
+
+# ---- ARA_ASYNC: no host synchronisation inside ara_run ----------------------
+@pytest.mark.parametrize("case", ["split", "primary", "overflow", "capped", "exact", "groups"])
+def test_async_runs_equal_sync(A, ctx, case, monkeypatch):
+    # the same YLT, counts and hashes bit for bit, whether ara_run waits for
+    # its status (sync: host-sized overflow / redo passes) or not (device-sized
+    # passes); errors none
+    cfg = aragen.load_config("cfg1")
+    if case == "groups":
+        cfg.update(n_layers=4, elts_per_layer=3, catalog=5000, records_per_elt=800, n_trials=300,
+                   layer_terms=[[2e5 * (l + 1), 5e6, 1.0e6, 5.0e7] for l in range(4)])
+        monkeypatch.setenv("ARA_GROUP_BYTES", "1")
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    if case == "capped":
+        pf["rec_sigma_i"] = pf["rec_sigma_i"].copy()
+        pf["rec_sigma_i"][::7] = pf["rec_max"][::7]          # table-less records: the fp64 redo pass
+    if case == "overflow":
+        monkeypatch.setenv("ARA_PAIR_CAP", "1")              # every trial through the overflow pass
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    kw = dict(seed=13, su=case != "primary", exact=case == "exact")
+    ref = A.run(ctx, P, Y, **kw)
+    got = A.run(ctx, P, Y, async_=True, **kw)
+    ctx.synchronize()
+    assert np.array_equal(ref.cpu().numpy(), got.cpu().numpy())
+    if case != "primary":
+        r2 = A.run(ctx, P, Y, debug=True, **kw)
+        g2 = A.run(ctx, P, Y, debug=True, async_=True, **kw)
+        ctx.synchronize()
+        for x, y in zip(r2, g2):
+            assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
+    assert A.last_run_timings(ctx)["sample_ms"] > 0
+
+
+def test_async_errors_reported_at_synchronize(A, monkeypatch):
+    ctx2 = A.Context(0)                                      # a fresh context: a small pre-sized pool
+    cfg = aragen.load_config("cfg1")
+    cfg["n_trials"] = 200
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P, Y = A.Portfolio(ctx2, pf), A.Yet.from_dict(ctx2, yet)
+    monkeypatch.setenv("ARA_PAIR_CAP", "1")
+    monkeypatch.setenv("ARA_ASYNC_POOL_PAIRS", "100")
+    A.run(ctx2, P, Y, seed=1, async_=True)                   # returns at once
+    with pytest.raises(A.AraError) as ei:
+        ctx2.synchronize()
+    assert ei.value.code == A.ENOMEM
+    ctx2.synchronize()                                       # the latch is cleared
+    monkeypatch.delenv("ARA_PAIR_CAP")
+    yet["events"][17] = cfg["catalog"]                       # an event id out of range
+    Y2 = A.Yet.from_dict(ctx2, yet)
+    A.run(ctx2, P, Y2, seed=1, async_=True)
+    with pytest.raises(A.AraError) as ei:
+        ctx2.synchronize()
+    assert ei.value.code == A.ERANGE

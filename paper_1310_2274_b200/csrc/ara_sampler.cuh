@@ -232,37 +232,37 @@ __device__ __forceinline__ double lambda_exact64(double v, double a, double b, d
 
 // ------------------------------------------------------------ table eval --
 
-__device__ __forceinline__ void sigmoid2(float lam, float &x, float &y) {
+// x = 1/(1 + e^-lambda) at a table node (lambda clamped to +-80: normal MUFU operands)
+__device__ __forceinline__ float sigmoid_node(float lam) {
     const float l = fminf(fmaxf(lam, -80.0f), 80.0f);
-    const float e = ex2_ftz(-1.44269504088896340736f * l);   // e^-l, normal
-    x = rcp_ftz(1.0f + e);                               // MUFU.RCP
-    y = e * x;
+    return rcp_ftz(1.0f + ex2_ftz(-1.44269504088896340736f * l));
 }
 
 // quintic Hermite on [v_i, v_i + h] from the two nodes' (lambda, lambda'),
-// lambda'' from the ODE at each node; t in [0,1]
+// lambda'' from the ODE at each node, evaluated in Horner form in t in [0,1]:
+// p(t) = l0 + B t + C/2 t^2 + c3 t^3 + c4 t^4 + c5 t^5 with B = h l0', C = h^2 l0'',
+// E = h l1', F = h^2 l1'', D = l1 - l0 and (from p, p', p'' at t = 1)
+// c3 = 10D - 6B - 3C/2 - 4E + F/2, c4 = -15D + 8B + 3C/2 + 7E - F,
+// c5 = 6D - 3B - C/2 - 3E + F/2.  Every operation an explicit fmaf / fmul, so
+// the rounding is the same in every kernel instantiation (no contraction choice).
 __device__ __forceinline__ float quintic_from_nodes(float2 n0, float2 n1, int i, float t, float a, float b) {
-    const float v0 = fmaf((float)i, kTabH, kTabV0), v1 = v0 + kTabH;
-    float x0, y0, x1, y1;
-    sigmoid2(n0.x, x0, y0);
-    sigmoid2(n1.x, x1, y1);
-    const float s0 = n0.y * (-v0 - fmaf(a, y0, -b * x0) * n0.y);   // lambda'' at the nodes
-    const float s1 = n1.y * (-v1 - fmaf(a, y1, -b * x1) * n1.y);
-    const float t2 = t * t, t3 = t2 * t;
-    const float omt = 1.0f - t;
-    // quintic Hermite basis on [0,1] (derivatives scaled by h, h^2)
-    const float h01 = t3 * fmaf(t, fmaf(6.0f, t, -15.0f), 10.0f);             // 10t^3-15t^4+6t^5
-    const float h10 = t * omt * omt * omt * fmaf(3.0f, t, 1.0f);                // t(1-t)^3(1+3t)
-    const float h11 = -t3 * omt * fmaf(-3.0f, t, 4.0f);                         // -t^3(1-t)(4-3t)
-    const float h20 = 0.5f * t2 * omt * omt * omt;                              // t^2(1-t)^3/2
-    const float h21 = 0.5f * t3 * omt * omt;                                    // t^3(1-t)^2/2
-    const float H = kTabH, H2 = kTabH * kTabH;
-    float lam = fmaf(h01, n1.x - n0.x, n0.x);
-    lam = fmaf(h10 * H, n0.y, lam);
-    lam = fmaf(h11 * H, n1.y, lam);
-    lam = fmaf(h20 * H2, s0, lam);
-    lam = fmaf(h21 * H2, s1, lam);
-    return lam;
+    const float v0 = fmaf((float)i, kTabH, kTabV0), v1 = __fadd_rn(v0, kTabH);
+    const float apb = __fadd_rn(a, b);
+    const float x0 = sigmoid_node(n0.x), x1 = sigmoid_node(n1.x);
+    const float g0 = fmaf(-apb, x0, a), g1 = fmaf(-apb, x1, a);          // a(1-x) - b x
+    const float s0 = __fmul_rn(n0.y, fmaf(-g0, n0.y, -v0));               // lambda'' = l' (-v - g l')
+    const float s1 = __fmul_rn(n1.y, fmaf(-g1, n1.y, -v1));
+    const float D = __fsub_rn(n1.x, n0.x);
+    const float B = __fmul_rn(kTabH, n0.y), E = __fmul_rn(kTabH, n1.y);
+    const float C = __fmul_rn(kTabH * kTabH, s0), F = __fmul_rn(kTabH * kTabH, s1);
+    const float c3 = fmaf(10.0f, D, fmaf(-6.0f, B, fmaf(-1.5f, C, fmaf(-4.0f, E, __fmul_rn(0.5f, F)))));
+    const float c4 = fmaf(-15.0f, D, fmaf(8.0f, B, fmaf(1.5f, C, fmaf(7.0f, E, -F))));
+    const float c5 = fmaf(6.0f, D, fmaf(-3.0f, B, fmaf(-0.5f, C, fmaf(-3.0f, E, __fmul_rn(0.5f, F)))));
+    float p = fmaf(c5, t, c4);
+    p = fmaf(p, t, c3);
+    p = fmaf(p, t, __fmul_rn(0.5f, C));
+    p = fmaf(p, t, B);
+    return fmaf(p, t, n0.x);
 }
 
 // quintic Hermite in v on record `rec`'s table

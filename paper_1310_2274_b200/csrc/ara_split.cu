@@ -221,20 +221,19 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         // lane has >= 8 pairs in the chunk; np <= 4 * ARA_MAX_SLOTS = 896
         // < 2^10, so 10 slices cover every case
         static_assert(4 * ARA_MAX_SLOTS < (1 << 10), "pair count of a lane's 4 events must fit 10 bits");
-        uint32_t excl = 0, tot = 0;
+        uint32_t excl = 0;
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, np);   // the chunk's pairs (one REDUX)
         const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
             const uint32_t m = __ballot_sync(0xffffffffu, (np >> b) & 1u);
             excl += (uint32_t)__popc(m & lt) << b;
-            tot += (uint32_t)__popc(m) << b;
         }
         if (__any_sync(0xffffffffu, np > 7u)) {
 #pragma unroll 1
             for (int b = 3; b < 10; ++b) {
                 const uint32_t m = __ballot_sync(0xffffffffu, (np >> b) & 1u);
                 excl += (uint32_t)__popc(m & lt) << b;
-                tot += (uint32_t)__popc(m) << b;
             }
         }
         if (S.c == 0) out = sink.begin(S.t);

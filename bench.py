@@ -280,16 +280,26 @@ def run_ours(args, cfg, rank, world, local):
             return [(pml[i], tvar[i]) for i in range(len(layers))]
         return [ara.risk_measures(ctx, src, L, N_total, layer, rps=rps, n_shards=n_shards) for layer in layers]
 
-    def step(Yx, timed=False):
-        # ara_run with ARA_ASYNC: no host synchronisation inside the run; the
-        # measures' read-back is the step's one synchronisation (errors latched
-        # by the runs are checked by ctx.synchronize() after the loop)
+    meas_dev = torch.empty((len(layers), len(rps), 3), dtype=torch.float64, device=dev)
+    meas_host = torch.empty((args.steps, len(layers), len(rps), 3), dtype=torch.float64).pin_memory()
+
+    def step(Yx, timed=False, slot=None):
+        # ara_run with ARA_ASYNC: no host synchronisation inside the run (errors
+        # latched by the runs are checked by ctx.synchronize() after the loop).
+        # slot None: the measures read back synchronously (the e2e path);
+        # slot s: ara_risk_measures_async into device memory + an async copy to
+        # pinned host row s -- the steps queue back to back, one sync at the end
         ara.run(ctx, P, Yx, seed=cfg["seed"], su=cfg["su"], ylt=ylt, async_=True)
         if timed:
             m0 = torch.cuda.Event(enable_timing=True); m1 = torch.cuda.Event(enable_timing=True)
             m0.record(stream)
         src, n_shards = gather_ylt(ylt, world, N_total, gathered, padded)
-        out = measures(src, n_shards)
+        if slot is None:
+            out = measures(src, n_shards)
+        else:
+            ara.risk_measures_async(ctx, src, L, N_total, layers, rps=rps, n_shards=n_shards, out=meas_dev)
+            meas_host[slot].copy_(meas_dev, non_blocking=True)
+            out = None
         if timed:
             m1.record(stream)
             meas_ev.append((m0, m1))
@@ -309,8 +319,8 @@ def run_ours(args, cfg, rank, world, local):
     with ClockSampler(local) as clk:
         t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for _ in range(args.steps):
-            res = step(Y, timed=True)
+        for s_ in range(args.steps):
+            step(Y, timed=True, slot=s_)
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -318,6 +328,14 @@ def run_ours(args, cfg, rank, world, local):
         torch.cuda.synchronize()
     elapsed = t0.elapsed_time(t1) / 1e3
     ctx.synchronize()                                    # errors latched by the ARA_ASYNC runs, if any
+    # every timed step's measures (read back asynchronously) equal a synchronous call's
+    res = step(Y)
+    for s_ in range(args.steps):
+        for i in range(len(layers)):
+            got = [tuple(float(meas_host[s_, i, q, c]) for q in range(len(rps))) for c in (0, 1)]
+            want = [tuple(float(x) for x in res[i][0]), tuple(float(x) for x in res[i][1])]
+            if got != want:
+                raise RuntimeError(f"step {s_} table {layers[i]}: async measures {got} != {want}")
     if world > 1:
         t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

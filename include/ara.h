@@ -326,6 +326,20 @@ int ara_risk_measures_batch(ara_ctx *ctx, const float *ylt, uint32_t n_layers, u
                             uint32_t n_shards, const int32_t *layers, uint32_t n_sel, const double *rps,
                             uint32_t n_rp, double *pml_out, double *tvar_out, double *var_out);
 
+/* ara_risk_measures_batch without the read-back: the same launches, enqueued
+ * on the context stream, the results written to DEVICE memory and the call
+ * returning at once (no host synchronisation) -- so consecutive analyses
+ * (ARA_ASYNC runs + measures) queue back to back on the GPU.
+ *   d_out   DEVICE fp64 [n_sel][n_rp][3], caller-allocated: (PML, TVaR, VaR)
+ *           of table i, return period q at d_out[3 (n_rp i + q) + 0..2];
+ *           valid once the stream reaches the launches (e.g. after
+ *           ara_ctx_synchronize or an event / copy on that stream).
+ * Arguments and argument errors as ara_risk_measures_batch; ARA_EINVAL also
+ * for a host d_out. */
+int ara_risk_measures_async(ara_ctx *ctx, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                            uint32_t n_shards, const int32_t *layers, uint32_t n_sel, const double *rps,
+                            uint32_t n_rp, double *d_out);
+
 /* The exceedance curve (SPEC ExceedanceCurve S:345-352) of one
  * layer's YLT, or of the roll-up over layers (layer = -1, G16): the losses
  * sorted descending, L(1) >= ... >= L(N); the empirical exceedance

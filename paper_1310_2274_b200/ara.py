@@ -38,7 +38,7 @@ EXPORTS = (
     "ara_yet_refill", "ara_yet_refill_packed", "ara_yet_num_trials", "ara_yet_destroy", "ara_run", "ara_run_ep", "ara_last_run_timings", "ara_risk_measures_var", "ara_risk_measures_batch", "ara_exceedance_curve",
     "ara_risk_measures",
     "ara_sample_losses", "ara_draw_uniforms", "ara_normal_quantiles", "ara_beta_quantiles", "ara_prepare",
-    "ara_yet_set_z", "ara_portfolio_set_z", "ara_last_run_launches",
+    "ara_yet_set_z", "ara_portfolio_set_z", "ara_last_run_launches", "ara_risk_measures_async",
 )
 
 
@@ -75,6 +75,7 @@ def _load():
     L.ara_risk_measures_var.argtypes = [vp, vp, u32, u64, u32, i32, vp, u32, vp, vp, vp]
     L.ara_exceedance_curve.argtypes = [vp, vp, u32, u64, u32, i32, vp]
     L.ara_risk_measures_batch.argtypes = [vp, vp, u32, u64, u32, vp, u32, vp, u32, vp, vp, vp]
+    L.ara_risk_measures_async.argtypes = [vp, vp, u32, u64, u32, vp, u32, vp, u32, vp]
     L.ara_last_run_timings.argtypes = [vp, vp, vp, vp]
     L.ara_sample_losses.argtypes = [vp, u64, vp, vp, vp, u32, vp]
     L.ara_draw_uniforms.argtypes = [vp, u64, u64, vp, vp]
@@ -359,6 +360,21 @@ def risk_measures_batch(ctx: Context, ylt, n_layers: int, n_total: int, layers, 
     _check(lib.ara_risk_measures_batch(ctx.h, _p(ylt), int(n_layers), int(n_total), int(n_shards), _p(ls),
                                        len(ls), _p(r), len(r), _p(pml), _p(tvar), _p(var)))
     return pml, tvar, var
+
+
+def risk_measures_async(ctx: Context, ylt, n_layers: int, n_total: int, layers, rps=(100, 250, 500),
+                        n_shards: int = 1, out=None):
+    """ara_risk_measures_async: the measures of every listed table enqueued on the
+    context stream, no synchronisation; returns the device fp64 tensor
+    [len(layers)][n_rp][3] of (PML, TVaR, VaR) they will be written to."""
+    import torch
+    r = np.ascontiguousarray(rps, np.float64)
+    ls = np.ascontiguousarray(layers, np.int32)
+    if out is None:
+        out = torch.empty((len(ls), len(r), 3), dtype=torch.float64, device=ylt.device)
+    _check(lib.ara_risk_measures_async(ctx.h, _p(ylt), int(n_layers), int(n_total), int(n_shards), _p(ls),
+                                       len(ls), _p(r), len(r), _p(out)))
+    return out
 
 
 def exceedance_curve(ctx: Context, ylt, n_layers: int, n_total: int, layer: int = 0, n_shards: int = 1,

@@ -169,17 +169,16 @@ struct RecordStore {
     uint64_t n = 0;                    // input records
     BetaRec *d_recs = nullptr;         // [n]
     float *d_mu = nullptr;             // [n]
-    float2 *d_hot = nullptr;           // [n][kHotN] central table nodes
-    float2 *d_cold = nullptr;          // [n][kColdN] tail table nodes
+    float2 *d_nodes = nullptr;         // kTabPad + [n][kTabNodes] quantile-table nodes (internal.cuh)
     uint32_t n_exact = 0;              // records whose table failed its midpoint check
     std::vector<uint32_t> pos;         // store position of each input record (the store follows the first
                                        // kernel group's event-major device order, so for a portfolio of one
                                        // group without shared XELTs a pair's table is its device record's)
     ~RecordStore() {
         cudaSetDevice(device);
-        cudaFree(d_recs); cudaFree(d_mu); cudaFree(d_hot); cudaFree(d_cold);
+        cudaFree(d_recs); cudaFree(d_mu); cudaFree(d_nodes);
     }
-    uint64_t bytes() const { return n * (sizeof(BetaRec) + sizeof(float) + (kHotN + kColdN) * sizeof(float2)); }
+    uint64_t bytes() const { return n * (sizeof(BetaRec) + sizeof(float) + kTabNodes * sizeof(float2)); }
 };
 
 struct ara_portfolio {
@@ -193,6 +192,7 @@ struct ara_portfolio {
     SlotInfo *d_slots = nullptr;
     LayerInfo *d_layers = nullptr;
     float *d_occ = nullptr;            // [catalog][occ_lp] occurrence losses without draws (fast path)
+    uint32_t *d_occ_bitmap = nullptr;  // [bitmap words] nonzero occurrence losses (the fast path's filter)
     float *d_rec_z = nullptr;          // ARA_RNG_SUPPLIED: z_(E) per device record (ara_portfolio_set_z)
     std::vector<uint32_t> rec_src;     // input record of each device record
     uint32_t max_prog = 0;             // largest program id of the layers
@@ -417,8 +417,7 @@ static int create_store(ara_ctx *c, const ara_record *rec, uint64_t R, const std
     ara_record *d_raw = nullptr;
     uint32_t *d_order = nullptr;
     cudaStream_t s = c->stream;
-    if (dalloc(&st->d_recs, R) || dalloc(&st->d_mu, R) || dalloc(&st->d_hot, R * kHotN) ||
-        dalloc(&st->d_cold, R * kColdN) ||
+    if (dalloc(&st->d_recs, R) || dalloc(&st->d_mu, R) || dalloc(&st->d_nodes, R * kTabNodes + kTabPad) ||
         dalloc(&d_raw, R) || dalloc(&d_order, R)) {
         cudaGetLastError();
         cudaFree(d_raw); cudaFree(d_order);
@@ -426,10 +425,12 @@ static int create_store(ara_ctx *c, const ara_record *rec, uint64_t R, const std
                     (unsigned long long)R);
     }
     cudaError_t e = R ? cudaMemcpyAsync(d_raw, rec, R * sizeof(ara_record), cudaMemcpyHostToDevice, s) : cudaSuccess;
+    // table-less records keep zero nodes (the split sampler reads them, then redoes the trial)
+    if (e == cudaSuccess) e = cudaMemsetAsync(st->d_nodes, 0, (R * kTabNodes + kTabPad) * sizeof(float2), s);
     if (e == cudaSuccess && R) e = cudaMemcpyAsync(d_order, order.data(), R * sizeof(uint32_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
     if (e == cudaSuccess) {
-        launch_prep_records(d_raw, d_order, R, st->d_recs, st->d_mu, st->d_hot, st->d_cold,
+        launch_prep_records(d_raw, d_order, R, st->d_recs, st->d_mu, st->d_nodes + kTabPad,
                             &c->d_status->nonconverged, s);
         e = cudaGetLastError();
     }
@@ -610,7 +611,8 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
         dalloc(&p->d_cidx, (size_t)C) || dalloc(&d_rec_meta, (size_t)total) || dalloc(&p->d_srecs, (size_t)total) ||
         dalloc(&p->d_mm, (size_t)total) || dalloc(&p->d_rec_orig, total) || dalloc(&d_rec_src, total) ||
         dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) ||
-        dalloc(&p->d_occ, (size_t)C * occ_lp) || dalloc(&p->d_slot_terms, slot_terms.size())) {
+        dalloc(&p->d_occ, (size_t)C * occ_lp) || dalloc(&p->d_occ_bitmap, words) ||
+        dalloc(&p->d_slot_terms, slot_terms.size())) {
         cudaGetLastError();
         return cleanup(fail(ARA_ENOMEM, "device allocation failed in ara_create_portfolio"));
     }
@@ -634,6 +636,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     if (e == cudaSuccess) {       // lines 6-11 per (event, layer) at the mean losses (fast path)
         launch_occ_table(p->d_cidx, p->d_mm, p->d_slot_terms, p->d_layers, n_layers, occ_lp, C,
                          p->d_occ, s);
+        launch_occ_bitmap(p->d_occ, occ_lp, C, shift, words, p->d_occ_bitmap, s);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);     // host vectors die at return
@@ -656,7 +659,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     }
     d.n_exact_records = store->n_exact;
     d.bitmap = p->d_bitmap; d.recs = store->d_recs; d.rec_mu = store->d_mu;
-    d.tables = TablePtr{store->d_hot, store->d_cold};
+    d.tables = TablePtr{store->d_nodes + kTabPad};
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
     d.cidx = p->d_cidx; d.srecs = p->d_srecs; d.mu_meta = p->d_mm;
     d.any_terms = et ? 1u : 0u;
@@ -666,6 +669,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     d.all_sigma_zero = all_sigma_zero ? 1u : 0u;
     d.occ_lp = occ_lp;
     d.occ = p->d_occ;
+    d.occ_bitmap = p->d_occ_bitmap;
     *out = p;
     return ARA_OK;
 }
@@ -673,7 +677,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
 static uint64_t group_bytes(const ara_portfolio *g) {          // per-group arrays (not the record store)
     const PortfolioDev &d = g->dev;
     return (uint64_t)d.catalog * (sizeof(uint2) + d.occ_lp * sizeof(float)) +
-           (uint64_t)d.bitmap_words * 4 +
+           (uint64_t)d.bitmap_words * 8 +
            d.n_dev_records * (sizeof(SplitRec) + sizeof(uint2) + sizeof(uint32_t)) +
            d.n_slots * (sizeof(SlotInfo) + 4 * sizeof(double)) + d.n_layers * sizeof(LayerInfo);
 }
@@ -703,7 +707,7 @@ void ara_portfolio_destroy(ara_portfolio *p) {
     cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig);
     cudaFree(p->d_cidx); cudaFree(p->d_srecs); cudaFree(p->d_mm);
     cudaFree(p->d_slots); cudaFree(p->d_layers);
-    cudaFree(p->d_occ); cudaFree(p->d_slot_terms); cudaFree(p->d_rec_z);
+    cudaFree(p->d_occ); cudaFree(p->d_occ_bitmap); cudaFree(p->d_slot_terms); cudaFree(p->d_rec_z);
     delete p;
 }
 
@@ -1270,11 +1274,10 @@ int ara_risk_measures(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t 
                                  nullptr);
 }
 
-int ara_risk_measures_batch(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
+// the joint-select launches of ara_risk_measures_batch / _async, results to device d_out
+static int measures_enqueue(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
                             uint32_t n_shards, const int32_t *layers, uint32_t n_sel, const double *rps,
-                            uint32_t n_rp, double *pml_out, double *tvar_out, double *var_out) {
-    NvtxRange nvtx("ara_risk_measures_batch");
-    if (!c || !ylt || !layers || !rps || !pml_out || !tvar_out) return fail(ARA_EINVAL, "NULL argument");
+                            uint32_t n_rp, double *d_out) {
     if (n_total == 0) return fail(ARA_EINVAL, "empty YLT");
     if (n_layers == 0 || n_shards == 0 || n_total % n_shards)
         return fail(ARA_EINVAL, "need n_layers >= 1, n_shards >= 1 dividing n_total");
@@ -1294,10 +1297,30 @@ int ara_risk_measures_batch(ara_ctx *c, const float *ylt, uint32_t n_layers, uin
         CU(dalloc(&c->ms.vals, n_total));
         c->ms.capacity = n_total;
     }
-    // one joint-select launch per table, back to back on the stream, one read-back
+    // one joint-select launch per table, back to back on the stream
     for (uint32_t i = 0; i < n_sel; ++i)
         CU(launch_measures_multi(ylt, n_layers, n_total, n_shards, layers[i], rps, n_rp, c->ms,
-                                 c->ms.d_out + 3 * n_rp * i, c->stream));
+                                 d_out + 3 * n_rp * i, c->stream));
+    return ARA_OK;
+}
+
+int ara_risk_measures_async(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                            uint32_t n_shards, const int32_t *layers, uint32_t n_sel, const double *rps,
+                            uint32_t n_rp, double *d_out) {
+    NvtxRange nvtx("ara_risk_measures_async");
+    if (!c || !ylt || !layers || !rps || !d_out) return fail(ARA_EINVAL, "NULL argument");
+    if (!is_device_ptr(d_out)) return fail(ARA_EINVAL, "d_out must be device memory");
+    return measures_enqueue(c, ylt, n_layers, n_total, n_shards, layers, n_sel, rps, n_rp, d_out);
+}
+
+int ara_risk_measures_batch(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64_t n_total,
+                            uint32_t n_shards, const int32_t *layers, uint32_t n_sel, const double *rps,
+                            uint32_t n_rp, double *pml_out, double *tvar_out, double *var_out) {
+    NvtxRange nvtx("ara_risk_measures_batch");
+    if (!c || !ylt || !layers || !rps || !pml_out || !tvar_out) return fail(ARA_EINVAL, "NULL argument");
+    // one read-back for every table
+    const int st = measures_enqueue(c, ylt, n_layers, n_total, n_shards, layers, n_sel, rps, n_rp, c->ms.d_out);
+    if (st != ARA_OK) return st;
     double *out = c->h_out;
     CU(cudaMemcpyAsync(out, c->ms.d_out, 3 * n_rp * n_sel * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -1371,12 +1394,12 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
     CU(cudaSetDevice(c->device));
     ara_record *d_raw = nullptr;
     BetaRec *d_recs = nullptr;
-    float2 *d_hot = nullptr, *d_cold = nullptr;
+    float2 *d_nodes = nullptr;
     float *d_mu = nullptr, *d_zp = nullptr, *d_ze = nullptr, *d_out = nullptr;
     int code = ARA_OK;
     cudaError_t e = cudaSuccess;
     if (dalloc(&d_raw, n) || dalloc(&d_recs, n) || dalloc(&d_mu, n) || dalloc(&d_zp, n) ||
-        dalloc(&d_ze, n) || dalloc(&d_out, n) || dalloc(&d_hot, n * kHotN) || dalloc(&d_cold, n * kColdN)) {
+        dalloc(&d_ze, n) || dalloc(&d_out, n) || dalloc(&d_nodes, n * kTabNodes + kTabPad)) {
         cudaGetLastError();
         code = fail(ARA_ENOMEM, "device allocation failed");
     } else {
@@ -1385,8 +1408,9 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
         if (!e) e = cudaMemcpyAsync(d_zp, zp, n * sizeof(float), cudaMemcpyHostToDevice, s);
         if (!e) e = cudaMemcpyAsync(d_ze, ze, n * sizeof(float), cudaMemcpyHostToDevice, s);
         if (!e) e = cudaMemsetAsync(c->d_status, 0, sizeof(RunStatus), s);
-        if (!e) { launch_prep_records(d_raw, nullptr, n, d_recs, d_mu, d_hot, d_cold, nullptr, s); e = cudaGetLastError(); }
-        if (!e) e = launch_sample_losses(d_recs, TablePtr{d_hot, d_cold}, d_zp, d_ze, n, (flags & ARA_EXACT) != 0, d_out,
+        if (!e) e = cudaMemsetAsync(d_nodes, 0, (n * kTabNodes + kTabPad) * sizeof(float2), s);
+        if (!e) { launch_prep_records(d_raw, nullptr, n, d_recs, d_mu, d_nodes + kTabPad, nullptr, s); e = cudaGetLastError(); }
+        if (!e) e = launch_sample_losses(d_recs, TablePtr{d_nodes + kTabPad}, d_zp, d_ze, n, (flags & ARA_EXACT) != 0, d_out,
                                          c->d_status, s);
         if (!e) e = cudaMemcpyAsync(loss_out, d_out, n * sizeof(float), cudaMemcpyDeviceToHost, s);
         if (!e) e = cudaMemcpyAsync(c->h_status, c->d_status, sizeof(RunStatus), cudaMemcpyDeviceToHost, s);
@@ -1396,7 +1420,7 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
             code = fail(ARA_ECONVERGE, "beta quantile did not converge for %u samples", c->h_status->nonconverged);
     }
     cudaFree(d_raw); cudaFree(d_recs); cudaFree(d_mu); cudaFree(d_zp); cudaFree(d_ze); cudaFree(d_out);
-    cudaFree(d_hot); cudaFree(d_cold);
+    cudaFree(d_nodes);
     return code;
 }
 

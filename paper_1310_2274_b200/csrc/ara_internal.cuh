@@ -34,23 +34,22 @@ struct LayerInfo {
 //   mode      : kModeTable (quantile table), kModeExact (per-sample fp64
 //               solve), kModeDegenerate (loss = scale)
 // quantile tables: lambda(v) = logit I^-1(Phi(v); a, b) at v = -7.75 + 0.5 j,
-// j = 0..31 (|v| <= 7.48 for the draws of U's grid), stored in two dense
-// arrays per record: the "hot" central nodes j = 8..23 (v in [-3.75, 3.75]:
-// 99.98 % of samples; 128 B = one line per record, the part that stays
-// L2-resident) and the "cold" tail nodes (144 B): j = 23..31 then 0..8, node
-// j at (j + 9) mod 32, so every tail interval's two nodes are adjacent and
-// the boundary nodes 8 and 23 are kept in both arrays
+// j = 0..31 (|v| <= 7.48 for the draws of U's grid), 256 B per record in one
+// array whose first node sits 64 B past a 128-B boundary: each record's
+// central nodes j = 8..23 (v in [-3.75, 3.75], 99.98 % of samples) fill
+// exactly one 128-B line -- the part that stays L2-resident -- and the nodes
+// of any interval are adjacent (one address computation per sample; round 2's
+// separate hot / cold arrays cost a 64-bit select per sample)
 constexpr int kTabNodes = 32;
 constexpr float kTabV0 = -7.75f, kTabH = 0.5f;
-constexpr int kHotJ0 = 8, kHotN = 16, kColdN = 18;
+constexpr int kTabPad = 8;    // float2 before node 0 of record 0 (64 B)
+constexpr float kTabDegenerate = 88.0f;   // every node of a degenerate record's table (G10): x = 1
 struct TablePtr {
-    const float2 *hot;        // [records][kHotN]
-    const float2 *cold;       // [records][kColdN]
+    const float2 *nodes;      // [records][kTabNodes], nodes - kTabPad is 128-B aligned
 };
 // the nodes of interval ti (ti, ti + 1 adjacent) of record rec
 __device__ __forceinline__ const float2 *table_row(const TablePtr &T, uint64_t rec, int ti) {
-    return (unsigned)(ti - kHotJ0) < (unsigned)(kHotN - 1) ? T.hot + rec * kHotN + (ti - kHotJ0)
-                                                          : T.cold + rec * kColdN + ((ti + 9) & 31);
+    return (T.nodes + ti) + rec * kTabNodes;
 }
 
 constexpr uint32_t kModeTable = 0, kModeExact = 1, kModeDegenerate = 2;
@@ -86,7 +85,7 @@ struct PortfolioDev {
     uint32_t n_exact_records; // records without a quantile table (fp64 per-sample solve)
     const uint32_t *bitmap;   // [bitmap_words]
     const BetaRec *recs;      // [input records] (the record store, shared by the groups)
-    TablePtr tables;          // [input records] (lambda, lambda') nodes, hot + cold
+    TablePtr tables;          // [input records] (lambda, lambda') nodes
     const float *rec_mu;      // [input records] mean loss (primary uncertainty)
     const uint32_t *rec_orig; // [n_dev_records] record index within its XELT
     const uint2 *cidx;        // [catalog] (first device record, record count) of each event
@@ -98,6 +97,9 @@ struct PortfolioDev {
     uint32_t occ_lp;          // occurrence losses per event in occ (n_layers rounded up to 1, 2, 4, 8)
     const float *occ;         // [catalog][occ_lp] occurrence loss of each (event, layer) without draws
                               // (lines 6-11 at the mean losses; the primary-uncertainty fast path)
+    const uint32_t *occ_bitmap; // [bitmap_words] as bitmap, but bit set only if some event of the bit has a
+                              // nonzero occurrence loss in some layer (the primary path's filter; a subset
+                              // of the presence bits, so the sentinel event's bit is 0 here too)
     const SlotInfo *slots;    // [n_slots]
     const LayerInfo *layers;  // [n_layers]
 };
@@ -184,6 +186,8 @@ cudaError_t launch_primary(const PrimaryArgs &A, cudaStream_t s, int num_sms);
 void launch_occ_table(const uint2 *cidx, const uint2 *mu_meta, const double *slot_terms,
                       const LayerInfo *layers, uint32_t n_layers, uint32_t lp, uint32_t catalog, float *out,
                       cudaStream_t s);
+void launch_occ_bitmap(const float *occ, uint32_t lp, uint32_t catalog, uint32_t shift, uint32_t words,
+                       uint32_t *out, cudaStream_t s);
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms);
 // ARA_ASYNC overflow plan: exclusive scan of the listed trials' pair counts
 // into pool offsets, as many as fit pool_pairs (status->n_ovf_fit; the rest
@@ -202,7 +206,7 @@ void launch_split_recs(const BetaRec *recs, const uint32_t *rec_src, const uint3
                        const SlotInfo *slots, const float *mu, uint64_t n, SplitRec *out, uint2 *mu_meta,
                        cudaStream_t s);
 void launch_prep_records(const ara_record *raw, const uint32_t *rec_src, uint64_t n,
-                         BetaRec *out, float *out_mu, float2 *hot, float2 *cold,
+                         BetaRec *out, float *out_mu, float2 *nodes,
                          unsigned int *n_exact, cudaStream_t s);
 // Scan every trial of `yet`, or (trial_list != null) only the n_list listed
 // trials.  Without ARA_EXACT the table-only kernel runs and appends to

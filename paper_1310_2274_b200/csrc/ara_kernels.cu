@@ -40,8 +40,7 @@ __device__ double quintic_mid64(float l0, float d0, float l1, float d1, double v
 
 __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const uint32_t *__restrict__ src,
                                     uint64_t n, BetaRec *__restrict__ out, float *__restrict__ out_mu,
-                                    float2 *__restrict__ hot, float2 *__restrict__ cold,
-                                    unsigned int *n_exact) {
+                                    float2 *__restrict__ nodes, unsigned int *n_exact) {
     const double LN_SQRT_2PI = 0.91893853320467274178;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
          t += (uint64_t)gridDim.x * blockDim.x) {
@@ -55,6 +54,11 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
             r.scale = (sigma == 0.0) ? q.mean_loss : (mu == 0.0 ? 0.0f : q.max_loss);
             r.mu_l = 0.0f; r.sd_l = 0.0f; r.mode = kModeDegenerate;
             out[t] = r;
+            // a constant table (lambda = 88, lambda' = 0): the split sampler's
+            // quintic returns 88 exactly and 1 / (1 + 2^(-88 log2 e)) = 1 in fp32
+            // (the power flushes to 0), so its loss is scale * 1 = the loss
+            if (nodes)
+                for (int j = 0; j < kTabNodes; ++j) nodes[t * kTabNodes + j] = make_float2(kTabDegenerate, 0.0f);
             continue;
         }
         const double mub = mu / mx, sb0 = sigma / mx;
@@ -72,7 +76,7 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
         r.mu_l = (float)mu_l;
         r.sd_l = (float)sqrt(trigamma_d(a) + trigamma_d(b));
         r.mode = kModeTable;
-        if (hot) {
+        if (nodes) {
             float2 tab[kTabNodes];
             double lam[kTabNodes], d1[kTabNodes], d2[kTabNodes];
             bool good = true;
@@ -111,9 +115,7 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
                 }
             }
             if (good) {
-                for (int j = 0; j < kHotN; ++j) hot[t * kHotN + j] = tab[kHotJ0 + j];
-                for (int j = 0; j <= kHotJ0; ++j) cold[t * kColdN + ((j + 9) & 31)] = tab[j];
-                for (int j = kHotJ0 + kHotN - 1; j < kTabNodes; ++j) cold[t * kColdN + ((j + 9) & 31)] = tab[j];
+                for (int j = 0; j < kTabNodes; ++j) nodes[t * kTabNodes + j] = tab[j];
             } else {
                 r.mode = kModeExact;
                 if (n_exact) atomicAdd(n_exact, 1u);
@@ -124,12 +126,12 @@ __global__ void prep_records_kernel(const ara_record *__restrict__ raw, const ui
 }
 
 void launch_prep_records(const ara_record *raw, const uint32_t *src, uint64_t n, BetaRec *out,
-                         float *out_mu, float2 *hot, float2 *cold, unsigned int *n_exact, cudaStream_t s) {
+                         float *out_mu, float2 *nodes, unsigned int *n_exact, cudaStream_t s) {
     if (n == 0) return;
     const int threads = 128;
     const uint64_t blocks = (n + threads - 1) / threads;
     prep_records_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), threads, 0, s>>>(
-        raw, src, n, out, out_mu, hot, cold, n_exact);
+        raw, src, n, out, out_mu, nodes, n_exact);
 }
 
 // ---------------------------------------------------------------------------
@@ -287,7 +289,7 @@ __device__ __noinline__ int flush_queue(const SampleArgs G, const WarpMem M, uin
             int ti[U];
             float tt[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {       // table rows (hot centre / cold tails)
+            for (int u = 0; u < U; ++u) {       // table rows
                 const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
                 ti[u] = min((int)uu, kTabNodes - 2);
                 tt[u] = uu - (float)ti[u];

@@ -75,6 +75,33 @@ void launch_occ_table(const uint2 *cidx, const uint2 *mu_meta, const double *slo
         cidx, mu_meta, slot_terms, layers, n_layers, lp, catalog, out);
 }
 
+// occ_bitmap bit b = some event e of the bit (e >> shift == b, e < catalog) has
+// a nonzero occurrence loss in some layer.  An event whose occurrence losses
+// are all 0 adds exactly 0 to every trial sum (and to no occurrence maximum),
+// so the primary path may skip it like an absent one: the YLT is unchanged
+// bit for bit, and the gathers drop to the events that carry a loss (cfg2:
+// the occurrence retention zeroes ~40 % of the present events).
+__global__ void occ_bitmap_kernel(const float *__restrict__ occ, uint32_t lp, uint32_t catalog, uint32_t shift,
+                                  uint32_t words, uint32_t *__restrict__ out) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+        uint32_t m = 0;
+        for (uint32_t b = 0; b < 32; ++b) {
+            const uint64_t e0 = ((uint64_t)w * 32 + b) << shift, e1 = (((uint64_t)w * 32 + b + 1) << shift);
+            bool nz = false;
+            for (uint64_t e = e0; e < e1 && e < catalog && !nz; ++e)
+                for (uint32_t l = 0; l < lp; ++l) nz = nz || occ[e * lp + l] != 0.0f;
+            m |= (nz ? 1u : 0u) << b;
+        }
+        out[w] = m;
+    }
+}
+
+void launch_occ_bitmap(const float *occ, uint32_t lp, uint32_t catalog, uint32_t shift, uint32_t words,
+                       uint32_t *out, cudaStream_t s) {
+    if (words == 0) return;
+    occ_bitmap_kernel<<<(words + 255) / 256, 256, 0, s>>>(occ, lp, catalog, shift, words, out);
+}
+
 // ---------------------------------------------------------------------------
 // primary_kernel: one warp per trial (dynamic scheduler), one CTA of 32 warps
 // per SM with the presence bitmap in shared memory.  Per 128-event chunk one
@@ -103,6 +130,135 @@ __device__ __forceinline__ void load_occ(bool p, const float *src, float (&g)[LP
     }
 }
 
+// One or two layers: the warp walks the flat sequence of 128-event chunks of
+// the trials it claims as a register pipeline (as compact_kernel does), so the
+// loss gathers of chunk c+1 and the id loads of chunks c+2, c+3 are in flight
+// while chunk c is summed; a trial's sums are reduced and written after its
+// last chunk.  (The per-trial loop below keeps one chunk of ids and no gathers
+// in flight: it waited on L2 latency once per chunk.)
+struct PrimRaw {
+    uint4 v;
+    uint32_t t, c, len;             // trial (kNoTrial: none), chunk, trial length
+};
+template <int LP>
+struct PrimG {
+    float g[4][LP];
+    uint32_t t, c, len;
+};
+constexpr uint32_t kNoTrial = 0xffffffffu;
+
+template <int LP, int BM, bool OM>
+__device__ __forceinline__ void primary_flat(const PrimaryArgs &A, const uint32_t *bitmap) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t shift = A.pf.bitmap_shift, nl = A.pf.n_layers;
+    const uint64_t n_trials = A.yet.n_trials;
+    const uint32_t *events = A.yet.events;
+    const uint64_t *offsets = A.yet.offsets;
+    const uint32_t K = A.yet.fixed_len;
+    const bool vec = offsets == nullptr && (K & 3u) == 0;
+    const uint32_t sent = BM == 2 ? 0u : A.pf.sentinel_event;
+    const float *__restrict__ occ = A.occ;
+
+    uint32_t pt = kNoTrial, pc = 0, plen = 0;       // fetch side (warp-uniform)
+    uint64_t pbase = 0;
+    auto next_trial = [&]() {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(A.sched, 1ull);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        pt = t < n_trials ? (uint32_t)t : kNoTrial;
+        pc = 0;
+        if (pt != kNoTrial) {
+            if (offsets) { pbase = offsets[pt]; plen = (uint32_t)(offsets[pt + 1] - pbase); }
+            else { pbase = (uint64_t)pt * K; plen = K; }
+            if (plen == 0) {                          // empty trial: S = 0 (YLT = the clip of 0)
+                if (lane == 0)
+                    for (uint32_t l = 0; l < nl; ++l) {
+                        const LayerInfo &L = A.pf.layers[l];
+                        A.ylt[(uint64_t)l * n_trials + pt] = (float)clip64(0.0 - L.agg_r, L.agg_l);
+                        if (OM) A.occ_max[(uint64_t)l * n_trials + pt] = 0.0f;
+                    }
+            }
+        }
+    };
+    auto fetch = [&](PrimRaw &r) {
+        while (pt != kNoTrial && plen == 0) next_trial();
+        r.t = pt; r.c = pc; r.len = pt != kNoTrial ? plen : 0u;
+        r.v = make_uint4(sent, sent, sent, sent);
+        if (pt != kNoTrial) {
+            const uint32_t k = pc * 128u + 4u * lane;
+            const uint32_t *src = events + pbase + k;
+            if (vec) {
+                if (k < plen) r.v = __ldcs(reinterpret_cast<const uint4 *>(src));
+            } else {
+                if (k < plen) r.v.x = __ldcs(src);
+                if (k + 1 < plen) r.v.y = __ldcs(src + 1);
+                if (k + 2 < plen) r.v.z = __ldcs(src + 2);
+                if (k + 3 < plen) r.v.w = __ldcs(src + 3);
+            }
+            if ((pc + 1) * 128u >= plen) next_trial();
+            else ++pc;
+        }
+    };
+    auto stage_a = [&](const PrimRaw &r, PrimG<LP> &G) {      // bitmap, gathers issued
+        G.t = r.t; G.c = r.c; G.len = r.len;
+        const uint32_t k0 = r.c * 128u + 4u * lane;
+        const uint32_t ee[4] = {r.v.x, r.v.y, r.v.z, r.v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t bit = BM == 0 ? ee[q] : ee[q] >> shift;
+            bool hit = __funnelshift_r(bitmap[bit >> 5], 0u, bit) & 1u;
+            if (BM == 2) hit = hit && k0 + q < r.len;
+            load_occ<LP>(hit, occ + (uint64_t)ee[q] * LP, G.g[q]);
+        }
+    };
+    double S[LP];
+    float M[LP];
+    auto stage_b = [&](const PrimG<LP> &G) {                 // sums; the trial's end -> YLT
+        if (G.c == 0) {
+#pragma unroll
+            for (int l = 0; l < LP; ++l) { S[l] = 0.0; M[l] = 0.0f; }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int l = 0; l < LP; ++l) {
+                S[l] += (double)G.g[q][l];               // line 12's trial sum, occurrence order per lane
+                if (OM) M[l] = fmaxf(M[l], G.g[q][l]);
+            }
+        if ((G.c + 1) * 128u >= G.len) {
+#pragma unroll
+            for (int l = 0; l < LP; ++l) {
+                double s = S[l];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                unsigned mb = 0;
+                if (OM) mb = __reduce_max_sync(0xffffffffu, __float_as_uint(M[l]));
+                if (lane == 0 && (uint32_t)l < nl) {
+                    const LayerInfo &L = A.pf.layers[l];
+                    A.ylt[(uint64_t)l * n_trials + G.t] = (float)clip64(s - L.agg_r, L.agg_l);
+                    if (OM) A.occ_max[(uint64_t)l * n_trials + G.t] = __uint_as_float(mb);
+                }
+            }
+        }
+    };
+    next_trial();
+    PrimRaw ra, rb;
+    PrimG<LP> ga, gb;
+    fetch(ra);
+    fetch(rb);
+    stage_a(ra, ga);
+    fetch(ra);
+    while (ga.t != kNoTrial) {
+        stage_a(rb, gb);
+        fetch(rb);
+        stage_b(ga);
+        if (gb.t == kNoTrial) break;
+        stage_a(ra, ga);
+        fetch(ra);
+        stage_b(gb);
+    }
+}
+
 template <int LP, int BM, bool OM>
 __global__ void __launch_bounds__(kPrimaryWarps * 32, 1) primary_kernel(const __grid_constant__ PrimaryArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -112,8 +268,12 @@ __global__ void __launch_bounds__(kPrimaryWarps * 32, 1) primary_kernel(const __
         return;
     }
     for (uint32_t t = threadIdx.x; t <= A.pf.bitmap_words; t += blockDim.x)   // + one zero word (sentinel)
-        bitmap[t] = t < A.pf.bitmap_words ? A.pf.bitmap[t] : 0u;
+        bitmap[t] = t < A.pf.bitmap_words ? A.pf.occ_bitmap[t] : 0u;   // nonzero losses only
     __syncthreads();
+    if constexpr (LP == 1 || (LP == 2 && !OM)) {      // (registers: LP 2 with occ_max would spill)
+        primary_flat<LP, BM, OM>(A, bitmap);
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const uint32_t shift = A.pf.bitmap_shift, nl = A.pf.n_layers;
     const uint64_t n_trials = A.yet.n_trials;

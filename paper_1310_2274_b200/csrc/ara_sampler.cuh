@@ -32,11 +32,12 @@
 namespace ara {
 
 // ------------------------------------------------- fast fp32 intrinsics ---
-// MUFU approximations with flush-to-zero: the sampler only feeds them normal
-// arguments with normal results (the node sigmoids clamp lambda to +-80, the
-// erfinv log's argument is >= 2^-23, reciprocals are of 1 + e >= 1), where
-// the .ftz forms return exactly what __expf / __logf / __fdividef return --
-// without the subnormal fix-ups those emit (3 instructions each)
+// MUFU approximations with flush-to-zero: the sampler feeds them normal
+// arguments (the erfinv log's argument is >= 2^-23, reciprocals are of
+// 1 + e >= 1), where the .ftz forms return exactly what __expf / __logf /
+// __fdividef return -- without the subnormal fix-ups those emit (3
+// instructions each); a sigmoid's power that overflows to +inf or flushes to
+// 0 gives x = 0 or 1, its limits
 __device__ __forceinline__ float ex2_ftz(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -232,10 +233,10 @@ __device__ __forceinline__ double lambda_exact64(double v, double a, double b, d
 
 // ------------------------------------------------------------ table eval --
 
-// x = 1/(1 + e^-lambda) at a table node (lambda clamped to +-80: normal MUFU operands)
+// x = 1/(1 + e^-lambda) at a table node: e^-lambda overflows to +inf for
+// lambda < -88.7 (rcp(inf) = +0: x = 0) and flushes to 0 above 87.3 (x = 1)
 __device__ __forceinline__ float sigmoid_node(float lam) {
-    const float l = fminf(fmaxf(lam, -80.0f), 80.0f);
-    return rcp_ftz(1.0f + ex2_ftz(-1.44269504088896340736f * l));
+    return rcp_ftz(1.0f + ex2_ftz(-1.44269504088896340736f * lam));
 }
 
 // quintic Hermite on [v_i, v_i + h] from the two nodes' (lambda, lambda'),
@@ -275,10 +276,9 @@ __device__ __forceinline__ float lambda_table(const TablePtr &tables, uint64_t r
 }
 
 __device__ __forceinline__ float sigmoidf_(float lam) {
-    // 1/(1+e^-lam); e^-lam = inf for lam < -88 gives 0 (the loss underflows to 0);
-    // e^-lam below 2^-126 flushes to 0, where 1/(1+e) is 1 either way
-    const float e = ex2_ftz(-1.44269504088896340736f * lam);
-    return e < 3.0e38f ? rcp_ftz(1.0f + e) : 0.0f;
+    // 1/(1+e^-lam); e^-lam = inf for lam < -88.7 gives rcp(inf) = +0 (the loss
+    // underflows to 0); e^-lam below 2^-126 flushes to 0, where 1/(1+e) is 1 either way
+    return rcp_ftz(1.0f + ex2_ftz(-1.44269504088896340736f * lam));
 }
 
 // Per-sample fp64 solve (table-less records, ARA_EXACT); kept out of line so

@@ -78,6 +78,13 @@ template <class T>
 __device__ __forceinline__ T xl_clip_t_(T d, T lim) {
     return d > (T)0 ? (d < lim ? d : lim) : (T)0;
 }
+// p ? a : 0 in one SEL the optimiser keeps on the fp32 value (written plainly,
+// the select is moved past the widening conversion and doubled)
+__device__ __forceinline__ float sel_f32_(bool p, float a) {
+    float r;
+    asm("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n selp.f32 %0, %1, 0f00000000, q;\n}" : "=f"(r) : "f"(a), "r"((uint32_t)p));
+    return r;
+}
 __device__ __forceinline__ double warp_sum_f64_(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -468,20 +475,17 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const uint32_t mode = meta[u] >> 28;
-                    if (mode == kModeTable) {
-                        const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
-                        const int ti = min((int)uu, kTabNodes - 2);
-                        const float tt = uu - (float)ti;
-                        const float2 *row = table_row(tables, r[u].tab, ti);
-                        x[u] = r[u].scale * sigmoidf_(quintic_from_nodes(__ldg(row), __ldg(row + 1), ti, tt,
-                                                                         r[u].a, r[u].b));
-                    } else if (mode == kModeDegenerate) {
-                        x[u] = r[u].scale;
-                    } else {
-                        x[u] = 0.0f;              // table-less record: trial redone in fp64
-                        redo |= live[u];
-                    }
+                    // every record has a table: degenerate records (G10) a constant
+                    // one whose value is exactly scale (prep_records_kernel); a
+                    // table-less record (mode exact) reads zeros and its trial is
+                    // redone in fp64 -- no branch per sample
+                    const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
+                    const int ti = min((int)uu, kTabNodes - 2);
+                    const float tt = uu - (float)ti;
+                    const float2 *row = table_row(tables, r[u].tab, ti);
+                    x[u] = r[u].scale * sigmoidf_(quintic_from_nodes(__ldg(row), __ldg(row + 1), ti, tt,
+                                                                     r[u].a, r[u].b));
+                    redo |= live[u] && (meta[u] >> 28) == kModeExact;
                 }
             } else {
 #pragma unroll
@@ -532,15 +536,16 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
             const bool end = (q >> 31) != 0u;
             const uint32_t lay = SL ? 0u : (uint32_t)fl[i];
             const RunT orr = SL ? occ_r0 : (RunT)layers[lay].occ_r, oll = SL ? occ_l0 : (RunT)layers[lay].occ_l;
-            const double g = (double)xl_clip_t_(o - orr, oll);
+            const RunT gr = xl_clip_t_(o - orr, oll);   // (fp32: the run's clip, G28)
             const bool first = end && !has_end, inner = end && has_end;
             head = first ? o : head;
             head_layer = first ? lay : head_layer;
-            if (SL) acc += inner ? g : 0.0;
-            else if (inner) accs[lay * 32] += g;
+            // (the select on the fp32 value, then one widening add: acc + 0.0 = acc)
+            if (SL) acc += (double)sel_f32_(inner, gr);
+            else if (inner) accs[lay * 32] += (double)gr;
             if (OM) {                                  // OEP basis (G29); fp32 rounding is monotone
-                if (SL) mo = fmaxf(mo, inner ? (float)g : 0.0f);
-                else if (inner) W.mos[lay * 32] = fmaxf(W.mos[lay * 32], (float)g);
+                if (SL) mo = fmaxf(mo, inner ? (float)gr : 0.0f);
+                else if (inner) W.mos[lay * 32] = fmaxf(W.mos[lay * 32], (float)gr);
             }
             has_end = has_end || end;
             o = end ? (RunT)0 : o;
@@ -609,13 +614,20 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 32 / kSampleWarps)   // <= 
     sample_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t nl = A.pf.n_layers;
+    // carved by byte offsets from the shared base (no integer round trip), so
+    // every pointer below stays in the shared address space (LDS / STS)
+    size_t o = 0;
     SlotInfo *slots = reinterpret_cast<SlotInfo *>(smem);
-    LayerInfo *layers = reinterpret_cast<LayerInfo *>(slots + ARA_MAX_SLOTS);
-    double *accw = reinterpret_cast<double *>(layers + ARA_MAX_LAYERS);                       // [warps][nl][32]
-    unsigned int *cw = reinterpret_cast<unsigned int *>(accw + kSampleWarps * nl * 32);
-    unsigned long long *hw = reinterpret_cast<unsigned long long *>(
-        ((uintptr_t)(cw + kSampleWarps * nl) + 7) & ~(uintptr_t)7);            // [warps][nl]
-    float *mow = reinterpret_cast<float *>(hw + kSampleWarps * nl);             // OM && !SL: [warps][nl][32]
+    o += ARA_MAX_SLOTS * sizeof(SlotInfo);
+    LayerInfo *layers = reinterpret_cast<LayerInfo *>(smem + o);
+    o += ARA_MAX_LAYERS * sizeof(LayerInfo);
+    double *accw = reinterpret_cast<double *>(smem + o);                        // [warps][nl][32]
+    o += kSampleWarps * nl * 32 * sizeof(double);
+    unsigned int *cw = reinterpret_cast<unsigned int *>(smem + o);              // [warps][nl]
+    o += (kSampleWarps * nl * sizeof(unsigned int) + 7) & ~(size_t)7;
+    unsigned long long *hw = reinterpret_cast<unsigned long long *>(smem + o);  // [warps][nl]
+    o += kSampleWarps * nl * sizeof(unsigned long long);
+    float *mow = reinterpret_cast<float *>(smem + o);                           // OM && !SL: [warps][nl][32]
     if (A.n_items_dev && *A.n_items_dev == 0) return; // a device-sized pass with nothing to do
     for (uint32_t t = threadIdx.x; t < A.pf.n_slots; t += blockDim.x) slots[t] = A.pf.slots[t];
     for (uint32_t t = threadIdx.x; t < nl; t += blockDim.x) layers[t] = A.pf.layers[t];

@@ -945,6 +945,25 @@ def test_measures_batch_equals_single_calls(A, ctx):
         assert np.array_equal(pml[i], p1) and np.array_equal(tvar[i], t1) and np.array_equal(var[i], v1)
 
 
+def test_measures_async_equals_batch(A, ctx):
+    # ara_risk_measures_async (device output, no sync) == the batched call, bit
+    # for bit, also when queued behind other work and reused across calls
+    import torch
+    rng = np.random.default_rng(22)
+    L, n, P = 3, 90000, 2
+    layers = [0, -1, 2]
+    out = torch.empty((len(layers), 3, 3), dtype=torch.float64, device="cuda")
+    for rep in range(3):
+        y = torch.from_numpy(rng.lognormal(13 + rep, 1, (P, L, n // P)).astype(np.float32)).cuda()
+        A.risk_measures_async(ctx, y, L, n, layers, rps=(100, 250, 500), n_shards=P, out=out)
+        torch.cuda.synchronize()
+        pml, tvar, var = A.risk_measures_batch(ctx, y, L, n, layers, rps=(100, 250, 500), n_shards=P)
+        o = out.cpu().numpy()
+        assert np.array_equal(o[:, :, 0], pml) and np.array_equal(o[:, :, 1], tvar) and np.array_equal(o[:, :, 2], var)
+    with pytest.raises(A.AraError):                   # host output buffer
+        A.risk_measures_async(ctx, y, L, n, layers, out=np.zeros((3, 3, 3)))
+
+
 def test_batch_and_curve_errors(A, ctx):
     import torch
     y = torch.ones((2, 100), dtype=torch.float32, device="cuda")

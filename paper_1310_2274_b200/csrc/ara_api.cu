@@ -254,7 +254,8 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
         dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 4 * 256) != cudaSuccess ||
         dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
         dalloc(&c->ms.d_out, kOutDoubles) != cudaSuccess ||
-        dalloc(&c->ms.mhist, 4 * kMaxPlanRanks * 256) != cudaSuccess || dalloc(&c->ms.macc, 8) != cudaSuccess || dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
+        dalloc(&c->ms.mhist, 4 * kMaxPlanRanks * 256) != cudaSuccess || dalloc(&c->ms.macc, 8) != cudaSuccess ||
+        dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
         dalloc(&c->ms.part_sum, kRedBlocks) != cudaSuccess ||
         dalloc(&c->ms.part_cnt, kRedBlocks) != cudaSuccess || cudaEventCreate(&c->ev[0]) != cudaSuccess ||
         cudaEventCreate(&c->ev[1]) != cudaSuccess || cudaEventCreate(&c->ev[2]) != cudaSuccess ||

@@ -7,7 +7,6 @@
 // descending order statistics at r = (N+1)/RP; TVaR is the mean of all
 // losses >= VaR = L(ceil(N/RP)).
 #include <algorithm>
-#include <cstdlib>
 #include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -209,10 +208,6 @@ __global__ void __launch_bounds__(256) select_coop_kernel(const float *ylt, uint
 #define ARA_MULTI_THREADS 1024
 #endif
 constexpr int kMultiThreads = ARA_MULTI_THREADS;     // one block per SM: cheap grid barriers
-#ifndef ARA_MEAS_PER_BLOCK
-#define ARA_MEAS_PER_BLOCK 0
-#endif
-constexpr uint64_t kMeasPerBlock = ARA_MEAS_PER_BLOCK;   // entries per block of the joint select (0: one block per SM)
 
 struct __align__(8) MeasPlan {
     uint64_t rank[kMaxPlanRanks];                  // distinct ranks (1-based, descending order)
@@ -402,18 +397,9 @@ cudaError_t launch_measures_multi(const float *ylt, uint32_t n_layers, uint64_t 
     unsigned int *hist = S.mhist;
     unsigned long long *acc = S.macc;
     uint64_t nt = n_total;
-    // the grid: enough blocks for ~kMeasPerBlock entries each, at most one per
-    // SM -- every pass ends in a grid-wide barrier whose cost grows with the
-    // block count, while a block streams its share of an L2-resident table fast
-    static const uint64_t per_block = [] {                 // (test aid: ARA_MEAS_PER_BLOCK overrides)
-        const char *e = getenv("ARA_MEAS_PER_BLOCK");
-        return e && *e ? (uint64_t)strtoull(e, nullptr, 10) : kMeasPerBlock;
-    }();
-    const uint64_t want = per_block ? (n_total + per_block - 1) / per_block : (uint64_t)blocks;
-    const int nb = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)blocks, want));
     void *args[] = {(void *)&ylt, (void *)&n_layers, (void *)&per, (void *)&n_shards, (void *)&layer,
                     (void *)&vals, (void *)&M, (void *)&hist, (void *)&acc, (void *)&nt, (void *)&d_out};
-    return cudaLaunchCooperativeKernel((void *)select_multi_kernel, dim3(nb), dim3(kMultiThreads), args, 0, s);
+    return cudaLaunchCooperativeKernel((void *)select_multi_kernel, dim3(blocks), dim3(kMultiThreads), args, 0, s);
 }
 
 // one CTA of 1024 threads: bitonic sort (descending) of P = 1024 E values,

@@ -87,10 +87,12 @@ __device__ __forceinline__ float u01_from_bits(uint32_t x) {
 __device__ __forceinline__ float norm_quantile_from_bits(uint32_t x) {
     const int yi = (int)((x >> 9) << 1) + 1 - (1 << 23);
     const float y = (float)yi * 1.1920928955078125e-07f;      // exact
-    float w = -0.69314718055994530942f * lg2_ftz((1.0f - y) * (1.0f + y));   // -ln((1-y)(1+y))
+    // 1 - y^2 by one fma: the exact product rounded once, the same value as
+    // (1 - y)(1 + y) (both factors exact on U's grid); w - 2.5 = -ln(1 - y^2) - 2.5 in one fma
+    const float l = lg2_ftz(fmaf(-y, y, 1.0f));
+    float w = fmaf(l, -0.69314718055994530942f, -2.5f);     // w - 2.5
     float p;                                                  // sqrt(2) x Giles' coefficients
-    if (w < 5.0f) {
-        w = w - 2.5f;
+    if (w < 2.5f) {
         p = 3.974260232e-08f;
         p = fmaf(p, w, 4.854626601e-07f);
         p = fmaf(p, w, -4.982822671e-06f);
@@ -101,7 +103,7 @@ __device__ __forceinline__ float norm_quantile_from_bits(uint32_t x) {
         p = fmaf(p, w, 3.488026612e-01f);
         p = fmaf(p, w, 2.123313550e+00f);
     } else {
-        w = sqrtf(w) - 3.0f;
+        w = sqrtf(w + 2.5f) - 3.0f;
         p = -2.831457176e-04f;
         p = fmaf(p, w, 1.427656483e-04f);
         p = fmaf(p, w, 1.908259482e-03f);

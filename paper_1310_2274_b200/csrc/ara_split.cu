@@ -166,10 +166,13 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
     uint32_t pt = kNoItem;
     uint32_t pc = 0, plen = 0;
     uint64_t pbase = 0;
-    auto next_item = [&]() {                          // claim the next item of the launch
-        uint32_t i = 0;
-        if (lane == 0) i = (uint32_t)atomicAdd(A.sched, 1ull);
-        i = __shfl_sync(0xffffffffu, i, 0);
+    // items are claimed one ahead (lane 0's atomic for the next item in flight
+    // while this one streams); a claimed item is always the claiming warp's next
+    uint32_t claim = 0;
+    if (lane == 0) claim = (uint32_t)atomicAdd(A.sched, 1ull);
+    auto next_item = [&]() {                          // start the claimed item, claim the next
+        const uint32_t i = __shfl_sync(0xffffffffu, claim, 0);
+        if (lane == 0 && i < n_items) claim = (uint32_t)atomicAdd(A.sched, 1ull);
         pt = i < n_items ? i : kNoItem;
         pc = 0;
         if (pt != kNoItem) {

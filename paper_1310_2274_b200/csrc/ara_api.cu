@@ -186,6 +186,7 @@ struct ara_portfolio {
     PortfolioDev dev{};
     uint32_t *d_bitmap = nullptr, *d_rec_orig = nullptr;
     uint2 *d_cidx = nullptr;
+    uint32_t *d_cidx4 = nullptr;       // [C] packed index entries (compaction), if every first < 2^24
     SplitRec *d_srecs = nullptr;
     uint2 *d_mm = nullptr;             // (mean loss bits, meta) per device record (primary uncertainty)
     std::shared_ptr<RecordStore> store;   // per input record (shared by the groups)
@@ -609,7 +610,8 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
         return code;
     };
     if (dalloc(&p->d_bitmap, words) ||
-        dalloc(&p->d_cidx, (size_t)C) || dalloc(&d_rec_meta, (size_t)total) || dalloc(&p->d_srecs, (size_t)total) ||
+        dalloc(&p->d_cidx, (size_t)C) || (total < (1ull << 24) && dalloc(&p->d_cidx4, (size_t)C)) ||
+        dalloc(&d_rec_meta, (size_t)total) || dalloc(&p->d_srecs, (size_t)total) ||
         dalloc(&p->d_mm, (size_t)total) || dalloc(&p->d_rec_orig, total) || dalloc(&d_rec_src, total) ||
         dalloc(&p->d_slots, S) || dalloc(&p->d_layers, n_layers) ||
         dalloc(&p->d_occ, (size_t)C * occ_lp) || dalloc(&p->d_occ_bitmap, words) ||
@@ -622,6 +624,12 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     UP(p->d_bitmap, bitmap.data(), (size_t)words);
     UP(p->d_rec_orig, rec_orig.data(), (size_t)total);
     UP(p->d_cidx, cidx.data(), (size_t)C);
+    std::vector<uint32_t> cidx4;
+    if (p->d_cidx4) {                                   // first | count << 24 (count <= ARA_MAX_SLOTS < 256)
+        cidx4.resize(C);
+        for (uint32_t e = 0; e < C; ++e) cidx4[e] = cidx[e].x | (cidx[e].y << 24);
+        UP(p->d_cidx4, cidx4.data(), (size_t)C);
+    }
     UP(d_rec_meta, rec_meta.data(), (size_t)total);
     UP(p->d_slots, slots.data(), (size_t)S);
     UP(p->d_layers, layers.data(), (size_t)n_layers);
@@ -662,7 +670,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     d.bitmap = p->d_bitmap; d.recs = store->d_recs; d.rec_mu = store->d_mu;
     d.tables = TablePtr{store->d_nodes + kTabPad};
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;
-    d.cidx = p->d_cidx; d.srecs = p->d_srecs; d.mu_meta = p->d_mm;
+    d.cidx = p->d_cidx; d.cidx4 = p->d_cidx4; d.srecs = p->d_srecs; d.mu_meta = p->d_mm;
     d.any_terms = et ? 1u : 0u;
     p->rec_src = std::move(rec_src);
     p->n_input_records = eoff[n_elts];
@@ -677,7 +685,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
 
 static uint64_t group_bytes(const ara_portfolio *g) {          // per-group arrays (not the record store)
     const PortfolioDev &d = g->dev;
-    return (uint64_t)d.catalog * (sizeof(uint2) + d.occ_lp * sizeof(float)) +
+    return (uint64_t)d.catalog * (sizeof(uint2) + (d.cidx4 ? 4 : 0) + d.occ_lp * sizeof(float)) +
            (uint64_t)d.bitmap_words * 8 +
            d.n_dev_records * (sizeof(SplitRec) + sizeof(uint2) + sizeof(uint32_t)) +
            d.n_slots * (sizeof(SlotInfo) + 4 * sizeof(double)) + d.n_layers * sizeof(LayerInfo);
@@ -706,7 +714,7 @@ void ara_portfolio_destroy(ara_portfolio *p) {
     for (ara_portfolio *g : p->groups) ara_portfolio_destroy(g);
     if (p->ctx) cudaSetDevice(p->ctx->device);
     cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig);
-    cudaFree(p->d_cidx); cudaFree(p->d_srecs); cudaFree(p->d_mm);
+    cudaFree(p->d_cidx); cudaFree(p->d_cidx4); cudaFree(p->d_srecs); cudaFree(p->d_mm);
     cudaFree(p->d_slots); cudaFree(p->d_layers);
     cudaFree(p->d_occ); cudaFree(p->d_occ_bitmap); cudaFree(p->d_slot_terms); cudaFree(p->d_rec_z);
     delete p;

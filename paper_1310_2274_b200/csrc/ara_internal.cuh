@@ -89,6 +89,7 @@ struct PortfolioDev {
     const float *rec_mu;      // [input records] mean loss (primary uncertainty)
     const uint32_t *rec_orig; // [n_dev_records] record index within its XELT
     const uint2 *cidx;        // [catalog] (first device record, record count) of each event
+    const uint32_t *cidx4;    // [catalog] the same packed as first | count << 24, or null (>= 2^24 device records)
     const SplitRec *srecs;    // [n_dev_records]
     const uint2 *mu_meta;     // [n_dev_records] (mean loss bits, meta = slot | run_end << 8 | layer << 16):
                               // one 8 B gather per pair with SU off

@@ -147,7 +147,11 @@ struct PrimG {
 };
 constexpr uint32_t kNoTrial = 0xffffffffu;
 
-template <int LP, int BM, bool OM>
+// VEC: fixed-length trials, K % 4 == 0, K > 0: trials assigned to the warps
+// round-robin (equal work per trial; a claim's atomic round trip at every
+// trial start stalled the warp: 18 % of the stall samples), one uint4 per lane
+// from a per-trial pointer.  Else the dynamic scheduler and per-id loads.
+template <int LP, int BM, bool OM, bool VEC>
 __device__ __forceinline__ void primary_flat(const PrimaryArgs &A, const uint32_t *bitmap) {
     const int lane = threadIdx.x & 31;
     const uint32_t shift = A.pf.bitmap_shift, nl = A.pf.n_layers;
@@ -155,25 +159,34 @@ __device__ __forceinline__ void primary_flat(const PrimaryArgs &A, const uint32_
     const uint32_t *events = A.yet.events;
     const uint64_t *offsets = A.yet.offsets;
     const uint32_t K = A.yet.fixed_len;
-    const bool vec = offsets == nullptr && (K & 3u) == 0;
     const uint32_t sent = BM == 2 ? 0u : A.pf.sentinel_event;
     const float *__restrict__ occ = A.occ;
 
-    uint32_t pt = kNoTrial, pc = 0, plen = 0;       // fetch side (warp-uniform)
+    uint32_t pt = kNoTrial, pc = 0, plen = 0;       // fetch side (warp-uniform; plen 0 without a trial)
     uint64_t pbase = 0;
-    // (claiming the next trial one ahead measured slower: 0.139 -> 0.143 ms
-    // at cfg2, ~21 trials per warp, so the end-of-launch imbalance it adds
-    // costs more than the claim latency it hides)
+    const uint4 *psrc = nullptr;                    // VEC: this lane's uint4 of the trial's chunk 0
+    // VEC: this warp's next trial (round-robin over the grid's warps)
+    uint64_t next_t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint64_t n_warps = gridDim.x * (uint64_t)(blockDim.x >> 5);
+    // (dynamic: claiming the next trial one ahead measured slower -- 0.139 ->
+    // 0.143 ms at cfg2, the end-of-launch imbalance it adds)
     auto next_trial = [&]() {
         unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(A.sched, 1ull);
-        t = __shfl_sync(0xffffffffu, t, 0);
+        if (VEC) {
+            t = next_t;
+            next_t += n_warps;
+        } else {
+            if (lane == 0) t = atomicAdd(A.sched, 1ull);
+            t = __shfl_sync(0xffffffffu, t, 0);
+        }
         pt = t < n_trials ? (uint32_t)t : kNoTrial;
         pc = 0;
+        plen = 0;
         if (pt != kNoTrial) {
-            if (offsets) { pbase = offsets[pt]; plen = (uint32_t)(offsets[pt + 1] - pbase); }
+            if (VEC) { pbase = (uint64_t)pt * K; plen = K; psrc = reinterpret_cast<const uint4 *>(events + pbase) + lane; }
+            else if (offsets) { pbase = offsets[pt]; plen = (uint32_t)(offsets[pt + 1] - pbase); }
             else { pbase = (uint64_t)pt * K; plen = K; }
-            if (plen == 0) {                          // empty trial: S = 0 (YLT = the clip of 0)
+            if (!VEC && plen == 0) {                          // empty trial: S = 0 (YLT = the clip of 0)
                 if (lane == 0)
                     for (uint32_t l = 0; l < nl; ++l) {
                         const LayerInfo &L = A.pf.layers[l];
@@ -184,20 +197,21 @@ __device__ __forceinline__ void primary_flat(const PrimaryArgs &A, const uint32_
         }
     };
     auto fetch = [&](PrimRaw &r) {
-        while (pt != kNoTrial && plen == 0) next_trial();
-        r.t = pt; r.c = pc; r.len = pt != kNoTrial ? plen : 0u;
+        if (!VEC)
+            while (pt != kNoTrial && plen == 0) next_trial();
+        r.t = pt; r.c = pc; r.len = plen;
         r.v = make_uint4(sent, sent, sent, sent);
-        if (pt != kNoTrial) {
-            const uint32_t k = pc * 128u + 4u * lane;
+        const uint32_t k = pc * 128u + 4u * lane;
+        if (VEC) {
+            if (k < plen) r.v = __ldcs(psrc + pc * 32u);
+        } else if (pt != kNoTrial) {
             const uint32_t *src = events + pbase + k;
-            if (vec) {
-                if (k < plen) r.v = __ldcs(reinterpret_cast<const uint4 *>(src));
-            } else {
-                if (k < plen) r.v.x = __ldcs(src);
-                if (k + 1 < plen) r.v.y = __ldcs(src + 1);
-                if (k + 2 < plen) r.v.z = __ldcs(src + 2);
-                if (k + 3 < plen) r.v.w = __ldcs(src + 3);
-            }
+            if (k < plen) r.v.x = __ldcs(src);
+            if (k + 1 < plen) r.v.y = __ldcs(src + 1);
+            if (k + 2 < plen) r.v.z = __ldcs(src + 2);
+            if (k + 3 < plen) r.v.w = __ldcs(src + 3);
+        }
+        if (pt != kNoTrial) {
             if ((pc + 1) * 128u >= plen) next_trial();
             else ++pc;
         }
@@ -274,7 +288,10 @@ __global__ void __launch_bounds__(kPrimaryWarps * 32, 1) primary_kernel(const __
         bitmap[t] = t < A.pf.bitmap_words ? A.pf.occ_bitmap[t] : 0u;   // nonzero losses only
     __syncthreads();
     if constexpr (LP == 1 || (LP == 2 && !OM)) {      // (registers: LP 2 with occ_max would spill)
-        primary_flat<LP, BM, OM>(A, bitmap);
+        if (A.yet.offsets == nullptr && A.yet.fixed_len > 0 && (A.yet.fixed_len & 3u) == 0)
+            primary_flat<LP, BM, OM, true>(A, bitmap);
+        else
+            primary_flat<LP, BM, OM, false>(A, bitmap);
         return;
     }
     const int lane = threadIdx.x & 31;

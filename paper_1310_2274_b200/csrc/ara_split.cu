@@ -118,9 +118,24 @@ struct RawChunk {
     uint32_t t, c, len;             // item (kNoItem: none), chunk, trial length
 };
 
-struct ChunkA {                     // stage A output of one chunk
-    uint2 ci[4];                    // (first record, count) of this lane's 4 events (0 if absent)
+// stage A output of one chunk: the index entries of this lane's 4 events (0 if
+// absent).  IX4: packed 4-byte entries first | count << 24 (cidx4: half the
+// gathered bytes and fewer L1 data-pipe wavefronts); else (first, count)
+template <bool IX4>
+struct ChunkA;
+template <>
+struct ChunkA<false> {
+    uint2 ci[4];
     uint32_t t, c, len;
+    __device__ __forceinline__ uint32_t first(int q) const { return ci[q].x; }
+    __device__ __forceinline__ uint32_t cnt(int q) const { return ci[q].y; }
+};
+template <>
+struct ChunkA<true> {
+    uint32_t ci[4];
+    uint32_t t, c, len;
+    __device__ __forceinline__ uint32_t first(int q) const { return ci[q] & 0xffffffu; }
+    __device__ __forceinline__ uint32_t cnt(int q) const { return ci[q] >> 24; }
 };
 constexpr uint32_t kNoItem = 0xffffffffu;
 
@@ -149,23 +164,27 @@ __device__ __forceinline__ uint32_t item_trial(const SplitArgs &A, uint32_t i) {
 // BM: 0 = bitmap shift 0 and a sentinel event (lanes past a trial's end hold
 // an id whose presence bit is 0, so no length test per event), 1 = any shift
 // with the sentinel, 2 = any shift, length test per event.
-template <bool PK, int BM, class Sink>
+// VEC: fixed-length trials with K % 4 == 0 (every chunk 16-B aligned): one
+// uint4 per lane from a per-item pointer, no per-id length tests.
+template <bool PK, int BM, bool VEC, bool IX4, class Sink>
 __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t *bitmap, Sink &sink) {
+    using CA = ChunkA<IX4>;
     const int lane = threadIdx.x & 31;
     const uint32_t shift = A.pf.bitmap_shift, cap = A.cap;
     const uint32_t n_items = A.n_items_dev ? *A.n_items_dev : A.n_items;
     const uint32_t *events = A.yet.events;
     const uint64_t *offsets = A.yet.offsets;
     const uint2 *__restrict__ cidx = A.pf.cidx;
+    const uint32_t *__restrict__ cidx4 = A.pf.cidx4;
     const uint32_t K = A.yet.fixed_len;
     const uint32_t mul = 1u << A.kbits;
-    const bool vec = offsets == nullptr && (K & 3u) == 0;   // every chunk 16 B aligned
     const uint32_t sent = BM == 2 ? 0u : A.pf.sentinel_event;
 
     // fetch side: the item being fetched and the chunk within it (warp-uniform)
     uint32_t pt = kNoItem;
-    uint32_t pc = 0, plen = 0;
+    uint32_t pc = 0, plen = 0;                        // (plen = 0 when there is no item)
     uint64_t pbase = 0;
+    const uint4 *psrc = nullptr;                      // VEC: this lane's uint4 of the item's chunk 0
     // items are claimed one ahead (lane 0's atomic for the next item in flight
     // while this one streams); a claimed item is always the claiming warp's next
     uint32_t claim = 0;
@@ -175,31 +194,34 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         if (lane == 0 && i < n_items) claim = (uint32_t)atomicAdd(A.sched, 1ull);
         pt = i < n_items ? i : kNoItem;
         pc = 0;
+        plen = 0;
         if (pt != kNoItem) {
             const uint32_t t = item_trial(A, pt);
-            if (offsets) { pbase = offsets[t]; plen = (uint32_t)(offsets[t + 1] - pbase); }
+            if (VEC) { pbase = (uint64_t)t * K; plen = K; }
+            else if (offsets) { pbase = offsets[t]; plen = (uint32_t)(offsets[t + 1] - pbase); }
             else { pbase = (uint64_t)t * K; plen = K; }
+            if (VEC) psrc = reinterpret_cast<const uint4 *>(events + pbase) + lane;
         }
     };
     auto fetch = [&](RawChunk &r) {
-        r.t = pt; r.c = pc; r.len = pt != kNoItem ? plen : 0u;
+        r.t = pt; r.c = pc; r.len = plen;
         r.v = make_uint4(sent, sent, sent, sent);
-        if (pt != kNoItem) {
-            const uint32_t k = pc * 128u + 4u * lane;
+        const uint32_t k = pc * 128u + 4u * lane;
+        if (VEC) {
+            if (k < plen) r.v = __ldcs(psrc + pc * 32u);
+        } else if (pt != kNoItem) {
             const uint32_t *src = events + pbase + k;
-            if (vec) {
-                if (k < plen) r.v = __ldcs(reinterpret_cast<const uint4 *>(src));
-            } else {
-                if (k < plen) r.v.x = __ldcs(src);
-                if (k + 1 < plen) r.v.y = __ldcs(src + 1);
-                if (k + 2 < plen) r.v.z = __ldcs(src + 2);
-                if (k + 3 < plen) r.v.w = __ldcs(src + 3);
-            }
+            if (k < plen) r.v.x = __ldcs(src);
+            if (k + 1 < plen) r.v.y = __ldcs(src + 1);
+            if (k + 2 < plen) r.v.z = __ldcs(src + 2);
+            if (k + 3 < plen) r.v.w = __ldcs(src + 3);
+        }
+        if (pt != kNoItem) {
             if ((pc + 1) * 128u >= plen) next_item();
             else ++pc;
         }
     };
-    auto stage_a = [&](const RawChunk &r, ChunkA &S) {
+    auto stage_a = [&](const RawChunk &r, CA &S) {
         S.t = r.t; S.c = r.c; S.len = r.len;
         const uint32_t k0 = r.c * 128u + 4u * lane;
         const uint32_t ee[4] = {r.v.x, r.v.y, r.v.z, r.v.w};
@@ -209,11 +231,19 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
             const uint32_t w = bitmap[bit >> 5];
             bool hit = __funnelshift_r(w, 0u, bit) & 1u;      // w >> (bit & 31)
             if (BM == 2) hit = hit && k0 + q < r.len;
-            S.ci[q] = make_uint2(0u, 0u);
-            asm volatile(                                 // predicated load through L2, no branch
-                "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.cg.v2.u32 {%0, %1}, [%3];\n}"
-                : "+r"(S.ci[q].x), "+r"(S.ci[q].y)
-                : "r"((uint32_t)hit), "l"(cidx + ee[q]));
+            if constexpr (IX4) {
+                S.ci[q] = 0u;
+                asm volatile(                             // predicated load through L2, no branch
+                    "{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p ld.global.cg.u32 %0, [%2];\n}"
+                    : "+r"(S.ci[q])
+                    : "r"((uint32_t)hit), "l"(cidx4 + ee[q]));
+            } else {
+                S.ci[q] = make_uint2(0u, 0u);
+                asm volatile(
+                    "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.cg.v2.u32 {%0, %1}, [%3];\n}"
+                    : "+r"(S.ci[q].x), "+r"(S.ci[q].y)
+                    : "r"((uint32_t)hit), "l"(cidx + ee[q]));
+            }
         }
     };
     // stage B: pairs out.  One warp prefix sum of the pair counts; a present
@@ -222,10 +252,10 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
     // pairs (usually one pass).
     uint32_t n = 0;                                   // pairs of the current item (warp-uniform)
     uint2 *out = nullptr;                             // the current item's pair region
-    auto stage_b = [&](const ChunkA &S) {
+    auto stage_b = [&](const CA &S) {
         if (S.c == 0) n = 0;
         const uint32_t k0 = S.c * 128u + 4u * lane;
-        const uint32_t np = S.ci[0].y + S.ci[1].y + S.ci[2].y + S.ci[3].y;
+        const uint32_t np = S.cnt(0) + S.cnt(1) + S.cnt(2) + S.cnt(3);
         // exclusive warp prefix of np, bit-sliced over ballots (votes, no
         // shuffles through the shared-memory pipe): 3 slices unless some
         // lane has >= 8 pairs in the chunk; np <= 4 * ARA_MAX_SLOTS = 896
@@ -260,30 +290,30 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     pq[q] = o;
-                    pv[q] = S.ci[q].x * mul + (k0 + q);
-                    st_u32_if(S.ci[q].y != 0u, reinterpret_cast<uint64_t>(out32 + o), pv[q]);
-                    st_u32_if(S.ci[q].y > 1u, reinterpret_cast<uint64_t>(out32 + o + 1), pv[q] + mul);
-                    o += S.ci[q].y;
-                    mx = max(mx, S.ci[q].y);
+                    pv[q] = S.first(q) * mul + (k0 + q);
+                    st_u32_if(S.cnt(q) != 0u, reinterpret_cast<uint64_t>(out32 + o), pv[q]);
+                    st_u32_if(S.cnt(q) > 1u, reinterpret_cast<uint64_t>(out32 + o + 1), pv[q] + mul);
+                    o += S.cnt(q);
+                    mx = max(mx, S.cnt(q));
                 }
 #pragma unroll 1
                 for (uint32_t j = 2; __any_sync(0xffffffffu, j < mx); ++j)   // events with three or more pairs
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        st_u32_if(j < S.ci[q].y, reinterpret_cast<uint64_t>(out32 + (pq[q] + j)), pv[q] + j * mul);
+                        st_u32_if(j < S.cnt(q), reinterpret_cast<uint64_t>(out32 + (pq[q] + j)), pv[q] + j * mul);
             } else {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     pq[q] = o;
-                    st_pair_if(S.ci[q].y != 0u, reinterpret_cast<uint64_t>(out + o), S.ci[q].x, k0 + q);
-                    o += S.ci[q].y;
-                    mx = max(mx, S.ci[q].y);
+                    st_pair_if(S.cnt(q) != 0u, reinterpret_cast<uint64_t>(out + o), S.first(q), k0 + q);
+                    o += S.cnt(q);
+                    mx = max(mx, S.cnt(q));
                 }
 #pragma unroll 1
                 for (uint32_t j = 1; __any_sync(0xffffffffu, j < mx); ++j)
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        st_pair_if(j < S.ci[q].y, reinterpret_cast<uint64_t>(out + (pq[q] + j)), S.ci[q].x + j, k0 + q);
+                        st_pair_if(j < S.cnt(q), reinterpret_cast<uint64_t>(out + (pq[q] + j)), S.first(q) + j, k0 + q);
             }
         }
         // (a chunk that does not fit: nothing is stored, the count goes on --
@@ -296,7 +326,7 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
     // chunks X+2, X+3 are in flight from HBM
     next_item();
     RawChunk ra, rb;
-    ChunkA ca, cb;
+    CA ca, cb;
     fetch(ra);
     fetch(rb);
     stage_a(ra, ca);
@@ -343,7 +373,7 @@ struct PoolSink {
     __device__ void end(uint32_t, uint32_t) const {}
 };
 
-template <bool PK, int BM>
+template <bool PK, int BM, bool VEC, bool IX4>
 __global__ void __launch_bounds__(kCompactThreads, 32 / ARA_COMPACT_WARPS) compact_kernel(const __grid_constant__ SplitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);
@@ -357,10 +387,10 @@ __global__ void __launch_bounds__(kCompactThreads, 32 / ARA_COMPACT_WARPS) compa
     __syncthreads();
     if (A.list) {
         PoolSink sink{A};
-        produce_pairs<PK, BM>(A, bitmap, sink);
+        produce_pairs<PK, BM, VEC, IX4>(A, bitmap, sink);
     } else {
         SlotSink sink{A};
-        produce_pairs<PK, BM>(A, bitmap, sink);
+        produce_pairs<PK, BM, VEC, IX4>(A, bitmap, sink);
     }
 }
 
@@ -842,14 +872,27 @@ cudaError_t prepare_launch(const void *kern, size_t smem, int threads, int &per_
     return cudaSuccess;
 }
 
+static bool env_compact_ix4() {                 // (test aid: ARA_COMPACT_IX4=0 selects 8-byte entries)
+    static const bool on = [] {
+        const char *e = getenv("ARA_COMPACT_IX4");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms) {
     const size_t smem = (A.pf.bitmap_words * 4u + 4u + 15u) & ~15u;
     using K = void (*)(SplitArgs);
     const int bm = !A.pf.sentinel_ok ? 2 : A.pf.bitmap_shift == 0 ? 0 : 1;
-    const K kern = A.kbits ? (bm == 0 ? (K)compact_kernel<true, 0> : bm == 1 ? (K)compact_kernel<true, 1>
-                                                                      : (K)compact_kernel<true, 2>)
-                           : (bm == 0 ? (K)compact_kernel<false, 0> : bm == 1 ? (K)compact_kernel<false, 1>
-                                                                       : (K)compact_kernel<false, 2>);
+    const bool vec = A.yet.offsets == nullptr && (A.yet.fixed_len & 3u) == 0;   // every chunk 16-B aligned
+    // packed pairs of fixed-length trials read 4-byte index entries (< 2^24 device records)
+    const bool ix4 = A.kbits && vec && A.pf.cidx4 && env_compact_ix4();
+#define ARA_CK(PK_, V_, I_) (bm == 0 ? (K)compact_kernel<PK_, 0, V_, I_> : bm == 1 ? (K)compact_kernel<PK_, 1, V_, I_> \
+                                                                             : (K)compact_kernel<PK_, 2, V_, I_>)
+    const K kern = ix4 ? ARA_CK(true, true, true)
+                 : A.kbits ? (vec ? ARA_CK(true, true, false) : ARA_CK(true, false, false))
+                           : (vec ? ARA_CK(false, true, false) : ARA_CK(false, false, false));
+#undef ARA_CK
     int per_sm = 0;
     cudaError_t err = prepare_launch((const void *)kern, smem, kCompactThreads, per_sm);
     if (err != cudaSuccess) return err;

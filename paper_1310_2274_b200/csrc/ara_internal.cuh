@@ -52,6 +52,40 @@ __device__ __forceinline__ const float2 *table_row(const TablePtr &T, uint64_t r
     return (T.nodes + ti) + rec * kTabNodes;
 }
 
+// Shared-memory copy of a presence bitmap (words) plus one zero word after it
+// (the sentinel event's bit), by bulk asynchronous copies (TMA engine,
+// cp.async.bulk) completing on an mbarrier: one thread issues the 16-B
+// multiple in 32 KiB pieces, the block writes the remaining <= 3 words and the
+// zero word, then every thread waits on the barrier.  smem: the bitmap at
+// offset 0 (16-B aligned), the 8-B barrier at bitmap_smem_barrier(words).
+// The per-thread load loop it replaced kept one load in flight per thread
+// (10 % of the primary kernel's stall samples at cfg2).
+__host__ __device__ constexpr uint32_t bitmap_smem_barrier(uint32_t words) { return ((words + 1) * 4u + 15u) & ~15u; }
+__host__ __device__ constexpr uint32_t bitmap_smem_bytes(uint32_t words) { return bitmap_smem_barrier(words) + 16u; }
+__device__ __forceinline__ void load_bitmap_smem(unsigned char *smem, const uint32_t *__restrict__ g, uint32_t words) {
+    uint32_t *bm = reinterpret_cast<uint32_t *>(smem);
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(smem + bitmap_smem_barrier(words));
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t bulk = (words * 4u) & ~15u;                  // bytes by the copy engine
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bulk) : "memory");
+        for (uint32_t o = 0; o < bulk; o += 32768u) {
+            const uint32_t n = bulk - o < 32768u ? bulk - o : 32768u;
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(dst + o), "l"(reinterpret_cast<const unsigned char *>(g) + o), "r"(n), "r"(bar)
+                         : "memory");
+        }
+    }
+    for (uint32_t t = bulk / 4u + threadIdx.x; t <= words; t += blockDim.x) bm[t] = t < words ? g[t] : 0u;
+    __syncthreads();                                            // (the barrier is initialised; the tail written)
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(bar) : "memory");
+}
+
 constexpr uint32_t kModeTable = 0, kModeExact = 1, kModeDegenerate = 2;
 struct __align__(16) BetaRec {
     float a, b, wi, wc;

@@ -284,9 +284,7 @@ __global__ void __launch_bounds__(kPrimaryWarps * 32, 1) primary_kernel(const __
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&A.status->bad_event, 1u);
         return;
     }
-    for (uint32_t t = threadIdx.x; t <= A.pf.bitmap_words; t += blockDim.x)   // + one zero word (sentinel)
-        bitmap[t] = t < A.pf.bitmap_words ? A.pf.occ_bitmap[t] : 0u;   // nonzero losses only
-    __syncthreads();
+    load_bitmap_smem(smem, A.pf.occ_bitmap, A.pf.bitmap_words);   // nonzero losses only (+ the zero word)
     if constexpr (LP == 1 || (LP == 2 && !OM)) {      // (registers: LP 2 with occ_max would spill)
         if (A.yet.offsets == nullptr && A.yet.fixed_len > 0 && (A.yet.fixed_len & 3u) == 0)
             primary_flat<LP, BM, OM, true>(A, bitmap);
@@ -370,7 +368,7 @@ __global__ void __launch_bounds__(kPrimaryWarps * 32, 1) primary_kernel(const __
 }
 
 cudaError_t launch_primary(const PrimaryArgs &A, cudaStream_t s, int num_sms) {
-    const size_t smem = (A.pf.bitmap_words * 4u + 4u + 15u) & ~15u;
+    const size_t smem = bitmap_smem_bytes(A.pf.bitmap_words);
     const int bm = !A.pf.sentinel_ok ? 2 : A.pf.bitmap_shift == 0 ? 0 : 1;
     using K = void (*)(PrimaryArgs);
     K kern = nullptr;

@@ -382,9 +382,7 @@ __global__ void __launch_bounds__(kCompactThreads, 32 / ARA_COMPACT_WARPS) compa
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&A.status->bad_event, 1u);
         return;
     }
-    for (uint32_t t = threadIdx.x; t <= A.pf.bitmap_words; t += blockDim.x)   // + one zero word (sentinel)
-        bitmap[t] = t < A.pf.bitmap_words ? A.pf.bitmap[t] : 0u;
-    __syncthreads();
+    load_bitmap_smem(smem, A.pf.bitmap, A.pf.bitmap_words);      // (+ one zero word: the sentinel's bit)
     if (A.list) {
         PoolSink sink{A};
         produce_pairs<PK, BM, VEC, IX4>(A, bitmap, sink);
@@ -881,7 +879,7 @@ static bool env_compact_ix4() {                 // (test aid: ARA_COMPACT_IX4=0 
 }
 
 cudaError_t launch_compact(const SplitArgs &A, cudaStream_t s, int num_sms) {
-    const size_t smem = (A.pf.bitmap_words * 4u + 4u + 15u) & ~15u;
+    const size_t smem = bitmap_smem_bytes(A.pf.bitmap_words);
     using K = void (*)(SplitArgs);
     const int bm = !A.pf.sentinel_ok ? 2 : A.pf.bitmap_shift == 0 ? 0 : 1;
     const bool vec = A.yet.offsets == nullptr && (A.yet.fixed_len & 3u) == 0;   // every chunk 16-B aligned

@@ -1041,6 +1041,7 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
         S.ze_mask = S.rng_mode == 2 ? 0u : 0xffffffffu;
         S.ze_tag = S.rng_mode == 2 ? 7u : 2u;
         S.kbits = pl.kbits;
+        S.kmask = (1u << pl.kbits) - 1u;
         const uint64_t pair_bytes = S.kbits ? 4 : 8;
         for (int r = 0; r < 10; ++r) {                   // Philox4x32-10 key schedule of the seed
             S.pkey[2 * r] = (uint32_t)seed + (uint32_t)r * 0x9E3779B9u;

@@ -195,6 +195,7 @@ struct SplitArgs {
     uint32_t *redo;               // trials with a table-less record (fp64 kernel)
     uint32_t pkey[20];            // Philox key schedule of the seed (round r: pkey[2r], pkey[2r+1])
     uint32_t kbits;               // > 0: pairs packed in 4 B as device record << kbits | k
+    uint32_t kmask;               // (1 << kbits) - 1
     float *occ_max;               // null, or [n_layers][n_trials] largest occurrence loss (G29)
     uint32_t rng_mode;            // 0: reading G2; 1: ARA_RNG_RECORD; 2: ARA_RNG_OCCURRENCE; 3: ARA_RNG_SUPPLIED
     const float *zp_sup;          // mode 3: z_(Prog,E) per YET occurrence, [program][zp_stride]

@@ -242,7 +242,7 @@ __device__ __forceinline__ void primary_flat(const PrimaryArgs &A, const uint32_
                 S[l] += (double)G.g[q][l];               // line 12's trial sum, occurrence order per lane
                 if (OM) M[l] = fmaxf(M[l], G.g[q][l]);
             }
-        if ((G.c + 1) * 128u >= G.len) {
+        if ((G.c + 1) * 128u >= (VEC ? K : G.len)) {     // (VEC: every trial has K ids)
 #pragma unroll
             for (int l = 0; l < LP; ++l) {
                 double s = S[l];

@@ -440,15 +440,15 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
     unsigned long long *dhs = W.dhs;
     const SplitRec *__restrict__ srecs = A.pf.srecs;
     const TablePtr tables = A.pf.tables;
-    const uint32_t kb = A.kbits, kmask = (1u << kb) - 1u;
     auto ldpair = [&](const uint2 *q) -> uint2 {    // {device record, k}
-        if (PK) {                                     // packed: record << kbits | k
-            const uint32_t w = __ldcs(reinterpret_cast<const uint32_t *>(in) + (q - in));
-            return make_uint2(w >> kb, w & kmask);
+        if (PK) {                                     // packed: record << kbits | k (operands from the
+            const uint32_t w = __ldcs(reinterpret_cast<const uint32_t *>(in) + (q - in));   // constant bank)
+            return make_uint2(w >> A.kbits, w & A.kmask);
         }
         return CG ? __ldcg(q) : __ldcs(q);
     };
     const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);
+    const bool any_exact = A.pf.n_exact_records != 0;   // some record is table-less (its trials are redone)
     // RS 2: index of the trial's first occurrence in the YET (supplied z_(Prog,E))
     const uint64_t occ_base = RS != 2 ? 0 : A.yet.offsets ? A.yet.offsets[t] : t * (uint64_t)A.yet.fixed_len;
     if (!SL)
@@ -516,7 +516,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                     const float2 *row = table_row(tables, r[u].tab, ti);
                     x[u] = r[u].scale * sigmoidf_(quintic_from_nodes(__ldg(row), __ldg(row + 1), ti, tt,
                                                                      r[u].a, r[u].b));
-                    redo |= live[u] && (meta[u] >> 28) == kModeExact;
+                    if (any_exact) redo |= live[u] && (meta[u] >> 28) == kModeExact;   // (warp-uniform test)
                 }
             } else {
 #pragma unroll
@@ -542,7 +542,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 }
                 if (live[u]) {                                // (losses are >= 0)
                     const uint32_t p = b + 32u * u + lane;
-                    xs[p] = (__float_as_uint(x[u]) & 0x7fffffffu) | ((meta[u] & 0x100u) << 23);
+                    xs[p] = __float_as_uint(x[u]) | ((meta[u] & 0x100u) << 23);   // (x >= +0: bit 31 free)
                     if (!SL) fl[p] = (uint8_t)layer;
                 }
             }

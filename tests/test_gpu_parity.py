@@ -1168,3 +1168,28 @@ def test_async_errors_reported_at_synchronize(A, monkeypatch):
     with pytest.raises(A.AraError) as ei:
         ctx2.synchronize()
     assert ei.value.code == A.ERANGE
+
+
+# ---- multi-rank bench path through libara (ranks sharing the GPU over gloo) ----
+@pytest.mark.parametrize("cfg_name,ranks", [("cfg1", 2), ("cfg1", 3)])
+def test_bench_multirank_measures_equal(cfg_name, ranks, tmp_path):
+    # bench.py's multi-rank path (trial shards with global Philox keys, the YLT
+    # all-gather, measures on the gathered layout, max-over-ranks timing) with
+    # libara on every rank: 2 and 3 ranks (unequal shards for 3) sharing one GPU
+    # over gloo print the same PML / TVaR as the 1-rank run
+    import json, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    args = ["--config", cfg_name, "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
+    one = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert one.returncode == 0, one.stderr[-2000:]
+    env = dict(os.environ, ARA_BENCH_BACKEND="gloo")
+    port = str(29600 + ranks)
+    multi = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                            f"--nproc-per-node={ranks}", "--master-addr", "127.0.0.1", "--master-port", port,
+                            os.path.join(root, "bench.py"), "--gpus", str(ranks)] + args,
+                           cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert multi.returncode == 0, multi.stderr[-2000:]
+    a = json.loads(one.stdout.strip().splitlines()[-1])
+    b = json.loads(multi.stdout.strip().splitlines()[-1])
+    assert b["n_gpus"] == ranks and a["measures"] == b["measures"]

@@ -474,6 +474,60 @@ def test_determinism_and_sharding(A, ctx):
     assert np.array_equal(np.concatenate(parts, axis=1), a)
 
 
+@pytest.mark.parametrize("K", [1000, 1002, 64])
+def test_fixed_length_equals_csr_form(A, ctx, K):
+    # the same trials as a fixed-length YET (compaction: the VEC specialisation
+    # with 4-byte index entries; primary path: round-robin trials) and as CSR
+    # offsets (per-id loads, 8-byte entries, dynamic scheduler): the YLT is a
+    # function of the YET's contents alone -- bit-identical YLT, counts, hashes,
+    # with and without draws (K = 1002: not a multiple of 4, no VEC either side)
+    cfg = aragen.load_config("cfg3")
+    cfg.update(n_trials=6000, events_per_trial=K, layer_terms=[[2e5, 5e6, 1.0e6, 5.0e9]])
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    P = A.Portfolio(ctx, pf)
+    fixed = A.Yet.from_dict(ctx, yet)
+    off = np.arange(cfg["n_trials"] + 1, dtype=np.uint64) * np.uint64(K)
+    csr = A.Yet(ctx, yet["events"], trial_off=off)
+    for su in (True, False):
+        for dbg in (True, False):
+            a = A.run(ctx, P, fixed, seed=13, su=su, debug=dbg)
+            b = A.run(ctx, P, csr, seed=13, su=su, debug=dbg)
+            for x, y in zip(a if dbg else [a], b if dbg else [b]):
+                assert np.array_equal(x.cpu().numpy(), y.cpu().numpy())
+
+
+_IX_SCRIPT = r"""
+import sys, hashlib, numpy as np
+sys.path.insert(0, {root!r})
+import aragen
+from paper_1310_2274_b200 import ara
+ctx = ara.Context(0)
+cfg = aragen.load_config("cfg3")
+cfg.update(n_trials=20000, layer_terms=[[2e5, 5e6, 1.0e6, 5.0e9]])
+pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+P, Y = ara.Portfolio(ctx, pf), ara.Yet.from_dict(ctx, yet)
+h = hashlib.sha256()
+for x in ara.run(ctx, P, Y, seed=3, debug=True):
+    h.update(x.cpu().numpy().tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_compaction_index_entry_widths_identical():
+    # the compaction's packed 4-byte index entries (first | count << 24) and the
+    # 8-byte (first, count) pairs it falls back to (>= 2^24 device records; forced
+    # here by ARA_COMPACT_IX4=0, read once per process): bit-identical YLT, counts, hashes
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", _IX_SCRIPT.format(root=root)], env=dict(os.environ, ARA_COMPACT_IX4=v),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip())
+    assert outs[0] == outs[1]
+
+
 @pytest.mark.parametrize("n_layers,J,K", [(1, 16, 1000), (3, 4, 1500)])
 def test_packed_wide_pairs_and_batching_identical(A, ctx, n_layers, J, K, monkeypatch):
     # 4-byte packed and 8-byte pair records, any trial batching

@@ -243,27 +243,33 @@ __device__ __forceinline__ float sigmoid_node(float lam) {
 
 // quintic Hermite on [v_i, v_i + h] from the two nodes' (lambda, lambda'),
 // lambda'' from the ODE at each node, evaluated in Horner form in t in [0,1]:
-// p(t) = l0 + B t + C/2 t^2 + c3 t^3 + c4 t^4 + c5 t^5 with B = h l0', C = h^2 l0'',
-// E = h l1', F = h^2 l1'', D = l1 - l0 and (from p, p', p'' at t = 1)
-// c3 = 10D - 6B - 3C/2 - 4E + F/2, c4 = -15D + 8B + 3C/2 + 7E - F,
-// c5 = 6D - 3B - C/2 - 3E + F/2.  Every operation an explicit fmaf / fmul, so
-// the rounding is the same in every kernel instantiation (no contraction choice).
+// p(t) = l0 + B t + C/2 t^2 + t^3 (c3 + c4 t + c5 t^2) with B = h l0', C = h^2 l0'',
+// E = h l1', F = h^2 l1'', D = l1 - l0.  p, p', p'' at t = 1 leave the residuals
+// R0 = D - B - C/2, R1 = E - B - C, R2 = F - C, and c3 = 10 R0 - 4 R1 + R2/2,
+// c4 = -15 R0 + 7 R1 - R2, c5 = 6 R0 - 3 R1 + R2/2 (the same polynomial as the
+// expanded c3 = 10D - 6B - 3C/2 - 4E + F/2, ... in 5 fewer operations).  Every
+// operation an explicit fmaf / fmul / fadd, so the rounding is the same in every
+// kernel instantiation (no contraction choice).
 __device__ __forceinline__ float quintic_from_nodes(float2 n0, float2 n1, int i, float t, float a, float b) {
+    constexpr float kH2 = kTabH * kTabH;
     const float v0 = fmaf((float)i, kTabH, kTabV0), v1 = __fadd_rn(v0, kTabH);
     const float apb = __fadd_rn(a, b);
     const float x0 = sigmoid_node(n0.x), x1 = sigmoid_node(n1.x);
     const float g0 = fmaf(-apb, x0, a), g1 = fmaf(-apb, x1, a);          // a(1-x) - b x
     const float s0 = __fmul_rn(n0.y, fmaf(-g0, n0.y, -v0));               // lambda'' = l' (-v - g l')
     const float s1 = __fmul_rn(n1.y, fmaf(-g1, n1.y, -v1));
+    const float B = __fmul_rn(kTabH, n0.y);                               // h l0'
+    const float Ch = __fmul_rn(0.5f * kH2, s0);                           // C / 2
     const float D = __fsub_rn(n1.x, n0.x);
-    const float B = __fmul_rn(kTabH, n0.y), E = __fmul_rn(kTabH, n1.y);
-    const float C = __fmul_rn(kTabH * kTabH, s0), F = __fmul_rn(kTabH * kTabH, s1);
-    const float c3 = fmaf(10.0f, D, fmaf(-6.0f, B, fmaf(-1.5f, C, fmaf(-4.0f, E, __fmul_rn(0.5f, F)))));
-    const float c4 = fmaf(-15.0f, D, fmaf(8.0f, B, fmaf(1.5f, C, fmaf(7.0f, E, -F))));
-    const float c5 = fmaf(6.0f, D, fmaf(-3.0f, B, fmaf(-0.5f, C, fmaf(-3.0f, E, __fmul_rn(0.5f, F)))));
+    const float R0 = __fsub_rn(__fsub_rn(D, B), Ch);                      // D - B - C/2
+    const float R1 = fmaf(-2.0f, Ch, fmaf(kTabH, n1.y, -B));              // E - B - C
+    const float T = __fmul_rn(0.5f * kH2, __fsub_rn(s1, s0));             // R2 / 2
+    const float c3 = fmaf(10.0f, R0, fmaf(-4.0f, R1, T));
+    const float c4 = fmaf(-15.0f, R0, fmaf(7.0f, R1, __fmul_rn(-2.0f, T)));
+    const float c5 = fmaf(6.0f, R0, fmaf(-3.0f, R1, T));
     float p = fmaf(c5, t, c4);
     p = fmaf(p, t, c3);
-    p = fmaf(p, t, __fmul_rn(0.5f, C));
+    p = fmaf(p, t, Ch);
     p = fmaf(p, t, B);
     return fmaf(p, t, n0.x);
 }

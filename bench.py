@@ -271,8 +271,8 @@ def run_ours(args, cfg, rank, world, local):
     ylt_host = torch.empty((L, n_loc), dtype=torch.float32).pin_memory()
     ara.prepare(ctx, P, Y, su=cfg["su"], async_=True)   # every ara_run scratch buffer, allocated once here
 
-    kern_ms = []          # per-kernel CUDA-event sums of each timed ara_run (ara_last_run_timings)
-    meas_ev = []          # CUDA events around each timed step's all-gather + measures
+    kern_ms = []          # per-kernel CUDA-event sums of each profiled ara_run (ara_last_run_timings)
+    meas_ev = []          # CUDA events around each profiled step's all-gather + measures
 
     def measures(src, n_shards):
         if len(layers) > 1 and len(rps) <= 4:        # every table in one call, one read-back
@@ -283,14 +283,14 @@ def run_ours(args, cfg, rank, world, local):
     meas_dev = torch.empty((args.steps, len(layers), len(rps), 3), dtype=torch.float64, device=dev)
     meas_host = torch.empty((args.steps, len(layers), len(rps), 3), dtype=torch.float64).pin_memory()
 
-    def step(Yx, timed=False, slot=None):
+    def step(Yx, profiled=False, slot=None):
         # ara_run with ARA_ASYNC: no host synchronisation inside the run (errors
         # latched by the runs are checked by ctx.synchronize() after the loop).
         # slot None: the measures read back synchronously (the e2e path);
         # slot s: ara_risk_measures_async into device row s (read back once after
         # the timed steps) -- the steps queue back to back, one sync at the end
         ara.run(ctx, P, Yx, seed=cfg["seed"], su=cfg["su"], ylt=ylt, async_=True)
-        if timed:
+        if profiled:
             m0 = torch.cuda.Event(enable_timing=True); m1 = torch.cuda.Event(enable_timing=True)
             m0.record(stream)
         src, n_shards = gather_ylt(ylt, world, N_total, gathered, padded)
@@ -299,10 +299,10 @@ def run_ours(args, cfg, rank, world, local):
         else:
             ara.risk_measures_async(ctx, src, L, N_total, layers, rps=rps, n_shards=n_shards, out=meas_dev[slot])
             out = None
-        if timed:
+        if profiled:
             m1.record(stream)
             meas_ev.append((m0, m1))
-            kern_ms.append(ara.last_run_timings(ctx))    # (the run is complete: no wait)
+            kern_ms.append(ara.last_run_timings(ctx))    # (waits for the run's last event)
         return out
 
     # exact number of present (occurrence, slot) pairs = SU samples per launch
@@ -318,8 +318,8 @@ def run_ours(args, cfg, rank, world, local):
     with ClockSampler(local) as clk:
         t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for s_ in range(args.steps):
-            step(Y, timed=True, slot=s_)
+        for s_ in range(args.steps):                   # (no host synchronisation inside)
+            step(Y, slot=s_)
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -328,6 +328,11 @@ def run_ours(args, cfg, rank, world, local):
     elapsed = t0.elapsed_time(t1) / 1e3
     ctx.synchronize()                                    # errors latched by the ARA_ASYNC runs, if any
     meas_host.copy_(meas_dev)
+    # the per-kernel breakdown (roofline): the same steps again, outside the timed
+    # region, each read back (the per-run kernel timings wait for the run's end)
+    for s_ in range(args.steps):
+        step(Y, profiled=True, slot=s_)
+    torch.cuda.synchronize()
     # every timed step's measures equal a synchronous call's
     res = step(Y)
     for s_ in range(args.steps):

@@ -372,6 +372,9 @@ def risk_measures_async(ctx: Context, ylt, n_layers: int, n_total: int, layers, 
     ls = np.ascontiguousarray(layers, np.int32)
     if out is None:
         out = torch.empty((len(ls), len(r), 3), dtype=torch.float64, device=ylt.device)
+    elif not (isinstance(out, torch.Tensor) and out.dtype == torch.float64 and out.is_contiguous()
+              and out.numel() >= 3 * len(ls) * len(r)):
+        raise AraError(EINVAL, "out must be a contiguous float64 tensor of >= 3 * len(layers) * len(rps) elements")
     _check(lib.ara_risk_measures_async(ctx.h, _p(ylt), int(n_layers), int(n_total), int(n_shards), _p(ls),
                                        len(ls), _p(r), len(r), _p(out)))
     return out

@@ -1014,8 +1014,12 @@ def test_measures_async_equals_batch(A, ctx):
         pml, tvar, var = A.risk_measures_batch(ctx, y, L, n, layers, rps=(100, 250, 500), n_shards=P)
         o = out.cpu().numpy()
         assert np.array_equal(o[:, :, 0], pml) and np.array_equal(o[:, :, 1], tvar) and np.array_equal(o[:, :, 2], var)
-    with pytest.raises(A.AraError):                   # host output buffer
+    with pytest.raises(A.AraError):                   # host output buffer (binding check)
         A.risk_measures_async(ctx, y, L, n, layers, out=np.zeros((3, 3, 3)))
+    with pytest.raises(A.AraError):                   # host output buffer (the library's check)
+        A.risk_measures_async(ctx, y, L, n, layers, out=torch.zeros((3, 3, 3), dtype=torch.float64))
+    with pytest.raises(A.AraError):                   # too small
+        A.risk_measures_async(ctx, y, L, n, layers, out=torch.zeros((2, 3, 3), dtype=torch.float64, device="cuda"))
 
 
 def test_batch_and_curve_errors(A, ctx):

@@ -667,6 +667,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
                 }
     }
     d.n_exact_records = store->n_exact;
+    d.n_tables = store->n;
     d.bitmap = p->d_bitmap; d.recs = store->d_recs; d.rec_mu = store->d_mu;
     d.tables = TablePtr{store->d_nodes + kTabPad};
     d.rec_orig = p->d_rec_orig; d.slots = p->d_slots; d.layers = p->d_layers;

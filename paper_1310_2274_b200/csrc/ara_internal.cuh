@@ -107,6 +107,18 @@ struct __align__(32) SplitRec {    // 32 B: one 256-bit load
     uint32_t tab, key;
 };
 
+// ARA_DEVICE_CHECKS builds (tools/build_variant.sh chk -DARA_DEVICE_CHECKS=1)
+// trap on a failed bounds check in the hot kernels: the GPU test suite runs
+// against such a build as a bounds-checked pass (compute-sanitizer is not
+// available on every pool)
+#ifndef ARA_DEVICE_CHECKS
+#define ARA_DEVICE_CHECKS 0
+#endif
+#define ARA_CHECK(cond)                                   \
+    do {                                                  \
+        if (ARA_DEVICE_CHECKS && !(cond)) __trap();       \
+    } while (0)
+
 struct PortfolioDev {
     uint32_t catalog;
     uint32_t n_slots, n_layers;
@@ -117,6 +129,7 @@ struct PortfolioDev {
     uint32_t sentinel_ok;     // 0: no such id fits in 32 bits (per-event length test instead)
     uint64_t n_dev_records;
     uint32_t n_exact_records; // records without a quantile table (fp64 per-sample solve)
+    uint64_t n_tables;        // input records in the record store (quantile tables)
     const uint32_t *bitmap;   // [bitmap_words]
     const BetaRec *recs;      // [input records] (the record store, shared by the groups)
     TablePtr tables;          // [input records] (lambda, lambda') nodes

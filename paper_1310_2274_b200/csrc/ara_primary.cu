@@ -225,6 +225,7 @@ __device__ __forceinline__ void primary_flat(const PrimaryArgs &A, const uint32_
             const uint32_t bit = BM == 0 ? ee[q] : ee[q] >> shift;
             bool hit = __funnelshift_r(bitmap[bit >> 5], 0u, bit) & 1u;
             if (BM == 2) hit = hit && k0 + q < r.len;
+            ARA_CHECK(!hit || ee[q] < A.pf.catalog);
             load_occ<LP>(hit, occ + (uint64_t)ee[q] * LP, G.g[q]);
         }
     };

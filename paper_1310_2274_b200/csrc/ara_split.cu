@@ -231,6 +231,7 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
             const uint32_t w = bitmap[bit >> 5];
             bool hit = __funnelshift_r(w, 0u, bit) & 1u;      // w >> (bit & 31)
             if (BM == 2) hit = hit && k0 + q < r.len;
+            ARA_CHECK(!hit || ee[q] < A.pf.catalog);
             if constexpr (IX4) {
                 S.ci[q] = 0u;
                 asm volatile(                             // predicated load through L2, no branch
@@ -279,6 +280,7 @@ __device__ __forceinline__ void produce_pairs(const SplitArgs &A, const uint32_t
         if (S.c == 0) out = sink.begin(S.t);
         uint32_t pos = n + excl;
         if (n + tot <= cap) {                         // the chunk fits (warp-uniform)
+            ARA_CHECK(pos + np <= cap);
             // one 64-bit address per event, predicated stores (no branches)
             uint32_t pq[4], mx = 0, o = pos;
             if (PK) {                                 // pair = record * 2^kbits + k (one IMAD)
@@ -513,6 +515,8 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                     const float uu = (fminf(fmaxf(v[u], kTabV0), -kTabV0) - kTabV0) * (1.0f / kTabH);
                     const int ti = min((int)uu, kTabNodes - 2);
                     const float tt = uu - (float)ti;
+                    ARA_CHECK(!(live[u]) || (e[u].x < A.pf.n_dev_records && r[u].tab < A.pf.n_tables &&
+                                             ti >= 0 && ti <= kTabNodes - 2));
                     const float2 *row = table_row(tables, r[u].tab, ti);
                     x[u] = r[u].scale * sigmoidf_(quintic_from_nodes(__ldg(row), __ldg(row + 1), ti, tt,
                                                                      r[u].a, r[u].b));
@@ -542,6 +546,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                 }
                 if (live[u]) {                                // (losses are >= 0)
                     const uint32_t p = b + 32u * u + lane;
+                    ARA_CHECK(p < kXCap);
                     xs[p] = __float_as_uint(x[u]) | ((meta[u] & 0x100u) << 23);   // (x >= +0: bit 31 free)
                     if (!SL) fl[p] = (uint8_t)layer;
                 }

@@ -1251,3 +1251,21 @@ def test_bench_multirank_measures_equal(cfg_name, ranks, tmp_path):
     a = json.loads(one.stdout.strip().splitlines()[-1])
     b = json.loads(multi.stdout.strip().splitlines()[-1])
     assert b["n_gpus"] == ranks and a["measures"] == b["measures"]
+
+
+@pytest.mark.parametrize("su", [True, False])
+def test_large_catalog_coarse_bitmap(A, ctx, su):
+    # a 5M-event catalogue: the shared-memory bitmap holds one bit per 8 events
+    # (shift 3), so most bitmap hits are false and the index entry (or, without
+    # draws, the occurrence loss) decides; lookups bit-exact, YLT within the bar
+    cfg = aragen.load_config("cfg3")
+    cfg.update(catalog=5_000_000, n_layers=1, elts_per_layer=4, records_per_elt=50_000, n_trials=1500,
+               layer_terms=[[2e5, 5e6, 1.0e5, 5.0e9]])
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    (g, cnt, hsh), ref = run_both(A, ctx, pf, yet, seed=17, su=su)
+    assert np.array_equal(cnt, ref["count"]) and np.array_equal(hsh, ref["hash"])
+    ylt_check(g[0], ref, 0)
+    if not su:                                  # the primary kernel (no debug lookup) on the same trials
+        P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+        gp = A.run(ctx, P, Y, seed=17, su=False).cpu().numpy()
+        ylt_check(gp[0], ref, 0)

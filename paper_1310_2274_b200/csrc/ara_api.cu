@@ -48,6 +48,14 @@ int fail(int code, const char *fmt, ...) {
                         __FILE__, __LINE__);                                            \
     } while (0)
 
+// Every entry point starts here: launches are checked with cudaGetLastError, so
+// an error some earlier runtime call left behind (a destroy's cudaFree, a probe)
+// must not be reported against this call.
+cudaError_t enter_device(int device) {
+    cudaGetLastError();
+    return cudaSetDevice(device);
+}
+
 bool is_device_ptr(const void *p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -183,6 +191,7 @@ struct RecordStore {
 
 struct ara_portfolio {
     ara_ctx *ctx = nullptr;
+    int device = 0;                    // (destroy uses this, not ctx: the context may be gone first)
     PortfolioDev dev{};
     uint32_t *d_bitmap = nullptr, *d_rec_orig = nullptr;
     uint2 *d_cidx = nullptr;
@@ -209,6 +218,7 @@ struct ara_portfolio {
 
 struct ara_yet {
     ara_ctx *ctx = nullptr;
+    int device = 0;                    // (destroy uses this, not ctx: the context may be gone first)
     YetDev dev{};
     uint32_t *d_events = nullptr;
     uint64_t *d_offsets = nullptr;
@@ -239,7 +249,7 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
         return fail(ARA_ECUDA, "no CUDA device available (%s); libara has no CPU path",
                     cudaGetErrorString(e));
     if (device < 0 || device >= n) return fail(ARA_EINVAL, "device %d out of range [0,%d)", device, n);
-    CU(cudaSetDevice(device));
+    CU(enter_device(device));
     cudaDeviceProp prop;
     CU(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10)
@@ -307,7 +317,7 @@ void ara_ctx_destroy(ara_ctx *c) {
 
 int ara_ctx_synchronize(ara_ctx *c) {
     if (!c) return fail(ARA_EINVAL, "ctx is NULL");
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     CU(cudaStreamSynchronize(c->stream));
     CU(fold_latched(c));
     CU(cudaStreamSynchronize(c->stream));
@@ -454,6 +464,7 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
     *out = nullptr;
     int st = ara_validate_portfolio(C, n_elts, eoff, rec, et, n_layers, lprog, loff, lelts, lt);
     if (st != ARA_OK) return st;
+    CU(enter_device(c->device));
     // Kernel groups of consecutive layers: <= kSplitMaxLayers layers, <=
     // ARA_MAX_SLOTS slots, and -- so that each pass's gathered tables stay
     // L2-resident -- at most ARA_GROUP_BYTES (default 128 MiB)
@@ -472,12 +483,13 @@ int ara_create_portfolio(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t
         for (uint32_t l = l0; l <= l1; ++l) recs += layer_records(l);
         return l1 == l0 || recs * 160 + (uint64_t)C * 8 <= budget;
     };
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     std::shared_ptr<RecordStore> store;              // built by the first group (its device order)
     if (fits(0, n_layers - 1))
         return create_group(c, C, n_elts, eoff, rec, et, n_layers, lprog, loff, lelts, lt, store, out);
     ara_portfolio *p = new ara_portfolio();
     p->ctx = c;
+    p->device = c->device;
     p->n_layers_total = n_layers;
     for (uint32_t l0 = 0; l0 < n_layers;) {
         uint32_t l1 = l0 + 1;
@@ -505,7 +517,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
                         const uint32_t *lprog, const uint64_t *loff, const uint32_t *lelts,
                         const ara_layer_terms *lt, std::shared_ptr<RecordStore> &store,
                         ara_portfolio **out) {
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
 
     // slots: (layer, XELT) pairs, layer-major
     const uint32_t S = (uint32_t)loff[n_layers];
@@ -601,6 +613,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     for (uint64_t r = 0; r < total; ++r) tab[r] = store->pos[rec_src[r]];
     ara_portfolio *p = new ara_portfolio();
     p->ctx = c;
+    p->device = c->device;
     p->store = store;
     cudaStream_t s = c->stream;
     uint32_t *d_rec_meta = nullptr, *d_rec_src = nullptr;   // build-time arrays
@@ -713,12 +726,13 @@ int ara_portfolio_info(const ara_portfolio *p, uint64_t *n_dev, uint64_t *n_tl, 
 void ara_portfolio_destroy(ara_portfolio *p) {
     if (!p) return;
     for (ara_portfolio *g : p->groups) ara_portfolio_destroy(g);
-    if (p->ctx) cudaSetDevice(p->ctx->device);
+    cudaSetDevice(p->device);
     cudaFree(p->d_bitmap); cudaFree(p->d_rec_orig);
     cudaFree(p->d_cidx); cudaFree(p->d_cidx4); cudaFree(p->d_srecs); cudaFree(p->d_mm);
     cudaFree(p->d_slots); cudaFree(p->d_layers);
     cudaFree(p->d_occ); cudaFree(p->d_occ_bitmap); cudaFree(p->d_slot_terms); cudaFree(p->d_rec_z);
     delete p;
+    cudaGetLastError();                    // (a destroy cannot report: leave no stale error behind)
 }
 
 int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint64_t *toff,
@@ -752,9 +766,10 @@ int ara_load_yet(ara_ctx *c, uint64_t n_trials, uint64_t first_trial, const uint
             }
         }
     }
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     ara_yet *y = new ara_yet();
     y->ctx = c;
+    y->device = c->device;
     // +4 words: the compaction kernel's bulk copies round each piece up to 16 B
     if (dalloc(&y->d_events, total + 4) != cudaSuccess || dalloc(&y->d_redo, n_trials) != cudaSuccess ||
         dalloc(&y->d_ovf, n_trials) != cudaSuccess || dalloc(&y->d_ovf_n, n_trials) != cudaSuccess ||
@@ -796,7 +811,7 @@ int ara_yet_refill(ara_ctx *c, ara_yet *y, const uint32_t *events) {
     if (!c || !y) return fail(ARA_EINVAL, "ctx/yet is NULL");
     if (y->dev.n_events == 0) return ARA_OK;
     if (!events) return fail(ARA_EINVAL, "event_ids is NULL");
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     CU(cudaMemcpyAsync(y->d_events, events, y->dev.n_events * sizeof(uint32_t),
                        is_device_ptr(events) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        c->stream));
@@ -810,7 +825,7 @@ int ara_yet_refill_packed(ara_ctx *c, ara_yet *y, uint32_t bits, const uint32_t 
     if (y->dev.n_events == 0) return ARA_OK;
     if (!packed) return fail(ARA_EINVAL, "packed is NULL");
     const uint64_t words = (y->dev.n_events * (uint64_t)bits + 31) / 32;
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     if (y->packed_capacity < words + 2) {              // staging grows once, then is reused
         cudaFree(y->d_packed);
     cudaFree(y->d_zprog);
@@ -836,7 +851,7 @@ int ara_yet_set_z(ara_ctx *c, ara_yet *y, uint32_t n_programs, const float *z_pr
             return fail(ARA_EINVAL, "z_(Prog,E) must lie in (0,1): program %llu occurrence %llu",
                         (unsigned long long)(x / std::max<uint64_t>(y->dev.n_events, 1)),
                         (unsigned long long)(x % std::max<uint64_t>(y->dev.n_events, 1)));
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     cudaFree(y->d_zprog);
     y->d_zprog = nullptr;
     y->zprog_programs = 0;
@@ -862,7 +877,7 @@ int ara_portfolio_set_z(ara_ctx *c, ara_portfolio *p, const float *z_event) {
             return fail(ARA_EINVAL, "z_(E) must lie in (0,1): record %llu", (unsigned long long)r);
     std::vector<float> z(p->rec_src.size());           // per device record (layout only, no arithmetic)
     for (size_t r = 0; r < z.size(); ++r) z[r] = z_event[p->rec_src[r]];
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     cudaFree(p->d_rec_z);
     p->d_rec_z = nullptr;
     CU(dalloc(&p->d_rec_z, z.size()));
@@ -875,7 +890,7 @@ uint64_t ara_yet_num_trials(const ara_yet *y) { return y ? y->dev.n_trials : 0; 
 
 void ara_yet_destroy(ara_yet *y) {
     if (!y) return;
-    if (y->ctx) cudaSetDevice(y->ctx->device);
+    cudaSetDevice(y->device);
     cudaFree(y->d_events);
     cudaFree(y->d_offsets);
     cudaFree(y->d_redo);
@@ -885,6 +900,7 @@ void ara_yet_destroy(ara_yet *y) {
     cudaFree(y->d_packed);
     cudaFree(y->d_zprog);
     delete y;
+    cudaGetLastError();                    // (a destroy cannot report: leave no stale error behind)
 }
 
 // Layout of one split-path run: per-trial pair regions of 2x the expected
@@ -994,7 +1010,7 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
         return fail(ARA_EINVAL, "dbg_count/dbg_hash need ARA_DEBUG_LOOKUP");
     if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
     if (occ_max && !is_device_ptr(occ_max)) return fail(ARA_EINVAL, "occ_max must be device memory");
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     const uint64_t N = y->dev.n_trials;
     const bool exact = (flags & ARA_EXACT) != 0 && (flags & ARA_SU) != 0;
     const bool async = (flags & ARA_ASYNC) != 0;
@@ -1198,7 +1214,7 @@ static int run_group(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint6
 
 int ara_prepare(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint32_t flags) {
     if (!c || !p || !y) return fail(ARA_EINVAL, "ctx/portfolio/yet is NULL");
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     if (flags & ARA_ASYNC) {                         // the pre-sized overflow pool of ARA_ASYNC runs
         const std::vector<const ara_portfolio *> gs =
             p->groups.empty() ? std::vector<const ara_portfolio *>{p}
@@ -1230,7 +1246,7 @@ int ara_last_run_launches(const ara_ctx *c, uint32_t *kernel_launches, uint32_t 
 int ara_last_run_timings(const ara_ctx *cc, double *compact_ms, double *sample_ms, double *redo_ms) {
     if (!cc) return fail(ARA_EINVAL, "ctx is NULL");
     ara_ctx *c = const_cast<ara_ctx *>(cc);        // (the lazy evaluation of an ARA_ASYNC run's events)
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     CU(compute_timings(c));
     if (compact_ms) *compact_ms = c->last_ms[0];
     if (sample_ms) *sample_ms = c->last_ms[1];
@@ -1264,7 +1280,7 @@ int ara_exceedance_curve(ara_ctx *c, const float *ylt, uint32_t n_layers, uint64
         return fail(ARA_EINVAL, "need n_layers >= 1, n_shards >= 1 dividing n_total");
     if (layer < -1 || layer >= (int32_t)n_layers) return fail(ARA_EINVAL, "layer %d out of range", layer);
     if (!is_device_ptr(ylt) || !is_device_ptr(losses_out)) return fail(ARA_EINVAL, "ylt and losses_out must be device memory");
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     const uint64_t need = 2 * n_total + 256ull * (2 * (uint64_t)c->num_sms);
     if (c->ep_capacity < need) {                       // scratch grows once, then is reused
         cudaFree(c->d_ep);
@@ -1300,7 +1316,7 @@ static int measures_enqueue(ara_ctx *c, const float *ylt, uint32_t n_layers, uin
     for (uint32_t i = 0; i < n_sel; ++i)
         if (layers[i] < -1 || layers[i] >= (int32_t)n_layers) return fail(ARA_EINVAL, "layer %d out of range", layers[i]);
     if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     if (c->ms.capacity < n_total) {
         cudaFree(c->ms.vals);
         c->ms.vals = nullptr;
@@ -1362,7 +1378,7 @@ int ara_risk_measures_var(ara_ctx *c, const float *ylt, uint32_t n_layers, uint6
         if (k > k_need) k_need = k;
     }
     if (!is_device_ptr(ylt)) return fail(ARA_EINVAL, "ylt must be device memory");
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     if (c->ms.capacity < n_total) {
         cudaFree(c->ms.vals);
         c->ms.vals = nullptr;
@@ -1402,7 +1418,7 @@ int ara_sample_losses(ara_ctx *c, uint64_t n, const ara_record *recs, const floa
     for (uint64_t t = 0; t < n; ++t)
         if (!(zp[t] > 0.0f && zp[t] < 1.0f && ze[t] > 0.0f && ze[t] < 1.0f))
             return fail(ARA_EINVAL, "z values must lie in (0,1) (index %llu)", (unsigned long long)t);
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     ara_record *d_raw = nullptr;
     BetaRec *d_recs = nullptr;
     float2 *d_nodes = nullptr;
@@ -1444,7 +1460,7 @@ int ara_beta_quantiles(ara_ctx *c, uint64_t n, const double *alpha, const double
         if (!(alpha[t] > 0.0 && beta[t] > 0.0 && std::isfinite(alpha[t]) && std::isfinite(beta[t]) &&
               std::isfinite(v[t])))
             return fail(ARA_EINVAL, "need finite alpha, beta > 0 and finite v (index %llu)", (unsigned long long)t);
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     double *d = nullptr;
     int code = ARA_OK;
     if (dalloc(&d, 5 * n)) {
@@ -1472,7 +1488,7 @@ int ara_draw_uniforms(ara_ctx *c, uint64_t seed, uint64_t n, const uint32_t *ctr
     if (!c) return fail(ARA_EINVAL, "ctx is NULL");
     if (n == 0) return ARA_OK;
     if (!ctr || !u_out) return fail(ARA_EINVAL, "NULL argument");
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     uint4 *d_ctr = nullptr;
     float *d_out = nullptr;
     int code = ARA_OK;
@@ -1494,7 +1510,7 @@ int ara_normal_quantiles(ara_ctx *c, uint64_t n, const uint32_t *bits, float *v_
     if (!c) return fail(ARA_EINVAL, "ctx is NULL");
     if (n == 0) return ARA_OK;
     if (!bits || !v_out) return fail(ARA_EINVAL, "NULL argument");
-    CU(cudaSetDevice(c->device));
+    CU(enter_device(c->device));
     uint32_t *d_bits = nullptr;
     float *d_out = nullptr;
     int code = ARA_OK;

@@ -640,7 +640,7 @@ static int create_group(ara_ctx *c, uint32_t C, uint32_t n_elts, const uint64_t 
     std::vector<uint32_t> cidx4;
     if (p->d_cidx4) {                                   // first | count << 24 (count <= ARA_MAX_SLOTS < 256)
         cidx4.resize(C);
-        for (uint32_t e = 0; e < C; ++e) cidx4[e] = cidx[e].x | (cidx[e].y << 24);
+        for (uint32_t ev = 0; ev < C; ++ev) cidx4[ev] = cidx[ev].x | (cidx[ev].y << 24);
         UP(p->d_cidx4, cidx4.data(), (size_t)C);
     }
     UP(d_rec_meta, rec_meta.data(), (size_t)total);

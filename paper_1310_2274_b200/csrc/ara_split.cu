@@ -450,7 +450,6 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
         return CG ? __ldcg(q) : __ldcs(q);
     };
     const uint32_t trial_g = (uint32_t)(A.yet.first_trial + t);
-    const bool any_exact = A.pf.n_exact_records != 0;   // some record is table-less (its trials are redone)
     // RS 2: index of the trial's first occurrence in the YET (supplied z_(Prog,E))
     const uint64_t occ_base = RS != 2 ? 0 : A.yet.offsets ? A.yet.offsets[t] : t * (uint64_t)A.yet.fixed_len;
     if (!SL)
@@ -462,7 +461,8 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
         for (uint32_t l = lane; l < nl; l += 32) { dc[l] = 0u; dhs[l] = 0ull; }
     double acc = 0.0;                              // SL: this lane's share of the trial sum
     double carry = 0.0;                            // run open at the previous segment's end
-    int redo = 0;
+    uint32_t modes = 0;                            // OR of the live pairs' meta: bit 28 = a table-less record
+                                                   // (mode exact: the trial is redone in fp64)
     uint2 pn[kU];                                   // next round's pairs, prefetched
 #pragma unroll
     for (int u = 0; u < kU; ++u) pn[u] = 32u * u + lane < n ? ldpair(in + 32u * u + lane) : make_uint2(0u, 0u);
@@ -520,7 +520,7 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
                     const float2 *row = table_row(tables, r[u].tab, ti);
                     x[u] = r[u].scale * sigmoidf_(quintic_from_nodes(__ldg(row), __ldg(row + 1), ti, tt,
                                                                      r[u].a, r[u].b));
-                    if (any_exact) redo |= live[u] && (meta[u] >> 28) == kModeExact;   // (warp-uniform test)
+                    modes |= live[u] ? meta[u] : 0u;             // (a select and an OR: no predicated test)
                 }
             } else {
 #pragma unroll
@@ -616,7 +616,8 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
         carry = __shfl_sync(0xffffffffu, last, 31);
         __syncwarp();
     }
-    redo = __any_sync(0xffffffffu, redo);
+    static_assert(kModeExact == 1u, "the table-less flag is meta bit 28");
+    const bool redo = __any_sync(0xffffffffu, (modes >> 28) & 1u);
     if (redo) {
         if (lane == 0) A.redo[atomicAdd(&A.status->n_redo, 1u)] = (uint32_t)t;
         return;

@@ -438,6 +438,11 @@ def run_ours(args, cfg, rank, world, local):
         pk["frac"] = pk["achieved"] / hbm_peak if pk["achieved"] else None
         pc = consts.get("primary_kernel", {})
         pk["traffic"] = pc.get("dram_bytes_per_occurrence", 0) * n_loc * K if pc else None
+        if pc.get("ncu", {}).get("l1_lsu_wavefronts_pct") is not None:
+            pk["binding"] = {"resource": "L1 data-pipe (LSU) wavefronts",
+                             "frac": pc["ncu"]["l1_lsu_wavefronts_pct"] / 100.0,
+                             "issue_frac": (pc["ncu"].get("issue_active_pct") or 0) / 100.0,
+                             "source": pc.get("source")}
         kernels["primary_kernel"] = pk
         dom = pk
     else:
@@ -449,6 +454,13 @@ def run_ours(args, cfg, rank, world, local):
         compact["traffic"] = cc.get("dram_bytes_per_occurrence", 0) * n_loc * K if cc else None
         if cc.get("ncu"):
             compact["ncu"] = dict(cc["ncu"], source=cc.get("source"))
+            # the resource that binds it: the L1 data pipe's wavefronts,
+            # from the committed ncu capture of the same kernel (not a live measurement)
+            if cc["ncu"].get("l1_lsu_wavefronts_pct") is not None:
+                compact["binding"] = {"resource": "L1 data-pipe (LSU) wavefronts",
+                                      "frac": cc["ncu"]["l1_lsu_wavefronts_pct"] / 100.0,
+                                      "issue_frac": (cc["ncu"].get("issue_active_pct") or 0) / 100.0,
+                                      "source": cc.get("source")}
         # the sampler: ALU-bound; achieved = the floor's algorithmic
         # lane-instructions (300 per SU sample, implementation-independent) / time
         sample = {"kernel": "sample_kernel", "bound": "alu", "unit": "Tinst/s", "kernel_ms": t_sample * 1e3,

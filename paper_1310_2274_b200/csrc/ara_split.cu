@@ -44,7 +44,14 @@ constexpr int kSampleWarps = ARA_SAMPLE_WARPS;            // sampling
 #define ARA_SAMPLE_U 2                // pairs per lane in flight per sampler round
 #endif
 constexpr int kU = ARA_SAMPLE_U;
-constexpr uint32_t kXCap = 512;       // pairs per sampler segment (a multiple of 32 kU, >= ARA_MAX_SLOTS; the
+#ifndef ARA_XCAP
+#define ARA_XCAP 512
+#endif
+constexpr uint32_t kXCap = ARA_XCAP;
+#ifndef ARA_RED_UNROLL
+#define ARA_RED_UNROLL 4
+#endif
+constexpr int kRedUnroll = ARA_RED_UNROLL;   // the run reduction's unroll       // pairs per sampler segment (a multiple of 32 kU, >= ARA_MAX_SLOTS; the
                                       // shared memory left to L1 serves the record and table gathers)
 static_assert(kXCap % (32 * kU) == 0 && kXCap >= ARA_MAX_SLOTS, "segment must hold one occurrence");
 
@@ -560,12 +567,16 @@ __device__ __forceinline__ void sample_trial(const SplitArgs &A, const SampleWs 
         __syncwarp();
         // ---- reduce: runs (line 9) and occurrence terms (line 11)
         // (an odd stretch length keeps the lanes' reads on distinct banks)
-        const uint32_t per = ((ns + 31) / 32) | 1u, i0 = min(lane * per, ns), i1 = min(i0 + per, ns);
+#ifndef ARA_ODD_STRETCH
+#define ARA_ODD_STRETCH 1
+#endif
+        const uint32_t per = ((ns + 31) / 32) | (ARA_ODD_STRETCH ? 1u : 0u), i0 = min(lane * per, ns),
+                       i1 = min(i0 + per, ns);
         RunT o = 0, head = 0;                          // (RunT: the in-stretch run sums)
         bool has_end = false;
         uint32_t head_layer = 0;
         const RunT occ_r0 = (RunT)layers[0].occ_r, occ_l0 = (RunT)layers[0].occ_l;
-#pragma unroll 2
+#pragma unroll kRedUnroll
         for (uint32_t i = i0; i < i1; ++i) {           // branch-free
             const uint32_t q = xs[i];                  // loss bits | run end << 31
             o += (RunT)__uint_as_float(q & 0x7fffffffu);

@@ -98,6 +98,14 @@ def gather_ylt(ylt, world, n_total, gathered=None, padded=None):
     return torch.cat(parts, dim=1).contiguous(), 1
 
 
+def table_shard(n_tables, rank, world):
+    """The measure tables (layers, roll-up) a rank computes in the multi-GPU
+    step: round-robin, so at 8 ranks cfg5's 9 tables cost each rank one or two
+    selects instead of nine; the (PML, TVaR, VaR) rows are then summed across
+    ranks (every other rank contributes zeros: exact)."""
+    return list(range(rank, n_tables, world))
+
+
 def launch_command(gpus, argv, port=None):
     """The command `bench.py --gpus N` re-executes itself under when started
     without a torchrun environment: one process per GPU (torch.distributed.run,
@@ -296,6 +304,15 @@ def run_ours(args, cfg, rank, world, local):
         src, n_shards = gather_ylt(ylt, world, N_total, gathered, padded)
         if slot is None:
             out = measures(src, n_shards)
+        elif world > 1 and len(layers) > 1:
+            # every rank has the whole YLT; each computes its share of the tables
+            # and the rows are summed across the ranks (zeros elsewhere: exact)
+            meas_dev[slot].zero_()
+            for i in table_shard(len(layers), rank, world):
+                ara.risk_measures_async(ctx, src, L, N_total, [layers[i]], rps=rps, n_shards=n_shards,
+                                        out=meas_dev[slot][i])
+            dist.all_reduce(meas_dev[slot], op=dist.ReduceOp.SUM)
+            out = None
         else:
             ara.risk_measures_async(ctx, src, L, N_total, layers, rps=rps, n_shards=n_shards, out=meas_dev[slot])
             out = None
@@ -552,7 +569,11 @@ def main():
     if world != args.gpus:
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; run with --gpus equal to the rank count")
     name = args.config or "cfg3"
-    cfg = aragen.load_config(name)
+    if name.endswith(".json"):                 # (a config file: test shapes of the multi-rank path)
+        with open(name) as f:
+            cfg = aragen.load_config(json.load(f))
+    else:
+        cfg = aragen.load_config(name)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
     else:

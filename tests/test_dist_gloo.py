@@ -133,3 +133,40 @@ def test_shard_range_covers_exactly():
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+
+
+def _table_shard_worker(rank, world, port, out_dir, n_tables):
+    # the multi-table measures exchange of bench.run_ours: each rank fills the
+    # (PML, TVaR, VaR) rows of its bench.table_shard share (the oracle's measures
+    # in place of ara_risk_measures_async), zeros elsewhere, then an all_reduce SUM
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    rng = np.random.default_rng(5)
+    tables = rng.lognormal(14, 1.1, (n_tables, 3000))              # the same on every rank
+    rows = torch.zeros((n_tables, 2, 3), dtype=torch.float64)
+    for i in bench.table_shard(n_tables, rank, world):
+        for q, rp in enumerate((10, 50)):
+            var, tv = OM.tvar_rp(tables[i], rp)
+            rows[i, q] = torch.tensor([OM.pml(tables[i], rp), tv, var], dtype=torch.float64)
+    dist.all_reduce(rows, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "rows.npy"), rows.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world,n_tables", [(2, 9), (3, 9), (8, 9), (3, 2)])
+def test_table_shard_measures_exchange(tmp_path, world, n_tables):
+    import bench
+    covered = sorted(i for r in range(world) for i in bench.table_shard(n_tables, r, world))
+    assert covered == list(range(n_tables))                  # every table exactly once
+    mp.spawn(_table_shard_worker, args=(world, _free_port(), str(tmp_path), n_tables), nprocs=world, join=True)
+    rows = np.load(tmp_path / "rows.npy")
+    rng = np.random.default_rng(5)
+    tables = rng.lognormal(14, 1.1, (n_tables, 3000))
+    for i in range(n_tables):
+        for q, rp in enumerate((10, 50)):
+            var, tv = OM.tvar_rp(tables[i], rp)
+            assert rows[i, q, 0] == OM.pml(tables[i], rp) and rows[i, q, 1] == tv and rows[i, q, 2] == var

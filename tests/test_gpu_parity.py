@@ -1229,7 +1229,7 @@ def test_async_errors_reported_at_synchronize(A, monkeypatch):
 
 
 # ---- multi-rank bench path through libara (ranks sharing the GPU over gloo) ----
-@pytest.mark.parametrize("cfg_name,ranks", [("cfg1", 2), ("cfg1", 3)])
+@pytest.mark.parametrize("cfg_name,ranks", [("cfg1", 2), ("cfg1", 3), ("layers5", 2), ("layers5", 3)])
 def test_bench_multirank_measures_equal(cfg_name, ranks, tmp_path):
     # bench.py's multi-rank path (trial shards with global Philox keys, the YLT
     # all-gather, measures on the gathered layout, max-over-ranks timing) with
@@ -1237,6 +1237,13 @@ def test_bench_multirank_measures_equal(cfg_name, ranks, tmp_path):
     # over gloo print the same PML / TVaR as the 1-rank run
     import json, os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if cfg_name == "layers5":                 # cfg5's shape, small: 5 layers + the roll-up = 6 tables, each
+        cfg = aragen.load_config("cfg5")      # rank computing its round-robin share (bench.table_shard)
+        cfg.update(name="layers5", n_layers=5, n_trials=3000, catalog=200000, records_per_elt=4000,
+                   layer_terms=cfg["layer_terms"][:5])
+        cfg_name = str(tmp_path / "layers5.json")
+        with open(cfg_name, "w") as f:
+            json.dump(cfg, f)
     args = ["--config", cfg_name, "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
     one = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, cwd=root,
                          capture_output=True, text=True, timeout=600)

@@ -527,7 +527,8 @@ def run_ours(args, cfg, rank, world, local):
     n_batches = int(kern_ms[-1].get("batches", 1)) if kern_ms else 1
     # libara kernels per timed step: ara_run's (counted by the library) + one joint-select
     # launch per measured table
-    gpu_launches = sum(k["launches"] for k in kern_ms) + args.steps * len(layers)
+    n_meas = len(table_shard(len(layers), rank, world)) if world > 1 and len(layers) > 1 else len(layers)
+    gpu_launches = sum(k["launches"] for k in kern_ms) + args.steps * n_meas   # (this rank's selects)
     ms = elapsed / args.steps * 1e3
     value = N_total / (elapsed / args.steps)
     line = {

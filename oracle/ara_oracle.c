@@ -18,8 +18,11 @@
  * the closed-form mean/variance of the loss draw, and a brute-force
  * straight-line Python engine on tiny portfolios.
  *
- * Parity-unpinned parts (no value printed by the paper): the RNG keying
- * (reading G2/G4) -- pinned only distributionally.
+ * What no paper number can confirm: the RNG keying is a reading (G2/G4), not
+ * a value the paper prints.  Its implementation here is pinned (Random123
+ * known-answer vectors; an independent brute-force engine with its own
+ * Philox and keying; the distribution of the draws), but the paper prints no
+ * config-level YLT/PML/TVaR to check the reading itself against.
  */
 #include <math.h>
 #include <pthread.h>

@@ -565,7 +565,7 @@ def test_event_out_of_range(A, ctx):
 
 
 # ---- row a12: PML / TVaR -------------------------------------------------------
-@pytest.mark.parametrize("n", [1, 7, 1000, 100003, 800000])
+@pytest.mark.parametrize("n", [1, 7, 1000, 100003, 800000, 3000001])
 def test_measures_vs_oracle_sort(A, ctx, n):
     import torch
     rng = np.random.default_rng(n)

@@ -300,7 +300,9 @@ def run_ours(args, cfg, rank, world, local):
         # slot None: the measures read back synchronously (the e2e path);
         # slot s: ara_risk_measures_async into device row s (read back once after
         # the timed steps) -- the steps queue back to back, one sync at the end
-        ara.run(ctx, P, Yx, seed=cfg["seed"], su=cfg["su"], ylt=ylt, async_=True)
+        # (the profiled pass runs synchronously: a grouped portfolio's per-group
+        # kernel times are summed only then)
+        ara.run(ctx, P, Yx, seed=cfg["seed"], su=cfg["su"], ylt=ylt, async_=not profiled)
         if profiled:
             m0 = torch.cuda.Event(enable_timing=True); m1 = torch.cuda.Event(enable_timing=True)
             m0.record(stream)

@@ -72,7 +72,10 @@ extern "C" {
                                 errors, non-convergence and an exhausted pool
                                 are latched and reported by the next
                                 ara_ctx_synchronize.  ara_last_run_timings
-                                waits for the run.                            */
+                                waits for the run (for a portfolio of several
+                                kernel groups: the last group's times; a
+                                synchronous run sums them).  Every launch of
+                                such a run can be captured into a CUDA graph. */
 #define ARA_RNG_SUPPLIED 128u /* the paper's data model: z_(Prog,E)
                                 of each YET occurrence and z_(E) of each XELT
                                 record are inputs, supplied by ara_yet_set_z

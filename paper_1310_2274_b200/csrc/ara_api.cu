@@ -980,12 +980,17 @@ static int run_impl(ara_ctx *c, const ara_portfolio *p, const ara_yet *y, uint64
                                  occ_max ? occ_max + off : nullptr, dbg_count ? dbg_count + off : nullptr,
                                  dbg_hash ? dbg_hash + off : nullptr);
         if (st != ARA_OK) return st;
-        CU(compute_timings(c));          // (an ARA_ASYNC run of a grouped portfolio waits for each group here)
-        for (int k = 0; k < 3; ++k) ms[k] += c->last_ms[k];
         launches += c->last_launches;
         batches += c->last_batches;
+        // a synchronous run sums the groups' kernel times; an ARA_ASYNC run
+        // must not wait (nor may a run being captured into a CUDA graph): its
+        // ara_last_run_timings are those of the last group
+        if (flags & ARA_ASYNC) continue;
+        CU(compute_timings(c));
+        for (int k = 0; k < 3; ++k) ms[k] += c->last_ms[k];
     }
-    for (int k = 0; k < 3; ++k) c->last_ms[k] = ms[k];
+    if (!(flags & ARA_ASYNC))
+        for (int k = 0; k < 3; ++k) c->last_ms[k] = ms[k];
     c->last_launches = launches;
     c->last_batches = batches;
     return ARA_OK;

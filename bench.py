@@ -399,35 +399,64 @@ def run_ours(args, cfg, rank, world, local):
     ara.prepare(ctx, P, Ys[1], su=cfg["su"], async_=True)
 
     def e2e(bits):
-        if bits < 32:
+        # The copy stream moves each step's YET from pinned host memory while the
+        # compute stream runs the previous step (double buffers, ordered by
+        # events, no host synchronisation inside the timed loop):
+        #   packed (bits < 32): H2D of the packed words into a device staging
+        #     buffer; the compute stream unpacks them into the step's YET
+        #     (ara_yet_refill_packed from device words), so the copy engine
+        #     moves the next step's words while this step unpacks and runs
+        #   uint32 (bits = 32): H2D straight into the step's YET (ara_yet_refill)
+        # Every step reads its YLT and its measures back (async D2H into pinned
+        # memory); one synchronisation at the end.
+        packed = bits < 32
+        if packed:
             words = (n_loc * K * bits + 31) // 32
             up_host = torch.empty(words, dtype=torch.int32).pin_memory()
             aragen.pack_yet(ev_host.numpy().view(np.uint32), bits, out=up_host.numpy().view(np.uint32))
+            stage = [torch.empty(words, dtype=torch.int32, device=dev) for _ in range(2)]
             h2d = words * 4
-
-            def upload(Yx):
-                Yx.refill_packed(up_host, bits, ctx=ctx_copy)
         else:
             h2d = n_loc * K * 4
+        ev_up = [torch.cuda.Event() for _ in range(2)]
+        ev_free = [torch.cuda.Event() for _ in range(2)]
+        meas_e2e = torch.empty((len(layers), len(rps), 3), dtype=torch.float64).pin_memory()
 
-            def upload(Yx):
-                Yx.refill(ev_host, ctx=ctx_copy)
-        for Yx in Ys:                                # untimed: the upload path's staging is allocated once
-            upload(Yx)
-        ctx_copy.synchronize()
+        def upload(b):                                  # on the copy stream
+            with torch.cuda.stream(copy_stream):
+                if packed:
+                    stage[b].copy_(up_host, non_blocking=True)
+                else:
+                    Ys[b].refill(ev_host, ctx=ctx_copy)
+                ev_up[b].record(copy_stream)
+
+        for b in range(2):                              # untimed: every buffer touched once
+            upload(b)
+            stream.wait_event(ev_up[b])
+            if packed:
+                Ys[b].refill_packed(stage[b], bits, ctx=ctx)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         te0 = torch.cuda.Event(enable_timing=True); te1 = torch.cuda.Event(enable_timing=True)
         te0.record(stream)
         copy_stream.wait_event(te0)
-        upload(Ys[0])                               # H2D of step 0's YET
+        upload(0)                                       # H2D of step 0's YET
         for s_ in range(e2e_steps):
-            ctx_copy.synchronize()                  # step s's YET is on the device
-            if s_ + 1 < e2e_steps:
-                upload(Ys[(s_ + 1) % 2])            # H2D of step s+1 overlaps step s
-            step(Ys[s_ % 2])
-            ylt_host.copy_(ylt, non_blocking=True)  # D2H of the step's result
+            b = s_ % 2
+            if s_ + 1 < e2e_steps:                      # H2D of step s+1 overlaps step s
+                if s_ >= 1:
+                    copy_stream.wait_event(ev_free[1 - b])   # (its buffer's previous step is done with it)
+                upload(1 - b)
+            stream.wait_event(ev_up[b])
+            if packed:
+                Ys[b].refill_packed(stage[b], bits, ctx=ctx)     # unpack on the compute stream
+                ev_free[b].record(stream)
+            step(Ys[b], slot=0)
+            if not packed:
+                ev_free[b].record(stream)
+            ylt_host.copy_(ylt, non_blocking=True)      # D2H of the step's results
+            meas_e2e.copy_(meas_dev[0], non_blocking=True)
         te1.record(stream)
         torch.cuda.synchronize()
         ctx.synchronize()
@@ -437,15 +466,16 @@ def run_ours(args, cfg, rank, world, local):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t[0])
         return {"value": N_total / (el / e2e_steps), "unit": "trials/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": L * n_loc * 4 + 16 * len(rps) * len(layers), "steps": e2e_steps,
+                "d2h_bytes_per_step": L * n_loc * 4 + 24 * len(rps) * len(layers), "steps": e2e_steps,
                 "yet_upload_bits": bits}
     bits = aragen.yet_bits(cfg["catalog"]) if not args.plain_upload else 32
     e2e_main = e2e(bits)
-    e2e_main["how"] = (("pinned host YET stored bit-packed at %d bits per event id, copied every step and "
-                        "unpacked on the device (ara_yet_refill_packed)" % bits) if bits < 32 else
-                       "pinned host YET (uint32 ids) copied every step (ara_yet_refill)") + \
-        " on a second stream into a double-buffered device YET (step s+1's H2D overlaps step s), " \
-        "ara_run + all-gather + measures, YLT read back every step"
+    e2e_main["how"] = (("pinned host YET stored bit-packed at %d bits per event id, copied every step into "
+                        "device words on a copy stream and unpacked by the compute stream "
+                        "(ara_yet_refill_packed from device memory)" % bits) if bits < 32 else
+                       "pinned host YET (uint32 ids) copied every step on a copy stream (ara_yet_refill)") + \
+        ", double-buffered (step s+1's H2D overlaps step s), ara_run + all-gather + measures, YLT and " \
+        "measures read back every step (async D2H), one synchronisation at the end"
     if bits < 32:                                   # the plain uint32 encoding beside it
         e2e_main["plain_uint32"] = e2e(32)
     del Ys[1]

@@ -217,8 +217,11 @@ int ara_yet_refill(ara_ctx *ctx, ara_yet *yet, const uint32_t *event_ids);
  * [x*bits, (x+1)*bits) of the little-endian uint32 word stream `packed`
  * (ceil(total*bits/32) words, host or device), bits in [1, 32]; with
  * bits = ceil(log2 catalog) the host->device copy moves bits/32 of the bytes
- * of ara_yet_refill.  The words are staged on the device and unpacked there
- * by a kernel; asynchronous like ara_yet_refill.  Ids >= catalog_size are
+ * of ara_yet_refill.  Host words are staged on the device, device words are
+ * read where they are (they must stay valid until the context stream passes
+ * the unpack: a caller may copy host words into its own device buffer on
+ * another stream and overlap that copy with earlier work); a kernel unpacks
+ * them; asynchronous like ara_yet_refill.  Ids >= catalog_size are
  * caught by ara_run (ARA_ERANGE).  ARA_EINVAL for bits out of range. */
 int ara_yet_refill_packed(ara_ctx *ctx, ara_yet *yet, uint32_t bits, const uint32_t *packed);
 /* The paper's YET tuples (E, t, z_(Prog,E)): attach the

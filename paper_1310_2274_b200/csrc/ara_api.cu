@@ -826,18 +826,19 @@ int ara_yet_refill_packed(ara_ctx *c, ara_yet *y, uint32_t bits, const uint32_t 
     if (!packed) return fail(ARA_EINVAL, "packed is NULL");
     const uint64_t words = (y->dev.n_events * (uint64_t)bits + 31) / 32;
     CU(enter_device(c->device));
-    if (y->packed_capacity < words + 2) {              // staging grows once, then is reused
-        cudaFree(y->d_packed);
-    cudaFree(y->d_zprog);
-        y->d_packed = nullptr;
-        y->packed_capacity = 0;
-        CU(dalloc(&y->d_packed, words + 2));
-        y->packed_capacity = words + 2;
-    }
-    CU(cudaMemsetAsync(y->d_packed + words, 0, 2 * sizeof(uint32_t), c->stream));   // read past the end
-    CU(cudaMemcpyAsync(y->d_packed, packed, words * sizeof(uint32_t),
-                       is_device_ptr(packed) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
-    CU(launch_unpack_yet(y->d_packed, y->dev.n_events, bits, y->d_events, c->stream, c->num_sms));
+    const uint32_t *src = packed;
+    if (!is_device_ptr(packed)) {                       // host words: staged on the device first
+        if (y->packed_capacity < words) {              // (the staging grows once, then is reused)
+            cudaFree(y->d_packed);
+            y->d_packed = nullptr;
+            y->packed_capacity = 0;
+            CU(dalloc(&y->d_packed, words));
+            y->packed_capacity = words;
+        }
+        CU(cudaMemcpyAsync(y->d_packed, packed, words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+        src = y->d_packed;
+    }                                                   // device words: unpacked where they are
+    CU(launch_unpack_yet(src, y->dev.n_events, bits, y->d_events, c->stream, c->num_sms));
     CU(launch_yet_max(y->d_events, y->dev.n_events, y->d_max, c->stream, c->num_sms));
     return ARA_OK;
 }

@@ -793,7 +793,7 @@ cudaError_t launch_ovf_plan(RunStatus *status, const uint32_t *ovf_n, uint64_t *
 // per id -> uint32 event ids.  Four ids per thread, one 16 B store; the
 // packed words are read through L1 (each word serves ~32/bits ids).
 __global__ void unpack_yet_kernel(const uint32_t *__restrict__ packed, uint64_t n, uint32_t bits,
-                                  uint32_t *__restrict__ out) {
+                                  uint64_t words, uint32_t *__restrict__ out) {
     const uint32_t mask = bits == 32u ? 0xffffffffu : (1u << bits) - 1u;
     const uint64_t n4 = (n + 3) / 4;
     for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n4; q += (uint64_t)gridDim.x * blockDim.x) {
@@ -803,7 +803,10 @@ __global__ void unpack_yet_kernel(const uint32_t *__restrict__ packed, uint64_t 
             const uint64_t x = 4 * q + j, bit = x * (uint64_t)bits, w = bit >> 5;
             const uint32_t sh = (uint32_t)(bit & 31u);
             uint32_t lo = 0u, hi = 0u;
-            if (x < n) { lo = __ldg(packed + w); hi = __ldg(packed + w + 1); }   // (+2 words of padding)
+            if (x < n) {                                 // (no read past the packed words)
+                lo = __ldg(packed + w);
+                hi = w + 1 < words ? __ldg(packed + w + 1) : 0u;
+            }
             v[j] = __funnelshift_r(lo, hi, sh) & mask;
         }
         reinterpret_cast<uint4 *>(out)[q] = make_uint4(v[0], v[1], v[2], v[3]);   // (+4 words of padding)
@@ -813,7 +816,8 @@ __global__ void unpack_yet_kernel(const uint32_t *__restrict__ packed, uint64_t 
 cudaError_t launch_unpack_yet(const uint32_t *packed, uint64_t n, uint32_t bits, uint32_t *out, cudaStream_t s,
                               int num_sms) {
     if (n == 0) return cudaSuccess;
-    unpack_yet_kernel<<<num_sms * 8, 256, 0, s>>>(packed, n, bits, out);
+    const uint64_t words = (n * (uint64_t)bits + 31) / 32;
+    unpack_yet_kernel<<<num_sms * 8, 256, 0, s>>>(packed, n, bits, words, out);
     return cudaGetLastError();
 }
 

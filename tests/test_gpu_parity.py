@@ -865,6 +865,15 @@ def test_packed_refill_matches_plain(A, ctx, ragged):
         got = A.run(ctx, P, Y, seed=cfg["seed"], debug=True)
         for a, b in zip(got, ref):
             assert np.array_equal(a.cpu().numpy(), b.cpu().numpy()), bits
+        # the same words from device memory (unpacked where they are, no staging):
+        # an exact-size buffer, so the unpack must not read past its last word
+        import torch
+        dw = torch.from_numpy(np.ascontiguousarray(words).view(np.int32)).cuda()
+        Y.refill(np.zeros(yet["events"].size, np.uint32))
+        Y.refill_packed(dw, bits)
+        got = A.run(ctx, P, Y, seed=cfg["seed"], debug=True)
+        for a, b in zip(got, ref):
+            assert np.array_equal(a.cpu().numpy(), b.cpu().numpy()), ("device words", bits)
 
 
 def test_packed_refill_errors(A, ctx):
@@ -1075,6 +1084,29 @@ def test_supplied_z_vs_oracle(A, ctx, case):
     # the seed plays no part: the numbers come with the inputs
     g2 = A.run(ctx, P, Y, seed=cfg["seed"] + 99, rng="supplied").cpu().numpy()
     assert np.array_equal(g2, A.run(ctx, P, Y, seed=cfg["seed"], rng="supplied").cpu().numpy())
+
+
+def test_supplied_z_survives_packed_refill(A, ctx):
+    # the YET's supplied z_(Prog,E) stay attached when its ids are re-uploaded
+    # from a packed copy (the staging buffer grows on the first packed upload:
+    # it once freed the z array with it -- a dangling pointer and a double free)
+    cfg = aragen.load_config("cfg1")
+    pf, yet = aragen.build_portfolio(cfg), aragen.build_yet(cfg)
+    rng = np.random.default_rng(7)
+    zp = ((rng.integers(0, 2 ** 23, (1, yet["events"].size)) * 2 + 1) * 2.0 ** -24).astype(np.float32)
+    ze = ((rng.integers(0, 2 ** 23, pf["rec_event"].size) * 2 + 1) * 2.0 ** -24).astype(np.float32)
+    P, Y = A.Portfolio(ctx, pf), A.Yet.from_dict(ctx, yet)
+    P.set_z(ze)
+    Y.set_z(zp)
+    before = A.run(ctx, P, Y, seed=1, rng="supplied").cpu().numpy()
+    bits = aragen.yet_bits(cfg["catalog"])
+    Y.refill_packed(aragen.pack_yet(np.ascontiguousarray(yet["events"], np.uint32), bits), bits)
+    filler = A.Portfolio(ctx, pf)                 # allocations that could reuse a freed z array
+    after = A.run(ctx, P, Y, seed=1, rng="supplied").cpu().numpy()
+    assert np.array_equal(before, after)
+    del filler, Y                                 # destroy: no double free, no error left behind
+    P2 = A.Portfolio(ctx, pf)
+    assert P2.info()["n_device_records"] > 0
 
 
 def test_supplied_z_errors(A, ctx):

@@ -47,12 +47,12 @@ constexpr int kU = ARA_SAMPLE_U;
 #ifndef ARA_XCAP
 #define ARA_XCAP 512
 #endif
-constexpr uint32_t kXCap = ARA_XCAP;
+constexpr uint32_t kXCap = ARA_XCAP;    // pairs per sampler segment (a multiple of 32 kU, >= ARA_MAX_SLOTS; the
+                                        // shared memory left to L1 serves the record and table gathers)
 #ifndef ARA_RED_UNROLL
 #define ARA_RED_UNROLL 4
 #endif
-constexpr int kRedUnroll = ARA_RED_UNROLL;   // the run reduction's unroll       // pairs per sampler segment (a multiple of 32 kU, >= ARA_MAX_SLOTS; the
-                                      // shared memory left to L1 serves the record and table gathers)
+constexpr int kRedUnroll = ARA_RED_UNROLL;   // the run reduction's unroll
 static_assert(kXCap % (32 * kU) == 0 && kXCap >= ARA_MAX_SLOTS, "segment must hold one occurrence");
 
 __device__ __forceinline__ uint64_t splitmix64_(uint64_t z) {

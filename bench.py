@@ -393,6 +393,7 @@ def run_ours(args, cfg, rank, world, local):
     # the YET: bit-packed at ceil(log2 catalog) bits per id (unpacked on the
     # device by ara_yet_refill_packed) and plain uint32 ids (ara_yet_refill).
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 5))
+    ylt_ref = ylt.cpu()                                # the device-resident run's YLT (checked below)
     copy_stream = torch.cuda.Stream(dev)
     ctx_copy = ara.Context(local, copy_stream)
     Ys = [Y, ara.Yet(ctx, ev_host, fixed_len=K, first_trial=lo, n_trials=n_loc)]
@@ -465,6 +466,14 @@ def run_ours(args, cfg, rank, world, local):
             t = torch.tensor([el], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t[0])
+        # the last e2e step's read-back equals the device-resident run's results
+        if not torch.equal(ylt_host, ylt_ref):
+            raise RuntimeError(f"e2e ({bits}-bit upload): YLT read back differs from the device-resident run")
+        for i in range(len(layers)):
+            got = [tuple(float(meas_e2e[i, q, c]) for q in range(len(rps))) for c in (0, 1)]
+            want = [tuple(float(x) for x in res[i][0]), tuple(float(x) for x in res[i][1])]
+            if got != want:
+                raise RuntimeError(f"e2e ({bits}-bit upload) table {layers[i]}: measures {got} != {want}")
         return {"value": N_total / (el / e2e_steps), "unit": "trials/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": L * n_loc * 4 + 24 * len(rps) * len(layers), "steps": e2e_steps,
                 "yet_upload_bits": bits}
@@ -475,7 +484,8 @@ def run_ours(args, cfg, rank, world, local):
                         "(ara_yet_refill_packed from device memory)" % bits) if bits < 32 else
                        "pinned host YET (uint32 ids) copied every step on a copy stream (ara_yet_refill)") + \
         ", double-buffered (step s+1's H2D overlaps step s), ara_run + all-gather + measures, YLT and " \
-        "measures read back every step (async D2H), one synchronisation at the end"
+        "measures read back every step (async D2H), one synchronisation at the end; the last step's " \
+        "read-back checked equal to the device-resident run"
     if bits < 32:                                   # the plain uint32 encoding beside it
         e2e_main["plain_uint32"] = e2e(32)
     del Ys[1]

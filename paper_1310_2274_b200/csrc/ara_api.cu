@@ -265,7 +265,7 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
         dalloc(&c->ms.buf, kSortCap) != cudaSuccess || dalloc(&c->ms.hist, 4 * 256) != cudaSuccess ||
         dalloc(&c->ms.state, 1) != cudaSuccess || dalloc(&c->ms.d_rps, 64) != cudaSuccess ||
         dalloc(&c->ms.d_out, kOutDoubles) != cudaSuccess ||
-        dalloc(&c->ms.mhist, 4 * kMaxPlanRanks * 256) != cudaSuccess || dalloc(&c->ms.macc, 8) != cudaSuccess ||
+        dalloc(&c->ms.mhist, kMultiHistWords) != cudaSuccess || dalloc(&c->ms.macc, 8) != cudaSuccess ||
         dalloc(&c->ms.states, kMaxRanks) != cudaSuccess ||
         dalloc(&c->ms.part_sum, kRedBlocks) != cudaSuccess ||
         dalloc(&c->ms.part_cnt, kRedBlocks) != cudaSuccess || cudaEventCreate(&c->ev[0]) != cudaSuccess ||
@@ -280,6 +280,14 @@ int ara_ctx_create(int device, void *cuda_stream, ara_ctx **out) {
             ara_ctx_destroy(c);
             return fail(ARA_ECUDA, "event creation failed in ara_ctx_create");
         }
+    // the joint select's histograms and tail sums start zeroed; each launch
+    // leaves them zeroed for the next (select_multi_kernel)
+    if (cudaMemset(c->ms.mhist, 0, kMultiHistWords * sizeof(unsigned int)) != cudaSuccess ||
+        cudaMemset(c->ms.macc, 0, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+        ara_ctx_destroy(c);
+        return fail(ARA_ECUDA, "scratch initialisation failed in ara_ctx_create");
+    }
     *out = c;
     return ARA_OK;
 }

@@ -199,8 +199,9 @@ __global__ void __launch_bounds__(256) select_coop_kernel(const float *ylt, uint
 
 // ---- every needed order statistic in one cooperative launch (n_rp <= 4) ----
 // The host plans the ranks (PML's L(fl), L(fl+1), VaR = L(m) per return
-// period, L(1), L(N); G13b); four 8-bit radix passes select all of them at
-// once -- ranks that share a key prefix share a histogram -- and a last pass
+// period, L(1), L(N); G13b); three radix passes (digits of 12, 10 and 10
+// bits: one 4096-bin histogram for every rank, then 1024 bins per group of
+// ranks that share a key prefix) select all of them at once, and a last pass
 // forms the TVaR tail sums as int64 fixed-point sums (order-independent, so
 // exact and deterministic under atomics).  No tail buffer, no sort, no rank
 // limit (deep return periods take the same path).
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(256) select_coop_kernel(const float *ylt, uint
 #define ARA_MULTI_THREADS 1024
 #endif
 constexpr int kMultiThreads = ARA_MULTI_THREADS;     // one block per SM: cheap grid barriers
+constexpr uint32_t kMultiSmemWords = kMaxPlanRanks * 1024u;   // >= 4096 (pass 0)
 
 struct __align__(8) MeasPlan {
     uint64_t rank[kMaxPlanRanks];                  // distinct ranks (1-based, descending order)
@@ -217,13 +219,71 @@ struct __align__(8) MeasPlan {
     uint32_t nr, nq;
 };
 
+// one warp: the digit of the need-th largest key among a group's nb bins (a
+// shared-memory histogram, nb = 1024 or 4096), by two levels of warp scans:
+// lane L first sums the nb/32 bins nb-1-(nb/32)L .. nb-(nb/32)(L+1) (read in a
+// rotated order, so the lanes hit distinct banks), then the lanes split the
+// chunk holding the rank.  As pick_digit: a group with fewer than need keys
+// takes the lowest digit.
+__device__ __forceinline__ void pick_digit_smem(const unsigned int *hs, uint32_t nb, int shift, uint64_t &need,
+                                                uint32_t &prefix) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t per = nb >> 5, sub = per >> 5;     // bins per lane: 128 / 32; second level 4 / 1
+    const uint32_t base = nb - per * (uint32_t)(lane + 1);
+    uint32_t tot = 0;
+    for (uint32_t j = 0; j < per; ++j) tot += hs[base + ((j + (uint32_t)lane) & (per - 1u))];
+    uint64_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint64_t before = incl - tot;               // keys in higher bins
+    const unsigned hit = __ballot_sync(0xffffffffu, before < need && need <= incl);
+    uint32_t d = 0;
+    uint64_t rem;
+    if (hit) {
+        const int L = __ffs(hit) - 1;
+        rem = need - __shfl_sync(0xffffffffu, before, L);            // 1 <= rem <= the chunk's keys
+        const uint32_t top = nb - 1u - per * (uint32_t)L;            // the chunk's highest bin
+        uint32_t c[4], t2 = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            c[r] = (uint32_t)r < sub ? hs[top - (uint32_t)lane * sub - (uint32_t)r] : 0u;
+            t2 += c[r];
+        }
+        uint64_t incl2 = t2;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, incl2, o);
+            if (lane >= o) incl2 += y;
+        }
+        const uint64_t before2 = incl2 - t2;
+        const int L2 = __ffs(__ballot_sync(0xffffffffu, before2 < rem && rem <= incl2)) - 1;
+        if (lane == L2) {
+            rem -= before2;
+            d = top - (uint32_t)lane * sub;
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                if ((uint32_t)r + 1u < sub && rem > c[r]) { rem -= c[r]; --d; } else break;
+        }
+        d = __shfl_sync(0xffffffffu, d, L2);
+        rem = __shfl_sync(0xffffffffu, rem, L2);
+    } else {                                          // fewer keys than need: the lowest digit
+        const uint64_t all = __shfl_sync(0xffffffffu, incl, 31);
+        rem = need - (all - hs[0]);
+    }
+    need = rem;
+    prefix |= d << shift;
+}
+
 __global__ void __launch_bounds__(kMultiThreads) select_multi_kernel(const float *ylt, uint32_t n_layers, uint64_t per,
                                                            uint32_t n_shards, int32_t layer, float *vals,
                                                            const __grid_constant__ MeasPlan M,
                                                            unsigned int *ghist, unsigned long long *gacc,
                                                            uint64_t n_total, double *out) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ unsigned int h[kMaxPlanRanks][256];
+    extern __shared__ unsigned int h[];               // kMultiSmemWords: a pass's block histograms
     __shared__ uint64_t s_need[kMaxPlanRanks];
     __shared__ uint32_t s_prefix[kMaxPlanRanks];
     __shared__ int s_grp[kMaxPlanRanks];
@@ -234,21 +294,22 @@ __global__ void __launch_bounds__(kMultiThreads) select_multi_kernel(const float
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + tid, gstride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t wbase = gtid - lane;               // warp-uniform loop base
-    for (uint64_t i = gtid; i < 4ull * kMaxPlanRanks * 256; i += gstride) ghist[i] = 0u;
-    if (gtid < 8) gacc[gtid] = 0ull;
+    // (ghist and gacc arrive zeroed: ara_ctx_create, then the end of every launch)
     if (tid < kMaxPlanRanks) { s_need[tid] = M.rank[tid]; s_prefix[tid] = 0u; }
-    grid.sync();
+    __syncthreads();
     uint32_t pmask = 0u;
-    for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
-        unsigned int *hist = ghist + pass * kMaxPlanRanks * 256;
+    for (int pass = 0; pass < 3; ++pass) {             // digits of 12, 10, 10 bits
+        const int width = pass == 0 ? 12 : 10, shift = pass == 0 ? 20 : pass == 1 ? 10 : 0;
+        const uint32_t nb = 1u << width;
+        const uint32_t ng = pass == 0 ? 1u : (uint32_t)nr;   // (pass 0: every rank in group 0)
+        unsigned int *hist = ghist + (pass == 0 ? 0u : 4096u + (uint32_t)(pass - 1) * kMaxPlanRanks * 1024u);
         if (tid < kMaxPlanRanks) {                     // group = first rank with the same prefix
             int g = (int)tid;
             for (int i = 0; i < (int)tid; ++i)
                 if (s_prefix[i] == s_prefix[tid]) { g = i; break; }
             s_grp[tid] = g;
         }
-        for (uint32_t i = tid; i < kMaxPlanRanks * 256u; i += blockDim.x) (&h[0][0])[i] = 0u;
+        for (uint32_t i = tid; i < ng * nb; i += blockDim.x) h[i] = 0u;
         __syncthreads();
         uint32_t gp[kMaxPlanRanks];                    // group leaders' prefixes in registers
 #pragma unroll
@@ -274,25 +335,26 @@ __global__ void __launch_bounds__(kMultiThreads) select_multi_kernel(const float
                 const uint32_t k = okey(v), kp = k & pmask;
 #pragma unroll
                 for (int g = kMaxPlanRanks - 1; g >= 0; --g)   // groups are disjoint
-                    if (kp == gp[g]) gd = (uint32_t)g << 8 | ((k >> shift) & 0xffu);
+                    if (kp == gp[g]) gd = (uint32_t)g << 12 | ((k >> shift) & (nb - 1u));
             }
             const unsigned peers = __match_any_sync(0xffffffffu, gd);
             if (gd != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
-                atomicAdd(&h[gd >> 8][gd & 0xffu], (unsigned)__popc(peers));
+                atomicAdd(&h[(gd >> 12) * nb + (gd & 0xfffu)], (unsigned)__popc(peers));
         }
         __syncthreads();
-        for (uint32_t i = tid; i < (uint32_t)nr * 256u; i += blockDim.x)
-            if ((&h[0][0])[i]) atomicAdd(&hist[i], (&h[0][0])[i]);
+        for (uint32_t i = tid; i < ng * nb; i += blockDim.x)
+            if (h[i]) atomicAdd(&hist[i], h[i]);
         grid.sync();
-        if ((int)warp < nr) {                          // every block: the digits of its ranks
-            for (int r = (int)warp; r < nr; r += (int)(blockDim.x >> 5)) {
-                uint64_t need = s_need[r];
-                uint32_t prefix = s_prefix[r], pm = pmask;
-                pick_digit(hist + s_grp[r] * 256, shift, need, prefix, pm);
-                if (lane == 0) { s_need[r] = need; s_prefix[r] = prefix; }
-            }
+        for (uint32_t i = tid; i < ng * nb; i += blockDim.x)   // the leaders' global histograms
+            if (s_grp[i >> width] == (int)(i >> width)) h[i] = __ldcg(&hist[i]);
+        __syncthreads();
+        for (int r = (int)warp; r < nr; r += (int)(blockDim.x >> 5)) {   // every block: its ranks' digits
+            uint64_t need = s_need[r];
+            uint32_t prefix = s_prefix[r];
+            pick_digit_smem(h + (pass == 0 ? 0u : (uint32_t)s_grp[r] * nb), nb, shift, need, prefix);
+            if (lane == 0) { s_need[r] = need; s_prefix[r] = prefix; }
         }
-        pmask |= 0xffu << shift;
+        pmask |= (nb - 1u) << shift;
         __syncthreads();
     }
     // TVaR tail sums: entries >= VaR (ties included), fixed point v * 2^E
@@ -332,6 +394,8 @@ __global__ void __launch_bounds__(kMultiThreads) select_multi_kernel(const float
         if (sc) atomicAdd(&gacc[4 + tid], sc);
     }
     grid.sync();
+    // every block is past its last histogram read: zero them for the next launch
+    for (uint64_t i = gtid; i < kMultiHistWords; i += gstride) ghist[i] = 0u;
     if (blockIdx.x == 0 && tid < (uint32_t)nq) {
         const int q = (int)tid;
         auto L = [&](int i) -> double { return (double)okey_inv(s_prefix[i]); };
@@ -345,6 +409,10 @@ __global__ void __launch_bounds__(kMultiThreads) select_multi_kernel(const float
         out[3 * q] = pml;
         out[3 * q + 1] = sum / (double)__ldcg(&gacc[4 + q]);
         out[3 * q + 2] = L(M.i_m[q]);
+    }
+    if (blockIdx.x == 0) {                            // (block 0 alone read the tail sums)
+        __syncthreads();
+        if (tid < 8) gacc[tid] = 0ull;
     }
 }
 
@@ -388,7 +456,10 @@ cudaError_t launch_measures_multi(const float *ylt, uint32_t n_layers, uint64_t 
     if (!blocks) {
         int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_multi_kernel, kMultiThreads, 0);
+        cudaFuncSetAttribute(select_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kMultiSmemWords * sizeof(unsigned int)));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_multi_kernel, kMultiThreads,
+                                                      kMultiSmemWords * sizeof(unsigned int));
         blocks = sms * std::min(per_sm, 1);           // one block per SM (0 if it cannot be resident)
         if (!blocks) return cudaErrorCooperativeLaunchTooLarge;
     }
@@ -399,7 +470,8 @@ cudaError_t launch_measures_multi(const float *ylt, uint32_t n_layers, uint64_t 
     uint64_t nt = n_total;
     void *args[] = {(void *)&ylt, (void *)&n_layers, (void *)&per, (void *)&n_shards, (void *)&layer,
                     (void *)&vals, (void *)&M, (void *)&hist, (void *)&acc, (void *)&nt, (void *)&d_out};
-    return cudaLaunchCooperativeKernel((void *)select_multi_kernel, dim3(blocks), dim3(kMultiThreads), args, 0, s);
+    return cudaLaunchCooperativeKernel((void *)select_multi_kernel, dim3(blocks), dim3(kMultiThreads), args,
+                                       kMultiSmemWords * sizeof(unsigned int), s);
 }
 
 // one CTA of 1024 threads: bitonic sort (descending) of P = 1024 E values,

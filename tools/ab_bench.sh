@@ -6,5 +6,5 @@ for L in "$@"; do
   ARA_LIB_PATH=$PWD/$L timeout 300 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); r=d['roofline']['kernels']
-print('$L', round(d['ms_per_step'],3), 'compact', round(r['compact_kernel']['kernel_ms'],3), 'sample', round(r['sample_kernel']['kernel_ms'],3), d['clocks']['sm_mhz'])"
+print('$L', round(d['ms_per_step'],4), ' '.join(f'{k} {round(v[\"kernel_ms\"],4)}' for k, v in r.items() if isinstance(v, dict)), d['clocks']['sm_mhz'])"
 done

@@ -586,6 +586,52 @@ def test_measures_vs_oracle_sort(A, ctx, n):
         assert var[q] == vo                     # an order statistic: exact
 
 
+def _adversarial_table(kind, n, rng):
+    """Tables whose keys stress the joint select's digit boundaries (12-, 10-, 10-bit
+    digits of the order-preserving key): ties, keys that differ only in the low
+    digit or only across a digit boundary, negative values, subnormals."""
+    if kind == "all_equal":
+        return np.full(n, 123456.75, dtype=np.float32)
+    if kind == "low_bits":            # one high prefix, the last 10 bits random
+        base = np.float32(7.5e6).view(np.uint32) & ~np.uint32(0x3ff)
+        return (base | rng.integers(0, 1024, n, dtype=np.uint32)).view(np.float32)
+    if kind == "digit_edges":         # keys at +-1 ulp around 2^10 / 2^20 key boundaries
+        base = np.float32(3.0e7).view(np.uint32) & ~np.uint32(0xfffff)
+        off = rng.choice(np.array([0, 1, 0x3ff, 0x400, 0x401, 0xfffff, 0x100000, 0x100001], np.uint32), n)
+        return (base - np.uint32(0x100000) + off).view(np.float32)
+    if kind == "signed":              # negative and positive values, zeros of both signs
+        x = (rng.standard_normal(n) * 1e5).astype(np.float32)
+        x[rng.uniform(size=n) < 0.05] = np.float32(-0.0)
+        x[rng.uniform(size=n) < 0.05] = np.float32(0.0)
+        return x
+    if kind == "subnormal":           # mostly zero, a tail of subnormal and tiny normal values
+        x = np.zeros(n, dtype=np.float32)
+        m = rng.uniform(size=n) < 0.3
+        x[m] = rng.integers(1, 1 << 23, int(m.sum()), dtype=np.uint32).view(np.float32)
+        x[rng.uniform(size=n) < 0.01] = np.float32(2.0e-30)
+        return x
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["all_equal", "low_bits", "digit_edges", "signed", "subnormal"])
+@pytest.mark.parametrize("n", [1000, 100003, 800000])
+def test_measures_adversarial_keys(A, ctx, kind, n):
+    # the joint select (<= 4 return periods) and the tail-sort path (> 4) against
+    # the oracle's sort: VaR exact, PML to rounding, TVaR to the fixed-point sum
+    import torch
+    rng = np.random.default_rng([n, len(kind), ord(kind[0])])
+    x = _adversarial_table(kind, n, rng)
+    d = torch.from_numpy(x).cuda()
+    for rps in ([100, 250, 500], [2, 10, 100, 250, 500]):
+        pml, tvar, var = A.risk_measures_var(ctx, d, 1, n, 0, rps=rps)
+        x64 = x.astype(np.float64)
+        for q, rp in enumerate(rps):
+            vo, to = OM.tvar_rp(x64, rp)
+            assert var[q] == vo, (kind, n, rp)
+            assert pml[q] == pytest.approx(OM.pml(x64, rp), rel=1e-12, abs=0.0)
+            assert tvar[q] == pytest.approx(to, rel=1e-9, abs=0.0)
+
+
 @pytest.mark.parametrize("rp_min", [533, 266, 133, 66, 33])
 def test_measures_every_sort_size(A, ctx, rp_min):
     # the deepest rank decides the sort size (1024 E values, E = 2 .. 32 in

@@ -219,59 +219,61 @@ struct __align__(8) MeasPlan {
     uint32_t nr, nq;
 };
 
-// one warp: the digit of the need-th largest key among a group's nb bins (a
-// shared-memory histogram, nb = 1024 or 4096), by two levels of warp scans:
-// lane L first sums the nb/32 bins nb-1-(nb/32)L .. nb-(nb/32)(L+1) (read in a
-// rotated order, so the lanes hit distinct banks), then the lanes split the
-// chunk holding the rank.  As pick_digit: a group with fewer than need keys
-// takes the lowest digit.
-__device__ __forceinline__ void pick_digit_smem(const unsigned int *hs, uint32_t nb, int shift, uint64_t &need,
-                                                uint32_t &prefix) {
+// one warp: the digit of the need-th largest key among a group's nb bins
+// (nb = 1024 or 4096; global, complete after the pass's grid barrier) from the
+// group's chunk sums (32 bins per chunk, summed by the blocks with their
+// histograms): the lanes scan the chunk sums (nb/1024 per lane, descending),
+// then the 32 bins of the chunk holding the rank (one per lane).  As
+// pick_digit: a group with fewer than need keys takes the lowest digit.
+__device__ __forceinline__ void pick_digit_2l(const unsigned int *gh, const unsigned int *gc, uint32_t nb,
+                                              int shift, uint64_t &need, uint32_t &prefix) {
     const int lane = threadIdx.x & 31;
-    const uint32_t per = nb >> 5, sub = per >> 5;     // bins per lane: 128 / 32; second level 4 / 1
-    const uint32_t base = nb - per * (uint32_t)(lane + 1);
-    uint32_t tot = 0;
-    for (uint32_t j = 0; j < per; ++j) tot += hs[base + ((j + (uint32_t)lane) & (per - 1u))];
+    const uint32_t nch = nb >> 5, k = nch >> 5;       // chunks; chunks per lane (4 or 1)
+    const uint32_t top = nch - 1u - k * (uint32_t)lane;   // this lane's highest chunk
+    uint32_t c[4], tot = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        c[r] = (uint32_t)r < k ? __ldcg(&gc[top - (uint32_t)r]) : 0u;
+        tot += c[r];
+    }
     uint64_t incl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
     }
-    const uint64_t before = incl - tot;               // keys in higher bins
+    const uint64_t before = incl - tot;               // keys in higher chunks
     const unsigned hit = __ballot_sync(0xffffffffu, before < need && need <= incl);
     uint32_t d = 0;
     uint64_t rem;
     if (hit) {
         const int L = __ffs(hit) - 1;
-        rem = need - __shfl_sync(0xffffffffu, before, L);            // 1 <= rem <= the chunk's keys
-        const uint32_t top = nb - 1u - per * (uint32_t)L;            // the chunk's highest bin
-        uint32_t c[4], t2 = 0;
+        uint32_t ch = 0;
+        rem = need;
+        if (lane == L) {                              // the chunk within the lane's k
+            rem = need - before;
+            ch = top;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            c[r] = (uint32_t)r < sub ? hs[top - (uint32_t)lane * sub - (uint32_t)r] : 0u;
-            t2 += c[r];
+            for (int r = 0; r < 3; ++r)
+                if ((uint32_t)r + 1u < k && rem > c[r]) { rem -= c[r]; --ch; } else break;
         }
-        uint64_t incl2 = t2;
+        ch = __shfl_sync(0xffffffffu, ch, L);
+        rem = __shfl_sync(0xffffffffu, rem, L);       // 1 <= rem <= the chunk's keys
+        const uint32_t bin = ch * 32u + 31u - (uint32_t)lane;   // lane 0: the chunk's highest bin
+        const uint32_t cb = __ldcg(&gh[bin]);
+        uint64_t incl2 = cb;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint64_t y = __shfl_up_sync(0xffffffffu, incl2, o);
             if (lane >= o) incl2 += y;
         }
-        const uint64_t before2 = incl2 - t2;
+        const uint64_t before2 = incl2 - cb;
         const int L2 = __ffs(__ballot_sync(0xffffffffu, before2 < rem && rem <= incl2)) - 1;
-        if (lane == L2) {
-            rem -= before2;
-            d = top - (uint32_t)lane * sub;
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-                if ((uint32_t)r + 1u < sub && rem > c[r]) { rem -= c[r]; --d; } else break;
-        }
-        d = __shfl_sync(0xffffffffu, d, L2);
-        rem = __shfl_sync(0xffffffffu, rem, L2);
+        d = __shfl_sync(0xffffffffu, bin, L2);
+        rem -= __shfl_sync(0xffffffffu, before2, L2);
     } else {                                          // fewer keys than need: the lowest digit
         const uint64_t all = __shfl_sync(0xffffffffu, incl, 31);
-        rem = need - (all - hs[0]);
+        rem = need - (all - __ldcg(&gh[0]));
     }
     need = rem;
     prefix |= d << shift;
@@ -303,6 +305,7 @@ __global__ void __launch_bounds__(kMultiThreads) select_multi_kernel(const float
         const uint32_t nb = 1u << width;
         const uint32_t ng = pass == 0 ? 1u : (uint32_t)nr;   // (pass 0: every rank in group 0)
         unsigned int *hist = ghist + (pass == 0 ? 0u : 4096u + (uint32_t)(pass - 1) * kMaxPlanRanks * 1024u);
+        unsigned int *chist = ghist + kMultiBinWords + (pass == 0 ? 0u : 128u + (uint32_t)(pass - 1) * kMaxPlanRanks * 32u);
         if (tid < kMaxPlanRanks) {                     // group = first rank with the same prefix
             int g = (int)tid;
             for (int i = 0; i < (int)tid; ++i)
@@ -344,14 +347,17 @@ __global__ void __launch_bounds__(kMultiThreads) select_multi_kernel(const float
         __syncthreads();
         for (uint32_t i = tid; i < ng * nb; i += blockDim.x)
             if (h[i]) atomicAdd(&hist[i], h[i]);
+        for (uint32_t ci = tid; ci < ng * (nb >> 5); ci += blockDim.x) {   // chunk sums (32 bins; the
+            uint32_t cs = 0;                                                 // rotated reads: distinct banks)
+            for (uint32_t j = 0; j < 32u; ++j) cs += h[ci * 32u + ((j + ci) & 31u)];
+            if (cs) atomicAdd(&chist[ci], cs);
+        }
         grid.sync();
-        for (uint32_t i = tid; i < ng * nb; i += blockDim.x)   // the leaders' global histograms
-            if (s_grp[i >> width] == (int)(i >> width)) h[i] = __ldcg(&hist[i]);
-        __syncthreads();
         for (int r = (int)warp; r < nr; r += (int)(blockDim.x >> 5)) {   // every block: its ranks' digits
             uint64_t need = s_need[r];
             uint32_t prefix = s_prefix[r];
-            pick_digit_smem(h + (pass == 0 ? 0u : (uint32_t)s_grp[r] * nb), nb, shift, need, prefix);
+            const uint32_t g = pass == 0 ? 0u : (uint32_t)s_grp[r];
+            pick_digit_2l(hist + g * nb, chist + g * (nb >> 5), nb, shift, need, prefix);
             if (lane == 0) { s_need[r] = need; s_prefix[r] = prefix; }
         }
         pmask |= (nb - 1u) << shift;

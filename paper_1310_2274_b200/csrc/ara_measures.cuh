@@ -8,8 +8,9 @@ namespace ara {
 constexpr uint32_t kSortCap = 32768;   // max K (deepest rank needed) per call
 constexpr int kMaxPlanRanks = 16;      // joint select: 3 ranks per return period (n_rp <= 4) + L(1), L(N)
 // joint select histograms: 12-bit digits for the first pass (one group), 10-bit
-// digits per rank group for the second and third
-constexpr uint32_t kMultiHistWords = 4096u + 2u * kMaxPlanRanks * 1024u;
+// digits per rank group for the second and third, then their chunk sums (32 bins each)
+constexpr uint32_t kMultiBinWords = 4096u + 2u * kMaxPlanRanks * 1024u;
+constexpr uint32_t kMultiHistWords = kMultiBinWords + kMultiBinWords / 32u;
 
 struct SelectState {
     uint64_t k_rem;            // rank still to find within the current prefix

@@ -297,7 +297,10 @@ int ara_last_run_launches(const ara_ctx *ctx, uint32_t *kernel_launches, uint32_
 
 /* PML and TVaR (reading G17) at each return period of one layer's
  * YLT, or of the portfolio roll-up sum over layers (layer = -1, G16), by a
- * device radix select over the fp32 bit patterns plus a sort of the tail.
+ * device radix select over the fp32 bit patterns (up to 4 return periods: one
+ * cooperative launch selecting every needed rank at once in three digit passes
+ * of 12/10/10 bits, TVaR tail sums in exact int64 fixed point; more return
+ * periods: a select plus a sort of the tail, or per-rank selects).
  *   ylt        DEVICE fp32, laid out [n_shards][n_layers][n_total/n_shards]
  *              (n_shards = 1 for a single run; > 1 for an all-gathered set
  *              of per-rank shards -- the measures are permutation-invariant)
